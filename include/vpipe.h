@@ -1,0 +1,199 @@
+/*
+ * vpipe — C-ABI of the B200-native Varuna pipeline executor (libvpipe.so).
+ *
+ * Drop-in boundary. Each entry point names the reference interface it
+ * replaces (paths relative to /root/reference; sp/ = pkg/src/spotpipe/).
+ * All functions are extern "C", take plain pointers + int64 sizes (+ a
+ * cudaStream_t passed as void* for device work) and return int status:
+ * VP_OK (0) or a negative VP_ERR_* code, or a positive cudaError_t.
+ * PyTorch (or any caller) owns all memory; the library never frees caller
+ * memory. There is no CPU fallback for any device entry point.
+ */
+#ifndef VPIPE_H_
+#define VPIPE_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+#define VP_OK 0
+#define VP_ERR_ARGS (-1)       /* malformed input  -> ConfigError   (sp/core.py:29-30)   */
+#define VP_ERR_INFEASIBLE (-2) /* no answer        -> InfeasibleError (sp/core.py:33-34) */
+#define VP_ERR_DEADLOCK (-3)   /* event loop stuck -> RuntimeError (sp/engine/_kernel.pyx:544-547) */
+#define VP_ERR_NOMEM (-4)      /* -> MemoryError (sp/engine/_kernel.pyx:451-460) */
+#define VP_ERR_CAPACITY (-5)   /* caller buffer too small */
+#define VP_ERR_UNSUPPORTED (-6)/* shape/layout outside what the kernel supports */
+#define VP_ERR_NOTIMPL (-7)
+
+/* Task kind codes; also the within-instant tie-break priority (sp/core.py:22-26). */
+#define VP_KIND_BACKWARD 0
+#define VP_KIND_RECOMPUTE 1
+#define VP_KIND_FORWARD 2
+
+const char* vp_version(void);
+
+/* ======================================================================
+ * Control plane (host only)
+ * ====================================================================== */
+
+/* Varuna static plan by zero-delay rule simulation.
+ * Replaces generate_varuna_schedule -> _simulate_rules
+ * (sp/scheduler.py:128-145, 179-284). Times in integer microseconds
+ * (the reference rounds seconds with us_from_seconds, sp/core.py:37-38).
+ * Outputs: kinds/mbs[capacity] (0-based micro-batches), offsets[P+1]. */
+int vp_varuna_schedule(int64_t P, int64_t N, int64_t tf_us, int64_t tb_us, int64_t tr_us,
+                       int64_t capacity, int64_t* kinds, int64_t* mbs, int64_t* offsets);
+
+/* GPipe baseline plan. Replaces generate_gpipe_schedule (sp/scheduler.py:148-176). */
+int vp_gpipe_schedule(int64_t P, int64_t N, int64_t capacity, int64_t* kinds, int64_t* mbs,
+                      int64_t* offsets);
+
+/* Output record of vp_run_replica: caller-allocated arrays, capacity
+ * offsets[P] tasks and 2*(P-1)*N messages; per-stage arrays of size P.
+ * Mirrors the dict returned by engine.run_replica (sp/engine/py_kernel.py:343-360). */
+typedef struct vp_replica_out {
+  int64_t *task_stage, *task_kind, *task_mb, *task_start, *task_end;
+  int64_t *msg_send, *msg_grant, *msg_arrive, *msg_boundary, *msg_dir, *msg_mb;
+  int64_t *last_bwd_end, *peak_stash, *peak_sets, *peak_mem;
+  int64_t n_tasks, n_msgs, makespan;
+} vp_replica_out;
+
+/* One pipeline replica through the opportunistic Varuna runtime policy.
+ * Replaces engine.run_replica (sp/engine/_kernel.pyx:334-351 ≡
+ * sp/engine/py_kernel.py:41-360); same 16 arguments, bit-identical results. */
+int vp_run_replica(int64_t n_stages, int64_t n_micro, const int64_t* kinds, const int64_t* mbs,
+                   const int64_t* offsets, const int64_t* fwd_us, const int64_t* bwd_us,
+                   const int64_t* rec_us, const int64_t* act_tx_us, const int64_t* grad_tx_us,
+                   const int64_t* exp_grad_tx_us, const int64_t* in_act_bytes,
+                   const int64_t* work_bytes, const int64_t* stash_cap, int opportunistic,
+                   int serialize_links, vp_replica_out* out);
+
+/* CutPoint -> stage grouping DP. Replaces assign_stages
+ * (sp/partitioner.py:269-374); returns boundaries_out[P]. */
+int vp_assign_stages(int64_t K, const int64_t* forward_us, const int64_t* acts, int64_t P,
+                     double last_stage_weight, int64_t* boundaries_out);
+
+/* CutPoint identification DP. Replaces identify_cutpoints
+ * (sp/partitioner.py:124-246); breakable[n-1]; returns boundaries_out[K]. */
+int vp_identify_cutpoints(int64_t n, const int64_t* compute_us, const int64_t* acts,
+                          const uint8_t* breakable, int64_t K, double tolerance,
+                          int64_t* boundaries_out);
+
+/* ======================================================================
+ * Device kernels (sm_100a). The reference only prices these
+ * (F_i = c_f*params*(m+0.15), B = 2F, R = F: sp/calibration.py:219-221,
+ * sp/simulator.py:241-253); see DESIGN.md for each kernel's roofline.
+ * Pointers are device pointers; `stream` is a cudaStream_t.
+ * ====================================================================== */
+
+/* Device info / runtime. */
+int vp_device_sm_count(int* out);
+
+/* GEMM, bf16 operands, fp32 accumulate in TMEM (tcgen05 + TMA).
+ *   D[M,N] = epilogue( sum_k A(m,k) * B(n,k) )
+ * Operand layouts: a_kmajor=1 -> A stored [M,K] row-major (lda = row stride),
+ *                  a_kmajor=0 -> A stored [K,M] row-major (A^T).
+ *                  b_kmajor=1 -> B stored [N,K] row-major, b_kmajor=0 -> [K,N].
+ * Epilogues (VP_EPI_*), `bias` [N] bf16, `aux` [M,N] bf16 (ldaux):
+ *   STORE       D = acc                              (bf16)
+ *   BIAS        D = acc + bias                       (bf16)
+ *   BIAS_GELU   D = gelu(acc + bias), aux <- acc+bias (pre-activation, bf16)
+ *   BIAS_RESID  D = aux + acc + bias  (residual add; D may alias aux)
+ *   DGELU       D = acc * gelu'(aux)                 (bf16)
+ *   ACC_F32     Df32 += acc  (fp32 D, ldd in elements; weight-grad accumulate)
+ *   STORE_F32   Df32 = acc   (fp32 D)
+ * Replaces the F_i/B_i cost terms of sp/calibration.py:219-221. */
+#define VP_EPI_STORE 0
+#define VP_EPI_BIAS 1
+#define VP_EPI_BIAS_GELU 2
+#define VP_EPI_BIAS_RESID 3
+#define VP_EPI_DGELU 4
+#define VP_EPI_ACC_F32 5
+#define VP_EPI_STORE_F32 6
+int vp_gemm_bf16(int a_kmajor, int b_kmajor, int epilogue, const void* A, int64_t lda,
+                 const void* B, int64_t ldb, void* D, int64_t ldd, const void* bias, void* aux,
+                 int64_t ldaux, int64_t M, int64_t N, int64_t K, void* stream);
+
+/* LayerNorm over rows of x[rows, cols] (bf16 in/out, fp32 stats saved). */
+int vp_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean,
+                     float* rstd, int64_t rows, int64_t cols, float eps, void* stream);
+/* dx (bf16, optionally accumulated into an existing residual grad when
+ * accumulate=1: dx += ...), dgamma/dbeta accumulated in fp32. */
+int vp_layernorm_bwd(const void* dy, const void* x, const void* gamma, const float* mean,
+                     const float* rstd, void* dx, float* dgamma, float* dbeta, int64_t rows,
+                     int64_t cols, int accumulate, float* workspace, void* stream);
+
+/* Causal/bidirectional fused attention over packed qkv[T, 3h] (T = B*S),
+ * heads of size head_dim; o[T, h] bf16; lse[B*heads*S] fp32 saved for bwd. */
+int vp_attention_fwd(const void* qkv, void* o, float* lse, int64_t batch, int64_t seq,
+                     int64_t heads, int64_t head_dim, int causal, void* stream);
+int vp_attention_bwd(const void* qkv, const void* o, const void* dout, const float* lse,
+                     void* dqkv, float* delta_ws, int64_t batch, int64_t seq, int64_t heads,
+                     int64_t head_dim, int causal, void* stream);
+
+/* Token + position embedding gather: x[T,h] = wte[ids] + wpe[pos]. */
+int vp_embed_fwd(const int64_t* ids, const void* wte, const void* wpe, void* x, int64_t batch,
+                 int64_t seq, int64_t hidden, void* stream);
+/* dwte[V,h] += scatter(dx), dwpe[S,h] += sum over batch (fp32 accumulators). */
+int vp_embed_bwd(const int64_t* ids, const void* dx, float* dwte, float* dwpe, int64_t batch,
+                 int64_t seq, int64_t hidden, void* stream);
+
+/* Softmax cross-entropy over logits[T,V] (bf16). Writes per-row loss (fp32)
+ * and overwrites logits with dlogits = (softmax - onehot) * scale.
+ * labels < 0 are ignored (zero grad, zero loss). */
+int vp_xent_fwd_bwd(void* logits, const int64_t* labels, float* loss_rows, int64_t rows,
+                    int64_t vocab, float scale, void* stream);
+
+/* Column sum of dy[rows, cols] (bf16) accumulated into dbias (fp32). */
+int vp_bias_grad(const void* dy, float* dbias, int64_t rows, int64_t cols, float* workspace,
+                 void* stream);
+
+/* Philox-keyed dropout applied in place: x *= mask(seed, offset, i)/(1-p). */
+int vp_dropout(void* x, int64_t n, float p, uint64_t seed, uint64_t offset, void* stream);
+
+/* Residual add: y = a + b (bf16), n elements. */
+int vp_add(const void* a, const void* b, void* y, int64_t n, void* stream);
+
+/* Squared-L2 norm and non-finite flag of an fp32 buffer, accumulated into
+ * out[0] (sum of squares, fp32) and out[1] (count of non-finite values).
+ * Feeds the pipeline-wide overflow/grad-norm agreement. */
+int vp_grad_norm_sq(const float* g, int64_t n, float* out, void* stream);
+
+/* Fused unscale + (skip on overflow) + clip + AdamW + fp32 master update +
+ * bf16 weight write. `flags` = device [sum_sq, n_nonfinite] after the global
+ * reduction; step skipped on device when flags[1] != 0. grad is zeroed.
+ * Replaces the 16 B/param optimizer-state model (sp/core.py:17-18). */
+int vp_adam_step(float* master, void* weight_bf16, float* grad, float* exp_avg, float* exp_avg_sq,
+                 int64_t n, const float* flags, float lr, float beta1, float beta2, float eps,
+                 float weight_decay, float inv_loss_scale, float max_grad_norm,
+                 float bias_c1, float bias_c2, void* stream);
+
+/* Cast fp32 -> bf16 (n elements). */
+int vp_cast_f32_bf16(const float* x, void* y, int64_t n, void* stream);
+
+/* ======================================================================
+ * Inter-stage P2P over NVLink (device-initiated copies into registered
+ * peer buffers). Replaces the modeled transfer + serialized link of
+ * send() (sp/engine/py_kernel.py:184-214, sp/calibration.py:95-110).
+ * ====================================================================== */
+#define VP_IPC_HANDLE_BYTES 64
+/* Export a device allocation / create+export an interprocess event. */
+int vp_ipc_get_mem_handle(void* dev_ptr, void* handle_out /*64 bytes*/);
+int vp_ipc_open_mem_handle(const void* handle /*64 bytes*/, void** dev_ptr_out);
+int vp_ipc_close_mem_handle(void* dev_ptr);
+int vp_ipc_event_create(void** event_out, void* handle_out /*64 bytes*/);
+int vp_ipc_event_open(const void* handle, void** event_out);
+int vp_event_destroy(void* event);
+int vp_event_record(void* event, void* stream);
+int vp_stream_wait_event(void* stream, void* event);
+int vp_event_query(void* event); /* 0 = complete, 1 = pending, else error */
+/* SM-driven copy of `bytes` from src into a (peer-mapped) dst, 16B vectors. */
+int vp_p2p_put(void* dst, const void* src, int64_t bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VPIPE_H_ */
