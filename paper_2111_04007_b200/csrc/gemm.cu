@@ -1,0 +1,442 @@
+// Persistent warp-specialised bf16 GEMM for sm_100a: TMA -> SMEM (128B
+// swizzle) -> tcgen05.mma (cta_group::1, UMMA 128xBNx16) -> TMEM (double-
+// buffered fp32 accumulator) -> fused epilogue.
+//
+//   warp 0     : TMA producer (one elected lane)
+//   warp 1     : MMA issuer   (one elected lane)
+//   warp 2     : TMEM allocator
+//   warps 4..7 : epilogue (TMEM lane quadrant = warp % 4)
+//
+// This is the K1 kernel of DESIGN.md: every dense contraction of a stage's
+// forward, recompute and backward (QKV, attention-out, FC1, FC2, LM head;
+// dgrad and wgrad). The reference only prices it (sp/calibration.py:219-221).
+#include "sm100.cuh"
+#include "vpipe.h"
+
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+
+namespace vp {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kThreads = 256;
+
+struct EpiArgs {
+  void* D;
+  int64_t ldd;
+  const __nv_bfloat16* bias;
+  __nv_bfloat16* aux;
+  int64_t ldaux;
+};
+
+template <int BN, int STAGES>
+struct Smem {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFFSET = STAGES * STAGE_BYTES;
+  static constexpr int TOTAL = BAR_OFFSET + 256 + 1024;  // + barriers + align slack
+};
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+template <int EPI>
+__device__ __forceinline__ void epilogue_chunk(const EpiArgs& e, int64_t row, int64_t col0,
+                                               int64_t M, int64_t N, const uint32_t (&raw)[32]) {
+  if (row >= M) return;
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(raw[i]);
+  const bool full = (col0 + 32 <= N);
+  if constexpr (EPI == VP_EPI_ACC_F32 || EPI == VP_EPI_STORE_F32) {
+    float* d = reinterpret_cast<float*>(e.D) + row * e.ldd + col0;
+    if (full) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        if constexpr (EPI == VP_EPI_ACC_F32) {
+          float4 p = *reinterpret_cast<const float4*>(d + i);
+          o.x += p.x; o.y += p.y; o.z += p.z; o.w += p.w;
+        }
+        *reinterpret_cast<float4*>(d + i) = o;
+      }
+    } else {
+      for (int i = 0; i < 32 && col0 + i < N; ++i) {
+        if constexpr (EPI == VP_EPI_ACC_F32) d[i] += v[i];
+        else d[i] = v[i];
+      }
+    }
+    return;
+  } else {
+    __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(e.D) + row * e.ldd + col0;
+    if constexpr (EPI == VP_EPI_BIAS || EPI == VP_EPI_BIAS_GELU || EPI == VP_EPI_BIAS_RESID) {
+      if (full) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 bb = *reinterpret_cast<const uint4*>(e.bias + col0 + i);
+          const __nv_bfloat16* bh = reinterpret_cast<const __nv_bfloat16*>(&bb);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[i + j] += __bfloat162float(bh[j]);
+        }
+      } else {
+        for (int i = 0; i < 32 && col0 + i < N; ++i) v[i] += __bfloat162float(e.bias[col0 + i]);
+      }
+    }
+    if constexpr (EPI == VP_EPI_BIAS_GELU) {
+      if (e.aux) {
+        __nv_bfloat16* a = e.aux + row * e.ldaux + col0;
+        if (full) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            uint4 o;
+            o.x = pack_bf16(v[i], v[i + 1]);
+            o.y = pack_bf16(v[i + 2], v[i + 3]);
+            o.z = pack_bf16(v[i + 4], v[i + 5]);
+            o.w = pack_bf16(v[i + 6], v[i + 7]);
+            *reinterpret_cast<uint4*>(a + i) = o;
+          }
+        } else {
+          for (int i = 0; i < 32 && col0 + i < N; ++i) a[i] = __float2bfloat16(v[i]);
+        }
+      }
+      // The stored pre-activation is bf16; apply GELU to the rounded value so
+      // the backward (which only sees the bf16 pre-activation) is consistent.
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(__bfloat162float(__float2bfloat16(v[i])));
+    }
+    if constexpr (EPI == VP_EPI_BIAS_RESID || EPI == VP_EPI_DGELU) {
+      const __nv_bfloat16* a = e.aux + row * e.ldaux + col0;
+      if (full) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 bb = *reinterpret_cast<const uint4*>(a + i);
+          const __nv_bfloat16* ah = reinterpret_cast<const __nv_bfloat16*>(&bb);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float x = __bfloat162float(ah[j]);
+            if constexpr (EPI == VP_EPI_BIAS_RESID) v[i + j] += x;
+            else v[i + j] *= gelu_tanh_grad(x);
+          }
+        }
+      } else {
+        for (int i = 0; i < 32 && col0 + i < N; ++i) {
+          float x = __bfloat162float(a[i]);
+          if constexpr (EPI == VP_EPI_BIAS_RESID) v[i] += x;
+          else v[i] *= gelu_tanh_grad(x);
+        }
+      }
+    }
+    if (full) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {
+        uint4 o;
+        o.x = pack_bf16(v[i], v[i + 1]);
+        o.y = pack_bf16(v[i + 2], v[i + 3]);
+        o.z = pack_bf16(v[i + 4], v[i + 5]);
+        o.w = pack_bf16(v[i + 6], v[i + 7]);
+        *reinterpret_cast<uint4*>(d + i) = o;
+      }
+    } else {
+      for (int i = 0; i < 32 && col0 + i < N; ++i) d[i] = __float2bfloat16(v[i]);
+    }
+  }
+}
+
+__device__ __forceinline__ void tile_coords(int64_t t, int64_t tiles_m, int64_t tiles_n,
+                                            int64_t& mb, int64_t& nb) {
+  // Grouped rasterisation: 8 M-tiles share each sweep over N for L2 reuse of B.
+  constexpr int64_t G = 8;
+  const int64_t per_group = G * tiles_n;
+  const int64_t group = t / per_group;
+  const int64_t first_m = group * G;
+  const int64_t gsize = min(tiles_m - first_m, G);
+  const int64_t r = t % per_group;
+  mb = first_m + r % gsize;
+  nb = r / gsize;
+}
+
+template <int BN, int STAGES, int EPI, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                int64_t M, int64_t N, int64_t K, EpiArgs epi) {
+  using S = Smem<BN, STAGES>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S::BAR_OFFSET);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;   // [2]
+  uint64_t* tempty_bar = tfull_bar + 2;       // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const uint32_t warp = warp_id();
+  const int64_t tiles_m = (M + BM - 1) / BM;
+  const int64_t tiles_n = (N + BN - 1) / BN;
+  const int64_t n_tiles = tiles_m * tiles_n;
+  const int64_t n_kb = (K + BK - 1) / BK;
+  constexpr uint32_t kTmemCols = 2 * BN;
+
+  if (warp == 0 && lane_id() == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane_id() == 0) {
+      // ===== TMA producer =====
+      uint32_t stage = 0, phase = 0;
+      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        int64_t mb, nb;
+        tile_coords(t, tiles_m, tiles_n, mb, nb);
+        const int32_t m0 = static_cast<int32_t>(mb * BM);
+        const int32_t n0 = static_cast<int32_t>(nb * BN);
+        for (int64_t kb = 0; kb < n_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * S::STAGE_BYTES;
+          uint8_t* sb = sa + S::A_BYTES;
+          mbar_expect_tx(&full_bar[stage], S::STAGE_BYTES);
+          const int32_t k0 = static_cast<int32_t>(kb * BK);
+          if constexpr (!A_MN) {
+            tma_load_2d(sa, &tmA, &full_bar[stage], k0, m0);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BM / 64; ++c)
+              tma_load_2d(sa + c * (64 * BK * 2), &tmA, &full_bar[stage], m0 + 64 * c, k0);
+          }
+          if constexpr (!B_MN) {
+            tma_load_2d(sb, &tmB, &full_bar[stage], k0, n0);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BN / 64; ++c)
+              tma_load_2d(sb + c * (64 * BK * 2), &tmB, &full_bar[stage], n0 + 64 * c, k0);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane_id() == 0) {
+      // ===== MMA issuer =====
+      constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN, B_MN);
+      uint32_t stage = 0, phase = 0;
+      uint32_t local = 0;
+      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++local) {
+        const uint32_t acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int64_t kb = 0; kb < n_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * S::STAGE_BYTES);
+          const uint32_t sb = sa + S::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // K-major: +32 B per 16-element K step inside the 128 B swizzle row.
+            // MN-major: +16 rows * 128 B per K step; 64-wide M/N chunks are
+            // 64*BK*2 bytes apart (LBO).
+            const uint64_t ad = A_MN ? sdesc_sw128(sa + k * 2048, 64 * BK * 2, 1024)
+                                     : sdesc_sw128(sa + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? sdesc_sw128(sb + k * 2048, 64 * BK * 2, 1024)
+                                     : sdesc_sw128(sb + k * 32, 16, 1024);
+            umma_f16(tmem_d, ad, bd, idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty_bar[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tfull_bar[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ===== Epilogue =====
+    const uint32_t q = warp & 3;  // TMEM lane quadrant
+    uint32_t local = 0;
+    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++local) {
+      int64_t mb, nb;
+      tile_coords(t, tiles_m, tiles_n, mb, nb);
+      const uint32_t acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const int64_t row = mb * BM + q * 32 + lane_id();
+      const uint32_t taddr = tmem_base + ((q * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        const int64_t col0 = nb * BN + c;
+        if (col0 >= N) break;
+        uint32_t raw[32];
+        tmem_ld32(taddr + c, raw);
+        tmem_ld_wait();
+        epilogue_chunk<EPI>(epi, row, col0, M, N, raw);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(&tempty_bar[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, kTmemCols);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host side
+// ---------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2D bf16 tensor map: inner dim contiguous, rows `ld` elements apart.
+bool make_tmap(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
+               uint32_t box_inner, uint32_t box_outer) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int g_sm_count = 0;
+int sm_count() {
+  if (!g_sm_count) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sm_count <= 0) g_sm_count = 148;
+  }
+  return g_sm_count;
+}
+
+template <int BN, int STAGES, int EPI, bool A_MN, bool B_MN>
+int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, int64_t M, int64_t N, int64_t K,
+             const EpiArgs& e, cudaStream_t st) {
+  using S = Smem<BN, STAGES>;
+  auto kern = gemm_kernel<BN, STAGES, EPI, A_MN, B_MN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t err =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL);
+    if (err != cudaSuccess) return err;
+    attr_set = true;
+  }
+  const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int grid = static_cast<int>(std::min<int64_t>(tiles, sm_count()));
+  kern<<<grid, kThreads, S::TOTAL, st>>>(ta, tb, M, N, K, e);
+  return cudaGetLastError();
+}
+
+template <int BN, int EPI>
+int dispatch_layout(bool a_mn, bool b_mn, const CUtensorMap& ta, const CUtensorMap& tb,
+                    int64_t M, int64_t N, int64_t K, const EpiArgs& e, cudaStream_t st) {
+  constexpr int STAGES = BN == 256 ? 4 : 6;
+  if (!a_mn && !b_mn) return launch_t<BN, STAGES, EPI, false, false>(ta, tb, M, N, K, e, st);
+  if (!a_mn && b_mn) return launch_t<BN, STAGES, EPI, false, true>(ta, tb, M, N, K, e, st);
+  if (a_mn && !b_mn) return launch_t<BN, STAGES, EPI, true, false>(ta, tb, M, N, K, e, st);
+  return launch_t<BN, STAGES, EPI, true, true>(ta, tb, M, N, K, e, st);
+}
+
+template <int BN>
+int dispatch_epi(int epi, bool a_mn, bool b_mn, const CUtensorMap& ta, const CUtensorMap& tb,
+                 int64_t M, int64_t N, int64_t K, const EpiArgs& e, cudaStream_t st) {
+  switch (epi) {
+    case VP_EPI_STORE: return dispatch_layout<BN, VP_EPI_STORE>(a_mn, b_mn, ta, tb, M, N, K, e, st);
+    case VP_EPI_BIAS: return dispatch_layout<BN, VP_EPI_BIAS>(a_mn, b_mn, ta, tb, M, N, K, e, st);
+    case VP_EPI_BIAS_GELU:
+      return dispatch_layout<BN, VP_EPI_BIAS_GELU>(a_mn, b_mn, ta, tb, M, N, K, e, st);
+    case VP_EPI_BIAS_RESID:
+      return dispatch_layout<BN, VP_EPI_BIAS_RESID>(a_mn, b_mn, ta, tb, M, N, K, e, st);
+    case VP_EPI_DGELU: return dispatch_layout<BN, VP_EPI_DGELU>(a_mn, b_mn, ta, tb, M, N, K, e, st);
+    case VP_EPI_ACC_F32:
+      return dispatch_layout<BN, VP_EPI_ACC_F32>(a_mn, b_mn, ta, tb, M, N, K, e, st);
+    case VP_EPI_STORE_F32:
+      return dispatch_layout<BN, VP_EPI_STORE_F32>(a_mn, b_mn, ta, tb, M, N, K, e, st);
+    default: return VP_ERR_ARGS;
+  }
+}
+
+}  // namespace
+}  // namespace vp
+
+extern "C" int vp_device_sm_count(int* out) {
+  if (!out) return VP_ERR_ARGS;
+  *out = vp::sm_count();
+  return VP_OK;
+}
+
+extern "C" int vp_gemm_bf16(int a_kmajor, int b_kmajor, int epilogue, const void* A, int64_t lda,
+                            const void* B, int64_t ldb, void* D, int64_t ldd, const void* bias,
+                            void* aux, int64_t ldaux, int64_t M, int64_t N, int64_t K,
+                            void* stream) {
+  using namespace vp;
+  if (M <= 0 || N <= 0 || K <= 0 || !A || !B || !D) return VP_ERR_ARGS;
+  // TMA: 16-byte aligned bases and row strides.
+  if ((lda % 8) || (ldb % 8) || (ldd % 8)) return VP_ERR_UNSUPPORTED;
+  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) |
+       reinterpret_cast<uintptr_t>(D)) & 15)
+    return VP_ERR_UNSUPPORTED;
+  const bool needs_bias = epilogue == VP_EPI_BIAS || epilogue == VP_EPI_BIAS_GELU ||
+                          epilogue == VP_EPI_BIAS_RESID;
+  if (needs_bias && !bias) return VP_ERR_ARGS;
+  if ((epilogue == VP_EPI_BIAS_RESID || epilogue == VP_EPI_DGELU) && !aux) return VP_ERR_ARGS;
+  if (aux && (ldaux % 8)) return VP_ERR_UNSUPPORTED;
+  const bool a_mn = !a_kmajor, b_mn = !b_kmajor;
+  // Choose BN: 256 unless that leaves the last wave badly filled.
+  const int64_t tm = (M + BM - 1) / BM;
+  const int sms = sm_count();
+  auto waste = [&](int64_t bn) {
+    const int64_t tiles = tm * ((N + bn - 1) / bn);
+    const int64_t waves = (tiles + sms - 1) / sms;
+    return double(waves * sms) * bn / double(tiles * bn);  // slots per useful tile
+  };
+  const int BNsel = (N <= 128 || waste(128) * 0.92 < waste(256)) ? 128 : 256;
+  CUtensorMap ta, tb;
+  bool ok = a_mn ? make_tmap(&ta, A, M, K, lda, 64, BK) : make_tmap(&ta, A, K, M, lda, BK, BM);
+  ok = ok && (b_mn ? make_tmap(&tb, B, N, K, ldb, 64, BK)
+                   : make_tmap(&tb, B, K, N, ldb, BK, BNsel));
+  if (!ok) return VP_ERR_UNSUPPORTED;
+  EpiArgs e{D, ldd, reinterpret_cast<const __nv_bfloat16*>(bias),
+            reinterpret_cast<__nv_bfloat16*>(aux), ldaux};
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (BNsel == 256) return dispatch_epi<256>(epilogue, a_mn, b_mn, ta, tb, M, N, K, e, st);
+  return dispatch_epi<128>(epilogue, a_mn, b_mn, ta, tb, M, N, K, e, st);
+}
