@@ -1,0 +1,358 @@
+// HBM-bound fused kernels: embedding gather/scatter (K8), softmax
+// cross-entropy fwd+bwd (K6), bias-grad column reduction, dropout (K7),
+// residual add, grad-norm/overflow reduction (K11), fused AdamW (K10), casts.
+#include <algorithm>
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace vp {
+namespace {
+
+// ---------------------------------------------------------------- embedding
+__global__ void embed_fwd_kernel(const int64_t* __restrict__ ids,
+                                 const __nv_bfloat16* __restrict__ wte,
+                                 const __nv_bfloat16* __restrict__ wpe,
+                                 __nv_bfloat16* __restrict__ x, int64_t tokens, int64_t seq,
+                                 int64_t hidden) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (t >= tokens) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t nvec = hidden >> 3;
+  const uint4* a = reinterpret_cast<const uint4*>(wte + ids[t] * hidden);
+  const uint4* p = reinterpret_cast<const uint4*>(wpe + (t % seq) * hidden);
+  uint4* o = reinterpret_cast<uint4*>(x + t * hidden);
+  for (int64_t c = lane; c < nvec; c += 32) {
+    float fa[8], fp[8];
+    unpack8(a[c], fa);
+    unpack8(p[c], fp);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) fa[j] += fp[j];
+    o[c] = pack8(fa);
+  }
+}
+
+__global__ void embed_bwd_tok_kernel(const int64_t* __restrict__ ids,
+                                     const __nv_bfloat16* __restrict__ dx,
+                                     float* __restrict__ dwte, int64_t tokens, int64_t hidden) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (t >= tokens) return;
+  const int lane = threadIdx.x & 31;
+  const uint4* g = reinterpret_cast<const uint4*>(dx + t * hidden);
+  float* dst = dwte + ids[t] * hidden;
+  for (int64_t c = lane; c < (hidden >> 3); c += 32) {
+    float f[8];
+    unpack8(g[c], f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) atomicAdd(dst + c * 8 + j, f[j]);
+  }
+}
+
+__global__ void embed_bwd_pos_kernel(const __nv_bfloat16* __restrict__ dx,
+                                     float* __restrict__ dwpe, int64_t batch, int64_t seq,
+                                     int64_t hidden) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= seq * hidden) return;
+  float acc = 0.f;
+  for (int64_t b = 0; b < batch; ++b) acc += __bfloat162float(dx[b * seq * hidden + i]);
+  dwpe[i] += acc;
+}
+
+// ------------------------------------------------------------ cross-entropy
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS)
+    xent_kernel(__nv_bfloat16* __restrict__ logits, const int64_t* __restrict__ labels,
+                float* __restrict__ loss_rows, int64_t vocab, float scale) {
+  const int64_t row = blockIdx.x;
+  __nv_bfloat16* lr = logits + row * vocab;
+  const int64_t label = labels[row];
+  __shared__ float s_m[THREADS / 32], s_s[THREADS / 32];
+  __shared__ float s_lse;
+  float m = -FLT_MAX, s = 0.f;
+  const int64_t nvec = vocab >> 3;
+  const uint4* lv = reinterpret_cast<const uint4*>(lr);
+  for (int64_t c = threadIdx.x; c < nvec; c += THREADS) {
+    float f[8];
+    unpack8(lv[c], f);
+    float mm = f[0];
+#pragma unroll
+    for (int j = 1; j < 8; ++j) mm = fmaxf(mm, f[j]);
+    if (mm > m) {
+      s *= __expf(m - mm);
+      m = mm;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += __expf(f[j] - m);
+  }
+  // warp then block merge of (max, sum)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float om = __shfl_xor_sync(0xffffffffu, m, o);
+    const float os = __shfl_xor_sync(0xffffffffu, s, o);
+    const float nm = fmaxf(m, om);
+    s = s * __expf(m - nm) + os * __expf(om - nm);
+    m = nm;
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    s_m[w] = m;
+    s_s[w] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float M = s_m[0], S = s_s[0];
+    for (int i = 1; i < THREADS / 32; ++i) {
+      const float nm = fmaxf(M, s_m[i]);
+      S = S * __expf(M - nm) + s_s[i] * __expf(s_m[i] - nm);
+      M = nm;
+    }
+    const float lse = M + __logf(S);
+    s_lse = lse;
+    if (label >= 0 && label < vocab)
+      loss_rows[row] = lse - __bfloat162float(lr[label]);
+    else
+      loss_rows[row] = 0.f;
+  }
+  __syncthreads();
+  const float lse = s_lse;
+  const bool valid = label >= 0 && label < vocab;
+  uint4* ov = reinterpret_cast<uint4*>(lr);
+  for (int64_t c = threadIdx.x; c < nvec; c += THREADS) {
+    float f[8];
+    unpack8(ov[c], f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float p = valid ? __expf(f[j] - lse) : 0.f;
+      if (c * 8 + j == label) p -= 1.f;
+      f[j] = p * scale;
+    }
+    ov[c] = pack8(f);
+  }
+}
+
+// ---------------------------------------------------------------- bias grad
+__global__ void colsum_partial(const __nv_bfloat16* __restrict__ dy, float* __restrict__ ws,
+                               int64_t rows, int64_t cols, int64_t rows_per_part) {
+  // grid: (ceil(cols/256), parts)
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
+  if (c >= cols) return;
+  const int64_t r0 = blockIdx.y * rows_per_part;
+  const int64_t r1 = min(rows, r0 + rows_per_part);
+  float acc = 0.f;
+  for (int64_t r = r0; r < r1; ++r) acc += __bfloat162float(dy[r * cols + c]);
+  ws[blockIdx.y * cols + c] = acc;
+}
+__global__ void colsum_final(const float* __restrict__ ws, float* __restrict__ out, int parts,
+                             int64_t cols) {
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  float acc = 0.f;
+  for (int p = 0; p < parts; ++p) acc += ws[p * cols + c];
+  out[c] += acc;
+}
+
+// ------------------------------------------------------------ dropout / add
+__global__ void dropout_kernel(__nv_bfloat16* __restrict__ x, int64_t n, float p, uint64_t seed,
+                               uint64_t offset) {
+  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 8;
+  if (i >= n) return;
+  const uint32_t thresh = static_cast<uint32_t>(p * 4294967296.0);
+  const float keep = 1.f / (1.f - p);
+  if (i + 8 <= n) {
+    uint4* v = reinterpret_cast<uint4*>(x + i);
+    float f[8];
+    unpack8(*v, f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[j] = hash_u32(seed, offset + i + j) < thresh ? 0.f : f[j] * keep;
+    *v = pack8(f);
+  } else {
+    for (int64_t k = i; k < n; ++k) {
+      const float f = __bfloat162float(x[k]);
+      x[k] = __float2bfloat16(hash_u32(seed, offset + k) < thresh ? 0.f : f * keep);
+    }
+  }
+}
+
+__global__ void add_kernel(const __nv_bfloat16* __restrict__ a, const __nv_bfloat16* __restrict__ b,
+                           __nv_bfloat16* __restrict__ y, int64_t n) {
+  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 8;
+  if (i + 8 <= n) {
+    float fa[8], fb[8];
+    unpack8(*reinterpret_cast<const uint4*>(a + i), fa);
+    unpack8(*reinterpret_cast<const uint4*>(b + i), fb);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) fa[j] += fb[j];
+    *reinterpret_cast<uint4*>(y + i) = pack8(fa);
+  } else {
+    for (int64_t k = i; k < n; ++k)
+      y[k] = __float2bfloat16(__bfloat162float(a[k]) + __bfloat162float(b[k]));
+  }
+}
+
+// ---------------------------------------------------------- grad norm / Adam
+__global__ void norm_kernel(const float* __restrict__ g, int64_t n, float* __restrict__ out) {
+  float ss = 0.f, bad = 0.f;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * 4;
+  for (int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4; i < n;
+       i += stride) {
+    if (i + 4 <= n) {
+      const float4 v = *reinterpret_cast<const float4*>(g + i);
+      const float a[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (isfinite(a[j])) ss += a[j] * a[j];
+        else bad += 1.f;
+      }
+    } else {
+      for (int64_t k = i; k < n; ++k) {
+        if (isfinite(g[k])) ss += g[k] * g[k];
+        else bad += 1.f;
+      }
+    }
+  }
+  ss = warp_sum(ss);
+  bad = warp_sum(bad);
+  __shared__ float sh[2][32];
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sh[0][w] = ss;
+    sh[1][w] = bad;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float a = 0.f, b = 0.f;
+    for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) {
+      a += sh[0][i];
+      b += sh[1][i];
+    }
+    atomicAdd(out, a);
+    if (b > 0.f) atomicAdd(out + 1, b);
+  }
+}
+
+__global__ void adam_kernel(float* __restrict__ master, __nv_bfloat16* __restrict__ w,
+                            float* __restrict__ grad, float* __restrict__ m, float* __restrict__ v,
+                            int64_t n, const float* __restrict__ flags, float lr, float b1,
+                            float b2, float eps, float wd, float inv_scale, float max_norm,
+                            float bc1, float bc2) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t base = i * 4;
+  if (base >= n) return;
+  const bool skip = flags[1] != 0.f;
+  float coef = inv_scale;
+  if (max_norm > 0.f) {
+    const float norm = sqrtf(flags[0]) * inv_scale;
+    if (norm > max_norm) coef *= max_norm / (norm + 1e-6f);
+  }
+  const int cnt = static_cast<int>(std::min<int64_t>(4, n - base));
+  for (int j = 0; j < cnt; ++j) {
+    const int64_t k = base + j;
+    const float g = grad[k] * coef;
+    grad[k] = 0.f;
+    if (skip) continue;
+    const float mk = b1 * m[k] + (1.f - b1) * g;
+    const float vk = b2 * v[k] + (1.f - b2) * g * g;
+    m[k] = mk;
+    v[k] = vk;
+    const float upd = (mk / bc1) / (sqrtf(vk / bc2) + eps) + wd * master[k];
+    const float nw = master[k] - lr * upd;
+    master[k] = nw;
+    w[k] = __float2bfloat16(nw);
+  }
+}
+
+__global__ void cast_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ y, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = __float2bfloat16(x[i]);
+}
+
+inline unsigned blocks_for(int64_t n, int per_block) {
+  return static_cast<unsigned>((n + per_block - 1) / per_block);
+}
+
+}  // namespace
+}  // namespace vp
+
+using namespace vp;
+#define ST reinterpret_cast<cudaStream_t>(stream)
+#define BF(p) reinterpret_cast<__nv_bfloat16*>(p)
+#define CBF(p) reinterpret_cast<const __nv_bfloat16*>(p)
+
+extern "C" int vp_embed_fwd(const int64_t* ids, const void* wte, const void* wpe, void* x,
+                            int64_t batch, int64_t seq, int64_t hidden, void* stream) {
+  if (batch <= 0 || seq <= 0 || hidden <= 0 || (hidden % 8)) return VP_ERR_ARGS;
+  const int64_t tokens = batch * seq;
+  embed_fwd_kernel<<<blocks_for(tokens, 8), 256, 0, ST>>>(ids, CBF(wte), CBF(wpe), BF(x), tokens,
+                                                         seq, hidden);
+  return launch_status();
+}
+
+extern "C" int vp_embed_bwd(const int64_t* ids, const void* dx, float* dwte, float* dwpe,
+                            int64_t batch, int64_t seq, int64_t hidden, void* stream) {
+  if (batch <= 0 || seq <= 0 || hidden <= 0 || (hidden % 8)) return VP_ERR_ARGS;
+  const int64_t tokens = batch * seq;
+  embed_bwd_tok_kernel<<<blocks_for(tokens, 8), 256, 0, ST>>>(ids, CBF(dx), dwte, tokens, hidden);
+  if (dwpe)
+    embed_bwd_pos_kernel<<<blocks_for(seq * hidden, 256), 256, 0, ST>>>(CBF(dx), dwpe, batch, seq,
+                                                                       hidden);
+  return launch_status();
+}
+
+extern "C" int vp_xent_fwd_bwd(void* logits, const int64_t* labels, float* loss_rows,
+                               int64_t rows, int64_t vocab, float scale, void* stream) {
+  if (rows <= 0 || vocab <= 0 || (vocab % 8)) return VP_ERR_ARGS;
+  xent_kernel<512><<<static_cast<unsigned>(rows), 512, 0, ST>>>(BF(logits), labels, loss_rows,
+                                                                vocab, scale);
+  return launch_status();
+}
+
+// workspace >= 64 * cols floats.
+extern "C" int vp_bias_grad(const void* dy, float* dbias, int64_t rows, int64_t cols,
+                            float* workspace, void* stream) {
+  if (rows <= 0 || cols <= 0 || !workspace) return VP_ERR_ARGS;
+  const int parts = static_cast<int>(std::min<int64_t>(64, rows));
+  const int64_t rpp = (rows + parts - 1) / parts;
+  dim3 grid(blocks_for(cols, 256), parts);
+  colsum_partial<<<grid, 256, 0, ST>>>(CBF(dy), workspace, rows, cols, rpp);
+  colsum_final<<<blocks_for(cols, 256), 256, 0, ST>>>(workspace, dbias, parts, cols);
+  return launch_status();
+}
+
+extern "C" int vp_dropout(void* x, int64_t n, float p, uint64_t seed, uint64_t offset,
+                          void* stream) {
+  if (n <= 0 || p < 0.f || p >= 1.f) return VP_ERR_ARGS;
+  if (p == 0.f) return VP_OK;
+  dropout_kernel<<<blocks_for(n, 256 * 8), 256, 0, ST>>>(BF(x), n, p, seed, offset);
+  return launch_status();
+}
+
+extern "C" int vp_add(const void* a, const void* b, void* y, int64_t n, void* stream) {
+  if (n <= 0) return VP_ERR_ARGS;
+  add_kernel<<<blocks_for(n, 256 * 8), 256, 0, ST>>>(CBF(a), CBF(b), BF(y), n);
+  return launch_status();
+}
+
+extern "C" int vp_grad_norm_sq(const float* g, int64_t n, float* out, void* stream) {
+  if (n <= 0) return VP_OK;
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(1184, (n + 1023) / 1024));
+  norm_kernel<<<blocks, 256, 0, ST>>>(g, n, out);
+  return launch_status();
+}
+
+extern "C" int vp_adam_step(float* master, void* weight_bf16, float* grad, float* exp_avg,
+                            float* exp_avg_sq, int64_t n, const float* flags, float lr,
+                            float beta1, float beta2, float eps, float weight_decay,
+                            float inv_loss_scale, float max_grad_norm, float bias_c1,
+                            float bias_c2, void* stream) {
+  if (n <= 0) return VP_OK;
+  adam_kernel<<<blocks_for(n, 256 * 4), 256, 0, ST>>>(
+      master, BF(weight_bf16), grad, exp_avg, exp_avg_sq, n, flags, lr, beta1, beta2, eps,
+      weight_decay, inv_loss_scale, max_grad_norm, bias_c1, bias_c2);
+  return launch_status();
+}
+
+extern "C" int vp_cast_f32_bf16(const float* x, void* y, int64_t n, void* stream) {
+  if (n <= 0) return VP_OK;
+  cast_kernel<<<blocks_for(n, 256), 256, 0, ST>>>(x, BF(y), n);
+  return launch_status();
+}

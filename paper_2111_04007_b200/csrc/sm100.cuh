@@ -6,11 +6,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-namespace vp {
+#include "common.cuh"
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
+namespace vp {
 
 __device__ __forceinline__ uint32_t warp_id() { return threadIdx.x >> 5; }
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }

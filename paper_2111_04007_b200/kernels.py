@@ -98,3 +98,102 @@ def gemm(a, b, out, *, a_kmajor=True, b_kmajor=True, epilogue=EPI_STORE, bias=No
                          _p(aux), aux.stride(0) if aux is not None else 0, M, N, K,
                          _stream(stream)), "vp_gemm_bf16")
     return out
+
+
+def layernorm_fwd(x, gamma, beta, y, mean, rstd, eps=1e-5, stream=None):
+    rows, cols = x.shape
+    check(L.vp_layernorm_fwd(x.data_ptr(), gamma.data_ptr(), beta.data_ptr(), y.data_ptr(),
+                             mean.data_ptr(), rstd.data_ptr(), rows, cols, eps, _stream(stream)),
+          "vp_layernorm_fwd")
+    return y
+
+
+def layernorm_ws_elems(cols: int) -> int:
+    return 2 * 296 * cols
+
+
+def layernorm_bwd(dy, x, gamma, mean, rstd, dx, dgamma, dbeta, workspace, accumulate=False,
+                  stream=None):
+    rows, cols = x.shape
+    check(L.vp_layernorm_bwd(dy.data_ptr(), x.data_ptr(), gamma.data_ptr(), mean.data_ptr(),
+                             rstd.data_ptr(), dx.data_ptr(), dgamma.data_ptr(), dbeta.data_ptr(),
+                             rows, cols, int(accumulate), workspace.data_ptr(), _stream(stream)),
+          "vp_layernorm_bwd")
+    return dx
+
+
+def attention_fwd(qkv, out, lse, batch, seq, heads, head_dim, causal=True, stream=None):
+    check(L.vp_attention_fwd(qkv.data_ptr(), out.data_ptr(), lse.data_ptr(), batch, seq, heads,
+                             head_dim, int(causal), _stream(stream)), "vp_attention_fwd")
+    return out
+
+
+def attention_bwd(qkv, out, dout, lse, dqkv, delta_ws, batch, seq, heads, head_dim, causal=True,
+                  stream=None):
+    check(L.vp_attention_bwd(qkv.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(),
+                             dqkv.data_ptr(), delta_ws.data_ptr(), batch, seq, heads, head_dim,
+                             int(causal), _stream(stream)), "vp_attention_bwd")
+    return dqkv
+
+
+def embed_fwd(ids, wte, wpe, x, batch, seq, stream=None):
+    check(L.vp_embed_fwd(ids.data_ptr(), wte.data_ptr(), wpe.data_ptr(), x.data_ptr(), batch, seq,
+                         wte.shape[1], _stream(stream)), "vp_embed_fwd")
+    return x
+
+
+def embed_bwd(ids, dx, dwte, dwpe, batch, seq, stream=None):
+    check(L.vp_embed_bwd(ids.data_ptr(), dx.data_ptr(), dwte.data_ptr(), _p(dwpe), batch, seq,
+                         dx.shape[1], _stream(stream)), "vp_embed_bwd")
+
+
+def xent_fwd_bwd(logits, labels, loss_rows, scale, stream=None):
+    rows, vocab = logits.shape
+    check(L.vp_xent_fwd_bwd(logits.data_ptr(), labels.data_ptr(), loss_rows.data_ptr(), rows,
+                            vocab, scale, _stream(stream)), "vp_xent_fwd_bwd")
+    return loss_rows
+
+
+def bias_grad_ws_elems(cols: int) -> int:
+    return 64 * cols
+
+
+def bias_grad(dy, dbias, workspace, stream=None):
+    rows, cols = dy.shape
+    check(L.vp_bias_grad(dy.data_ptr(), dbias.data_ptr(), rows, cols, workspace.data_ptr(),
+                         _stream(stream)), "vp_bias_grad")
+
+
+def dropout_(x, p, seed, offset, stream=None):
+    check(L.vp_dropout(x.data_ptr(), x.numel(), p, seed, offset, _stream(stream)), "vp_dropout")
+    return x
+
+
+def add(a, b, y, stream=None):
+    check(L.vp_add(a.data_ptr(), b.data_ptr(), y.data_ptr(), a.numel(), _stream(stream)), "vp_add")
+    return y
+
+
+def grad_norm_sq(g, out, stream=None):
+    check(L.vp_grad_norm_sq(g.data_ptr(), g.numel(), out.data_ptr(), _stream(stream)),
+          "vp_grad_norm_sq")
+
+
+def adam_step(master, weight, grad, m, v, flags, lr, beta1, beta2, eps, weight_decay,
+              inv_loss_scale, max_grad_norm, step, stream=None):
+    bc1 = 1.0 - beta1 ** step
+    bc2 = 1.0 - beta2 ** step
+    check(L.vp_adam_step(master.data_ptr(), weight.data_ptr(), grad.data_ptr(), m.data_ptr(),
+                         v.data_ptr(), master.numel(), flags.data_ptr(), lr, beta1, beta2, eps,
+                         weight_decay, inv_loss_scale, max_grad_norm, bc1, bc2, _stream(stream)),
+          "vp_adam_step")
+
+
+def cast_f32_bf16(x, y, stream=None):
+    check(L.vp_cast_f32_bf16(x.data_ptr(), y.data_ptr(), x.numel(), _stream(stream)),
+          "vp_cast_f32_bf16")
+
+
+def p2p_put(dst_ptr: int, src, nbytes=None, stream=None):
+    nbytes = src.numel() * src.element_size() if nbytes is None else nbytes
+    check(L.vp_p2p_put(dst_ptr, src.data_ptr(), nbytes, _stream(stream)), "vp_p2p_put")

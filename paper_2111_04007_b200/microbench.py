@@ -1,10 +1,11 @@
 """Time vp_gemm_bf16 on the BASELINE shapes with CUDA events (L2-flushed)."""
 import json
+import os
 import sys
 
 import torch
 
-sys.path.insert(0, ".")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2111_04007_b200 import kernels as K  # noqa: E402
 
 

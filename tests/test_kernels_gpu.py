@@ -1,0 +1,193 @@
+"""Fused HBM-bound kernels + attention vs torch fp32 references of the same
+ops (stated tolerances; bf16 storage)."""
+
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2111_04007_b200 import kernels as K
+
+
+def rel(a, b):
+    return ((a.float() - b.float()).norm() / b.float().norm().clamp_min(1e-12)).item()
+
+
+@pytest.mark.parametrize("rows,cols", [(8192, 1024), (4096, 1920), (4096, 3072), (512, 256),
+                                       (33, 64)])
+def test_layernorm(rows, cols):
+    torch.manual_seed(0)
+    x = (torch.randn(rows, cols, device="cuda") * 2 + 0.5).bfloat16()
+    g = (1 + 0.1 * torch.randn(cols, device="cuda")).bfloat16()
+    b = (0.1 * torch.randn(cols, device="cuda")).bfloat16()
+    y = torch.empty_like(x)
+    mean = torch.empty(rows, device="cuda")
+    rstd = torch.empty(rows, device="cuda")
+    K.layernorm_fwd(x, g, b, y, mean, rstd)
+    xr = x.float().requires_grad_()
+    gr = g.float().requires_grad_()
+    br = b.float().requires_grad_()
+    yr = torch.nn.functional.layer_norm(xr, (cols,), gr, br, 1e-5)
+    assert rel(y, yr) < 1e-2
+    dy = torch.randn(rows, cols, device="cuda").bfloat16()
+    yr.backward(dy.float())
+    dx = torch.zeros_like(x)
+    dg = torch.zeros(cols, device="cuda")
+    db = torch.zeros(cols, device="cuda")
+    ws = torch.empty(K.layernorm_ws_elems(cols), device="cuda")
+    K.layernorm_bwd(dy, x, g, mean, rstd, dx, dg, db, ws)
+    assert rel(dx, xr.grad) < 1e-2
+    assert rel(dg, gr.grad) < 1e-3
+    assert rel(db, br.grad) < 1e-3
+    # accumulate mode adds into an existing residual gradient
+    dx2 = dy.clone()
+    K.layernorm_bwd(dy, x, g, mean, rstd, dx2, dg, db, ws, accumulate=True)
+    assert rel(dx2, xr.grad + dy.float()) < 1e-2
+
+
+def ref_attention(qkv, B, S, H, D, causal):
+    q, k, v = qkv.float().view(B, S, 3, H, D).permute(2, 0, 3, 1, 4)
+    s = q @ k.transpose(-1, -2) / math.sqrt(D)
+    if causal:
+        mask = torch.ones(S, S, device=qkv.device, dtype=torch.bool).triu(1)
+        s = s.masked_fill(mask, float("-inf"))
+    p = s.softmax(-1)
+    return (p @ v).permute(0, 2, 1, 3).reshape(B * S, H * D)
+
+
+@pytest.mark.parametrize("B,S,H,D,causal", [(2, 128, 4, 64, True), (2, 1024, 4, 64, True),
+                                            (1, 1024, 2, 96, True), (2, 512, 4, 64, False),
+                                            (1, 200, 3, 64, True), (1, 77, 2, 96, False),
+                                            (1, 256, 2, 128, True)])
+def test_attention(B, S, H, D, causal):
+    torch.manual_seed(0)
+    qkv = torch.randn(B * S, 3 * H * D, device="cuda").bfloat16()
+    o = torch.empty(B * S, H * D, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(B * H * S, device="cuda")
+    K.attention_fwd(qkv, o, lse, B, S, H, D, causal)
+    q = qkv.float().requires_grad_()
+    ref = ref_attention(q, B, S, H, D, causal)
+    assert rel(o, ref) < 1e-2
+    do = torch.randn_like(o)
+    ref.backward(do.float())
+    dqkv = torch.empty_like(qkv)
+    delta = torch.empty(B * H * S, device="cuda")
+    K.attention_bwd(qkv, o, do, lse, dqkv, delta, B, S, H, D, causal)
+    g = q.grad.view(B * S, 3, H * D)
+    d = dqkv.view(B * S, 3, H * D)
+    for i, name in enumerate("qkv"):
+        assert rel(d[:, i], g[:, i]) < 2e-2, name
+
+
+def test_attention_forward_deterministic():
+    torch.manual_seed(1)
+    B, S, H, D = 2, 512, 4, 64
+    qkv = torch.randn(B * S, 3 * H * D, device="cuda").bfloat16()
+    o1 = torch.empty(B * S, H * D, device="cuda", dtype=torch.bfloat16)
+    o2 = torch.empty_like(o1)
+    lse = torch.empty(B * H * S, device="cuda")
+    K.attention_fwd(qkv, o1, lse, B, S, H, D, True)
+    K.attention_fwd(qkv, o2, lse, B, S, H, D, True)
+    assert torch.equal(o1, o2)  # recompute (R) must reproduce F bitwise
+
+
+def test_embedding():
+    torch.manual_seed(0)
+    B, S, V, Hd = 4, 128, 1000, 256
+    ids = torch.randint(0, V, (B * S,), device="cuda")
+    wte = torch.randn(V, Hd, device="cuda").bfloat16()
+    wpe = torch.randn(S, Hd, device="cuda").bfloat16()
+    x = torch.empty(B * S, Hd, device="cuda", dtype=torch.bfloat16)
+    K.embed_fwd(ids, wte, wpe, x, B, S)
+    ref = wte.float()[ids] + wpe.float().repeat(B, 1)
+    assert rel(x, ref) < 1e-2
+    dx = torch.randn(B * S, Hd, device="cuda").bfloat16()
+    dwte = torch.zeros(V, Hd, device="cuda")
+    dwpe = torch.zeros(S, Hd, device="cuda")
+    K.embed_bwd(ids, dx, dwte, dwpe, B, S)
+    ref_wte = torch.zeros(V, Hd, device="cuda").index_add_(0, ids, dx.float())
+    assert rel(dwte, ref_wte) < 1e-5
+    assert rel(dwpe, dx.float().view(B, S, Hd).sum(0)) < 1e-5
+
+
+@pytest.mark.parametrize("rows,V", [(512, 51200), (64, 30528), (100, 1000)])
+def test_xent(rows, V):
+    torch.manual_seed(0)
+    logits = (torch.randn(rows, V, device="cuda") * 3).bfloat16()
+    labels = torch.randint(0, V, (rows,), device="cuda")
+    labels[::7] = -100
+    lg = logits.float().requires_grad_()
+    ref = torch.nn.functional.cross_entropy(lg, labels, ignore_index=-100, reduction="none")
+    n_valid = int((labels >= 0).sum())
+    ref.sum().div(n_valid).backward()
+    loss = torch.empty(rows, device="cuda")
+    work = logits.clone()
+    K.xent_fwd_bwd(work, labels, loss, 1.0 / n_valid)
+    assert rel(loss, ref) < 1e-3
+    assert rel(work, lg.grad) < 1e-2
+
+
+def test_bias_grad_and_misc():
+    torch.manual_seed(0)
+    dy = torch.randn(8192, 3072, device="cuda").bfloat16()
+    db = torch.ones(3072, device="cuda")
+    ws = torch.empty(K.bias_grad_ws_elems(3072), device="cuda")
+    K.bias_grad(dy, db, ws)
+    assert rel(db, 1 + dy.float().sum(0)) < 1e-5
+    a = torch.randn(1000, 24, device="cuda").bfloat16()
+    b = torch.randn(1000, 24, device="cuda").bfloat16()
+    y = torch.empty_like(a)
+    K.add(a, b, y)
+    assert rel(y, a.float() + b.float()) < 1e-2
+    x = torch.ones(1 << 20, device="cuda").bfloat16()
+    K.dropout_(x, 0.1, 1234, 0)
+    frac = (x == 0).float().mean().item()
+    assert abs(frac - 0.1) < 0.01
+    assert abs(x.float().mean().item() - 1.0) < 0.02
+    x2 = torch.ones(1 << 20, device="cuda").bfloat16()
+    K.dropout_(x2, 0.1, 1234, 0)
+    assert torch.equal(x, x2)  # recompute regenerates the identical mask
+
+
+def test_adam_matches_torch():
+    torch.manual_seed(0)
+    n = 100_003
+    w0 = torch.randn(n, device="cuda")
+    master = w0.clone()
+    wbf = w0.bfloat16()
+    m = torch.zeros(n, device="cuda")
+    v = torch.zeros(n, device="cuda")
+    ref = w0.clone().requires_grad_()
+    opt = torch.optim.AdamW([ref], lr=1e-3, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.01)
+    for step in range(1, 4):
+        g = torch.randn(n, device="cuda")
+        grad = g.clone()
+        flags = torch.zeros(2, device="cuda")
+        K.grad_norm_sq(grad, flags)
+        assert abs(flags[0].item() - (g * g).sum().item()) / (g * g).sum().item() < 1e-4
+        K.adam_step(master, wbf, grad, m, v, flags, 1e-3, 0.9, 0.999, 1e-8, 0.01, 1.0, 0.0, step)
+        ref.grad = g
+        opt.step()
+        assert torch.all(grad == 0)
+    # torch AdamW applies decoupled decay as w *= (1 - lr*wd) before the Adam update.
+    assert rel(master, ref.detach()) < 1e-4
+    assert rel(wbf, ref.detach()) < 1e-2
+    flags = torch.tensor([1.0, 1.0], device="cuda")  # overflow -> skipped step
+    before = master.clone()
+    grad = torch.randn(n, device="cuda")
+    K.adam_step(master, wbf, grad, m, v, flags, 1e-3, 0.9, 0.999, 1e-8, 0.01, 1.0, 0.0, 4)
+    assert torch.equal(master, before)
+
+
+def test_p2p_put_local():
+    src = torch.randn(1 << 22, device="cuda")
+    dst = torch.zeros_like(src)
+    K.p2p_put(dst.data_ptr(), src)
+    assert torch.equal(src, dst)
+    s2 = torch.randint(0, 255, (1001,), device="cuda", dtype=torch.uint8)
+    d2 = torch.zeros_like(s2)
+    K.p2p_put(d2.data_ptr(), s2)
+    assert torch.equal(s2, d2)
