@@ -141,11 +141,11 @@ int vp_embed_fwd(const int64_t* ids, const void* wte, const void* wpe, void* x, 
 int vp_embed_bwd(const int64_t* ids, const void* dx, float* dwte, float* dwpe, int64_t batch,
                  int64_t seq, int64_t hidden, void* stream);
 
-/* Softmax cross-entropy over logits[T,V] (bf16). Writes per-row loss (fp32)
- * and overwrites logits with dlogits = (softmax - onehot) * scale.
- * labels < 0 are ignored (zero grad, zero loss). */
-int vp_xent_fwd_bwd(void* logits, const int64_t* labels, float* loss_rows, int64_t rows,
-                    int64_t vocab, float scale, void* stream);
+/* Softmax cross-entropy over logits[T,V] (bf16). Writes per-row loss (fp32),
+ * adds sum(row_loss)*scale into *loss_sum (optional), and overwrites logits
+ * with dlogits = (softmax - onehot) * scale. labels < 0 are ignored. */
+int vp_xent_fwd_bwd(void* logits, const int64_t* labels, float* loss_rows, float* loss_sum,
+                    int64_t rows, int64_t vocab, float scale, void* stream);
 
 /* Column sum of dy[rows, cols] (bf16) accumulated into dbias (fp32). */
 int vp_bias_grad(const void* dy, float* dbias, int64_t rows, int64_t cols, float* workspace,
@@ -180,6 +180,10 @@ int vp_cast_f32_bf16(const float* x, void* y, int64_t n, void* stream);
  * send() (sp/engine/py_kernel.py:184-214, sp/calibration.py:95-110).
  * ====================================================================== */
 #define VP_IPC_HANDLE_BYTES 64
+/* Dedicated device allocation (its own cudaMalloc, so an IPC handle maps
+ * exactly this buffer at offset 0) and release. */
+int vp_device_alloc(int64_t bytes, void** ptr_out);
+int vp_device_free(void* ptr);
 /* Export a device allocation / create+export an interprocess event. */
 int vp_ipc_get_mem_handle(void* dev_ptr, void* handle_out /*64 bytes*/);
 int vp_ipc_open_mem_handle(const void* handle /*64 bytes*/, void** dev_ptr_out);

@@ -62,7 +62,8 @@ __global__ void embed_bwd_pos_kernel(const __nv_bfloat16* __restrict__ dx,
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS)
     xent_kernel(__nv_bfloat16* __restrict__ logits, const int64_t* __restrict__ labels,
-                float* __restrict__ loss_rows, int64_t vocab, float scale) {
+                float* __restrict__ loss_rows, float* __restrict__ loss_sum, int64_t vocab,
+                float scale) {
   const int64_t row = blockIdx.x;
   __nv_bfloat16* lr = logits + row * vocab;
   const int64_t label = labels[row];
@@ -108,10 +109,9 @@ __global__ void __launch_bounds__(THREADS)
     }
     const float lse = M + __logf(S);
     s_lse = lse;
-    if (label >= 0 && label < vocab)
-      loss_rows[row] = lse - __bfloat162float(lr[label]);
-    else
-      loss_rows[row] = 0.f;
+    const float l = (label >= 0 && label < vocab) ? lse - __bfloat162float(lr[label]) : 0.f;
+    loss_rows[row] = l;
+    if (loss_sum && l != 0.f) atomicAdd(loss_sum, l * scale);
   }
   __syncthreads();
   const float lse = s_lse;
@@ -299,10 +299,11 @@ extern "C" int vp_embed_bwd(const int64_t* ids, const void* dx, float* dwte, flo
 }
 
 extern "C" int vp_xent_fwd_bwd(void* logits, const int64_t* labels, float* loss_rows,
-                               int64_t rows, int64_t vocab, float scale, void* stream) {
+                               float* loss_sum, int64_t rows, int64_t vocab, float scale,
+                               void* stream) {
   if (rows <= 0 || vocab <= 0 || (vocab % 8)) return VP_ERR_ARGS;
   xent_kernel<512><<<static_cast<unsigned>(rows), 512, 0, ST>>>(BF(logits), labels, loss_rows,
-                                                                vocab, scale);
+                                                                loss_sum, vocab, scale);
   return launch_status();
 }
 

@@ -37,6 +37,12 @@ __global__ void put_tail_kernel(uint8_t* dst, const uint8_t* src, int64_t n) {
 
 using namespace vp;
 
+extern "C" int vp_device_alloc(int64_t bytes, void** ptr_out) {
+  if (bytes <= 0 || !ptr_out) return VP_ERR_ARGS;
+  return cudaMalloc(ptr_out, static_cast<size_t>(bytes));
+}
+extern "C" int vp_device_free(void* ptr) { return cudaFree(ptr); }
+
 extern "C" int vp_ipc_get_mem_handle(void* dev_ptr, void* handle_out) {
   if (!dev_ptr || !handle_out) return VP_ERR_ARGS;
   cudaIpcMemHandle_t h;

@@ -30,7 +30,9 @@ _SIGS = {
     "vp_attention_bwd": [vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, c_int, vp],
     "vp_embed_fwd": [vp, vp, vp, vp, i64, i64, i64, vp],
     "vp_embed_bwd": [vp, vp, vp, vp, i64, i64, i64, vp],
-    "vp_xent_fwd_bwd": [vp, vp, vp, i64, i64, f32, vp],
+    "vp_xent_fwd_bwd": [vp, vp, vp, vp, i64, i64, f32, vp],
+    "vp_device_alloc": [i64, ctypes.POINTER(vp)],
+    "vp_device_free": [vp],
     "vp_bias_grad": [vp, vp, i64, i64, vp, vp],
     "vp_dropout": [vp, i64, f32, u64, u64, vp],
     "vp_add": [vp, vp, vp, i64, vp],
@@ -77,7 +79,7 @@ def sm_count() -> int:
 
 
 def gemm(a, b, out, *, a_kmajor=True, b_kmajor=True, epilogue=EPI_STORE, bias=None, aux=None,
-         M=None, N=None, K=None, stream=None):
+         M=None, N=None, K=None, stream=None, out_ptr=None, ldd=None):
     """out[M,N] = epi(op(a) @ op(b)^T) where op(a) is [M,K] (a_kmajor: a is
     [M,K], else a is [K,M]) and op(b) is [N,K] (b_kmajor: b is [N,K], else
     [K,N]). All operands bf16 row-major with unit inner stride; out is bf16
@@ -90,11 +92,13 @@ def gemm(a, b, out, *, a_kmajor=True, b_kmajor=True, epilogue=EPI_STORE, bias=No
         K = a.shape[1] if a_kmajor else a.shape[0]
     if N is None:
         N = b.shape[0] if b_kmajor else b.shape[1]
-    for t in (a, b, out) + ((aux,) if aux is not None else ()):
+    for t in (a, b) + tuple(x for x in (out, aux) if x is not None):
         if t.stride(-1) != 1:
             raise ValueError("gemm: inner stride must be 1")
+    if out is not None:
+        out_ptr, ldd = out.data_ptr(), out.stride(0)
     check(L.vp_gemm_bf16(int(a_kmajor), int(b_kmajor), epilogue, a.data_ptr(), a.stride(0),
-                         b.data_ptr(), b.stride(0), out.data_ptr(), out.stride(0), _p(bias),
+                         b.data_ptr(), b.stride(0), out_ptr, ldd, _p(bias),
                          _p(aux), aux.stride(0) if aux is not None else 0, M, N, K,
                          _stream(stream)), "vp_gemm_bf16")
     return out
@@ -147,10 +151,10 @@ def embed_bwd(ids, dx, dwte, dwpe, batch, seq, stream=None):
                          dx.shape[1], _stream(stream)), "vp_embed_bwd")
 
 
-def xent_fwd_bwd(logits, labels, loss_rows, scale, stream=None):
+def xent_fwd_bwd(logits, labels, loss_rows, scale, loss_sum=None, stream=None):
     rows, vocab = logits.shape
-    check(L.vp_xent_fwd_bwd(logits.data_ptr(), labels.data_ptr(), loss_rows.data_ptr(), rows,
-                            vocab, scale, _stream(stream)), "vp_xent_fwd_bwd")
+    check(L.vp_xent_fwd_bwd(logits.data_ptr(), labels.data_ptr(), loss_rows.data_ptr(),
+                            _p(loss_sum), rows, vocab, scale, _stream(stream)), "vp_xent_fwd_bwd")
     return loss_rows
 
 
@@ -197,3 +201,38 @@ def cast_f32_bf16(x, y, stream=None):
 def p2p_put(dst_ptr: int, src, nbytes=None, stream=None):
     nbytes = src.numel() * src.element_size() if nbytes is None else nbytes
     check(L.vp_p2p_put(dst_ptr, src.data_ptr(), nbytes, _stream(stream)), "vp_p2p_put")
+
+
+class DeviceBuffer:
+    """A dedicated cudaMalloc allocation (IPC-exportable at offset 0), exposed
+    to torch zero-copy through __cuda_array_interface__."""
+
+    def __init__(self, nbytes: int):
+        p = vp()
+        check(L.vp_device_alloc(nbytes, ctypes.byref(p)), "vp_device_alloc")
+        self.ptr = p.value
+        self.nbytes = nbytes
+
+    def tensor(self, shape, dtype=torch.bfloat16, offset_bytes=0):
+        import math
+        itemsize = torch.tensor([], dtype=dtype).element_size()
+        n = math.prod(shape)
+        assert offset_bytes + n * itemsize <= self.nbytes
+        typestr = {torch.bfloat16: "<f2", torch.float32: "<f4", torch.int64: "<i8",
+                   torch.uint8: "|u1"}[dtype]
+        holder = self
+
+        class _Iface:
+            __cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                        "data": (self.ptr + offset_bytes, False), "version": 2,
+                                        "strides": None}
+            _keep = holder
+        t = torch.as_tensor(_Iface(), device=torch.cuda.current_device())
+        if dtype == torch.bfloat16:
+            t = t.view(torch.bfloat16)
+        return t
+
+    def free(self):
+        if self.ptr:
+            L.vp_device_free(self.ptr)
+            self.ptr = 0

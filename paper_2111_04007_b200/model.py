@@ -1,0 +1,407 @@
+"""GPT-2 pipeline stage on sm_100a kernels.
+
+A stage owns the transformer layers (= CutPoints, one per layer boundary;
+the K = L block model of sp/core.py:93-114) that ``stage_map`` assigns to it,
+plus the token/position embedding on stage 0 and the final LayerNorm + tied
+LM head on the last stage. Every dense contraction is ``vp_gemm_bf16``
+(tcgen05/TMEM), attention is ``vp_attention_*``, LayerNorm/GELU/softmax/
+cross-entropy/embedding are fused kernels — PyTorch only allocates memory.
+
+Memory layout (HBM): all stage parameters live in flat buffers — bf16
+weights, fp32 master, fp32 grad, fp32 Adam moments — so the optimizer is one
+kernel per stage and the DP allreduce one NCCL call per stage. Per layer the
+*working set* (saved intermediates for backward) is allocated once: Varuna's
+rule 2 (R(j) is immediately followed by B(j), sp/scheduler.py:228-235) and
+the last stage's F/B alternation guarantee at most one live working set.
+
+Forward modes: ``save=False`` keeps only the stage input (the stash) —
+Varuna's checkpointed F on stages k < P-1; ``save=True`` (R, and F on the
+last stage) writes the working set. Both run the identical kernel sequence,
+so R reproduces F bit for bit.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Tuple
+
+import torch
+
+from . import kernels as K
+
+
+@dataclass(frozen=True)
+class GPT2Config:
+    vocab_size: int = 51200
+    n_layer: int = 24
+    hidden: int = 1024
+    heads: int = 16
+    seq_len: int = 1024
+    ln_eps: float = 1e-5
+    dropout: float = 0.0
+    init_std: float = 0.02
+    causal: bool = True
+
+    @property
+    def head_dim(self) -> int:
+        return self.hidden // self.heads
+
+    def layer_param_count(self) -> int:
+        h = self.hidden
+        return 12 * h * h + 13 * h
+
+    def flops_per_token_layer(self) -> int:
+        """Forward FLOPs per token per layer, Megatron convention (full
+        attention, causal half not subtracted): 24 h^2 + 4 s h."""
+        return 24 * self.hidden ** 2 + 4 * self.seq_len * self.hidden
+
+    def head_flops_per_token(self) -> int:
+        return 2 * self.hidden * self.vocab_size
+
+
+# BASELINE.json configs.
+CONFIGS = {
+    "tiny": GPT2Config(vocab_size=50304, n_layer=4, hidden=256, heads=4, seq_len=128),
+    "gpt2_355m": GPT2Config(vocab_size=51200, n_layer=24, hidden=1024, heads=16, seq_len=1024),
+    "gpt2_2_5b": GPT2Config(vocab_size=51200, n_layer=54, hidden=1920, heads=20, seq_len=1024),
+    "gpt2_8_3b": GPT2Config(vocab_size=51200, n_layer=72, hidden=3072, heads=32, seq_len=1024),
+}
+
+
+def layer_param_shapes(cfg: GPT2Config) -> List[Tuple[str, Tuple[int, ...]]]:
+    h = cfg.hidden
+    return [("ln1_g", (h,)), ("ln1_b", (h,)), ("w_qkv", (3 * h, h)), ("b_qkv", (3 * h,)),
+            ("w_o", (h, h)), ("b_o", (h,)), ("ln2_g", (h,)), ("ln2_b", (h,)),
+            ("w_fc1", (4 * h, h)), ("b_fc1", (4 * h,)), ("w_fc2", (h, 4 * h)), ("b_fc2", (h,))]
+
+
+def init_layer(cfg: GPT2Config, layer: int, seed: int, device="cpu") -> Dict[str, torch.Tensor]:
+    """Deterministic per-layer init keyed by (seed, layer) so every stage map
+    (and the CPU oracle) sees identical weights. N(0, std); residual output
+    projections N(0, std/sqrt(2L)); LN gamma=1, beta=0; biases 0."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed * 1000003 + layer + 1)
+    out = {}
+    proj_std = cfg.init_std / math.sqrt(2 * cfg.n_layer)
+    for name, shape in layer_param_shapes(cfg):
+        if name.endswith("_g"):
+            out[name] = torch.ones(shape, device=device)
+        elif name.startswith("b_") or name.endswith("_b"):
+            out[name] = torch.zeros(shape, device=device)
+        else:
+            std = proj_std if name in ("w_o", "w_fc2") else cfg.init_std
+            out[name] = torch.randn(shape, generator=g, device=device) * std
+    return out
+
+
+def init_embeddings(cfg: GPT2Config, seed: int, device="cpu") -> Dict[str, torch.Tensor]:
+    g = torch.Generator(device=device)
+    g.manual_seed(seed * 1000003)
+    return {"wte": torch.randn((cfg.vocab_size, cfg.hidden), generator=g, device=device)
+            * cfg.init_std,
+            "wpe": torch.randn((cfg.seq_len, cfg.hidden), generator=g, device=device) * 0.01}
+
+
+def round_bf16(t: torch.Tensor) -> torch.Tensor:
+    return t.to(torch.bfloat16).to(torch.float32)
+
+
+class FlatParams:
+    """All parameters of one stage in flat, 256-byte-aligned HBM buffers."""
+
+    def __init__(self, specs: List[Tuple[str, Tuple[int, ...]]], device):
+        self.names = [n for n, _ in specs]
+        self.shapes = dict(specs)
+        self.offsets = {}
+        off = 0
+        for n, s in specs:
+            self.offsets[n] = off
+            numel = math.prod(s)
+            off += (numel + 127) // 128 * 128
+        self.numel = off
+        self.weight = torch.zeros(off, dtype=torch.bfloat16, device=device)
+        self.master = torch.zeros(off, dtype=torch.float32, device=device)
+        self.grad = torch.zeros(off, dtype=torch.float32, device=device)
+        self.exp_avg = torch.zeros(off, dtype=torch.float32, device=device)
+        self.exp_avg_sq = torch.zeros(off, dtype=torch.float32, device=device)
+
+    def view(self, buf: torch.Tensor, name: str) -> torch.Tensor:
+        o = self.offsets[name]
+        s = self.shapes[name]
+        return buf[o:o + math.prod(s)].view(s)
+
+    def w(self, name):
+        return self.view(self.weight, name)
+
+    def g(self, name):
+        return self.view(self.grad, name)
+
+    def load(self, name: str, value: torch.Tensor):
+        """Set fp32 master (rounded to bf16 first, so master == weight) and the
+        bf16 weight."""
+        v = round_bf16(value.float())
+        self.view(self.master, name).copy_(v)
+        self.view(self.weight, name).copy_(v)
+
+    def segment(self, names) -> Tuple[int, int]:
+        lo = min(self.offsets[n] for n in names)
+        hi = max(self.offsets[n] + math.prod(self.shapes[n]) for n in names)
+        return lo, hi
+
+
+class _LayerWS:
+    """Saved intermediates of one transformer layer for one micro-batch."""
+
+    def __init__(self, cfg: GPT2Config, T: int, B: int, dev):
+        h = cfg.hidden
+        bf = dict(dtype=torch.bfloat16, device=dev)
+        f32 = dict(dtype=torch.float32, device=dev)
+        self.a = torch.empty(T, h, **bf)
+        self.qkv = torch.empty(T, 3 * h, **bf)
+        self.o = torch.empty(T, h, **bf)
+        self.lse = torch.empty(B * cfg.heads * cfg.seq_len, **f32)
+        self.x1 = torch.empty(T, h, **bf)
+        self.c = torch.empty(T, h, **bf)
+        self.pre = torch.empty(T, 4 * h, **bf)
+        self.f = torch.empty(T, 4 * h, **bf)
+        self.mean1 = torch.empty(T, **f32)
+        self.rstd1 = torch.empty(T, **f32)
+        self.mean2 = torch.empty(T, **f32)
+        self.rstd2 = torch.empty(T, **f32)
+
+
+@dataclass
+class StageSpec:
+    stage: int
+    n_stages: int
+    layers: Tuple[int, ...]   # global layer (CutPoint) indices owned
+
+    @property
+    def first(self) -> bool:
+        return self.stage == 0
+
+    @property
+    def last(self) -> bool:
+        return self.stage == self.n_stages - 1
+
+
+class GPT2Stage:
+    """One pipeline stage of GPT-2 for micro-batches of ``micro_batch`` rows."""
+
+    def __init__(self, cfg: GPT2Config, spec: StageSpec, micro_batch: int, device,
+                 seed: int = 0, init_device: str = "cpu"):
+        self.cfg, self.spec, self.mb = cfg, spec, micro_batch
+        self.dev = torch.device(device)
+        self.T = micro_batch * cfg.seq_len
+        specs = []
+        if spec.first:
+            specs += [("wte", (cfg.vocab_size, cfg.hidden)), ("wpe", (cfg.seq_len, cfg.hidden))]
+        for li in spec.layers:
+            specs += [(f"l{li}.{n}", s) for n, s in layer_param_shapes(cfg)]
+        if spec.last:
+            specs += [("lnf_g", (cfg.hidden,)), ("lnf_b", (cfg.hidden,))]
+            if not spec.first:
+                specs += [("wte_head", (cfg.vocab_size, cfg.hidden))]
+        self.params = FlatParams(specs, self.dev)
+        self._init(seed, init_device)
+        self._alloc()
+
+    # ------------------------------------------------------------------ init
+    def _init(self, seed, init_device):
+        cfg, spec, P = self.cfg, self.spec, self.params
+        if spec.first or spec.last:
+            emb = init_embeddings(cfg, seed, init_device)
+            if spec.first:
+                P.load("wte", emb["wte"])
+                P.load("wpe", emb["wpe"])
+            if spec.last and not spec.first:
+                P.load("wte_head", emb["wte"])
+        for li in spec.layers:
+            for n, v in init_layer(cfg, li, seed, init_device).items():
+                P.load(f"l{li}.{n}", v)
+        if spec.last:
+            P.load("lnf_g", torch.ones(cfg.hidden))
+            P.load("lnf_b", torch.zeros(cfg.hidden))
+
+    @property
+    def head_weight_name(self) -> str:
+        return "wte" if self.spec.first else "wte_head"
+
+    def _alloc(self):
+        cfg, T, dev = self.cfg, self.T, self.dev
+        h = cfg.hidden
+        bf = dict(dtype=torch.bfloat16, device=dev)
+        f32 = dict(dtype=torch.float32, device=dev)
+        nl = len(self.spec.layers)
+        # residual stream: xs[0] = stage input, xs[i+1] = output of layer i
+        self.xs = [None] + [torch.empty(T, h, **bf) for _ in range(nl)]
+        self.ws = [_LayerWS(cfg, T, self.mb, dev) for _ in range(nl)]
+        self.scratch = _LayerWS(cfg, T, self.mb, dev)   # no-save forward temporaries
+        self.emb_out = torch.empty(T, h, **bf) if self.spec.first else None
+        # backward scratch
+        self.g = torch.empty(T, h, **bf)           # running residual gradient
+        self.dpre = torch.empty(T, 4 * h, **bf)
+        self.dc = torch.empty(T, h, **bf)
+        self.do = torch.empty(T, h, **bf)
+        self.dqkv = torch.empty(T, 3 * h, **bf)
+        self.delta = torch.empty(self.mb * cfg.heads * cfg.seq_len, **f32)
+        self.ln_ws = torch.empty(K.layernorm_ws_elems(h), **f32)
+        self.bias_ws = torch.empty(K.bias_grad_ws_elems(4 * h), **f32)
+        if self.spec.last:
+            self.lnf_out = torch.empty(T, h, **bf)
+            self.lnf_mean = torch.empty(T, **f32)
+            self.lnf_rstd = torch.empty(T, **f32)
+            self.logits = torch.empty(T, cfg.vocab_size, **bf)
+            self.loss_rows = torch.empty(T, **f32)
+        self.drop_tmp = torch.empty(T, h, **bf) if cfg.dropout > 0 else None
+
+    # --------------------------------------------------------------- forward
+    def _layer_fwd(self, li: int, x: torch.Tensor, out, w: _LayerWS, dseed: int, stream=None):
+        cfg, P = self.cfg, self.params
+        p = f"l{li}."
+        K.layernorm_fwd(x, P.w(p + "ln1_g"), P.w(p + "ln1_b"), w.a, w.mean1, w.rstd1,
+                        cfg.ln_eps, stream)
+        K.gemm(w.a, P.w(p + "w_qkv"), w.qkv, epilogue=K.EPI_BIAS, bias=P.w(p + "b_qkv"),
+               stream=stream)
+        K.attention_fwd(w.qkv, w.o, w.lse, self.mb, cfg.seq_len, cfg.heads, cfg.head_dim,
+                        cfg.causal, stream)
+        self._proj_resid(w.o, P.w(p + "w_o"), P.w(p + "b_o"), x, w.x1, dseed, 0, stream)
+        K.layernorm_fwd(w.x1, P.w(p + "ln2_g"), P.w(p + "ln2_b"), w.c, w.mean2, w.rstd2,
+                        cfg.ln_eps, stream)
+        K.gemm(w.c, P.w(p + "w_fc1"), w.f, epilogue=K.EPI_BIAS_GELU, bias=P.w(p + "b_fc1"),
+               aux=w.pre, stream=stream)
+        self._proj_resid(w.f, P.w(p + "w_fc2"), P.w(p + "b_fc2"), w.x1, out, dseed, 1, stream)
+
+    def _proj_resid(self, a, wt, b, resid, out, dseed, which, stream):
+        """out = resid + dropout(a @ wt^T + b) (fused epilogue when p = 0)."""
+        out_t, out_ptr = (None, out) if isinstance(out, int) else (out, None)
+        ld = self.cfg.hidden
+        if self.cfg.dropout <= 0:
+            K.gemm(a, wt, out_t, epilogue=K.EPI_BIAS_RESID, bias=b, aux=resid, stream=stream,
+                   out_ptr=out_ptr, ldd=ld)
+            return
+        tmp = self.drop_tmp
+        K.gemm(a, wt, tmp, epilogue=K.EPI_BIAS, bias=b, stream=stream)
+        K.dropout_(tmp, self.cfg.dropout, dseed, which * tmp.numel(), stream)
+        if out_t is None:
+            out_t = tmp  # dropout + peer write: add locally, then ship
+            K.add(tmp, resid, tmp, stream)
+            K.p2p_put(out_ptr, tmp, stream=stream)
+        else:
+            K.add(tmp, resid, out_t, stream)
+
+    def forward(self, x_in: Optional[torch.Tensor], ids: Optional[torch.Tensor], save: bool,
+                dseed: int = 0, stream=None, out_ptr: Optional[int] = None) -> torch.Tensor:
+        """Run the stage on one micro-batch. Stage 0 takes token ``ids``
+        [T] (int64); others take the received activation ``x_in`` [T, h].
+        Returns the stage output (residual stream after the last layer).
+        ``out_ptr``: write the final layer's output straight into this
+        (NVLink peer-mapped) address from the FC2 GEMM epilogue — the fused
+        compute + P2P send of a checkpointed forward (K9 fused into K1)."""
+        cfg, P = self.cfg, self.params
+        if self.spec.first:
+            K.embed_fwd(ids, P.w("wte"), P.w("wpe"), self.emb_out, self.mb, cfg.seq_len, stream)
+            x = self.emb_out
+            if cfg.dropout > 0:
+                K.dropout_(x, cfg.dropout, dseed ^ 0x5EED, 7 * x.numel(), stream)
+        else:
+            x = x_in
+        self.xs[0] = x
+        nl = len(self.spec.layers)
+        for i, li in enumerate(self.spec.layers):
+            w = self.ws[i] if save else self.scratch
+            dst = out_ptr if (out_ptr is not None and i == nl - 1) else self.xs[i + 1]
+            self._layer_fwd(li, x, dst, w, dseed * 1315423911 + li, stream)
+            x = self.xs[i + 1]
+        return x
+
+    def loss_and_head_backward(self, labels: torch.Tensor, loss_scale: float, loss_sum=None,
+                               stream=None):
+        """Last stage: final LN + tied head + softmax cross-entropy fwd/bwd.
+        Leaves d(stage output) in ``self.g``; returns the per-row losses."""
+        cfg, P = self.cfg, self.params
+        x = self.xs[-1]
+        K.layernorm_fwd(x, P.w("lnf_g"), P.w("lnf_b"), self.lnf_out, self.lnf_mean,
+                        self.lnf_rstd, cfg.ln_eps, stream)
+        wte = P.w(self.head_weight_name)
+        K.gemm(self.lnf_out, wte, self.logits, stream=stream)
+        K.xent_fwd_bwd(self.logits, labels, self.loss_rows, loss_scale, loss_sum, stream)
+        # dlnf_out = dlogits @ wte ; dwte += dlogits^T @ lnf_out
+        K.gemm(self.logits, wte, self.dc, b_kmajor=False, stream=stream)
+        K.gemm(self.logits, self.lnf_out, P.g(self.head_weight_name), a_kmajor=False,
+               b_kmajor=False, epilogue=K.EPI_ACC_F32, stream=stream)
+        K.layernorm_bwd(self.dc, x, P.w("lnf_g"), self.lnf_mean, self.lnf_rstd, self.g,
+                        P.g("lnf_g"), P.g("lnf_b"), self.ln_ws, accumulate=False, stream=stream)
+        return self.loss_rows
+
+    # -------------------------------------------------------------- backward
+    def _drop_grad(self, g, dseed, which, stream):
+        """Gradient through out = resid + dropout(y): dy = dropout_mask(g)."""
+        if self.cfg.dropout <= 0:
+            return g
+        self.drop_tmp.copy_(g)
+        K.dropout_(self.drop_tmp, self.cfg.dropout, dseed, which * g.numel(), stream)
+        return self.drop_tmp
+
+    def _layer_bwd(self, li: int, w: _LayerWS, x: torch.Tensor, dseed: int, stream=None):
+        """self.g holds d(layer output); on return it holds d(layer input)."""
+        cfg, P = self.cfg, self.params
+        p = f"l{li}."
+        g = self.g
+        # --- MLP: out = x1 + fc2(gelu(fc1(ln2(x1))))
+        gy = self._drop_grad(g, dseed, 1, stream)
+        K.gemm(gy, P.w(p + "w_fc2"), self.dpre, b_kmajor=False, epilogue=K.EPI_DGELU,
+               aux=w.pre, stream=stream)
+        K.gemm(gy, w.f, P.g(p + "w_fc2"), a_kmajor=False, b_kmajor=False,
+               epilogue=K.EPI_ACC_F32, stream=stream)
+        K.bias_grad(gy, P.g(p + "b_fc2"), self.bias_ws, stream)
+        K.gemm(self.dpre, P.w(p + "w_fc1"), self.dc, b_kmajor=False, stream=stream)
+        K.gemm(self.dpre, w.c, P.g(p + "w_fc1"), a_kmajor=False, b_kmajor=False,
+               epilogue=K.EPI_ACC_F32, stream=stream)
+        K.bias_grad(self.dpre, P.g(p + "b_fc1"), self.bias_ws, stream)
+        K.layernorm_bwd(self.dc, w.x1, P.w(p + "ln2_g"), w.mean2, w.rstd2, g,
+                        P.g(p + "ln2_g"), P.g(p + "ln2_b"), self.ln_ws, accumulate=True,
+                        stream=stream)
+        # --- attention: x1 = x + proj(attn(qkv(ln1(x))))
+        gy = self._drop_grad(g, dseed, 0, stream)
+        K.gemm(gy, P.w(p + "w_o"), self.do, b_kmajor=False, stream=stream)
+        K.gemm(gy, w.o, P.g(p + "w_o"), a_kmajor=False, b_kmajor=False,
+               epilogue=K.EPI_ACC_F32, stream=stream)
+        K.bias_grad(gy, P.g(p + "b_o"), self.bias_ws, stream)
+        K.attention_bwd(w.qkv, w.o, self.do, w.lse, self.dqkv, self.delta, self.mb,
+                        cfg.seq_len, cfg.heads, cfg.head_dim, cfg.causal, stream)
+        K.gemm(self.dqkv, P.w(p + "w_qkv"), self.dc, b_kmajor=False, stream=stream)
+        K.gemm(self.dqkv, w.a, P.g(p + "w_qkv"), a_kmajor=False, b_kmajor=False,
+               epilogue=K.EPI_ACC_F32, stream=stream)
+        K.bias_grad(self.dqkv, P.g(p + "b_qkv"), self.bias_ws, stream)
+        K.layernorm_bwd(self.dc, x, P.w(p + "ln1_g"), w.mean1, w.rstd1, g,
+                        P.g(p + "ln1_g"), P.g(p + "ln1_b"), self.ln_ws, accumulate=True,
+                        stream=stream)
+
+    def backward(self, grad_out: Optional[torch.Tensor], ids: Optional[torch.Tensor],
+                 dseed: int = 0, stream=None) -> torch.Tensor:
+        """Backward through the stage's layers using the saved working set.
+        ``grad_out`` = d(stage output) from the next stage (None on the last
+        stage, where loss_and_head_backward already filled ``self.g``).
+        Returns d(stage input) (in ``self.g``); on stage 0 it is consumed by
+        the embedding backward instead."""
+        cfg, P = self.cfg, self.params
+        if grad_out is not None:
+            self.g.copy_(grad_out)
+        for i in range(len(self.spec.layers) - 1, -1, -1):
+            li = self.spec.layers[i]
+            self._layer_bwd(li, self.ws[i], self.xs[i], dseed * 1315423911 + li, stream)
+        if self.spec.first:
+            if cfg.dropout > 0:
+                K.dropout_(self.g, cfg.dropout, dseed ^ 0x5EED, 7 * self.g.numel(), stream)
+            K.embed_bwd(ids, self.g, P.g("wte"), P.g("wpe"), self.mb, cfg.seq_len, stream)
+        return self.g
+
+    # ------------------------------------------------------------- utilities
+    def flops_per_microbatch(self) -> int:
+        """Algorithmic forward FLOPs of this stage for one micro-batch."""
+        f = len(self.spec.layers) * self.cfg.flops_per_token_layer() * self.T
+        if self.spec.last:
+            f += self.cfg.head_flops_per_token() * self.T
+        return f

@@ -1,0 +1,473 @@
+"""The Varuna executor: ``Varuna`` wrapper, ``CutPoint`` markers, ``step()``.
+
+One process per GPU. Rank = r·P + s — the reference placement (stage s of
+replica r on slot r·P + s, sp/simulator.py:58-81). Each rank instantiates
+only the layers ``ParallelConfig.stage_map`` gives its stage (the CutPoint
+→ stage assignment computed by ``assign_stages``, sp/partitioner.py:269-374)
+and walks its slice of the Varuna plan (``generate_varuna_schedule(P, N_m,
+1, 2, 1)``, sp/scheduler.py:128-145; always (1,2,1): sp/planner.py:204-208):
+
+* F(j): stage forward WITHOUT saving intermediates (k < P-1); the last
+  layer's FC2 epilogue writes the stage output straight into stage k+1's
+  activation ring slot j over NVLink (IPC-mapped peer memory), then an
+  interprocess event is recorded that stage k+1's stream waits on.
+* R(j): the same forward from the stashed input (the received ring slot),
+  this time saving the working set (Varuna's recompute; bitwise ≡ F).
+* B(j): backward from the gradient ring slot j; the input gradient is put
+  into stage k-1's gradient ring slot j by an SM copy kernel over NVLink.
+* the last stage runs F(j) with saving and B(j) right after (no R).
+
+End of mini-batch (per stage, as soon as its last B is done —
+allreduce_barrier=False, sp/simulator.py:334-342): NCCL allreduce of the
+flat fp32 gradient over the stage's DP group (C1), tied-embedding gradient
+allreduce between stage 0 and P-1 (C3), a pipeline-wide (grad-norm²,
+non-finite count) allreduce (C2), then one fused unscale + overflow-skip +
+clip + AdamW kernel over the stage's flat parameters.
+
+Host↔host ordering uses per-slot sequence counters in POSIX shared memory
+(all ranks of one box); device ordering uses the IPC events only — no host
+synchronisation on the data path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import time
+from dataclasses import dataclass, field
+from multiprocessing import shared_memory
+from typing import Dict, List, Optional
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import kernels as K
+from ._lib import check
+from .core import KIND_BACKWARD, KIND_FORWARD, KIND_RECOMPUTE, ConfigError, ParallelConfig
+from .model import GPT2Config, GPT2Stage, StageSpec
+from .scheduler import Schedule, generate_varuna_schedule
+from .simulator import bubble_fraction
+
+F, R, B = KIND_FORWARD, KIND_RECOMPUTE, KIND_BACKWARD
+
+
+class CutPoint(torch.nn.Module):
+    """Marks a candidate pipeline boundary. Identity in the
+    forward pass; whether it is an active stage boundary is decided by
+    ``ParallelConfig.stage_map``. The GPT-2 model carries one CutPoint after
+    every transformer layer (K = n_layer)."""
+
+    def __init__(self, index: int = 0):
+        super().__init__()
+        self.index = index
+
+    def forward(self, x):
+        return x
+
+
+@dataclass(frozen=True)
+class AdamWConfig:
+    lr: float = 1e-4
+    betas: tuple = (0.9, 0.999)
+    eps: float = 1e-8
+    weight_decay: float = 0.01
+    max_grad_norm: float = 1.0
+
+
+@dataclass
+class StepResult:
+    """Loss is only known on last-stage ranks (None elsewhere)."""
+
+    _loss: Optional[torch.Tensor]
+    _flags: torch.Tensor
+    inv_scale: float
+    timeline: Optional[dict] = None
+
+    @property
+    def loss(self) -> Optional[float]:
+        return None if self._loss is None else float(self._loss.item())
+
+    @property
+    def overflow(self) -> bool:
+        return bool(self._flags[1].item() != 0)
+
+    @property
+    def grad_norm(self) -> float:
+        return math.sqrt(max(float(self._flags[0].item()), 0.0)) * self.inv_scale
+
+
+def synthetic_batch(cfg: GPT2Config, rows: int, replica: int, step: int = 0, seed: int = 1234):
+    """Deterministic token rows for one replica: global row g = replica·rows + i
+    (DP replicas partition M_total). Labels are inputs shifted by one."""
+    g = torch.Generator()
+    g.manual_seed(seed + 7919 * replica + 104729 * step)
+    toks = torch.randint(0, cfg.vocab_size, (rows, cfg.seq_len + 1), generator=g)
+    return {"input_ids": toks[:, :-1].contiguous(), "labels": toks[:, 1:].contiguous()}
+
+
+class _Shm:
+    """Per-(sender rank, direction, slot) int64 sequence counters shared by
+    the processes of one box."""
+
+    def __init__(self, name: str, world: int, slots: int, create: bool):
+        self.shape = (world, 2, slots)
+        nbytes = 8 * world * 2 * slots
+        if create:
+            try:
+                old = shared_memory.SharedMemory(name=name)
+                old.close()
+                old.unlink()
+            except FileNotFoundError:
+                pass
+            self.shm = shared_memory.SharedMemory(name=name, create=True, size=nbytes)
+            np.ndarray(self.shape, dtype=np.int64, buffer=self.shm.buf)[:] = 0
+        else:
+            self.shm = shared_memory.SharedMemory(name=name)
+        self.arr = np.ndarray(self.shape, dtype=np.int64, buffer=self.shm.buf)
+        self.owner = create
+
+    def post(self, rank, direction, slot, seq):
+        self.arr[rank, direction, slot] = seq
+
+    def wait(self, rank, direction, slot, seq, timeout=600.0):
+        a = self.arr
+        if a[rank, direction, slot] >= seq:
+            return
+        t0 = time.monotonic()
+        while a[rank, direction, slot] < seq:
+            if time.monotonic() - t0 > timeout:
+                raise TimeoutError(f"p2p handshake timed out (peer {rank}, dir {direction}, "
+                                   f"slot {slot}, seq {seq})")
+            time.sleep(20e-6)
+
+    def close(self):
+        self.shm.close()
+        if self.owner:
+            try:
+                self.shm.unlink()
+            except FileNotFoundError:
+                pass
+
+
+class _Links:
+    """IPC-registered activation / gradient rings between adjacent stages of
+    one replica. Ring slot j holds micro-batch j of the current mini-batch;
+    a slot is rewritten only in the next mini-batch, after its consumer B(j)
+    has completed (guaranteed by the schedule's dependency chain)."""
+
+    ACT, GRAD = 0, 1
+
+    def __init__(self, rank, stage, P, n_micro, slot_elems, gloo_group, shm):
+        self.rank, self.stage, self.P, self.N = rank, stage, P, n_micro
+        self.slot_bytes = slot_elems * 2
+        self.shm = shm
+        self.rx = {}       # direction -> DeviceBuffer (local ring I receive into)
+        self.tx_events = {}  # direction -> [event handles I record]
+        mine = {"rank": rank}
+        if stage > 0:      # receive activations, send gradients upstream
+            buf = K.DeviceBuffer(n_micro * self.slot_bytes)
+            self.rx[self.ACT] = buf
+            mine["act_ring"] = self._mem_handle(buf.ptr)
+            self.tx_events[self.GRAD], mine["grad_events"] = self._events(n_micro)
+        if stage < P - 1:  # receive gradients, send activations downstream
+            buf = K.DeviceBuffer(n_micro * self.slot_bytes)
+            self.rx[self.GRAD] = buf
+            mine["grad_ring"] = self._mem_handle(buf.ptr)
+            self.tx_events[self.ACT], mine["act_events"] = self._events(n_micro)
+        world = dist.get_world_size()
+        allinfo = [None] * world
+        dist.all_gather_object(allinfo, mine, group=gloo_group)
+        self.peer_ring = {}    # direction -> mapped peer base pointer I write into
+        self.rx_events = {}    # direction -> [opened peer events I wait on]
+        if stage > 0:
+            up = allinfo[rank - 1]
+            self.peer_ring[self.GRAD] = self._open_mem(up["grad_ring"])
+            self.rx_events[self.ACT] = [self._open_event(h) for h in up["act_events"]]
+        if stage < P - 1:
+            down = allinfo[rank + 1]
+            self.peer_ring[self.ACT] = self._open_mem(down["act_ring"])
+            self.rx_events[self.GRAD] = [self._open_event(h) for h in down["grad_events"]]
+
+    @staticmethod
+    def _mem_handle(ptr):
+        h = ctypes.create_string_buffer(64)
+        check(K.L.vp_ipc_get_mem_handle(ptr, h), "vp_ipc_get_mem_handle")
+        return h.raw
+
+    @staticmethod
+    def _open_mem(handle):
+        p = ctypes.c_void_p()
+        check(K.L.vp_ipc_open_mem_handle(handle, ctypes.byref(p)), "vp_ipc_open_mem_handle")
+        return p.value
+
+    @staticmethod
+    def _events(n):
+        evs, hs = [], []
+        for _ in range(n):
+            e = ctypes.c_void_p()
+            h = ctypes.create_string_buffer(64)
+            check(K.L.vp_ipc_event_create(ctypes.byref(e), h), "vp_ipc_event_create")
+            evs.append(e.value)
+            hs.append(h.raw)
+        return evs, hs
+
+    @staticmethod
+    def _open_event(handle):
+        e = ctypes.c_void_p()
+        check(K.L.vp_ipc_event_open(handle, ctypes.byref(e)), "vp_ipc_event_open")
+        return e.value
+
+    def rx_slot(self, direction, j, shape):
+        return self.rx[direction].tensor(shape, torch.bfloat16, j * self.slot_bytes)
+
+    def peer_slot_ptr(self, direction, j):
+        return self.peer_ring[direction] + j * self.slot_bytes
+
+    def signal(self, direction, j, seq, stream):
+        """After the producing work on ``stream``: record the slot's IPC event,
+        then publish the sequence number to the receiver's host."""
+        check(K.L.vp_event_record(self.tx_events[direction][j], stream.cuda_stream),
+              "vp_event_record")
+        self.shm.post(self.rank, direction, j, seq)
+
+    def wait(self, direction, j, seq, stream):
+        peer = self.rank - 1 if direction == self.ACT else self.rank + 1
+        self.shm.wait(peer, direction, j, seq)
+        check(K.L.vp_stream_wait_event(stream.cuda_stream, self.rx_events[direction][j]),
+              "vp_stream_wait_event")
+
+
+class Varuna:
+    """Pipeline-parallel training of a GPT-2 described by ``model`` under the
+    ``config`` (P, D, m, N_m, stage_map) chosen by the reference planner."""
+
+    def __init__(self, model: GPT2Config, config: ParallelConfig, *,
+                 optimizer: AdamWConfig = AdamWConfig(), seed: int = 0, loss_scale: float = 1.0,
+                 device=None, init_device: str = "cpu", trace: bool = False):
+        if len(config.stage_map) != model.n_layer:
+            raise ConfigError(f"stage_map covers {len(config.stage_map)} cut-points, model has "
+                              f"{model.n_layer} (one CutPoint per transformer layer)")
+        P, D = config.pipeline_depth, config.data_parallel
+        self.cfg, self.pc, self.opt = model, config, optimizer
+        self.P, self.D = P, D
+        self.m, self.N = config.micro_batch_size, config.num_micro_batches
+        if dist.is_available() and dist.is_initialized():
+            self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        else:
+            self.rank, self.world = 0, 1
+        if self.world != P * D:
+            raise ConfigError(f"world size {self.world} != P*D = {P * D}")
+        self.stage_id, self.replica = self.rank % P, self.rank // P
+        layers = tuple(i for i, s in enumerate(config.stage_map) if s == self.stage_id)
+        if not layers:
+            raise ConfigError(f"stage {self.stage_id} owns no cut-points")
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        self.device = torch.device(device)
+        torch.cuda.set_device(self.device)
+        self.stream = torch.cuda.Stream(self.device)
+        self.spec = StageSpec(self.stage_id, P, layers)
+        self.stage = GPT2Stage(model, self.spec, self.m, self.device, seed, init_device)
+        self.schedule: Schedule = generate_varuna_schedule(P, self.N, 1.0, 2.0, 1.0)
+        kinds, mbs = self.schedule.stage_slice(self.stage_id)
+        self.tasks = list(zip(kinds.tolist(), mbs.tolist()))
+        self._check_plan()
+        self.loss_scale = loss_scale
+        self.step_count = 0
+        self.trace = trace
+        self.loss_sum = torch.zeros(1, device=self.device)
+        self.flags = torch.zeros(2, device=self.device)
+        self._setup_groups()
+        self.links = None
+        if P > 1:
+            slot_elems = self.m * model.seq_len * model.hidden
+            self.links = _Links(self.rank, self.stage_id, P, self.N, slot_elems,
+                                self.gloo, self.shm)
+        self.gpu_launches_per_step = None
+
+    # ---------------------------------------------------------------- setup
+    def _check_plan(self):
+        """The executor relies on rule 2 (R(j) directly before B(j)) and on the
+        last stage's F(j)/B(j) alternation (sp/scheduler.py:228-241)."""
+        last = self.spec.last
+        for i, (kind, j) in enumerate(self.tasks):
+            if kind == B:
+                prev = self.tasks[i - 1] if i else None
+                want = F if last else R
+                if prev != (want, j):
+                    raise ConfigError(f"stage {self.stage_id}: B{j + 1} not preceded by "
+                                      f"{'F' if last else 'R'}{j + 1}")
+
+    def _setup_groups(self):
+        P, D = self.P, self.D
+        self.dp_group = self.pipe_group = self.tie_group = None
+        self.gloo = None
+        self.shm = None
+        if self.world == 1:
+            return
+        for s in range(P):
+            g = dist.new_group([r * P + s for r in range(D)])
+            if s == self.stage_id:
+                self.dp_group = g
+        for r in range(D):
+            g = dist.new_group([r * P + s for s in range(P)])
+            if r == self.replica:
+                self.pipe_group = g
+        if P > 1:
+            for r in range(D):
+                g = dist.new_group([r * P, r * P + P - 1])
+                if r == self.replica and (self.spec.first or self.spec.last):
+                    self.tie_group = g
+        self.gloo = dist.new_group(list(range(self.world)), backend="gloo")
+        tag = os.environ.get("MASTER_PORT", "0")
+        name = f"vpipe_{tag}_{os.getuid()}"
+        if self.rank == 0:
+            self.shm = _Shm(name, self.world, self.N, create=True)
+        dist.barrier(group=self.gloo)
+        if self.rank != 0:
+            self.shm = _Shm(name, self.world, self.N, create=False)
+        dist.barrier(group=self.gloo)
+
+    # ----------------------------------------------------------------- data
+    def _device_batch(self, batch):
+        """Micro-batch views of this replica's rows; a partial last
+        micro-batch is padded with ignored labels (M_total semantics,
+        sp/planner.py:99-103). Host tensors are copied H2D here."""
+        ids = batch.get("input_ids") if self.spec.first else None
+        labels = batch.get("labels") if self.spec.last else None
+        rows = self.N * self.m
+        out = {}
+        for key, t, fill in (("ids", ids, 0), ("labels", labels, -100)):
+            if t is None:
+                continue
+            if t.shape[0] < rows:
+                pad = torch.full((rows - t.shape[0], t.shape[1]), fill, dtype=torch.int64,
+                                 device=t.device)
+                t = torch.cat([t, pad], 0)
+            if t.device != self.device:
+                t = t.to(self.device, non_blocking=True)
+            out[key] = t.view(self.N, self.m * self.cfg.seq_len)
+        return out
+
+    # ----------------------------------------------------------------- step
+    def step(self, batch: Dict[str, torch.Tensor], apply: bool = True) -> StepResult:
+        """One mini-batch: N_m micro-batches through this stage's task list,
+        then gradient synchronisation and the optimizer update."""
+        self.step_count += 1
+        seq_no = self.step_count
+        st = self.stream
+        cfg, stage = self.cfg, self.stage
+        total_tokens = self.pc.micro_batch_size * self.N * self.D * cfg.seq_len
+        scale = self.loss_scale / total_tokens
+        ev = [] if self.trace else None
+        st.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(st):
+            data = self._device_batch(batch)
+            if self.spec.last:
+                self.loss_sum.zero_()
+            t_start = self._mark(ev)
+            x_in = {}
+            for kind, j in self.tasks:
+                dseed = (self.step_count * 1000003 + j) & 0x7FFFFFFF
+                ids = data["ids"][j] if self.spec.first else None
+                e0 = self._mark(ev)
+                if kind == F or kind == R:
+                    if not self.spec.first and j not in x_in:
+                        self.links.wait(_Links.ACT, j, seq_no, st)
+                        x_in[j] = self.links.rx_slot(_Links.ACT, j, (stage.T, cfg.hidden))
+                    save = kind == R or self.spec.last
+                    out_ptr = None
+                    if kind == F and not self.spec.last:
+                        out_ptr = self.links.peer_slot_ptr(_Links.ACT, j)
+                    stage.forward(x_in.get(j), ids, save=save, dseed=dseed, stream=st,
+                                  out_ptr=out_ptr)
+                    if out_ptr is not None:
+                        self.links.signal(_Links.ACT, j, seq_no, st)
+                else:
+                    if self.spec.last:
+                        stage.loss_and_head_backward(data["labels"][j], scale, self.loss_sum,
+                                                     stream=st)
+                        g_in = None
+                    else:
+                        self.links.wait(_Links.GRAD, j, seq_no, st)
+                        g_in = self.links.rx_slot(_Links.GRAD, j, (stage.T, cfg.hidden))
+                    g = stage.backward(g_in, ids, dseed=dseed, stream=st)
+                    if not self.spec.first:
+                        K.p2p_put(self.links.peer_slot_ptr(_Links.GRAD, j), g, stream=st)
+                        self.links.signal(_Links.GRAD, j, seq_no, st)
+                    x_in.pop(j, None)
+                if ev is not None:
+                    ev.append((kind, j, e0, self._mark(ev)))
+            t_ar0 = self._mark(ev)
+            self._sync_grads()
+            t_ar1 = self._mark(ev)
+            if apply:
+                self._optimizer_step()
+            t_end = self._mark(ev)
+        timeline = None
+        if ev is not None:
+            st.synchronize()
+            timeline = self._timeline(t_start, ev, t_ar0, t_ar1, t_end)
+        loss = self.loss_sum if self.spec.last else None
+        return StepResult(loss, self.flags, 1.0 / self.loss_scale, timeline)
+
+    def _mark(self, ev):
+        if ev is None:
+            return None
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(self.stream)
+        return e
+
+    def _timeline(self, t0, ev, ar0, ar1, t_end):
+        tasks = [(k, j, t0.elapsed_time(a) * 1e3, t0.elapsed_time(b) * 1e3) for k, j, a, b in ev]
+        busy = sum(b - a for _, _, a, b in tasks)
+        return {"tasks": tasks, "allreduce_us": (t0.elapsed_time(ar0) * 1e3,
+                                                 t0.elapsed_time(ar1) * 1e3),
+                "step_us": t0.elapsed_time(t_end) * 1e3, "busy_us": busy}
+
+    # --------------------------------------------------- gradients + update
+    def _tied_segment(self):
+        P = self.stage.params
+        if self.P == 1:
+            return None
+        name = "wte" if self.spec.first else ("wte_head" if self.spec.last else None)
+        if name is None:
+            return None
+        return P.segment([name])
+
+    def _sync_grads(self):
+        P = self.stage.params
+        if self.D > 1:
+            dist.all_reduce(P.grad, group=self.dp_group)                       # C1
+            if self.spec.last:
+                dist.all_reduce(self.loss_sum, group=self.dp_group)
+        seg = self._tied_segment()
+        if seg is not None:
+            dist.all_reduce(P.grad[seg[0]:seg[1]], group=self.tie_group)       # C3
+        self.flags.zero_()
+        n_unique = P.numel
+        if self.spec.last and not self.spec.first:
+            n_unique = P.offsets["wte_head"]   # the tied copy is counted on stage 0
+        K.grad_norm_sq(P.grad[:n_unique], self.flags, stream=self.stream)
+        if self.P > 1:
+            dist.all_reduce(self.flags, group=self.pipe_group)                 # C2
+
+    def _optimizer_step(self):
+        P, o = self.stage.params, self.opt
+        K.adam_step(P.master, P.weight, P.grad, P.exp_avg, P.exp_avg_sq, self.flags, o.lr,
+                    o.betas[0], o.betas[1], o.eps, o.weight_decay, 1.0 / self.loss_scale,
+                    o.max_grad_norm, self.step_count, stream=self.stream)
+
+    # ------------------------------------------------------------- inspection
+    def param_tensors(self, which: str = "master") -> Dict[str, torch.Tensor]:
+        """Named fp32 views (``master``/``grad``) or bf16 ``weight`` views of
+        this stage's parameters, keyed like the CPU oracle."""
+        P = self.stage.params
+        buf = {"master": P.master, "grad": P.grad, "weight": P.weight}[which]
+        return {n: P.view(buf, n) for n in P.names}
+
+    def close(self):
+        if self.shm is not None:
+            self.shm.close()

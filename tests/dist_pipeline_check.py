@@ -1,0 +1,65 @@
+"""torchrun helper: run one Varuna mini-batch on P*D GPUs and compare each
+rank's gradients / the loss with the fp32 CPU oracle (tiny GPT-2)."""
+
+import argparse
+import os
+import sys
+
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--P", type=int, default=2)
+    ap.add_argument("--D", type=int, default=1)
+    ap.add_argument("--N", type=int, default=4)
+    args = ap.parse_args()
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2111_04007_b200 import ParallelConfig, assign_stages, make_block_model, uniform_profile
+    from paper_2111_04007_b200.model import CONFIGS
+    from paper_2111_04007_b200.runtime import Varuna, synthetic_batch
+    from oracle.gpt2_fp32 import PipelineOracle
+    cfg = CONFIGS["tiny"]
+    P, D, N, m = args.P, args.D, args.N, 4
+    model = make_block_model("tiny", cfg.n_layer, cfg.hidden, cfg.seq_len)
+    a = assign_stages(model, P, m, uniform_profile(cfg.n_layer, 1.0, 2.0, m_grid=(m,)))
+    pc = ParallelConfig(P, D, m, N, a.stage_map)
+    v = Varuna(cfg, pc, seed=0)
+    batches = [synthetic_batch(cfg, m * N, r) for r in range(D)]
+    res = v.step(batches[v.replica], apply=False)
+    torch.cuda.synchronize()
+    # oracle: D replicas' mini-batches, summed gradients
+    o = PipelineOracle(cfg.n_layer, cfg.hidden, cfg.heads, cfg.vocab_size, cfg.seq_len,
+                       pc.stage_map, m, N, seed=0)
+    total = m * N * D * cfg.seq_len
+    loss = sum(o.run_minibatch(b["input_ids"], b["labels"], total) for b in batches)
+    og = o.grads()
+    ok = True
+    for name, g in v.param_tensors("grad").items():
+        key = "wte" if name == "wte_head" else name
+        ref = og[key]
+        err = ((g.float().cpu() - ref).norm() / ref.norm().clamp_min(1e-12)).item()
+        if err > 3e-2:
+            print(f"rank {v.rank} {name}: rel err {err:.3e}", flush=True)
+            ok = False
+    if v.spec.last:
+        lerr = abs(res.loss - loss) / abs(loss)
+        print(f"rank {v.rank} loss {res.loss:.6f} oracle {loss:.6f} rel {lerr:.2e}", flush=True)
+        ok = ok and lerr < 5e-3
+    flag = torch.tensor([0 if ok else 1], device="cuda")
+    dist.all_reduce(flag)
+    v.close()
+    if dist.get_rank() == 0:
+        print("PARITY OK" if flag.item() == 0 else "PARITY FAIL", flush=True)
+    dist.destroy_process_group()
+    sys.exit(0 if flag.item() == 0 else 1)
+
+
+if __name__ == "__main__":
+    main()

@@ -125,7 +125,9 @@ def test_xent(rows, V):
     ref.sum().div(n_valid).backward()
     loss = torch.empty(rows, device="cuda")
     work = logits.clone()
-    K.xent_fwd_bwd(work, labels, loss, 1.0 / n_valid)
+    lsum = torch.zeros(1, device="cuda")
+    K.xent_fwd_bwd(work, labels, loss, 1.0 / n_valid, lsum)
+    assert abs(lsum.item() - ref.sum().item() / n_valid) < 1e-3 * abs(ref.sum().item() / n_valid)
     assert rel(loss, ref) < 1e-3
     assert rel(work, lg.grad) < 1e-2
 
