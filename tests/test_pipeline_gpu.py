@@ -57,15 +57,25 @@ def test_single_gpu_loss_grads_and_update():
         key = name
         assert key in og, name
         assert rel(g, og[key]) < 3e-2, (name, rel(g, og[key]))
-    # optimizer: apply on both sides
-    v.step_count -= 1
+    # optimizer: apply on both sides. Adam's first update is ~lr*sign(g), so
+    # compare the UPDATE direction (cosine >= 0.9 over entries whose oracle
+    # gradient is >= 5% of the tensor's RMS gradient — entries with ~zero
+    # true gradient, e.g. the key bias, get a noise-sign update) and the weights (rel L2 <= 1e-2 where non-zero).
+    before = {k: t.clone() for k, t in v.param_tensors("master").items()}
+    ref_before = {k: p.detach().clone() for k, p in o.params.items()}
     v._optimizer_step()
     o.adamw_step(1)
     torch.cuda.synchronize()
-    w = v.param_tensors("master")
-    for name, t in w.items():
+    for name, t in v.param_tensors("master").items():
         ref = o.params[name].detach()
-        assert rel(t, ref) < 1e-2, name
+        d_gpu = (t - before[name]).float().cpu().flatten()
+        d_ref = (ref - ref_before[name]).flatten()
+        gref = og[name].flatten().abs()
+        keep = gref >= 0.05 * gref.pow(2).mean().sqrt()  # drop ~zero-gradient entries
+        cos = torch.nn.functional.cosine_similarity(d_gpu[keep], d_ref[keep], dim=0).item()
+        assert cos > 0.9, (name, cos)
+        if ref_before[name].norm() > 0:
+            assert rel(t, ref) < 1e-2, name
 
 
 def test_recompute_is_bitwise_forward():
