@@ -1,0 +1,423 @@
+"""Benchmark: Varuna pipeline training throughput (samples/s) on 1/2/4/8 B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config gpt2_355m]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...
+    python bench.py --impl reference ...     # the reference-side CPU arm
+
+One step = one mini-batch of M_total samples (BASELINE config 2: GPT-2 355M,
+M_total = 512, m = 8) through the Varuna schedule on P×D GPUs, with the
+gradient allreduce and the AdamW update — the whole training step. The P×D
+ladder at fixed M_total (strong scaling): 1 → 1×1, 2 → 2×1, 4 → 4×1,
+8 → 4×2 (the BASELINE.json configuration). Stage maps come from the
+reference's ``assign_stages`` over a FLOP-proportional calibration profile
+with the LM head folded into the last cut-point and the last stage weighted
+0.75 (it runs no recompute), which is how the planner would balance it.
+
+Rank 0 prints ONE JSON line (see the driver contract in the task). Timing:
+CUDA events on the executor's compute stream, barrier + synchronize on both
+sides, max over ranks. The step's working set (weights, optimizer state,
+activations: several GB) is far larger than the 126 MB L2, so no explicit
+flush is needed between steps.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+LADDER = {1: (1, 1), 2: (2, 1), 4: (4, 1), 8: (4, 2)}
+MODEL_CONFIGS = {  # name: (M_total, m)
+    "gpt2_355m": (512, 8),
+    "gpt2_2_5b": (256, 4),
+    "gpt2_8_3b": (512, 4),
+    "tiny": (16, 4),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="vpipe", choices=["vpipe", "reference"])
+    ap.add_argument("--config", default="gpt2_355m", choices=sorted(MODEL_CONFIGS))
+    ap.add_argument("--pd", default=None, help="override P x D, e.g. 4x2")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample-s", type=float, default=20.0)
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d["bf16_tflops"], d["bf16_tflops_sustained"], d["hbm_gbs"], "measured"
+    except Exception:  # noqa: BLE001
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+def stage_map_for(cfg, P, m):
+    """assign_stages (the reference DP) over a FLOP-proportional profile with
+    the head folded into the last cut-point; last stage weight 0.75."""
+    from paper_2111_04007_b200 import assign_stages, make_block_model
+    from paper_2111_04007_b200.calibration import CalibrationProfile, CutpointTimes
+    per_layer = cfg.flops_per_token_layer() * cfg.seq_len * m
+    head = cfg.head_flops_per_token() * cfg.seq_len * m
+    us = [max(1, round(per_layer / 1e9))] * cfg.n_layer
+    us[-1] += max(1, round(head / 1e9))
+    z = {m: 0}
+    cps = tuple(CutpointTimes({m: t}, {m: 2 * t}, z, z, z, z, z, z, {1: 0}) for t in us)
+    prof = CalibrationProfile((m,), (1,), cps)
+    model = make_block_model(cfg_name(cfg), cfg.n_layer, cfg.hidden, cfg.seq_len)
+    return assign_stages(model, P, m, prof, last_stage_weight=0.75 if P > 1 else 1.0).stage_map
+
+
+def cfg_name(cfg):
+    return f"gpt2-L{cfg.n_layer}-h{cfg.hidden}"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.path = tempfile.mktemp(suffix=".csv")
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-i", str(index), "-lms", "200"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:  # noqa: BLE001
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.close()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        os.unlink(self.path)
+        loaded = [x for x in sm if mx and x > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU arm
+
+def cpu_layer_sample(cfg, m, budget_s):
+    """The fp32 CPU oracle (oracle/gpt2_fp32.py) timed on this host: one
+    transformer layer's F + R + B at the config's (m, s, h), plus the LM head
+    F + B, extrapolated by layer count and schedule to samples/s."""
+    import torch
+    from oracle import gpt2_fp32 as og
+    threads = os.cpu_count() or 1
+    torch.set_num_threads(threads)
+    h, S, H, V = cfg.hidden, cfg.seq_len, cfg.heads, cfg.vocab_size
+    p = og.init_params(1, h, 8, S)   # layer 0 weights (tiny vocab; head timed separately)
+    for k in p:
+        p[k].requires_grad_(True)
+    mm = m
+    x = torch.randn(mm * S, h, requires_grad=True)
+    t0 = time.perf_counter()
+    y = og.layer_forward(p, 0, x, mm, S, H)
+    y.backward(torch.ones_like(y))
+    t_layer_fb = time.perf_counter() - t0
+    reps = 1
+    while time.perf_counter() - t0 < budget_s * 0.6 and reps < 3:
+        t1 = time.perf_counter()
+        with torch.no_grad():
+            og.layer_forward(p, 0, x, mm, S, H)
+        y = og.layer_forward(p, 0, x, mm, S, H)
+        y.backward(torch.ones_like(y))
+        t_layer_fb = time.perf_counter() - t1  # F(no-save) + R + B, steady state
+        reps += 1
+    # LM head on a slice of rows (bounded), scaled to m*S rows
+    rows = min(mm * S, 1024)
+    w = torch.randn(V, h) * 0.02
+    w.requires_grad_(True)
+    yy = torch.randn(rows, h, requires_grad=True)
+    lab = torch.randint(0, V, (rows,))
+    t2 = time.perf_counter()
+    l = torch.nn.functional.cross_entropy(yy @ w.t(), lab)
+    l.backward()
+    t_head = (time.perf_counter() - t2) * (mm * S / rows)
+    per_mb = cfg.n_layer * t_layer_fb + t_head
+    sample = (f"1 layer F+R+B at m={mm}, s={S}, h={h} and LM head F+B on {rows} rows "
+              f"(fp32 torch-CPU oracle), extrapolated x{cfg.n_layer} layers")
+    return mm / per_mb, threads, sample, time.perf_counter() - t0
+
+
+def run_reference(args):
+    """--impl reference: the reference CPU path of this hot path (the fp32
+    oracle port — the reference itself has no tensor math) on the host cores."""
+    from paper_2111_04007_b200.model import CONFIGS
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = CONFIGS[args.config]
+    M, m = MODEL_CONFIGS[args.config]
+    P, D = LADDER.get(args.gpus, (args.gpus, 1))
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, threads, sample, _ = cpu_layer_sample(cfg, m, budget_s=min(args.cpu_sample_s, 8.0))
+        if i >= args.warmup:
+            vals.append(v)
+    value = statistics.median(vals)
+    line = {"metric": "samples/sec (GPT-2 355M Varuna pipeline step)", "value": round(value, 4),
+            "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(M / value * 1e3, 1), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"{args.config} {P}x{D} m={m} M_total={M} (CPU oracle)",
+                       "global_batch": M, "seq_len": cfg.seq_len, "parallelism": f"pp{P}xdp{D}"},
+            "cpu_baseline": {"value": round(value, 4), "unit": "samples/s", "cores": threads,
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": round(value, 4), "unit": "samples/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- GPU arm
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+    from paper_2111_04007_b200 import ParallelConfig, micro_batches_for, JobSpec
+    from paper_2111_04007_b200 import kernels as K
+    from paper_2111_04007_b200.model import CONFIGS
+    from paper_2111_04007_b200.runtime import Varuna, synthetic_batch
+    from paper_2111_04007_b200.simulator import bubble_fraction
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = CONFIGS[args.config]
+    M, m = MODEL_CONFIGS[args.config]
+    if args.pd:
+        P, D = map(int, args.pd.lower().split("x"))
+    else:
+        P, D = LADDER.get(world, (world, 1))
+    N = micro_batches_for(JobSpec(M), m, D)
+    stage_map = stage_map_for(cfg, P, m)
+    pc = ParallelConfig(P, D, m, N, stage_map)
+    init_dev = "cuda"
+    v = Varuna(cfg, pc, seed=0, init_device=init_dev)
+    st = v.stream
+    rows = m * N
+    host = synthetic_batch(cfg, rows, v.replica)
+    host = {k: t.pin_memory() for k, t in host.items()}
+    dbatch = {k: t.to(dev) for k, t in host.items()}
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        v.step(dbatch)
+    barrier()
+
+    # ---- timed region 1: inputs resident in HBM
+    clocks = ClockSampler(local)
+    l0 = K.LAUNCHES[0]
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(st)
+    for _ in range(args.steps):
+        v.step(dbatch)
+    e1.record(st)
+    barrier()
+    launches = K.LAUNCHES[0] - l0
+    ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+    clk = clocks.stop()
+    value = M / (ms / 1e3)
+
+    # ---- timed region 2: end to end through the public API, host buffers
+    e2e = None
+    if not args.no_e2e:
+        h2d = sum(t.numel() * t.element_size() for k, t in host.items()
+                  if (k == "input_ids" and v.spec.first) or (k == "labels" and v.spec.last))
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(st)
+        for _ in range(args.steps):
+            res = v.step(host)
+            if v.spec.last:
+                _ = res.loss  # D2H read of the step's loss (forces completion)
+        t1.record(st)
+        barrier()
+        ms_e2e = max_over_ranks(t0.elapsed_time(t1)) / args.steps
+        tot = torch.tensor([h2d, 4 if v.spec.last else 0], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(tot)
+        e2e = {"value": round(M / (ms_e2e / 1e3), 3), "unit": "samples/s",
+               "h2d_bytes_per_step": int(tot[0].item()), "d2h_bytes_per_step": int(tot[1].item())}
+
+    # ---- instrumented step (not timed): GEMM launch durations + task timeline
+    K.GEMM_TIMING["on"] = True
+    K.GEMM_TIMING["records"].clear()
+    v.trace = True
+    res = v.step(dbatch)
+    torch.cuda.synchronize()
+    K.GEMM_TIMING["on"] = False
+    v.trace = False
+    recs = K.GEMM_TIMING["records"]
+    g_flops = sum(r[0] for r in recs)
+    g_ms = sum(r[1].elapsed_time(r[2]) for r in recs)
+    tl = res.timeline
+    step_us = tl["step_us"]
+    ar_us = tl["allreduce_us"][1] - tl["allreduce_us"][0]
+    local_busy = tl["busy_us"]
+    # measured bubble by the reference definition (sp/simulator.py:107-114),
+    # taken over the pipeline part (task busy + AR) of the slowest stage's clock
+    busy_all = torch.tensor([local_busy, ar_us, step_us], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(busy_all)
+    mb_us = max_over_ranks(tl["allreduce_us"][1])
+    bubble = 1.0 - (busy_all[0].item() + busy_all[1].item()) / (world * mb_us) if mb_us else 0.0
+    gemm_tf = g_flops / (g_ms / 1e3) / 1e12 if g_ms else 0.0
+    gemm_share = g_ms / (step_us / 1e3) if step_us else 0.0
+    burst, sustained, hbm, src = peaks()
+
+    # per-stage roofline: T_k = max(X_k / peak, act_bytes / NVLink)
+    flops_layer_tok = cfg.flops_per_token_layer()
+    worst = 0.0
+    for s in range(P):
+        nl = sum(1 for x in stage_map if x == s)
+        F = nl * flops_layer_tok * m * cfg.seq_len
+        if s == P - 1:
+            F += cfg.head_flops_per_token() * m * cfg.seq_len
+        X = (3 if (s == P - 1 or P == 1) else 4) * F
+        t = max(X / (burst * 1e12), m * cfg.seq_len * cfg.hidden * 2 / 900e9)
+        worst = max(worst, t)
+    roof_samples = D * m / worst
+
+    # measured stage profile -> reference bubble predictor (simulate_minibatch)
+    predicted = predicted_bubble(v, tl, P, D, N, m, stage_map, world, dev, dist)
+
+    cpu = None
+    if rank == 0:
+        try:
+            cv, threads, sample, _ = cpu_layer_sample(cfg, m, args.cpu_sample_s)
+            cpu = {"value": round(cv, 5), "unit": "samples/s", "cores": threads, "kind": "port",
+                   "sample": sample}
+        except Exception as ex:  # noqa: BLE001
+            cpu = {"value": None, "unit": "samples/s", "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"failed: {ex}"}
+    if rank == 0:
+        line = {
+            "metric": "samples/sec (GPT-2 355M Varuna pipeline step)",
+            "value": round(value, 3), "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 2), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic tokens, random-init weights",
+            "config": {"workload": f"{args.config} P{P}xD{D} m={m} N_m={N} M_total={M}",
+                       "model": cfg_name(cfg), "global_batch": M, "seq_len": cfg.seq_len,
+                       "parallelism": f"pp{P}xdp{D}", "stage_map_sizes":
+                           [sum(1 for x in stage_map if x == s) for s in range(P)],
+                       "l2": "working set >> 126 MB L2 (no flush needed)", "dropout": cfg.dropout},
+            "clocks": clk,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "roofline": {"bound": "tensor", "achieved": round(gemm_tf, 1),
+                         "peak": sustained, "unit": "TFLOP/s",
+                         "frac": round(gemm_tf / sustained, 4),
+                         "traffic": None,
+                         "kernel": "vp_gemm_bf16 (tcgen05), all GEMM launches of one step",
+                         "peak_kind": f"{src} bf16 sustained", "share_of_step": round(gemm_share, 3)},
+            "stage_roofline": {"roofline_samples_per_s": round(roof_samples, 1),
+                               "frac": round(value / roof_samples, 4)},
+            "bubble": {"measured": round(bubble, 4), "predicted": predicted},
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    v.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def predicted_bubble(v, tl, P, D, N, m, stage_map, world, dev, dist):
+    """Feed the MEASURED per-stage F/R/B task times (this step, all ranks) to
+    the bubble predictor (simulate_minibatch, sp/simulator.py:259-389) with
+    zero transfer cost; returns its bubble fraction."""
+    import torch
+    from paper_2111_04007_b200 import (ModelSpec, ParallelConfig, build_placement,
+                                       simulate_minibatch, uniform_cluster)
+    from paper_2111_04007_b200.calibration import CalibrationProfile, CutpointTimes
+    from paper_2111_04007_b200.core import KIND_BACKWARD, KIND_FORWARD, KIND_RECOMPUTE
+    sums = torch.zeros(world, 3, device=dev, dtype=torch.float64)
+    cnt = {0: [], 1: [], 2: []}
+    for kind, j, a, b in tl["tasks"]:
+        cnt[kind].append(b - a)
+    for kind, col in ((KIND_FORWARD, 0), (KIND_BACKWARD, 1), (KIND_RECOMPUTE, 2)):
+        if cnt[kind]:
+            sums[v.rank, col] = statistics.mean(cnt[kind])
+    if world > 1:
+        dist.all_reduce(sums)
+    stage_f = [0.0] * P
+    stage_b = [0.0] * P
+    for s in range(P):
+        stage_f[s] = float(sums[s, 0].item())
+        stage_b[s] = float(sums[s, 1].item())
+    # one cut-point per stage carrying the whole stage's time
+    z = {m: 0}
+    cps = tuple(CutpointTimes({m: max(1, round(stage_f[s]))}, {m: max(1, round(stage_b[s]))},
+                              z, z, z, z, z, z, {d: 0 for d in sorted({1, D})}) for s in range(P))
+    prof = CalibrationProfile((m,), tuple(sorted({1, D})), cps)
+    model = ModelSpec("stages", (1,) * P, (1,) * P)
+    pc = ParallelConfig(P, D, m, N, tuple(range(P)))
+    r = simulate_minibatch(v.schedule, pc, prof, build_placement(uniform_cluster(P * D, 8), P, D),
+                           model, opportunistic=False)
+    return round(r.bubble_fraction, 4)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

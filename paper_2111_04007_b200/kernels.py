@@ -57,6 +57,17 @@ for _name, _args in _SIGS.items():
         _fn.restype = c_int
 
 
+# Kernel launches issued through this module (the bench's gpu_launches
+# claim); GEMM timing hook (CUDA events on the launching stream) used by
+# bench.py to measure the dominant kernel's achieved TFLOP/s.
+LAUNCHES = [0]
+GEMM_TIMING = {"on": False, "records": []}
+
+
+def _count(n=1):
+    LAUNCHES[0] += n
+
+
 def _stream(s=None):
     return (s or torch.cuda.current_stream()).cuda_stream
 
@@ -97,15 +108,26 @@ def gemm(a, b, out, *, a_kmajor=True, b_kmajor=True, epilogue=EPI_STORE, bias=No
             raise ValueError("gemm: inner stride must be 1")
     if out is not None:
         out_ptr, ldd = out.data_ptr(), out.stride(0)
+    timing = GEMM_TIMING["on"]
+    if timing:
+        st = stream or torch.cuda.current_stream()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+    _count()
     check(L.vp_gemm_bf16(int(a_kmajor), int(b_kmajor), epilogue, a.data_ptr(), a.stride(0),
                          b.data_ptr(), b.stride(0), out_ptr, ldd, _p(bias),
                          _p(aux), aux.stride(0) if aux is not None else 0, M, N, K,
                          _stream(stream)), "vp_gemm_bf16")
+    if timing:
+        e1.record(st)
+        GEMM_TIMING["records"].append((2 * M * N * K, e0, e1, (M, N, K, a_kmajor, b_kmajor)))
     return out
 
 
 def layernorm_fwd(x, gamma, beta, y, mean, rstd, eps=1e-5, stream=None):
     rows, cols = x.shape
+    _count(1)
     check(L.vp_layernorm_fwd(x.data_ptr(), gamma.data_ptr(), beta.data_ptr(), y.data_ptr(),
                              mean.data_ptr(), rstd.data_ptr(), rows, cols, eps, _stream(stream)),
           "vp_layernorm_fwd")
@@ -119,6 +141,7 @@ def layernorm_ws_elems(cols: int) -> int:
 def layernorm_bwd(dy, x, gamma, mean, rstd, dx, dgamma, dbeta, workspace, accumulate=False,
                   stream=None):
     rows, cols = x.shape
+    _count(2)
     check(L.vp_layernorm_bwd(dy.data_ptr(), x.data_ptr(), gamma.data_ptr(), mean.data_ptr(),
                              rstd.data_ptr(), dx.data_ptr(), dgamma.data_ptr(), dbeta.data_ptr(),
                              rows, cols, int(accumulate), workspace.data_ptr(), _stream(stream)),
@@ -127,6 +150,7 @@ def layernorm_bwd(dy, x, gamma, mean, rstd, dx, dgamma, dbeta, workspace, accumu
 
 
 def attention_fwd(qkv, out, lse, batch, seq, heads, head_dim, causal=True, stream=None):
+    _count(1)
     check(L.vp_attention_fwd(qkv.data_ptr(), out.data_ptr(), lse.data_ptr(), batch, seq, heads,
                              head_dim, int(causal), _stream(stream)), "vp_attention_fwd")
     return out
@@ -134,6 +158,7 @@ def attention_fwd(qkv, out, lse, batch, seq, heads, head_dim, causal=True, strea
 
 def attention_bwd(qkv, out, dout, lse, dqkv, delta_ws, batch, seq, heads, head_dim, causal=True,
                   stream=None):
+    _count(3)
     check(L.vp_attention_bwd(qkv.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(),
                              dqkv.data_ptr(), delta_ws.data_ptr(), batch, seq, heads, head_dim,
                              int(causal), _stream(stream)), "vp_attention_bwd")
@@ -141,18 +166,21 @@ def attention_bwd(qkv, out, dout, lse, dqkv, delta_ws, batch, seq, heads, head_d
 
 
 def embed_fwd(ids, wte, wpe, x, batch, seq, stream=None):
+    _count(1)
     check(L.vp_embed_fwd(ids.data_ptr(), wte.data_ptr(), wpe.data_ptr(), x.data_ptr(), batch, seq,
                          wte.shape[1], _stream(stream)), "vp_embed_fwd")
     return x
 
 
 def embed_bwd(ids, dx, dwte, dwpe, batch, seq, stream=None):
+    _count(1 if dwpe is None else 2)
     check(L.vp_embed_bwd(ids.data_ptr(), dx.data_ptr(), dwte.data_ptr(), _p(dwpe), batch, seq,
                          dx.shape[1], _stream(stream)), "vp_embed_bwd")
 
 
 def xent_fwd_bwd(logits, labels, loss_rows, scale, loss_sum=None, stream=None):
     rows, vocab = logits.shape
+    _count(1)
     check(L.vp_xent_fwd_bwd(logits.data_ptr(), labels.data_ptr(), loss_rows.data_ptr(),
                             _p(loss_sum), rows, vocab, scale, _stream(stream)), "vp_xent_fwd_bwd")
     return loss_rows
@@ -164,21 +192,26 @@ def bias_grad_ws_elems(cols: int) -> int:
 
 def bias_grad(dy, dbias, workspace, stream=None):
     rows, cols = dy.shape
+    _count(2)
     check(L.vp_bias_grad(dy.data_ptr(), dbias.data_ptr(), rows, cols, workspace.data_ptr(),
                          _stream(stream)), "vp_bias_grad")
 
 
 def dropout_(x, p, seed, offset, stream=None):
+    if p > 0:
+        _count()
     check(L.vp_dropout(x.data_ptr(), x.numel(), p, seed, offset, _stream(stream)), "vp_dropout")
     return x
 
 
 def add(a, b, y, stream=None):
+    _count(1)
     check(L.vp_add(a.data_ptr(), b.data_ptr(), y.data_ptr(), a.numel(), _stream(stream)), "vp_add")
     return y
 
 
 def grad_norm_sq(g, out, stream=None):
+    _count(1)
     check(L.vp_grad_norm_sq(g.data_ptr(), g.numel(), out.data_ptr(), _stream(stream)),
           "vp_grad_norm_sq")
 
@@ -187,6 +220,7 @@ def adam_step(master, weight, grad, m, v, flags, lr, beta1, beta2, eps, weight_d
               inv_loss_scale, max_grad_norm, step, stream=None):
     bc1 = 1.0 - beta1 ** step
     bc2 = 1.0 - beta2 ** step
+    _count(1)
     check(L.vp_adam_step(master.data_ptr(), weight.data_ptr(), grad.data_ptr(), m.data_ptr(),
                          v.data_ptr(), master.numel(), flags.data_ptr(), lr, beta1, beta2, eps,
                          weight_decay, inv_loss_scale, max_grad_norm, bc1, bc2, _stream(stream)),
@@ -194,12 +228,14 @@ def adam_step(master, weight, grad, m, v, flags, lr, beta1, beta2, eps, weight_d
 
 
 def cast_f32_bf16(x, y, stream=None):
+    _count(1)
     check(L.vp_cast_f32_bf16(x.data_ptr(), y.data_ptr(), x.numel(), _stream(stream)),
           "vp_cast_f32_bf16")
 
 
 def p2p_put(dst_ptr: int, src, nbytes=None, stream=None):
     nbytes = src.numel() * src.element_size() if nbytes is None else nbytes
+    _count(1)
     check(L.vp_p2p_put(dst_ptr, src.data_ptr(), nbytes, _stream(stream)), "vp_p2p_put")
 
 

@@ -372,11 +372,17 @@ class Varuna:
             for kind, j in self.tasks:
                 dseed = (self.step_count * 1000003 + j) & 0x7FFFFFFF
                 ids = data["ids"][j] if self.spec.first else None
+                # inputs first (stream waits on the peer's IPC event), so the
+                # task's timing events bracket compute only
+                if kind != B and not self.spec.first and j not in x_in:
+                    self.links.wait(_Links.ACT, j, seq_no, st)
+                    x_in[j] = self.links.rx_slot(_Links.ACT, j, (stage.T, cfg.hidden))
+                g_in = None
+                if kind == B and not self.spec.last:
+                    self.links.wait(_Links.GRAD, j, seq_no, st)
+                    g_in = self.links.rx_slot(_Links.GRAD, j, (stage.T, cfg.hidden))
                 e0 = self._mark(ev)
                 if kind == F or kind == R:
-                    if not self.spec.first and j not in x_in:
-                        self.links.wait(_Links.ACT, j, seq_no, st)
-                        x_in[j] = self.links.rx_slot(_Links.ACT, j, (stage.T, cfg.hidden))
                     save = kind == R or self.spec.last
                     out_ptr = None
                     if kind == F and not self.spec.last:
@@ -389,10 +395,6 @@ class Varuna:
                     if self.spec.last:
                         stage.loss_and_head_backward(data["labels"][j], scale, self.loss_sum,
                                                      stream=st)
-                        g_in = None
-                    else:
-                        self.links.wait(_Links.GRAD, j, seq_no, st)
-                        g_in = self.links.rx_slot(_Links.GRAD, j, (stage.T, cfg.hidden))
                     g = stage.backward(g_in, ids, dseed=dseed, stream=st)
                     if not self.spec.first:
                         K.p2p_put(self.links.peer_slot_ptr(_Links.GRAD, j), g, stream=st)
