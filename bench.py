@@ -131,7 +131,7 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- CPU arm
 
-def cpu_layer_sample(cfg, m, budget_s):
+def cpu_layer_sample(cfg, m, budget_s, recompute=False):
     """The fp32 CPU oracle (oracle/gpt2_fp32.py) timed on this host: one
     transformer layer's F + R + B at the config's (m, s, h), plus the LM head
     F + B, extrapolated by layer count and schedule to samples/s."""
@@ -152,11 +152,12 @@ def cpu_layer_sample(cfg, m, budget_s):
     reps = 1
     while time.perf_counter() - t0 < budget_s * 0.6 and reps < 3:
         t1 = time.perf_counter()
-        with torch.no_grad():
-            og.layer_forward(p, 0, x, mm, S, H)
+        if recompute:
+            with torch.no_grad():
+                og.layer_forward(p, 0, x, mm, S, H)
         y = og.layer_forward(p, 0, x, mm, S, H)
         y.backward(torch.ones_like(y))
-        t_layer_fb = time.perf_counter() - t1  # F(no-save) + R + B, steady state
+        t_layer_fb = time.perf_counter() - t1  # [F(no-save) +] F/R + B, steady state
         reps += 1
     # LM head on a slice of rows (bounded), scaled to m*S rows
     rows = min(mm * S, 1024)
@@ -169,7 +170,7 @@ def cpu_layer_sample(cfg, m, budget_s):
     l.backward()
     t_head = (time.perf_counter() - t2) * (mm * S / rows)
     per_mb = cfg.n_layer * t_layer_fb + t_head
-    sample = (f"1 layer F+R+B at m={mm}, s={S}, h={h} and LM head F+B on {rows} rows "
+    sample = (f"1 layer F{'+R' if recompute else ''}+B at m={mm}, s={S}, h={h} and LM head F+B on {rows} rows "
               f"(fp32 torch-CPU oracle), extrapolated x{cfg.n_layer} layers")
     return mm / per_mb, threads, sample, time.perf_counter() - t0
 
@@ -186,7 +187,8 @@ def run_reference(args):
     P, D = LADDER.get(args.gpus, (args.gpus, 1))
     vals = []
     for i in range(args.warmup + args.steps):
-        v, threads, sample, _ = cpu_layer_sample(cfg, m, budget_s=min(args.cpu_sample_s, 8.0))
+        v, threads, sample, _ = cpu_layer_sample(cfg, m, budget_s=min(args.cpu_sample_s, 8.0),
+                                                 recompute=P > 1)
         if i >= args.warmup:
             vals.append(v)
     value = statistics.median(vals)
@@ -345,7 +347,7 @@ def main():
     cpu = None
     if rank == 0:
         try:
-            cv, threads, sample, _ = cpu_layer_sample(cfg, m, args.cpu_sample_s)
+            cv, threads, sample, _ = cpu_layer_sample(cfg, m, args.cpu_sample_s, recompute=P > 1)
             cpu = {"value": round(cv, 5), "unit": "samples/s", "cores": threads, "kind": "port",
                    "sample": sample}
         except Exception as ex:  # noqa: BLE001
