@@ -131,24 +131,54 @@ __global__ void __launch_bounds__(THREADS)
 }
 
 // ---------------------------------------------------------------- bias grad
-__global__ void colsum_partial(const __nv_bfloat16* __restrict__ dy, float* __restrict__ ws,
-                               int64_t rows, int64_t cols, int64_t rows_per_part) {
-  // grid: (ceil(cols/256), parts)
-  const int64_t c = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
-  if (c >= cols) return;
+// Block = 32 column-groups (8 bf16 columns each, one 16-byte load) x 8
+// row-lanes; blockIdx.y = row chunk. Fixed-order reductions (deterministic).
+__global__ void __launch_bounds__(256) colsum_partial(const __nv_bfloat16* __restrict__ dy,
+                                                      float* __restrict__ ws, int64_t rows,
+                                                      int64_t cols, int64_t rows_per_part) {
+  __shared__ float sh[8][32 * 8 + 4];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t c0 = (static_cast<int64_t>(blockIdx.x) * 32 + tx) * 8;
   const int64_t r0 = blockIdx.y * rows_per_part;
   const int64_t r1 = min(rows, r0 + rows_per_part);
-  float acc = 0.f;
-  for (int64_t r = r0; r < r1; ++r) acc += __bfloat162float(dy[r * cols + c]);
-  ws[blockIdx.y * cols + c] = acc;
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (c0 < cols) {
+    for (int64_t r = r0 + ty; r < r1; r += 8) {
+      float f[8];
+      unpack8(*reinterpret_cast<const uint4*>(dy + r * cols + c0), f);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += f[j];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) sh[ty][tx * 8 + j] = acc[j];
+  __syncthreads();
+  const int64_t cb = static_cast<int64_t>(blockIdx.x) * 256;
+  for (int i = threadIdx.x; i < 256; i += 256) {
+    if (cb + i >= cols) break;
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += sh[k][i];
+    ws[blockIdx.y * cols + cb + i] = t;
+  }
 }
-__global__ void colsum_final(const float* __restrict__ ws, float* __restrict__ out, int parts,
-                             int64_t cols) {
-  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (c >= cols) return;
+__global__ void __launch_bounds__(256) colsum_final(const float* __restrict__ ws,
+                                                    float* __restrict__ out, int parts,
+                                                    int64_t cols) {
+  __shared__ float sh[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * 32 + tx;
   float acc = 0.f;
-  for (int p = 0; p < parts; ++p) acc += ws[p * cols + c];
-  out[c] += acc;
+  if (c < cols)
+    for (int p = ty; p < parts; p += 8) acc += ws[p * cols + c];
+  sh[ty][tx] = acc;
+  __syncthreads();
+  if (ty == 0 && c < cols) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += sh[i][tx];
+    out[c] += t;
+  }
 }
 
 // ------------------------------------------------------------ dropout / add
@@ -311,11 +341,15 @@ extern "C" int vp_xent_fwd_bwd(void* logits, const int64_t* labels, float* loss_
 extern "C" int vp_bias_grad(const void* dy, float* dbias, int64_t rows, int64_t cols,
                             float* workspace, void* stream) {
   if (rows <= 0 || cols <= 0 || !workspace) return VP_ERR_ARGS;
-  const int parts = static_cast<int>(std::min<int64_t>(64, rows));
+  if (cols % 8) return VP_ERR_UNSUPPORTED;
+  const int64_t col_blocks = (cols + 255) / 256;
+  // ~4 waves of 148 SMs worth of blocks
+  int parts = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(64, 592 / col_blocks)));
+  parts = static_cast<int>(std::min<int64_t>(parts, rows));
   const int64_t rpp = (rows + parts - 1) / parts;
-  dim3 grid(blocks_for(cols, 256), parts);
+  dim3 grid(static_cast<unsigned>(col_blocks), parts);
   colsum_partial<<<grid, 256, 0, ST>>>(CBF(dy), workspace, rows, cols, rpp);
-  colsum_final<<<blocks_for(cols, 256), 256, 0, ST>>>(workspace, dbias, parts, cols);
+  colsum_final<<<blocks_for(cols, 32), 256, 0, ST>>>(workspace, dbias, parts, cols);
   return launch_status();
 }
 

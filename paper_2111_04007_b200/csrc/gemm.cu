@@ -16,6 +16,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 namespace vp {
@@ -428,7 +429,8 @@ extern "C" int vp_gemm_bf16(int a_kmajor, int b_kmajor, int epilogue, const void
     const int64_t waves = (tiles + sms - 1) / sms;
     return double(waves * sms) * bn / double(tiles * bn);  // slots per useful tile
   };
-  const int BNsel = (N <= 128 || waste(128) * 0.92 < waste(256)) ? 128 : 256;
+  int BNsel = (N <= 128 || waste(128) * 0.92 < waste(256)) ? 128 : 256;
+  if (const char* f = getenv("VP_GEMM_BN")) BNsel = atoi(f) == 256 ? 256 : 128;
   CUtensorMap ta, tb;
   bool ok = a_mn ? make_tmap(&ta, A, M, K, lda, 64, BK) : make_tmap(&ta, A, K, M, lda, BK, BM);
   ok = ok && (b_mn ? make_tmap(&tb, B, N, K, ldb, 64, BK)

@@ -79,7 +79,9 @@ __global__ void __launch_bounds__(kWarps * 32)
                   const float* __restrict__ rstd, __nv_bfloat16* __restrict__ dx,
                   float* __restrict__ ws, int64_t rows, int cols, int accumulate,
                   int rows_per_cta) {
-  extern __shared__ float red[];  // [kWarps][2][cols]
+  // [kWarps][2][8][nvec]: element j of vector c at [j * nvec + c] so the 32
+  // lanes of a warp (consecutive c) hit consecutive banks.
+  extern __shared__ float red[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nvec = cols >> 3;
   float* mine = red + warp * 2 * cols;
@@ -101,16 +103,14 @@ __global__ void __launch_bounds__(kWarps * 32)
         unpack8(xr[c], xv);
         unpack8(dyr[c], dv);
         unpack8(gv[c], gg);
-        float* dgp = mine + c * 8;
-        float* dbp = mine + cols + c * 8;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const float xh = (xv[j] - mu) * rs;
           const float gy = dv[j] * gg[j];
           s1 += gy;
           s2 += gy * xh;
-          dgp[j] += dv[j] * xh;
-          dbp[j] += dv[j];
+          mine[j * nvec + c] += dv[j] * xh;
+          mine[cols + j * nvec + c] += dv[j];
         }
       }
     }
@@ -137,22 +137,37 @@ __global__ void __launch_bounds__(kWarps * 32)
     }
   }
   __syncthreads();
-  for (int c = threadIdx.x; c < 2 * cols; c += blockDim.x) {
+  // ws[part][2*cols] in natural column order
+  for (int i = threadIdx.x; i < 2 * cols; i += blockDim.x) {
+    const int half = i / cols, col = i % cols;
+    const int src = half * cols + (col & 7) * nvec + (col >> 3);
     float acc = 0.f;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) acc += red[w * 2 * cols + c];
-    ws[static_cast<int64_t>(blockIdx.x) * 2 * cols + c] = acc;
+    for (int w = 0; w < kWarps; ++w) acc += red[w * 2 * cols + src];
+    ws[static_cast<int64_t>(blockIdx.x) * 2 * cols + i] = acc;
   }
 }
 
-__global__ void ln_param_reduce(const float* __restrict__ ws, float* __restrict__ dgamma,
-                                float* __restrict__ dbeta, int parts, int cols) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= 2 * cols) return;
+// 32 columns x 8 part-lanes per block; fixed-order tree => deterministic.
+__global__ void __launch_bounds__(256) ln_param_reduce(const float* __restrict__ ws,
+                                                       float* __restrict__ dgamma,
+                                                       float* __restrict__ dbeta, int parts,
+                                                       int cols) {
+  __shared__ float sh[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + tx;
   float acc = 0.f;
-  for (int p = 0; p < parts; ++p) acc += ws[static_cast<int64_t>(p) * 2 * cols + c];
-  if (c < cols) dgamma[c] += acc;
-  else dbeta[c - cols] += acc;
+  if (c < 2 * cols)
+    for (int p = ty; p < parts; p += 8) acc += ws[static_cast<int64_t>(p) * 2 * cols + c];
+  sh[ty][tx] = acc;
+  __syncthreads();
+  if (ty == 0 && c < 2 * cols) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += sh[i][tx];
+    if (c < cols) dgamma[c] += t;
+    else dbeta[c - cols] += t;
+  }
 }
 
 }  // namespace
@@ -226,7 +241,7 @@ extern "C" int vp_layernorm_bwd(const void* dy, const void* x, const void* gamma
         rpc);
   });
   const int c2 = static_cast<int>(2 * cols);
-  ln_param_reduce<<<(c2 + 255) / 256, 256, 0, st>>>(workspace, dgamma, dbeta, parts,
-                                                    static_cast<int>(cols));
+  ln_param_reduce<<<(c2 + 31) / 32, 256, 0, st>>>(workspace, dgamma, dbeta, parts,
+                                                  static_cast<int>(cols));
   return launch_status();
 }

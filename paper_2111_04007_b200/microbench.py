@@ -49,6 +49,12 @@ def bench(M, N, Kd, layout="nt", epi=K.EPI_STORE, iters=20):
             "tflops": round(tf, 1), "cublas_tflops": round(2 * M * N * Kd / ct / 1e9, 1)}
 
 
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "one":
+    # python microbench.py one M N K layout epi
+    M, N, Kd = map(int, sys.argv[2:5])
+    print(json.dumps(bench(M, N, Kd, sys.argv[5], int(sys.argv[6]), iters=5)), flush=True)
+    sys.exit(0)
+
 if __name__ == "__main__":
     shapes = [
         (8192, 3072, 1024, "nt"), (8192, 1024, 1024, "nt"), (8192, 4096, 1024, "nt"),

@@ -125,6 +125,11 @@ class _Shm:
             np.ndarray(self.shape, dtype=np.int64, buffer=self.shm.buf)[:] = 0
         else:
             self.shm = shared_memory.SharedMemory(name=name)
+            try:  # the creator owns unlinking; keep the tracker out of it
+                from multiprocessing import resource_tracker
+                resource_tracker.unregister(self.shm._name, "shared_memory")
+            except Exception:  # noqa: BLE001
+                pass
         self.arr = np.ndarray(self.shape, dtype=np.int64, buffer=self.shm.buf)
         self.owner = create
 
