@@ -429,7 +429,10 @@ extern "C" int vp_gemm_bf16(int a_kmajor, int b_kmajor, int epilogue, const void
     const int64_t waves = (tiles + sms - 1) / sms;
     return double(waves * sms) * bn / double(tiles * bn);  // slots per useful tile
   };
-  int BNsel = (N <= 128 || waste(128) * 0.92 < waste(256)) ? 128 : 256;
+  // BN=256 halves the B-operand smem/L2 traffic per FLOP and measures
+  // faster on every BASELINE shape; 128 only when N itself is small.
+  (void)waste;
+  int BNsel = N <= 128 ? 128 : 256;
   if (const char* f = getenv("VP_GEMM_BN")) BNsel = atoi(f) == 256 ? 256 : 128;
   CUtensorMap ta, tb;
   bool ok = a_mn ? make_tmap(&ta, A, M, K, lda, 64, BK) : make_tmap(&ta, A, K, M, lda, BK, BM);
