@@ -116,6 +116,14 @@ int vp_device_sm_count(int* out);
 int vp_gemm_bf16(int a_kmajor, int b_kmajor, int epilogue, const void* A, int64_t lda,
                  const void* B, int64_t ldb, void* D, int64_t ldd, const void* bias, void* aux,
                  int64_t ldaux, int64_t M, int64_t N, int64_t K, void* stream);
+/* Same, with flags: VP_GEMM_DIRECT_STORE writes D with per-thread stores
+ * from the epilogue (use when D is an NVLink peer-mapped pointer — the fused
+ * "FC2 epilogue -> next stage's ring slot" send). The default path is the
+ * 2-CTA (cta_group::2) kernel with TMA-store / TMA-reduce-add epilogues. */
+#define VP_GEMM_DIRECT_STORE 1
+int vp_gemm_bf16_ex(int a_kmajor, int b_kmajor, int epilogue, const void* A, int64_t lda,
+                    const void* B, int64_t ldb, void* D, int64_t ldd, const void* bias, void* aux,
+                    int64_t ldaux, int64_t M, int64_t N, int64_t K, int flags, void* stream);
 
 /* LayerNorm over rows of x[rows, cols] (bf16 in/out, fp32 stats saved). */
 int vp_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean,

@@ -305,6 +305,331 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ===========================================================================
+// 2-CTA variant (the default path): a cluster of two SMs computes a 256x256
+// tile with tcgen05.mma.cta_group::2 (UMMA 256x256x16). Each CTA loads its
+// 128 rows of A and its 128-column half of B (halving per-SM operand
+// traffic), the leader CTA issues the MMAs, and each CTA drains its 128-row
+// half of the accumulator from its own TMEM. The epilogue stages each
+// warp's 32-row sub-tile in 128B-swizzled smem and writes it with TMA
+// (bulk store, or bulk reduce-add for fp32 gradient accumulation), so global
+// writes are full-line and asynchronous. Split-K (weight gradients with a
+// small output and long K) is only used with the reduce-add epilogue.
+// ===========================================================================
+constexpr int kStages2 = 5;
+constexpr int kStageBytes2 = 2 * 128 * BK * 2;        // A half + B half per CTA = 32 KB
+constexpr int kStagingPerWarp = 8192;                  // 2 x 4 KB epilogue buffers
+constexpr int kSmem2 = kStages2 * kStageBytes2 + 4 * kStagingPerWarp + 256 + 1024;
+
+struct Epi2 {
+  const __nv_bfloat16* bias;
+  const __nv_bfloat16* aux_in;  // RESID / DGELU operand
+  int64_t ldaux;
+};
+
+__device__ __forceinline__ void store_row_swizzled(uint8_t* buf, uint32_t row,
+                                                   const uint4 (&chunks)[8]) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    *reinterpret_cast<uint4*>(buf + row * 128 + ((k ^ (row & 7)) << 4)) = chunks[k];
+}
+
+template <int EPI>
+__device__ __forceinline__ void epi2_apply(const Epi2& e, int64_t row, int64_t col0, int64_t M,
+                                           int64_t N, float (&v)[64], float (&pre)[64]) {
+  // bias (columns col0..col0+63), guarded for the ragged right edge
+  if constexpr (EPI == VP_EPI_BIAS || EPI == VP_EPI_BIAS_GELU || EPI == VP_EPI_BIAS_RESID) {
+    if (col0 + 64 <= N) {
+#pragma unroll
+      for (int i = 0; i < 64; i += 8) {
+        float b[8];
+        unpack8(*reinterpret_cast<const uint4*>(e.bias + col0 + i), b);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[i + j] += b[j];
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 64; ++i)
+        if (col0 + i < N) v[i] += __bfloat162float(e.bias[col0 + i]);
+    }
+  }
+  if constexpr (EPI == VP_EPI_BIAS_GELU) {
+#pragma unroll
+    for (int i = 0; i < 64; ++i) {
+      pre[i] = __bfloat162float(__float2bfloat16(v[i]));
+      v[i] = gelu_tanh(pre[i]);
+    }
+  }
+  if constexpr (EPI == VP_EPI_BIAS_RESID || EPI == VP_EPI_DGELU) {
+    if (row < M) {
+      const __nv_bfloat16* a = e.aux_in + row * e.ldaux + col0;
+      if (col0 + 64 <= N) {
+#pragma unroll
+        for (int i = 0; i < 64; i += 8) {
+          float x[8];
+          unpack8(*reinterpret_cast<const uint4*>(a + i), x);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if constexpr (EPI == VP_EPI_BIAS_RESID) v[i + j] += x[j];
+            else v[i + j] *= gelu_tanh_grad(x[j]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          if (col0 + i < N) {
+            const float x = __bfloat162float(a[i]);
+            if constexpr (EPI == VP_EPI_BIAS_RESID) v[i] += x;
+            else v[i] *= gelu_tanh_grad(x);
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int EPI, bool A_MN, bool B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX,
+                 int64_t M, int64_t N, int64_t K, int split_k, Epi2 epi) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* staging = smem + kStages2 * kStageBytes2;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(staging + 4 * kStagingPerWarp);
+  uint64_t* empty_bar = full_bar + kStages2;
+  uint64_t* tfull_bar = empty_bar + kStages2;  // [2]
+  uint64_t* tempty_bar = tfull_bar + 2;        // [2] (leader's are used)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  constexpr bool kF32Out = (EPI == VP_EPI_ACC_F32 || EPI == VP_EPI_STORE_F32);
+  const uint32_t warp = warp_id();
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int64_t tiles_m = (M + 255) / 256;
+  const int64_t tiles_n = (N + 255) / 256;
+  const int64_t n_tiles = tiles_m * tiles_n;
+  const int64_t n_kb = (K + BK - 1) / BK;
+  const int64_t kb_per = (n_kb + split_k - 1) / split_k;
+  const int64_t n_units = n_tiles * split_k;
+  const int64_t cid = blockIdx.x >> 1;
+  const int64_t n_clusters = gridDim.x >> 1;
+
+  if (warp == 0 && lane_id() == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    tma_prefetch(&tmD);
+    for (int s = 0; s < kStages2; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 8);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc_2sm(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto unit_coords = [&](int64_t u, int64_t& mb, int64_t& nb, int64_t& kb0, int64_t& kb1) {
+    const int64_t t = u / split_k, ks = u % split_k;
+    tile_coords(t, tiles_m, tiles_n, mb, nb);
+    kb0 = ks * kb_per;
+    kb1 = min(n_kb, kb0 + kb_per);
+  };
+
+  if (warp == 0) {
+    if (lane_id() == 0) {
+      // ===== TMA producer (both CTAs) =====
+      uint32_t stage = 0, phase = 0;
+      for (int64_t u = cid; u < n_units; u += n_clusters) {
+        int64_t mb, nb, kb0, kb1;
+        unit_coords(u, mb, nb, kb0, kb1);
+        const int32_t m0 = static_cast<int32_t>(mb * 256 + rank * 128);
+        const int32_t n0 = static_cast<int32_t>(nb * 256 + rank * 128);
+        for (int64_t kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * kStageBytes2;
+          uint8_t* sb = sa + 128 * BK * 2;
+          if (leader) mbar_expect_tx(&full_bar[stage], 2 * kStageBytes2);
+          const int32_t k0 = static_cast<int32_t>(kb * BK);
+          if constexpr (!A_MN) {
+            tma_load_2d_2sm(sa, &tmA, &full_bar[stage], k0, m0);
+          } else {
+            tma_load_2d_2sm(sa, &tmA, &full_bar[stage], m0, k0);
+            tma_load_2d_2sm(sa + 64 * BK * 2, &tmA, &full_bar[stage], m0 + 64, k0);
+          }
+          if constexpr (!B_MN) {
+            tma_load_2d_2sm(sb, &tmB, &full_bar[stage], k0, n0);
+          } else {
+            tma_load_2d_2sm(sb, &tmB, &full_bar[stage], n0, k0);
+            tma_load_2d_2sm(sb + 64 * BK * 2, &tmB, &full_bar[stage], n0 + 64, k0);
+          }
+          if (++stage == kStages2) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane_id() == 0) {
+      // ===== MMA issuer (leader CTA only) =====
+      constexpr uint32_t idesc = idesc_bf16(256, 256, A_MN, B_MN);
+      uint32_t stage = 0, phase = 0, local = 0;
+      for (int64_t u = cid; u < n_units; u += n_clusters, ++local) {
+        int64_t mb, nb, kb0, kb1;
+        unit_coords(u, mb, nb, kb0, kb1);
+        const uint32_t acc = local & 1;
+        mbar_wait(&tempty_bar[acc], ((local >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * 256;
+        for (int64_t kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * kStageBytes2);
+          const uint32_t sb = sa + 128 * BK * 2;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = A_MN ? sdesc_sw128(sa + k * 2048, 64 * BK * 2, 1024)
+                                     : sdesc_sw128(sa + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? sdesc_sw128(sb + k * 2048, 64 * BK * 2, 1024)
+                                     : sdesc_sw128(sb + k * 32, 16, 1024);
+            umma_f16_2sm(tmem_d, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          umma_commit_2sm(&empty_bar[stage], 0x3);
+          if (++stage == kStages2) { stage = 0; phase ^= 1; }
+        }
+        umma_commit_2sm(&tfull_bar[acc], 0x3);
+      }
+    }
+  } else if (warp >= 4) {
+    // ===== Epilogue (both CTAs): rows [rank*128 + q*32, +32) of the tile =====
+    const uint32_t q = warp & 3;
+    uint8_t* wbuf = staging + q * kStagingPerWarp;
+    uint32_t local = 0, nbuf = 0;
+    const uint32_t lane = lane_id();
+    for (int64_t u = cid; u < n_units; u += n_clusters, ++local) {
+      int64_t mb, nb, kb0, kb1;
+      unit_coords(u, mb, nb, kb0, kb1);
+      const uint32_t acc = local & 1;
+      mbar_wait(&tfull_bar[acc], (local >> 1) & 1);
+      tc_fence_after();
+      const int32_t row0 = static_cast<int32_t>(mb * 256 + rank * 128 + q * 32);
+      const int64_t row = row0 + lane;
+      const uint32_t taddr = tmem_base + ((q * 32) << 16) + acc * 256;
+      if constexpr (kF32Out) {
+#pragma unroll 1
+        for (int c = 0; c < 256; c += 32) {
+          const int32_t col0 = static_cast<int32_t>(nb * 256 + c);
+          if (col0 >= N) break;
+          uint32_t raw[32];
+          tmem_ld32(taddr + c, raw);
+          tmem_ld_wait();
+          uint8_t* buf = wbuf + (nbuf & 1) * 4096;
+          if (lane == 0) bulk_wait_read<1>();
+          __syncwarp();
+          uint4 ch[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            ch[k] = make_uint4(raw[4 * k], raw[4 * k + 1], raw[4 * k + 2], raw[4 * k + 3]);
+          store_row_swizzled(buf, lane, ch);
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (EPI == VP_EPI_ACC_F32) tma_reduce_add_2d(&tmD, buf, col0, row0);
+            else tma_store_2d(&tmD, buf, col0, row0);
+            bulk_commit();
+          }
+          ++nbuf;
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < 256; c += 64) {
+          const int32_t col0 = static_cast<int32_t>(nb * 256 + c);
+          if (col0 >= N) break;
+          float v[64], pre[64];
+          {
+            uint32_t raw[32];
+            tmem_ld32(taddr + c, raw);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(raw[i]);
+            tmem_ld32(taddr + c + 32, raw);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[32 + i] = __uint_as_float(raw[i]);
+          }
+          epi2_apply<EPI>(epi, row, col0, M, N, v, pre);
+          if constexpr (EPI == VP_EPI_BIAS_GELU) {
+            // pre-activation (aux) then activation (D): both buffers in turn
+            if (lane == 0) bulk_wait_read<0>();
+            __syncwarp();
+            uint4 ch[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              float f[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) f[j] = pre[8 * k + j];
+              ch[k] = pack8(f);
+            }
+            store_row_swizzled(wbuf, lane, ch);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              float f[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) f[j] = v[8 * k + j];
+              ch[k] = pack8(f);
+            }
+            store_row_swizzled(wbuf + 4096, lane, ch);
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmX, wbuf, col0, row0);
+              tma_store_2d(&tmD, wbuf + 4096, col0, row0);
+              bulk_commit();
+            }
+          } else {
+            uint8_t* buf = wbuf + (nbuf & 1) * 4096;
+            if (lane == 0) bulk_wait_read<1>();
+            __syncwarp();
+            uint4 ch[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              float f[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) f[j] = v[8 * k + j];
+              ch[k] = pack8(f);
+            }
+            store_row_swizzled(buf, lane, ch);
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmD, buf, col0, row0);
+              bulk_commit();
+            }
+            ++nbuf;
+          }
+        }
+      }
+      // accumulator drained: release it to the leader's MMA warp
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&tempty_bar[acc], 0);
+    }
+    if (lane == 0) bulk_wait_all();
+    __syncwarp();
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_2sm(tmem_base, 512);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Host side
 // ---------------------------------------------------------------------------
@@ -322,17 +647,19 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 2D bf16 tensor map: inner dim contiguous, rows `ld` elements apart.
+// 2D tensor map (bf16 or fp32): inner dim contiguous, rows `ld` elements apart.
 bool make_tmap(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
-               uint32_t box_inner, uint32_t box_outer) {
+               uint32_t box_inner, uint32_t box_outer, bool f32 = false) {
   auto fn = encode_fn();
   if (!fn) return false;
+  const uint64_t esz = f32 ? 4 : 2;
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {ld * 2};
+  cuuint64_t strides[1] = {ld * esz};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
-                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  CUresult r = fn(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                  2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -395,6 +722,52 @@ int dispatch_epi(int epi, bool a_mn, bool b_mn, const CUtensorMap& ta, const CUt
   }
 }
 
+
+template <int EPI, bool A_MN, bool B_MN>
+int launch2_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td,
+              const CUtensorMap& tx, int64_t M, int64_t N, int64_t K, int split_k,
+              const Epi2& e, cudaStream_t st) {
+  auto kern = gemm2_kernel<EPI, A_MN, B_MN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2);
+    if (err != cudaSuccess) return err;
+    attr_set = true;
+  }
+  const int64_t units = ((M + 255) / 256) * ((N + 255) / 256) * split_k;
+  const int64_t clusters = std::min<int64_t>(units, sm_count() / 2);
+  kern<<<static_cast<unsigned>(2 * clusters), kThreads, kSmem2, st>>>(ta, tb, td, tx, M, N, K,
+                                                                       split_k, e);
+  return cudaGetLastError();
+}
+
+template <int EPI>
+int dispatch2_layout(bool a_mn, bool b_mn, const CUtensorMap& ta, const CUtensorMap& tb,
+                     const CUtensorMap& td, const CUtensorMap& tx, int64_t M, int64_t N, int64_t K,
+                     int split_k, const Epi2& e, cudaStream_t st) {
+  if (!a_mn && !b_mn) return launch2_t<EPI, false, false>(ta, tb, td, tx, M, N, K, split_k, e, st);
+  if (!a_mn && b_mn) return launch2_t<EPI, false, true>(ta, tb, td, tx, M, N, K, split_k, e, st);
+  if (a_mn && !b_mn) return launch2_t<EPI, true, false>(ta, tb, td, tx, M, N, K, split_k, e, st);
+  return launch2_t<EPI, true, true>(ta, tb, td, tx, M, N, K, split_k, e, st);
+}
+
+int gemm2_dispatch(int epi, bool a_mn, bool b_mn, const CUtensorMap& ta, const CUtensorMap& tb,
+                   const CUtensorMap& td, const CUtensorMap& tx, int64_t M, int64_t N, int64_t K,
+                   int split_k, const Epi2& e, cudaStream_t st) {
+#define D2(E) return dispatch2_layout<E>(a_mn, b_mn, ta, tb, td, tx, M, N, K, split_k, e, st)
+  switch (epi) {
+    case VP_EPI_STORE: D2(VP_EPI_STORE);
+    case VP_EPI_BIAS: D2(VP_EPI_BIAS);
+    case VP_EPI_BIAS_GELU: D2(VP_EPI_BIAS_GELU);
+    case VP_EPI_BIAS_RESID: D2(VP_EPI_BIAS_RESID);
+    case VP_EPI_DGELU: D2(VP_EPI_DGELU);
+    case VP_EPI_ACC_F32: D2(VP_EPI_ACC_F32);
+    case VP_EPI_STORE_F32: D2(VP_EPI_STORE_F32);
+    default: return VP_ERR_ARGS;
+  }
+#undef D2
+}
+
 }  // namespace
 }  // namespace vp
 
@@ -404,13 +777,12 @@ extern "C" int vp_device_sm_count(int* out) {
   return VP_OK;
 }
 
-extern "C" int vp_gemm_bf16(int a_kmajor, int b_kmajor, int epilogue, const void* A, int64_t lda,
-                            const void* B, int64_t ldb, void* D, int64_t ldd, const void* bias,
-                            void* aux, int64_t ldaux, int64_t M, int64_t N, int64_t K,
-                            void* stream) {
+static int gemm_entry(int a_kmajor, int b_kmajor, int epilogue, const void* A, int64_t lda,
+                      const void* B, int64_t ldb, void* D, int64_t ldd, const void* bias,
+                      void* aux, int64_t ldaux, int64_t M, int64_t N, int64_t K, int flags,
+                      void* stream) {
   using namespace vp;
   if (M <= 0 || N <= 0 || K <= 0 || !A || !B || !D) return VP_ERR_ARGS;
-  // TMA: 16-byte aligned bases and row strides.
   if ((lda % 8) || (ldb % 8) || (ldd % 8)) return VP_ERR_UNSUPPORTED;
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) |
        reinterpret_cast<uintptr_t>(D)) & 15)
@@ -421,19 +793,35 @@ extern "C" int vp_gemm_bf16(int a_kmajor, int b_kmajor, int epilogue, const void
   if ((epilogue == VP_EPI_BIAS_RESID || epilogue == VP_EPI_DGELU) && !aux) return VP_ERR_ARGS;
   if (aux && (ldaux % 8)) return VP_ERR_UNSUPPORTED;
   const bool a_mn = !a_kmajor, b_mn = !b_kmajor;
-  // Choose BN: 256 unless that leaves the last wave badly filled.
-  const int64_t tm = (M + BM - 1) / BM;
-  const int sms = sm_count();
-  auto waste = [&](int64_t bn) {
-    const int64_t tiles = tm * ((N + bn - 1) / bn);
-    const int64_t waves = (tiles + sms - 1) / sms;
-    return double(waves * sms) * bn / double(tiles * bn);  // slots per useful tile
-  };
-  // BN=256 halves the B-operand smem/L2 traffic per FLOP and measures
-  // faster on every BASELINE shape; 128 only when N itself is small.
-  (void)waste;
-  int BNsel = N <= 128 ? 128 : 256;
-  if (const char* f = getenv("VP_GEMM_BN")) BNsel = atoi(f) == 256 ? 256 : 128;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bool f32_out = epilogue == VP_EPI_ACC_F32 || epilogue == VP_EPI_STORE_F32;
+  const bool use2 = !(flags & VP_GEMM_DIRECT_STORE) && !getenv("VP_GEMM_1SM") &&
+                    !(epilogue == VP_EPI_BIAS_GELU && !aux) && (ldd % (f32_out ? 4 : 8)) == 0;
+  if (use2) {
+    CUtensorMap ta, tb, td, tx;
+    bool ok = a_mn ? make_tmap(&ta, A, M, K, lda, 64, BK) : make_tmap(&ta, A, K, M, lda, BK, 128);
+    ok = ok && (b_mn ? make_tmap(&tb, B, N, K, ldb, 64, BK) : make_tmap(&tb, B, K, N, ldb, BK, 128));
+    ok = ok && (f32_out ? make_tmap(&td, D, N, M, ldd, 32, 32, true)
+                        : make_tmap(&td, D, N, M, ldd, 64, 32));
+    if (epilogue == VP_EPI_BIAS_GELU) ok = ok && make_tmap(&tx, aux, N, M, ldaux, 64, 32);
+    else tx = td;
+    if (!ok) return VP_ERR_UNSUPPORTED;
+    // Split K only when the reduce-add epilogue makes it exact-by-construction
+    // per split and the output tiles cannot fill the clusters.
+    int split = 1;
+    const int64_t tiles = ((M + 255) / 256) * ((N + 255) / 256);
+    const int64_t clusters = sm_count() / 2;
+    if (epilogue == VP_EPI_ACC_F32 && tiles < clusters) {
+      const int64_t n_kb = (K + BK - 1) / BK;
+      split = static_cast<int>(std::min<int64_t>((clusters + tiles - 1) / tiles, n_kb / 8));
+      if (split < 1) split = 1;
+      if (const char* f = getenv("VP_GEMM_SPLITK")) split = std::max(1, atoi(f));
+    }
+    Epi2 e{reinterpret_cast<const __nv_bfloat16*>(bias), reinterpret_cast<const __nv_bfloat16*>(aux),
+           ldaux};
+    return gemm2_dispatch(epilogue, a_mn, b_mn, ta, tb, td, tx, M, N, K, split, e, st);
+  }
+  const int BNsel = N <= 128 ? 128 : 256;
   CUtensorMap ta, tb;
   bool ok = a_mn ? make_tmap(&ta, A, M, K, lda, 64, BK) : make_tmap(&ta, A, K, M, lda, BK, BM);
   ok = ok && (b_mn ? make_tmap(&tb, B, N, K, ldb, 64, BK)
@@ -441,7 +829,22 @@ extern "C" int vp_gemm_bf16(int a_kmajor, int b_kmajor, int epilogue, const void
   if (!ok) return VP_ERR_UNSUPPORTED;
   EpiArgs e{D, ldd, reinterpret_cast<const __nv_bfloat16*>(bias),
             reinterpret_cast<__nv_bfloat16*>(aux), ldaux};
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (BNsel == 256) return dispatch_epi<256>(epilogue, a_mn, b_mn, ta, tb, M, N, K, e, st);
   return dispatch_epi<128>(epilogue, a_mn, b_mn, ta, tb, M, N, K, e, st);
+}
+
+extern "C" int vp_gemm_bf16(int a_kmajor, int b_kmajor, int epilogue, const void* A, int64_t lda,
+                            const void* B, int64_t ldb, void* D, int64_t ldd, const void* bias,
+                            void* aux, int64_t ldaux, int64_t M, int64_t N, int64_t K,
+                            void* stream) {
+  return gemm_entry(a_kmajor, b_kmajor, epilogue, A, lda, B, ldb, D, ldd, bias, aux, ldaux, M, N,
+                    K, 0, stream);
+}
+
+extern "C" int vp_gemm_bf16_ex(int a_kmajor, int b_kmajor, int epilogue, const void* A,
+                               int64_t lda, const void* B, int64_t ldb, void* D, int64_t ldd,
+                               const void* bias, void* aux, int64_t ldaux, int64_t M, int64_t N,
+                               int64_t K, int flags, void* stream) {
+  return gemm_entry(a_kmajor, b_kmajor, epilogue, A, lda, B, ldb, D, ldd, bias, aux, ldaux, M, N,
+                    K, flags, stream);
 }

@@ -24,6 +24,8 @@ EPI_STORE, EPI_BIAS, EPI_BIAS_GELU, EPI_BIAS_RESID, EPI_DGELU, EPI_ACC_F32, EPI_
 _SIGS = {
     "vp_device_sm_count": [ctypes.POINTER(c_int)],
     "vp_gemm_bf16": [c_int, c_int, c_int, vp, i64, vp, i64, vp, i64, vp, vp, i64, i64, i64, i64, vp],
+    "vp_gemm_bf16_ex": [c_int, c_int, c_int, vp, i64, vp, i64, vp, i64, vp, vp, i64, i64, i64, i64,
+                        c_int, vp],
     "vp_layernorm_fwd": [vp, vp, vp, vp, vp, vp, i64, i64, f32, vp],
     "vp_layernorm_bwd": [vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, c_int, vp, vp],
     "vp_attention_fwd": [vp, vp, vp, i64, i64, i64, i64, c_int, vp],
@@ -90,7 +92,7 @@ def sm_count() -> int:
 
 
 def gemm(a, b, out, *, a_kmajor=True, b_kmajor=True, epilogue=EPI_STORE, bias=None, aux=None,
-         M=None, N=None, K=None, stream=None, out_ptr=None, ldd=None):
+         M=None, N=None, K=None, stream=None, out_ptr=None, ldd=None, direct=False):
     """out[M,N] = epi(op(a) @ op(b)^T) where op(a) is [M,K] (a_kmajor: a is
     [M,K], else a is [K,M]) and op(b) is [N,K] (b_kmajor: b is [N,K], else
     [K,N]). All operands bf16 row-major with unit inner stride; out is bf16
@@ -115,10 +117,10 @@ def gemm(a, b, out, *, a_kmajor=True, b_kmajor=True, epilogue=EPI_STORE, bias=No
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(st)
     _count()
-    check(L.vp_gemm_bf16(int(a_kmajor), int(b_kmajor), epilogue, a.data_ptr(), a.stride(0),
-                         b.data_ptr(), b.stride(0), out_ptr, ldd, _p(bias),
-                         _p(aux), aux.stride(0) if aux is not None else 0, M, N, K,
-                         _stream(stream)), "vp_gemm_bf16")
+    check(L.vp_gemm_bf16_ex(int(a_kmajor), int(b_kmajor), epilogue, a.data_ptr(), a.stride(0),
+                            b.data_ptr(), b.stride(0), out_ptr, ldd, _p(bias),
+                            _p(aux), aux.stride(0) if aux is not None else 0, M, N, K,
+                            1 if direct else 0, _stream(stream)), "vp_gemm_bf16")
     if timing:
         e1.record(st)
         GEMM_TIMING["records"].append((2 * M * N * K, e0, e1, (M, N, K, a_kmajor, b_kmajor)))

@@ -279,7 +279,7 @@ class GPT2Stage:
         ld = self.cfg.hidden
         if self.cfg.dropout <= 0:
             K.gemm(a, wt, out_t, epilogue=K.EPI_BIAS_RESID, bias=b, aux=resid, stream=stream,
-                   out_ptr=out_ptr, ldd=ld)
+                   out_ptr=out_ptr, ldd=ld, direct=out_ptr is not None)
             return
         tmp = self.drop_tmp
         K.gemm(a, wt, tmp, epilogue=K.EPI_BIAS, bias=b, stream=stream)

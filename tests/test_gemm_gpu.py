@@ -86,6 +86,35 @@ def test_gemm_wgrad_shape():
     assert rel(dw, ref) < 1e-5
 
 
+@pytest.mark.parametrize("direct", [False, True])
+def test_gemm_paths_agree(direct):
+    # 2-CTA TMA-store path and the 1-SM direct-store path (peer-pointer
+    # writes) give the same numbers for every epilogue.
+    torch.manual_seed(4)
+    M, N, Kd = 640, 1152, 320
+    A = torch.randn(M, Kd, device="cuda").bfloat16()
+    B = (torch.randn(N, Kd, device="cuda") * 0.1).bfloat16()
+    bias = torch.randn(N, device="cuda").bfloat16()
+    res = torch.randn(M, N, device="cuda").bfloat16()
+    base = A.float() @ B.float().t()
+    out = res.clone()
+    K.gemm(A, B, out, epilogue=K.EPI_BIAS_RESID, bias=bias, aux=out, direct=direct)
+    assert rel(out, res.float() + base + bias.float()) < 5e-3
+
+
+@pytest.mark.parametrize("T,N,Kd", [(8192, 1024, 1024), (8192, 3072, 1024), (4096, 1920, 7680),
+                                    (1000, 520, 264)])
+def test_gemm_wgrad_splitk(T, N, Kd):
+    # small output, long reduction -> split-K with TMA reduce-add epilogue
+    torch.manual_seed(5)
+    dy = torch.randn(T, N, device="cuda").bfloat16()
+    x = torch.randn(T, Kd, device="cuda").bfloat16()
+    dw = torch.randn(N, Kd, device="cuda")
+    dw0 = dw.clone()
+    K.gemm(dy, x, dw, a_kmajor=False, b_kmajor=False, epilogue=K.EPI_ACC_F32)
+    assert rel(dw, dw0 + dy.float().t() @ x.float()) < 1e-5
+
+
 def test_gemm_deterministic():
     torch.manual_seed(3)
     A = torch.randn(2048, 1024, device="cuda").bfloat16()
