@@ -260,34 +260,65 @@ __global__ void norm_kernel(const float* __restrict__ g, int64_t n, float* __res
   }
 }
 
-__global__ void adam_kernel(float* __restrict__ master, __nv_bfloat16* __restrict__ w,
-                            float* __restrict__ grad, float* __restrict__ m, float* __restrict__ v,
-                            int64_t n, const float* __restrict__ flags, float lr, float b1,
-                            float b2, float eps, float wd, float inv_scale, float max_norm,
-                            float bc1, float bc2) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t base = i * 4;
-  if (base >= n) return;
+// One float4 of every state array per thread (coalesced 16-byte accesses);
+// ~34 B/param of HBM traffic: read master/grad/m/v, write master/m/v/grad
+// (zeroed) + the bf16 weight.
+__global__ void __launch_bounds__(256) adam_kernel(
+    float* __restrict__ master, __nv_bfloat16* __restrict__ w, float* __restrict__ grad,
+    float* __restrict__ m, float* __restrict__ v, int64_t n, const float* __restrict__ flags,
+    float lr, float b1, float b2, float eps, float wd, float inv_scale, float max_norm, float bc1,
+    float bc2) {
   const bool skip = flags[1] != 0.f;
   float coef = inv_scale;
   if (max_norm > 0.f) {
     const float norm = sqrtf(flags[0]) * inv_scale;
     if (norm > max_norm) coef *= max_norm / (norm + 1e-6f);
   }
-  const int cnt = static_cast<int>(std::min<int64_t>(4, n - base));
-  for (int j = 0; j < cnt; ++j) {
-    const int64_t k = base + j;
+  const float ib1 = 1.f / bc1, ib2 = 1.f / bc2;
+  const int64_t n4 = n >> 2;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
+       i += stride) {
+    float4 g = reinterpret_cast<float4*>(grad)[i];
+    reinterpret_cast<float4*>(grad)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (skip) continue;
+    float4 p = reinterpret_cast<float4*>(master)[i];
+    float4 mm = reinterpret_cast<float4*>(m)[i];
+    float4 vv = reinterpret_cast<float4*>(v)[i];
+    float gs[4] = {g.x * coef, g.y * coef, g.z * coef, g.w * coef};
+    float ps[4] = {p.x, p.y, p.z, p.w};
+    float ms[4] = {mm.x, mm.y, mm.z, mm.w};
+    float vs[4] = {vv.x, vv.y, vv.z, vv.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      ms[j] = b1 * ms[j] + (1.f - b1) * gs[j];
+      vs[j] = b2 * vs[j] + (1.f - b2) * gs[j] * gs[j];
+      ps[j] -= lr * ((ms[j] * ib1) / (sqrtf(vs[j] * ib2) + eps) + wd * ps[j]);
+    }
+    reinterpret_cast<float4*>(master)[i] = make_float4(ps[0], ps[1], ps[2], ps[3]);
+    reinterpret_cast<float4*>(m)[i] = make_float4(ms[0], ms[1], ms[2], ms[3]);
+    reinterpret_cast<float4*>(v)[i] = make_float4(vs[0], vs[1], vs[2], vs[3]);
+    __nv_bfloat162 lo = __floats2bfloat162_rn(ps[0], ps[1]);
+    __nv_bfloat162 hi = __floats2bfloat162_rn(ps[2], ps[3]);
+    uint2 pk;
+    pk.x = *reinterpret_cast<uint32_t*>(&lo);
+    pk.y = *reinterpret_cast<uint32_t*>(&hi);
+    reinterpret_cast<uint2*>(w)[i] = pk;
+  }
+  // scalar tail (n % 4)
+  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
+    const int64_t k = n4 * 4 + threadIdx.x;
     const float g = grad[k] * coef;
     grad[k] = 0.f;
-    if (skip) continue;
-    const float mk = b1 * m[k] + (1.f - b1) * g;
-    const float vk = b2 * v[k] + (1.f - b2) * g * g;
-    m[k] = mk;
-    v[k] = vk;
-    const float upd = (mk / bc1) / (sqrtf(vk / bc2) + eps) + wd * master[k];
-    const float nw = master[k] - lr * upd;
-    master[k] = nw;
-    w[k] = __float2bfloat16(nw);
+    if (!skip) {
+      const float mk = b1 * m[k] + (1.f - b1) * g;
+      const float vk = b2 * v[k] + (1.f - b2) * g * g;
+      m[k] = mk;
+      v[k] = vk;
+      const float nw = master[k] - lr * ((mk * ib1) / (sqrtf(vk * ib2) + eps) + wd * master[k]);
+      master[k] = nw;
+      w[k] = __float2bfloat16(nw);
+    }
   }
 }
 
@@ -380,7 +411,13 @@ extern "C" int vp_adam_step(float* master, void* weight_bf16, float* grad, float
                             float inv_loss_scale, float max_grad_norm, float bias_c1,
                             float bias_c2, void* stream) {
   if (n <= 0) return VP_OK;
-  adam_kernel<<<blocks_for(n, 256 * 4), 256, 0, ST>>>(
+  // 16-byte alignment of every state array is required for the float4 path
+  if ((reinterpret_cast<uintptr_t>(master) | reinterpret_cast<uintptr_t>(grad) |
+       reinterpret_cast<uintptr_t>(exp_avg) | reinterpret_cast<uintptr_t>(exp_avg_sq)) & 15 ||
+      reinterpret_cast<uintptr_t>(weight_bf16) & 7)
+    return VP_ERR_UNSUPPORTED;
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(148 * 16, (n / 4 + 255) / 256 + 1));
+  adam_kernel<<<grid, 256, 0, ST>>>(
       master, BF(weight_bf16), grad, exp_avg, exp_avg_sq, n, flags, lr, beta1, beta2, eps,
       weight_decay, inv_loss_scale, max_grad_norm, bias_c1, bias_c2);
   return launch_status();
