@@ -8,6 +8,7 @@
 // ldmatrix operand loads and cp.async double buffering; the tcgen05/TMEM
 // version is the next step listed in DESIGN.md.
 #include <cfloat>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -572,6 +573,10 @@ int bwd_t(const void* qkv, const void* o, const void* dout, const float* lse, vo
 }
 
 }  // namespace
+
+int attention_fwd_tc(const void* qkv, void* o, float* lse, int64_t B, int64_t S, int64_t H,
+                     int64_t D, int causal, cudaStream_t st);
+
 }  // namespace vp
 
 using namespace vp;
@@ -580,6 +585,10 @@ extern "C" int vp_attention_fwd(const void* qkv, void* o, float* lse, int64_t ba
                                 int64_t heads, int64_t head_dim, int causal, void* stream) {
   if (batch <= 0 || seq <= 0 || heads <= 0) return VP_ERR_ARGS;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  // tcgen05/TMEM kernel (attention_tc.cu); the mma.sync kernel below is kept
+  // only as an A/B reference (VP_ATTN_LEGACY=1).
+  if (!getenv("VP_ATTN_LEGACY"))
+    return attention_fwd_tc(qkv, o, lse, batch, seq, heads, head_dim, causal, st);
   switch (head_dim) {
     case 64: return causal ? fwd_t<64, true>(qkv, o, lse, batch, seq, heads, st)
                            : fwd_t<64, false>(qkv, o, lse, batch, seq, heads, st);
