@@ -23,19 +23,22 @@ namespace vp {
 namespace {
 
 constexpr int TA_BM = 128;
-constexpr int TA_BN = 128;
+constexpr int TA_BN = 64;   // keys per block: TMEM S0|S1|O = 64+64+<=128 <= 256 cols -> 2 CTAs/SM
 constexpr int TA_THREADS = 256;
 constexpr int TA_STAGES = 2;
 
 template <int D>
 struct TaSmem {
   static constexpr int CH = (D + 63) / 64;           // 64-wide d-chunks (128 B rows)
-  static constexpr int TILE = 128 * 128 * CH;        // bytes of one [128 x D] tile (padded)
+  static constexpr int QCH = 128 * 128;              // one Q d-chunk: 128 rows x 128 B
+  static constexpr int KCH = TA_BN * 128;            // one K/V d-chunk: 64 rows x 128 B
+  static constexpr int QTILE = QCH * CH;
+  static constexpr int KTILE = KCH * CH;
   static constexpr int Q_OFF = 0;
-  static constexpr int K_OFF = TILE;                 // [stage]
-  static constexpr int V_OFF = K_OFF + TA_STAGES * TILE;
-  static constexpr int P_OFF = V_OFF + TA_STAGES * TILE;  // [128 x 128] bf16 = 32 KB
-  static constexpr int BAR_OFF = P_OFF + 2 * 16384;
+  static constexpr int K_OFF = QTILE;                // [stage]
+  static constexpr int V_OFF = K_OFF + TA_STAGES * KTILE;
+  static constexpr int P_OFF = V_OFF + TA_STAGES * KTILE;  // [128 x 64] bf16 = 16 KB
+  static constexpr int BAR_OFF = P_OFF + 128 * TA_BN * 2;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
 
@@ -71,8 +74,9 @@ __device__ __forceinline__ float fast_exp2(float x) {
 }
 
 template <int D, bool CAUSAL>
-__global__ void __launch_bounds__(TA_THREADS, 1)
-    attn_fwd_tc(const __grid_constant__ CUtensorMap tmQKV, __nv_bfloat16* __restrict__ out,
+__global__ void __launch_bounds__(TA_THREADS, 2)
+    attn_fwd_tc(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmKV,
+                __nv_bfloat16* __restrict__ out,
                 float* __restrict__ lse, int S, int H, int n_qb, float scale_log2) {
   using L = TaSmem<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -99,6 +103,7 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmQKV);
+    tma_prefetch(&tmKV);
     mbar_init(q_full, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&kv_full[i], 1);
@@ -110,7 +115,7 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
     mbar_init(p_full, 4);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  if (warp == 2) tmem_alloc(tmem_slot, 256);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -119,19 +124,19 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ===== producer =====
-      mbar_expect_tx(q_full, L::TILE);
+      mbar_expect_tx(q_full, L::QTILE);
 #pragma unroll
       for (int c = 0; c < L::CH; ++c)
-        tma_load_3d(smem + L::Q_OFF + c * 16384, &tmQKV, q_full, h * D + c * 64, q0, b);
+        tma_load_3d(smem + L::Q_OFF + c * L::QCH, &tmQKV, q_full, h * D + c * 64, q0, b);
       for (int j = 0; j < n_kb; ++j) {
         const int st = j % TA_STAGES;
         mbar_wait(&kv_empty[st], ((j / TA_STAGES) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[st], 2 * L::TILE);
+        mbar_expect_tx(&kv_full[st], 2 * L::KTILE);
 #pragma unroll
         for (int c = 0; c < L::CH; ++c) {
-          tma_load_3d(smem + L::K_OFF + st * L::TILE + c * 16384, &tmQKV, &kv_full[st],
+          tma_load_3d(smem + L::K_OFF + st * L::KTILE + c * L::KCH, &tmKV, &kv_full[st],
                       Hd + h * D + c * 64, j * TA_BN, b);
-          tma_load_3d(smem + L::V_OFF + st * L::TILE + c * 16384, &tmQKV, &kv_full[st],
+          tma_load_3d(smem + L::V_OFF + st * L::KTILE + c * L::KCH, &tmKV, &kv_full[st],
                       2 * Hd + h * D + c * 64, j * TA_BN, b);
         }
       }
@@ -139,7 +144,7 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       // ===== MMA issuer =====
-      constexpr uint32_t idS = idesc_bf16(128, 128, false, false);
+      constexpr uint32_t idS = idesc_bf16(128, TA_BN, false, false);
       constexpr uint32_t idO = idesc_bf16(128, D, false, true);
       const uint32_t sQ = smem_u32(smem + L::Q_OFF);
       const uint32_t sP = smem_u32(smem + L::P_OFF);
@@ -148,14 +153,14 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
         const int st = j % TA_STAGES;
         mbar_wait(p_full, j & 1);  // P_j written and O rescaled by the softmax warps
         tc_fence_after();
-        const uint32_t sV = smem_u32(smem + L::V_OFF + st * L::TILE);
+        const uint32_t sV = smem_u32(smem + L::V_OFF + st * L::KTILE);
 #pragma unroll
         for (int k = 0; k < TA_BN / 16; ++k) {
-          // A = P [q][key] K-major: chunk k/4, +32 B per 16 keys
-          const uint64_t ad = sdesc_sw128(sP + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
-          // B = V [key][d] MN-major: +16 rows * 128 B per 16 keys; d-chunks 16 KB apart
-          const uint64_t bd = sdesc_sw128(sV + k * 2048, 16384, 1024);
-          umma_f16(tmem + 256, ad, bd, idO, (j > 0 || k > 0) ? 1u : 0u);
+          // A = P [q][key] K-major (one 128 B row chunk): +32 B per 16 keys
+          const uint64_t ad = sdesc_sw128(sP + k * 32, 16, 1024);
+          // B = V [key][d] MN-major: +16 rows * 128 B per 16 keys; d-chunks KCH apart
+          const uint64_t bd = sdesc_sw128(sV + k * 2048, L::KCH, 1024);
+          umma_f16(tmem + 2 * TA_BN, ad, bd, idO, (j > 0 || k > 0) ? 1u : 0u);
         }
         umma_commit(o_full);
         umma_commit(&kv_empty[st]);
@@ -165,12 +170,12 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
         mbar_wait(&kv_full[st], (j / TA_STAGES) & 1);
         mbar_wait(&s_empty[j & 1], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t sK = smem_u32(smem + L::K_OFF + st * L::TILE);
+        const uint32_t sK = smem_u32(smem + L::K_OFF + st * L::KTILE);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off = (k >> 2) * 16384 + (k & 3) * 32;
-          umma_f16(tmem + (j & 1) * 128, sdesc_sw128(sQ + off, 16, 1024),
-                   sdesc_sw128(sK + off, 16, 1024), idS, k > 0);
+          umma_f16(tmem + (j & 1) * TA_BN,
+                   sdesc_sw128(sQ + (k >> 2) * L::QCH + (k & 3) * 32, 16, 1024),
+                   sdesc_sw128(sK + (k >> 2) * L::KCH + (k & 3) * 32, 16, 1024), idS, k > 0);
         }
         umma_commit(&s_full[j & 1]);
         if (j >= 1) issue_pv(j - 1);
@@ -183,13 +188,13 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
     const int r = qd * 32 + lane;
     const int q = q0 + r;
     const uint32_t trow = (qd * 32) << 16;
-    const uint32_t tO = tmem + trow + 256;
+    const uint32_t tO = tmem + trow + 2 * TA_BN;
     uint8_t* sP = smem + L::P_OFF;
     float m = -FLT_MAX, l = 0.f;
     for (int j = 0; j < n_kb; ++j) {
       mbar_wait(&s_full[j & 1], (j >> 1) & 1);
       tc_fence_after();
-      const uint32_t ts = tmem + trow + (j & 1) * 128;
+      const uint32_t ts = tmem + trow + (j & 1) * TA_BN;
       const int k0 = j * TA_BN;
       const bool need_mask = (k0 + TA_BN > S) || (CAUSAL && k0 + TA_BN - 1 > q0);
       // pass 1: row max
@@ -237,8 +242,8 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
         uint32_t raw[32];
         tmem_ld32(ts + c, raw);
         tmem_ld_wait();
-        // 32 keys = 4 x 16-byte chunks of the 128 B row in chunk (c / 64)
-        uint8_t* rowp = sP + (c >> 6) * 16384 + r * 128;
+        // 32 keys = 4 x 16-byte chunks of the row's 128 B (64 keys)
+        uint8_t* rowp = sP + r * 128;
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           float f[8];
@@ -292,7 +297,7 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem, 512);
+    tmem_dealloc(tmem, 256);
   }
 }
 
@@ -309,13 +314,14 @@ PFN_cuTensorMapEncodeTiled_v12000 encode3() {
   return fn;
 }
 
-// 3D map over a [B, S, cols] bf16 activation: box {64 cols, 128 rows, 1}.
-bool make_tmap_bsc(CUtensorMap* map, const void* base, uint64_t cols, uint64_t S, uint64_t B) {
+// 3D map over a [B, S, cols] bf16 activation: box {64 cols, rows, 1}.
+bool make_tmap_bsc(CUtensorMap* map, const void* base, uint64_t cols, uint64_t S, uint64_t B,
+                   uint32_t rows) {
   auto fn = encode3();
   if (!fn) return false;
   cuuint64_t dims[3] = {cols, S, B};
   cuuint64_t strides[2] = {cols * 2, S * cols * 2};
-  cuuint32_t box[3] = {64, 128, 1};
+  cuuint32_t box[3] = {64, rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box,
             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -326,8 +332,9 @@ template <int D, bool CAUSAL>
 int fwd_tc_t(const void* qkv, void* o, float* lse, int64_t B, int64_t S, int64_t H,
              cudaStream_t st) {
   using L = TaSmem<D>;
-  CUtensorMap tm;
-  if (!make_tmap_bsc(&tm, qkv, 3 * H * D, S, B)) return VP_ERR_UNSUPPORTED;
+  CUtensorMap tm, tkv;
+  if (!make_tmap_bsc(&tm, qkv, 3 * H * D, S, B, 128)) return VP_ERR_UNSUPPORTED;
+  if (!make_tmap_bsc(&tkv, qkv, 3 * H * D, S, B, TA_BN)) return VP_ERR_UNSUPPORTED;
   auto k = attn_fwd_tc<D, CAUSAL>;
   static bool set = false;
   if (!set) {
@@ -338,7 +345,7 @@ int fwd_tc_t(const void* qkv, void* o, float* lse, int64_t B, int64_t S, int64_t
   const int n_qb = static_cast<int>((S + TA_BM - 1) / TA_BM);
   dim3 grid(n_qb, static_cast<unsigned>(B * H));
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(D));
-  k<<<grid, TA_THREADS, L::TOTAL, st>>>(tm, reinterpret_cast<__nv_bfloat16*>(o), lse,
+  k<<<grid, TA_THREADS, L::TOTAL, st>>>(tm, tkv, reinterpret_cast<__nv_bfloat16*>(o), lse,
                                         static_cast<int>(S), static_cast<int>(H), n_qb,
                                         scale_log2);
   return launch_status();
