@@ -13,6 +13,13 @@
 #include "common.cuh"
 
 namespace vp {
+
+int attention_fwd_tc(const void* qkv, void* o, float* lse, int64_t B, int64_t S, int64_t H,
+                     int64_t D, int causal, cudaStream_t st);
+int attention_bwd_tc(const void* qkv, const void* dout, const float* lse, const float* delta,
+                     void* dqkv, int64_t B, int64_t S, int64_t H, int64_t D, int causal,
+                     cudaStream_t st);
+
 namespace {
 
 constexpr int ATT_BM = 64;  // query rows per CTA (16 per warp)
@@ -552,6 +559,8 @@ int bwd_t(const void* qkv, const void* o, const void* dout, const float* lse, vo
   attn_delta_kernel<D><<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, st>>>(
       reinterpret_cast<const __nv_bfloat16*>(o), reinterpret_cast<const __nv_bfloat16*>(dout),
       delta, tokens, static_cast<int>(S), static_cast<int>(H));
+  if (!getenv("VP_ATTN_LEGACY"))
+    return attention_bwd_tc(qkv, dout, lse, delta, dqkv, B, S, H, D, CAUSAL, st);
   const float scale = 1.f / sqrtf(static_cast<float>(D));
   const float scale_log2 = 1.4426950408889634f * scale;
   dim3 grid(static_cast<unsigned>((S + 63) / 64), static_cast<unsigned>(B * H));
@@ -573,9 +582,6 @@ int bwd_t(const void* qkv, const void* o, const void* dout, const float* lse, vo
 }
 
 }  // namespace
-
-int attention_fwd_tc(const void* qkv, void* o, float* lse, int64_t B, int64_t S, int64_t H,
-                     int64_t D, int causal, cudaStream_t st);
 
 }  // namespace vp
 

@@ -328,6 +328,496 @@ bool make_tmap_bsc(CUtensorMap* map, const void* base, uint64_t cols, uint64_t S
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+
+// ===========================================================================
+// Backward on tcgen05 (K3 of DESIGN.md). Deterministic: no atomics.
+//   dkdv kernel: CTA = 128 keys of one (b, h); loops over 64-query blocks.
+//     S^T = K Q^T, dP^T = V dO^T            (TMEM, double-buffered)
+//     P^T = exp2(S^T*scale - lse[q]), dS^T = P^T (dP^T - delta[q])  (thread = key)
+//     dV += P^T dO, dK += dS^T Q            (TMEM accumulators, A from smem)
+//   dq kernel:   CTA = 128 queries; loops over 64-key blocks.
+//     S = Q K^T, dP = dO V^T; dS = P (dP - delta)  (thread = query)
+//     dQ += dS K
+// The same smem tile serves as a K-major operand (QK^T) and as an MN-major
+// operand (dS^T Q) through two descriptors — no transposes in memory.
+// ===========================================================================
+constexpr int TB_M = 128;  // rows owned by the CTA (keys for dkdv, queries for dq)
+constexpr int TB_N = 64;   // inner block (queries for dkdv, keys for dq)
+
+template <int D>
+struct TbSmem {
+  static constexpr int CH = (D + 63) / 64;
+  static constexpr int BIG = 128 * 128;   // one d-chunk of a 128-row tile
+  static constexpr int SMALL = TB_N * 128;  // one d-chunk of a 64-row tile
+  static constexpr int A_OFF = 0;                         // K (dkdv) / Q (dq)   [128 x D]
+  static constexpr int B_OFF = A_OFF + BIG * CH;          // V (dkdv) / dO (dq)  [128 x D]
+  static constexpr int X_OFF = B_OFF + BIG * CH;          // Q_i / K_j  [2 stages][64 x D]
+  static constexpr int Y_OFF = X_OFF + 2 * SMALL * CH;    // dO_i / V_j [2 stages][64 x D]
+  static constexpr int P_OFF = Y_OFF + 2 * SMALL * CH;    // P^T [2][128 x 64] (dkdv only)
+  static constexpr int G_OFF = P_OFF + 2 * 128 * TB_N * 2;  // dS / dS^T [2][128 x 64]
+  static constexpr int V_OFF = G_OFF + 2 * 128 * TB_N * 2;  // lse/delta [2 stages][2][64] f32
+  static constexpr int BAR_OFF = V_OFF + 2 * 2 * TB_N * 4;
+  static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+};
+
+template <int D, bool CAUSAL>
+__global__ void __launch_bounds__(TA_THREADS, 1)
+    attn_bwd_dkdv_tc(const __grid_constant__ CUtensorMap tmQKV128,
+                     const __grid_constant__ CUtensorMap tmQKV64,
+                     const __grid_constant__ CUtensorMap tmDO64, const float* __restrict__ lse,
+                     const float* __restrict__ delta, __nv_bfloat16* __restrict__ dqkv, int S,
+                     int H, float scale_log2, float scale) {
+  using L = TbSmem<D>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* kv_full = bars + 0;
+  uint64_t* q_full = bars + 1;     // [2] (TMA tx + producer-warp arrive for lse/delta)
+  uint64_t* q_empty = bars + 3;    // [2]
+  uint64_t* st_full = bars + 5;    // [2]
+  uint64_t* st_empty = bars + 7;   // [2]
+  uint64_t* p_full = bars + 9;     // [2]
+  uint64_t* p_empty = bars + 11;   // [2]
+  uint64_t* acc_full = bars + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+
+  const int kb = blockIdx.x, bh = blockIdx.y;
+  const int b = bh / H, h = bh % H;
+  const int k0 = kb * TB_M;
+  const int n_qb = (S + TB_N - 1) / TB_N;
+  const int i0 = CAUSAL ? k0 / TB_N : 0;
+  const int n_it = n_qb - i0;
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int Hd = H * D;
+  const float* lse_bh = lse + static_cast<int64_t>(bh) * S;
+  const float* del_bh = delta + static_cast<int64_t>(bh) * S;
+  float* sv = reinterpret_cast<float*>(smem + L::V_OFF);  // [stage][lse|delta][64]
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmQKV128);
+    tma_prefetch(&tmQKV64);
+    tma_prefetch(&tmDO64);
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 2);
+      mbar_init(&q_empty[i], 1);
+      mbar_init(&st_full[i], 1);
+      mbar_init(&st_empty[i], 4);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&p_empty[i], 1);
+    }
+    mbar_init(acc_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tP = tmem + 128, tDV = tmem + 256, tDK = tmem + 256 + D;
+
+  if (warp == 0) {
+    // ===== producer: K/V once; per query block Q_i, dO_i (TMA) + lse/delta (warp) =====
+    if (lane == 0) {
+      mbar_expect_tx(kv_full, 2 * L::BIG * L::CH);
+#pragma unroll
+      for (int c = 0; c < L::CH; ++c) {
+        tma_load_3d(smem + L::A_OFF + c * L::BIG, &tmQKV128, kv_full, Hd + h * D + c * 64, k0, b);
+        tma_load_3d(smem + L::B_OFF + c * L::BIG, &tmQKV128, kv_full, 2 * Hd + h * D + c * 64,
+                    k0, b);
+      }
+    }
+    for (int it = 0; it < n_it; ++it) {
+      const int st = it & 1;
+      const int qi = (i0 + it) * TB_N;
+      if (lane == 0) {
+        mbar_wait(&q_empty[st], ((it >> 1) & 1) ^ 1);
+        mbar_expect_tx(&q_full[st], 2 * L::SMALL * L::CH);
+#pragma unroll
+        for (int c = 0; c < L::CH; ++c) {
+          tma_load_3d(smem + L::X_OFF + st * L::SMALL * L::CH + c * L::SMALL, &tmQKV64,
+                      &q_full[st], h * D + c * 64, qi, b);
+          tma_load_3d(smem + L::Y_OFF + st * L::SMALL * L::CH + c * L::SMALL, &tmDO64,
+                      &q_full[st], h * D + c * 64, qi, b);
+        }
+      }
+      __syncwarp();
+      mbar_wait(&q_empty[st], ((it >> 1) & 1) ^ 1);  // all lanes: stage free
+      float* dst = sv + st * 2 * TB_N;
+      for (int t = lane; t < TB_N; t += 32) {
+        const int q = qi + t;
+        dst[t] = q < S ? lse_bh[q] : 0.f;
+        dst[TB_N + t] = q < S ? del_bh[q] : 0.f;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&q_full[st]);
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ===== MMA issuer =====
+      constexpr uint32_t idST = idesc_bf16(128, TB_N, false, false);
+      constexpr uint32_t idG = idesc_bf16(128, D, false, true);
+      const uint32_t sK = smem_u32(smem + L::A_OFF), sV = smem_u32(smem + L::B_OFF);
+      mbar_wait(kv_full, 0);
+      auto issue_grad = [&](int it) {
+        const int st = it & 1;
+        mbar_wait(&p_full[st], (it >> 1) & 1);
+        tc_fence_after();
+        const uint32_t sQ = smem_u32(smem + L::X_OFF + st * L::SMALL * L::CH);
+        const uint32_t sdO = smem_u32(smem + L::Y_OFF + st * L::SMALL * L::CH);
+        const uint32_t sPt = smem_u32(smem + L::P_OFF + st * 128 * TB_N * 2);
+        const uint32_t sdSt = smem_u32(smem + L::G_OFF + st * 128 * TB_N * 2);
+#pragma unroll
+        for (int k = 0; k < TB_N / 16; ++k) {
+          const uint32_t acc = (it > 0 || k > 0) ? 1u : 0u;
+          umma_f16(tDV, sdesc_sw128(sPt + k * 32, 16, 1024),
+                   sdesc_sw128(sdO + k * 2048, L::SMALL, 1024), idG, acc);
+          umma_f16(tDK, sdesc_sw128(sdSt + k * 32, 16, 1024),
+                   sdesc_sw128(sQ + k * 2048, L::SMALL, 1024), idG, acc);
+        }
+        umma_commit(&p_empty[st]);
+        umma_commit(&q_empty[st]);
+      };
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it & 1;
+        mbar_wait(&q_full[st], (it >> 1) & 1);
+        mbar_wait(&st_empty[st], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t sQ = smem_u32(smem + L::X_OFF + st * L::SMALL * L::CH);
+        const uint32_t sdO = smem_u32(smem + L::Y_OFF + st * L::SMALL * L::CH);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t ob = (k >> 2) * L::BIG + (k & 3) * 32;
+          const uint32_t os = (k >> 2) * L::SMALL + (k & 3) * 32;
+          umma_f16(tS + st * TB_N, sdesc_sw128(sK + ob, 16, 1024), sdesc_sw128(sQ + os, 16, 1024),
+                   idST, k > 0);
+          umma_f16(tP + st * TB_N, sdesc_sw128(sV + ob, 16, 1024),
+                   sdesc_sw128(sdO + os, 16, 1024), idST, k > 0);
+        }
+        umma_commit(&st_full[st]);
+        if (it >= 1) issue_grad(it - 1);
+      }
+      if (n_it > 0) issue_grad(n_it - 1);
+      umma_commit(acc_full);
+    }
+  } else if (warp >= 4) {
+    // ===== P^T / dS^T: thread = key row =====
+    const uint32_t qd = warp & 3;
+    const int r = qd * 32 + lane;
+    const int key = k0 + r;
+    const uint32_t trow = (qd * 32) << 16;
+    for (int it = 0; it < n_it; ++it) {
+      const int st = it & 1;
+      const int qi = (i0 + it) * TB_N;
+      mbar_wait(&st_full[st], (it >> 1) & 1);
+      mbar_wait(&p_empty[st], ((it >> 1) & 1) ^ 1);
+      mbar_wait(&q_full[st], (it >> 1) & 1);  // lse/delta of this stage
+      tc_fence_after();
+      const float* slse = sv + st * 2 * TB_N;
+      const float* sdel = slse + TB_N;
+      const bool need_mask = (qi + TB_N > S) || (CAUSAL && qi < k0 + TB_M - 1);
+      uint8_t* rowP = smem + L::P_OFF + st * 128 * TB_N * 2 + r * 128;
+      uint8_t* rowG = smem + L::G_OFF + st * 128 * TB_N * 2 + r * 128;
+#pragma unroll
+      for (int c = 0; c < TB_N; c += 32) {
+        uint32_t rs[32], rd[32];
+        tmem_ld32(tS + trow + st * TB_N + c, rs);
+        tmem_ld32(tP + trow + st * TB_N + c, rd);
+        tmem_ld_wait();
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          float fp[8], fg[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const int i = g * 8 + t;
+            const int qq = qi + c + i;
+            float pv = fast_exp2(fmaf(__uint_as_float(rs[i]), scale_log2, -slse[c + i]));
+            if (need_mask && (qq >= S || (CAUSAL && key > qq))) pv = 0.f;
+            fp[t] = pv;
+            fg[t] = pv * (__uint_as_float(rd[i]) - sdel[c + i]);
+          }
+          const int chunk = (c >> 3) + g;
+          const int sw = (chunk ^ (r & 7)) << 4;
+          *reinterpret_cast<uint4*>(rowP + sw) = pack8(fp);
+          *reinterpret_cast<uint4*>(rowG + sw) = pack8(fg);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&st_empty[st]);
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[st]);
+    }
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    __nv_bfloat16* row = dqkv + (static_cast<int64_t>(b) * S + key) * (3 * Hd);
+#pragma unroll 1
+    for (int c = 0; c < D; c += 32) {
+      uint32_t rk[32], rv[32];
+      tmem_ld32(tDK + trow + c, rk);
+      tmem_ld32(tDV + trow + c, rv);
+      tmem_ld_wait();
+      if (key < S) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          float fk[8], fv[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            fk[t] = n_it > 0 ? __uint_as_float(rk[i + t]) * scale : 0.f;
+            fv[t] = n_it > 0 ? __uint_as_float(rv[i + t]) : 0.f;
+          }
+          *reinterpret_cast<uint4*>(row + Hd + h * D + c + i) = pack8(fk);
+          *reinterpret_cast<uint4*>(row + 2 * Hd + h * D + c + i) = pack8(fv);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+template <int D, bool CAUSAL>
+__global__ void __launch_bounds__(TA_THREADS, 1)
+    attn_bwd_dq_tc(const __grid_constant__ CUtensorMap tmQKV128,
+                   const __grid_constant__ CUtensorMap tmQKV64,
+                   const __grid_constant__ CUtensorMap tmDO128, const float* __restrict__ lse,
+                   const float* __restrict__ delta, __nv_bfloat16* __restrict__ dqkv, int S, int H,
+                   int n_qb, float scale_log2, float scale) {
+  using L = TbSmem<D>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* a_full = bars + 0;
+  uint64_t* k_full = bars + 1;     // [2]
+  uint64_t* k_empty = bars + 3;    // [2]
+  uint64_t* s_full = bars + 5;     // [2]
+  uint64_t* s_empty = bars + 7;    // [2]
+  uint64_t* g_full = bars + 9;     // [2]
+  uint64_t* g_empty = bars + 11;   // [2]
+  uint64_t* acc_full = bars + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+
+  const int qb = n_qb - 1 - static_cast<int>(blockIdx.x);
+  const int bh = blockIdx.y;
+  const int b = bh / H, h = bh % H;
+  const int q0 = qb * TB_M;
+  int n_kb = (S + TB_N - 1) / TB_N;
+  if (CAUSAL) n_kb = min(n_kb, (q0 + TB_M + TB_N - 1) / TB_N);
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int Hd = H * D;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmQKV128);
+    tma_prefetch(&tmQKV64);
+    tma_prefetch(&tmDO128);
+    mbar_init(a_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 4);
+      mbar_init(&g_full[i], 4);
+      mbar_init(&g_empty[i], 1);
+    }
+    mbar_init(acc_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tP = tmem + 128, tDQ = tmem + 256;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(a_full, 2 * L::BIG * L::CH);
+#pragma unroll
+      for (int c = 0; c < L::CH; ++c) {
+        tma_load_3d(smem + L::A_OFF + c * L::BIG, &tmQKV128, a_full, h * D + c * 64, q0, b);
+        tma_load_3d(smem + L::B_OFF + c * L::BIG, &tmDO128, a_full, h * D + c * 64, q0, b);
+      }
+      for (int j = 0; j < n_kb; ++j) {
+        const int st = j & 1;
+        mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&k_full[st], 2 * L::SMALL * L::CH);
+#pragma unroll
+        for (int c = 0; c < L::CH; ++c) {
+          tma_load_3d(smem + L::X_OFF + st * L::SMALL * L::CH + c * L::SMALL, &tmQKV64,
+                      &k_full[st], Hd + h * D + c * 64, j * TB_N, b);
+          tma_load_3d(smem + L::Y_OFF + st * L::SMALL * L::CH + c * L::SMALL, &tmQKV64,
+                      &k_full[st], 2 * Hd + h * D + c * 64, j * TB_N, b);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idS = idesc_bf16(128, TB_N, false, false);
+      constexpr uint32_t idG = idesc_bf16(128, D, false, true);
+      const uint32_t sQ = smem_u32(smem + L::A_OFF), sdO = smem_u32(smem + L::B_OFF);
+      mbar_wait(a_full, 0);
+      auto issue_dq = [&](int j) {
+        const int st = j & 1;
+        mbar_wait(&g_full[st], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t sK = smem_u32(smem + L::X_OFF + st * L::SMALL * L::CH);
+        const uint32_t sdS = smem_u32(smem + L::G_OFF + st * 128 * TB_N * 2);
+#pragma unroll
+        for (int k = 0; k < TB_N / 16; ++k)
+          umma_f16(tDQ, sdesc_sw128(sdS + k * 32, 16, 1024),
+                   sdesc_sw128(sK + k * 2048, L::SMALL, 1024), idG, (j > 0 || k > 0) ? 1u : 0u);
+        umma_commit(&g_empty[st]);
+        umma_commit(&k_empty[st]);
+      };
+      for (int j = 0; j < n_kb; ++j) {
+        const int st = j & 1;
+        mbar_wait(&k_full[st], (j >> 1) & 1);
+        mbar_wait(&s_empty[st], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t sK = smem_u32(smem + L::X_OFF + st * L::SMALL * L::CH);
+        const uint32_t sV = smem_u32(smem + L::Y_OFF + st * L::SMALL * L::CH);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t ob = (k >> 2) * L::BIG + (k & 3) * 32;
+          const uint32_t os = (k >> 2) * L::SMALL + (k & 3) * 32;
+          umma_f16(tS + st * TB_N, sdesc_sw128(sQ + ob, 16, 1024), sdesc_sw128(sK + os, 16, 1024),
+                   idS, k > 0);
+          umma_f16(tP + st * TB_N, sdesc_sw128(sdO + ob, 16, 1024),
+                   sdesc_sw128(sV + os, 16, 1024), idS, k > 0);
+        }
+        umma_commit(&s_full[st]);
+        if (j >= 1) issue_dq(j - 1);
+      }
+      issue_dq(n_kb - 1);
+      umma_commit(acc_full);
+    }
+  } else if (warp >= 4) {
+    const uint32_t qd = warp & 3;
+    const int r = qd * 32 + lane;
+    const int q = q0 + r;
+    const uint32_t trow = (qd * 32) << 16;
+    const float lrow = q < S ? lse[static_cast<int64_t>(bh) * S + q] : 0.f;
+    const float drow = q < S ? delta[static_cast<int64_t>(bh) * S + q] : 0.f;
+    for (int j = 0; j < n_kb; ++j) {
+      const int st = j & 1;
+      const int kj = j * TB_N;
+      mbar_wait(&s_full[st], (j >> 1) & 1);
+      mbar_wait(&g_empty[st], ((j >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const bool need_mask = (kj + TB_N > S) || (CAUSAL && kj + TB_N - 1 > q0);
+      uint8_t* rowG = smem + L::G_OFF + st * 128 * TB_N * 2 + r * 128;
+#pragma unroll
+      for (int c = 0; c < TB_N; c += 32) {
+        uint32_t rs[32], rd[32];
+        tmem_ld32(tS + trow + st * TB_N + c, rs);
+        tmem_ld32(tP + trow + st * TB_N + c, rd);
+        tmem_ld_wait();
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          float fg[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const int i = g * 8 + t;
+            const int kk = kj + c + i;
+            float pv = fast_exp2(fmaf(__uint_as_float(rs[i]), scale_log2, -lrow));
+            if (need_mask && (kk >= S || (CAUSAL && kk > q))) pv = 0.f;
+            fg[t] = pv * (__uint_as_float(rd[i]) - drow);
+          }
+          const int chunk = (c >> 3) + g;
+          *reinterpret_cast<uint4*>(rowG + ((chunk ^ (r & 7)) << 4)) = pack8(fg);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[st]);
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&g_full[st]);
+    }
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    __nv_bfloat16* row = dqkv + (static_cast<int64_t>(b) * S + q) * (3 * Hd) + h * D;
+#pragma unroll 1
+    for (int c = 0; c < D; c += 32) {
+      uint32_t rq[32];
+      tmem_ld32(tDQ + trow + c, rq);
+      tmem_ld_wait();
+      if (q < S) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          float f[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) f[t] = __uint_as_float(rq[i + t]) * scale;
+          *reinterpret_cast<uint4*>(row + c + i) = pack8(f);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+template <int D, bool CAUSAL>
+int bwd_tc_t(const void* qkv, const void* dout, const float* lse, const float* delta, void* dqkv,
+             int64_t B, int64_t S, int64_t H, cudaStream_t st) {
+  using L = TbSmem<D>;
+  CUtensorMap q128, q64, do64, do128;
+  const uint64_t cols = 3 * H * D;
+  if (!make_tmap_bsc(&q128, qkv, cols, S, B, 128) || !make_tmap_bsc(&q64, qkv, cols, S, B, 64) ||
+      !make_tmap_bsc(&do64, dout, H * D, S, B, 64) || !make_tmap_bsc(&do128, dout, H * D, S, B, 128))
+    return VP_ERR_UNSUPPORTED;
+  auto k1 = attn_bwd_dkdv_tc<D, CAUSAL>;
+  auto k2 = attn_bwd_dq_tc<D, CAUSAL>;
+  static bool set = false;
+  if (!set) {
+    cudaError_t e = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+    if (e != cudaSuccess) return e;
+    set = true;
+  }
+  const float scale = 1.f / sqrtf(static_cast<float>(D));
+  const float scale_log2 = 1.4426950408889634f * scale;
+  const int n_kb = static_cast<int>((S + TB_M - 1) / TB_M);
+  k1<<<dim3(n_kb, static_cast<unsigned>(B * H)), TA_THREADS, L::TOTAL, st>>>(
+      q128, q64, do64, lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), static_cast<int>(S),
+      static_cast<int>(H), scale_log2, scale);
+  const int n_qb = static_cast<int>((S + TB_M - 1) / TB_M);
+  k2<<<dim3(n_qb, static_cast<unsigned>(B * H)), TA_THREADS, L::TOTAL, st>>>(
+      q128, q64, do128, lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), static_cast<int>(S),
+      static_cast<int>(H), n_qb, scale_log2, scale);
+  return launch_status();
+}
+
+}  // namespace
+
+int attention_bwd_tc(const void* qkv, const void* dout, const float* lse, const float* delta,
+                     void* dqkv, int64_t B, int64_t S, int64_t H, int64_t D, int causal,
+                     cudaStream_t st) {
+  if ((3 * H * D) % 8) return VP_ERR_UNSUPPORTED;
+  switch (D) {
+    case 64: return causal ? bwd_tc_t<64, true>(qkv, dout, lse, delta, dqkv, B, S, H, st)
+                           : bwd_tc_t<64, false>(qkv, dout, lse, delta, dqkv, B, S, H, st);
+    case 96: return causal ? bwd_tc_t<96, true>(qkv, dout, lse, delta, dqkv, B, S, H, st)
+                           : bwd_tc_t<96, false>(qkv, dout, lse, delta, dqkv, B, S, H, st);
+    case 128: return causal ? bwd_tc_t<128, true>(qkv, dout, lse, delta, dqkv, B, S, H, st)
+                            : bwd_tc_t<128, false>(qkv, dout, lse, delta, dqkv, B, S, H, st);
+    default: return VP_ERR_UNSUPPORTED;
+  }
+}
+
+namespace {
 template <int D, bool CAUSAL>
 int fwd_tc_t(const void* qkv, void* o, float* lse, int64_t B, int64_t S, int64_t H,
              cudaStream_t st) {
