@@ -25,7 +25,9 @@ namespace {
 constexpr int TA_BM = 128;
 constexpr int TA_BN = 64;   // keys per block: TMEM S0|S1|O = 64+64+<=128 <= 256 cols -> 2 CTAs/SM
 constexpr int TA_THREADS = 256;
-constexpr int TA_STAGES = 2;
+// K/V ring depth: deep enough to cover the L2->SMEM TMA latency of a block
+// while the previous ones are consumed (2 CTAs/SM still fit at D=64).
+__host__ __device__ constexpr int ta_stages(int D) { return D <= 64 ? 4 : 3; }
 
 template <int D>
 struct TaSmem {
@@ -36,8 +38,9 @@ struct TaSmem {
   static constexpr int KTILE = KCH * CH;
   static constexpr int Q_OFF = 0;
   static constexpr int K_OFF = QTILE;                // [stage]
-  static constexpr int V_OFF = K_OFF + TA_STAGES * KTILE;
-  static constexpr int P_OFF = V_OFF + TA_STAGES * KTILE;  // [128 x 64] bf16 = 16 KB
+  static constexpr int STAGES = ta_stages(D);
+  static constexpr int V_OFF = K_OFF + STAGES * KTILE;
+  static constexpr int P_OFF = V_OFF + STAGES * KTILE;  // [128 x 64] bf16 = 16 KB
   static constexpr int BAR_OFF = P_OFF + 128 * TA_BN * 2;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
@@ -84,13 +87,13 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;              // [2]
-  uint64_t* kv_empty = bars + 3;             // [2]
-  uint64_t* s_full = bars + 5;               // [2]
-  uint64_t* s_empty = bars + 7;              // [2]
-  uint64_t* o_full = bars + 9;
-  uint64_t* p_full = bars + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* kv_full = bars + 1;              // [STAGES <= 4]
+  uint64_t* kv_empty = bars + 5;             // [STAGES]
+  uint64_t* s_full = bars + 9;               // [2]
+  uint64_t* s_empty = bars + 11;             // [2]
+  uint64_t* o_full = bars + 13;
+  uint64_t* p_full = bars + 14;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
 
   const int qb = n_qb - 1 - static_cast<int>(blockIdx.x);  // heavy (late) causal blocks first
   const int bh = blockIdx.y;
@@ -105,9 +108,11 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
     tma_prefetch(&tmQKV);
     tma_prefetch(&tmKV);
     mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < L::STAGES; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], 4);
     }
@@ -129,8 +134,8 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
       for (int c = 0; c < L::CH; ++c)
         tma_load_3d(smem + L::Q_OFF + c * L::QCH, &tmQKV, q_full, h * D + c * 64, q0, b);
       for (int j = 0; j < n_kb; ++j) {
-        const int st = j % TA_STAGES;
-        mbar_wait(&kv_empty[st], ((j / TA_STAGES) & 1) ^ 1);
+        const int st = j % L::STAGES;
+        mbar_wait(&kv_empty[st], ((j / L::STAGES) & 1) ^ 1);
         mbar_expect_tx(&kv_full[st], 2 * L::KTILE);
 #pragma unroll
         for (int c = 0; c < L::CH; ++c) {
@@ -150,7 +155,7 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
       const uint32_t sP = smem_u32(smem + L::P_OFF);
       mbar_wait(q_full, 0);
       auto issue_pv = [&](int j) {
-        const int st = j % TA_STAGES;
+        const int st = j % L::STAGES;
         mbar_wait(p_full, j & 1);  // P_j written and O rescaled by the softmax warps
         tc_fence_after();
         const uint32_t sV = smem_u32(smem + L::V_OFF + st * L::KTILE);
@@ -166,8 +171,8 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
         umma_commit(&kv_empty[st]);
       };
       for (int j = 0; j < n_kb; ++j) {
-        const int st = j % TA_STAGES;
-        mbar_wait(&kv_full[st], (j / TA_STAGES) & 1);
+        const int st = j % L::STAGES;
+        mbar_wait(&kv_full[st], (j / L::STAGES) & 1);
         mbar_wait(&s_empty[j & 1], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t sK = smem_u32(smem + L::K_OFF + st * L::KTILE);
@@ -346,17 +351,18 @@ constexpr int TB_N = 64;   // inner block (queries for dkdv, keys for dq)
 
 template <int D>
 struct TbSmem {
+  static constexpr int NS = D <= 64 ? 4 : 3;   // stages of the streamed 64-row operands
   static constexpr int CH = (D + 63) / 64;
   static constexpr int BIG = 128 * 128;   // one d-chunk of a 128-row tile
   static constexpr int SMALL = TB_N * 128;  // one d-chunk of a 64-row tile
   static constexpr int A_OFF = 0;                         // K (dkdv) / Q (dq)   [128 x D]
   static constexpr int B_OFF = A_OFF + BIG * CH;          // V (dkdv) / dO (dq)  [128 x D]
-  static constexpr int X_OFF = B_OFF + BIG * CH;          // Q_i / K_j  [2 stages][64 x D]
-  static constexpr int Y_OFF = X_OFF + 2 * SMALL * CH;    // dO_i / V_j [2 stages][64 x D]
-  static constexpr int P_OFF = Y_OFF + 2 * SMALL * CH;    // P^T [2][128 x 64] (dkdv only)
+  static constexpr int X_OFF = B_OFF + BIG * CH;          // Q_i / K_j  [NS][64 x D]
+  static constexpr int Y_OFF = X_OFF + NS * SMALL * CH;   // dO_i / V_j [NS][64 x D]
+  static constexpr int P_OFF = Y_OFF + NS * SMALL * CH;   // P^T [2][128 x 64] (dkdv only)
   static constexpr int G_OFF = P_OFF + 2 * 128 * TB_N * 2;  // dS / dS^T [2][128 x 64]
-  static constexpr int V_OFF = G_OFF + 2 * 128 * TB_N * 2;  // lse/delta [2 stages][2][64] f32
-  static constexpr int BAR_OFF = V_OFF + 2 * 2 * TB_N * 4;
+  static constexpr int V_OFF = G_OFF + 2 * 128 * TB_N * 2;  // lse/delta [NS][2][64] f32
+  static constexpr int BAR_OFF = V_OFF + NS * 2 * TB_N * 4;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
 
@@ -373,14 +379,14 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* kv_full = bars + 0;
-  uint64_t* q_full = bars + 1;     // [2] (TMA tx + producer-warp arrive for lse/delta)
-  uint64_t* q_empty = bars + 3;    // [2]
-  uint64_t* st_full = bars + 5;    // [2]
-  uint64_t* st_empty = bars + 7;   // [2]
-  uint64_t* p_full = bars + 9;     // [2]
-  uint64_t* p_empty = bars + 11;   // [2]
-  uint64_t* acc_full = bars + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* q_full = bars + 1;     // [NS] (TMA tx + producer-warp arrive for lse/delta)
+  uint64_t* q_empty = bars + 5;    // [NS]
+  uint64_t* st_full = bars + 9;    // [2]
+  uint64_t* st_empty = bars + 11;  // [2]
+  uint64_t* p_full = bars + 13;    // [2]
+  uint64_t* p_empty = bars + 15;   // [2]
+  uint64_t* acc_full = bars + 17;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
 
   const int kb = blockIdx.x, bh = blockIdx.y;
   const int b = bh / H, h = bh % H;
@@ -399,9 +405,11 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
     tma_prefetch(&tmQKV64);
     tma_prefetch(&tmDO64);
     mbar_init(kv_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < L::NS; ++i) {
       mbar_init(&q_full[i], 2);
       mbar_init(&q_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&st_full[i], 1);
       mbar_init(&st_empty[i], 4);
       mbar_init(&p_full[i], 4);
@@ -429,10 +437,11 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
       }
     }
     for (int it = 0; it < n_it; ++it) {
-      const int st = it & 1;
+      const int st = it % L::NS;
+      const uint32_t ph = (it / L::NS) & 1;
       const int qi = (i0 + it) * TB_N;
       if (lane == 0) {
-        mbar_wait(&q_empty[st], ((it >> 1) & 1) ^ 1);
+        mbar_wait(&q_empty[st], ph ^ 1);
         mbar_expect_tx(&q_full[st], 2 * L::SMALL * L::CH);
 #pragma unroll
         for (int c = 0; c < L::CH; ++c) {
@@ -443,7 +452,7 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
         }
       }
       __syncwarp();
-      mbar_wait(&q_empty[st], ((it >> 1) & 1) ^ 1);  // all lanes: stage free
+      mbar_wait(&q_empty[st], ph ^ 1);  // all lanes: stage free
       float* dst = sv + st * 2 * TB_N;
       for (int t = lane; t < TB_N; t += 32) {
         const int q = qi + t;
@@ -462,10 +471,11 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
       mbar_wait(kv_full, 0);
       auto issue_grad = [&](int it) {
         const int st = it & 1;
+        const int qs = it % L::NS;
         mbar_wait(&p_full[st], (it >> 1) & 1);
         tc_fence_after();
-        const uint32_t sQ = smem_u32(smem + L::X_OFF + st * L::SMALL * L::CH);
-        const uint32_t sdO = smem_u32(smem + L::Y_OFF + st * L::SMALL * L::CH);
+        const uint32_t sQ = smem_u32(smem + L::X_OFF + qs * L::SMALL * L::CH);
+        const uint32_t sdO = smem_u32(smem + L::Y_OFF + qs * L::SMALL * L::CH);
         const uint32_t sPt = smem_u32(smem + L::P_OFF + st * 128 * TB_N * 2);
         const uint32_t sdSt = smem_u32(smem + L::G_OFF + st * 128 * TB_N * 2);
 #pragma unroll
@@ -477,15 +487,16 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
                    sdesc_sw128(sQ + k * 2048, L::SMALL, 1024), idG, acc);
         }
         umma_commit(&p_empty[st]);
-        umma_commit(&q_empty[st]);
+        umma_commit(&q_empty[qs]);
       };
       for (int it = 0; it < n_it; ++it) {
         const int st = it & 1;
-        mbar_wait(&q_full[st], (it >> 1) & 1);
+        const int qs = it % L::NS;
+        mbar_wait(&q_full[qs], (it / L::NS) & 1);
         mbar_wait(&st_empty[st], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t sQ = smem_u32(smem + L::X_OFF + st * L::SMALL * L::CH);
-        const uint32_t sdO = smem_u32(smem + L::Y_OFF + st * L::SMALL * L::CH);
+        const uint32_t sQ = smem_u32(smem + L::X_OFF + qs * L::SMALL * L::CH);
+        const uint32_t sdO = smem_u32(smem + L::Y_OFF + qs * L::SMALL * L::CH);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t ob = (k >> 2) * L::BIG + (k & 3) * 32;
@@ -512,9 +523,9 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
       const int qi = (i0 + it) * TB_N;
       mbar_wait(&st_full[st], (it >> 1) & 1);
       mbar_wait(&p_empty[st], ((it >> 1) & 1) ^ 1);
-      mbar_wait(&q_full[st], (it >> 1) & 1);  // lse/delta of this stage
+      mbar_wait(&q_full[it % L::NS], (it / L::NS) & 1);  // lse/delta of this stage
       tc_fence_after();
-      const float* slse = sv + st * 2 * TB_N;
+      const float* slse = sv + (it % L::NS) * 2 * TB_N;
       const float* sdel = slse + TB_N;
       const bool need_mask = (qi + TB_N > S) || (CAUSAL && qi < k0 + TB_M - 1);
       uint8_t* rowP = smem + L::P_OFF + st * 128 * TB_N * 2 + r * 128;
@@ -595,14 +606,14 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* a_full = bars + 0;
-  uint64_t* k_full = bars + 1;     // [2]
-  uint64_t* k_empty = bars + 3;    // [2]
-  uint64_t* s_full = bars + 5;     // [2]
-  uint64_t* s_empty = bars + 7;    // [2]
-  uint64_t* g_full = bars + 9;     // [2]
-  uint64_t* g_empty = bars + 11;   // [2]
-  uint64_t* acc_full = bars + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* k_full = bars + 1;     // [NS]
+  uint64_t* k_empty = bars + 5;    // [NS]
+  uint64_t* s_full = bars + 9;     // [2]
+  uint64_t* s_empty = bars + 11;   // [2]
+  uint64_t* g_full = bars + 13;    // [2]
+  uint64_t* g_empty = bars + 15;   // [2]
+  uint64_t* acc_full = bars + 17;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
 
   const int qb = n_qb - 1 - static_cast<int>(blockIdx.x);
   const int bh = blockIdx.y;
@@ -618,9 +629,11 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
     tma_prefetch(&tmQKV64);
     tma_prefetch(&tmDO128);
     mbar_init(a_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < L::NS; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], 4);
       mbar_init(&g_full[i], 4);
@@ -645,8 +658,8 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
         tma_load_3d(smem + L::B_OFF + c * L::BIG, &tmDO128, a_full, h * D + c * 64, q0, b);
       }
       for (int j = 0; j < n_kb; ++j) {
-        const int st = j & 1;
-        mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
+        const int st = j % L::NS;
+        mbar_wait(&k_empty[st], ((j / L::NS) & 1) ^ 1);
         mbar_expect_tx(&k_full[st], 2 * L::SMALL * L::CH);
 #pragma unroll
         for (int c = 0; c < L::CH; ++c) {
@@ -665,24 +678,26 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
       mbar_wait(a_full, 0);
       auto issue_dq = [&](int j) {
         const int st = j & 1;
+        const int ks = j % L::NS;
         mbar_wait(&g_full[st], (j >> 1) & 1);
         tc_fence_after();
-        const uint32_t sK = smem_u32(smem + L::X_OFF + st * L::SMALL * L::CH);
+        const uint32_t sK = smem_u32(smem + L::X_OFF + ks * L::SMALL * L::CH);
         const uint32_t sdS = smem_u32(smem + L::G_OFF + st * 128 * TB_N * 2);
 #pragma unroll
         for (int k = 0; k < TB_N / 16; ++k)
           umma_f16(tDQ, sdesc_sw128(sdS + k * 32, 16, 1024),
                    sdesc_sw128(sK + k * 2048, L::SMALL, 1024), idG, (j > 0 || k > 0) ? 1u : 0u);
         umma_commit(&g_empty[st]);
-        umma_commit(&k_empty[st]);
+        umma_commit(&k_empty[ks]);
       };
       for (int j = 0; j < n_kb; ++j) {
         const int st = j & 1;
-        mbar_wait(&k_full[st], (j >> 1) & 1);
+        const int ks = j % L::NS;
+        mbar_wait(&k_full[ks], (j / L::NS) & 1);
         mbar_wait(&s_empty[st], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t sK = smem_u32(smem + L::X_OFF + st * L::SMALL * L::CH);
-        const uint32_t sV = smem_u32(smem + L::Y_OFF + st * L::SMALL * L::CH);
+        const uint32_t sK = smem_u32(smem + L::X_OFF + ks * L::SMALL * L::CH);
+        const uint32_t sV = smem_u32(smem + L::Y_OFF + ks * L::SMALL * L::CH);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t ob = (k >> 2) * L::BIG + (k & 3) * 32;
