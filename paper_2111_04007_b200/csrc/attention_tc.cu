@@ -27,7 +27,7 @@ constexpr int TA_BN = 64;   // keys per block: TMEM S0|S1|O = 64+64+<=128 <= 256
 constexpr int TA_THREADS = 256;
 // K/V ring depth: deep enough to cover the L2->SMEM TMA latency of a block
 // while the previous ones are consumed (2 CTAs/SM still fit at D=64).
-__host__ __device__ constexpr int ta_stages(int D) { return D <= 64 ? 4 : 3; }
+__host__ __device__ constexpr int ta_stages(int D) { return 3; }
 
 template <int D>
 struct TaSmem {
@@ -40,8 +40,8 @@ struct TaSmem {
   static constexpr int K_OFF = QTILE;                // [stage]
   static constexpr int STAGES = ta_stages(D);
   static constexpr int V_OFF = K_OFF + STAGES * KTILE;
-  static constexpr int P_OFF = V_OFF + STAGES * KTILE;  // [128 x 64] bf16 = 16 KB
-  static constexpr int BAR_OFF = P_OFF + 128 * TA_BN * 2;
+  static constexpr int P_OFF = V_OFF + STAGES * KTILE;  // [2][128 x 64] bf16 = 2 x 16 KB
+  static constexpr int BAR_OFF = P_OFF + 2 * 128 * TA_BN * 2;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
 
@@ -91,9 +91,9 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
   uint64_t* kv_empty = bars + 5;             // [STAGES]
   uint64_t* s_full = bars + 9;               // [2]
   uint64_t* s_empty = bars + 11;             // [2]
-  uint64_t* o_full = bars + 13;
-  uint64_t* p_full = bars + 14;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
+  uint64_t* o_full = bars + 13;              // [2]: PV_j commits o_full[j & 1]
+  uint64_t* p_full = bars + 15;              // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
 
   const int qb = n_qb - 1 - static_cast<int>(blockIdx.x);  // heavy (late) causal blocks first
   const int bh = blockIdx.y;
@@ -116,8 +116,10 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], 4);
     }
-    mbar_init(o_full, 1);
-    mbar_init(p_full, 4);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&o_full[i], 1);
+      mbar_init(&p_full[i], 4);
+    }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 256);
@@ -156,18 +158,19 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
       mbar_wait(q_full, 0);
       auto issue_pv = [&](int j) {
         const int st = j % L::STAGES;
-        mbar_wait(p_full, j & 1);  // P_j written and O rescaled by the softmax warps
+        mbar_wait(&p_full[j & 1], (j >> 1) & 1);  // P_j written (and O rescaled if needed)
         tc_fence_after();
         const uint32_t sV = smem_u32(smem + L::V_OFF + st * L::KTILE);
+        const uint32_t sPj = sP + (j & 1) * 128 * TA_BN * 2;
 #pragma unroll
         for (int k = 0; k < TA_BN / 16; ++k) {
           // A = P [q][key] K-major (one 128 B row chunk): +32 B per 16 keys
-          const uint64_t ad = sdesc_sw128(sP + k * 32, 16, 1024);
+          const uint64_t ad = sdesc_sw128(sPj + k * 32, 16, 1024);
           // B = V [key][d] MN-major: +16 rows * 128 B per 16 keys; d-chunks KCH apart
           const uint64_t bd = sdesc_sw128(sV + k * 2048, L::KCH, 1024);
           umma_f16(tmem + 2 * TA_BN, ad, bd, idO, (j > 0 || k > 0) ? 1u : 0u);
         }
-        umma_commit(o_full);
+        umma_commit(&o_full[j & 1]);
         umma_commit(&kv_empty[st]);
       };
       for (int j = 0; j < n_kb; ++j) {
@@ -223,11 +226,13 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
       const bool grow = m_cand > m + 8.f;   // lazy: keep a stale max unless it grew > 2^8
       const float m_new = grow ? m_cand : m;
       const float corr = fast_exp2(m - m_new);  // 1 when !grow; 0 for the first block
-      if (j >= 1) {
-        // PV_{j-1} done: O is final for m and the P buffer is free
-        mbar_wait(o_full, (j - 1) & 1);
+      // P buffer (j & 1) was last read by PV_{j-2}
+      if (j >= 2) mbar_wait(&o_full[j & 1], ((j - 2) >> 1) & 1);
+      if (j >= 1 && __any_sync(0xffffffffu, grow)) {
+        // rescale O in place: needs PV_{j-1} complete
+        mbar_wait(&o_full[(j - 1) & 1], ((j - 1) >> 1) & 1);
         tc_fence_after();
-        if (__any_sync(0xffffffffu, grow)) {
+        {
 #pragma unroll 1
           for (int c = 0; c < D; c += 32) {
             uint32_t raw[32];
@@ -248,7 +253,7 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
         tmem_ld32(ts + c, raw);
         tmem_ld_wait();
         // 32 keys = 4 x 16-byte chunks of the row's 128 B (64 keys)
-        uint8_t* rowp = sP + r * 128;
+        uint8_t* rowp = sP + (j & 1) * 128 * TA_BN * 2 + r * 128;
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           float f[8];
@@ -273,11 +278,11 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
       if (lane == 0) mbar_arrive(&s_empty[j & 1]);
       fence_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      if (lane == 0) mbar_arrive(&p_full[j & 1]);
       l = l * corr + sum;
       m = m_new;
     }
-    mbar_wait(o_full, (n_kb - 1) & 1);
+    mbar_wait(&o_full[(n_kb - 1) & 1], ((n_kb - 1) >> 1) & 1);
     tc_fence_after();
     const float inv = 1.f / l;
     __nv_bfloat16* orow = out + (static_cast<int64_t>(b) * S + q) * Hd + h * D;
