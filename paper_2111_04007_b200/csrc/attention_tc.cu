@@ -205,8 +205,10 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
       const uint32_t ts = tmem + trow + (j & 1) * TA_BN;
       const int k0 = j * TA_BN;
       const bool need_mask = (k0 + TA_BN > S) || (CAUSAL && k0 + TA_BN - 1 > q0);
-      // pass 1: row max
-      float mx = -FLT_MAX;
+      // pass 1: row max (8 independent partial maxima: short dependency chains)
+      float pm[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) pm[t] = -FLT_MAX;
 #pragma unroll
       for (int c = 0; c < TA_BN; c += 32) {
         uint32_t raw[32];
@@ -219,9 +221,11 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
             const int key = k0 + c + i;
             if (key >= S || (CAUSAL && key > q)) x = -FLT_MAX;
           }
-          mx = fmaxf(mx, x);
+          pm[i & 7] = fmaxf(pm[i & 7], x);
         }
       }
+      const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
+                             fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
       const float m_cand = fmaxf(m, mx * scale_log2);
       const bool grow = m_cand > m + 8.f;   // lazy: keep a stale max unless it grew > 2^8
       const float m_new = grow ? m_cand : m;
@@ -246,7 +250,7 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
         }
       }
       // pass 2: P = exp2(s*scale - m), row sum, P -> smem (bf16, swizzled)
-      float sum = 0.f;
+      float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int c = 0; c < TA_BN; c += 32) {
         uint32_t raw[32];
@@ -267,12 +271,13 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
               dead = key >= S || (CAUSAL && key > q);
             }
             f[t] = dead ? 0.f : fast_exp2(fmaf(x, scale_log2, -m_new));
-            sum += f[t];
+            ps[t] += f[t];
           }
           const int chunk = ((c & 63) >> 3) + g;
           *reinterpret_cast<uint4*>(rowp + ((chunk ^ (r & 7)) << 4)) = pack8(f);
         }
       }
+      const float sum = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_empty[j & 1]);
