@@ -70,6 +70,12 @@ __device__ __forceinline__ void tmem_st_wait() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void sts128(uint32_t addr, const uint4& v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -205,7 +211,10 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
       const uint32_t ts = tmem + trow + (j & 1) * TA_BN;
       const int k0 = j * TA_BN;
       const bool need_mask = (k0 + TA_BN > S) || (CAUSAL && k0 + TA_BN - 1 > q0);
-      // pass 1: row max (8 independent partial maxima: short dependency chains)
+      // pass 1: row max (8 independent partial maxima: short dependency chains).
+      // Masking is one compare per element against the row's key limit
+      // (keys >= lim are dead: past the sequence or above the diagonal).
+      const int lim = CAUSAL ? min(S, q + 1) : S;
       float pm[8];
 #pragma unroll
       for (int t = 0; t < 8; ++t) pm[t] = -FLT_MAX;
@@ -214,14 +223,15 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
         uint32_t raw[32];
         tmem_ld32(ts + c, raw);
         tmem_ld_wait();
+        if (need_mask) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          float x = __uint_as_float(raw[i]);
-          if (need_mask) {
-            const int key = k0 + c + i;
-            if (key >= S || (CAUSAL && key > q)) x = -FLT_MAX;
+          for (int i = 0; i < 32; ++i) {
+            const float x = (k0 + c + i < lim) ? __uint_as_float(raw[i]) : -FLT_MAX;
+            pm[i & 7] = fmaxf(pm[i & 7], x);
           }
-          pm[i & 7] = fmaxf(pm[i & 7], x);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) pm[i & 7] = fmaxf(pm[i & 7], __uint_as_float(raw[i]));
         }
       }
       const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
@@ -257,24 +267,19 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
         tmem_ld32(ts + c, raw);
         tmem_ld_wait();
         // 32 keys = 4 x 16-byte chunks of the row's 128 B (64 keys)
-        uint8_t* rowp = sP + (j & 1) * 128 * TA_BN * 2 + r * 128;
+        const uint32_t rowp = smem_u32(sP + (j & 1) * 128 * TA_BN * 2 + r * 128);
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           float f[8];
 #pragma unroll
           for (int t = 0; t < 8; ++t) {
             const int i = g * 8 + t;
-            const float x = __uint_as_float(raw[i]);
-            bool dead = false;
-            if (need_mask) {
-              const int key = k0 + c + i;
-              dead = key >= S || (CAUSAL && key > q);
-            }
-            f[t] = dead ? 0.f : fast_exp2(fmaf(x, scale_log2, -m_new));
+            const float e = fast_exp2(fmaf(__uint_as_float(raw[i]), scale_log2, -m_new));
+            f[t] = (!need_mask || k0 + c + i < lim) ? e : 0.f;
             ps[t] += f[t];
           }
           const int chunk = ((c & 63) >> 3) + g;
-          *reinterpret_cast<uint4*>(rowp + ((chunk ^ (r & 7)) << 4)) = pack8(f);
+          sts128(rowp + ((chunk ^ (r & 7)) << 4), pack8(f));
         }
       }
       const float sum = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
@@ -538,8 +543,8 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
       const float* slse = sv + (it % L::NS) * 2 * TB_N;
       const float* sdel = slse + TB_N;
       const bool need_mask = (qi + TB_N > S) || (CAUSAL && qi < k0 + TB_M - 1);
-      uint8_t* rowP = smem + L::P_OFF + st * 128 * TB_N * 2 + r * 128;
-      uint8_t* rowG = smem + L::G_OFF + st * 128 * TB_N * 2 + r * 128;
+      const uint32_t rowP = smem_u32(smem + L::P_OFF + st * 128 * TB_N * 2 + r * 128);
+      const uint32_t rowG = smem_u32(smem + L::G_OFF + st * 128 * TB_N * 2 + r * 128);
 #pragma unroll
       for (int c = 0; c < TB_N; c += 32) {
         uint32_t rs[32], rd[32];
@@ -560,8 +565,8 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
           }
           const int chunk = (c >> 3) + g;
           const int sw = (chunk ^ (r & 7)) << 4;
-          *reinterpret_cast<uint4*>(rowP + sw) = pack8(fp);
-          *reinterpret_cast<uint4*>(rowG + sw) = pack8(fg);
+          sts128(rowP + sw, pack8(fp));
+          sts128(rowG + sw, pack8(fg));
         }
       }
       tc_fence_before();
@@ -737,7 +742,7 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
       mbar_wait(&g_empty[st], ((j >> 1) & 1) ^ 1);
       tc_fence_after();
       const bool need_mask = (kj + TB_N > S) || (CAUSAL && kj + TB_N - 1 > q0);
-      uint8_t* rowG = smem + L::G_OFF + st * 128 * TB_N * 2 + r * 128;
+      const uint32_t rowG = smem_u32(smem + L::G_OFF + st * 128 * TB_N * 2 + r * 128);
 #pragma unroll
       for (int c = 0; c < TB_N; c += 32) {
         uint32_t rs[32], rd[32];
@@ -756,7 +761,7 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
             fg[t] = pv * (__uint_as_float(rd[i]) - drow);
           }
           const int chunk = (c >> 3) + g;
-          *reinterpret_cast<uint4*>(rowG + ((chunk ^ (r & 7)) << 4)) = pack8(fg);
+          sts128(rowG + ((chunk ^ (r & 7)) << 4), pack8(fg));
         }
       }
       tc_fence_before();
