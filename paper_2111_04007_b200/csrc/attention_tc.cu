@@ -532,6 +532,7 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
     const uint32_t qd = warp & 3;
     const int r = qd * 32 + lane;
     const int key = k0 + r;
+    const int qlo = CAUSAL ? key : 0;
     const uint32_t trow = (qd * 32) << 16;
     for (int it = 0; it < n_it; ++it) {
       const int st = it & 1;
@@ -559,7 +560,8 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
             const int i = g * 8 + t;
             const int qq = qi + c + i;
             float pv = fast_exp2(fmaf(__uint_as_float(rs[i]), scale_log2, -slse[c + i]));
-            if (need_mask && (qq >= S || (CAUSAL && key > qq))) pv = 0.f;
+            // valid queries for this key: qlo <= q < S (branch-free select)
+            pv = (!need_mask || (qq >= qlo && qq < S)) ? pv : 0.f;
             fp[t] = pv;
             fg[t] = pv * (__uint_as_float(rd[i]) - sdel[c + i]);
           }
@@ -733,6 +735,7 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
     const int r = qd * 32 + lane;
     const int q = q0 + r;
     const uint32_t trow = (qd * 32) << 16;
+    const int lim = CAUSAL ? min(S, q + 1) : S;
     const float lrow = q < S ? lse[static_cast<int64_t>(bh) * S + q] : 0.f;
     const float drow = q < S ? delta[static_cast<int64_t>(bh) * S + q] : 0.f;
     for (int j = 0; j < n_kb; ++j) {
@@ -757,7 +760,7 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
             const int i = g * 8 + t;
             const int kk = kj + c + i;
             float pv = fast_exp2(fmaf(__uint_as_float(rs[i]), scale_log2, -lrow));
-            if (need_mask && (kk >= S || (CAUSAL && kk > q))) pv = 0.f;
+            pv = (!need_mask || kk < lim) ? pv : 0.f;
             fg[t] = pv * (__uint_as_float(rd[i]) - drow);
           }
           const int chunk = (c >> 3) + g;
