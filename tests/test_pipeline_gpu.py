@@ -108,3 +108,17 @@ def test_two_stage_pipeline_matches_oracle():
     p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-4000:]
     assert "PARITY OK" in p.stdout
+
+
+@pytest.mark.multigpu
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 4,
+                    reason="needs 4 GPUs")
+@pytest.mark.parametrize("P,D", [(2, 2), (4, 1)])
+def test_four_gpu_pipeline_matches_oracle(P, D):
+    env = dict(os.environ, PYTHONPATH=ROOT)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4",
+           "--master-addr=127.0.0.1", f"--master-port={29541 + P}",
+           os.path.join(ROOT, "tests", "dist_pipeline_check.py"), "--P", str(P), "--D", str(D)]
+    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-4000:]
+    assert "PARITY OK" in p.stdout
