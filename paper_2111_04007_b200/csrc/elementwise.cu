@@ -143,6 +143,7 @@ __global__ void __launch_bounds__(256) colsum_partial(const __nv_bfloat16* __res
   const int64_t r1 = min(rows, r0 + rows_per_part);
   float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (c0 < cols) {
+#pragma unroll 4
     for (int64_t r = r0 + ty; r < r1; r += 8) {
       float f[8];
       unpack8(*reinterpret_cast<const uint4*>(dy + r * cols + c0), f);

@@ -318,8 +318,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ===========================================================================
 constexpr int kStages2 = 5;
 constexpr int kStageBytes2 = 2 * 128 * BK * 2;        // A half + B half per CTA = 32 KB
+constexpr int kEpiWarps2 = 8;                          // 2 per TMEM lane quadrant (column halves)
+constexpr int kThreads2 = 128 + 32 * kEpiWarps2;
 constexpr int kStagingPerWarp = 8192;                  // 2 x 4 KB epilogue buffers
-constexpr int kSmem2 = kStages2 * kStageBytes2 + 4 * kStagingPerWarp + 256 + 1024;
+constexpr int kSmem2 = kStages2 * kStageBytes2 + kEpiWarps2 * kStagingPerWarp + 256 + 1024;
 
 struct Epi2 {
   const __nv_bfloat16* bias;
@@ -389,7 +391,7 @@ __device__ __forceinline__ void epi2_apply(const Epi2& e, int64_t row, int64_t c
 }
 
 template <int EPI, bool A_MN, bool B_MN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX,
                  int64_t M, int64_t N, int64_t K, int split_k, Epi2 epi) {
@@ -397,7 +399,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* staging = smem + kStages2 * kStageBytes2;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(staging + 4 * kStagingPerWarp);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(staging + kEpiWarps2 * kStagingPerWarp);
   uint64_t* empty_bar = full_bar + kStages2;
   uint64_t* tfull_bar = empty_bar + kStages2;  // [2]
   uint64_t* tempty_bar = tfull_bar + 2;        // [2] (leader's are used)
@@ -426,7 +428,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 8);
+      mbar_init(&tempty_bar[a], 2 * kEpiWarps2);
     }
     fence_mbar_init();
   }
@@ -506,9 +508,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= 4) {
-    // ===== Epilogue (both CTAs): rows [rank*128 + q*32, +32) of the tile =====
+    // ===== Epilogue (both CTAs): rows [rank*128 + q*32, +32) of the tile,
+    // columns [half*128, +128) =====
     const uint32_t q = warp & 3;
-    uint8_t* wbuf = staging + q * kStagingPerWarp;
+    const uint32_t half = (warp - 4) >> 2;
+    uint8_t* wbuf = staging + (warp - 4) * kStagingPerWarp;
     uint32_t local = 0, nbuf = 0;
     const uint32_t lane = lane_id();
     for (int64_t u = cid; u < n_units; u += n_clusters, ++local) {
@@ -522,7 +526,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint32_t taddr = tmem_base + ((q * 32) << 16) + acc * 256;
       if constexpr (kF32Out) {
 #pragma unroll 1
-        for (int c = 0; c < 256; c += 32) {
+        for (int c = half * 128; c < half * 128 + 128; c += 32) {
           const int32_t col0 = static_cast<int32_t>(nb * 256 + c);
           if (col0 >= N) break;
           uint32_t raw[32];
@@ -547,7 +551,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
       } else {
 #pragma unroll 1
-        for (int c = 0; c < 256; c += 64) {
+        for (int c = half * 128; c < half * 128 + 128; c += 64) {
           const int32_t col0 = static_cast<int32_t>(nb * 256 + c);
           if (col0 >= N) break;
           float v[64], pre[64];
@@ -736,8 +740,8 @@ int launch2_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& t
   }
   const int64_t units = ((M + 255) / 256) * ((N + 255) / 256) * split_k;
   const int64_t clusters = std::min<int64_t>(units, sm_count() / 2);
-  kern<<<static_cast<unsigned>(2 * clusters), kThreads, kSmem2, st>>>(ta, tb, td, tx, M, N, K,
-                                                                       split_k, e);
+  kern<<<static_cast<unsigned>(2 * clusters), kThreads2, kSmem2, st>>>(ta, tb, td, tx, M, N, K,
+                                                                        split_k, e);
   return cudaGetLastError();
 }
 

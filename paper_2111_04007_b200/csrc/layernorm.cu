@@ -148,6 +148,104 @@ __global__ void __launch_bounds__(kWarps * 32)
   }
 }
 
+// Small-row variant (cols <= 1024): each warp keeps its row (x, dy) in
+// registers and its lanes' dgamma/dbeta partials in registers across all
+// rows it handles; gamma is read from L1; one shared-memory reduction per
+// CTA at the end.
+template <int NV>
+__global__ void __launch_bounds__(kWarps * 32)
+    ln_bwd_reg_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+                      const __nv_bfloat16* __restrict__ g, const float* __restrict__ mean,
+                      const float* __restrict__ rstd, __nv_bfloat16* __restrict__ dx,
+                      float* __restrict__ ws, int64_t rows, int cols, int accumulate,
+                      int rows_per_cta) {
+  extern __shared__ float red[];  // [kWarps][2][cols]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nvec = cols >> 3;
+  float dg[NV][8], db[NV][8];
+  const uint4* gv = reinterpret_cast<const uint4*>(g);
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) dg[i][j] = db[i][j] = 0.f;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * rows_per_cta;
+  const int64_t r1 = min(rows, r0 + rows_per_cta);
+  for (int64_t row = r0 + warp; row < r1; row += kWarps) {
+    const uint4* xr = reinterpret_cast<const uint4*>(x + row * cols);
+    const uint4* dyr = reinterpret_cast<const uint4*>(dy + row * cols);
+    uint4* dxr = reinterpret_cast<uint4*>(dx + row * cols);
+    const float mu = mean[row], rs = rstd[row];
+    uint4 xu[NV], du[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = lane + i * 32;
+      if (c < nvec) {
+        xu[i] = xr[c];
+        du[i] = dyr[c];
+      }
+    }
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = lane + i * 32;
+      if (c < nvec) {
+        float xv[8], dv[8], gg[8];
+        unpack8(xu[i], xv);
+        unpack8(du[i], dv);
+        unpack8(gv[c], gg);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float xh = (xv[j] - mu) * rs;
+          const float gy = dv[j] * gg[j];
+          s1 += gy;
+          s2 += gy * xh;
+          dg[i][j] += dv[j] * xh;
+          db[i][j] += dv[j];
+        }
+      }
+    }
+    const float m1 = warp_sum(s1) / cols, m2 = warp_sum(s2) / cols;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = lane + i * 32;
+      if (c < nvec) {
+        float xv[8], dv[8], gg[8], o[8];
+        unpack8(xu[i], xv);
+        unpack8(du[i], dv);
+        unpack8(gv[c], gg);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = rs * (dv[j] * gg[j] - m1 - (xv[j] - mu) * rs * m2);
+        if (accumulate) {
+          float p[8];
+          unpack8(dxr[c], p);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) o[j] += p[j];
+        }
+        dxr[c] = pack8(o);
+      }
+    }
+  }
+  float* mine = red + warp * 2 * cols;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = lane + i * 32;
+    if (c < nvec) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        mine[c * 8 + j] = dg[i][j];
+        mine[cols + c * 8 + j] = db[i][j];
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2 * cols; i += blockDim.x) {
+    float acc = 0.f;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) acc += red[w * 2 * cols + i];
+    ws[static_cast<int64_t>(blockIdx.x) * 2 * cols + i] = acc;
+  }
+}
+
 // 32 columns x 8 part-lanes per block; fixed-order tree => deterministic.
 __global__ void __launch_bounds__(256) ln_param_reduce(const float* __restrict__ ws,
                                                        float* __restrict__ dgamma,
@@ -232,6 +330,7 @@ extern "C" int vp_layernorm_bwd(const void* dy, const void* x, const void* gamma
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   LN_DISPATCH(nv, {
     auto k = ln_bwd_kernel<NV>;
+    if constexpr (NV <= 4) k = ln_bwd_reg_kernel<NV>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                static_cast<int>(smem));
     k<<<parts, kWarps * 32, smem, st>>>(

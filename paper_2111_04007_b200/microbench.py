@@ -16,15 +16,22 @@ def bench(M, N, Kd, layout="nt", epi=K.EPI_STORE, iters=20):
     a = A if a_k else A.t().contiguous()
     b = B if b_k else B.t().contiguous()
     out = torch.empty(M, N, device="cuda", dtype=torch.float32 if epi >= K.EPI_ACC_F32 else torch.bfloat16)
+    bias = torch.randn(N, device="cuda").bfloat16()
+    aux = torch.randn(M, N, device="cuda").bfloat16()
+    kw = {}
+    if epi in (K.EPI_BIAS, K.EPI_BIAS_GELU, K.EPI_BIAS_RESID):
+        kw["bias"] = bias
+    if epi in (K.EPI_BIAS_GELU, K.EPI_BIAS_RESID, K.EPI_DGELU):
+        kw["aux"] = aux
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     for _ in range(3):
-        K.gemm(a, b, out, a_kmajor=a_k, b_kmajor=b_k, epilogue=epi)
+        K.gemm(a, b, out, a_kmajor=a_k, b_kmajor=b_k, epilogue=epi, **kw)
     ts = []
     for _ in range(iters):
         flush.zero_()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        K.gemm(a, b, out, a_kmajor=a_k, b_kmajor=b_k, epilogue=epi)
+        K.gemm(a, b, out, a_kmajor=a_k, b_kmajor=b_k, epilogue=epi, **kw)
         e.record()
         torch.cuda.synchronize()
         ts.append(s.elapsed_time(e))
@@ -65,3 +72,10 @@ if __name__ == "__main__":
     ]
     for M, N, Kd, lay in shapes:
         print(json.dumps(bench(M, N, Kd, lay)), flush=True)
+    # the 355M stage GEMMs with their fused epilogues (fwd, dgrad, wgrad)
+    for M, N, Kd, lay, epi in [(8192, 3072, 1024, "nt", K.EPI_BIAS), (8192, 1024, 1024, "nt", K.EPI_BIAS_RESID),
+                               (8192, 4096, 1024, "nt", K.EPI_BIAS_GELU), (8192, 1024, 4096, "nt", K.EPI_BIAS_RESID),
+                               (8192, 4096, 1024, "nn", K.EPI_DGELU), (8192, 1024, 4096, "nn", K.EPI_STORE),
+                               (1024, 4096, 8192, "tn", K.EPI_ACC_F32), (3072, 1024, 8192, "tn", K.EPI_ACC_F32),
+                               (1024, 1024, 8192, "tn", K.EPI_ACC_F32)]:
+        print(json.dumps(bench(M, N, Kd, lay, epi)), flush=True)
