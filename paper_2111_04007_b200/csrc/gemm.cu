@@ -321,7 +321,7 @@ constexpr int kStageBytes2 = 2 * 128 * BK * 2;        // A half + B half per CTA
 constexpr int kEpiWarps2 = 8;                          // 2 per TMEM lane quadrant (column halves)
 constexpr int kThreads2 = 128 + 32 * kEpiWarps2;
 constexpr int kStagingPerWarp = 8192;                  // 2 x 4 KB epilogue buffers
-constexpr int kSmem2 = kStages2 * kStageBytes2 + kEpiWarps2 * kStagingPerWarp + 256 + 1024;
+constexpr int kSmem2 = kStages2 * kStageBytes2 + kEpiWarps2 * kStagingPerWarp + 512 + 1024;
 
 struct Epi2 {
   const __nv_bfloat16* bias;
@@ -338,7 +338,8 @@ __device__ __forceinline__ void store_row_swizzled(uint8_t* buf, uint32_t row,
 
 template <int EPI>
 __device__ __forceinline__ void epi2_apply(const Epi2& e, int64_t row, int64_t col0, int64_t M,
-                                           int64_t N, float (&v)[64], float (&pre)[64]) {
+                                           int64_t N, float (&v)[64], float (&pre)[64],
+                                           const float (&xin)[64]) {
   // bias (columns col0..col0+63), guarded for the ragged right edge
   if constexpr (EPI == VP_EPI_BIAS || EPI == VP_EPI_BIAS_GELU || EPI == VP_EPI_BIAS_RESID) {
     if (col0 + 64 <= N) {
@@ -363,30 +364,22 @@ __device__ __forceinline__ void epi2_apply(const Epi2& e, int64_t row, int64_t c
     }
   }
   if constexpr (EPI == VP_EPI_BIAS_RESID || EPI == VP_EPI_DGELU) {
-    if (row < M) {
-      const __nv_bfloat16* a = e.aux_in + row * e.ldaux + col0;
-      if (col0 + 64 <= N) {
+    // aux row values were staged in smem by TMA (see gemm2_kernel)
 #pragma unroll
-        for (int i = 0; i < 64; i += 8) {
-          float x[8];
-          unpack8(*reinterpret_cast<const uint4*>(a + i), x);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            if constexpr (EPI == VP_EPI_BIAS_RESID) v[i + j] += x[j];
-            else v[i + j] *= gelu_tanh_grad(x[j]);
-          }
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 64; ++i) {
-          if (col0 + i < N) {
-            const float x = __bfloat162float(a[i]);
-            if constexpr (EPI == VP_EPI_BIAS_RESID) v[i] += x;
-            else v[i] *= gelu_tanh_grad(x);
-          }
-        }
-      }
+    for (int i = 0; i < 64; ++i) {
+      if constexpr (EPI == VP_EPI_BIAS_RESID) v[i] += xin[i];
+      else v[i] *= gelu_tanh_grad(xin[i]);
     }
+  }
+}
+
+__device__ __forceinline__ void load_row_swizzled(const uint8_t* buf, uint32_t row, float (&x)[64]) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    float f[8];
+    unpack8(*reinterpret_cast<const uint4*>(buf + row * 128 + ((k ^ (row & 7)) << 4)), f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[8 * k + j] = f[j];
   }
 }
 
@@ -403,9 +396,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
   uint64_t* empty_bar = full_bar + kStages2;
   uint64_t* tfull_bar = empty_bar + kStages2;  // [2]
   uint64_t* tempty_bar = tfull_bar + 2;        // [2] (leader's are used)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* aux_bar = tempty_bar + 2;          // [kEpiWarps2][2] aux-tile TMA prefetch
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + 2 * kEpiWarps2);
 
   constexpr bool kF32Out = (EPI == VP_EPI_ACC_F32 || EPI == VP_EPI_STORE_F32);
+  constexpr bool kAuxIn = (EPI == VP_EPI_BIAS_RESID || EPI == VP_EPI_DGELU);
   const uint32_t warp = warp_id();
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
@@ -430,6 +425,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       mbar_init(&tfull_bar[a], 1);
       mbar_init(&tempty_bar[a], 2 * kEpiWarps2);
     }
+    for (int a = 0; a < 2 * kEpiWarps2; ++a) mbar_init(&aux_bar[a], 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc_2sm(tmem_slot, 512);
@@ -550,11 +546,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
           ++nbuf;
         }
       } else {
+        uint64_t* abar = aux_bar + 2 * (warp - 4);
+        if constexpr (kAuxIn) {
+          // Prefetch this warp's two 32x64 aux sub-tiles into its staging
+          // buffers (they are overwritten in place by the outputs below).
+          if (lane == 0) {
+            bulk_wait_read<0>();
+#pragma unroll
+            for (int ci = 0; ci < 2; ++ci) {
+              const int32_t col0 = static_cast<int32_t>(nb * 256 + half * 128 + ci * 64);
+              if (col0 < N) {
+                mbar_expect_tx(&abar[ci], 4096);
+                tma_load_2d(wbuf + ci * 4096, &tmX, &abar[ci], col0, row0);
+              }
+            }
+          }
+          __syncwarp();
+        }
 #pragma unroll 1
-        for (int c = half * 128; c < half * 128 + 128; c += 64) {
+        for (int ci = 0; ci < 2; ++ci) {
+          const int c = half * 128 + ci * 64;
           const int32_t col0 = static_cast<int32_t>(nb * 256 + c);
           if (col0 >= N) break;
-          float v[64], pre[64];
+          float v[64], pre[64], xin[64];
           {
             uint32_t raw[32];
             tmem_ld32(taddr + c, raw);
@@ -566,7 +580,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[32 + i] = __uint_as_float(raw[i]);
           }
-          epi2_apply<EPI>(epi, row, col0, M, N, v, pre);
+          if constexpr (kAuxIn) {
+            mbar_wait(&abar[ci], local & 1);
+            load_row_swizzled(wbuf + ci * 4096, lane, xin);
+            __syncwarp();  // every lane has read its aux row before outputs overwrite it
+          }
+          epi2_apply<EPI>(epi, row, col0, M, N, v, pre, xin);
           if constexpr (EPI == VP_EPI_BIAS_GELU) {
             // pre-activation (aux) then activation (D): both buffers in turn
             if (lane == 0) bulk_wait_read<0>();
@@ -596,9 +615,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
               bulk_commit();
             }
           } else {
-            uint8_t* buf = wbuf + (nbuf & 1) * 4096;
-            if (lane == 0) bulk_wait_read<1>();
-            __syncwarp();
+            uint8_t* buf = wbuf + (kAuxIn ? ci : (nbuf & 1)) * 4096;
+            if (!kAuxIn) {
+              if (lane == 0) bulk_wait_read<1>();
+              __syncwarp();
+            }
             uint4 ch[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
@@ -807,7 +828,8 @@ static int gemm_entry(int a_kmajor, int b_kmajor, int epilogue, const void* A, i
     ok = ok && (b_mn ? make_tmap(&tb, B, N, K, ldb, 64, BK) : make_tmap(&tb, B, K, N, ldb, BK, 128));
     ok = ok && (f32_out ? make_tmap(&td, D, N, M, ldd, 32, 32, true)
                         : make_tmap(&td, D, N, M, ldd, 64, 32));
-    if (epilogue == VP_EPI_BIAS_GELU) ok = ok && make_tmap(&tx, aux, N, M, ldaux, 64, 32);
+    if (epilogue == VP_EPI_BIAS_GELU || epilogue == VP_EPI_BIAS_RESID || epilogue == VP_EPI_DGELU)
+      ok = ok && make_tmap(&tx, aux, N, M, ldaux, 64, 32);
     else tx = td;
     if (!ok) return VP_ERR_UNSUPPORTED;
     // Split K only when the reduce-add epilogue makes it exact-by-construction
@@ -816,9 +838,19 @@ static int gemm_entry(int a_kmajor, int b_kmajor, int epilogue, const void* A, i
     const int64_t tiles = ((M + 255) / 256) * ((N + 255) / 256);
     const int64_t clusters = sm_count() / 2;
     if (epilogue == VP_EPI_ACC_F32 && tiles < clusters) {
+      // choose the split with the best wave efficiency (ties -> smaller split),
+      // keeping >= 4 k-blocks per split
       const int64_t n_kb = (K + BK - 1) / BK;
-      split = static_cast<int>(std::min<int64_t>((clusters + tiles - 1) / tiles, n_kb / 8));
-      if (split < 1) split = 1;
+      double best = 0.0;
+      for (int64_t sp = 1; sp <= std::max<int64_t>(1, n_kb / 4) && sp <= 16; ++sp) {
+        const int64_t units = tiles * sp;
+        const int64_t rounds = (units + clusters - 1) / clusters;
+        const double eff = double(units) / double(rounds * clusters);
+        if (eff > best + 0.02) {
+          best = eff;
+          split = static_cast<int>(sp);
+        }
+      }
       if (const char* f = getenv("VP_GEMM_SPLITK")) split = std::max(1, atoi(f));
     }
     Epi2 e{reinterpret_cast<const __nv_bfloat16*>(bias), reinterpret_cast<const __nv_bfloat16*>(aux),
