@@ -846,7 +846,7 @@ static int gemm_entry(int a_kmajor, int b_kmajor, int epilogue, const void* A, i
         const int64_t units = tiles * sp;
         const int64_t rounds = (units + clusters - 1) / clusters;
         const double eff = double(units) / double(rounds * clusters);
-        if (eff > best + 0.02) {
+        if (eff >= best - 0.02) {  // ties -> the larger split (shorter units)
           best = eff;
           split = static_cast<int>(sp);
         }

@@ -1,0 +1,43 @@
+"""The C-ABI library loads on a CPU-only host and exports every function
+include/vpipe.h declares (no device compute is invoked here)."""
+
+import os
+import re
+import subprocess
+
+import paper_2111_04007_b200._lib as L
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared():
+    text = open(os.path.join(ROOT, "include", "vpipe.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(vp_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_every_declared_symbol_is_exported():
+    names = declared()
+    assert len(names) >= 30
+    for n in names:
+        assert hasattr(L.lib, n), n
+    nm = subprocess.run(["nm", "-D", "--defined-only", L.LIB_PATH], capture_output=True,
+                        text=True).stdout
+    exported = set(re.findall(r"\sT\s(vp_[a-z0-9_]+)", nm))
+    assert set(names) <= exported, sorted(set(names) - exported)
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", L.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_no_cpu_fallback_module():
+    # the product package must not import the oracle anywhere
+    pkg = os.path.join(ROOT, "paper_2111_04007_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in src and "from oracle" not in src, f
