@@ -363,6 +363,10 @@ bool make_tmap_bsc(CUtensorMap* map, const void* base, uint64_t cols, uint64_t S
 // ===========================================================================
 constexpr int TB_M = 128;  // rows owned by the CTA (keys for dkdv, queries for dq)
 constexpr int TB_N = 64;   // inner block (queries for dkdv, keys for dq)
+// 8 compute warps: two per TMEM lane quadrant, each owning half of the 64
+// columns (the backward has no row reductions, so columns split freely).
+constexpr int TB_CW = 8;
+constexpr int TB_THREADS = 128 + 32 * TB_CW;
 
 template <int D>
 struct TbSmem {
@@ -382,7 +386,7 @@ struct TbSmem {
 };
 
 template <int D, bool CAUSAL>
-__global__ void __launch_bounds__(TA_THREADS, 1)
+__global__ void __launch_bounds__(TB_THREADS, 1)
     attn_bwd_dkdv_tc(const __grid_constant__ CUtensorMap tmQKV128,
                      const __grid_constant__ CUtensorMap tmQKV64,
                      const __grid_constant__ CUtensorMap tmDO64, const float* __restrict__ lse,
@@ -426,8 +430,8 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&st_full[i], 1);
-      mbar_init(&st_empty[i], 4);
-      mbar_init(&p_full[i], 4);
+      mbar_init(&st_empty[i], TB_CW);
+      mbar_init(&p_full[i], TB_CW);
       mbar_init(&p_empty[i], 1);
     }
     mbar_init(acc_full, 1);
@@ -528,8 +532,9 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
       umma_commit(acc_full);
     }
   } else if (warp >= 4) {
-    // ===== P^T / dS^T: thread = key row =====
+    // ===== P^T / dS^T: thread = key row; this warp owns 32 of the 64 columns =====
     const uint32_t qd = warp & 3;
+    const int chalf = static_cast<int>(warp - 4) >> 2;
     const int r = qd * 32 + lane;
     const int key = k0 + r;
     const int qlo = CAUSAL ? key : 0;
@@ -546,8 +551,8 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
       const bool need_mask = (qi + TB_N > S) || (CAUSAL && qi < k0 + TB_M - 1);
       const uint32_t rowP = smem_u32(smem + L::P_OFF + st * 128 * TB_N * 2 + r * 128);
       const uint32_t rowG = smem_u32(smem + L::G_OFF + st * 128 * TB_N * 2 + r * 128);
-#pragma unroll
-      for (int c = 0; c < TB_N; c += 32) {
+      {
+        const int c = chalf * 32;
         uint32_t rs[32], rd[32];
         tmem_ld32(tS + trow + st * TB_N + c, rs);
         tmem_ld32(tP + trow + st * TB_N + c, rd);
@@ -582,7 +587,7 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
     tc_fence_after();
     __nv_bfloat16* row = dqkv + (static_cast<int64_t>(b) * S + key) * (3 * Hd);
 #pragma unroll 1
-    for (int c = 0; c < D; c += 32) {
+    for (int c = chalf * 32; c < D; c += 64) {
       uint32_t rk[32], rv[32];
       tmem_ld32(tDK + trow + c, rk);
       tmem_ld32(tDV + trow + c, rv);
@@ -611,7 +616,7 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
 }
 
 template <int D, bool CAUSAL>
-__global__ void __launch_bounds__(TA_THREADS, 1)
+__global__ void __launch_bounds__(TB_THREADS, 1)
     attn_bwd_dq_tc(const __grid_constant__ CUtensorMap tmQKV128,
                    const __grid_constant__ CUtensorMap tmQKV64,
                    const __grid_constant__ CUtensorMap tmDO128, const float* __restrict__ lse,
@@ -652,8 +657,8 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 4);
-      mbar_init(&g_full[i], 4);
+      mbar_init(&s_empty[i], TB_CW);
+      mbar_init(&g_full[i], TB_CW);
       mbar_init(&g_empty[i], 1);
     }
     mbar_init(acc_full, 1);
@@ -732,6 +737,7 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
     }
   } else if (warp >= 4) {
     const uint32_t qd = warp & 3;
+    const int chalf = static_cast<int>(warp - 4) >> 2;
     const int r = qd * 32 + lane;
     const int q = q0 + r;
     const uint32_t trow = (qd * 32) << 16;
@@ -746,8 +752,8 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
       tc_fence_after();
       const bool need_mask = (kj + TB_N > S) || (CAUSAL && kj + TB_N - 1 > q0);
       const uint32_t rowG = smem_u32(smem + L::G_OFF + st * 128 * TB_N * 2 + r * 128);
-#pragma unroll
-      for (int c = 0; c < TB_N; c += 32) {
+      {
+        const int c = chalf * 32;
         uint32_t rs[32], rd[32];
         tmem_ld32(tS + trow + st * TB_N + c, rs);
         tmem_ld32(tP + trow + st * TB_N + c, rd);
@@ -778,7 +784,7 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
     tc_fence_after();
     __nv_bfloat16* row = dqkv + (static_cast<int64_t>(b) * S + q) * (3 * Hd) + h * D;
 #pragma unroll 1
-    for (int c = 0; c < D; c += 32) {
+    for (int c = chalf * 32; c < D; c += 64) {
       uint32_t rq[32];
       tmem_ld32(tDQ + trow + c, rq);
       tmem_ld_wait();
@@ -823,11 +829,11 @@ int bwd_tc_t(const void* qkv, const void* dout, const float* lse, const float* d
   const float scale = 1.f / sqrtf(static_cast<float>(D));
   const float scale_log2 = 1.4426950408889634f * scale;
   const int n_kb = static_cast<int>((S + TB_M - 1) / TB_M);
-  k1<<<dim3(n_kb, static_cast<unsigned>(B * H)), TA_THREADS, L::TOTAL, st>>>(
+  k1<<<dim3(n_kb, static_cast<unsigned>(B * H)), TB_THREADS, L::TOTAL, st>>>(
       q128, q64, do64, lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), static_cast<int>(S),
       static_cast<int>(H), scale_log2, scale);
   const int n_qb = static_cast<int>((S + TB_M - 1) / TB_M);
-  k2<<<dim3(n_qb, static_cast<unsigned>(B * H)), TA_THREADS, L::TOTAL, st>>>(
+  k2<<<dim3(n_qb, static_cast<unsigned>(B * H)), TB_THREADS, L::TOTAL, st>>>(
       q128, q64, do128, lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), static_cast<int>(S),
       static_cast<int>(H), n_qb, scale_log2, scale);
   return launch_status();
