@@ -76,6 +76,15 @@ __device__ __forceinline__ void sts128(uint32_t addr, const uint4& v) {
                : "memory");
 }
 
+// 1D bulk copy global -> shared, completion counted on an mbarrier (bytes % 16 == 0).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -459,9 +468,15 @@ __global__ void __launch_bounds__(TB_THREADS, 1)
       const int st = it % L::NS;
       const uint32_t ph = (it / L::NS) & 1;
       const int qi = (i0 + it) * TB_N;
+      // lse/delta rows of a full 64-query block arrive by bulk copy on the
+      // same barrier (no thread waits on global latency); a ragged last
+      // block is loaded by the warp.
+      const bool full_blk = qi + TB_N <= S && ((reinterpret_cast<uintptr_t>(lse_bh + qi) |
+                                                reinterpret_cast<uintptr_t>(del_bh + qi)) & 15) == 0;
+      float* dst = sv + st * 2 * TB_N;
       if (lane == 0) {
         mbar_wait(&q_empty[st], ph ^ 1);
-        mbar_expect_tx(&q_full[st], 2 * L::SMALL * L::CH);
+        mbar_expect_tx(&q_full[st], 2 * L::SMALL * L::CH + (full_blk ? 2 * TB_N * 4 : 0));
 #pragma unroll
         for (int c = 0; c < L::CH; ++c) {
           tma_load_3d(smem + L::X_OFF + st * L::SMALL * L::CH + c * L::SMALL, &tmQKV64,
@@ -469,17 +484,23 @@ __global__ void __launch_bounds__(TB_THREADS, 1)
           tma_load_3d(smem + L::Y_OFF + st * L::SMALL * L::CH + c * L::SMALL, &tmDO64,
                       &q_full[st], h * D + c * 64, qi, b);
         }
+        if (full_blk) {
+          bulk_g2s(dst, lse_bh + qi, TB_N * 4, &q_full[st]);
+          bulk_g2s(dst + TB_N, del_bh + qi, TB_N * 4, &q_full[st]);
+          mbar_arrive(&q_full[st]);
+        }
       }
-      __syncwarp();
-      mbar_wait(&q_empty[st], ph ^ 1);  // all lanes: stage free
-      float* dst = sv + st * 2 * TB_N;
-      for (int t = lane; t < TB_N; t += 32) {
-        const int q = qi + t;
-        dst[t] = q < S ? lse_bh[q] : 0.f;
-        dst[TB_N + t] = q < S ? del_bh[q] : 0.f;
+      if (!full_blk) {
+        __syncwarp();
+        mbar_wait(&q_empty[st], ph ^ 1);  // all lanes: stage free
+        for (int t = lane; t < TB_N; t += 32) {
+          const int q = qi + t;
+          dst[t] = q < S ? lse_bh[q] : 0.f;
+          dst[TB_N + t] = q < S ? del_bh[q] : 0.f;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&q_full[st]);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&q_full[st]);
     }
   } else if (warp == 1) {
     if (lane == 0) {
