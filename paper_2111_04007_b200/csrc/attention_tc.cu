@@ -578,18 +578,34 @@ __global__ void __launch_bounds__(TB_THREADS, 1)
         tmem_ld32(tS + trow + st * TB_N + c, rs);
         tmem_ld32(tP + trow + st * TB_N + c, rd);
         tmem_ld_wait();
+        // lse/delta for these 32 queries: broadcast 16-byte shared loads
+        float lq[32], dq[32];
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          const float4 a = *reinterpret_cast<const float4*>(slse + c + i);
+          const float4 d = *reinterpret_cast<const float4*>(sdel + c + i);
+          lq[i] = a.x; lq[i + 1] = a.y; lq[i + 2] = a.z; lq[i + 3] = a.w;
+          dq[i] = d.x; dq[i + 1] = d.y; dq[i + 2] = d.z; dq[i + 3] = d.w;
+        }
+        float pv[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          pv[i] = fast_exp2(fmaf(__uint_as_float(rs[i]), scale_log2, -lq[i]));
+        if (need_mask) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int qq = qi + c + i;
+            pv[i] = (qq >= qlo && qq < S) ? pv[i] : 0.f;
+          }
+        }
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           float fp[8], fg[8];
 #pragma unroll
           for (int t = 0; t < 8; ++t) {
             const int i = g * 8 + t;
-            const int qq = qi + c + i;
-            float pv = fast_exp2(fmaf(__uint_as_float(rs[i]), scale_log2, -slse[c + i]));
-            // valid queries for this key: qlo <= q < S (branch-free select)
-            pv = (!need_mask || (qq >= qlo && qq < S)) ? pv : 0.f;
-            fp[t] = pv;
-            fg[t] = pv * (__uint_as_float(rd[i]) - sdel[c + i]);
+            fp[t] = pv[i];
+            fg[t] = pv[i] * (__uint_as_float(rd[i]) - dq[i]);
           }
           const int chunk = (c >> 3) + g;
           const int sw = (chunk ^ (r & 7)) << 4;
@@ -779,16 +795,21 @@ __global__ void __launch_bounds__(TB_THREADS, 1)
         tmem_ld32(tS + trow + st * TB_N + c, rs);
         tmem_ld32(tP + trow + st * TB_N + c, rd);
         tmem_ld_wait();
+        float pv[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          pv[i] = fast_exp2(fmaf(__uint_as_float(rs[i]), scale_log2, -lrow));
+        if (need_mask) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) pv[i] = (kj + c + i < lim) ? pv[i] : 0.f;
+        }
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           float fg[8];
 #pragma unroll
           for (int t = 0; t < 8; ++t) {
             const int i = g * 8 + t;
-            const int kk = kj + c + i;
-            float pv = fast_exp2(fmaf(__uint_as_float(rs[i]), scale_log2, -lrow));
-            pv = (!need_mask || kk < lim) ? pv : 0.f;
-            fg[t] = pv * (__uint_as_float(rd[i]) - drow);
+            fg[t] = pv[i] * (__uint_as_float(rd[i]) - drow);
           }
           const int chunk = (c >> 3) + g;
           sts128(rowG + ((chunk ^ (r & 7)) << 4), pack8(fg));
