@@ -22,8 +22,11 @@ def t(fn, iters=10):
     return s.elapsed_time(e) / iters
 
 
-for B, S, H, D in [(8, 1024, 16, 64), (4, 1024, 20, 96), (4, 1024, 32, 96), (32, 512, 16, 64)]:
-    causal = S == 1024
+cases = [(8, 1024, 16, 64, True), (4, 1024, 20, 96, True), (4, 1024, 32, 96, True),
+         (32, 512, 16, 64, False)]
+if len(sys.argv) > 1 and sys.argv[1] == "long":
+    cases = [(2, 4096, 16, 64, False), (2, 4096, 16, 64, True), (8, 1024, 16, 64, False)]
+for B, S, H, D, causal in cases:
     qkv = torch.randn(B * S, 3 * H * D, device="cuda").bfloat16()
     o = torch.empty(B * S, H * D, device="cuda", dtype=torch.bfloat16)
     lse = torch.empty(B * H * S, device="cuda")

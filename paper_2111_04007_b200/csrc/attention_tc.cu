@@ -66,6 +66,15 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32
       "r"(v[29]), "r"(v[30]), "r"(v[31])
       : "memory");
 }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_st_wait() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
@@ -379,7 +388,12 @@ constexpr int TB_THREADS = 128 + 32 * TB_CW;
 
 template <int D>
 struct TbSmem {
-  static constexpr int NS = D <= 64 ? 4 : 3;   // stages of the streamed 64-row operands
+  // D <= 64: 2 CTAs/SM (one S/dP/P buffer, 2 stages, 256 TMEM cols, < 113 KB
+  // smem) so one CTA's prologue / final drain overlaps the other's loop.
+  // D > 64: 1 CTA/SM with double buffers and 3 stages.
+  static constexpr int NB = D <= 64 ? 1 : 2;   // S/dP (TMEM) and P/dS (smem) buffers
+  static constexpr int NS = D <= 64 ? 2 : 3;   // stages of the streamed 64-row operands
+  static constexpr int MINB = D <= 64 ? 2 : 1; // CTAs per SM
   static constexpr int CH = (D + 63) / 64;
   static constexpr int BIG = 128 * 128;   // one d-chunk of a 128-row tile
   static constexpr int SMALL = TB_N * 128;  // one d-chunk of a 64-row tile
@@ -387,15 +401,17 @@ struct TbSmem {
   static constexpr int B_OFF = A_OFF + BIG * CH;          // V (dkdv) / dO (dq)  [128 x D]
   static constexpr int X_OFF = B_OFF + BIG * CH;          // Q_i / K_j  [NS][64 x D]
   static constexpr int Y_OFF = X_OFF + NS * SMALL * CH;   // dO_i / V_j [NS][64 x D]
-  static constexpr int P_OFF = Y_OFF + NS * SMALL * CH;   // P^T [2][128 x 64] (dkdv only)
-  static constexpr int G_OFF = P_OFF + 2 * 128 * TB_N * 2;  // dS / dS^T [2][128 x 64]
-  static constexpr int V_OFF = G_OFF + 2 * 128 * TB_N * 2;  // lse/delta [NS][2][64] f32
+  static constexpr int P_OFF = Y_OFF + NS * SMALL * CH;   // P^T [NB][128 x 64] (dkdv only)
+  static constexpr int G_OFF = P_OFF + NB * 128 * TB_N * 2;  // dS / dS^T [NB][128 x 64]
+  static constexpr int V_OFF = G_OFF + NB * 128 * TB_N * 2;  // lse/delta [NS][2][64] f32
   static constexpr int BAR_OFF = V_OFF + NS * 2 * TB_N * 4;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+  static constexpr int TMEM_KV = NB * 128 + 2 * D <= 256 ? 256 : 512;  // dkdv allocation
+  static constexpr int TMEM_Q = NB * 128 + D <= 256 ? 256 : 512;       // dq allocation
 };
 
 template <int D, bool CAUSAL>
-__global__ void __launch_bounds__(TB_THREADS, 1)
+__global__ void __launch_bounds__(TB_THREADS, TbSmem<D>::MINB)
     attn_bwd_dkdv_tc(const __grid_constant__ CUtensorMap tmQKV128,
                      const __grid_constant__ CUtensorMap tmQKV64,
                      const __grid_constant__ CUtensorMap tmDO64, const float* __restrict__ lse,
@@ -446,12 +462,13 @@ __global__ void __launch_bounds__(TB_THREADS, 1)
     mbar_init(acc_full, 1);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  if (warp == 2) tmem_alloc(tmem_slot, L::TMEM_KV);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS = tmem, tP = tmem + 128, tDV = tmem + 256, tDK = tmem + 256 + D;
+  constexpr int NB = L::NB;
+  const uint32_t tS = tmem, tP = tmem + NB * 64, tDV = tmem + NB * 128, tDK = tmem + NB * 128 + D;
 
   if (warp == 0) {
     // ===== producer: K/V once; per query block Q_i, dO_i (TMA) + lse/delta (warp) =====
@@ -510,9 +527,9 @@ __global__ void __launch_bounds__(TB_THREADS, 1)
       const uint32_t sK = smem_u32(smem + L::A_OFF), sV = smem_u32(smem + L::B_OFF);
       mbar_wait(kv_full, 0);
       auto issue_grad = [&](int it) {
-        const int st = it & 1;
+        const int st = it % NB;
         const int qs = it % L::NS;
-        mbar_wait(&p_full[st], (it >> 1) & 1);
+        mbar_wait(&p_full[st], (it / NB) & 1);
         tc_fence_after();
         const uint32_t sQ = smem_u32(smem + L::X_OFF + qs * L::SMALL * L::CH);
         const uint32_t sdO = smem_u32(smem + L::Y_OFF + qs * L::SMALL * L::CH);
@@ -530,10 +547,10 @@ __global__ void __launch_bounds__(TB_THREADS, 1)
         umma_commit(&q_empty[qs]);
       };
       for (int it = 0; it < n_it; ++it) {
-        const int st = it & 1;
+        const int st = it % NB;
         const int qs = it % L::NS;
         mbar_wait(&q_full[qs], (it / L::NS) & 1);
-        mbar_wait(&st_empty[st], ((it >> 1) & 1) ^ 1);
+        mbar_wait(&st_empty[st], ((it / NB) & 1) ^ 1);
         tc_fence_after();
         const uint32_t sQ = smem_u32(smem + L::X_OFF + qs * L::SMALL * L::CH);
         const uint32_t sdO = smem_u32(smem + L::Y_OFF + qs * L::SMALL * L::CH);
@@ -561,10 +578,10 @@ __global__ void __launch_bounds__(TB_THREADS, 1)
     const int qlo = CAUSAL ? key : 0;
     const uint32_t trow = (qd * 32) << 16;
     for (int it = 0; it < n_it; ++it) {
-      const int st = it & 1;
+      const int st = it % NB;
       const int qi = (i0 + it) * TB_N;
-      mbar_wait(&st_full[st], (it >> 1) & 1);
-      mbar_wait(&p_empty[st], ((it >> 1) & 1) ^ 1);
+      mbar_wait(&st_full[st], (it / NB) & 1);
+      mbar_wait(&p_empty[st], ((it / NB) & 1) ^ 1);
       mbar_wait(&q_full[it % L::NS], (it / L::NS) & 1);  // lse/delta of this stage
       tc_fence_after();
       const float* slse = sv + (it % L::NS) * 2 * TB_N;
@@ -572,40 +589,36 @@ __global__ void __launch_bounds__(TB_THREADS, 1)
       const bool need_mask = (qi + TB_N > S) || (CAUSAL && qi < k0 + TB_M - 1);
       const uint32_t rowP = smem_u32(smem + L::P_OFF + st * 128 * TB_N * 2 + r * 128);
       const uint32_t rowG = smem_u32(smem + L::G_OFF + st * 128 * TB_N * 2 + r * 128);
-      {
-        const int c = chalf * 32;
-        uint32_t rs[32], rd[32];
-        tmem_ld32(tS + trow + st * TB_N + c, rs);
-        tmem_ld32(tP + trow + st * TB_N + c, rd);
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        // 16 queries at a time (keeps the register footprint small enough
+        // for 2 CTAs/SM)
+        const int c = chalf * 32 + hh * 16;
+        uint32_t rs[16], rd[16];
+        tmem_ld16(tS + trow + st * TB_N + c, rs);
+        tmem_ld16(tP + trow + st * TB_N + c, rd);
         tmem_ld_wait();
-        // lse/delta for these 32 queries: broadcast 16-byte shared loads
-        float lq[32], dq[32];
 #pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          const float4 a = *reinterpret_cast<const float4*>(slse + c + i);
-          const float4 d = *reinterpret_cast<const float4*>(sdel + c + i);
-          lq[i] = a.x; lq[i + 1] = a.y; lq[i + 2] = a.z; lq[i + 3] = a.w;
-          dq[i] = d.x; dq[i + 1] = d.y; dq[i + 2] = d.z; dq[i + 3] = d.w;
-        }
-        float pv[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          pv[i] = fast_exp2(fmaf(__uint_as_float(rs[i]), scale_log2, -lq[i]));
-        if (need_mask) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int qq = qi + c + i;
-            pv[i] = (qq >= qlo && qq < S) ? pv[i] : 0.f;
-          }
-        }
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          float fp[8], fg[8];
+        for (int g = 0; g < 2; ++g) {
+          float lq[8], dq[8], fp[8], fg[8];
+          const float4 a0 = *reinterpret_cast<const float4*>(slse + c + g * 8);
+          const float4 a1 = *reinterpret_cast<const float4*>(slse + c + g * 8 + 4);
+          const float4 d0 = *reinterpret_cast<const float4*>(sdel + c + g * 8);
+          const float4 d1 = *reinterpret_cast<const float4*>(sdel + c + g * 8 + 4);
+          lq[0] = a0.x; lq[1] = a0.y; lq[2] = a0.z; lq[3] = a0.w;
+          lq[4] = a1.x; lq[5] = a1.y; lq[6] = a1.z; lq[7] = a1.w;
+          dq[0] = d0.x; dq[1] = d0.y; dq[2] = d0.z; dq[3] = d0.w;
+          dq[4] = d1.x; dq[5] = d1.y; dq[6] = d1.z; dq[7] = d1.w;
 #pragma unroll
           for (int t = 0; t < 8; ++t) {
             const int i = g * 8 + t;
-            fp[t] = pv[i];
-            fg[t] = pv[i] * (__uint_as_float(rd[i]) - dq[i]);
+            float pv = fast_exp2(fmaf(__uint_as_float(rs[i]), scale_log2, -lq[t]));
+            if (need_mask) {
+              const int qq = qi + c + i;
+              pv = (qq >= qlo && qq < S) ? pv : 0.f;
+            }
+            fp[t] = pv;
+            fg[t] = pv * (__uint_as_float(rd[i]) - dq[t]);
           }
           const int chunk = (c >> 3) + g;
           const int sw = (chunk ^ (r & 7)) << 4;
@@ -648,12 +661,12 @@ __global__ void __launch_bounds__(TB_THREADS, 1)
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem, 512);
+    tmem_dealloc(tmem, L::TMEM_KV);
   }
 }
 
 template <int D, bool CAUSAL>
-__global__ void __launch_bounds__(TB_THREADS, 1)
+__global__ void __launch_bounds__(TB_THREADS, TbSmem<D>::MINB)
     attn_bwd_dq_tc(const __grid_constant__ CUtensorMap tmQKV128,
                    const __grid_constant__ CUtensorMap tmQKV64,
                    const __grid_constant__ CUtensorMap tmDO128, const float* __restrict__ lse,
@@ -701,12 +714,13 @@ __global__ void __launch_bounds__(TB_THREADS, 1)
     mbar_init(acc_full, 1);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  if (warp == 2) tmem_alloc(tmem_slot, L::TMEM_Q);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS = tmem, tP = tmem + 128, tDQ = tmem + 256;
+  constexpr int NB = L::NB;
+  const uint32_t tS = tmem, tP = tmem + NB * 64, tDQ = tmem + NB * 128;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -736,9 +750,9 @@ __global__ void __launch_bounds__(TB_THREADS, 1)
       const uint32_t sQ = smem_u32(smem + L::A_OFF), sdO = smem_u32(smem + L::B_OFF);
       mbar_wait(a_full, 0);
       auto issue_dq = [&](int j) {
-        const int st = j & 1;
+        const int st = j % NB;
         const int ks = j % L::NS;
-        mbar_wait(&g_full[st], (j >> 1) & 1);
+        mbar_wait(&g_full[st], (j / NB) & 1);
         tc_fence_after();
         const uint32_t sK = smem_u32(smem + L::X_OFF + ks * L::SMALL * L::CH);
         const uint32_t sdS = smem_u32(smem + L::G_OFF + st * 128 * TB_N * 2);
@@ -750,10 +764,10 @@ __global__ void __launch_bounds__(TB_THREADS, 1)
         umma_commit(&k_empty[ks]);
       };
       for (int j = 0; j < n_kb; ++j) {
-        const int st = j & 1;
+        const int st = j % NB;
         const int ks = j % L::NS;
         mbar_wait(&k_full[ks], (j / L::NS) & 1);
-        mbar_wait(&s_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_wait(&s_empty[st], ((j / NB) & 1) ^ 1);
         tc_fence_after();
         const uint32_t sK = smem_u32(smem + L::X_OFF + ks * L::SMALL * L::CH);
         const uint32_t sV = smem_u32(smem + L::Y_OFF + ks * L::SMALL * L::CH);
@@ -782,10 +796,10 @@ __global__ void __launch_bounds__(TB_THREADS, 1)
     const float lrow = q < S ? lse[static_cast<int64_t>(bh) * S + q] : 0.f;
     const float drow = q < S ? delta[static_cast<int64_t>(bh) * S + q] : 0.f;
     for (int j = 0; j < n_kb; ++j) {
-      const int st = j & 1;
+      const int st = j % NB;
       const int kj = j * TB_N;
-      mbar_wait(&s_full[st], (j >> 1) & 1);
-      mbar_wait(&g_empty[st], ((j >> 1) & 1) ^ 1);
+      mbar_wait(&s_full[st], (j / NB) & 1);
+      mbar_wait(&g_empty[st], ((j / NB) & 1) ^ 1);
       tc_fence_after();
       const bool need_mask = (kj + TB_N > S) || (CAUSAL && kj + TB_N - 1 > q0);
       const uint32_t rowG = smem_u32(smem + L::G_OFF + st * 128 * TB_N * 2 + r * 128);
@@ -845,7 +859,7 @@ __global__ void __launch_bounds__(TB_THREADS, 1)
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem, 512);
+    tmem_dealloc(tmem, L::TMEM_Q);
   }
 }
 
