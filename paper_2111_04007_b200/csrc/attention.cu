@@ -252,25 +252,38 @@ __global__ void __launch_bounds__(ATT_THREADS)
 }
 
 // ============================================================== backward
+// delta[b,h,s] = sum_d dO * O. One row (token, head) per group of D/8 lanes,
+// each lane one 16-byte vector of O and of dO: a warp reads contiguous
+// 512-byte spans; shuffle reduction inside the group.
 template <int D>
-__global__ void attn_delta_kernel(const __nv_bfloat16* __restrict__ o,
-                                  const __nv_bfloat16* __restrict__ dout,
-                                  float* __restrict__ delta, int64_t tokens, int S, int H) {
-  // one warp per (token, head)
-  const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+__global__ void __launch_bounds__(256) attn_delta_kernel(const __nv_bfloat16* __restrict__ o,
+                                                         const __nv_bfloat16* __restrict__ dout,
+                                                         float* __restrict__ delta, int64_t tokens,
+                                                         int S, int H) {
+  constexpr int G = D / 8;  // lanes per row: 8 (D=64), 12 (D=96: 32 lanes hold 2 rows + 8 idle)
+  constexpr int RPW = 32 / G;
   const int lane = threadIdx.x & 31;
-  if (gw >= tokens * H) return;
-  const int64_t t = gw / H;
-  const int h = static_cast<int>(gw % H);
-  const int64_t off = t * H * D + h * D;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int sub = lane / G, li = lane % G;
+  const int64_t row = warp * RPW + sub;  // row = token * H + head
   float acc = 0.f;
-  for (int d = lane * 2; d < D; d += 64) {
-    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(o + off + d));
-    const float2 g = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dout + off + d));
-    acc += a.x * g.x + a.y * g.y;
+  const bool ok = sub < RPW && row < tokens * H;
+  if (ok) {
+    const int64_t off = row * D + li * 8;  // rows are contiguous: [T, H*D]
+    float a[8], g[8];
+    unpack8(*reinterpret_cast<const uint4*>(o + off), a);
+    unpack8(*reinterpret_cast<const uint4*>(dout + off), g);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc += a[j] * g[j];
   }
-  acc = warp_sum(acc);
-  if (lane == 0) {
+  // group sum in fixed lane order (G need not be a power of two)
+  float tot = 0.f;
+#pragma unroll
+  for (int k = 0; k < G; ++k) tot += __shfl_sync(0xffffffffu, acc, (sub * G + k) & 31);
+  acc = tot;
+  if (ok && li == 0) {
+    const int64_t t = row / H;
+    const int h = static_cast<int>(row % H);
     const int64_t b = t / S, s = t % S;
     delta[(b * H + h) * S + s] = acc;
   }
@@ -555,7 +568,8 @@ template <int D, bool CAUSAL>
 int bwd_t(const void* qkv, const void* o, const void* dout, const float* lse, void* dqkv,
           float* delta, int64_t B, int64_t S, int64_t H, cudaStream_t st) {
   const int64_t tokens = B * S;
-  const int64_t warps = tokens * H;
+  constexpr int RPW = 32 / (D / 8);
+  const int64_t warps = (tokens * H + RPW - 1) / RPW;
   attn_delta_kernel<D><<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, st>>>(
       reinterpret_cast<const __nv_bfloat16*>(o), reinterpret_cast<const __nv_bfloat16*>(dout),
       delta, tokens, static_cast<int>(S), static_cast<int>(H));
