@@ -838,15 +838,17 @@ static int gemm_entry(int a_kmajor, int b_kmajor, int epilogue, const void* A, i
     const int64_t tiles = ((M + 255) / 256) * ((N + 255) / 256);
     const int64_t clusters = sm_count() / 2;
     if (epilogue == VP_EPI_ACC_F32 && tiles < clusters) {
-      // choose the split with the best wave efficiency (ties -> smaller split),
-      // keeping >= 4 k-blocks per split
+      // Smallest split reaching (near-)best wave efficiency; every split adds
+      // one fp32 reduce-add pass over the output, and each split keeps >= 16
+      // k-blocks (1024 of K) so the mainloop amortises the tile prologue.
       const int64_t n_kb = (K + BK - 1) / BK;
-      double best = 0.0;
-      for (int64_t sp = 1; sp <= std::max<int64_t>(1, n_kb / 4) && sp <= 16; ++sp) {
+      double best = double(tiles) / double(clusters);
+      const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(8, n_kb / 16));
+      for (int64_t sp = 2; sp <= smax; ++sp) {
         const int64_t units = tiles * sp;
         const int64_t rounds = (units + clusters - 1) / clusters;
         const double eff = double(units) / double(rounds * clusters);
-        if (eff >= best - 0.02) {  // ties -> the larger split (shorter units)
+        if (eff > best + 0.05) {
           best = eff;
           split = static_cast<int>(sp);
         }

@@ -246,23 +246,30 @@ __global__ void __launch_bounds__(kWarps * 32)
   }
 }
 
-// 32 columns x 8 part-lanes per block; fixed-order tree => deterministic.
-__global__ void __launch_bounds__(256) ln_param_reduce(const float* __restrict__ ws,
-                                                       float* __restrict__ dgamma,
-                                                       float* __restrict__ dbeta, int parts,
-                                                       int cols) {
-  __shared__ float sh[8][33];
+// 32 columns x 32 part-lanes per block, 8 independent loads in flight per
+// thread; fixed-order tree => deterministic.
+__global__ void __launch_bounds__(1024) ln_param_reduce(const float* __restrict__ ws,
+                                                        float* __restrict__ dgamma,
+                                                        float* __restrict__ dbeta, int parts,
+                                                        int cols) {
+  __shared__ float sh[32][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + tx;
-  float acc = 0.f;
-  if (c < 2 * cols)
-    for (int p = ty; p < parts; p += 8) acc += ws[static_cast<int64_t>(p) * 2 * cols + c];
-  sh[ty][tx] = acc;
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (c < 2 * cols) {
+    int p = ty;
+    for (; p + 7 * 32 < parts; p += 8 * 32) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[u] += ws[static_cast<int64_t>(p + u * 32) * 2 * cols + c];
+    }
+    for (; p < parts; p += 32) acc[0] += ws[static_cast<int64_t>(p) * 2 * cols + c];
+  }
+  sh[ty][tx] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
   __syncthreads();
   if (ty == 0 && c < 2 * cols) {
     float t = 0.f;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) t += sh[i][tx];
+    for (int i = 0; i < 32; ++i) t += sh[i][tx];
     if (c < cols) dgamma[c] += t;
     else dbeta[c - cols] += t;
   }
@@ -271,9 +278,11 @@ __global__ void __launch_bounds__(256) ln_param_reduce(const float* __restrict__
 }  // namespace
 
 int ln_partials(int64_t rows) {
-  // Enough CTAs to fill the chip twice; each covers a contiguous row range.
-  int64_t parts = 296;
-  if (rows < parts * kWarps) parts = (rows + kWarps - 1) / kWarps;
+  // ~2 rows per warp so many rows are in flight (the kernel is latency
+  // bound otherwise); each CTA covers a contiguous row range and writes one
+  // dgamma/dbeta partial.
+  int64_t parts = (rows + 2 * kWarps - 1) / (2 * kWarps);
+  if (parts > 1024) parts = 1024;
   return static_cast<int>(parts < 1 ? 1 : parts);
 }
 
@@ -340,7 +349,7 @@ extern "C" int vp_layernorm_bwd(const void* dy, const void* x, const void* gamma
         rpc);
   });
   const int c2 = static_cast<int>(2 * cols);
-  ln_param_reduce<<<(c2 + 31) / 32, 256, 0, st>>>(workspace, dgamma, dbeta, parts,
-                                                  static_cast<int>(cols));
+  ln_param_reduce<<<(c2 + 31) / 32, 1024, 0, st>>>(workspace, dgamma, dbeta, parts,
+                                                   static_cast<int>(cols));
   return launch_status();
 }

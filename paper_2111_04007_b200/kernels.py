@@ -137,7 +137,7 @@ def layernorm_fwd(x, gamma, beta, y, mean, rstd, eps=1e-5, stream=None):
 
 
 def layernorm_ws_elems(cols: int) -> int:
-    return 2 * 296 * cols
+    return 2 * 1024 * cols
 
 
 def layernorm_bwd(dy, x, gamma, mean, rstd, dx, dgamma, dbeta, workspace, accumulate=False,
