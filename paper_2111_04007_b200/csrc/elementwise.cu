@@ -369,15 +369,16 @@ extern "C" int vp_xent_fwd_bwd(void* logits, const int64_t* labels, float* loss_
   return launch_status();
 }
 
-// workspace >= 64 * cols floats.
+// workspace >= 256 * cols floats.
 extern "C" int vp_bias_grad(const void* dy, float* dbias, int64_t rows, int64_t cols,
                             float* workspace, void* stream) {
   if (rows <= 0 || cols <= 0 || !workspace) return VP_ERR_ARGS;
   if (cols % 8) return VP_ERR_UNSUPPORTED;
   const int64_t col_blocks = (cols + 255) / 256;
   // ~4 waves of 148 SMs worth of blocks
-  int parts = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(64, 592 / col_blocks)));
-  parts = static_cast<int>(std::min<int64_t>(parts, rows));
+  // ~32 rows per partition (4 per row-lane): enough CTAs in flight to cover
+  // HBM latency; partials stay small (parts x cols fp32)
+  int parts = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(256, (rows + 31) / 32)));
   const int64_t rpp = (rows + parts - 1) / parts;
   dim3 grid(static_cast<unsigned>(col_blocks), parts);
   colsum_partial<<<grid, 256, 0, ST>>>(CBF(dy), workspace, rows, cols, rpp);

@@ -246,6 +246,119 @@ __global__ void __launch_bounds__(kWarps * 32)
   }
 }
 
+
+// dx only (no parameter gradients): one warp per row, row in registers,
+// low register count -> full occupancy. Used with ln_param_partial below.
+template <int NV>
+__global__ void __launch_bounds__(kWarps * 32)
+    ln_bwd_dx_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+                     const __nv_bfloat16* __restrict__ g, const float* __restrict__ mean,
+                     const float* __restrict__ rstd, __nv_bfloat16* __restrict__ dx, int64_t rows,
+                     int cols, int accumulate) {
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * kWarps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const int nvec = cols >> 3;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + row * cols);
+  const uint4* dyr = reinterpret_cast<const uint4*>(dy + row * cols);
+  uint4* dxr = reinterpret_cast<uint4*>(dx + row * cols);
+  const uint4* gv = reinterpret_cast<const uint4*>(g);
+  const float mu = mean[row], rs = rstd[row];
+  uint4 xu[NV], du[NV], pu[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = lane + i * 32;
+    if (c < nvec) {
+      xu[i] = xr[c];
+      du[i] = dyr[c];
+      if (accumulate) pu[i] = dxr[c];
+    }
+  }
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = lane + i * 32;
+    if (c < nvec) {
+      float xv[8], dv[8], gg[8];
+      unpack8(xu[i], xv);
+      unpack8(du[i], dv);
+      unpack8(gv[c], gg);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float gy = dv[j] * gg[j];
+        s1 += gy;
+        s2 += gy * (xv[j] - mu) * rs;
+      }
+    }
+  }
+  const float m1 = warp_sum(s1) / cols, m2 = warp_sum(s2) / cols;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = lane + i * 32;
+    if (c < nvec) {
+      float xv[8], dv[8], gg[8], o[8];
+      unpack8(xu[i], xv);
+      unpack8(du[i], dv);
+      unpack8(gv[c], gg);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = rs * (dv[j] * gg[j] - m1 - (xv[j] - mu) * rs * m2);
+      if (accumulate) {
+        float p[8];
+        unpack8(pu[i], p);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] += p[j];
+      }
+      dxr[c] = pack8(o);
+    }
+  }
+}
+
+// dgamma/dbeta partial column sums: block = 32 column-groups (8 columns,
+// 16-byte loads) x 8 row-lanes over a row range; ws[part][2*cols].
+__global__ void __launch_bounds__(256) ln_param_partial(const __nv_bfloat16* __restrict__ dy,
+                                                        const __nv_bfloat16* __restrict__ x,
+                                                        const float* __restrict__ mean,
+                                                        const float* __restrict__ rstd,
+                                                        float* __restrict__ ws, int64_t rows,
+                                                        int cols, int64_t rows_per_part) {
+  __shared__ float sh[8][2][256 + 4];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t c0 = (static_cast<int64_t>(blockIdx.x) * 32 + tx) * 8;
+  const int64_t r0 = blockIdx.y * rows_per_part;
+  const int64_t r1 = min(rows, r0 + rows_per_part);
+  float ag[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  float ab[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (c0 < cols) {
+#pragma unroll 2
+    for (int64_t r = r0 + ty; r < r1; r += 8) {
+      float xv[8], dv[8];
+      unpack8(*reinterpret_cast<const uint4*>(x + r * cols + c0), xv);
+      unpack8(*reinterpret_cast<const uint4*>(dy + r * cols + c0), dv);
+      const float mu = mean[r], rs = rstd[r];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        ag[j] += dv[j] * (xv[j] - mu) * rs;
+        ab[j] += dv[j];
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    sh[ty][0][tx * 8 + j] = ag[j];
+    sh[ty][1][tx * 8 + j] = ab[j];
+  }
+  __syncthreads();
+  const int64_t cb = static_cast<int64_t>(blockIdx.x) * 256;
+  for (int i = threadIdx.x; i < 512; i += 256) {
+    const int half = i >> 8, cc = i & 255;
+    if (cb + cc >= cols) continue;
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += sh[k][half][cc];
+    ws[static_cast<int64_t>(blockIdx.y) * 2 * cols + half * cols + cb + cc] = t;
+  }
+}
+
 // 32 columns x 32 part-lanes per block, 8 independent loads in flight per
 // thread; fixed-order tree => deterministic.
 __global__ void __launch_bounds__(1024) ln_param_reduce(const float* __restrict__ ws,
@@ -278,10 +391,9 @@ __global__ void __launch_bounds__(1024) ln_param_reduce(const float* __restrict_
 }  // namespace
 
 int ln_partials(int64_t rows) {
-  // ~2 rows per warp so many rows are in flight (the kernel is latency
-  // bound otherwise); each CTA covers a contiguous row range and writes one
-  // dgamma/dbeta partial.
-  int64_t parts = (rows + 2 * kWarps - 1) / (2 * kWarps);
+  // row partitions of the dgamma/dbeta column reduction: ~32 rows each
+  // (4 per row-lane), at most 1024 partials.
+  int64_t parts = (rows + 31) / 32;
   if (parts > 1024) parts = 1024;
   return static_cast<int>(parts < 1 ? 1 : parts);
 }
@@ -333,21 +445,19 @@ extern "C" int vp_layernorm_bwd(const void* dy, const void* x, const void* gamma
                                 float* workspace, void* stream) {
   if (rows <= 0 || cols <= 0 || (cols % 8) || !workspace) return VP_ERR_ARGS;
   const int nv = pick_nv(cols);
-  const int parts = ln_partials(rows);
-  const int rpc = static_cast<int>((rows + parts - 1) / parts);
-  const size_t smem = static_cast<size_t>(kWarps) * 2 * cols * sizeof(float);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  LN_DISPATCH(nv, {
-    auto k = ln_bwd_kernel<NV>;
-    if constexpr (NV <= 4) k = ln_bwd_reg_kernel<NV>;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               static_cast<int>(smem));
-    k<<<parts, kWarps * 32, smem, st>>>(
-        reinterpret_cast<const __nv_bfloat16*>(dy), reinterpret_cast<const __nv_bfloat16*>(x),
-        reinterpret_cast<const __nv_bfloat16*>(gamma), mean, rstd,
-        reinterpret_cast<__nv_bfloat16*>(dx), workspace, rows, static_cast<int>(cols), accumulate,
-        rpc);
-  });
+  LN_DISPATCH(nv, ln_bwd_dx_kernel<NV><<<static_cast<unsigned>((rows + kWarps - 1) / kWarps),
+                                         kWarps * 32, 0, st>>>(
+                      reinterpret_cast<const __nv_bfloat16*>(dy),
+                      reinterpret_cast<const __nv_bfloat16*>(x),
+                      reinterpret_cast<const __nv_bfloat16*>(gamma), mean, rstd,
+                      reinterpret_cast<__nv_bfloat16*>(dx), rows, static_cast<int>(cols),
+                      accumulate));
+  const int parts = ln_partials(rows);
+  const int64_t rpp = (rows + parts - 1) / parts;
+  ln_param_partial<<<dim3(static_cast<unsigned>((cols + 255) / 256), parts), 256, 0, st>>>(
+      reinterpret_cast<const __nv_bfloat16*>(dy), reinterpret_cast<const __nv_bfloat16*>(x), mean,
+      rstd, workspace, rows, static_cast<int>(cols), rpp);
   const int c2 = static_cast<int>(2 * cols);
   ln_param_reduce<<<(c2 + 31) / 32, 1024, 0, st>>>(workspace, dgamma, dbeta, parts,
                                                    static_cast<int>(cols));

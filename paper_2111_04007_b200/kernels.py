@@ -143,7 +143,7 @@ def layernorm_ws_elems(cols: int) -> int:
 def layernorm_bwd(dy, x, gamma, mean, rstd, dx, dgamma, dbeta, workspace, accumulate=False,
                   stream=None):
     rows, cols = x.shape
-    _count(2)
+    _count(3)
     check(L.vp_layernorm_bwd(dy.data_ptr(), x.data_ptr(), gamma.data_ptr(), mean.data_ptr(),
                              rstd.data_ptr(), dx.data_ptr(), dgamma.data_ptr(), dbeta.data_ptr(),
                              rows, cols, int(accumulate), workspace.data_ptr(), _stream(stream)),
@@ -189,7 +189,7 @@ def xent_fwd_bwd(logits, labels, loss_rows, scale, loss_sum=None, stream=None):
 
 
 def bias_grad_ws_elems(cols: int) -> int:
-    return 64 * cols
+    return 256 * cols
 
 
 def bias_grad(dy, dbias, workspace, stream=None):
