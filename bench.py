@@ -36,6 +36,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 LADDER = {1: (1, 1), 2: (2, 1), 4: (4, 1), 8: (4, 2)}
+METRIC_NAMES = {"gpt2_355m": "GPT-2 355M", "gpt2_2_5b": "GPT-2 2.5B", "gpt2_8_3b": "GPT-2 8.3B",
+                "tiny": "tiny GPT-2", "bert_large": "BERT-large"}
 MODEL_CONFIGS = {  # name: (M_total, m)
     "gpt2_355m": (512, 8),
     "gpt2_2_5b": (256, 4),
@@ -192,7 +194,8 @@ def run_reference(args):
         if i >= args.warmup:
             vals.append(v)
     value = statistics.median(vals)
-    line = {"metric": "samples/sec (GPT-2 355M Varuna pipeline step)", "value": round(value, 4),
+    line = {"metric": f"samples/sec ({METRIC_NAMES[args.config]} Varuna pipeline step)",
+            "value": round(value, 4),
             "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(M / value * 1e3, 1), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
@@ -355,7 +358,7 @@ def main():
                    "sample": f"failed: {ex}"}
     if rank == 0:
         line = {
-            "metric": "samples/sec (GPT-2 355M Varuna pipeline step)",
+            "metric": f"samples/sec ({METRIC_NAMES[args.config]} Varuna pipeline step)",
             "value": round(value, 3), "unit": "samples/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 2), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16",

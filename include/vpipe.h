@@ -113,6 +113,7 @@ int vp_device_sm_count(int* out);
 #define VP_EPI_DGELU 4
 #define VP_EPI_ACC_F32 5
 #define VP_EPI_STORE_F32 6
+#define VP_EPI_RESID 7   /* D = aux + acc (bias-free residual add) */
 int vp_gemm_bf16(int a_kmajor, int b_kmajor, int epilogue, const void* A, int64_t lda,
                  const void* B, int64_t ldb, void* D, int64_t ldd, const void* bias, void* aux,
                  int64_t ldaux, int64_t M, int64_t N, int64_t K, void* stream);
@@ -148,6 +149,17 @@ int vp_embed_fwd(const int64_t* ids, const void* wte, const void* wpe, void* x, 
 /* dwte[V,h] += scatter(dx), dwpe[S,h] += sum over batch (fp32 accumulators). */
 int vp_embed_bwd(const int64_t* ids, const void* dx, float* dwte, float* dwpe, int64_t batch,
                  int64_t seq, int64_t hidden, void* stream);
+
+/* BERT-style embedding with token types: x = wte[ids] + wpe[pos] + tte[types]. */
+int vp_embed_typed_fwd(const int64_t* ids, const int64_t* types, const void* wte, const void* wpe,
+                       const void* tte, void* x, int64_t batch, int64_t seq, int64_t hidden,
+                       void* stream);
+/* dwte/dtte scatter-add (fp32), dwpe sum over batch. */
+int vp_embed_typed_bwd(const int64_t* ids, const int64_t* types, const void* dx, float* dwte,
+                       float* dwpe, float* dtte, int64_t batch, int64_t seq, int64_t hidden,
+                       void* stream);
+/* dx = dy * gelu'(pre) elementwise (bf16), n elements. */
+int vp_gelu_bwd(const void* dy, const void* pre, void* dx, int64_t n, void* stream);
 
 /* Softmax cross-entropy over logits[T,V] (bf16). Writes per-row loss (fp32),
  * adds sum(row_loss)*scale into *loss_sum (optional), and overwrites logits

@@ -35,7 +35,7 @@ def _round(t):
     return t.to(torch.bfloat16).to(torch.float32)
 
 
-def init_params(n_layer, hidden, vocab, seq, seed=0, init_std=0.02):
+def init_params(n_layer, hidden, vocab, seq, seed=0, init_std=0.02, arch="gpt2", type_vocab=2):
     """Same generator streams as the product's per-layer init (seeded by
     (seed, layer)); returns fp32 tensors rounded to bf16."""
     h = hidden
@@ -44,6 +44,10 @@ def init_params(n_layer, hidden, vocab, seq, seed=0, init_std=0.02):
     g.manual_seed(seed * 1000003)
     out["wte"] = _round(torch.randn((vocab, h), generator=g) * init_std)
     out["wpe"] = _round(torch.randn((seq, h), generator=g) * 0.01)
+    if arch == "bert":
+        out["tte"] = _round(torch.randn((type_vocab, h), generator=g) * init_std)
+        out["lne_g"] = torch.ones(h)
+        out["lne_b"] = torch.zeros(h)
     proj = init_std / math.sqrt(2 * n_layer)
     shapes = [("ln1_g", (h,)), ("ln1_b", (h,)), ("w_qkv", (3 * h, h)), ("b_qkv", (3 * h,)),
               ("w_o", (h, h)), ("b_o", (h,)), ("ln2_g", (h,)), ("ln2_b", (h,)),
@@ -60,13 +64,38 @@ def init_params(n_layer, hidden, vocab, seq, seed=0, init_std=0.02):
                 std = proj if name in ("w_o", "w_fc2") else init_std
                 v = torch.randn(shape, generator=g) * std
             out[f"l{li}.{name}"] = _round(v)
-    out["lnf_g"] = torch.ones(h)
-    out["lnf_b"] = torch.zeros(h)
+    if arch == "bert":
+        g = torch.Generator()
+        g.manual_seed(seed * 1000003 + n_layer + 1)
+        out["w_mlm"] = _round(torch.randn((h, h), generator=g) * init_std)
+        out["b_mlm"] = torch.zeros(h)
+        out["lnm_g"] = torch.ones(h)
+        out["lnm_b"] = torch.zeros(h)
+        out["b_dec"] = torch.zeros(vocab)
+    else:
+        out["lnf_g"] = torch.ones(h)
+        out["lnf_b"] = torch.zeros(h)
     return out
 
 
 def gelu(x):
     return 0.5 * x * (1.0 + torch.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3)))
+
+
+def layer_forward_post(p, li, x, B, S, H, eps=1e-12):
+    """BERT post-LN layer (bidirectional attention)."""
+    h = x.shape[-1]
+    D = h // H
+    pre = f"l{li}."
+    qkv = x @ p[pre + "w_qkv"].t() + p[pre + "b_qkv"]
+    q, k, v = qkv.view(B, S, 3, H, D).permute(2, 0, 3, 1, 4)
+    s = q @ k.transpose(-1, -2) / math.sqrt(D)
+    o = (s.softmax(-1) @ v).permute(0, 2, 1, 3).reshape(B * S, h)
+    y1 = x + o @ p[pre + "w_o"].t() + p[pre + "b_o"]
+    x1 = torch.nn.functional.layer_norm(y1, (h,), p[pre + "ln1_g"], p[pre + "ln1_b"], eps)
+    f = gelu(x1 @ p[pre + "w_fc1"].t() + p[pre + "b_fc1"])
+    y2 = x1 + f @ p[pre + "w_fc2"].t() + p[pre + "b_fc2"]
+    return torch.nn.functional.layer_norm(y2, (h,), p[pre + "ln2_g"], p[pre + "ln2_b"], eps)
 
 
 def layer_forward(p, li, x, B, S, H, eps=1e-5):
@@ -90,34 +119,50 @@ class PipelineOracle:
     """Sequential execution of a P-stage Varuna pipeline on CPU fp32."""
 
     def __init__(self, n_layer, hidden, heads, vocab, seq, stage_map, micro_batch, n_micro,
-                 seed=0):
+                 seed=0, arch="gpt2"):
         self.L, self.h, self.H, self.V, self.S = n_layer, hidden, heads, vocab, seq
+        self.arch = arch
+        self.eps = 1e-12 if arch == "bert" else 1e-5
         self.stage_map = list(stage_map)
         self.P = max(stage_map) + 1
         self.m, self.N = micro_batch, n_micro
         self.params = {k: v.clone().requires_grad_(True)
-                       for k, v in init_params(n_layer, hidden, vocab, seq, seed).items()}
+                       for k, v in init_params(n_layer, hidden, vocab, seq, seed,
+                                               arch=arch).items()}
         self.layers = [[i for i, s in enumerate(stage_map) if s == k] for k in range(self.P)]
 
-    def _stage_forward(self, k, x_or_ids):
+    def _stage_forward(self, k, x_or_ids, types=None):
         p = self.params
         if k == 0:
             ids = x_or_ids
             x = p["wte"][ids] + p["wpe"][torch.arange(self.S).repeat(self.m)]
+            if self.arch == "bert":
+                x = x + p["tte"][types]
+                x = torch.nn.functional.layer_norm(x, (self.h,), p["lne_g"], p["lne_b"], self.eps)
         else:
             x = x_or_ids
         for li in self.layers[k]:
-            x = layer_forward(p, li, x, self.m, self.S, self.H)
+            if self.arch == "bert":
+                x = layer_forward_post(p, li, x, self.m, self.S, self.H, self.eps)
+            else:
+                x = layer_forward(p, li, x, self.m, self.S, self.H)
         return x
 
     def _head_loss(self, x, labels, scale):
         p = self.params
+        if self.arch == "bert":
+            hm = gelu(x @ p["w_mlm"].t() + p["b_mlm"])
+            z = torch.nn.functional.layer_norm(hm, (self.h,), p["lnm_g"], p["lnm_b"], self.eps)
+            logits = z @ p["wte"].t() + p["b_dec"]
+            l = torch.nn.functional.cross_entropy(logits, labels, ignore_index=-100,
+                                                  reduction="sum")
+            return l * scale
         y = torch.nn.functional.layer_norm(x, (self.h,), p["lnf_g"], p["lnf_b"], 1e-5)
         logits = y @ p["wte"].t()
         l = torch.nn.functional.cross_entropy(logits, labels, ignore_index=-100, reduction="sum")
         return l * scale
 
-    def run_minibatch(self, ids, labels, total_tokens):
+    def run_minibatch(self, ids, labels, total_tokens, types=None):
         """ids/labels: [N*m, S] int64. Returns the (scaled) loss; grads are
         accumulated in ``self.params[*].grad`` in schedule order."""
         P, N = self.P, self.N
@@ -125,6 +170,8 @@ class PipelineOracle:
         order = _global_order(plan, P)
         ids = ids.view(N, self.m * self.S)
         labels = labels.view(N, self.m * self.S)
+        if types is not None:
+            types = types.reshape(N, self.m * self.S)
         scale = 1.0 / total_tokens
         act = {}     # (k, j) -> activation entering stage k (detached)
         saved = {}   # (k, j) -> (input leaf, output) with graph
@@ -133,13 +180,14 @@ class PipelineOracle:
         for k, kind, j in order:
             last = k == P - 1
             inp = ids[j] if k == 0 else act[(k, j)]
+            tj = types[j] if (types is not None and k == 0) else None
             if kind == osch.F and not last:
                 with torch.no_grad():
-                    out = self._stage_forward(k, inp)
+                    out = self._stage_forward(k, inp, tj)
                 act[(k + 1, j)] = out.detach()
             elif kind == osch.R or (kind == osch.F and last):
                 leaf = inp if k == 0 else inp.detach().requires_grad_(True)
-                out = self._stage_forward(k, leaf)
+                out = self._stage_forward(k, leaf, tj)
                 saved[(k, j)] = (leaf, out)
             else:  # backward
                 leaf, out = saved.pop((k, j))

@@ -58,6 +58,59 @@ __global__ void embed_bwd_pos_kernel(const __nv_bfloat16* __restrict__ dx,
   dwpe[i] += acc;
 }
 
+__global__ void embed_typed_fwd_kernel(const int64_t* __restrict__ ids,
+                                       const int64_t* __restrict__ types,
+                                       const __nv_bfloat16* __restrict__ wte,
+                                       const __nv_bfloat16* __restrict__ wpe,
+                                       const __nv_bfloat16* __restrict__ tte,
+                                       __nv_bfloat16* __restrict__ x, int64_t tokens, int64_t seq,
+                                       int64_t hidden) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (t >= tokens) return;
+  const int lane = threadIdx.x & 31;
+  const uint4* a = reinterpret_cast<const uint4*>(wte + ids[t] * hidden);
+  const uint4* p = reinterpret_cast<const uint4*>(wpe + (t % seq) * hidden);
+  const uint4* q = reinterpret_cast<const uint4*>(tte + types[t] * hidden);
+  uint4* o = reinterpret_cast<uint4*>(x + t * hidden);
+  for (int64_t c = lane; c < (hidden >> 3); c += 32) {
+    float fa[8], fp[8], fq[8];
+    unpack8(a[c], fa);
+    unpack8(p[c], fp);
+    unpack8(q[c], fq);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) fa[j] += fp[j] + fq[j];
+    o[c] = pack8(fa);
+  }
+}
+
+__global__ void gelu_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
+                                const __nv_bfloat16* __restrict__ pre,
+                                __nv_bfloat16* __restrict__ dx, int64_t n) {
+  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 8;
+  if (i + 8 <= n) {
+    float g[8], x[8];
+    unpack8(*reinterpret_cast<const uint4*>(dy + i), g);
+    unpack8(*reinterpret_cast<const uint4*>(pre + i), x);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+      const float u = k0 * (x[j] + k1 * x[j] * x[j] * x[j]);
+      const float t = tanhf(u);
+      g[j] *= 0.5f * (1.f + t) + 0.5f * x[j] * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x[j] * x[j]);
+    }
+    *reinterpret_cast<uint4*>(dx + i) = pack8(g);
+  } else {
+    for (int64_t k = i; k < n; ++k) {
+      const float x = __bfloat162float(pre[k]);
+      const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+      const float t = tanhf(k0 * (x + k1 * x * x * x));
+      dx[k] = __float2bfloat16(__bfloat162float(dy[k]) *
+                               (0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 *
+                                                       (1.f + 3.f * k1 * x * x)));
+    }
+  }
+}
+
 // ------------------------------------------------------------ cross-entropy
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS)
@@ -357,6 +410,34 @@ extern "C" int vp_embed_bwd(const int64_t* ids, const void* dx, float* dwte, flo
   if (dwpe)
     embed_bwd_pos_kernel<<<blocks_for(seq * hidden, 256), 256, 0, ST>>>(CBF(dx), dwpe, batch, seq,
                                                                        hidden);
+  return launch_status();
+}
+
+extern "C" int vp_embed_typed_fwd(const int64_t* ids, const int64_t* types, const void* wte,
+                                  const void* wpe, const void* tte, void* x, int64_t batch,
+                                  int64_t seq, int64_t hidden, void* stream) {
+  if (batch <= 0 || seq <= 0 || hidden <= 0 || (hidden % 8)) return VP_ERR_ARGS;
+  const int64_t tokens = batch * seq;
+  embed_typed_fwd_kernel<<<blocks_for(tokens, 8), 256, 0, ST>>>(ids, types, CBF(wte), CBF(wpe),
+                                                               CBF(tte), BF(x), tokens, seq, hidden);
+  return launch_status();
+}
+
+extern "C" int vp_embed_typed_bwd(const int64_t* ids, const int64_t* types, const void* dx,
+                                  float* dwte, float* dwpe, float* dtte, int64_t batch,
+                                  int64_t seq, int64_t hidden, void* stream) {
+  if (batch <= 0 || seq <= 0 || hidden <= 0 || (hidden % 8)) return VP_ERR_ARGS;
+  const int64_t tokens = batch * seq;
+  embed_bwd_tok_kernel<<<blocks_for(tokens, 8), 256, 0, ST>>>(ids, CBF(dx), dwte, tokens, hidden);
+  embed_bwd_tok_kernel<<<blocks_for(tokens, 8), 256, 0, ST>>>(types, CBF(dx), dtte, tokens, hidden);
+  embed_bwd_pos_kernel<<<blocks_for(seq * hidden, 256), 256, 0, ST>>>(CBF(dx), dwpe, batch, seq,
+                                                                     hidden);
+  return launch_status();
+}
+
+extern "C" int vp_gelu_bwd(const void* dy, const void* pre, void* dx, int64_t n, void* stream) {
+  if (n <= 0) return VP_ERR_ARGS;
+  gelu_bwd_kernel<<<blocks_for(n, 256 * 8), 256, 0, ST>>>(CBF(dy), CBF(pre), BF(dx), n);
   return launch_status();
 }
 

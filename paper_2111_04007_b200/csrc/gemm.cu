@@ -112,7 +112,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiArgs& e, int64_t row, in
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(__bfloat162float(__float2bfloat16(v[i])));
     }
-    if constexpr (EPI == VP_EPI_BIAS_RESID || EPI == VP_EPI_DGELU) {
+    if constexpr (EPI == VP_EPI_BIAS_RESID || EPI == VP_EPI_DGELU || EPI == VP_EPI_RESID) {
       const __nv_bfloat16* a = e.aux + row * e.ldaux + col0;
       if (full) {
 #pragma unroll
@@ -122,14 +122,14 @@ __device__ __forceinline__ void epilogue_chunk(const EpiArgs& e, int64_t row, in
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             float x = __bfloat162float(ah[j]);
-            if constexpr (EPI == VP_EPI_BIAS_RESID) v[i + j] += x;
+            if constexpr (EPI == VP_EPI_BIAS_RESID || EPI == VP_EPI_RESID) v[i + j] += x;
             else v[i + j] *= gelu_tanh_grad(x);
           }
         }
       } else {
         for (int i = 0; i < 32 && col0 + i < N; ++i) {
           float x = __bfloat162float(a[i]);
-          if constexpr (EPI == VP_EPI_BIAS_RESID) v[i] += x;
+          if constexpr (EPI == VP_EPI_BIAS_RESID || EPI == VP_EPI_RESID) v[i] += x;
           else v[i] *= gelu_tanh_grad(x);
         }
       }
@@ -363,12 +363,12 @@ __device__ __forceinline__ void epi2_apply(const Epi2& e, int64_t row, int64_t c
       v[i] = gelu_tanh(pre[i]);
     }
   }
-  if constexpr (EPI == VP_EPI_BIAS_RESID || EPI == VP_EPI_DGELU) {
+  if constexpr (EPI == VP_EPI_BIAS_RESID || EPI == VP_EPI_DGELU || EPI == VP_EPI_RESID) {
     // aux row values were staged in smem by TMA (see gemm2_kernel)
 #pragma unroll
     for (int i = 0; i < 64; ++i) {
-      if constexpr (EPI == VP_EPI_BIAS_RESID) v[i] += xin[i];
-      else v[i] *= gelu_tanh_grad(xin[i]);
+      if constexpr (EPI == VP_EPI_DGELU) v[i] *= gelu_tanh_grad(xin[i]);
+      else v[i] += xin[i];
     }
   }
 }
@@ -400,7 +400,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + 2 * kEpiWarps2);
 
   constexpr bool kF32Out = (EPI == VP_EPI_ACC_F32 || EPI == VP_EPI_STORE_F32);
-  constexpr bool kAuxIn = (EPI == VP_EPI_BIAS_RESID || EPI == VP_EPI_DGELU);
+  constexpr bool kAuxIn = (EPI == VP_EPI_BIAS_RESID || EPI == VP_EPI_DGELU || EPI == VP_EPI_RESID);
   const uint32_t warp = warp_id();
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
@@ -739,6 +739,7 @@ int dispatch_epi(int epi, bool a_mn, bool b_mn, const CUtensorMap& ta, const CUt
     case VP_EPI_BIAS_RESID:
       return dispatch_layout<BN, VP_EPI_BIAS_RESID>(a_mn, b_mn, ta, tb, M, N, K, e, st);
     case VP_EPI_DGELU: return dispatch_layout<BN, VP_EPI_DGELU>(a_mn, b_mn, ta, tb, M, N, K, e, st);
+    case VP_EPI_RESID: return dispatch_layout<BN, VP_EPI_RESID>(a_mn, b_mn, ta, tb, M, N, K, e, st);
     case VP_EPI_ACC_F32:
       return dispatch_layout<BN, VP_EPI_ACC_F32>(a_mn, b_mn, ta, tb, M, N, K, e, st);
     case VP_EPI_STORE_F32:
@@ -786,6 +787,7 @@ int gemm2_dispatch(int epi, bool a_mn, bool b_mn, const CUtensorMap& ta, const C
     case VP_EPI_BIAS_GELU: D2(VP_EPI_BIAS_GELU);
     case VP_EPI_BIAS_RESID: D2(VP_EPI_BIAS_RESID);
     case VP_EPI_DGELU: D2(VP_EPI_DGELU);
+    case VP_EPI_RESID: D2(VP_EPI_RESID);
     case VP_EPI_ACC_F32: D2(VP_EPI_ACC_F32);
     case VP_EPI_STORE_F32: D2(VP_EPI_STORE_F32);
     default: return VP_ERR_ARGS;
@@ -815,7 +817,9 @@ static int gemm_entry(int a_kmajor, int b_kmajor, int epilogue, const void* A, i
   const bool needs_bias = epilogue == VP_EPI_BIAS || epilogue == VP_EPI_BIAS_GELU ||
                           epilogue == VP_EPI_BIAS_RESID;
   if (needs_bias && !bias) return VP_ERR_ARGS;
-  if ((epilogue == VP_EPI_BIAS_RESID || epilogue == VP_EPI_DGELU) && !aux) return VP_ERR_ARGS;
+  if ((epilogue == VP_EPI_BIAS_RESID || epilogue == VP_EPI_DGELU || epilogue == VP_EPI_RESID) &&
+      !aux)
+    return VP_ERR_ARGS;
   if (aux && (ldaux % 8)) return VP_ERR_UNSUPPORTED;
   const bool a_mn = !a_kmajor, b_mn = !b_kmajor;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -828,7 +832,8 @@ static int gemm_entry(int a_kmajor, int b_kmajor, int epilogue, const void* A, i
     ok = ok && (b_mn ? make_tmap(&tb, B, N, K, ldb, 64, BK) : make_tmap(&tb, B, K, N, ldb, BK, 128));
     ok = ok && (f32_out ? make_tmap(&td, D, N, M, ldd, 32, 32, true)
                         : make_tmap(&td, D, N, M, ldd, 64, 32));
-    if (epilogue == VP_EPI_BIAS_GELU || epilogue == VP_EPI_BIAS_RESID || epilogue == VP_EPI_DGELU)
+    if (epilogue == VP_EPI_BIAS_GELU || epilogue == VP_EPI_BIAS_RESID || epilogue == VP_EPI_DGELU ||
+        epilogue == VP_EPI_RESID)
       ok = ok && make_tmap(&tx, aux, N, M, ldaux, 64, 32);
     else tx = td;
     if (!ok) return VP_ERR_UNSUPPORTED;

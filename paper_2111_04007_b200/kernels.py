@@ -19,7 +19,8 @@ L = _lib.lib
 c_int = ctypes.c_int
 u64 = ctypes.c_uint64
 
-EPI_STORE, EPI_BIAS, EPI_BIAS_GELU, EPI_BIAS_RESID, EPI_DGELU, EPI_ACC_F32, EPI_STORE_F32 = range(7)
+(EPI_STORE, EPI_BIAS, EPI_BIAS_GELU, EPI_BIAS_RESID, EPI_DGELU, EPI_ACC_F32, EPI_STORE_F32,
+ EPI_RESID) = range(8)
 
 _SIGS = {
     "vp_device_sm_count": [ctypes.POINTER(c_int)],
@@ -36,6 +37,9 @@ _SIGS = {
     "vp_device_alloc": [i64, ctypes.POINTER(vp)],
     "vp_device_free": [vp],
     "vp_bias_grad": [vp, vp, i64, i64, vp, vp],
+    "vp_embed_typed_fwd": [vp, vp, vp, vp, vp, vp, i64, i64, i64, vp],
+    "vp_embed_typed_bwd": [vp, vp, vp, vp, vp, vp, i64, i64, i64, vp],
+    "vp_gelu_bwd": [vp, vp, vp, i64, vp],
     "vp_dropout": [vp, i64, f32, u64, u64, vp],
     "vp_add": [vp, vp, vp, i64, vp],
     "vp_grad_norm_sq": [vp, i64, vp, vp],
@@ -178,6 +182,28 @@ def embed_bwd(ids, dx, dwte, dwpe, batch, seq, stream=None):
     _count(1 if dwpe is None else 2)
     check(L.vp_embed_bwd(ids.data_ptr(), dx.data_ptr(), dwte.data_ptr(), _p(dwpe), batch, seq,
                          dx.shape[1], _stream(stream)), "vp_embed_bwd")
+
+
+def embed_typed_fwd(ids, types, wte, wpe, tte, x, batch, seq, stream=None):
+    _count(1)
+    check(L.vp_embed_typed_fwd(ids.data_ptr(), types.data_ptr(), wte.data_ptr(), wpe.data_ptr(),
+                               tte.data_ptr(), x.data_ptr(), batch, seq, wte.shape[1],
+                               _stream(stream)), "vp_embed_typed_fwd")
+    return x
+
+
+def embed_typed_bwd(ids, types, dx, dwte, dwpe, dtte, batch, seq, stream=None):
+    _count(3)
+    check(L.vp_embed_typed_bwd(ids.data_ptr(), types.data_ptr(), dx.data_ptr(), dwte.data_ptr(),
+                               dwpe.data_ptr(), dtte.data_ptr(), batch, seq, dx.shape[1],
+                               _stream(stream)), "vp_embed_typed_bwd")
+
+
+def gelu_bwd(dy, pre, dx, stream=None):
+    _count(1)
+    check(L.vp_gelu_bwd(dy.data_ptr(), pre.data_ptr(), dx.data_ptr(), dy.numel(), _stream(stream)),
+          "vp_gelu_bwd")
+    return dx
 
 
 def xent_fwd_bwd(logits, labels, loss_rows, scale, loss_sum=None, stream=None):

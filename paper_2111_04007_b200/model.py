@@ -42,6 +42,11 @@ class GPT2Config:
     dropout: float = 0.0
     init_std: float = 0.02
     causal: bool = True
+    arch: str = "gpt2"          # "gpt2": pre-LN, causal, tied LM head
+                                # "bert": post-LN, bidirectional, typed embeddings +
+                                #         embedding LN, MLM head (dense+GELU+LN, tied decoder)
+    type_vocab: int = 0
+    mlm_per_seq: int = 0        # masked positions per sequence (fixed by the data generator)
 
     @property
     def head_dim(self) -> int:
@@ -66,6 +71,12 @@ CONFIGS = {
     "gpt2_355m": GPT2Config(vocab_size=51200, n_layer=24, hidden=1024, heads=16, seq_len=1024),
     "gpt2_2_5b": GPT2Config(vocab_size=51200, n_layer=54, hidden=1920, heads=20, seq_len=1024),
     "gpt2_8_3b": GPT2Config(vocab_size=51200, n_layer=72, hidden=3072, heads=32, seq_len=1024),
+    "bert_large": GPT2Config(vocab_size=30528, n_layer=24, hidden=1024, heads=16, seq_len=512,
+                             ln_eps=1e-12, causal=False, arch="bert", type_vocab=2,
+                             mlm_per_seq=77),
+    "tiny_bert": GPT2Config(vocab_size=2048, n_layer=4, hidden=256, heads=4, seq_len=128,
+                            ln_eps=1e-12, causal=False, arch="bert", type_vocab=2,
+                            mlm_per_seq=19),
 }
 
 
@@ -98,9 +109,20 @@ def init_layer(cfg: GPT2Config, layer: int, seed: int, device="cpu") -> Dict[str
 def init_embeddings(cfg: GPT2Config, seed: int, device="cpu") -> Dict[str, torch.Tensor]:
     g = torch.Generator(device=device)
     g.manual_seed(seed * 1000003)
-    return {"wte": torch.randn((cfg.vocab_size, cfg.hidden), generator=g, device=device)
-            * cfg.init_std,
-            "wpe": torch.randn((cfg.seq_len, cfg.hidden), generator=g, device=device) * 0.01}
+    out = {"wte": torch.randn((cfg.vocab_size, cfg.hidden), generator=g, device=device)
+           * cfg.init_std,
+           "wpe": torch.randn((cfg.seq_len, cfg.hidden), generator=g, device=device) * 0.01}
+    if cfg.arch == "bert":
+        out["tte"] = torch.randn((cfg.type_vocab, cfg.hidden), generator=g, device=device) \
+            * cfg.init_std
+    return out
+
+
+def init_mlm_head(cfg: GPT2Config, seed: int, device="cpu") -> Dict[str, torch.Tensor]:
+    g = torch.Generator(device=device)
+    g.manual_seed(seed * 1000003 + cfg.n_layer + 1)
+    return {"w_mlm": torch.randn((cfg.hidden, cfg.hidden), generator=g, device=device)
+            * cfg.init_std}
 
 
 def round_bf16(t: torch.Tensor) -> torch.Tensor:
@@ -194,15 +216,23 @@ class GPT2Stage:
         self.cfg, self.spec, self.mb = cfg, spec, micro_batch
         self.dev = torch.device(device)
         self.T = micro_batch * cfg.seq_len
+        self.bert = cfg.arch == "bert"
+        h, V = cfg.hidden, cfg.vocab_size
         specs = []
         if spec.first:
-            specs += [("wte", (cfg.vocab_size, cfg.hidden)), ("wpe", (cfg.seq_len, cfg.hidden))]
+            specs += [("wte", (V, h)), ("wpe", (cfg.seq_len, h))]
+            if self.bert:
+                specs += [("tte", (cfg.type_vocab, h)), ("lne_g", (h,)), ("lne_b", (h,))]
         for li in spec.layers:
             specs += [(f"l{li}.{n}", s) for n, s in layer_param_shapes(cfg)]
         if spec.last:
-            specs += [("lnf_g", (cfg.hidden,)), ("lnf_b", (cfg.hidden,))]
+            if self.bert:
+                specs += [("w_mlm", (h, h)), ("b_mlm", (h,)), ("lnm_g", (h,)), ("lnm_b", (h,)),
+                          ("b_dec", (V,))]
+            else:
+                specs += [("lnf_g", (h,)), ("lnf_b", (h,))]
             if not spec.first:
-                specs += [("wte_head", (cfg.vocab_size, cfg.hidden))]
+                specs += [("wte_head", (V, h))]
         self.params = FlatParams(specs, self.dev)
         self._init(seed, init_device)
         self._alloc()
@@ -210,19 +240,31 @@ class GPT2Stage:
     # ------------------------------------------------------------------ init
     def _init(self, seed, init_device):
         cfg, spec, P = self.cfg, self.spec, self.params
+        h = cfg.hidden
         if spec.first or spec.last:
             emb = init_embeddings(cfg, seed, init_device)
             if spec.first:
                 P.load("wte", emb["wte"])
                 P.load("wpe", emb["wpe"])
+                if self.bert:
+                    P.load("tte", emb["tte"])
+                    P.load("lne_g", torch.ones(h))
+                    P.load("lne_b", torch.zeros(h))
             if spec.last and not spec.first:
                 P.load("wte_head", emb["wte"])
         for li in spec.layers:
             for n, v in init_layer(cfg, li, seed, init_device).items():
                 P.load(f"l{li}.{n}", v)
         if spec.last:
-            P.load("lnf_g", torch.ones(cfg.hidden))
-            P.load("lnf_b", torch.zeros(cfg.hidden))
+            if self.bert:
+                P.load("w_mlm", init_mlm_head(cfg, seed, init_device)["w_mlm"])
+                P.load("b_mlm", torch.zeros(h))
+                P.load("lnm_g", torch.ones(h))
+                P.load("lnm_b", torch.zeros(h))
+                P.load("b_dec", torch.zeros(cfg.vocab_size))
+            else:
+                P.load("lnf_g", torch.ones(h))
+                P.load("lnf_b", torch.zeros(h))
 
     @property
     def head_weight_name(self) -> str:
@@ -247,13 +289,21 @@ class GPT2Stage:
         self.dqkv = torch.empty(T, 3 * h, **bf)
         self.delta = torch.empty(self.mb * cfg.heads * cfg.seq_len, **f32)
         self.ln_ws = torch.empty(K.layernorm_ws_elems(h), **f32)
-        self.bias_ws = torch.empty(K.bias_grad_ws_elems(4 * h), **f32)
+        bias_cols = max(4 * h, cfg.vocab_size) if (self.bert and self.spec.last) else 4 * h
+        self.bias_ws = torch.empty(K.bias_grad_ws_elems(bias_cols), **f32)
         if self.spec.last:
             self.lnf_out = torch.empty(T, h, **bf)
             self.lnf_mean = torch.empty(T, **f32)
             self.lnf_rstd = torch.empty(T, **f32)
             self.logits = torch.empty(T, cfg.vocab_size, **bf)
             self.loss_rows = torch.empty(T, **f32)
+            if self.bert:
+                self.mlm_pre = torch.empty(T, h, **bf)
+                self.mlm_act = torch.empty(T, h, **bf)
+        if self.bert and self.spec.first:
+            self.emb_pre = torch.empty(T, h, **bf)
+            self.emb_mean = torch.empty(T, **f32)
+            self.emb_rstd = torch.empty(T, **f32)
         self.drop_tmp = torch.empty(T, h, **bf) if cfg.dropout > 0 else None
 
     # --------------------------------------------------------------- forward
@@ -272,6 +322,67 @@ class GPT2Stage:
         K.gemm(w.c, P.w(p + "w_fc1"), w.f, epilogue=K.EPI_BIAS_GELU, bias=P.w(p + "b_fc1"),
                aux=w.pre, stream=stream)
         self._proj_resid(w.f, P.w(p + "w_fc2"), P.w(p + "b_fc2"), w.x1, out, dseed, 1, stream)
+
+    def _layer_fwd_post(self, li: int, x: torch.Tensor, out, w: _LayerWS, stream=None):
+        """BERT (post-LN) layer: y1 = x + proj(attn(qkv(x))); x1 = LN1(y1);
+        y2 = x1 + fc2(gelu(fc1(x1))); out = LN2(y2). Saved: qkv, o, lse,
+        y1 (w.x1), x1 (w.c), pre, f, y2 (w.a) and both LN statistics."""
+        cfg, P = self.cfg, self.params
+        p = f"l{li}."
+        K.gemm(x, P.w(p + "w_qkv"), w.qkv, epilogue=K.EPI_BIAS, bias=P.w(p + "b_qkv"),
+               stream=stream)
+        K.attention_fwd(w.qkv, w.o, w.lse, self.mb, cfg.seq_len, cfg.heads, cfg.head_dim,
+                        cfg.causal, stream)
+        K.gemm(w.o, P.w(p + "w_o"), w.x1, epilogue=K.EPI_BIAS_RESID, bias=P.w(p + "b_o"), aux=x,
+               stream=stream)
+        K.layernorm_fwd(w.x1, P.w(p + "ln1_g"), P.w(p + "ln1_b"), w.c, w.mean1, w.rstd1,
+                        cfg.ln_eps, stream)
+        K.gemm(w.c, P.w(p + "w_fc1"), w.f, epilogue=K.EPI_BIAS_GELU, bias=P.w(p + "b_fc1"),
+               aux=w.pre, stream=stream)
+        K.gemm(w.f, P.w(p + "w_fc2"), w.a, epilogue=K.EPI_BIAS_RESID, bias=P.w(p + "b_fc2"),
+               aux=w.c, stream=stream)
+        if isinstance(out, int):  # next stage's ring slot: normalise locally, then ship
+            K.layernorm_fwd(w.a, P.w(p + "ln2_g"), P.w(p + "ln2_b"), self.dc, w.mean2, w.rstd2,
+                            cfg.ln_eps, stream)
+            K.p2p_put(out, self.dc, stream=stream)
+        else:
+            K.layernorm_fwd(w.a, P.w(p + "ln2_g"), P.w(p + "ln2_b"), out, w.mean2, w.rstd2,
+                            cfg.ln_eps, stream)
+
+    def _layer_bwd_post(self, li: int, w: _LayerWS, x: torch.Tensor, stream=None):
+        """self.g = d(layer output) -> d(layer input), BERT post-LN layer."""
+        cfg, P = self.cfg, self.params
+        p = f"l{li}."
+        g = self.g
+        dy2 = self.do
+        K.layernorm_bwd(g, w.a, P.w(p + "ln2_g"), w.mean2, w.rstd2, dy2, P.g(p + "ln2_g"),
+                        P.g(p + "ln2_b"), self.ln_ws, accumulate=False, stream=stream)
+        K.gemm(dy2, P.w(p + "w_fc2"), self.dpre, b_kmajor=False, epilogue=K.EPI_DGELU,
+               aux=w.pre, stream=stream)
+        K.gemm(dy2, w.f, P.g(p + "w_fc2"), a_kmajor=False, b_kmajor=False,
+               epilogue=K.EPI_ACC_F32, stream=stream)
+        K.bias_grad(dy2, P.g(p + "b_fc2"), self.bias_ws, stream)
+        # dx1 = dy2 + dpre @ W1 (residual folded into the dgrad epilogue)
+        K.gemm(self.dpre, P.w(p + "w_fc1"), self.dc, b_kmajor=False, epilogue=K.EPI_RESID,
+               aux=dy2, stream=stream)
+        K.gemm(self.dpre, w.c, P.g(p + "w_fc1"), a_kmajor=False, b_kmajor=False,
+               epilogue=K.EPI_ACC_F32, stream=stream)
+        K.bias_grad(self.dpre, P.g(p + "b_fc1"), self.bias_ws, stream)
+        K.layernorm_bwd(self.dc, w.x1, P.w(p + "ln1_g"), w.mean1, w.rstd1, g, P.g(p + "ln1_g"),
+                        P.g(p + "ln1_b"), self.ln_ws, accumulate=False, stream=stream)
+        # g = dy1: attention branch
+        K.gemm(g, P.w(p + "w_o"), self.do, b_kmajor=False, stream=stream)
+        K.gemm(g, w.o, P.g(p + "w_o"), a_kmajor=False, b_kmajor=False,
+               epilogue=K.EPI_ACC_F32, stream=stream)
+        K.bias_grad(g, P.g(p + "b_o"), self.bias_ws, stream)
+        K.attention_bwd(w.qkv, w.o, self.do, w.lse, self.dqkv, self.delta, self.mb,
+                        cfg.seq_len, cfg.heads, cfg.head_dim, cfg.causal, stream)
+        K.gemm(self.dqkv, x, P.g(p + "w_qkv"), a_kmajor=False, b_kmajor=False,
+               epilogue=K.EPI_ACC_F32, stream=stream)
+        K.bias_grad(self.dqkv, P.g(p + "b_qkv"), self.bias_ws, stream)
+        # dx = dy1 + dqkv @ Wqkv (in place on g)
+        K.gemm(self.dqkv, P.w(p + "w_qkv"), g, b_kmajor=False, epilogue=K.EPI_RESID, aux=g,
+               stream=stream)
 
     def _proj_resid(self, a, wt, b, resid, out, dseed, which, stream):
         """out = resid + dropout(a @ wt^T + b) (fused epilogue when p = 0)."""
@@ -292,7 +403,8 @@ class GPT2Stage:
             K.add(tmp, resid, out_t, stream)
 
     def forward(self, x_in: Optional[torch.Tensor], ids: Optional[torch.Tensor], save: bool,
-                dseed: int = 0, stream=None, out_ptr: Optional[int] = None) -> torch.Tensor:
+                dseed: int = 0, stream=None, out_ptr: Optional[int] = None,
+                types: Optional[torch.Tensor] = None) -> torch.Tensor:
         """Run the stage on one micro-batch. Stage 0 takes token ``ids``
         [T] (int64); others take the received activation ``x_in`` [T, h].
         Returns the stage output (residual stream after the last layer).
@@ -301,7 +413,14 @@ class GPT2Stage:
         compute + P2P send of a checkpointed forward (K9 fused into K1)."""
         cfg, P = self.cfg, self.params
         if self.spec.first:
-            K.embed_fwd(ids, P.w("wte"), P.w("wpe"), self.emb_out, self.mb, cfg.seq_len, stream)
+            if self.bert:
+                K.embed_typed_fwd(ids, types, P.w("wte"), P.w("wpe"), P.w("tte"), self.emb_pre,
+                                  self.mb, cfg.seq_len, stream)
+                K.layernorm_fwd(self.emb_pre, P.w("lne_g"), P.w("lne_b"), self.emb_out,
+                                self.emb_mean, self.emb_rstd, cfg.ln_eps, stream)
+            else:
+                K.embed_fwd(ids, P.w("wte"), P.w("wpe"), self.emb_out, self.mb, cfg.seq_len,
+                            stream)
             x = self.emb_out
             if cfg.dropout > 0:
                 K.dropout_(x, cfg.dropout, dseed ^ 0x5EED, 7 * x.numel(), stream)
@@ -312,7 +431,10 @@ class GPT2Stage:
         for i, li in enumerate(self.spec.layers):
             w = self.ws[i] if save else self.scratch
             dst = out_ptr if (out_ptr is not None and i == nl - 1) else self.xs[i + 1]
-            self._layer_fwd(li, x, dst, w, dseed * 1315423911 + li, stream)
+            if self.bert:
+                self._layer_fwd_post(li, x, dst, w, stream)
+            else:
+                self._layer_fwd(li, x, dst, w, dseed * 1315423911 + li, stream)
             x = self.xs[i + 1]
         return x
 
@@ -322,6 +444,8 @@ class GPT2Stage:
         Leaves d(stage output) in ``self.g``; returns the per-row losses."""
         cfg, P = self.cfg, self.params
         x = self.xs[-1]
+        if self.bert:
+            return self._mlm_head(labels, loss_scale, loss_sum, stream)
         K.layernorm_fwd(x, P.w("lnf_g"), P.w("lnf_b"), self.lnf_out, self.lnf_mean,
                         self.lnf_rstd, cfg.ln_eps, stream)
         wte = P.w(self.head_weight_name)
@@ -333,6 +457,33 @@ class GPT2Stage:
                b_kmajor=False, epilogue=K.EPI_ACC_F32, stream=stream)
         K.layernorm_bwd(self.dc, x, P.w("lnf_g"), self.lnf_mean, self.lnf_rstd, self.g,
                         P.g("lnf_g"), P.g("lnf_b"), self.ln_ws, accumulate=False, stream=stream)
+        return self.loss_rows
+
+    def _mlm_head(self, labels, loss_scale, loss_sum, stream):
+        """BERT MLM head: z = LN(gelu(x W^T + b)); logits = z wte^T + b_dec;
+        cross-entropy on masked positions (labels >= 0). Leaves d(x) in g."""
+        cfg, P = self.cfg, self.params
+        x = self.xs[-1]
+        K.gemm(x, P.w("w_mlm"), self.mlm_act, epilogue=K.EPI_BIAS_GELU, bias=P.w("b_mlm"),
+               aux=self.mlm_pre, stream=stream)
+        K.layernorm_fwd(self.mlm_act, P.w("lnm_g"), P.w("lnm_b"), self.lnf_out, self.lnf_mean,
+                        self.lnf_rstd, cfg.ln_eps, stream)
+        wte = P.w(self.head_weight_name)
+        K.gemm(self.lnf_out, wte, self.logits, epilogue=K.EPI_BIAS, bias=P.w("b_dec"),
+               stream=stream)
+        K.xent_fwd_bwd(self.logits, labels, self.loss_rows, loss_scale, loss_sum, stream)
+        K.bias_grad(self.logits, P.g("b_dec"), self.bias_ws, stream)
+        K.gemm(self.logits, wte, self.dc, b_kmajor=False, stream=stream)
+        K.gemm(self.logits, self.lnf_out, P.g(self.head_weight_name), a_kmajor=False,
+               b_kmajor=False, epilogue=K.EPI_ACC_F32, stream=stream)
+        K.layernorm_bwd(self.dc, self.mlm_act, P.w("lnm_g"), self.lnf_mean, self.lnf_rstd,
+                        self.do, P.g("lnm_g"), P.g("lnm_b"), self.ln_ws, accumulate=False,
+                        stream=stream)
+        K.gelu_bwd(self.do, self.mlm_pre, self.dc, stream)
+        K.gemm(self.dc, P.w("w_mlm"), self.g, b_kmajor=False, stream=stream)
+        K.gemm(self.dc, x, P.g("w_mlm"), a_kmajor=False, b_kmajor=False,
+               epilogue=K.EPI_ACC_F32, stream=stream)
+        K.bias_grad(self.dc, P.g("b_mlm"), self.bias_ws, stream)
         return self.loss_rows
 
     # -------------------------------------------------------------- backward
@@ -380,7 +531,7 @@ class GPT2Stage:
                         stream=stream)
 
     def backward(self, grad_out: Optional[torch.Tensor], ids: Optional[torch.Tensor],
-                 dseed: int = 0, stream=None) -> torch.Tensor:
+                 dseed: int = 0, stream=None, types: Optional[torch.Tensor] = None) -> torch.Tensor:
         """Backward through the stage's layers using the saved working set.
         ``grad_out`` = d(stage output) from the next stage (None on the last
         stage, where loss_and_head_backward already filled ``self.g``).
@@ -391,16 +542,27 @@ class GPT2Stage:
             self.g.copy_(grad_out)
         for i in range(len(self.spec.layers) - 1, -1, -1):
             li = self.spec.layers[i]
-            self._layer_bwd(li, self.ws[i], self.xs[i], dseed * 1315423911 + li, stream)
+            if self.bert:
+                self._layer_bwd_post(li, self.ws[i], self.xs[i], stream)
+            else:
+                self._layer_bwd(li, self.ws[i], self.xs[i], dseed * 1315423911 + li, stream)
         if self.spec.first:
             if cfg.dropout > 0:
                 K.dropout_(self.g, cfg.dropout, dseed ^ 0x5EED, 7 * self.g.numel(), stream)
-            K.embed_bwd(ids, self.g, P.g("wte"), P.g("wpe"), self.mb, cfg.seq_len, stream)
+            if self.bert:
+                K.layernorm_bwd(self.g, self.emb_pre, P.w("lne_g"), self.emb_mean, self.emb_rstd,
+                                self.dc, P.g("lne_g"), P.g("lne_b"), self.ln_ws,
+                                accumulate=False, stream=stream)
+                K.embed_typed_bwd(ids, types, self.dc, P.g("wte"), P.g("wpe"), P.g("tte"),
+                                  self.mb, cfg.seq_len, stream)
+            else:
+                K.embed_bwd(ids, self.g, P.g("wte"), P.g("wpe"), self.mb, cfg.seq_len, stream)
         return self.g
 
     # ------------------------------------------------------------- utilities
     def flops_per_microbatch(self) -> int:
-        """Algorithmic forward FLOPs of this stage for one micro-batch."""
+        """Algorithmic forward FLOPs of this stage for one micro-batch (GPT-2
+        convention; the BERT MLM dense adds 2h^2 per token)."""
         f = len(self.spec.layers) * self.cfg.flops_per_token_layer() * self.T
         if self.spec.last:
             f += self.cfg.head_flops_per_token() * self.T

@@ -100,9 +100,21 @@ class StepResult:
 
 def synthetic_batch(cfg: GPT2Config, rows: int, replica: int, step: int = 0, seed: int = 1234):
     """Deterministic token rows for one replica: global row g = replica·rows + i
-    (DP replicas partition M_total). Labels are inputs shifted by one."""
+    (DP replicas partition M_total). GPT-2: labels are inputs shifted by one.
+    BERT: two segments (token types 0 | 1), exactly ``mlm_per_seq`` masked
+    positions per row with random targets, -100 elsewhere."""
     g = torch.Generator()
     g.manual_seed(seed + 7919 * replica + 104729 * step)
+    if cfg.arch == "bert":
+        S = cfg.seq_len
+        ids = torch.randint(0, cfg.vocab_size, (rows, S), generator=g)
+        types = torch.zeros(rows, S, dtype=torch.int64)
+        types[:, S // 2:] = 1
+        labels = torch.full((rows, S), -100, dtype=torch.int64)
+        pos = torch.argsort(torch.rand(rows, S, generator=g), dim=1)[:, :cfg.mlm_per_seq]
+        tgt = torch.randint(0, cfg.vocab_size, (rows, cfg.mlm_per_seq), generator=g)
+        labels.scatter_(1, pos, tgt)
+        return {"input_ids": ids, "token_type_ids": types, "labels": labels}
     toks = torch.randint(0, cfg.vocab_size, (rows, cfg.seq_len + 1), generator=g)
     return {"input_ids": toks[:, :-1].contiguous(), "labels": toks[:, 1:].contiguous()}
 
@@ -342,9 +354,14 @@ class Varuna:
         sp/planner.py:99-103). Host tensors are copied H2D here."""
         ids = batch.get("input_ids") if self.spec.first else None
         labels = batch.get("labels") if self.spec.last else None
+        types = None
+        if self.spec.first and self.cfg.arch == "bert":
+            types = batch.get("token_type_ids")
+            if types is None:
+                types = torch.zeros_like(ids)
         rows = self.N * self.m
         out = {}
-        for key, t, fill in (("ids", ids, 0), ("labels", labels, -100)):
+        for key, t, fill in (("ids", ids, 0), ("labels", labels, -100), ("types", types, 0)):
             if t is None:
                 continue
             if t.shape[0] < rows:
@@ -364,7 +381,10 @@ class Varuna:
         seq_no = self.step_count
         st = self.stream
         cfg, stage = self.cfg, self.stage
-        total_tokens = self.pc.micro_batch_size * self.N * self.D * cfg.seq_len
+        rows_total = self.pc.micro_batch_size * self.N * self.D
+        # loss = mean over the mini-batch's label tokens (BERT: the generator
+        # fixes mlm_per_seq masked positions per sequence)
+        total_tokens = rows_total * (cfg.mlm_per_seq if cfg.arch == "bert" else cfg.seq_len)
         scale = self.loss_scale / total_tokens
         ev = [] if self.trace else None
         st.wait_stream(torch.cuda.current_stream(self.device))
@@ -377,6 +397,7 @@ class Varuna:
             for kind, j in self.tasks:
                 dseed = (self.step_count * 1000003 + j) & 0x7FFFFFFF
                 ids = data["ids"][j] if self.spec.first else None
+                types = data["types"][j] if "types" in data else None
                 # inputs first (stream waits on the peer's IPC event), so the
                 # task's timing events bracket compute only
                 if kind != B and not self.spec.first and j not in x_in:
@@ -393,14 +414,14 @@ class Varuna:
                     if kind == F and not self.spec.last:
                         out_ptr = self.links.peer_slot_ptr(_Links.ACT, j)
                     stage.forward(x_in.get(j), ids, save=save, dseed=dseed, stream=st,
-                                  out_ptr=out_ptr)
+                                  out_ptr=out_ptr, types=types)
                     if out_ptr is not None:
                         self.links.signal(_Links.ACT, j, seq_no, st)
                 else:
                     if self.spec.last:
                         stage.loss_and_head_backward(data["labels"][j], scale, self.loss_sum,
                                                      stream=st)
-                    g = stage.backward(g_in, ids, dseed=dseed, stream=st)
+                    g = stage.backward(g_in, ids, dseed=dseed, stream=st, types=types)
                     if not self.spec.first:
                         K.p2p_put(self.links.peer_slot_ptr(_Links.GRAD, j), g, stream=st)
                         self.links.signal(_Links.GRAD, j, seq_no, st)

@@ -17,6 +17,7 @@ def main():
     ap.add_argument("--P", type=int, default=2)
     ap.add_argument("--D", type=int, default=1)
     ap.add_argument("--N", type=int, default=4)
+    ap.add_argument("--config", default="tiny")
     args = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
@@ -25,7 +26,7 @@ def main():
     from paper_2111_04007_b200.model import CONFIGS
     from paper_2111_04007_b200.runtime import Varuna, synthetic_batch
     from oracle.gpt2_fp32 import PipelineOracle
-    cfg = CONFIGS["tiny"]
+    cfg = CONFIGS[args.config]
     P, D, N, m = args.P, args.D, args.N, 4
     model = make_block_model("tiny", cfg.n_layer, cfg.hidden, cfg.seq_len)
     a = assign_stages(model, P, m, uniform_profile(cfg.n_layer, 1.0, 2.0, m_grid=(m,)))
@@ -36,9 +37,10 @@ def main():
     torch.cuda.synchronize()
     # oracle: D replicas' mini-batches, summed gradients
     o = PipelineOracle(cfg.n_layer, cfg.hidden, cfg.heads, cfg.vocab_size, cfg.seq_len,
-                       pc.stage_map, m, N, seed=0)
-    total = m * N * D * cfg.seq_len
-    loss = sum(o.run_minibatch(b["input_ids"], b["labels"], total) for b in batches)
+                       pc.stage_map, m, N, seed=0, arch=cfg.arch)
+    total = m * N * D * (cfg.mlm_per_seq if cfg.arch == "bert" else cfg.seq_len)
+    loss = sum(o.run_minibatch(b["input_ids"], b["labels"], total,
+                               types=b.get("token_type_ids")) for b in batches)
     og = o.grads()
     ok = True
     for name, g in v.param_tensors("grad").items():

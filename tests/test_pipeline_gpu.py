@@ -78,6 +78,32 @@ def test_single_gpu_loss_grads_and_update():
             assert rel(t, ref) < 1e-2, name
 
 
+def test_bert_single_gpu_loss_and_grads():
+    """Post-LN BERT (tiny_bert: 4x256, s=128, bidirectional, MLM head with
+    tied decoder) vs the fp32 oracle."""
+    from paper_2111_04007_b200 import ParallelConfig
+    from paper_2111_04007_b200.model import CONFIGS
+    from paper_2111_04007_b200.runtime import Varuna, synthetic_batch
+    from oracle.gpt2_fp32 import PipelineOracle
+    cfg = CONFIGS["tiny_bert"]
+    m, N = 4, 4
+    pc = ParallelConfig(1, 1, m, N, (0,) * cfg.n_layer)
+    batch = synthetic_batch(cfg, m * N, 0)
+    v = Varuna(cfg, pc, seed=0)
+    res = v.step(batch, apply=False)
+    torch.cuda.synchronize()
+    o = PipelineOracle(cfg.n_layer, cfg.hidden, cfg.heads, cfg.vocab_size, cfg.seq_len,
+                       pc.stage_map, m, N, seed=0, arch="bert")
+    loss = o.run_minibatch(batch["input_ids"], batch["labels"], m * N * cfg.mlm_per_seq,
+                           types=batch["token_type_ids"])
+    assert abs(res.loss - loss) / abs(loss) < 5e-3, (res.loss, loss)
+    og = o.grads()
+    for name, g in v.param_tensors("grad").items():
+        if name == "tte":  # only rows 0/1 exist; compare whole table
+            pass
+        assert rel(g, og[name]) < 3e-2, (name, rel(g, og[name]))
+
+
 def test_recompute_is_bitwise_forward():
     from paper_2111_04007_b200.model import CONFIGS, GPT2Stage, StageSpec
     cfg = CONFIGS["tiny"]
@@ -113,12 +139,13 @@ def test_two_stage_pipeline_matches_oracle():
 @pytest.mark.multigpu
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 4,
                     reason="needs 4 GPUs")
-@pytest.mark.parametrize("P,D", [(2, 2), (4, 1)])
-def test_four_gpu_pipeline_matches_oracle(P, D):
+@pytest.mark.parametrize("P,D,config", [(2, 2, "tiny"), (4, 1, "tiny"), (2, 2, "tiny_bert")])
+def test_four_gpu_pipeline_matches_oracle(P, D, config):
     env = dict(os.environ, PYTHONPATH=ROOT)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4",
-           "--master-addr=127.0.0.1", f"--master-port={29541 + P}",
-           os.path.join(ROOT, "tests", "dist_pipeline_check.py"), "--P", str(P), "--D", str(D)]
+           "--master-addr=127.0.0.1", f"--master-port={29541 + P + 7 * (config == 'tiny_bert')}",
+           os.path.join(ROOT, "tests", "dist_pipeline_check.py"), "--P", str(P), "--D", str(D),
+           "--config", config]
     p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-4000:]
     assert "PARITY OK" in p.stdout
