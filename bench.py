@@ -42,6 +42,7 @@ MODEL_CONFIGS = {  # name: (M_total, m)
     "gpt2_355m": (512, 8),
     "gpt2_2_5b": (256, 4),
     "gpt2_8_3b": (512, 4),
+    "bert_large": (8192, 32),
     "tiny": (16, 4),
 }
 
