@@ -70,11 +70,26 @@ def peaks():
         return 1590.0, 1400.0, 6650.0, "fallback"
 
 
-def stage_map_for(cfg, P, m):
-    """assign_stages (the reference DP) over a FLOP-proportional profile with
-    the head folded into the last cut-point; last stage weight 0.75."""
-    from paper_2111_04007_b200 import assign_stages, make_block_model
+def stage_map_for(cfg, P, m, config_name=None):
+    """Stage map by the reference DP (assign_stages). With a B200 calibration
+    profile (profiles/b200_<config>.yaml, written by
+    paper_2111_04007_b200.calibrate) each cut-point is priced at its executed
+    cost on a recomputing stage, 2F_i + B_i, and the last stage (no
+    recompute) is weighted by (F+B)/(2F+B); otherwise a FLOP-proportional
+    profile with the head folded into the last cut-point, weight 0.75."""
+    from paper_2111_04007_b200 import assign_stages, load_profile, make_block_model
     from paper_2111_04007_b200.calibration import CalibrationProfile, CutpointTimes
+    path = os.path.join(ROOT, "profiles", f"b200_{config_name}.yaml") if config_name else ""
+    if P > 1 and path and os.path.exists(path):
+        prof = load_profile(path)
+        if m in prof.m_grid and prof.num_cutpoints == cfg.n_layer:
+            cost = [2 * prof.forward_us(i, m) + prof.backward_us(i, m) for i in range(cfg.n_layer)]
+            f1, b1 = prof.forward_us(1, m), prof.backward_us(1, m)
+            z = {m: 0}
+            cps = tuple(CutpointTimes({m: c}, {m: c}, z, z, z, z, z, z, {1: 0}) for c in cost)
+            model = make_block_model(cfg_name(cfg), cfg.n_layer, cfg.hidden, cfg.seq_len)
+            return assign_stages(model, P, m, CalibrationProfile((m,), (1,), cps),
+                                 last_stage_weight=(f1 + b1) / (2 * f1 + b1)).stage_map
     per_layer = cfg.flops_per_token_layer() * cfg.seq_len * m
     head = cfg.head_flops_per_token() * cfg.seq_len * m
     us = [max(1, round(per_layer / 1e9))] * cfg.n_layer
@@ -241,7 +256,7 @@ def main():
     else:
         P, D = LADDER.get(world, (world, 1))
     N = micro_batches_for(JobSpec(M), m, D)
-    stage_map = stage_map_for(cfg, P, m)
+    stage_map = stage_map_for(cfg, P, m, args.config)
     pc = ParallelConfig(P, D, m, N, stage_map)
     init_dev = "cuda"
     v = Varuna(cfg, pc, seed=0, init_device=init_dev)
