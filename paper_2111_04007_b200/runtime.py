@@ -488,6 +488,27 @@ class Varuna:
                     o.betas[0], o.betas[1], o.eps, o.weight_decay, 1.0 / self.loss_scale,
                     o.max_grad_norm, self.step_count, stream=self.stream)
 
+    # ---------------------------------------------------------------- traces
+    def gantt_rows(self, timeline: dict):
+        """Measured per-task rows of this stage in the reference Gantt format
+        (stage, kind, micro_batch, start_us, end_us), 1-based stage and
+        micro-batch, plus the allreduce row 'A' (sp/simulator.py:116-131,
+        sp/gantt.py:26-32)."""
+        from .core import KIND_NAMES
+        rows = [(self.stage_id + 1, KIND_NAMES[k], j + 1, int(round(a)), int(round(b)))
+                for k, j, a, b in timeline["tasks"]]
+        a0, a1 = timeline["allreduce_us"]
+        rows.append((self.stage_id + 1, "A", 0, int(round(a0)), int(round(a1))))
+        return sorted(rows, key=lambda r: (r[0], r[3], r[1]))
+
+    @staticmethod
+    def gantt_csv(rows) -> str:
+        """``stage,kind,microbatch,start_us,end_us`` — loadable by the
+        reference's ``spotpipe gantt --from-csv`` (sp/cli.py:429-445)."""
+        out = ["stage,kind,microbatch,start_us,end_us"]
+        out += [f"{s},{k},{mb},{a},{b}" for s, k, mb, a, b in rows]
+        return "\n".join(out) + "\n"
+
     # ------------------------------------------------------------- inspection
     def param_tensors(self, which: str = "master") -> Dict[str, torch.Tensor]:
         """Named fp32 views (``master``/``grad``) or bf16 ``weight`` views of
@@ -496,6 +517,83 @@ class Varuna:
         buf = {"master": P.master, "grad": P.grad, "weight": P.weight}[which]
         return {n: P.view(buf, n) for n in P.names}
 
+    # ------------------------------------------------------ checkpoint / morph
+    def _owner_replica(self, name: str) -> int:
+        """Per-layer checkpoint sharding across the D replicas:
+        layer li is written by replica li mod D; embedding/head by replica 0."""
+        if name.startswith("l") and "." in name:
+            return int(name[1:name.index(".")]) % self.D
+        return 0
+
+    def save_layer_state(self, ckpt_dir: str) -> str:
+        """Write this rank's share of the stage's per-layer state (fp32 master,
+        Adam moments) keyed by GLOBAL parameter names, so a resume may use a
+        different stage map / P x D. Returns the file written."""
+        os.makedirs(ckpt_dir, exist_ok=True)
+        P = self.stage.params
+        state = {}
+        for name in P.names:
+            if name == "wte_head":      # tied copy: stage 0 owns "wte"
+                continue
+            if self._owner_replica(name) != self.replica:
+                continue
+            state[name] = {k: P.view(getattr(P, buf), name).detach().cpu().clone()
+                           for k, buf in (("master", "master"), ("exp_avg", "exp_avg"),
+                                          ("exp_avg_sq", "exp_avg_sq"))}
+        path = os.path.join(ckpt_dir, f"stage{self.stage_id}_replica{self.replica}.pt")
+        torch.save({"step": self.step_count, "state": state}, path)
+        return path
+
+    def load_layer_state(self, ckpt_dir: str) -> None:
+        """Load every parameter this rank owns from all shard files."""
+        P = self.stage.params
+        want = set(P.names)
+        found = set()
+        step = None
+        for fn in sorted(os.listdir(ckpt_dir)):
+            if not fn.endswith(".pt"):
+                continue
+            blob = torch.load(os.path.join(ckpt_dir, fn), map_location="cpu")
+            step = blob["step"]
+            for name, st in blob["state"].items():
+                targets = [name] + (["wte_head"] if name == "wte" else [])
+                for t in targets:
+                    if t not in want:
+                        continue
+                    for k in ("master", "exp_avg", "exp_avg_sq"):
+                        P.view(getattr(P, k), t).copy_(st[k].to(self.device))
+                    P.view(P.weight, t).copy_(st["master"].to(self.device).to(torch.bfloat16))
+                    found.add(t)
+        missing = want - found
+        if missing:
+            raise ConfigError(f"checkpoint {ckpt_dir} lacks {sorted(missing)[:4]}...")
+        self.step_count = int(step or 0)
+        torch.cuda.synchronize()
+
     def close(self):
         if self.shm is not None:
             self.shm.close()
+            self.shm = None
+
+
+def morph(v: Varuna, new_config: ParallelConfig, ckpt_dir: str, **kwargs) -> Varuna:
+    """Re-partition a running job onto ``new_config`` (the decision the
+    reference makes with ``plan()`` on a cluster change, sp/morphing.py:
+    383-448): every rank writes its per-layer shard, the old executor is torn
+    down, a new one is built for the new (P, D, stage_map) on the same ranks,
+    and each rank loads exactly the layers its new stage owns. M_total is
+    preserved through N_m = ceil(M/(m*D)) in ``new_config``."""
+    v.save_layer_state(ckpt_dir)
+    if dist.is_initialized():
+        dist.barrier()
+    torch.cuda.synchronize()
+    cfg = v.cfg
+    opt = v.opt
+    v.close()
+    del v
+    torch.cuda.empty_cache()
+    nv = Varuna(cfg, new_config, optimizer=opt, **kwargs)
+    nv.load_layer_state(ckpt_dir)
+    if dist.is_initialized():
+        dist.barrier()
+    return nv

@@ -149,3 +149,32 @@ def test_four_gpu_pipeline_matches_oracle(P, D, config):
     p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-4000:]
     assert "PARITY OK" in p.stdout
+
+
+@pytest.mark.multigpu
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs 2 GPUs")
+def test_morph_pipeline_to_data_parallel():
+    env = dict(os.environ, PYTHONPATH=ROOT)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29571",
+           os.path.join(ROOT, "tests", "dist_morph_check.py")]
+    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-4000:]
+    assert "MORPH OK" in p.stdout
+
+
+def test_gantt_export_format():
+    from paper_2111_04007_b200 import ParallelConfig
+    from paper_2111_04007_b200.model import CONFIGS
+    from paper_2111_04007_b200.runtime import Varuna, synthetic_batch
+    cfg = CONFIGS["tiny"]
+    v = Varuna(cfg, ParallelConfig(1, 1, 4, 2, (0,) * 4), seed=0, trace=True)
+    res = v.step(synthetic_batch(cfg, 8, 0))
+    rows = v.gantt_rows(res.timeline)
+    text = v.gantt_csv(rows)
+    lines = text.strip().splitlines()
+    assert lines[0] == "stage,kind,microbatch,start_us,end_us"
+    assert len(lines) - 1 == 2 * 2 + 1  # F,B per micro-batch + allreduce row
+    kinds = [ln.split(",")[1] for ln in lines[1:]]
+    assert kinds.count("F") == 2 and kinds.count("B") == 2 and kinds.count("A") == 1
