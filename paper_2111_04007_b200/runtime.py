@@ -262,7 +262,8 @@ class Varuna:
 
     def __init__(self, model: GPT2Config, config: ParallelConfig, *,
                  optimizer: AdamWConfig = AdamWConfig(), seed: int = 0, loss_scale: float = 1.0,
-                 device=None, init_device: str = "cpu", trace: bool = False):
+                 device=None, init_device: str = "cpu", trace: bool = False,
+                 dispatch: str = "static", profile=None):
         if len(config.stage_map) != model.n_layer:
             raise ConfigError(f"stage_map covers {len(config.stage_map)} cut-points, model has "
                               f"{model.n_layer} (one CutPoint per transformer layer)")
@@ -289,7 +290,13 @@ class Varuna:
         self.stage = GPT2Stage(model, self.spec, self.m, self.device, seed, init_device)
         self.schedule: Schedule = generate_varuna_schedule(P, self.N, 1.0, 2.0, 1.0)
         kinds, mbs = self.schedule.stage_slice(self.stage_id)
-        self.tasks = list(zip(kinds.tolist(), mbs.tolist()))
+        if dispatch == "static":
+            self.tasks = list(zip(kinds.tolist(), mbs.tolist()))
+        elif dispatch == "opportunistic":
+            self.tasks = self._opportunistic_order(profile)
+        else:
+            raise ConfigError(f"dispatch must be 'static' or 'opportunistic', not {dispatch!r}")
+        self.dispatch = dispatch
         self._check_plan()
         self.loss_scale = loss_scale
         self.step_count = 0
@@ -305,6 +312,21 @@ class Varuna:
         self.gpu_launches_per_step = None
 
     # ---------------------------------------------------------------- setup
+    def _opportunistic_order(self, profile):
+        """This stage's dispatch order as the reference's opportunistic replica
+        kernel runs the schedule under ``profile`` (default: the generator's
+        own 1:2:1 F:B:R times per cut-point, no transfer cost)."""
+        from .calibration import uniform_profile
+        from .core import make_block_model
+        from .simulator import execution_order
+        cfg, pc = self.cfg, self.pc
+        if profile is None:
+            profile = uniform_profile(cfg.n_layer, 1.0, 2.0, m_grid=(self.m,),
+                                      d_grid=tuple(sorted({1, self.D})))
+        model = make_block_model("stages", cfg.n_layer, cfg.hidden, cfg.seq_len)
+        order = execution_order(self.schedule, pc, profile, model, opportunistic=True)
+        return order[self.stage_id]
+
     def _check_plan(self):
         """The executor relies on rule 2 (R(j) directly before B(j)) and on the
         last stage's F(j)/B(j) alternation (sp/scheduler.py:228-241)."""

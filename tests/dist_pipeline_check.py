@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--D", type=int, default=1)
     ap.add_argument("--N", type=int, default=4)
     ap.add_argument("--config", default="tiny")
+    ap.add_argument("--dispatch", default="static")
     args = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
@@ -31,7 +32,17 @@ def main():
     model = make_block_model("tiny", cfg.n_layer, cfg.hidden, cfg.seq_len)
     a = assign_stages(model, P, m, uniform_profile(cfg.n_layer, 1.0, 2.0, m_grid=(m,)))
     pc = ParallelConfig(P, D, m, N, a.stage_map)
-    v = Varuna(cfg, pc, seed=0)
+    prof = None
+    if args.dispatch == "opportunistic":
+        # unbalanced per-cut-point times + slow, jittery links: the replica
+        # kernel reorders tasks relative to the static schedule
+        from tests.test_control_parity import skewed_profile
+        prof = skewed_profile(m)
+    v = Varuna(cfg, pc, seed=0, dispatch=args.dispatch, profile=prof)
+    if args.dispatch == "opportunistic":
+        kinds, mbs = v.schedule.stage_slice(v.stage_id)
+        moved = sum(a != b for a, b in zip(zip(kinds.tolist(), mbs.tolist()), v.tasks))
+        print(f"rank {v.rank} dispatch order differs from static at {moved} positions", flush=True)
     batches = [synthetic_batch(cfg, m * N, r) for r in range(D)]
     res = v.step(batches[v.replica], apply=False)
     torch.cuda.synchronize()

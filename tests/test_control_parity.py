@@ -148,3 +148,32 @@ def test_schedule_matches_oracle_large():
         s = vp.generate_varuna_schedule(p, n, *UNIT)
         k, m, o = osch.flatten(osch.varuna_plan(p, n, 1_000_000, 2_000_000, 1_000_000))
         assert s.kinds.tolist() == k and s.mbs.tolist() == m and s.offsets.tolist() == o
+
+
+def skewed_profile(m=4):
+    """Unbalanced 4-cut-point profile with slow, jittery links under which the
+    opportunistic replica kernel departs from the static order at P=2, N=4."""
+    from paper_2111_04007_b200.calibration import CalibrationProfile, CutpointTimes
+    cps = tuple(CutpointTimes({m: f}, {m: 2 * f}, {m: 195}, {m: 16}, {m: 195}, {m: 16},
+                              {m: 195}, {m: 16}, {1: 0}) for f in (84, 195, 266, 255))
+    return CalibrationProfile((m,), (1,), cps)
+
+
+def test_opportunistic_execution_order():
+    from paper_2111_04007_b200 import ParallelConfig, generate_varuna_schedule, make_block_model
+    from paper_2111_04007_b200.simulator import execution_order
+    sch = generate_varuna_schedule(2, 4, 1.0, 2.0, 1.0)
+    pc = ParallelConfig(2, 1, 4, 4, (0, 0, 1, 1))
+    order = execution_order(sch, pc, skewed_profile(), make_block_model("t", 4, 256, 128))
+    moved = 0
+    for k in range(2):
+        kinds, mbs = sch.stage_slice(k)
+        static = list(zip(kinds.tolist(), mbs.tolist()))
+        assert sorted(static) == sorted(order[k])          # a permutation of the stage's tasks
+        moved += sum(a != b for a, b in zip(static, order[k]))
+        for i, (kind, j) in enumerate(order[k]):           # rule 2 holds in the replayed order
+            if kind == 0 and k < 1:
+                assert order[k][i - 1] == (1, j)
+            if kind == 0:
+                assert (2, j) in order[k][:i]
+    assert moved > 0
