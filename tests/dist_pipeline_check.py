@@ -12,6 +12,16 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+def skewed_profile(m=4):
+    """Unbalanced 4-cut-point profile with slow, jittery links under which the
+    opportunistic replica kernel departs from the static order at P=2, N=4."""
+    from paper_2111_04007_b200.calibration import CalibrationProfile, CutpointTimes
+    cps = tuple(CutpointTimes({m: f}, {m: 2 * f}, {m: 195}, {m: 16}, {m: 195}, {m: 16},
+                              {m: 195}, {m: 16}, {1: 0}) for f in (84, 195, 266, 255))
+    return CalibrationProfile((m,), (1,), cps)
+
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--P", type=int, default=2)
@@ -36,7 +46,6 @@ def main():
     if args.dispatch == "opportunistic":
         # unbalanced per-cut-point times + slow, jittery links: the replica
         # kernel reorders tasks relative to the static schedule
-        from tests.test_control_parity import skewed_profile
         prof = skewed_profile(m)
     v = Varuna(cfg, pc, seed=0, dispatch=args.dispatch, profile=prof)
     if args.dispatch == "opportunistic":

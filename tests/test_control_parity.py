@@ -2,6 +2,8 @@
 (tests/golden/*, produced by spotpipe 0.1.0) and vs the pinned oracle on
 fresh random cases. Bit-exact: integer arrays must be identical."""
 
+import sys
+import os
 import hashlib
 
 import numpy as np
@@ -150,18 +152,11 @@ def test_schedule_matches_oracle_large():
         assert s.kinds.tolist() == k and s.mbs.tolist() == m and s.offsets.tolist() == o
 
 
-def skewed_profile(m=4):
-    """Unbalanced 4-cut-point profile with slow, jittery links under which the
-    opportunistic replica kernel departs from the static order at P=2, N=4."""
-    from paper_2111_04007_b200.calibration import CalibrationProfile, CutpointTimes
-    cps = tuple(CutpointTimes({m: f}, {m: 2 * f}, {m: 195}, {m: 16}, {m: 195}, {m: 16},
-                              {m: 195}, {m: 16}, {1: 0}) for f in (84, 195, 266, 255))
-    return CalibrationProfile((m,), (1,), cps)
-
-
 def test_opportunistic_execution_order():
     from paper_2111_04007_b200 import ParallelConfig, generate_varuna_schedule, make_block_model
     from paper_2111_04007_b200.simulator import execution_order
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from dist_pipeline_check import skewed_profile
     sch = generate_varuna_schedule(2, 4, 1.0, 2.0, 1.0)
     pc = ParallelConfig(2, 1, 4, 4, (0, 0, 1, 1))
     order = execution_order(sch, pc, skewed_profile(), make_block_model("t", 4, 256, 128))
