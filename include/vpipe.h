@@ -142,6 +142,19 @@ int vp_attention_fwd(const void* qkv, void* o, float* lse, int64_t batch, int64_
 int vp_attention_bwd(const void* qkv, const void* o, const void* dout, const float* lse,
                      void* dqkv, float* delta_ws, int64_t batch, int64_t seq, int64_t heads,
                      int64_t head_dim, int causal, void* stream);
+/* Workspace (fp32 elements) of vp_attention_bwd_ex: delta [B*H*S] + the fp32
+ * dQ accumulator [B*S*H*D]. */
+int64_t vp_attention_bwd_ws_elems(int64_t batch, int64_t seq, int64_t heads, int64_t head_dim);
+#define VP_ATTN_DETERMINISTIC 1
+/* Backward with one fused tcgen05 kernel per (key block, head) for head_dim
+ * 64: S/dP computed once, dK/dV in TMEM, dQ accumulated across key blocks by
+ * TMA reduce-add into the fp32 workspace (order-dependent rounding). flags
+ * VP_ATTN_DETERMINISTIC (or head_dim != 64) selects the two-kernel
+ * deterministic path of vp_attention_bwd. workspace 16-byte aligned. */
+int vp_attention_bwd_ex(const void* qkv, const void* o, const void* dout, const float* lse,
+                        void* dqkv, float* workspace, int64_t ws_elems, int64_t batch,
+                        int64_t seq, int64_t heads, int64_t head_dim, int causal, int flags,
+                        void* stream);
 
 /* Token + position embedding gather: x[T,h] = wte[ids] + wpe[pos]. */
 int vp_embed_fwd(const int64_t* ids, const void* wte, const void* wpe, void* x, int64_t batch,

@@ -32,10 +32,37 @@ for B, S, H, D, causal in cases:
     lse = torch.empty(B * H * S, device="cuda")
     do = torch.randn_like(o)
     dqkv = torch.empty_like(qkv)
-    delta = torch.empty_like(lse)
+    delta = torch.empty(K.attention_bwd_ws_elems(B, S, H, D), device="cuda")
     f = 4 * B * S * S * H * D * (0.5 if causal else 1.0)
     ms_f = t(lambda: K.attention_fwd(qkv, o, lse, B, S, H, D, causal))
     ms_b = t(lambda: K.attention_bwd(qkv, o, do, lse, dqkv, delta, B, S, H, D, causal))
+    ms_bd = t(lambda: K.attention_bwd(qkv, o, do, lse, dqkv, delta, B, S, H, D, causal,
+                                      deterministic=True))
     print(json.dumps({"B": B, "S": S, "H": H, "D": D, "causal": causal,
                       "fwd_ms": round(ms_f, 4), "fwd_tflops": round(f / ms_f / 1e9, 1),
-                      "bwd_ms": round(ms_b, 4), "bwd_tflops": round(2.5 * f / ms_b / 1e9, 1)}))
+                      "bwd_ms": round(ms_b, 4), "bwd_tflops": round(2.5 * f / ms_b / 1e9, 1),
+                      "bwd_det_ms": round(ms_bd, 4)}))
+
+if len(sys.argv) > 1 and sys.argv[1] == "sdpa":
+    # library reference points (not on the product path): torch SDPA backends
+    import torch.nn.functional as F
+    from torch.nn.attention import SDPBackend, sdpa_kernel
+    for B, S, H, D, causal in [(8, 1024, 16, 64, True), (4, 1024, 32, 96, True)]:
+        q, k, v = (torch.randn(B, H, S, D, device="cuda", dtype=torch.bfloat16,
+                               requires_grad=True) for _ in range(3))
+        f = 4 * B * S * S * H * D * (0.5 if causal else 1.0)
+        for be in (SDPBackend.CUDNN_ATTENTION, SDPBackend.FLASH_ATTENTION):
+            try:
+                with sdpa_kernel(be):
+                    out = F.scaled_dot_product_attention(q, k, v, is_causal=causal)
+                    go = torch.randn_like(out)
+                    ms_f = t(lambda: F.scaled_dot_product_attention(q, k, v, is_causal=causal))
+                    ms_fb = t(lambda: torch.autograd.grad(
+                        F.scaled_dot_product_attention(q, k, v, is_causal=causal), (q, k, v), go))
+                ms_b = ms_fb - ms_f
+                print(json.dumps({"backend": str(be), "B": B, "S": S, "H": H, "D": D,
+                                  "fwd_ms": round(ms_f, 4), "fwd_tflops": round(f / ms_f / 1e9, 1),
+                                  "bwd_ms": round(ms_b, 4),
+                                  "bwd_tflops": round(2.5 * f / ms_b / 1e9, 1)}))
+            except Exception as ex:  # noqa: BLE001
+                print(json.dumps({"backend": str(be), "error": str(ex)[:200]}))

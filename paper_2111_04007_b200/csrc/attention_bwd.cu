@@ -1,0 +1,451 @@
+// Fused attention backward on tcgen05 (K3 of DESIGN.md), head_dim 64.
+//
+// One CTA per (128-key block, batch*head); it loops over the 128-query blocks
+// the keys are visible to (causal: i >= kb) and produces dK, dV for its keys
+// plus its share of every dQ_i, accumulated across CTAs in an fp32 buffer by
+// TMA reduce-add (the only cross-CTA traffic). S and dP are computed once per
+// (key block, query block) pair — five MMAs per pair instead of the seven of
+// the two-kernel form (attention_tc.cu, kept as the deterministic path).
+//
+//   warp 0      TMA producer: K, V once; Q_i, dO_i and lse_i, delta_i (bulk
+//               copy) into a 2-stage ring
+//   warp 1      MMA issuer (one thread), per query block i:
+//                 S^T  = K Q_i^T              TMEM [0,128)
+//                 dP^T = V dO_i^T             TMEM [128,256)
+//                 dV  += P^T dO_i             TMEM [256,320)
+//                 dK  += dS^T Q_i             TMEM [320,384)
+//                 dQ_i = dS K                 TMEM [384,448) / [448,512) (ping-pong)
+//               S/dP of block i+1 are issued before the gradient MMAs of i,
+//               so the tensor core runs while block i's softmax is computed.
+//   warp 2      TMEM allocator (all 512 columns; 1 CTA per SM)
+//   warps 4-11  thread = key row (TMEM lane); the two warps of a lane
+//               quadrant split the 128 query columns. P^T = exp2(S^T c - lse),
+//               dS^T = P^T (dP^T - delta) -> smem (bf16, SW128, K-major for
+//               dV/dK and MN-major for dQ through a second descriptor);
+//               then dQ_{i-1}: TMEM -> smem (fp32, SW128) -> TMA reduce-add.
+//               At the end dK (x scale) and dV -> dqkv.
+// dQacc is zeroed by the delta pre-pass and scaled to bf16 by a post-pass.
+#include "sm100.cuh"
+#include "tmap.cuh"
+
+namespace vp {
+namespace {
+
+constexpr int FB_M = 128;  // keys per CTA
+constexpr int FB_N = 128;  // queries per inner block
+constexpr int FB_D = 64;
+constexpr int FB_NS = 2;   // Q/dO ring stages
+constexpr int FB_CW = 8;   // compute warps
+constexpr int FB_THREADS = 128 + 32 * FB_CW;
+
+struct FbSmem {
+  static constexpr int TILE = 128 * 128;                 // 128 rows x 64 bf16 (SW128)
+  static constexpr int K_OFF = 0;
+  static constexpr int V_OFF = K_OFF + TILE;
+  static constexpr int Q_OFF = V_OFF + TILE;             // [NS] stride 2*TILE
+  static constexpr int DO_OFF = Q_OFF + TILE;            // [NS] stride 2*TILE
+  static constexpr int PT_OFF = Q_OFF + FB_NS * 2 * TILE;  // P^T: 2 chunks of 64 queries
+  static constexpr int DST_OFF = PT_OFF + 2 * TILE;        // dS^T: 2 chunks
+  static constexpr int STG_OFF = DST_OFF + 2 * TILE;       // dQ staging: 8 warps x 4 KB
+  static constexpr int LV_OFF = STG_OFF + FB_CW * 4096;    // lse/delta [NS][2][128] f32
+  static constexpr int BAR_OFF = LV_OFF + FB_NS * 2 * FB_N * 4;
+  static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+};
+static_assert(FbSmem::TOTAL <= 232448, "attention bwd smem");
+
+template <bool CAUSAL>
+__global__ void __launch_bounds__(FB_THREADS, 1)
+    attn_bwd_fused(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
+                   const __grid_constant__ CUtensorMap tmDQ, const float* __restrict__ lse,
+                   const float* __restrict__ delta, __nv_bfloat16* __restrict__ dqkv, int S, int H,
+                   int BH, float scale_log2, float scale) {
+  using L = FbSmem;
+  constexpr int D = FB_D;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* kv_full = bars + 0;
+  uint64_t* q_full = bars + 1;    // [NS]
+  uint64_t* q_empty = bars + 3;   // [NS]
+  uint64_t* st_full = bars + 5;
+  uint64_t* st_empty = bars + 6;
+  uint64_t* p_full = bars + 7;
+  uint64_t* p_empty = bars + 8;
+  uint64_t* dq_full = bars + 9;   // [2]
+  uint64_t* dq_empty = bars + 11; // [2]
+  uint64_t* acc_full = bars + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+
+  // longest-first order: all CTAs of key block 0 (most query blocks) first
+  const int kb = static_cast<int>(blockIdx.x) / BH;
+  const int bh = static_cast<int>(blockIdx.x) % BH;
+  const int b = bh / H, h = bh % H;
+  const int k0 = kb * FB_M;
+  const int n_qb = (S + FB_N - 1) / FB_N;
+  const int i0 = CAUSAL ? kb : 0;  // FB_M == FB_N
+  const int n_it = n_qb - i0;
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int Hd = H * D;
+  const float* lse_bh = lse + static_cast<int64_t>(bh) * S;
+  const float* del_bh = delta + static_cast<int64_t>(bh) * S;
+  float* sv = reinterpret_cast<float*>(smem + L::LV_OFF);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmQKV);
+    tma_prefetch(&tmDO);
+    tma_prefetch(&tmDQ);
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < FB_NS; ++i) {
+      mbar_init(&q_full[i], 2);
+      mbar_init(&q_empty[i], 1);
+    }
+    mbar_init(st_full, 1);
+    mbar_init(st_empty, FB_CW);
+    mbar_init(p_full, FB_CW);
+    mbar_init(p_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&dq_full[i], 1);
+      mbar_init(&dq_empty[i], FB_CW);
+    }
+    mbar_init(acc_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tdP = tmem + 128, tDV = tmem + 256, tDK = tmem + 320,
+                 tDQ = tmem + 384;
+
+  if (warp == 0) {
+    // ===== producer =====
+    if (lane == 0) {
+      mbar_expect_tx(kv_full, 2 * L::TILE);
+      tma_load_3d(smem + L::K_OFF, &tmQKV, kv_full, Hd + h * D, k0, b);
+      tma_load_3d(smem + L::V_OFF, &tmQKV, kv_full, 2 * Hd + h * D, k0, b);
+    }
+    for (int it = 0; it < n_it; ++it) {
+      const int st = it % FB_NS;
+      const uint32_t ph = (it / FB_NS) & 1;
+      const int qi = (i0 + it) * FB_N;
+      const bool full_blk = qi + FB_N <= S && ((reinterpret_cast<uintptr_t>(lse_bh + qi) |
+                                                reinterpret_cast<uintptr_t>(del_bh + qi)) & 15) == 0;
+      float* dst = sv + st * 2 * FB_N;
+      uint8_t* sq = smem + L::Q_OFF + st * 2 * L::TILE;
+      if (lane == 0) {
+        mbar_wait(&q_empty[st], ph ^ 1);
+        mbar_expect_tx(&q_full[st], 2 * L::TILE + (full_blk ? 2 * FB_N * 4 : 0));
+        tma_load_3d(sq, &tmQKV, &q_full[st], h * D, qi, b);
+        tma_load_3d(sq + L::TILE, &tmDO, &q_full[st], h * D, qi, b);
+        if (full_blk) {
+          bulk_g2s(dst, lse_bh + qi, FB_N * 4, &q_full[st]);
+          bulk_g2s(dst + FB_N, del_bh + qi, FB_N * 4, &q_full[st]);
+          mbar_arrive(&q_full[st]);
+        }
+      }
+      if (!full_blk) {
+        __syncwarp();
+        mbar_wait(&q_empty[st], ph ^ 1);
+        for (int t = lane; t < FB_N; t += 32) {
+          const int q = qi + t;
+          dst[t] = q < S ? lse_bh[q] : 0.f;
+          dst[FB_N + t] = q < S ? del_bh[q] : 0.f;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&q_full[st]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ===== MMA issuer =====
+      constexpr uint32_t idST = idesc_bf16(128, FB_N, false, false);
+      constexpr uint32_t idG = idesc_bf16(128, D, false, true);
+      constexpr uint32_t idQ = idesc_bf16(128, D, true, true);
+      const uint32_t sK = smem_u32(smem + L::K_OFF), sV = smem_u32(smem + L::V_OFF);
+      const uint32_t sPt = smem_u32(smem + L::PT_OFF), sdSt = smem_u32(smem + L::DST_OFF);
+      mbar_wait(kv_full, 0);
+      auto issue_grad = [&](int j) {
+        const int qs = j % FB_NS;
+        const uint32_t sQ = smem_u32(smem + L::Q_OFF + qs * 2 * L::TILE);
+        const uint32_t sdO = sQ + L::TILE;
+        mbar_wait(p_full, j & 1);
+        mbar_wait(&dq_empty[j & 1], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < FB_N / 16; ++k) {
+          const uint32_t koff = (k >> 2) * L::TILE + (k & 3) * 32;
+          const uint32_t acc = (j > 0 || k > 0) ? 1u : 0u;
+          umma_f16(tDV, sdesc_sw128(sPt + koff, 16, 1024), sdesc_sw128(sdO + k * 2048, L::TILE, 1024),
+                   idG, acc);
+          umma_f16(tDK, sdesc_sw128(sdSt + koff, 16, 1024), sdesc_sw128(sQ + k * 2048, L::TILE, 1024),
+                   idG, acc);
+        }
+#pragma unroll
+        for (int k = 0; k < FB_M / 16; ++k)
+          umma_f16(tDQ + (j & 1) * 64, sdesc_sw128(sdSt + k * 2048, L::TILE, 1024),
+                   sdesc_sw128(sK + k * 2048, L::TILE, 1024), idQ, k > 0 ? 1u : 0u);
+        umma_commit(p_empty);
+        umma_commit(&q_empty[qs]);
+        umma_commit(&dq_full[j & 1]);
+      };
+      for (int it = 0; it < n_it; ++it) {
+        const int qs = it % FB_NS;
+        const uint32_t sQ = smem_u32(smem + L::Q_OFF + qs * 2 * L::TILE);
+        const uint32_t sdO = sQ + L::TILE;
+        mbar_wait(&q_full[qs], (it / FB_NS) & 1);
+        mbar_wait(st_empty, (it & 1) ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          umma_f16(tS, sdesc_sw128(sK + k * 32, 16, 1024), sdesc_sw128(sQ + k * 32, 16, 1024), idST,
+                   k > 0);
+          umma_f16(tdP, sdesc_sw128(sV + k * 32, 16, 1024), sdesc_sw128(sdO + k * 32, 16, 1024),
+                   idST, k > 0);
+        }
+        umma_commit(st_full);
+        if (it >= 1) issue_grad(it - 1);
+      }
+      issue_grad(n_it - 1);
+      umma_commit(acc_full);
+    }
+  } else if (warp >= 4) {
+    // ===== softmax-gradient warps: thread = key row =====
+    const uint32_t qd = warp & 3;
+    const int chalf = static_cast<int>(warp - 4) >> 2;
+    const int r = qd * 32 + lane;
+    const int key = k0 + r;
+    const uint32_t trow = (qd * 32) << 16;
+    uint8_t* stg = smem + L::STG_OFF + (warp - 4) * 4096;
+    const uint32_t rowP = smem_u32(smem + L::PT_OFF + chalf * L::TILE + r * 128);
+    const uint32_t rowG = smem_u32(smem + L::DST_OFF + chalf * L::TILE + r * 128);
+
+    auto drain_dq = [&](int j) {
+      const int buf = j & 1;
+      mbar_wait(&dq_full[buf], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t v[32];
+      tmem_ld32(tDQ + buf * 64 + trow + chalf * 32, v);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&dq_empty[buf]);
+        bulk_wait_read<0>();  // previous reduce has read the staging tile
+      }
+      __syncwarp();
+      const uint32_t srow = smem_u32(stg + lane * 128);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        sts128(srow + ((k ^ (lane & 7)) << 4),
+               make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]));
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_reduce_add_3d(&tmDQ, stg, h * D + chalf * 32, (i0 + j) * FB_N + qd * 32, b);
+        bulk_commit();
+      }
+    };
+
+    for (int it = 0; it < n_it; ++it) {
+      const int qs = it % FB_NS;
+      const int qi = (i0 + it) * FB_N;
+      mbar_wait(st_full, it & 1);
+      mbar_wait(&q_full[qs], (it / FB_NS) & 1);
+      tc_fence_after();
+      const float* slse = sv + qs * 2 * FB_N;
+      const float* sdel = slse + FB_N;
+      const bool need_mask = (qi + FB_N > S) || (CAUSAL && qi < k0 + FB_M - 1);
+      const int qlo = CAUSAL ? key : 0;
+      uint32_t pp[32], pg[32];  // packed bf16x2 P^T / dS^T for this thread's 64 queries
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        const int c = chalf * 64 + cc * 32;
+        uint32_t rs[32], rd[32];
+        tmem_ld32(tS + trow + c, rs);
+        tmem_ld32(tdP + trow + c, rd);
+        tmem_ld_wait();
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          const float4 lq = *reinterpret_cast<const float4*>(slse + c + 4 * g);
+          const float4 dq = *reinterpret_cast<const float4*>(sdel + c + 4 * g);
+          const float l4[4] = {lq.x, lq.y, lq.z, lq.w};
+          const float d4[4] = {dq.x, dq.y, dq.z, dq.w};
+          float p[4], gr[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int i = 4 * g + t;
+            float pv = fast_exp2(fmaf(__uint_as_float(rs[i]), scale_log2, -l4[t]));
+            if (need_mask) {
+              const int q = qi + c + i;
+              pv = (q >= qlo && q < S) ? pv : 0.f;
+            }
+            p[t] = pv;
+            gr[t] = pv * (__uint_as_float(rd[i]) - d4[t]);
+          }
+          const __nv_bfloat162 p01 = __floats2bfloat162_rn(p[0], p[1]);
+          const __nv_bfloat162 p23 = __floats2bfloat162_rn(p[2], p[3]);
+          const __nv_bfloat162 g01 = __floats2bfloat162_rn(gr[0], gr[1]);
+          const __nv_bfloat162 g23 = __floats2bfloat162_rn(gr[2], gr[3]);
+          pp[cc * 16 + 2 * g] = *reinterpret_cast<const uint32_t*>(&p01);
+          pp[cc * 16 + 2 * g + 1] = *reinterpret_cast<const uint32_t*>(&p23);
+          pg[cc * 16 + 2 * g] = *reinterpret_cast<const uint32_t*>(&g01);
+          pg[cc * 16 + 2 * g + 1] = *reinterpret_cast<const uint32_t*>(&g23);
+        }
+      }
+      // S/dP consumed: the next block's S^T/dP^T MMAs may overwrite them
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(st_empty);
+      // P^T/dS^T smem free once the previous block's gradient MMAs finished
+      mbar_wait(p_empty, (it & 1) ^ 1);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t sw = (k ^ (r & 7)) << 4;
+        sts128(rowP + sw, make_uint4(pp[4 * k], pp[4 * k + 1], pp[4 * k + 2], pp[4 * k + 3]));
+        sts128(rowG + sw, make_uint4(pg[4 * k], pg[4 * k + 1], pg[4 * k + 2], pg[4 * k + 3]));
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+      if (it >= 1) drain_dq(it - 1);
+    }
+    drain_dq(n_it - 1);
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    {
+      const int c = chalf * 32;
+      uint32_t rk[32], rv[32];
+      tmem_ld32(tDK + trow + c, rk);
+      tmem_ld32(tDV + trow + c, rv);
+      tmem_ld_wait();
+      if (key < S) {
+        __nv_bfloat16* row = dqkv + (static_cast<int64_t>(b) * S + key) * (3 * Hd) + h * D + c;
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          float fk[8], fv[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            fk[t] = __uint_as_float(rk[i + t]) * scale;
+            fv[t] = __uint_as_float(rv[i + t]);
+          }
+          *reinterpret_cast<uint4*>(row + Hd + i) = pack8(fk);
+          *reinterpret_cast<uint4*>(row + 2 * Hd + i) = pack8(fv);
+        }
+      }
+    }
+    if (lane == 0) bulk_wait_all();
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// delta[b,h,s] = sum_d O * dO (fp32) and dQacc[t, :] = 0, one (token, head)
+// row per 8-lane group.
+__global__ void __launch_bounds__(256) attn_delta_zero_kernel(
+    const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
+    float* __restrict__ delta, float* __restrict__ dq_acc, int64_t tokens, int S, int H) {
+  constexpr int G = FB_D / 8;
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / G;
+  const int li = lane % G;
+  float acc = 0.f;
+  const bool ok = row < tokens * H;
+  if (ok) {
+    const int64_t off = row * FB_D + li * 8;
+    float a[8], g[8];
+    unpack8(*reinterpret_cast<const uint4*>(o + off), a);
+    unpack8(*reinterpret_cast<const uint4*>(dout + off), g);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc += a[j] * g[j];
+    float4* z = reinterpret_cast<float4*>(dq_acc + off);
+    z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+#pragma unroll
+  for (int m = G / 2; m > 0; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+  if (ok && li == 0) {
+    const int64_t t = row / H;
+    const int h = static_cast<int>(row % H);
+    const int64_t b = t / S, s = t % S;
+    delta[(b * H + h) * S + s] = acc;
+  }
+}
+
+// dqkv[t, 0:Hd] = bf16(dQacc[t, :] * scale)
+__global__ void __launch_bounds__(256) dq_convert_kernel(const float* __restrict__ dq_acc,
+                                                         __nv_bfloat16* __restrict__ dqkv,
+                                                         int64_t tokens, int Hd, float scale) {
+  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 8;
+  if (i >= tokens * Hd) return;
+  const int64_t t = i / Hd;
+  const int c = static_cast<int>(i % Hd);
+  const float4 a = reinterpret_cast<const float4*>(dq_acc + i)[0];
+  const float4 b = reinterpret_cast<const float4*>(dq_acc + i)[1];
+  float f[8] = {a.x * scale, a.y * scale, a.z * scale, a.w * scale,
+                b.x * scale, b.y * scale, b.z * scale, b.w * scale};
+  *reinterpret_cast<uint4*>(dqkv + t * (3 * static_cast<int64_t>(Hd)) + c) = pack8(f);
+}
+
+template <bool CAUSAL>
+int fused_t(const void* qkv, const void* o, const void* dout, const float* lse, float* delta,
+            float* dq_acc, void* dqkv, int64_t B, int64_t S, int64_t H, cudaStream_t st) {
+  using L = FbSmem;
+  constexpr int D = FB_D;
+  const int64_t tokens = B * S;
+  const int Hd = static_cast<int>(H * D);
+  CUtensorMap tq, tdo, tdq;
+  if (!make_tmap_bsc(&tq, qkv, 3 * H * D, S, B, 128) ||
+      !make_tmap_bsc(&tdo, dout, H * D, S, B, 128) ||
+      !make_tmap_bsc_f32(&tdq, dq_acc, H * D, S, B, 32))
+    return VP_ERR_UNSUPPORTED;
+  auto k = attn_bwd_fused<CAUSAL>;
+  static bool set = false;
+  if (!set) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+    if (e != cudaSuccess) return e;
+    set = true;
+  }
+  const int64_t rows = tokens * H;
+  attn_delta_zero_kernel<<<static_cast<unsigned>((rows * (D / 8) + 255) / 256), 256, 0, st>>>(
+      reinterpret_cast<const __nv_bfloat16*>(o), reinterpret_cast<const __nv_bfloat16*>(dout),
+      delta, dq_acc, tokens, static_cast<int>(S), static_cast<int>(H));
+  const float scale = 1.f / sqrtf(static_cast<float>(D));
+  const float scale_log2 = 1.4426950408889634f * scale;
+  const int n_kb = static_cast<int>((S + FB_M - 1) / FB_M);
+  const int BH = static_cast<int>(B * H);
+  k<<<static_cast<unsigned>(n_kb * BH), FB_THREADS, L::TOTAL, st>>>(
+      tq, tdo, tdq, lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), static_cast<int>(S),
+      static_cast<int>(H), BH, scale_log2, scale);
+  dq_convert_kernel<<<static_cast<unsigned>((tokens * Hd / 8 + 255) / 256), 256, 0, st>>>(
+      dq_acc, reinterpret_cast<__nv_bfloat16*>(dqkv), tokens, Hd, scale);
+  return launch_status();
+}
+
+}  // namespace
+
+// Workspace of the fused backward: delta [B*H*S] then dQacc [B*S*H*D] (fp32),
+// dQacc 16-byte aligned.
+int64_t attention_bwd_fused_ws(int64_t B, int64_t S, int64_t H, int64_t D) {
+  const int64_t d = (B * H * S + 3) / 4 * 4;
+  return d + B * S * H * D;
+}
+
+bool attention_bwd_fused_ok(int64_t D) { return D == FB_D; }
+
+int attention_bwd_fused(const void* qkv, const void* o, const void* dout, const float* lse,
+                        void* dqkv, float* ws, int64_t B, int64_t S, int64_t H, int causal,
+                        cudaStream_t st) {
+  float* delta = ws;
+  float* dq_acc = ws + (B * H * S + 3) / 4 * 4;
+  return causal ? fused_t<true>(qkv, o, dout, lse, delta, dq_acc, dqkv, B, S, H, st)
+                : fused_t<false>(qkv, o, dout, lse, delta, dq_acc, dqkv, B, S, H, st);
+}
+
+}  // namespace vp

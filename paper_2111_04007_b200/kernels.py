@@ -31,6 +31,8 @@ _SIGS = {
     "vp_layernorm_bwd": [vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, c_int, vp, vp],
     "vp_attention_fwd": [vp, vp, vp, i64, i64, i64, i64, c_int, vp],
     "vp_attention_bwd": [vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, c_int, vp],
+    "vp_attention_bwd_ex": [vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, i64, c_int, c_int, vp],
+    "vp_attention_bwd_ws_elems": [i64, i64, i64, i64],
     "vp_embed_fwd": [vp, vp, vp, vp, i64, i64, i64, vp],
     "vp_embed_bwd": [vp, vp, vp, vp, i64, i64, i64, vp],
     "vp_xent_fwd_bwd": [vp, vp, vp, vp, i64, i64, f32, vp],
@@ -61,6 +63,7 @@ for _name, _args in _SIGS.items():
     if _fn is not None:
         _fn.argtypes = _args
         _fn.restype = c_int
+L.vp_attention_bwd_ws_elems.restype = ctypes.c_int64
 
 
 # Kernel launches issued through this module (the bench's gpu_launches
@@ -162,12 +165,24 @@ def attention_fwd(qkv, out, lse, batch, seq, heads, head_dim, causal=True, strea
     return out
 
 
-def attention_bwd(qkv, out, dout, lse, dqkv, delta_ws, batch, seq, heads, head_dim, causal=True,
-                  stream=None):
+def attention_bwd_ws_elems(batch, seq, heads, head_dim) -> int:
+    return int(L.vp_attention_bwd_ws_elems(batch, seq, heads, head_dim))
+
+
+def attention_bwd(qkv, out, dout, lse, dqkv, ws, batch, seq, heads, head_dim, causal=True,
+                  stream=None, deterministic=False):
+    """dqkv = d(qkv). ``ws``: fp32 workspace of attention_bwd_ws_elems()
+    elements. head_dim 64 runs the fused one-pass kernel (dQ accumulated by
+    TMA reduce-add); ``deterministic`` (or other head dims) the two-kernel
+    path."""
+    need = attention_bwd_ws_elems(batch, seq, heads, head_dim)
+    if ws.numel() < need or ws.dtype != torch.float32:
+        raise ValueError(f"attention_bwd: workspace needs {need} fp32 elements")
     _count(3)
-    check(L.vp_attention_bwd(qkv.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(),
-                             dqkv.data_ptr(), delta_ws.data_ptr(), batch, seq, heads, head_dim,
-                             int(causal), _stream(stream)), "vp_attention_bwd")
+    check(L.vp_attention_bwd_ex(qkv.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(),
+                                dqkv.data_ptr(), ws.data_ptr(), ws.numel(), batch, seq, heads,
+                                head_dim, int(causal), 1 if deterministic else 0,
+                                _stream(stream)), "vp_attention_bwd")
     return dqkv
 
 

@@ -287,7 +287,8 @@ class GPT2Stage:
         self.dc = torch.empty(T, h, **bf)
         self.do = torch.empty(T, h, **bf)
         self.dqkv = torch.empty(T, 3 * h, **bf)
-        self.delta = torch.empty(self.mb * cfg.heads * cfg.seq_len, **f32)
+        self.delta = torch.empty(K.attention_bwd_ws_elems(self.mb, cfg.seq_len, cfg.heads,
+                                                          cfg.head_dim), **f32)
         self.ln_ws = torch.empty(K.layernorm_ws_elems(h), **f32)
         bias_cols = max(4 * h, cfg.vocab_size) if (self.bert and self.spec.last) else 4 * h
         self.bias_ws = torch.empty(K.bias_grad_ws_elems(bias_cols), **f32)

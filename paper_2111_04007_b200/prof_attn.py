@@ -13,7 +13,7 @@ o = torch.empty(B * S, H * D, device="cuda", dtype=torch.bfloat16)
 lse = torch.empty(B * H * S, device="cuda")
 do = torch.randn_like(o)
 dqkv = torch.empty_like(qkv)
-delta = torch.empty_like(lse)
+delta = torch.empty(K.attention_bwd_ws_elems(B, S, H, D), device="cuda")
 for _ in range(2):
     K.attention_fwd(qkv, o, lse, B, S, H, D, True)
     K.attention_bwd(qkv, o, do, lse, dqkv, delta, B, S, H, D, True)
