@@ -10,7 +10,8 @@ import os
 from .errors import ConfigError, InfeasibleError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvpipe.so")
+# VP_LIB_PATH: load an alternative build (e.g. an instrumented one) instead
+LIB_PATH = os.environ.get("VP_LIB_PATH") or os.path.join(_HERE, "libvpipe.so")
 
 VP_OK = 0
 VP_ERR_ARGS = -1

@@ -28,31 +28,62 @@
 #include "sm100.cuh"
 #include "tmap.cuh"
 
+#include <type_traits>
+
 namespace vp {
+#ifdef VP_BWD_TRACE
+__device__ unsigned long long g_vp_trace[4][16][16];
+#define TR(slot) \
+  do { if (blockIdx.x < 4 && it < 16) g_vp_trace[blockIdx.x][it][slot] = clock64(); } while (0)
+#else
+#define TR(slot) do {} while (0)
+#endif
 namespace {
 
 constexpr int FB_M = 128;  // keys per CTA
 constexpr int FB_N = 128;  // queries per inner block
 constexpr int FB_D = 64;
-constexpr int FB_NS = 2;   // Q/dO ring stages
-constexpr int FB_CW = 8;   // compute warps
-constexpr int FB_THREADS = 128 + 32 * FB_CW;
+constexpr int FB_NS = 3;   // Q/dO ring stages
+constexpr int FB_CW = 8;   // softmax-gradient warps (4..11)
+constexpr int FB_DW = 4;   // dQ drain warps (12..15), one per TMEM lane quadrant
+constexpr int FB_THREADS = 128 + 32 * (FB_CW + FB_DW);
 
 struct FbSmem {
-  static constexpr int TILE = 128 * 128;                 // 128 rows x 64 bf16 (SW128)
+  static constexpr int TILE = 128 * 128;                     // 128 rows x 64 bf16 (SW128)
   static constexpr int K_OFF = 0;
   static constexpr int V_OFF = K_OFF + TILE;
-  static constexpr int Q_OFF = V_OFF + TILE;             // [NS] stride 2*TILE
-  static constexpr int DO_OFF = Q_OFF + TILE;            // [NS] stride 2*TILE
-  static constexpr int PT_OFF = Q_OFF + FB_NS * 2 * TILE;  // P^T: 2 chunks of 64 queries
-  static constexpr int DST_OFF = PT_OFF + 2 * TILE;        // dS^T: 2 chunks
-  static constexpr int STG_OFF = DST_OFF + 2 * TILE;       // dQ staging: 8 warps x 4 KB
-  static constexpr int LV_OFF = STG_OFF + FB_CW * 4096;    // lse/delta [NS][2][128] f32
+  static constexpr int Q_OFF = V_OFF + TILE;                 // [NS] {Q, dO}, stride 2*TILE
+  static constexpr int DST_OFF = Q_OFF + FB_NS * 2 * TILE;   // dS^T [2 buffers][2 chunks]
+  static constexpr int STG_OFF = DST_OFF + 2 * 2 * TILE;     // dQ staging: 4 warps x 4 KB
+  static constexpr int LV_OFF = STG_OFF + FB_DW * 4096;      // lse/delta [NS][2][128] f32
   static constexpr int BAR_OFF = LV_OFF + FB_NS * 2 * FB_N * 4;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
 static_assert(FbSmem::TOTAL <= 232448, "attention bwd smem");
 
+// D[tmem] (+)= A[tmem] * B[smem] (A: 128 lanes x 16 bf16 packed in 8 columns)
+__device__ __forceinline__ void umma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+      "r"(v[15])
+      : "memory");
+}
+
+// TMEM columns (512, one CTA per SM):
+//   [0,128) S^T   [128,256) dP^T   [256,320) dV   [320,384) dK   [384,448) dQ
+//   [448,512) P^T as packed bf16x2 (A operand of the dV MMA)
 template <bool CAUSAL>
 __global__ void __launch_bounds__(FB_THREADS, 1)
     attn_bwd_fused(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
@@ -66,16 +97,17 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* kv_full = bars + 0;
-  uint64_t* q_full = bars + 1;    // [NS]
-  uint64_t* q_empty = bars + 3;   // [NS]
-  uint64_t* st_full = bars + 5;
-  uint64_t* st_empty = bars + 6;
-  uint64_t* p_full = bars + 7;
-  uint64_t* p_empty = bars + 8;
-  uint64_t* dq_full = bars + 9;   // [2]
-  uint64_t* dq_empty = bars + 11; // [2]
-  uint64_t* acc_full = bars + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* q_full = bars + 1;     // [NS]
+  uint64_t* q_empty = bars + 4;    // [NS]
+  uint64_t* st_full = bars + 7;    // [2] per 64-query half of S^T/dP^T
+  uint64_t* st_empty = bars + 9;   // [2]
+  uint64_t* p_full = bars + 11;    // P^T (TMEM) + dS^T (smem) of a block written
+  uint64_t* pt_empty = bars + 12;  // dV MMA consumed P^T
+  uint64_t* ds_empty = bars + 13;  // [2] dK/dQ MMAs consumed dS^T buffer
+  uint64_t* dq_full = bars + 15;
+  uint64_t* dq_empty = bars + 16;
+  uint64_t* acc_full = bars + 17;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
 
   // longest-first order: all CTAs of key block 0 (most query blocks) first
   const int kb = static_cast<int>(blockIdx.x) / BH;
@@ -100,14 +132,15 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
       mbar_init(&q_full[i], 2);
       mbar_init(&q_empty[i], 1);
     }
-    mbar_init(st_full, 1);
-    mbar_init(st_empty, FB_CW);
-    mbar_init(p_full, FB_CW);
-    mbar_init(p_empty, 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&dq_full[i], 1);
-      mbar_init(&dq_empty[i], FB_CW);
+      mbar_init(&st_full[i], 1);
+      mbar_init(&st_empty[i], FB_CW);
+      mbar_init(&ds_empty[i], 1);
     }
+    mbar_init(p_full, FB_CW);
+    mbar_init(pt_empty, 1);
+    mbar_init(dq_full, 1);
+    mbar_init(dq_empty, FB_DW);
     mbar_init(acc_full, 1);
     fence_mbar_init();
   }
@@ -117,7 +150,7 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tS = tmem, tdP = tmem + 128, tDV = tmem + 256, tDK = tmem + 320,
-                 tDQ = tmem + 384;
+                 tDQ = tmem + 384, tP = tmem + 448;
 
   if (warp == 0) {
     // ===== producer =====
@@ -160,158 +193,159 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       // ===== MMA issuer =====
-      constexpr uint32_t idST = idesc_bf16(128, FB_N, false, false);
+      constexpr uint32_t idST = idesc_bf16(128, FB_N / 2, false, false);
       constexpr uint32_t idG = idesc_bf16(128, D, false, true);
       constexpr uint32_t idQ = idesc_bf16(128, D, true, true);
       const uint32_t sK = smem_u32(smem + L::K_OFF), sV = smem_u32(smem + L::V_OFF);
-      const uint32_t sPt = smem_u32(smem + L::PT_OFF), sdSt = smem_u32(smem + L::DST_OFF);
       mbar_wait(kv_full, 0);
       auto issue_grad = [&](int j) {
         const int qs = j % FB_NS;
         const uint32_t sQ = smem_u32(smem + L::Q_OFF + qs * 2 * L::TILE);
         const uint32_t sdO = sQ + L::TILE;
+        const uint32_t sdSt = smem_u32(smem + L::DST_OFF + (j & 1) * 2 * L::TILE);
         mbar_wait(p_full, j & 1);
-        mbar_wait(&dq_empty[j & 1], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
+        // dV += P^T dO (A = P^T from TMEM)
+#pragma unroll
+        for (int k = 0; k < FB_N / 16; ++k)
+          umma_f16_ts(tDV, tP + k * 8, sdesc_sw128(sdO + k * 2048, L::TILE, 1024), idG,
+                      (j > 0 || k > 0) ? 1u : 0u);
+        umma_commit(pt_empty);
+        // dK += dS^T Q
 #pragma unroll
         for (int k = 0; k < FB_N / 16; ++k) {
           const uint32_t koff = (k >> 2) * L::TILE + (k & 3) * 32;
-          const uint32_t acc = (j > 0 || k > 0) ? 1u : 0u;
-          umma_f16(tDV, sdesc_sw128(sPt + koff, 16, 1024), sdesc_sw128(sdO + k * 2048, L::TILE, 1024),
-                   idG, acc);
           umma_f16(tDK, sdesc_sw128(sdSt + koff, 16, 1024), sdesc_sw128(sQ + k * 2048, L::TILE, 1024),
-                   idG, acc);
+                   idG, (j > 0 || k > 0) ? 1u : 0u);
         }
+        umma_commit(&q_empty[qs]);  // Q_j, dO_j no longer needed
+        // dQ_j = dS K once the drain warps emptied dQ_{j-1}
+        mbar_wait(dq_empty, (j & 1) ^ 1);
+        tc_fence_after();
 #pragma unroll
         for (int k = 0; k < FB_M / 16; ++k)
-          umma_f16(tDQ + (j & 1) * 64, sdesc_sw128(sdSt + k * 2048, L::TILE, 1024),
+          umma_f16(tDQ, sdesc_sw128(sdSt + k * 2048, L::TILE, 1024),
                    sdesc_sw128(sK + k * 2048, L::TILE, 1024), idQ, k > 0 ? 1u : 0u);
-        umma_commit(p_empty);
-        umma_commit(&q_empty[qs]);
-        umma_commit(&dq_full[j & 1]);
+        umma_commit(dq_full);
+        umma_commit(&ds_empty[j & 1]);
       };
       for (int it = 0; it < n_it; ++it) {
         const int qs = it % FB_NS;
         const uint32_t sQ = smem_u32(smem + L::Q_OFF + qs * 2 * L::TILE);
         const uint32_t sdO = sQ + L::TILE;
         mbar_wait(&q_full[qs], (it / FB_NS) & 1);
-        mbar_wait(st_empty, (it & 1) ^ 1);
-        tc_fence_after();
+        TR(8);
+        // two 64-query halves: half 0 may overwrite TMEM as soon as every
+        // warp has loaded its half-0 columns of the previous block
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          umma_f16(tS, sdesc_sw128(sK + k * 32, 16, 1024), sdesc_sw128(sQ + k * 32, 16, 1024), idST,
-                   k > 0);
-          umma_f16(tdP, sdesc_sw128(sV + k * 32, 16, 1024), sdesc_sw128(sdO + k * 32, 16, 1024),
-                   idST, k > 0);
+        for (int hf = 0; hf < 2; ++hf) {
+          mbar_wait(&st_empty[hf], (it & 1) ^ 1);
+          if (hf == 0) TR(9); else TR(10);
+          tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            umma_f16(tS + hf * 64, sdesc_sw128(sK + k * 32, 16, 1024),
+                     sdesc_sw128(sQ + hf * 8192 + k * 32, 16, 1024), idST, k > 0);
+            umma_f16(tdP + hf * 64, sdesc_sw128(sV + k * 32, 16, 1024),
+                     sdesc_sw128(sdO + hf * 8192 + k * 32, 16, 1024), idST, k > 0);
+          }
+          umma_commit(&st_full[hf]);
         }
-        umma_commit(st_full);
         if (it >= 1) issue_grad(it - 1);
       }
       issue_grad(n_it - 1);
       umma_commit(acc_full);
     }
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && warp < 4 + FB_CW) {
     // ===== softmax-gradient warps: thread = key row =====
     const uint32_t qd = warp & 3;
     const int chalf = static_cast<int>(warp - 4) >> 2;
     const int r = qd * 32 + lane;
     const int key = k0 + r;
     const uint32_t trow = (qd * 32) << 16;
-    uint8_t* stg = smem + L::STG_OFF + (warp - 4) * 4096;
-    const uint32_t rowP = smem_u32(smem + L::PT_OFF + chalf * L::TILE + r * 128);
-    const uint32_t rowG = smem_u32(smem + L::DST_OFF + chalf * L::TILE + r * 128);
+    const uint32_t rowG = smem_u32(smem + L::DST_OFF + r * 128);
+    const uint32_t lv_base = smem_u32(sv);
 
-    auto drain_dq = [&](int j) {
-      const int buf = j & 1;
-      mbar_wait(&dq_full[buf], (j >> 1) & 1);
-      tc_fence_after();
-      uint32_t v[32];
-      tmem_ld32(tDQ + buf * 64 + trow + chalf * 32, v);
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&dq_empty[buf]);
-        bulk_wait_read<0>();  // previous reduce has read the staging tile
-      }
-      __syncwarp();
-      const uint32_t srow = smem_u32(stg + lane * 128);
+    // P^T, dS^T for 32 query columns starting at q0c into packed bf16x2 words
+    auto softmax_grad = [&](auto masked, const uint32_t (&rs)[32], const uint32_t (&rd)[32],
+                            uint32_t lv, int q0c, int qlo, uint32_t (&pp)[16],
+                            uint32_t (&pg)[16]) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        sts128(srow + ((k ^ (lane & 7)) << 4),
-               make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]));
-      fence_async_smem();
-      __syncwarp();
-      if (lane == 0) {
-        tma_reduce_add_3d(&tmDQ, stg, h * D + chalf * 32, (i0 + j) * FB_N + qd * 32, b);
-        bulk_commit();
+      for (int g = 0; g < 8; ++g) {
+        const float4 l4 = lds128f(lv + 16 * g);
+        const float4 d4 = lds128f(lv + FB_N * 4 + 16 * g);
+        const float lq[4] = {l4.x, l4.y, l4.z, l4.w};
+        const float dq[4] = {d4.x, d4.y, d4.z, d4.w};
+        float p[4], gr[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int i = 4 * g + t;
+          float pv = fast_exp2(fmaf(__uint_as_float(rs[i]), scale_log2, -lq[t]));
+          if constexpr (decltype(masked)::value) {
+            const int q = q0c + i;
+            pv = (q >= qlo && q < S) ? pv : 0.f;
+          }
+          p[t] = pv;
+          gr[t] = pv * (__uint_as_float(rd[i]) - dq[t]);
+        }
+        const __nv_bfloat162 p01 = __floats2bfloat162_rn(p[0], p[1]);
+        const __nv_bfloat162 p23 = __floats2bfloat162_rn(p[2], p[3]);
+        const __nv_bfloat162 g01 = __floats2bfloat162_rn(gr[0], gr[1]);
+        const __nv_bfloat162 g23 = __floats2bfloat162_rn(gr[2], gr[3]);
+        pp[2 * g] = *reinterpret_cast<const uint32_t*>(&p01);
+        pp[2 * g + 1] = *reinterpret_cast<const uint32_t*>(&p23);
+        pg[2 * g] = *reinterpret_cast<const uint32_t*>(&g01);
+        pg[2 * g + 1] = *reinterpret_cast<const uint32_t*>(&g23);
       }
     };
 
     for (int it = 0; it < n_it; ++it) {
       const int qs = it % FB_NS;
       const int qi = (i0 + it) * FB_N;
-      mbar_wait(st_full, it & 1);
-      mbar_wait(&q_full[qs], (it / FB_NS) & 1);
-      tc_fence_after();
-      const float* slse = sv + qs * 2 * FB_N;
-      const float* sdel = slse + FB_N;
       const bool need_mask = (qi + FB_N > S) || (CAUSAL && qi < k0 + FB_M - 1);
       const int qlo = CAUSAL ? key : 0;
-      uint32_t pp[32], pg[32];  // packed bf16x2 P^T / dS^T for this thread's 64 queries
+      const uint32_t dsb = rowG + (it & 1) * 2 * L::TILE;
+      if (warp == 4 && lane == 0) TR(0);
+      mbar_wait(&q_full[qs], (it / FB_NS) & 1);
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc) {
-        const int c = chalf * 64 + cc * 32;
-        uint32_t rs[32], rd[32];
+        const int c = cc * 64 + chalf * 32;
+        uint32_t rs[32], rd[32], pp[16], pg[16];
+        mbar_wait(&st_full[cc], it & 1);
+        if (warp == 4 && lane == 0) { if (cc == 0) TR(1); else TR(3); }
+        tc_fence_after();
         tmem_ld32(tS + trow + c, rs);
         tmem_ld32(tdP + trow + c, rd);
         tmem_ld_wait();
-#pragma unroll
-        for (int g = 0; g < 8; ++g) {
-          const float4 lq = *reinterpret_cast<const float4*>(slse + c + 4 * g);
-          const float4 dq = *reinterpret_cast<const float4*>(sdel + c + 4 * g);
-          const float l4[4] = {lq.x, lq.y, lq.z, lq.w};
-          const float d4[4] = {dq.x, dq.y, dq.z, dq.w};
-          float p[4], gr[4];
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const int i = 4 * g + t;
-            float pv = fast_exp2(fmaf(__uint_as_float(rs[i]), scale_log2, -l4[t]));
-            if (need_mask) {
-              const int q = qi + c + i;
-              pv = (q >= qlo && q < S) ? pv : 0.f;
-            }
-            p[t] = pv;
-            gr[t] = pv * (__uint_as_float(rd[i]) - d4[t]);
-          }
-          const __nv_bfloat162 p01 = __floats2bfloat162_rn(p[0], p[1]);
-          const __nv_bfloat162 p23 = __floats2bfloat162_rn(p[2], p[3]);
-          const __nv_bfloat162 g01 = __floats2bfloat162_rn(gr[0], gr[1]);
-          const __nv_bfloat162 g23 = __floats2bfloat162_rn(gr[2], gr[3]);
-          pp[cc * 16 + 2 * g] = *reinterpret_cast<const uint32_t*>(&p01);
-          pp[cc * 16 + 2 * g + 1] = *reinterpret_cast<const uint32_t*>(&p23);
-          pg[cc * 16 + 2 * g] = *reinterpret_cast<const uint32_t*>(&g01);
-          pg[cc * 16 + 2 * g + 1] = *reinterpret_cast<const uint32_t*>(&g23);
+        // this half of S/dP consumed: the next block's half may overwrite it
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&st_empty[cc]);
+        const uint32_t lv = lv_base + (qs * 2 * FB_N + c) * 4;
+        if (need_mask)
+          softmax_grad(std::true_type{}, rs, rd, lv, qi + c, qlo, pp, pg);
+        else
+          softmax_grad(std::false_type{}, rs, rd, lv, qi + c, qlo, pp, pg);
+        if (warp == 4 && lane == 0) { if (cc == 0) TR(2); else TR(4); }
+        if (cc == 0) {
+          mbar_wait(pt_empty, (it & 1) ^ 1);                  // dV of the previous block done
+          mbar_wait(&ds_empty[it & 1], ((it >> 1) & 1) ^ 1);  // dS^T buffer free
+          tc_fence_after();
+          if (warp == 4 && lane == 0) TR(5);
         }
-      }
-      // S/dP consumed: the next block's S^T/dP^T MMAs may overwrite them
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(st_empty);
-      // P^T/dS^T smem free once the previous block's gradient MMAs finished
-      mbar_wait(p_empty, (it & 1) ^ 1);
+        tmem_st16(tP + trow + (c >> 1), pp);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const uint32_t sw = (k ^ (r & 7)) << 4;
-        sts128(rowP + sw, make_uint4(pp[4 * k], pp[4 * k + 1], pp[4 * k + 2], pp[4 * k + 3]));
-        sts128(rowG + sw, make_uint4(pg[4 * k], pg[4 * k + 1], pg[4 * k + 2], pg[4 * k + 3]));
+        for (int k = 0; k < 4; ++k)
+          sts128(dsb + cc * L::TILE + (((chalf * 4 + k) ^ (r & 7)) << 4),
+                 make_uint4(pg[4 * k], pg[4 * k + 1], pg[4 * k + 2], pg[4 * k + 3]));
       }
+      tmem_st_wait();
+      tc_fence_before();
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
-      if (it >= 1) drain_dq(it - 1);
+      if (warp == 4 && lane == 0) TR(6);
     }
-    drain_dq(n_it - 1);
     mbar_wait(acc_full, 0);
     tc_fence_after();
     {
@@ -332,6 +366,43 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
           }
           *reinterpret_cast<uint4*>(row + Hd + i) = pack8(fk);
           *reinterpret_cast<uint4*>(row + 2 * Hd + i) = pack8(fv);
+        }
+      }
+    }
+  } else if (warp >= 4 + FB_CW) {
+    // ===== dQ drain: TMEM -> smem (fp32, SW128) -> TMA reduce-add =====
+    const uint32_t qd = warp & 3;
+    const uint32_t trow = (qd * 32) << 16;
+    uint8_t* stg = smem + L::STG_OFF + qd * 4096;
+    for (int j = 0; j < n_it; ++j) {
+      mbar_wait(dq_full, j & 1);
+      tc_fence_after();
+      uint32_t v0[32], v1[32];
+      tmem_ld32(tDQ + trow, v0);
+      tmem_ld32(tDQ + trow + 32, v1);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dq_empty);
+      const int q = (i0 + j) * FB_N + qd * 32;
+      const uint32_t s0 = smem_u32(stg + lane * 128);
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        if (lane == 0) bulk_wait_read<0>();  // previous reduce has read the staging tile
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t* v = half ? v1 : v0;
+          sts128(s0 + ((k ^ (lane & 7)) << 4),
+                 make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]));
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+#ifndef VP_NO_DQ_REDUCE
+          tma_reduce_add_3d(&tmDQ, stg, h * D + half * 32, q, b);
+#endif
+          bulk_commit();
         }
       }
     }
@@ -449,3 +520,9 @@ int attention_bwd_fused(const void* qkv, const void* o, const void* dout, const 
 }
 
 }  // namespace vp
+
+#ifdef VP_BWD_TRACE
+extern "C" int vp_debug_bwd_trace(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, vp::g_vp_trace, sizeof(vp::g_vp_trace));
+}
+#endif
