@@ -47,6 +47,9 @@ constexpr int FB_NS = 3;   // Q/dO ring stages
 constexpr int FB_CW = 8;   // softmax-gradient warps (4..11)
 constexpr int FB_DW = 4;   // dQ drain warps (12..15), one per TMEM lane quadrant
 constexpr int FB_THREADS = 128 + 32 * (FB_CW + FB_DW);
+#ifndef FB_SPLIT_S
+#define FB_SPLIT_S 0
+#endif
 
 struct FbSmem {
   static constexpr int TILE = 128 * 128;                     // 128 rows x 64 bf16 (SW128)
@@ -193,7 +196,7 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       // ===== MMA issuer =====
-      constexpr uint32_t idST = idesc_bf16(128, FB_N / 2, false, false);
+      constexpr uint32_t idST = idesc_bf16(128, FB_SPLIT_S ? FB_N / 2 : FB_N, false, false);
       constexpr uint32_t idG = idesc_bf16(128, D, false, true);
       constexpr uint32_t idQ = idesc_bf16(128, D, true, true);
       const uint32_t sK = smem_u32(smem + L::K_OFF), sV = smem_u32(smem + L::V_OFF);
@@ -237,6 +240,7 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
         TR(8);
         // two 64-query halves: half 0 may overwrite TMEM as soon as every
         // warp has loaded its half-0 columns of the previous block
+#if FB_SPLIT_S
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {
           mbar_wait(&st_empty[hf], (it & 1) ^ 1);
@@ -251,6 +255,21 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
           }
           umma_commit(&st_full[hf]);
         }
+#else
+        mbar_wait(&st_empty[0], (it & 1) ^ 1);
+        mbar_wait(&st_empty[1], (it & 1) ^ 1);
+        TR(9);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          umma_f16(tS, sdesc_sw128(sK + k * 32, 16, 1024), sdesc_sw128(sQ + k * 32, 16, 1024),
+                   idST, k > 0);
+          umma_f16(tdP, sdesc_sw128(sV + k * 32, 16, 1024), sdesc_sw128(sdO + k * 32, 16, 1024),
+                   idST, k > 0);
+        }
+        umma_commit(&st_full[0]);
+        umma_commit(&st_full[1]);
+#endif
         if (it >= 1) issue_grad(it - 1);
       }
       issue_grad(n_it - 1);
