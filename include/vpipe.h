@@ -134,6 +134,15 @@ int vp_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y
 int vp_layernorm_bwd(const void* dy, const void* x, const void* gamma, const float* mean,
                      const float* rstd, void* dx, float* dgamma, float* dbeta, int64_t rows,
                      int64_t cols, int accumulate, float* workspace, void* stream);
+/* fp32 workspace elements of vp_layernorm_bwd(_ex) for rows of `cols`. */
+int64_t vp_layernorm_ws_elems(int64_t cols);
+/* As vp_layernorm_bwd, plus (dsum != NULL) dsum[cols] += column sums of the
+ * finished dx — the bias gradient of the residual branch feeding dx — in the
+ * same pass. Deterministic (fixed-order cross-CTA reduction). */
+int vp_layernorm_bwd_ex(const void* dy, const void* x, const void* gamma, const float* mean,
+                        const float* rstd, void* dx, float* dgamma, float* dbeta, float* dsum,
+                        int64_t rows, int64_t cols, int accumulate, float* workspace,
+                        void* stream);
 
 /* Causal/bidirectional fused attention over packed qkv[T, 3h] (T = B*S),
  * heads of size head_dim; o[T, h] bf16; lse[B*heads*S] fp32 saved for bwd. */
@@ -180,7 +189,10 @@ int vp_gelu_bwd(const void* dy, const void* pre, void* dx, int64_t n, void* stre
 int vp_xent_fwd_bwd(void* logits, const int64_t* labels, float* loss_rows, float* loss_sum,
                     int64_t rows, int64_t vocab, float scale, void* stream);
 
-/* Column sum of dy[rows, cols] (bf16) accumulated into dbias (fp32). */
+/* Column sum of dy[rows, cols] (bf16) accumulated into dbias (fp32), one
+ * launch, deterministic. workspace: vp_bias_grad_ws_elems(cols) floats,
+ * zero-filled before its first use (arrival counters; left at zero). */
+int64_t vp_bias_grad_ws_elems(int64_t cols);
 int vp_bias_grad(const void* dy, float* dbias, int64_t rows, int64_t cols, float* workspace,
                  void* stream);
 

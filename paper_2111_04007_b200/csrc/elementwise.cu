@@ -186,18 +186,40 @@ __global__ void __launch_bounds__(THREADS)
 // ---------------------------------------------------------------- bias grad
 // Block = 32 column-groups (8 bf16 columns each, one 16-byte load) x 8
 // row-lanes; blockIdx.y = row chunk. Fixed-order reductions (deterministic).
-__global__ void __launch_bounds__(256) colsum_partial(const __nv_bfloat16* __restrict__ dy,
-                                                      float* __restrict__ ws, int64_t rows,
-                                                      int64_t cols, int64_t rows_per_part) {
-  __shared__ float sh[8][32 * 8 + 4];
+// Column sums of dy[rows, cols] (bf16) added into out[cols] (fp32) in one
+// launch. CTA (column block of 256 = 32 lanes x 8 columns, row part) sums
+// its rows with 8 row-lanes x 4 loads in flight into ws[part][cols]; the last
+// CTA of a column block to finish (arrival counter) adds the parts in a fixed
+// order, so the result does not depend on CTA timing. The counter is reset
+// by that CTA, so the workspace stays reusable (zero-filled once).
+__global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __restrict__ dy,
+                                                     float* __restrict__ ws,
+                                                     unsigned* __restrict__ counters,
+                                                     float* __restrict__ out, int64_t rows,
+                                                     int64_t cols, int64_t rpp, int parts) {
+  __shared__ float sh[8][256 + 4];
+  __shared__ bool is_last;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int64_t c0 = (static_cast<int64_t>(blockIdx.x) * 32 + tx) * 8;
-  const int64_t r0 = blockIdx.y * rows_per_part;
-  const int64_t r1 = min(rows, r0 + rows_per_part);
+  const int64_t cb = static_cast<int64_t>(blockIdx.x) * 256;
+  const int64_t c0 = cb + tx * 8;
+  const int64_t r0 = blockIdx.y * rpp;
+  const int64_t r1 = min(rows, r0 + rpp);
   float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (c0 < cols) {
-#pragma unroll 4
-    for (int64_t r = r0 + ty; r < r1; r += 8) {
+    int64_t r = r0 + ty;
+    for (; r + 24 < r1; r += 32) {
+      uint4 u[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) u[k] = *reinterpret_cast<const uint4*>(dy + (r + 8 * k) * cols + c0);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float f[8];
+        unpack8(u[k], f);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] += f[j];
+      }
+    }
+    for (; r < r1; r += 8) {
       float f[8];
       unpack8(*reinterpret_cast<const uint4*>(dy + r * cols + c0), f);
 #pragma unroll
@@ -207,32 +229,41 @@ __global__ void __launch_bounds__(256) colsum_partial(const __nv_bfloat16* __res
 #pragma unroll
   for (int j = 0; j < 8; ++j) sh[ty][tx * 8 + j] = acc[j];
   __syncthreads();
-  const int64_t cb = static_cast<int64_t>(blockIdx.x) * 256;
-  for (int i = threadIdx.x; i < 256; i += 256) {
-    if (cb + i >= cols) break;
+  {
+    const int i = threadIdx.x;
     float t = 0.f;
 #pragma unroll
     for (int k = 0; k < 8; ++k) t += sh[k][i];
-    ws[blockIdx.y * cols + cb + i] = t;
+    if (cb + i < cols) ws[static_cast<int64_t>(blockIdx.y) * cols + cb + i] = t;
   }
-}
-__global__ void __launch_bounds__(256) colsum_final(const float* __restrict__ ws,
-                                                    float* __restrict__ out, int parts,
-                                                    int64_t cols) {
-  __shared__ float sh[8][33];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int64_t c = static_cast<int64_t>(blockIdx.x) * 32 + tx;
-  float acc = 0.f;
-  if (c < cols)
-    for (int p = ty; p < parts; p += 8) acc += ws[p * cols + c];
-  sh[ty][tx] = acc;
+  __threadfence();
   __syncthreads();
-  if (ty == 0 && c < cols) {
+  if (threadIdx.x == 0) is_last = atomicAdd(&counters[blockIdx.x], 1u) == static_cast<unsigned>(parts - 1);
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  // fixed-order sum of the parts: thread (tx, ty) takes parts ty, ty+8, ...
+  float f[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (c0 < cols) {
+    for (int p = ty; p < parts; p += 8) {
+      const float4* src = reinterpret_cast<const float4*>(ws + static_cast<int64_t>(p) * cols + c0);
+      const float4 a = __ldcg(src), b = __ldcg(src + 1);
+      f[0] += a.x; f[1] += a.y; f[2] += a.z; f[3] += a.w;
+      f[4] += b.x; f[5] += b.y; f[6] += b.z; f[7] += b.w;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 8; ++j) sh[ty][tx * 8 + j] = f[j];
+  __syncthreads();
+  {
+    const int i = threadIdx.x;
     float t = 0.f;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) t += sh[i][tx];
-    out[c] += t;
+    for (int k = 0; k < 8; ++k) t += sh[k][i];
+    if (cb + i < cols) out[cb + i] += t;
   }
+  if (threadIdx.x == 0) counters[blockIdx.x] = 0u;
 }
 
 // ------------------------------------------------------------ dropout / add
@@ -450,20 +481,28 @@ extern "C" int vp_xent_fwd_bwd(void* logits, const int64_t* labels, float* loss_
   return launch_status();
 }
 
-// workspace >= 256 * cols floats.
+// workspace: vp_bias_grad_ws_elems(cols) floats, zero-filled before first use
+// (the arrival counters live at its end and are left at zero).
+static constexpr int64_t kColsumMaxParts = 128;
+extern "C" int64_t vp_bias_grad_ws_elems(int64_t cols) {
+  return kColsumMaxParts * cols + (cols + 255) / 256 + 64;
+}
+
 extern "C" int vp_bias_grad(const void* dy, float* dbias, int64_t rows, int64_t cols,
                             float* workspace, void* stream) {
   if (rows <= 0 || cols <= 0 || !workspace) return VP_ERR_ARGS;
   if (cols % 8) return VP_ERR_UNSUPPORTED;
   const int64_t col_blocks = (cols + 255) / 256;
-  // ~4 waves of 148 SMs worth of blocks
-  // ~32 rows per partition (4 per row-lane): enough CTAs in flight to cover
-  // HBM latency; partials stay small (parts x cols fp32)
-  int parts = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(256, (rows + 31) / 32)));
+  // ~4 CTAs per SM, >= 32 rows per part, <= kColsumMaxParts parts
+  int64_t parts = (4 * static_cast<int64_t>(device_sms()) + col_blocks - 1) / col_blocks;
+  parts = std::min<int64_t>(parts, std::max<int64_t>(1, rows / 32));
+  parts = std::max<int64_t>(1, std::min<int64_t>(parts, kColsumMaxParts));
   const int64_t rpp = (rows + parts - 1) / parts;
-  dim3 grid(static_cast<unsigned>(col_blocks), parts);
-  colsum_partial<<<grid, 256, 0, ST>>>(CBF(dy), workspace, rows, cols, rpp);
-  colsum_final<<<blocks_for(cols, 32), 256, 0, ST>>>(workspace, dbias, parts, cols);
+  parts = (rows + rpp - 1) / rpp;
+  unsigned* counters = reinterpret_cast<unsigned*>(workspace + kColsumMaxParts * cols);
+  dim3 grid(static_cast<unsigned>(col_blocks), static_cast<unsigned>(parts));
+  colsum_kernel<<<grid, 256, 0, ST>>>(CBF(dy), workspace, counters, dbias, rows, cols, rpp,
+                                      static_cast<int>(parts));
   return launch_status();
 }
 

@@ -33,6 +33,9 @@ _SIGS = {
     "vp_attention_bwd": [vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, c_int, vp],
     "vp_attention_bwd_ex": [vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, i64, c_int, c_int, vp],
     "vp_attention_bwd_ws_elems": [i64, i64, i64, i64],
+    "vp_layernorm_ws_elems": [i64],
+    "vp_bias_grad_ws_elems": [i64],
+    "vp_layernorm_bwd_ex": [vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, c_int, vp, vp],
     "vp_embed_fwd": [vp, vp, vp, vp, i64, i64, i64, vp],
     "vp_embed_bwd": [vp, vp, vp, vp, i64, i64, i64, vp],
     "vp_xent_fwd_bwd": [vp, vp, vp, vp, i64, i64, f32, vp],
@@ -64,6 +67,8 @@ for _name, _args in _SIGS.items():
         _fn.argtypes = _args
         _fn.restype = c_int
 L.vp_attention_bwd_ws_elems.restype = ctypes.c_int64
+L.vp_layernorm_ws_elems.restype = ctypes.c_int64
+L.vp_bias_grad_ws_elems.restype = ctypes.c_int64
 
 
 # Kernel launches issued through this module (the bench's gpu_launches
@@ -144,17 +149,20 @@ def layernorm_fwd(x, gamma, beta, y, mean, rstd, eps=1e-5, stream=None):
 
 
 def layernorm_ws_elems(cols: int) -> int:
-    return 2 * 1024 * cols
+    return int(L.vp_layernorm_ws_elems(cols))
 
 
 def layernorm_bwd(dy, x, gamma, mean, rstd, dx, dgamma, dbeta, workspace, accumulate=False,
-                  stream=None):
+                  stream=None, dsum=None):
+    """dx (= or += when ``accumulate``) and dgamma/dbeta += (fp32). ``dsum``
+    (optional fp32 [cols]) += the column sum of the finished dx: the bias
+    gradient of a residual branch whose output gradient is dx."""
     rows, cols = x.shape
-    _count(3)
-    check(L.vp_layernorm_bwd(dy.data_ptr(), x.data_ptr(), gamma.data_ptr(), mean.data_ptr(),
-                             rstd.data_ptr(), dx.data_ptr(), dgamma.data_ptr(), dbeta.data_ptr(),
-                             rows, cols, int(accumulate), workspace.data_ptr(), _stream(stream)),
-          "vp_layernorm_bwd")
+    _count(2 if cols <= 1024 else 3)
+    check(L.vp_layernorm_bwd_ex(dy.data_ptr(), x.data_ptr(), gamma.data_ptr(), mean.data_ptr(),
+                                rstd.data_ptr(), dx.data_ptr(), dgamma.data_ptr(),
+                                dbeta.data_ptr(), _p(dsum), rows, cols, int(accumulate),
+                                workspace.data_ptr(), _stream(stream)), "vp_layernorm_bwd")
     return dx
 
 
@@ -230,12 +238,13 @@ def xent_fwd_bwd(logits, labels, loss_rows, scale, loss_sum=None, stream=None):
 
 
 def bias_grad_ws_elems(cols: int) -> int:
-    return 256 * cols
+    """fp32 elements of the bias_grad workspace; allocate it zero-filled."""
+    return int(L.vp_bias_grad_ws_elems(cols))
 
 
 def bias_grad(dy, dbias, workspace, stream=None):
     rows, cols = dy.shape
-    _count(2)
+    _count(1)
     check(L.vp_bias_grad(dy.data_ptr(), dbias.data_ptr(), rows, cols, workspace.data_ptr(),
                          _stream(stream)), "vp_bias_grad")
 

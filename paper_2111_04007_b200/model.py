@@ -291,7 +291,7 @@ class GPT2Stage:
                                                           cfg.head_dim), **f32)
         self.ln_ws = torch.empty(K.layernorm_ws_elems(h), **f32)
         bias_cols = max(4 * h, cfg.vocab_size) if (self.bert and self.spec.last) else 4 * h
-        self.bias_ws = torch.empty(K.bias_grad_ws_elems(bias_cols), **f32)
+        self.bias_ws = torch.zeros(K.bias_grad_ws_elems(bias_cols), **f32)
         if self.spec.last:
             self.lnf_out = torch.empty(T, h, **bf)
             self.lnf_mean = torch.empty(T, **f32)
@@ -456,8 +456,13 @@ class GPT2Stage:
         K.gemm(self.logits, wte, self.dc, b_kmajor=False, stream=stream)
         K.gemm(self.logits, self.lnf_out, P.g(self.head_weight_name), a_kmajor=False,
                b_kmajor=False, epilogue=K.EPI_ACC_F32, stream=stream)
+        # d(stage output) leaves the final LN; its column sum is the FC2 bias
+        # gradient of the top layer (fused into the LN backward when p = 0)
+        fused = cfg.dropout <= 0
+        self._fc2_done = fused
         K.layernorm_bwd(self.dc, x, P.w("lnf_g"), self.lnf_mean, self.lnf_rstd, self.g,
-                        P.g("lnf_g"), P.g("lnf_b"), self.ln_ws, accumulate=False, stream=stream)
+                        P.g("lnf_g"), P.g("lnf_b"), self.ln_ws, accumulate=False, stream=stream,
+                        dsum=P.g(f"l{self.spec.layers[-1]}.b_fc2") if fused else None)
         return self.loss_rows
 
     def _mlm_head(self, labels, loss_scale, loss_sum, stream):
@@ -496,40 +501,52 @@ class GPT2Stage:
         K.dropout_(self.drop_tmp, self.cfg.dropout, dseed, which * g.numel(), stream)
         return self.drop_tmp
 
-    def _layer_bwd(self, li: int, w: _LayerWS, x: torch.Tensor, dseed: int, stream=None):
-        """self.g holds d(layer output); on return it holds d(layer input)."""
+    def _layer_bwd(self, li: int, w: _LayerWS, x: torch.Tensor, dseed: int, stream=None,
+                   fc2_done: bool = False, lower: Optional[int] = None) -> bool:
+        """self.g holds d(layer output); on return it holds d(layer input).
+        ``fc2_done``: this layer's FC2 bias gradient (= column sum of g) was
+        already accumulated by the LN backward that produced g. ``lower``:
+        the layer below in this stage, whose FC2 bias gradient the LN1
+        backward here accumulates in the same pass (returns True if so)."""
         cfg, P = self.cfg, self.params
         p = f"l{li}."
         g = self.g
+        fused = cfg.dropout <= 0  # dropout masks the branch gradients
         # --- MLP: out = x1 + fc2(gelu(fc1(ln2(x1))))
         gy = self._drop_grad(g, dseed, 1, stream)
         K.gemm(gy, P.w(p + "w_fc2"), self.dpre, b_kmajor=False, epilogue=K.EPI_DGELU,
                aux=w.pre, stream=stream)
         K.gemm(gy, w.f, P.g(p + "w_fc2"), a_kmajor=False, b_kmajor=False,
                epilogue=K.EPI_ACC_F32, stream=stream)
-        K.bias_grad(gy, P.g(p + "b_fc2"), self.bias_ws, stream)
+        if not (fc2_done and fused):
+            K.bias_grad(gy, P.g(p + "b_fc2"), self.bias_ws, stream)
         K.gemm(self.dpre, P.w(p + "w_fc1"), self.dc, b_kmajor=False, stream=stream)
         K.gemm(self.dpre, w.c, P.g(p + "w_fc1"), a_kmajor=False, b_kmajor=False,
                epilogue=K.EPI_ACC_F32, stream=stream)
         K.bias_grad(self.dpre, P.g(p + "b_fc1"), self.bias_ws, stream)
+        # g += LN2 backward; with p = 0 its column sum is the proj bias gradient
         K.layernorm_bwd(self.dc, w.x1, P.w(p + "ln2_g"), w.mean2, w.rstd2, g,
                         P.g(p + "ln2_g"), P.g(p + "ln2_b"), self.ln_ws, accumulate=True,
-                        stream=stream)
+                        stream=stream, dsum=P.g(p + "b_o") if fused else None)
         # --- attention: x1 = x + proj(attn(qkv(ln1(x))))
         gy = self._drop_grad(g, dseed, 0, stream)
         K.gemm(gy, P.w(p + "w_o"), self.do, b_kmajor=False, stream=stream)
         K.gemm(gy, w.o, P.g(p + "w_o"), a_kmajor=False, b_kmajor=False,
                epilogue=K.EPI_ACC_F32, stream=stream)
-        K.bias_grad(gy, P.g(p + "b_o"), self.bias_ws, stream)
+        if not fused:
+            K.bias_grad(gy, P.g(p + "b_o"), self.bias_ws, stream)
         K.attention_bwd(w.qkv, w.o, self.do, w.lse, self.dqkv, self.delta, self.mb,
                         cfg.seq_len, cfg.heads, cfg.head_dim, cfg.causal, stream)
         K.gemm(self.dqkv, P.w(p + "w_qkv"), self.dc, b_kmajor=False, stream=stream)
         K.gemm(self.dqkv, w.a, P.g(p + "w_qkv"), a_kmajor=False, b_kmajor=False,
                epilogue=K.EPI_ACC_F32, stream=stream)
         K.bias_grad(self.dqkv, P.g(p + "b_qkv"), self.bias_ws, stream)
+        # g = d(layer input) = d(output of the layer below)
+        lower_fc2 = P.g(f"l{lower}.b_fc2") if (fused and lower is not None) else None
         K.layernorm_bwd(self.dc, x, P.w(p + "ln1_g"), w.mean1, w.rstd1, g,
                         P.g(p + "ln1_g"), P.g(p + "ln1_b"), self.ln_ws, accumulate=True,
-                        stream=stream)
+                        stream=stream, dsum=lower_fc2)
+        return lower_fc2 is not None
 
     def backward(self, grad_out: Optional[torch.Tensor], ids: Optional[torch.Tensor],
                  dseed: int = 0, stream=None, types: Optional[torch.Tensor] = None) -> torch.Tensor:
@@ -539,14 +556,20 @@ class GPT2Stage:
         Returns d(stage input) (in ``self.g``); on stage 0 it is consumed by
         the embedding backward instead."""
         cfg, P = self.cfg, self.params
+        fc2_done = False
         if grad_out is not None:
             self.g.copy_(grad_out)
+        elif self.spec.last:
+            fc2_done = getattr(self, "_fc2_done", False)
+            self._fc2_done = False
         for i in range(len(self.spec.layers) - 1, -1, -1):
             li = self.spec.layers[i]
             if self.bert:
                 self._layer_bwd_post(li, self.ws[i], self.xs[i], stream)
             else:
-                self._layer_bwd(li, self.ws[i], self.xs[i], dseed * 1315423911 + li, stream)
+                lower = self.spec.layers[i - 1] if i > 0 else None
+                fc2_done = self._layer_bwd(li, self.ws[i], self.xs[i], dseed * 1315423911 + li,
+                                           stream, fc2_done=fc2_done, lower=lower)
         if self.spec.first:
             if cfg.dropout > 0:
                 K.dropout_(self.g, cfg.dropout, dseed ^ 0x5EED, 7 * self.g.numel(), stream)

@@ -44,8 +44,18 @@ def test_layernorm(rows, cols):
     assert rel(db, br.grad) < 1e-3
     # accumulate mode adds into an existing residual gradient
     dx2 = dy.clone()
-    K.layernorm_bwd(dy, x, g, mean, rstd, dx2, dg, db, ws, accumulate=True)
+    dsum = torch.zeros(cols, device="cuda")
+    K.layernorm_bwd(dy, x, g, mean, rstd, dx2, dg, db, ws, accumulate=True, dsum=dsum)
     assert rel(dx2, xr.grad + dy.float()) < 1e-2
+    # dsum = column sums of the finished (accumulated) dx, in the same pass
+    assert rel(dsum, (xr.grad + dy.float()).sum(0)) < 1e-2
+    assert rel(dsum, dx2.float().sum(0)) < 1e-2
+    # deterministic: the same call twice gives identical parameter sums
+    a1, b1 = torch.zeros(cols, device="cuda"), torch.zeros(cols, device="cuda")
+    a2, b2 = torch.zeros(cols, device="cuda"), torch.zeros(cols, device="cuda")
+    K.layernorm_bwd(dy, x, g, mean, rstd, dx, a1, b1, ws)
+    K.layernorm_bwd(dy, x, g, mean, rstd, dx, a2, b2, ws)
+    assert torch.equal(a1, a2) and torch.equal(b1, b2)
 
 
 def ref_attention(qkv, B, S, H, D, causal):
@@ -157,9 +167,18 @@ def test_bias_grad_and_misc():
     torch.manual_seed(0)
     dy = torch.randn(8192, 3072, device="cuda").bfloat16()
     db = torch.ones(3072, device="cuda")
-    ws = torch.empty(K.bias_grad_ws_elems(3072), device="cuda")
+    ws = torch.zeros(K.bias_grad_ws_elems(3072), device="cuda")
     K.bias_grad(dy, db, ws)
     assert rel(db, 1 + dy.float().sum(0)) < 1e-5
+    # one-launch reduction: deterministic, workspace reusable, ragged shapes
+    for rows, cols in ((8192, 3072), (77, 1024), (5000, 264), (1, 8)):
+        x = torch.randn(rows, cols, device="cuda").bfloat16()
+        w = torch.zeros(K.bias_grad_ws_elems(cols), device="cuda")
+        o1, o2 = torch.zeros(cols, device="cuda"), torch.zeros(cols, device="cuda")
+        K.bias_grad(x, o1, w)
+        K.bias_grad(x, o2, w)
+        assert torch.equal(o1, o2)
+        assert rel(o1, x.float().sum(0)) < 1e-5
     a = torch.randn(1000, 24, device="cuda").bfloat16()
     b = torch.randn(1000, 24, device="cuda").bfloat16()
     y = torch.empty_like(a)
