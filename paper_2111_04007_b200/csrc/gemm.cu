@@ -322,6 +322,19 @@ constexpr int kEpiWarps2 = 8;                          // 2 per TMEM lane quadra
 constexpr int kThreads2 = 128 + 32 * kEpiWarps2;
 constexpr int kStagingPerWarp = 8192;                  // 2 x 4 KB epilogue buffers
 constexpr int kSmem2 = kStages2 * kStageBytes2 + kEpiWarps2 * kStagingPerWarp + 512 + 1024;
+// Per-epilogue pipeline shape: single-output epilogues stage through one
+// 4 KB buffer per warp and spend the freed shared memory on a 6th operand
+// stage (more TMA bytes in flight: the mainloop of K=1024 tiles otherwise
+// waits on L2 latency ~20% of the time); two-buffer epilogues (an aux tile
+// prefetched or two outputs) keep 8 KB per warp and 5 stages.
+template <int EPI>
+struct G2Cfg {
+  static constexpr bool kTwoBuf = EPI == VP_EPI_BIAS_GELU || EPI == VP_EPI_BIAS_RESID ||
+                                  EPI == VP_EPI_DGELU || EPI == VP_EPI_RESID;
+  static constexpr int kStages = kTwoBuf ? 5 : 6;
+  static constexpr int kStaging = kTwoBuf ? 8192 : 4096;
+  static constexpr int kSmem = kStages * kStageBytes2 + kEpiWarps2 * kStaging + 512 + 1024;
+};
 
 struct Epi2 {
   const __nv_bfloat16* bias;
@@ -383,18 +396,22 @@ __device__ __forceinline__ void load_row_swizzled(const uint8_t* buf, uint32_t r
   }
 }
 
+#ifdef VP_GEMM_TRACE
+__device__ unsigned long long g_vp_gemm_trace[296][4];
+#endif
 template <int EPI, bool A_MN, bool B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX,
                  int64_t M, int64_t N, int64_t K, int split_k, Epi2 epi) {
+  using C = G2Cfg<EPI>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  uint8_t* staging = smem + kStages2 * kStageBytes2;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(staging + kEpiWarps2 * kStagingPerWarp);
-  uint64_t* empty_bar = full_bar + kStages2;
-  uint64_t* tfull_bar = empty_bar + kStages2;  // [2]
+  uint8_t* staging = smem + C::kStages * kStageBytes2;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(staging + kEpiWarps2 * C::kStaging);
+  uint64_t* empty_bar = full_bar + C::kStages;
+  uint64_t* tfull_bar = empty_bar + C::kStages;  // [2]
   uint64_t* tempty_bar = tfull_bar + 2;        // [2] (leader's are used)
   uint64_t* aux_bar = tempty_bar + 2;          // [kEpiWarps2][2] aux-tile TMA prefetch
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + 2 * kEpiWarps2);
@@ -417,7 +434,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     tma_prefetch(&tmD);
-    for (int s = 0; s < kStages2; ++s) {
+    for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
@@ -468,7 +485,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             tma_load_2d_2sm(sb, &tmB, &full_bar[stage], n0, k0);
             tma_load_2d_2sm(sb + 64 * BK * 2, &tmB, &full_bar[stage], n0 + 64, k0);
           }
-          if (++stage == kStages2) { stage = 0; phase ^= 1; }
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -477,15 +494,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       // ===== MMA issuer (leader CTA only) =====
       constexpr uint32_t idesc = idesc_bf16(256, 256, A_MN, B_MN);
       uint32_t stage = 0, phase = 0, local = 0;
+#ifdef VP_GEMM_TRACE
+      unsigned long long w_full = 0, w_tempty = 0, t_begin = clock64();
+#endif
       for (int64_t u = cid; u < n_units; u += n_clusters, ++local) {
         int64_t mb, nb, kb0, kb1;
         unit_coords(u, mb, nb, kb0, kb1);
         const uint32_t acc = local & 1;
+#ifdef VP_GEMM_TRACE
+        unsigned long long t0 = clock64();
+#endif
         mbar_wait(&tempty_bar[acc], ((local >> 1) & 1) ^ 1);
+#ifdef VP_GEMM_TRACE
+        w_tempty += clock64() - t0;
+#endif
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * 256;
         for (int64_t kb = kb0; kb < kb1; ++kb) {
+#ifdef VP_GEMM_TRACE
+          unsigned long long t1 = clock64();
+#endif
           mbar_wait(&full_bar[stage], phase);
+#ifdef VP_GEMM_TRACE
+          w_full += clock64() - t1;
+#endif
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * kStageBytes2);
           const uint32_t sb = sa + 128 * BK * 2;
@@ -498,17 +530,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             umma_f16_2sm(tmem_d, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
           umma_commit_2sm(&empty_bar[stage], 0x3);
-          if (++stage == kStages2) { stage = 0; phase ^= 1; }
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
         umma_commit_2sm(&tfull_bar[acc], 0x3);
       }
+#ifdef VP_GEMM_TRACE
+      g_vp_gemm_trace[blockIdx.x][0] = w_full;
+      g_vp_gemm_trace[blockIdx.x][1] = w_tempty;
+      g_vp_gemm_trace[blockIdx.x][2] = clock64() - t_begin;
+      g_vp_gemm_trace[blockIdx.x][3] = local;
+#endif
     }
   } else if (warp >= 4) {
     // ===== Epilogue (both CTAs): rows [rank*128 + q*32, +32) of the tile,
     // columns [half*128, +128) =====
     const uint32_t q = warp & 3;
     const uint32_t half = (warp - 4) >> 2;
-    uint8_t* wbuf = staging + (warp - 4) * kStagingPerWarp;
+    uint8_t* wbuf = staging + (warp - 4) * C::kStaging;
     uint32_t local = 0, nbuf = 0;
     const uint32_t lane = lane_id();
     for (int64_t u = cid; u < n_units; u += n_clusters, ++local) {
@@ -528,8 +566,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
           uint32_t raw[32];
           tmem_ld32(taddr + c, raw);
           tmem_ld_wait();
-          uint8_t* buf = wbuf + (nbuf & 1) * 4096;
-          if (lane == 0) bulk_wait_read<1>();
+          uint8_t* buf = wbuf + (C::kTwoBuf ? (nbuf & 1) * 4096 : 0);
+          if (lane == 0) {
+            if constexpr (C::kTwoBuf) bulk_wait_read<1>();
+            else bulk_wait_read<0>();
+          }
           __syncwarp();
           uint4 ch[8];
 #pragma unroll
@@ -615,9 +656,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
               bulk_commit();
             }
           } else {
-            uint8_t* buf = wbuf + (kAuxIn ? ci : (nbuf & 1)) * 4096;
+            uint8_t* buf = wbuf + (kAuxIn ? ci : (C::kTwoBuf ? (nbuf & 1) : 0)) * 4096;
             if (!kAuxIn) {
-              if (lane == 0) bulk_wait_read<1>();
+              if (lane == 0) {
+                if constexpr (C::kTwoBuf) bulk_wait_read<1>();
+                else bulk_wait_read<0>();
+              }
               __syncwarp();
             }
             uint4 ch[8];
@@ -756,13 +800,14 @@ int launch2_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& t
   auto kern = gemm2_kernel<EPI, A_MN, B_MN>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2);
+    cudaError_t err =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G2Cfg<EPI>::kSmem);
     if (err != cudaSuccess) return err;
     attr_set = true;
   }
   const int64_t units = ((M + 255) / 256) * ((N + 255) / 256) * split_k;
   const int64_t clusters = std::min<int64_t>(units, sm_count() / 2);
-  kern<<<static_cast<unsigned>(2 * clusters), kThreads2, kSmem2, st>>>(ta, tb, td, tx, M, N, K,
+  kern<<<static_cast<unsigned>(2 * clusters), kThreads2, G2Cfg<EPI>::kSmem, st>>>(ta, tb, td, tx, M, N, K,
                                                                         split_k, e);
   return cudaGetLastError();
 }
@@ -891,3 +936,9 @@ extern "C" int vp_gemm_bf16_ex(int a_kmajor, int b_kmajor, int epilogue, const v
   return gemm_entry(a_kmajor, b_kmajor, epilogue, A, lda, B, ldb, D, ldd, bias, aux, ldaux, M, N,
                     K, flags, stream);
 }
+
+#ifdef VP_GEMM_TRACE
+extern "C" int vp_debug_gemm_trace(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, vp::g_vp_gemm_trace, sizeof(vp::g_vp_gemm_trace));
+}
+#endif
