@@ -46,6 +46,13 @@ struct TaSmem {
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
 
+#ifdef VP_BWD_TRACE
+__device__ unsigned long long g_vp_ftrace[4][32][8];
+#define TRF(j, slot) \
+  do { if (blockIdx.x < 1 && blockIdx.y < 4 && (j) < 32) g_vp_ftrace[blockIdx.y][j][slot] = clock64(); } while (0)
+#else
+#define TRF(j, slot) do {} while (0)
+#endif
 template <int D, bool CAUSAL>
 __global__ void __launch_bounds__(TA_THREADS, 2)
     attn_fwd_tc(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmKV,
@@ -129,6 +136,7 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
       auto issue_pv = [&](int j) {
         const int st = j % L::STAGES;
         mbar_wait(&p_full[j & 1], (j >> 1) & 1);  // P_j written (and O rescaled if needed)
+        TRF(j, 5);
         tc_fence_after();
         const uint32_t sV = smem_u32(smem + L::V_OFF + st * L::KTILE);
         const uint32_t sPj = sP + (j & 1) * 128 * TA_BN * 2;
@@ -147,6 +155,7 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
         const int st = j % L::STAGES;
         mbar_wait(&kv_full[st], (j / L::STAGES) & 1);
         mbar_wait(&s_empty[j & 1], ((j >> 1) & 1) ^ 1);
+        TRF(j, 4);
         tc_fence_after();
         const uint32_t sK = smem_u32(smem + L::K_OFF + st * L::KTILE);
 #pragma unroll
@@ -170,40 +179,58 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
     uint8_t* sP = smem + L::P_OFF;
     float m = -FLT_MAX, l = 0.f;
     for (int j = 0; j < n_kb; ++j) {
+      if (warp == 4 && lane == 0) TRF(j, 0);
       mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      if (warp == 4 && lane == 0) TRF(j, 1);
       tc_fence_after();
       const uint32_t ts = tmem + trow + (j & 1) * TA_BN;
       const int k0 = j * TA_BN;
       const bool need_mask = (k0 + TA_BN > S) || (CAUSAL && k0 + TA_BN - 1 > q0);
-      // pass 1: row max (8 independent partial maxima: short dependency chains).
+      // One TMEM read of the block's scores (64 fp32 per row, in registers);
+      // row max with 8 independent partial maxima (short dependency chains).
       // Masking is one compare per element against the row's key limit
       // (keys >= lim are dead: past the sequence or above the diagonal).
       const int lim = CAUSAL ? min(S, q + 1) : S;
+      uint32_t sc[TA_BN];
+      tmem_ld32(ts, *reinterpret_cast<uint32_t(*)[32]>(sc));
+      tmem_ld32(ts + 32, *reinterpret_cast<uint32_t(*)[32]>(sc + 32));
+      tmem_ld_wait();
+      // S_j consumed: the MMA warp may reuse this TMEM buffer
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[j & 1]);
+      if (need_mask) {
+#pragma unroll
+        for (int i = 0; i < TA_BN; ++i)
+          if (k0 + i >= lim) sc[i] = __float_as_uint(-FLT_MAX);
+      }
       float pm[8];
 #pragma unroll
       for (int t = 0; t < 8; ++t) pm[t] = -FLT_MAX;
 #pragma unroll
-      for (int c = 0; c < TA_BN; c += 32) {
-        uint32_t raw[32];
-        tmem_ld32(ts + c, raw);
-        tmem_ld_wait();
-        if (need_mask) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const float x = (k0 + c + i < lim) ? __uint_as_float(raw[i]) : -FLT_MAX;
-            pm[i & 7] = fmaxf(pm[i & 7], x);
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) pm[i & 7] = fmaxf(pm[i & 7], __uint_as_float(raw[i]));
-        }
-      }
+      for (int i = 0; i < TA_BN; ++i) pm[i & 7] = fmaxf(pm[i & 7], __uint_as_float(sc[i]));
       const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
                              fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
       const float m_cand = fmaxf(m, mx * scale_log2);
       const bool grow = m_cand > m + 8.f;   // lazy: keep a stale max unless it grew > 2^8
       const float m_new = grow ? m_cand : m;
       const float corr = fast_exp2(m - m_new);  // 1 when !grow; 0 for the first block
+      // P = exp2(s*scale - m) (masked -> 0), row sum
+      float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      uint4 pk[TA_BN / 8];
+#pragma unroll
+      for (int g = 0; g < TA_BN / 8; ++g) {
+        float f[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const float xs = __uint_as_float(sc[g * 8 + t]);
+          const float e = fast_exp2(fmaf(xs, scale_log2, -m_new));
+          f[t] = (!need_mask || xs != -FLT_MAX) ? e : 0.f;
+          ps[t] += f[t];
+        }
+        pk[g] = pack8(f);
+      }
+      if (warp == 4 && lane == 0) TRF(j, 2);
       // P buffer (j & 1) was last read by PV_{j-2}
       if (j >= 2) mbar_wait(&o_full[j & 1], ((j - 2) >> 1) & 1);
       if (j >= 1 && __any_sync(0xffffffffu, grow)) {
@@ -223,33 +250,14 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
           tmem_st_wait();
         }
       }
-      // pass 2: P = exp2(s*scale - m), row sum, P -> smem (bf16, swizzled)
-      float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int c = 0; c < TA_BN; c += 32) {
-        uint32_t raw[32];
-        tmem_ld32(ts + c, raw);
-        tmem_ld_wait();
-        // 32 keys = 4 x 16-byte chunks of the row's 128 B (64 keys)
+      {
         const uint32_t rowp = smem_u32(sP + (j & 1) * 128 * TA_BN * 2 + r * 128);
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          float f[8];
-#pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            const int i = g * 8 + t;
-            const float e = fast_exp2(fmaf(__uint_as_float(raw[i]), scale_log2, -m_new));
-            f[t] = (!need_mask || k0 + c + i < lim) ? e : 0.f;
-            ps[t] += f[t];
-          }
-          const int chunk = ((c & 63) >> 3) + g;
-          sts128(rowp + ((chunk ^ (r & 7)) << 4), pack8(f));
-        }
+        for (int g = 0; g < TA_BN / 8; ++g) sts128(rowp + ((g ^ (r & 7)) << 4), pk[g]);
       }
+      if (warp == 4 && lane == 0) TRF(j, 3);
       const float sum = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
       tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[j & 1]);
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[j & 1]);
@@ -858,6 +866,11 @@ int fwd_tc_t(const void* qkv, void* o, float* lse, int64_t B, int64_t S, int64_t
 
 }  // namespace
 
+#ifdef VP_BWD_TRACE
+extern "C" int vp_debug_fwd_trace(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, g_vp_ftrace, sizeof(g_vp_ftrace));
+}
+#endif
 int attention_fwd_tc(const void* qkv, void* o, float* lse, int64_t B, int64_t S, int64_t H,
                      int64_t D, int causal, cudaStream_t st) {
   if ((3 * H * D) % 8) return VP_ERR_UNSUPPORTED;
