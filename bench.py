@@ -35,7 +35,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-LADDER = {1: (1, 1), 2: (2, 1), 4: (4, 1), 8: (4, 2)}
+LADDER = {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (4, 2)}
 METRIC_NAMES = {"gpt2_355m": "GPT-2 355M", "gpt2_2_5b": "GPT-2 2.5B", "gpt2_8_3b": "GPT-2 8.3B",
                 "tiny": "tiny GPT-2", "bert_large": "BERT-large"}
 MODEL_CONFIGS = {  # name: (M_total, m)
@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--config", default="gpt2_355m", choices=sorted(MODEL_CONFIGS))
     ap.add_argument("--pd", default=None, help="override P x D, e.g. 4x2")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dispatch", default="opportunistic", choices=["opportunistic", "static"],
+                    help="P>1 task order: the reference's opportunistic policy over the "
+                         "calibration profile (default) or the static Varuna schedule")
     ap.add_argument("--cpu-sample-s", type=float, default=20.0)
     return ap.parse_args()
 
@@ -259,7 +262,20 @@ def main():
     stage_map = stage_map_for(cfg, P, m, args.config)
     pc = ParallelConfig(P, D, m, N, stage_map)
     init_dev = "cuda"
-    v = Varuna(cfg, pc, seed=0, init_device=init_dev)
+    # P > 1: the reference's opportunistic policy (sp/engine decide) run over
+    # the B200 calibration profile gives each stage its dispatch order; the
+    # static Varuna order would idle the faster stage (it is generated for
+    # uniform stage times).
+    prof_path = os.path.join(ROOT, "profiles", f"b200_{args.config}.yaml")
+    dispatch, prof = "static", None
+    if P > 1 and os.path.exists(prof_path) and args.dispatch == "opportunistic":
+        from paper_2111_04007_b200 import load_profile
+        prof = load_profile(prof_path)
+        if m in prof.m_grid and prof.num_cutpoints == cfg.n_layer:
+            dispatch = "opportunistic"
+        else:
+            prof = None
+    v = Varuna(cfg, pc, seed=0, init_device=init_dev, dispatch=dispatch, profile=prof)
     st = v.stream
     rows = m * N
     host = synthetic_batch(cfg, rows, v.replica)
@@ -361,7 +377,8 @@ def main():
     roof_samples = D * m / worst
 
     # measured stage profile -> reference bubble predictor (simulate_minibatch)
-    predicted = predicted_bubble(v, tl, P, D, N, m, stage_map, world, dev, dist)
+    predicted = predicted_bubble(v, tl, P, D, N, m, stage_map, world, dev, dist,
+                                 opportunistic=dispatch == "opportunistic")
 
     cpu = None
     if rank == 0:
@@ -383,7 +400,8 @@ def main():
                        "model": cfg_name(cfg), "global_batch": M, "seq_len": cfg.seq_len,
                        "parallelism": f"pp{P}xdp{D}", "stage_map_sizes":
                            [sum(1 for x in stage_map if x == s) for s in range(P)],
-                       "l2": "working set >> 126 MB L2 (no flush needed)", "dropout": cfg.dropout},
+                       "l2": "working set >> 126 MB L2 (no flush needed)", "dropout": cfg.dropout,
+                       "dispatch": dispatch},
             "clocks": clk,
             "e2e": e2e,
             "gpu_launches": launches,
@@ -405,7 +423,7 @@ def main():
     return 0
 
 
-def predicted_bubble(v, tl, P, D, N, m, stage_map, world, dev, dist):
+def predicted_bubble(v, tl, P, D, N, m, stage_map, world, dev, dist, opportunistic=False):
     """Feed the MEASURED per-stage F/R/B task times (this step, all ranks) to
     the bubble predictor (simulate_minibatch, sp/simulator.py:259-389) with
     zero transfer cost; returns its bubble fraction."""
@@ -436,7 +454,7 @@ def predicted_bubble(v, tl, P, D, N, m, stage_map, world, dev, dist):
     model = ModelSpec("stages", (1,) * P, (1,) * P)
     pc = ParallelConfig(P, D, m, N, tuple(range(P)))
     r = simulate_minibatch(v.schedule, pc, prof, build_placement(uniform_cluster(P * D, 8), P, D),
-                           model, opportunistic=False)
+                           model, opportunistic=opportunistic)
     return round(r.bubble_fraction, 4)
 
 
