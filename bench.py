@@ -104,6 +104,18 @@ def stage_map_for(cfg, P, m, config_name=None):
     return assign_stages(model, P, m, prof, last_stage_weight=0.75 if P > 1 else 1.0).stage_map
 
 
+def gemm_traffic():
+    """DRAM bytes per launch of the representative GEMM (FC1 shape) from the
+    committed ncu --set full capture (profiles/r01b_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01b_traffic.json")) as f:
+            t = json.load(f)
+        return {"bytes_per_launch": t["dram_bytes"], "algorithmic_bytes": t["algorithmic_bytes"],
+                "kernel": t["kernel"], "source": t["source"]}
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def cfg_name(cfg):
     return f"gpt2-L{cfg.n_layer}-h{cfg.hidden}"
 
@@ -408,7 +420,7 @@ def main():
             "roofline": {"bound": "tensor", "achieved": round(gemm_tf, 1),
                          "peak": sustained, "unit": "TFLOP/s",
                          "frac": round(gemm_tf / sustained, 4),
-                         "traffic": None,
+                         "traffic": gemm_traffic(),
                          "kernel": "vp_gemm_bf16 (tcgen05), all GEMM launches of one step",
                          "peak_kind": f"{src} bf16 sustained", "share_of_step": round(gemm_share, 3)},
             "stage_roofline": {"roofline_samples_per_s": round(roof_samples, 1),
