@@ -151,9 +151,8 @@ __device__ __forceinline__ void epilogue_chunk(const EpiArgs& e, int64_t row, in
 }
 
 __device__ __forceinline__ void tile_coords(int64_t t, int64_t tiles_m, int64_t tiles_n,
-                                            int64_t& mb, int64_t& nb) {
-  // Grouped rasterisation: 8 M-tiles share each sweep over N for L2 reuse of B.
-  constexpr int64_t G = 8;
+                                            int64_t& mb, int64_t& nb, int64_t G = 8) {
+  // Grouped rasterisation: G M-tiles share each sweep over N for L2 reuse of B.
   const int64_t per_group = G * tiles_n;
   const int64_t group = t / per_group;
   const int64_t first_m = group * G;
@@ -340,6 +339,7 @@ struct Epi2 {
   const __nv_bfloat16* bias;
   const __nv_bfloat16* aux_in;  // RESID / DGELU operand
   int64_t ldaux;
+  int64_t group;                // rasterisation group (M tiles per N sweep)
 };
 
 __device__ __forceinline__ void store_row_swizzled(uint8_t* buf, uint32_t row,
@@ -453,7 +453,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
 
   auto unit_coords = [&](int64_t u, int64_t& mb, int64_t& nb, int64_t& kb0, int64_t& kb1) {
     const int64_t t = u / split_k, ks = u % split_k;
-    tile_coords(t, tiles_m, tiles_n, mb, nb);
+    tile_coords(t, tiles_m, tiles_n, mb, nb, epi.group);
     kb0 = ks * kb_per;
     kb1 = min(n_kb, kb0 + kb_per);
   };
@@ -905,8 +905,10 @@ static int gemm_entry(int a_kmajor, int b_kmajor, int epilogue, const void* A, i
       }
       if (const char* f = getenv("VP_GEMM_SPLITK")) split = std::max(1, atoi(f));
     }
+    int64_t group = 8;
+    if (const char* g = getenv("VP_GEMM_GROUP")) group = std::max(1, atoi(g));
     Epi2 e{reinterpret_cast<const __nv_bfloat16*>(bias), reinterpret_cast<const __nv_bfloat16*>(aux),
-           ldaux};
+           ldaux, group};
     return gemm2_dispatch(epilogue, a_mn, b_mn, ta, tb, td, tx, M, N, K, split, e, st);
   }
   const int BNsel = N <= 128 ? 128 : 256;
