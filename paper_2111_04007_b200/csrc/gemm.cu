@@ -627,7 +627,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             __syncwarp();  // every lane has read its aux row before outputs overwrite it
           }
           epi2_apply<EPI>(epi, row, col0, M, N, v, pre, xin);
-          if constexpr (EPI == VP_EPI_BIAS_GELU) {
+          if (EPI == VP_EPI_BIAS_GELU && epi.aux_in != nullptr) {
             // pre-activation (aux) then activation (D): both buffers in turn
             if (lane == 0) bulk_wait_read<0>();
             __syncwarp();
@@ -870,15 +870,15 @@ static int gemm_entry(int a_kmajor, int b_kmajor, int epilogue, const void* A, i
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const bool f32_out = epilogue == VP_EPI_ACC_F32 || epilogue == VP_EPI_STORE_F32;
   const bool use2 = !(flags & VP_GEMM_DIRECT_STORE) && !getenv("VP_GEMM_1SM") &&
-                    !(epilogue == VP_EPI_BIAS_GELU && !aux) && (ldd % (f32_out ? 4 : 8)) == 0;
+                    (ldd % (f32_out ? 4 : 8)) == 0;
   if (use2) {
     CUtensorMap ta, tb, td, tx;
     bool ok = a_mn ? make_tmap(&ta, A, M, K, lda, 64, BK) : make_tmap(&ta, A, K, M, lda, BK, 128);
     ok = ok && (b_mn ? make_tmap(&tb, B, N, K, ldb, 64, BK) : make_tmap(&tb, B, K, N, ldb, BK, 128));
     ok = ok && (f32_out ? make_tmap(&td, D, N, M, ldd, 32, 32, true)
                         : make_tmap(&td, D, N, M, ldd, 64, 32));
-    if (epilogue == VP_EPI_BIAS_GELU || epilogue == VP_EPI_BIAS_RESID || epilogue == VP_EPI_DGELU ||
-        epilogue == VP_EPI_RESID)
+    if ((epilogue == VP_EPI_BIAS_GELU && aux) || epilogue == VP_EPI_BIAS_RESID ||
+        epilogue == VP_EPI_DGELU || epilogue == VP_EPI_RESID)
       ok = ok && make_tmap(&tx, aux, N, M, ldaux, 64, 32);
     else tx = td;
     if (!ok) return VP_ERR_UNSUPPORTED;

@@ -320,8 +320,10 @@ class GPT2Stage:
         self._proj_resid(w.o, P.w(p + "w_o"), P.w(p + "b_o"), x, w.x1, dseed, 0, stream)
         K.layernorm_fwd(w.x1, P.w(p + "ln2_g"), P.w(p + "ln2_b"), w.c, w.mean2, w.rstd2,
                         cfg.ln_eps, stream)
+        # the pre-activation is only needed by the backward: a non-saving
+        # forward (F on a recomputing stage) writes the GELU output alone
         K.gemm(w.c, P.w(p + "w_fc1"), w.f, epilogue=K.EPI_BIAS_GELU, bias=P.w(p + "b_fc1"),
-               aux=w.pre, stream=stream)
+               aux=w.pre if w is not self.scratch else None, stream=stream)
         self._proj_resid(w.f, P.w(p + "w_fc2"), P.w(p + "b_fc2"), w.x1, out, dseed, 1, stream)
 
     def _layer_fwd_post(self, li: int, x: torch.Tensor, out, w: _LayerWS, stream=None):

@@ -59,6 +59,9 @@ def test_gemm_epilogues():
     K.gemm(A, B, out, epilogue=K.EPI_BIAS_GELU, bias=bias, aux=pre)
     assert rel(pre, base + bias.float()) < 5e-3
     assert rel(out, gelu(base + bias.float())) < 1e-2
+    out_only = torch.empty_like(out)  # no pre-activation output (non-saving forward)
+    K.gemm(A, B, out_only, epilogue=K.EPI_BIAS_GELU, bias=bias)
+    assert torch.equal(out_only, out)
     res = torch.randn(M, N, device="cuda").bfloat16()
     out2 = res.clone()
     K.gemm(A, B, out2, epilogue=K.EPI_BIAS_RESID, bias=bias, aux=out2)
