@@ -436,14 +436,17 @@ def main():
 
 
 def predicted_bubble(v, tl, P, D, N, m, stage_map, world, dev, dist, opportunistic=False):
-    """Feed the MEASURED per-stage F/R/B task times (this step, all ranks) to
-    the bubble predictor (simulate_minibatch, sp/simulator.py:259-389) with
-    zero transfer cost; returns its bubble fraction."""
+    """The reference bubble predictor (simulate_minibatch, sp/simulator.py:
+    259-389) applied to the task order this run EXECUTED (every stage's
+    dispatch list, replayed statically) with the MEASURED per-stage mean
+    F/B times and R/F ratio, zero transfer cost; returns its bubble fraction."""
+    import numpy as np
     import torch
     from paper_2111_04007_b200 import (ModelSpec, ParallelConfig, build_placement,
                                        simulate_minibatch, uniform_cluster)
     from paper_2111_04007_b200.calibration import CalibrationProfile, CutpointTimes
     from paper_2111_04007_b200.core import KIND_BACKWARD, KIND_FORWARD, KIND_RECOMPUTE
+    from paper_2111_04007_b200.scheduler import Schedule
     sums = torch.zeros(world, 3, device=dev, dtype=torch.float64)
     cnt = {0: [], 1: [], 2: []}
     for kind, j, a, b in tl["tasks"]:
@@ -453,11 +456,22 @@ def predicted_bubble(v, tl, P, D, N, m, stage_map, world, dev, dist, opportunist
             sums[v.rank, col] = statistics.mean(cnt[kind])
     if world > 1:
         dist.all_reduce(sums)
-    stage_f = [0.0] * P
-    stage_b = [0.0] * P
-    for s in range(P):
-        stage_f[s] = float(sums[s, 0].item())
-        stage_b[s] = float(sums[s, 1].item())
+    stage_f = [float(sums[s, 0].item()) for s in range(P)]
+    stage_b = [float(sums[s, 1].item()) for s in range(P)]
+    rec = [float(sums[s, 2].item()) / stage_f[s] for s in range(P) if sums[s, 2] > 0 and stage_f[s]]
+    rscale = statistics.mean(rec) if rec else 1.0
+    tasks = [None] * world
+    if world > 1:
+        dist.all_gather_object(tasks, v.tasks)
+    else:
+        tasks = [v.tasks]
+    kinds, mbs, offs = [], [], [0]
+    for s in range(P):          # replica 0's ranks are 0..P-1
+        kinds += [k for k, _ in tasks[s]]
+        mbs += [j for _, j in tasks[s]]
+        offs.append(len(kinds))
+    sched = Schedule("executed", P, N, np.array(kinds, np.int64), np.array(mbs, np.int64),
+                     np.array(offs, np.int64), 1, 2, 1)
     # one cut-point per stage carrying the whole stage's time
     z = {m: 0}
     cps = tuple(CutpointTimes({m: max(1, round(stage_f[s]))}, {m: max(1, round(stage_b[s]))},
@@ -465,8 +479,8 @@ def predicted_bubble(v, tl, P, D, N, m, stage_map, world, dev, dist, opportunist
     prof = CalibrationProfile((m,), tuple(sorted({1, D})), cps)
     model = ModelSpec("stages", (1,) * P, (1,) * P)
     pc = ParallelConfig(P, D, m, N, tuple(range(P)))
-    r = simulate_minibatch(v.schedule, pc, prof, build_placement(uniform_cluster(P * D, 8), P, D),
-                           model, opportunistic=opportunistic)
+    r = simulate_minibatch(sched, pc, prof, build_placement(uniform_cluster(P * D, 8), P, D),
+                           model, opportunistic=False, recompute_scale=rscale)
     return round(r.bubble_fraction, 4)
 
 

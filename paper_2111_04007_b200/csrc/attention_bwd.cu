@@ -84,6 +84,16 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
       : "memory");
 }
 
+__device__ __forceinline__ void red_add_v4(float* p, uint32_t a, uint32_t b, uint32_t c,
+                                           uint32_t d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(__uint_as_float(a)),
+               "f"(__uint_as_float(b)), "f"(__uint_as_float(c)), "f"(__uint_as_float(d))
+               : "memory");
+}
+#ifndef FB_DQ_RED
+#define FB_DQ_RED 0
+#endif
+
 // TMEM columns (512, one CTA per SM):
 //   [0,128) S^T   [128,256) dP^T   [256,320) dV   [320,384) dK   [384,448) dQ
 //   [448,512) P^T as packed bf16x2 (A operand of the dV MMA)
@@ -92,7 +102,7 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
     attn_bwd_fused(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
                    const __grid_constant__ CUtensorMap tmDQ, const float* __restrict__ lse,
                    const float* __restrict__ delta, __nv_bfloat16* __restrict__ dqkv, int S, int H,
-                   int BH, float scale_log2, float scale) {
+                   int BH, float scale_log2, float scale, float* __restrict__ dq_acc) {
   using L = FbSmem;
   constexpr int D = FB_D;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -404,6 +414,19 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(dq_empty);
       const int q = (i0 + j) * FB_N + qd * 32;
+#if FB_DQ_RED
+      // vector reductions straight from registers into the fp32 accumulator
+      if (q + static_cast<int>(lane) < S) {
+        float* dst = dq_acc + (static_cast<int64_t>(b) * S + q + lane) * Hd + h * D;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          red_add_v4(dst + 4 * k, v0[4 * k], v0[4 * k + 1], v0[4 * k + 2], v0[4 * k + 3]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          red_add_v4(dst + 32 + 4 * k, v1[4 * k], v1[4 * k + 1], v1[4 * k + 2], v1[4 * k + 3]);
+      }
+      continue;
+#endif
       const uint32_t s0 = smem_u32(stg + lane * 128);
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
@@ -512,7 +535,7 @@ int fused_t(const void* qkv, const void* o, const void* dout, const float* lse, 
   const int BH = static_cast<int>(B * H);
   k<<<static_cast<unsigned>(n_kb * BH), FB_THREADS, L::TOTAL, st>>>(
       tq, tdo, tdq, lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), static_cast<int>(S),
-      static_cast<int>(H), BH, scale_log2, scale);
+      static_cast<int>(H), BH, scale_log2, scale, dq_acc);
   dq_convert_kernel<<<static_cast<unsigned>((tokens * Hd / 8 + 255) / 256), 256, 0, st>>>(
       dq_acc, reinterpret_cast<__nv_bfloat16*>(dqkv), tokens, Hd, scale);
   return launch_status();
