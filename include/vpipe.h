@@ -125,6 +125,16 @@ int vp_gemm_bf16(int a_kmajor, int b_kmajor, int epilogue, const void* A, int64_
 int vp_gemm_bf16_ex(int a_kmajor, int b_kmajor, int epilogue, const void* A, int64_t lda,
                     const void* B, int64_t ldb, void* D, int64_t ldd, const void* bias, void* aux,
                     int64_t ldaux, int64_t M, int64_t N, int64_t K, int flags, void* stream);
+/* As vp_gemm_bf16 (2-CTA path, bf16 output), plus dbias[n] += sum_m D[m, n]
+ * (fp32, before the bf16 rounding of D) fused into the epilogue: each warp
+ * writes its 32-row partial column sums to `workspace`
+ * (vp_gemm_dbias_ws_elems(M, N) floats), reduced in a fixed order afterwards
+ * (deterministic). Used for the FC1 bias gradient from the DGELU dgrad. */
+int64_t vp_gemm_dbias_ws_elems(int64_t M, int64_t N);
+int vp_gemm_bf16_dbias(int a_kmajor, int b_kmajor, int epilogue, const void* A, int64_t lda,
+                       const void* B, int64_t ldb, void* D, int64_t ldd, const void* bias,
+                       void* aux, int64_t ldaux, int64_t M, int64_t N, int64_t K, float* dbias,
+                       float* workspace, void* stream);
 
 /* LayerNorm over rows of x[rows, cols] (bf16 in/out, fp32 stats saved). */
 int vp_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean,

@@ -340,7 +340,33 @@ struct Epi2 {
   const __nv_bfloat16* aux_in;  // RESID / DGELU operand
   int64_t ldaux;
   int64_t group;                // rasterisation group (M tiles per N sweep)
+  float* colsum_ws;             // optional: per-32-row partial column sums of D (fp32)
 };
+
+// Sum of v[0..63] over the 32 lanes (rows) of a warp, scattered so that lane
+// l ends with the totals of columns 2l and 2l+1 (5 halving exchange steps:
+// 62 shuffles instead of 64 full butterflies).
+__device__ __forceinline__ float2 warp_colsum64(const float (&v)[64], uint32_t lane) {
+  float t[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const bool hi = lane & 16;
+    const float send = hi ? v[i] : v[i + 32];
+    const float keep = hi ? v[i + 32] : v[i];
+    t[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int w = 16, bit = 8; w >= 2; w >>= 1, bit >>= 1) {
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const bool hi = lane & bit;
+      const float send = hi ? t[i] : t[i + w];
+      const float keep = hi ? t[i + w] : t[i];
+      t[i] = keep + __shfl_xor_sync(0xffffffffu, send, bit);
+    }
+  }
+  return make_float2(t[0], t[1]);
+}
 
 __device__ __forceinline__ void store_row_swizzled(uint8_t* buf, uint32_t row,
                                                    const uint4 (&chunks)[8]) {
@@ -627,6 +653,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             __syncwarp();  // every lane has read its aux row before outputs overwrite it
           }
           epi2_apply<EPI>(epi, row, col0, M, N, v, pre, xin);
+          if (epi.colsum_ws != nullptr) {
+            // fused bias gradient: this warp's 32-row partial sums of the
+            // 64 output columns -> colsum_ws[row0 / 32][col]
+            if (row >= M) {
+#pragma unroll
+              for (int i = 0; i < 64; ++i) v[i] = 0.f;
+            }
+            const float2 cs = warp_colsum64(v, lane);
+            const int64_t c = col0 + 2 * lane;
+            if (c < N && row0 < M)
+              *reinterpret_cast<float2*>(epi.colsum_ws + (row0 >> 5) * N + c) = cs;
+          }
           if (EPI == VP_EPI_BIAS_GELU && epi.aux_in != nullptr) {
             // pre-activation (aux) then activation (D): both buffers in turn
             if (lane == 0) bulk_wait_read<0>();
@@ -852,7 +890,7 @@ extern "C" int vp_device_sm_count(int* out) {
 static int gemm_entry(int a_kmajor, int b_kmajor, int epilogue, const void* A, int64_t lda,
                       const void* B, int64_t ldb, void* D, int64_t ldd, const void* bias,
                       void* aux, int64_t ldaux, int64_t M, int64_t N, int64_t K, int flags,
-                      void* stream) {
+                      void* stream, float* colsum_ws = nullptr) {
   using namespace vp;
   if (M <= 0 || N <= 0 || K <= 0 || !A || !B || !D) return VP_ERR_ARGS;
   if ((lda % 8) || (ldb % 8) || (ldd % 8)) return VP_ERR_UNSUPPORTED;
@@ -871,6 +909,7 @@ static int gemm_entry(int a_kmajor, int b_kmajor, int epilogue, const void* A, i
   const bool f32_out = epilogue == VP_EPI_ACC_F32 || epilogue == VP_EPI_STORE_F32;
   const bool use2 = !(flags & VP_GEMM_DIRECT_STORE) && !getenv("VP_GEMM_1SM") &&
                     (ldd % (f32_out ? 4 : 8)) == 0;
+  if (colsum_ws && (!use2 || f32_out || (N % 2))) return VP_ERR_UNSUPPORTED;
   if (use2) {
     CUtensorMap ta, tb, td, tx;
     bool ok = a_mn ? make_tmap(&ta, A, M, K, lda, 64, BK) : make_tmap(&ta, A, K, M, lda, BK, 128);
@@ -905,10 +944,11 @@ static int gemm_entry(int a_kmajor, int b_kmajor, int epilogue, const void* A, i
       }
       if (const char* f = getenv("VP_GEMM_SPLITK")) split = std::max(1, atoi(f));
     }
+    if (colsum_ws) split = 1;
     int64_t group = 8;
     if (const char* g = getenv("VP_GEMM_GROUP")) group = std::max(1, atoi(g));
     Epi2 e{reinterpret_cast<const __nv_bfloat16*>(bias), reinterpret_cast<const __nv_bfloat16*>(aux),
-           ldaux, group};
+           ldaux, group, colsum_ws};
     return gemm2_dispatch(epilogue, a_mn, b_mn, ta, tb, td, tx, M, N, K, split, e, st);
   }
   const int BNsel = N <= 128 ? 128 : 256;
@@ -944,3 +984,50 @@ extern "C" int vp_debug_gemm_trace(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, vp::g_vp_gemm_trace, sizeof(vp::g_vp_gemm_trace));
 }
 #endif
+
+namespace vp {
+namespace {
+// dbias[c] += sum over parts of ws[part][c] in a fixed order (32 columns x 32
+// part-lanes per block, 8 independent loads per thread).
+__global__ void __launch_bounds__(1024) colsum_f32_reduce(const float* __restrict__ ws,
+                                                          float* __restrict__ out, int parts,
+                                                          int64_t cols) {
+  __shared__ float sh[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * 32 + tx;
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (c < cols) {
+    int p = ty;
+    for (; p + 7 * 32 < parts; p += 8 * 32) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[u] += ws[static_cast<int64_t>(p + u * 32) * cols + c];
+    }
+    for (; p < parts; p += 32) acc[0] += ws[static_cast<int64_t>(p) * cols + c];
+  }
+  sh[ty][tx] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+  __syncthreads();
+  if (ty == 0 && c < cols) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) t += sh[i][tx];
+    out[c] += t;
+  }
+}
+}  // namespace
+}  // namespace vp
+
+extern "C" int64_t vp_gemm_dbias_ws_elems(int64_t M, int64_t N) { return ((M + 31) / 32) * N; }
+
+extern "C" int vp_gemm_bf16_dbias(int a_kmajor, int b_kmajor, int epilogue, const void* A,
+                                  int64_t lda, const void* B, int64_t ldb, void* D, int64_t ldd,
+                                  const void* bias, void* aux, int64_t ldaux, int64_t M, int64_t N,
+                                  int64_t K, float* dbias, float* workspace, void* stream) {
+  if (!dbias || !workspace) return VP_ERR_ARGS;
+  int rc = gemm_entry(a_kmajor, b_kmajor, epilogue, A, lda, B, ldb, D, ldd, bias, aux, ldaux, M,
+                      N, K, 0, stream, workspace);
+  if (rc) return rc;
+  const int parts = static_cast<int>((M + 31) / 32);
+  vp::colsum_f32_reduce<<<static_cast<unsigned>((N + 31) / 32), 1024, 0,
+                          reinterpret_cast<cudaStream_t>(stream)>>>(workspace, dbias, parts, N);
+  return cudaGetLastError();
+}

@@ -34,6 +34,9 @@ _SIGS = {
     "vp_attention_bwd_ex": [vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, i64, c_int, c_int, vp],
     "vp_attention_bwd_ws_elems": [i64, i64, i64, i64],
     "vp_layernorm_ws_elems": [i64],
+    "vp_gemm_dbias_ws_elems": [i64, i64],
+    "vp_gemm_bf16_dbias": [c_int, c_int, c_int, vp, i64, vp, i64, vp, i64, vp, vp, i64, i64, i64,
+                           i64, vp, vp, vp],
     "vp_bias_grad_ws_elems": [i64],
     "vp_layernorm_bwd_ex": [vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, c_int, vp, vp],
     "vp_embed_fwd": [vp, vp, vp, vp, i64, i64, i64, vp],
@@ -68,6 +71,7 @@ for _name, _args in _SIGS.items():
         _fn.restype = c_int
 L.vp_attention_bwd_ws_elems.restype = ctypes.c_int64
 L.vp_layernorm_ws_elems.restype = ctypes.c_int64
+L.vp_gemm_dbias_ws_elems.restype = ctypes.c_int64
 L.vp_bias_grad_ws_elems.restype = ctypes.c_int64
 
 
@@ -103,8 +107,13 @@ def sm_count() -> int:
     return n.value
 
 
+def gemm_dbias_ws_elems(M: int, N: int) -> int:
+    return int(L.vp_gemm_dbias_ws_elems(M, N))
+
+
 def gemm(a, b, out, *, a_kmajor=True, b_kmajor=True, epilogue=EPI_STORE, bias=None, aux=None,
-         M=None, N=None, K=None, stream=None, out_ptr=None, ldd=None, direct=False):
+         M=None, N=None, K=None, stream=None, out_ptr=None, ldd=None, direct=False,
+         dbias=None, dbias_ws=None):
     """out[M,N] = epi(op(a) @ op(b)^T) where op(a) is [M,K] (a_kmajor: a is
     [M,K], else a is [K,M]) and op(b) is [N,K] (b_kmajor: b is [N,K], else
     [K,N]). All operands bf16 row-major with unit inner stride; out is bf16
@@ -128,11 +137,22 @@ def gemm(a, b, out, *, a_kmajor=True, b_kmajor=True, epilogue=EPI_STORE, bias=No
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(st)
-    _count()
-    check(L.vp_gemm_bf16_ex(int(a_kmajor), int(b_kmajor), epilogue, a.data_ptr(), a.stride(0),
-                            b.data_ptr(), b.stride(0), out_ptr, ldd, _p(bias),
-                            _p(aux), aux.stride(0) if aux is not None else 0, M, N, K,
-                            1 if direct else 0, _stream(stream)), "vp_gemm_bf16")
+    if dbias is not None:
+        # bias gradient (column sums of the output) fused into the epilogue
+        if dbias_ws is None or dbias_ws.numel() < gemm_dbias_ws_elems(M, N):
+            raise ValueError("gemm: dbias needs a workspace of gemm_dbias_ws_elems(M, N)")
+        _count(2)
+        check(L.vp_gemm_bf16_dbias(int(a_kmajor), int(b_kmajor), epilogue, a.data_ptr(),
+                                   a.stride(0), b.data_ptr(), b.stride(0), out_ptr, ldd, _p(bias),
+                                   _p(aux), aux.stride(0) if aux is not None else 0, M, N, K,
+                                   dbias.data_ptr(), dbias_ws.data_ptr(), _stream(stream)),
+              "vp_gemm_bf16_dbias")
+    else:
+        _count()
+        check(L.vp_gemm_bf16_ex(int(a_kmajor), int(b_kmajor), epilogue, a.data_ptr(),
+                                a.stride(0), b.data_ptr(), b.stride(0), out_ptr, ldd, _p(bias),
+                                _p(aux), aux.stride(0) if aux is not None else 0, M, N, K,
+                                1 if direct else 0, _stream(stream)), "vp_gemm_bf16")
     if timing:
         e1.record(st)
         GEMM_TIMING["records"].append((2 * M * N * K, e0, e1, (M, N, K, a_kmajor, b_kmajor)))

@@ -292,6 +292,8 @@ class GPT2Stage:
         self.ln_ws = torch.empty(K.layernorm_ws_elems(h), **f32)
         bias_cols = max(4 * h, cfg.vocab_size) if (self.bert and self.spec.last) else 4 * h
         self.bias_ws = torch.zeros(K.bias_grad_ws_elems(bias_cols), **f32)
+        # FC1 bias gradient fused into the DGELU dgrad epilogue (partials)
+        self.dbias_ws = torch.empty(K.gemm_dbias_ws_elems(T, 4 * h), **f32)
         if self.spec.last:
             self.lnf_out = torch.empty(T, h, **bf)
             self.lnf_mean = torch.empty(T, **f32)
@@ -361,7 +363,7 @@ class GPT2Stage:
         K.layernorm_bwd(g, w.a, P.w(p + "ln2_g"), w.mean2, w.rstd2, dy2, P.g(p + "ln2_g"),
                         P.g(p + "ln2_b"), self.ln_ws, accumulate=False, stream=stream)
         K.gemm(dy2, P.w(p + "w_fc2"), self.dpre, b_kmajor=False, epilogue=K.EPI_DGELU,
-               aux=w.pre, stream=stream)
+               aux=w.pre, stream=stream, dbias=P.g(p + "b_fc1"), dbias_ws=self.dbias_ws)
         K.gemm(dy2, w.f, P.g(p + "w_fc2"), a_kmajor=False, b_kmajor=False,
                epilogue=K.EPI_ACC_F32, stream=stream)
         K.bias_grad(dy2, P.g(p + "b_fc2"), self.bias_ws, stream)
@@ -370,7 +372,6 @@ class GPT2Stage:
                aux=dy2, stream=stream)
         K.gemm(self.dpre, w.c, P.g(p + "w_fc1"), a_kmajor=False, b_kmajor=False,
                epilogue=K.EPI_ACC_F32, stream=stream)
-        K.bias_grad(self.dpre, P.g(p + "b_fc1"), self.bias_ws, stream)
         K.layernorm_bwd(self.dc, w.x1, P.w(p + "ln1_g"), w.mean1, w.rstd1, g, P.g(p + "ln1_g"),
                         P.g(p + "ln1_b"), self.ln_ws, accumulate=False, stream=stream)
         # g = dy1: attention branch
@@ -516,8 +517,9 @@ class GPT2Stage:
         fused = cfg.dropout <= 0  # dropout masks the branch gradients
         # --- MLP: out = x1 + fc2(gelu(fc1(ln2(x1))))
         gy = self._drop_grad(g, dseed, 1, stream)
+        # dpre = (gy W2) * gelu'(pre); its column sum (FC1 bias grad) in the epilogue
         K.gemm(gy, P.w(p + "w_fc2"), self.dpre, b_kmajor=False, epilogue=K.EPI_DGELU,
-               aux=w.pre, stream=stream)
+               aux=w.pre, stream=stream, dbias=P.g(p + "b_fc1"), dbias_ws=self.dbias_ws)
         K.gemm(gy, w.f, P.g(p + "w_fc2"), a_kmajor=False, b_kmajor=False,
                epilogue=K.EPI_ACC_F32, stream=stream)
         if not (fc2_done and fused):
@@ -525,7 +527,6 @@ class GPT2Stage:
         K.gemm(self.dpre, P.w(p + "w_fc1"), self.dc, b_kmajor=False, stream=stream)
         K.gemm(self.dpre, w.c, P.g(p + "w_fc1"), a_kmajor=False, b_kmajor=False,
                epilogue=K.EPI_ACC_F32, stream=stream)
-        K.bias_grad(self.dpre, P.g(p + "b_fc1"), self.bias_ws, stream)
         # g += LN2 backward; with p = 0 its column sum is the proj bias gradient
         K.layernorm_bwd(self.dc, w.x1, P.w(p + "ln2_g"), w.mean2, w.rstd2, g,
                         P.g(p + "ln2_g"), P.g(p + "ln2_b"), self.ln_ws, accumulate=True,

@@ -127,3 +127,26 @@ def test_gemm_deterministic():
     K.gemm(A, B, o1)
     K.gemm(A, B, o2)
     assert torch.equal(o1, o2)
+
+
+@pytest.mark.parametrize("M,N", [(8192, 4096), (300, 520), (1000, 96)])
+def test_gemm_fused_bias_grad(M, N):
+    """DGELU dgrad with the FC1 bias gradient (column sums of the output,
+    fp32 before rounding) fused into the epilogue: matches a separate column
+    sum and is deterministic."""
+    torch.manual_seed(2)
+    Kd = 256
+    A = torch.randn(M, Kd, device="cuda").bfloat16()
+    B = (torch.randn(Kd, N, device="cuda") * 0.05).bfloat16()
+    x = torch.randn(M, N, device="cuda").bfloat16()
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    ws = torch.empty(K.gemm_dbias_ws_elems(M, N), device="cuda")
+    db = torch.ones(N, device="cuda")
+    K.gemm(A, B, out, b_kmajor=False, epilogue=K.EPI_DGELU, aux=x, dbias=db, dbias_ws=ws)
+    ref = (A.float() @ B.float()) * dgelu(x.float())
+    assert rel(out, ref) < 1e-2
+    assert rel(db, 1 + ref.sum(0)) < 1e-3
+    db2 = torch.ones(N, device="cuda")
+    out2 = torch.empty_like(out)
+    K.gemm(A, B, out2, b_kmajor=False, epilogue=K.EPI_DGELU, aux=x, dbias=db2, dbias_ws=ws)
+    assert torch.equal(db, db2) and torch.equal(out, out2)
