@@ -32,6 +32,16 @@ __host__ __device__ constexpr int ta_stages(int D) { return 3; }
 
 template <int D>
 struct TaSmem {
+  // TMEM (256 columns, 2 CTAs/SM): S double-buffered [0,128), O [128,128+D),
+  // then, when they fit, Q (A operand of S = Q K^T, TS mode) and P (A operand
+  // of O += P V, TS mode) as packed bf16 pairs. Operands kept in TMEM are
+  // not re-read from shared memory by every MMA (the forward is bound by
+  // shared-memory bandwidth otherwise).
+  static constexpr bool QT = D == 64;                // Q in TMEM (32 cols)
+  static constexpr bool PT = D <= 96;                // P in TMEM (32 cols)
+  static constexpr int TQ = 128 + D;                 // TMEM column of Q
+  static constexpr int TP = 128 + D + (QT ? D / 2 : 0);  // TMEM column of P
+  static_assert(TP + (PT ? 32 : 0) <= 256, "attention fwd TMEM budget");
   static constexpr int CH = (D + 63) / 64;           // 64-wide d-chunks (128 B rows)
   static constexpr int QCH = 128 * 128;              // one Q d-chunk: 128 rows x 128 B
   static constexpr int KCH = TA_BN * 128;            // one K/V d-chunk: 64 rows x 128 B
@@ -70,7 +80,8 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
   uint64_t* s_empty = bars + 11;             // [2]
   uint64_t* o_full = bars + 13;              // [2]: PV_j commits o_full[j & 1]
   uint64_t* p_full = bars + 15;              // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  uint64_t* q_tmem = bars + 17;              // Q copied into TMEM (4 softmax warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
 
   const int qb = n_qb - 1 - static_cast<int>(blockIdx.x);  // heavy (late) causal blocks first
   const int bh = blockIdx.y;
@@ -97,6 +108,7 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
       mbar_init(&o_full[i], 1);
       mbar_init(&p_full[i], 4);
     }
+    mbar_init(q_tmem, 4);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 256);
@@ -133,6 +145,7 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
       const uint32_t sQ = smem_u32(smem + L::Q_OFF);
       const uint32_t sP = smem_u32(smem + L::P_OFF);
       mbar_wait(q_full, 0);
+      if constexpr (L::QT) mbar_wait(q_tmem, 0);  // softmax warps copied Q into TMEM
       auto issue_pv = [&](int j) {
         const int st = j % L::STAGES;
         mbar_wait(&p_full[j & 1], (j >> 1) & 1);  // P_j written (and O rescaled if needed)
@@ -142,11 +155,15 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
         const uint32_t sPj = sP + (j & 1) * 128 * TA_BN * 2;
 #pragma unroll
         for (int k = 0; k < TA_BN / 16; ++k) {
-          // A = P [q][key] K-major (one 128 B row chunk): +32 B per 16 keys
-          const uint64_t ad = sdesc_sw128(sPj + k * 32, 16, 1024);
           // B = V [key][d] MN-major: +16 rows * 128 B per 16 keys; d-chunks KCH apart
           const uint64_t bd = sdesc_sw128(sV + k * 2048, L::KCH, 1024);
-          umma_f16(tmem + 2 * TA_BN, ad, bd, idO, (j > 0 || k > 0) ? 1u : 0u);
+          if constexpr (L::PT) {
+            umma_f16_ts(tmem + 128, tmem + L::TP + k * 8, bd, idO, (j > 0 || k > 0) ? 1u : 0u);
+          } else {
+            // A = P [q][key] K-major (one 128 B row chunk): +32 B per 16 keys
+            const uint64_t ad = sdesc_sw128(sPj + k * 32, 16, 1024);
+            umma_f16(tmem + 128, ad, bd, idO, (j > 0 || k > 0) ? 1u : 0u);
+          }
         }
         umma_commit(&o_full[j & 1]);
         umma_commit(&kv_empty[st]);
@@ -160,9 +177,13 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
         const uint32_t sK = smem_u32(smem + L::K_OFF + st * L::KTILE);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
-          umma_f16(tmem + (j & 1) * TA_BN,
-                   sdesc_sw128(sQ + (k >> 2) * L::QCH + (k & 3) * 32, 16, 1024),
-                   sdesc_sw128(sK + (k >> 2) * L::KCH + (k & 3) * 32, 16, 1024), idS, k > 0);
+          const uint64_t bd = sdesc_sw128(sK + (k >> 2) * L::KCH + (k & 3) * 32, 16, 1024);
+          if constexpr (L::QT) {
+            umma_f16_ts(tmem + (j & 1) * TA_BN, tmem + L::TQ + k * 8, bd, idS, k > 0);
+          } else {
+            umma_f16(tmem + (j & 1) * TA_BN,
+                     sdesc_sw128(sQ + (k >> 2) * L::QCH + (k & 3) * 32, 16, 1024), bd, idS, k > 0);
+          }
         }
         umma_commit(&s_full[j & 1]);
         if (j >= 1) issue_pv(j - 1);
@@ -175,9 +196,29 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
     const int r = qd * 32 + lane;
     const int q = q0 + r;
     const uint32_t trow = (qd * 32) << 16;
-    const uint32_t tO = tmem + trow + 2 * TA_BN;
+    const uint32_t tO = tmem + trow + 128;
     uint8_t* sP = smem + L::P_OFF;
     float m = -FLT_MAX, l = 0.f;
+    if constexpr (L::QT) {
+      // Q row r (128 B, swizzled in smem) -> TMEM as the A operand of S = Q K^T
+      mbar_wait(q_full, 0);
+      const uint32_t qrow = smem_u32(smem + L::Q_OFF + r * 128);
+      uint32_t qw[32];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        uint4 u;
+        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
+                     : "r"(qrow + ((k ^ (r & 7)) << 4)));
+        qw[4 * k] = u.x; qw[4 * k + 1] = u.y; qw[4 * k + 2] = u.z; qw[4 * k + 3] = u.w;
+      }
+      tmem_st16(tmem + trow + L::TQ, qw);
+      tmem_st16(tmem + trow + L::TQ + 16, qw + 16);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(q_tmem);
+    }
     for (int j = 0; j < n_kb; ++j) {
       if (warp == 4 && lane == 0) TRF(j, 0);
       mbar_wait(&s_full[j & 1], (j >> 1) & 1);
@@ -231,8 +272,12 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
         pk[g] = pack8(f);
       }
       if (warp == 4 && lane == 0) TRF(j, 2);
-      // P buffer (j & 1) was last read by PV_{j-2}
-      if (j >= 2) mbar_wait(&o_full[j & 1], ((j - 2) >> 1) & 1);
+      // P buffer: TMEM (single, last read by PV_{j-1}) or smem (j & 1, by PV_{j-2})
+      if constexpr (L::PT) {
+        if (j >= 1) mbar_wait(&o_full[(j - 1) & 1], ((j - 1) >> 1) & 1);
+      } else {
+        if (j >= 2) mbar_wait(&o_full[j & 1], ((j - 2) >> 1) & 1);
+      }
       if (j >= 1 && __any_sync(0xffffffffu, grow)) {
         // rescale O in place: needs PV_{j-1} complete
         mbar_wait(&o_full[(j - 1) & 1], ((j - 1) >> 1) & 1);
@@ -250,7 +295,11 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
           tmem_st_wait();
         }
       }
-      {
+      if constexpr (L::PT) {
+        tmem_st16(tmem + trow + L::TP, reinterpret_cast<const uint32_t*>(pk));
+        tmem_st16(tmem + trow + L::TP + 16, reinterpret_cast<const uint32_t*>(pk + 4));
+        tmem_st_wait();
+      } else {
         const uint32_t rowp = smem_u32(sP + (j & 1) * 128 * TA_BN * 2 + r * 128);
 #pragma unroll
         for (int g = 0; g < TA_BN / 8; ++g) sts128(rowp + ((g ^ (r & 7)) << 4), pk[g]);
