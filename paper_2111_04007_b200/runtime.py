@@ -263,7 +263,7 @@ class Varuna:
     def __init__(self, model: GPT2Config, config: ParallelConfig, *,
                  optimizer: AdamWConfig = AdamWConfig(), seed: int = 0, loss_scale: float = 1.0,
                  device=None, init_device: str = "cpu", trace: bool = False,
-                 dispatch: str = "static", profile=None):
+                 dispatch: str = "static", profile=None, graphs: Optional[bool] = None):
         if len(config.stage_map) != model.n_layer:
             raise ConfigError(f"stage_map covers {len(config.stage_map)} cut-points, model has "
                               f"{model.n_layer} (one CutPoint per transformer layer)")
@@ -310,6 +310,18 @@ class Varuna:
             self.links = _Links(self.rank, self.stage_id, P, self.N, slot_elems,
                                 self.gloo, self.shm)
         self.gpu_launches_per_step = None
+        # Each task's launch sequence (tens to hundreds of kernels) is captured
+        # once into a CUDA graph and replayed: the per-launch host cost would
+        # otherwise approach the GPU time of the short kernels. Inputs reach
+        # the graph through fixed buffers; IPC waits / signals stay outside.
+        # Disabled with dropout (per-step seeds) and while kernel timing hooks
+        # are active.
+        self.use_graphs = (model.dropout <= 0) if graphs is None else bool(graphs)
+        self._graphs = {}
+        T = self.m * model.seq_len
+        self._in_ids = torch.zeros(T, dtype=torch.int64, device=self.device)
+        self._in_types = torch.zeros(T, dtype=torch.int64, device=self.device)
+        self._in_labels = torch.zeros(T, dtype=torch.int64, device=self.device)
 
     # ---------------------------------------------------------------- setup
     def _opportunistic_order(self, profile):
@@ -416,10 +428,9 @@ class Varuna:
                 self.loss_sum.zero_()
             t_start = self._mark(ev)
             x_in = {}
+            graphs = self.use_graphs and not K.GEMM_TIMING["on"] and self.step_count > 1
             for kind, j in self.tasks:
                 dseed = (self.step_count * 1000003 + j) & 0x7FFFFFFF
-                ids = data["ids"][j] if self.spec.first else None
-                types = data["types"][j] if "types" in data else None
                 # inputs first (stream waits on the peer's IPC event), so the
                 # task's timing events bracket compute only
                 if kind != B and not self.spec.first and j not in x_in:
@@ -429,23 +440,24 @@ class Varuna:
                 if kind == B and not self.spec.last:
                     self.links.wait(_Links.GRAD, j, seq_no, st)
                     g_in = self.links.rx_slot(_Links.GRAD, j, (stage.T, cfg.hidden))
+                if self.spec.first:
+                    self._in_ids.copy_(data["ids"][j], non_blocking=True)
+                    if "types" in data:
+                        self._in_types.copy_(data["types"][j], non_blocking=True)
+                if self.spec.last and kind == B:
+                    self._in_labels.copy_(data["labels"][j], non_blocking=True)
                 e0 = self._mark(ev)
-                if kind == F or kind == R:
-                    save = kind == R or self.spec.last
-                    out_ptr = None
-                    if kind == F and not self.spec.last:
-                        out_ptr = self.links.peer_slot_ptr(_Links.ACT, j)
-                    stage.forward(x_in.get(j), ids, save=save, dseed=dseed, stream=st,
-                                  out_ptr=out_ptr, types=types)
-                    if out_ptr is not None:
-                        self.links.signal(_Links.ACT, j, seq_no, st)
+                body = (lambda kind=kind, j=j, dseed=dseed, g_in=g_in:
+                        self._task(kind, j, dseed, x_in.get(j), g_in, scale, st,
+                                   "types" in data))
+                if graphs:
+                    self._replay(kind, j, body, st)
                 else:
-                    if self.spec.last:
-                        stage.loss_and_head_backward(data["labels"][j], scale, self.loss_sum,
-                                                     stream=st)
-                    g = stage.backward(g_in, ids, dseed=dseed, stream=st, types=types)
+                    body()
+                if kind == F and not self.spec.last:
+                    self.links.signal(_Links.ACT, j, seq_no, st)
+                if kind == B:
                     if not self.spec.first:
-                        K.p2p_put(self.links.peer_slot_ptr(_Links.GRAD, j), g, stream=st)
                         self.links.signal(_Links.GRAD, j, seq_no, st)
                     x_in.pop(j, None)
                 if ev is not None:
@@ -456,12 +468,53 @@ class Varuna:
             if apply:
                 self._optimizer_step()
             t_end = self._mark(ev)
+        # the caller's stream is ordered after the step (loss, flags, updated
+        # weights): the executor stream is non-blocking w.r.t. the default one
+        torch.cuda.current_stream(self.device).wait_stream(st)
         timeline = None
         if ev is not None:
             st.synchronize()
             timeline = self._timeline(t_start, ev, t_ar0, t_ar1, t_end)
         loss = self.loss_sum if self.spec.last else None
         return StepResult(loss, self.flags, 1.0 / self.loss_scale, timeline)
+
+    def _task(self, kind, j, dseed, x, g_in, scale, st, typed):
+        """The launches of one schedule task on this stage (graph-capturable:
+        every pointer is fixed for a given (kind, micro-batch))."""
+        stage = self.stage
+        ids = self._in_ids if self.spec.first else None
+        types = self._in_types if (self.spec.first and typed) else None
+        if kind == F or kind == R:
+            save = kind == R or self.spec.last
+            out_ptr = None
+            if kind == F and not self.spec.last:
+                out_ptr = self.links.peer_slot_ptr(_Links.ACT, j)
+            stage.forward(x, ids, save=save, dseed=dseed, stream=st, out_ptr=out_ptr,
+                          types=types)
+        else:
+            if self.spec.last:
+                stage.loss_and_head_backward(self._in_labels, scale, self.loss_sum, stream=st)
+            g = stage.backward(g_in, ids, dseed=dseed, stream=st, types=types)
+            if not self.spec.first:
+                K.p2p_put(self.links.peer_slot_ptr(_Links.GRAD, j), g, stream=st)
+
+    def _replay(self, kind, j, body, st):
+        """Run ``body`` through a CUDA graph captured on first use. Stages
+        without rings have the same pointers for every micro-batch, so one
+        graph per task kind serves them all."""
+        key = (kind, j) if self.links is not None else (kind, 0)
+        g = self._graphs.get(key)
+        if g is None:
+            n0 = K.LAUNCHES[0]
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=st):
+                body()
+            self._graphs[key] = (g, K.LAUNCHES[0] - n0)
+            g, n = self._graphs[key]
+        else:
+            g, n = g
+            K.LAUNCHES[0] += n
+        g.replay()
 
     def _mark(self, ev):
         if ev is None:

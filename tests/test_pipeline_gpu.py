@@ -192,3 +192,25 @@ def test_gantt_export_format():
     assert len(lines) - 1 == 2 * 2 + 1  # F,B per micro-batch + allreduce row
     kinds = [ln.split(",")[1] for ln in lines[1:]]
     assert kinds.count("F") == 2 and kinds.count("B") == 2 and kinds.count("A") == 1
+
+
+def test_graph_replay_matches_eager():
+    """Steps replayed from captured CUDA graphs give the losses of eager
+    execution (attention dQ is summed in CTA order: fp32-level tolerance)."""
+    from paper_2111_04007_b200 import ParallelConfig
+    from paper_2111_04007_b200.model import CONFIGS
+    from paper_2111_04007_b200.runtime import Varuna, synthetic_batch
+    cfg = CONFIGS["tiny"]
+    losses = {}
+    for graphs in (False, True):
+        v = Varuna(cfg, ParallelConfig(1, 1, 4, 3, (0,) * cfg.n_layer), seed=0, graphs=graphs)
+        out = []
+        for s in range(4):
+            b = synthetic_batch(cfg, 12, 0, step=s)
+            out.append(v.step(b).loss)
+        losses[graphs] = out
+        if graphs:
+            assert len(v._graphs) == 2  # one F and one B graph serve every micro-batch
+        v.close()
+    for a, b in zip(losses[False], losses[True]):
+        assert abs(a - b) <= 1e-4 * abs(a)
