@@ -69,8 +69,9 @@ def main():
     a = ap.parse_args()
     install()
     cfg = CONFIGS[a.config]
+    # eager launches (no CUDA graphs): the timing wrappers must run per call
     v = Varuna(cfg, ParallelConfig(1, 1, a.m, a.N, (0,) * cfg.n_layer), seed=0,
-               init_device="cuda")
+               init_device="cuda", graphs=False)
     b = {k: t.cuda() for k, t in synthetic_batch(cfg, a.m * a.N, 0).items()}
     for _ in range(2):
         v.step(b)
