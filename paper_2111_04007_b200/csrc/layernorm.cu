@@ -15,6 +15,9 @@
 // (deterministic). Wider rows use dx + column-partial kernels.
 #include "common.cuh"
 
+#include <algorithm>
+#include <cstdlib>
+
 namespace vp {
 namespace {
 
@@ -210,6 +213,152 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       float t = 0.f;
 #pragma unroll
       for (int w = 0; w < kWarps; ++w) t += red[w * cols + c];
+      ws[(static_cast<int64_t>(blockIdx.x) * 3 + q) * cols + c] = t;
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------- fused backward, warp pairs
+// A row is split between the two warps of a pair (half the 16-byte vectors
+// each): x and dy are unpacked once into fp32 registers, gamma stays in
+// registers for the whole kernel, and the two row sums (dy*g, dy*g*xhat) are
+// exchanged through shared memory with a 64-thread named barrier. Half the
+// columns per thread halves the register-resident partials (dgamma, dbeta,
+// dsum), so 12 warps fit per SM; ~40 % fewer instructions per element than
+// the one-warp-per-row kernel above.
+constexpr int kPairs = 6;
+template <int NV, bool SUM>
+__global__ void __launch_bounds__(kPairs * 64, 1)
+    ln_bwd_pair_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+                       const __nv_bfloat16* __restrict__ g, const float* __restrict__ mean,
+                       const float* __restrict__ rstd, __nv_bfloat16* __restrict__ dx,
+                       float* __restrict__ ws, int64_t rows, int cols, int accumulate) {
+  extern __shared__ float red[];  // [kPairs][cols] reduction buffer
+  __shared__ float xch[kPairs][2][2][2];  // [pair][row parity][half][s1, s2]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pair = warp >> 1, half = warp & 1;
+  const int nvec = cols >> 3, hvec = nvec >> 1;  // vectors per half row
+  const int v0 = half * hvec;
+  const int64_t npairs = static_cast<int64_t>(gridDim.x) * kPairs;
+  float gam[NV][8];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = lane + i * 32;
+    if (c < hvec) unpack8(reinterpret_cast<const uint4*>(g)[v0 + c], gam[i]);
+    else
+#pragma unroll
+      for (int j = 0; j < 8; ++j) gam[i][j] = 0.f;
+  }
+  float ag[NV][8], ab[NV][8], as[SUM ? NV : 1][8];
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      ag[i][j] = 0.f;
+      ab[i][j] = 0.f;
+      if constexpr (SUM) as[i][j] = 0.f;
+    }
+  auto load_half = [&](const __nv_bfloat16* base, int64_t row, uint4 (&v)[NV]) {
+    const uint4* r = reinterpret_cast<const uint4*>(base + row * cols) + v0;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = lane + i * 32;
+      v[i] = c < hvec ? r[c] : make_uint4(0u, 0u, 0u, 0u);
+    }
+  };
+  int64_t row = static_cast<int64_t>(blockIdx.x) * kPairs + pair;
+  uint4 xc[NV], dc[NV];
+  if (row < rows) {
+    load_half(x, row, xc);
+    load_half(dy, row, dc);
+  }
+  int parity = 0;
+  for (; row < rows; row += npairs, parity ^= 1) {
+    uint4 pu[NV];
+    if (accumulate) load_half(dx, row, pu);
+    uint4 xn[NV], dn[NV];
+    const int64_t nrow = row + npairs;
+    if (nrow < rows) {
+      load_half(x, nrow, xn);
+      load_half(dy, nrow, dn);
+    }
+    const float mu = mean[row], rs = rstd[row];
+    float xf[NV][8], df[NV][8];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      unpack8(xc[i], xf[i]);
+      unpack8(dc[i], df[i]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float xh = (xf[i][j] - mu) * rs;
+        const float gy = df[i][j] * gam[i][j];
+        s1 += gy;
+        s2 = fmaf(gy, xh, s2);
+        ag[i][j] = fmaf(df[i][j], xh, ag[i][j]);
+        ab[i][j] += df[i][j];
+      }
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if (lane == 0) {
+      xch[pair][parity][half][0] = s1;
+      xch[pair][parity][half][1] = s2;
+    }
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
+    const float m1 = (s1 + xch[pair][parity][half ^ 1][0]) / cols;
+    const float m2 = (s2 + xch[pair][parity][half ^ 1][1]) / cols;
+    uint4* dxr = reinterpret_cast<uint4*>(dx + row * cols) + v0;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = lane + i * 32;
+      if (c < hvec) {
+        float o[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float xh = (xf[i][j] - mu) * rs;
+          o[j] = rs * fmaf(-xh, m2, fmaf(df[i][j], gam[i][j], -m1));
+        }
+        if (accumulate) {
+          float pv[8];
+          unpack8(pu[i], pv);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) o[j] += pv[j];
+        }
+        if constexpr (SUM) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) as[i][j] += o[j];
+        }
+        dxr[c] = pack8(o);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      xc[i] = xn[i];
+      dc[i] = dn[i];
+    }
+  }
+  // CTA reduction over the pairs, one quantity at a time
+  constexpr int NQ = SUM ? 3 : 2;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    float* mine = red + pair * cols + v0 * 8;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = lane + i * 32;
+      if (c < hvec) {
+        const float* src = q == 0 ? ag[i] : (q == 1 ? ab[i] : as[SUM ? i : 0]);
+        float4* dst = reinterpret_cast<float4*>(mine + c * 8);
+        dst[0] = make_float4(src[0], src[1], src[2], src[3]);
+        dst[1] = make_float4(src[4], src[5], src[6], src[7]);
+      }
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+      float t = 0.f;
+#pragma unroll
+      for (int w = 0; w < kPairs; ++w) t += red[w * cols + c];
       ws[(static_cast<int64_t>(blockIdx.x) * 3 + q) * cols + c] = t;
     }
     __syncthreads();
@@ -431,7 +580,27 @@ extern "C" int vp_layernorm_bwd_ex(const void* dy, const void* x, const void* ga
   const int nq = dsum ? 3 : 2;
   const int c3 = static_cast<int>(nq * cols);
   int parts;
-  if (nv <= 4) {
+  const int64_t nvec = cols / 8;
+  const int64_t hneed = (nvec / 2 + 31) / 32;  // vectors per lane of a half row
+  if ((nvec % 2) == 0 && hneed <= 2 && !getenv("VP_LN_WARP_ROW")) {
+    // warp pairs, one CTA (12 warps) per SM, partials in registers
+    parts = static_cast<int>(std::min<int64_t>(device_sms(), (rows + kPairs - 1) / kPairs));
+    const size_t smem = static_cast<size_t>(kPairs) * cols * sizeof(float);
+    auto launch = [&](auto kern) {
+      static bool set = false;
+      if (!set) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        set = true;
+      }
+      kern<<<parts, kPairs * 64, smem, st>>>(
+          reinterpret_cast<const __nv_bfloat16*>(dy), reinterpret_cast<const __nv_bfloat16*>(x),
+          reinterpret_cast<const __nv_bfloat16*>(gamma), mean, rstd,
+          reinterpret_cast<__nv_bfloat16*>(dx), workspace, rows, static_cast<int>(cols),
+          accumulate);
+    };
+    if (hneed == 1) dsum ? launch(ln_bwd_pair_kernel<1, true>) : launch(ln_bwd_pair_kernel<1, false>);
+    else dsum ? launch(ln_bwd_pair_kernel<2, true>) : launch(ln_bwd_pair_kernel<2, false>);
+  } else if (nv <= 4) {
     // one CTA per SM (register-resident partials); 8 rows per warp pass
     parts = row_ctas(rows, 1);
     const size_t smem = static_cast<size_t>(kWarps) * cols * sizeof(float);  // <= 32 KB
