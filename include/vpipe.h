@@ -173,7 +173,10 @@ int64_t vp_attention_bwd_ws_elems(int64_t batch, int64_t seq, int64_t heads, int
 int vp_attention_bwd_ex(const void* qkv, const void* o, const void* dout, const float* lse,
                         void* dqkv, float* workspace, int64_t ws_elems, int64_t batch,
                         int64_t seq, int64_t heads, int64_t head_dim, int causal, int flags,
-                        void* stream);
+                        float* dbias, void* stream);
+/* dbias (optional, fused path only, else VP_ERR_UNSUPPORTED): dbias[3*H*D]
+ * += column sums of dqkv — the QKV bias gradient — from the dQ post-pass
+ * and the dK/dV epilogue partials (fixed-order reductions). */
 
 /* Token + position embedding gather: x[T,h] = wte[ids] + wpe[pos]. */
 int vp_embed_fwd(const int64_t* ids, const void* wte, const void* wpe, void* x, int64_t batch,

@@ -23,7 +23,7 @@ int64_t attention_bwd_fused_ws(int64_t B, int64_t S, int64_t H, int64_t D);
 bool attention_bwd_fused_ok(int64_t D);
 int attention_bwd_fused(const void* qkv, const void* o, const void* dout, const float* lse,
                         void* dqkv, float* ws, int64_t B, int64_t S, int64_t H, int causal,
-                        cudaStream_t st);
+                        float* dbias, cudaStream_t st);
 
 namespace {
 
@@ -652,7 +652,8 @@ extern "C" int64_t vp_attention_bwd_ws_elems(int64_t batch, int64_t seq, int64_t
 extern "C" int vp_attention_bwd_ex(const void* qkv, const void* o, const void* dout,
                                    const float* lse, void* dqkv, float* workspace,
                                    int64_t ws_elems, int64_t batch, int64_t seq, int64_t heads,
-                                   int64_t head_dim, int causal, int flags, void* stream) {
+                                   int64_t head_dim, int causal, int flags, float* dbias,
+                                   void* stream) {
   if (batch <= 0 || seq <= 0 || heads <= 0 || !workspace) return VP_ERR_ARGS;
   if (ws_elems < attention_bwd_fused_ws(batch, seq, heads, head_dim)) return VP_ERR_ARGS;
   if ((reinterpret_cast<uintptr_t>(workspace) & 15) != 0) return VP_ERR_ARGS;
@@ -660,7 +661,9 @@ extern "C" int vp_attention_bwd_ex(const void* qkv, const void* o, const void* d
   const bool det = (flags & VP_ATTN_DETERMINISTIC) || getenv("VP_ATTN_DETERMINISTIC") ||
                    getenv("VP_ATTN_LEGACY");
   if (!det && attention_bwd_fused_ok(head_dim))
-    return attention_bwd_fused(qkv, o, dout, lse, dqkv, workspace, batch, seq, heads, causal, st);
+    return attention_bwd_fused(qkv, o, dout, lse, dqkv, workspace, batch, seq, heads, causal,
+                               dbias, st);
+  if (dbias) return VP_ERR_UNSUPPORTED;  // bias sums are fused only into the one-pass kernel
   return vp_attention_bwd(qkv, o, dout, lse, dqkv, workspace, batch, seq, heads, head_dim, causal,
                           stream);
 }

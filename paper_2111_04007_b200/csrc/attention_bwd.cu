@@ -47,6 +47,7 @@ constexpr int FB_NS = 3;   // Q/dO ring stages
 constexpr int FB_CW = 8;   // softmax-gradient warps (4..11)
 constexpr int FB_DW = 4;   // dQ drain warps (12..15), one per TMEM lane quadrant
 constexpr int FB_THREADS = 128 + 32 * (FB_CW + FB_DW);
+constexpr int64_t kConvParts = 256;  // row parts of the dQ convert / Q-bias column sums
 #ifndef FB_SPLIT_S
 #define FB_SPLIT_S 0
 #endif
@@ -63,6 +64,26 @@ struct FbSmem {
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
 static_assert(FbSmem::TOTAL <= 232448, "attention bwd smem");
+
+// Sum of v[0..31] over the 32 lanes, lane l ending with the total of
+// element l (halving exchanges: 31 shuffles).
+__device__ __forceinline__ float warp_colsum32(const float (&v)[32], uint32_t lane) {
+  float t[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const bool hi = lane & 16;
+    t[i] = (hi ? v[i + 16] : v[i]) + __shfl_xor_sync(0xffffffffu, hi ? v[i] : v[i + 16], 16);
+  }
+#pragma unroll
+  for (int w = 8, bit = 8; w >= 1; w >>= 1, bit >>= 1) {
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const bool hi = lane & bit;
+      t[i] = (hi ? t[i + w] : t[i]) + __shfl_xor_sync(0xffffffffu, hi ? t[i] : t[i + w], bit);
+    }
+  }
+  return t[0];
+}
 
 __device__ __forceinline__ void red_add_v4(float* p, uint32_t a, uint32_t b, uint32_t c,
                                            uint32_t d) {
@@ -82,7 +103,8 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
     attn_bwd_fused(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
                    const __grid_constant__ CUtensorMap tmDQ, const float* __restrict__ lse,
                    const float* __restrict__ delta, __nv_bfloat16* __restrict__ dqkv, int S, int H,
-                   int BH, float scale_log2, float scale, float* __restrict__ dq_acc) {
+                   int BH, float scale_log2, float scale, float* __restrict__ dq_acc,
+                   float* __restrict__ kv_part) {
   using L = FbSmem;
   constexpr int D = FB_D;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -363,19 +385,27 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
       tmem_ld32(tDK + trow + c, rk);
       tmem_ld32(tDV + trow + c, rv);
       tmem_ld_wait();
+      float fk[32], fv[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        fk[i] = key < S ? __uint_as_float(rk[i]) * scale : 0.f;
+        fv[i] = key < S ? __uint_as_float(rv[i]) : 0.f;
+      }
       if (key < S) {
         __nv_bfloat16* row = dqkv + (static_cast<int64_t>(b) * S + key) * (3 * Hd) + h * D + c;
 #pragma unroll
         for (int i = 0; i < 32; i += 8) {
-          float fk[8], fv[8];
-#pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            fk[t] = __uint_as_float(rk[i + t]) * scale;
-            fv[t] = __uint_as_float(rv[i + t]);
-          }
-          *reinterpret_cast<uint4*>(row + Hd + i) = pack8(fk);
-          *reinterpret_cast<uint4*>(row + 2 * Hd + i) = pack8(fv);
+          *reinterpret_cast<uint4*>(row + Hd + i) = pack8(*reinterpret_cast<float(*)[8]>(fk + i));
+          *reinterpret_cast<uint4*>(row + 2 * Hd + i) = pack8(*reinterpret_cast<float(*)[8]>(fv + i));
         }
+      }
+      if (kv_part != nullptr) {
+        // K/V bias gradient: this warp's 32 keys summed per column (lane l
+        // ends with column c + l) -> kv_part[(b, kb, quadrant)][K | V column]
+        const float sk = warp_colsum32(fk, lane), sv = warp_colsum32(fv, lane);
+        float* dst = kv_part + ((static_cast<int64_t>(b) * gridDim.x / BH + kb) * 4 + qd) * (2 * Hd);
+        dst[h * D + c + lane] = sk;
+        dst[Hd + h * D + c + lane] = sv;
       }
     }
   } else if (warp >= 4 + FB_CW) {
@@ -443,8 +473,10 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
 // row per 8-lane group.
 __global__ void __launch_bounds__(256) attn_delta_zero_kernel(
     const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
-    float* __restrict__ delta, float* __restrict__ dq_acc, int64_t tokens, int S, int H) {
+    float* __restrict__ delta, float* __restrict__ dq_acc, int64_t tokens, int S, int H,
+    unsigned* __restrict__ counters) {
   constexpr int G = FB_D / 8;
+  if (blockIdx.x == 0 && threadIdx.x < 64) counters[threadIdx.x] = 0u;
   const int lane = threadIdx.x & 31;
   const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / G;
   const int li = lane % G;
@@ -486,9 +518,102 @@ __global__ void __launch_bounds__(256) dq_convert_kernel(const float* __restrict
   *reinterpret_cast<uint4*>(dqkv + t * (3 * static_cast<int64_t>(Hd)) + c) = pack8(f);
 }
 
+// The same conversion fused with the Q bias gradient: CTA (256 columns, row
+// part) with 8 row-lanes x 4 rows in flight, column partials ->
+// part_ws[part][Hd]; the last CTA of a column block (arrival counter) sums the
+// parts in a fixed order (deterministic) into dbias.
+__global__ void __launch_bounds__(256) dq_convert_bias_kernel(
+    const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv, int64_t tokens, int Hd,
+    float scale, int64_t rpp, int parts, float* __restrict__ part_ws,
+    unsigned* __restrict__ counters, float* __restrict__ dbias) {
+  __shared__ float sh[8][256 + 4];
+  __shared__ bool is_last;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int cb = blockIdx.x * 256;
+  const int c0 = cb + tx * 8;
+  const int64_t r0 = blockIdx.y * rpp, r1 = min(tokens, r0 + rpp);
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (c0 < Hd) {
+#pragma unroll 4
+    for (int64_t t = r0 + ty; t < r1; t += 8) {
+      const float4* src = reinterpret_cast<const float4*>(dq_acc + t * Hd + c0);
+      const float4 a = src[0], b = src[1];
+      float f[8] = {a.x * scale, a.y * scale, a.z * scale, a.w * scale,
+                    b.x * scale, b.y * scale, b.z * scale, b.w * scale};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += f[j];
+      *reinterpret_cast<uint4*>(dqkv + t * (3 * static_cast<int64_t>(Hd)) + c0) = pack8(f);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) sh[ty][tx * 8 + j] = acc[j];
+  __syncthreads();
+  {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += sh[k][threadIdx.x];
+    if (cb + static_cast<int>(threadIdx.x) < Hd)
+      part_ws[static_cast<int64_t>(blockIdx.y) * Hd + cb + threadIdx.x] = t;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0)
+    is_last = atomicAdd(&counters[blockIdx.x], 1u) == static_cast<unsigned>(parts - 1);
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  float f[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (c0 < Hd) {
+    for (int p = ty; p < parts; p += 8) {
+      const float4* src = reinterpret_cast<const float4*>(part_ws + static_cast<int64_t>(p) * Hd + c0);
+      const float4 a = __ldcg(src), b = __ldcg(src + 1);
+      f[0] += a.x; f[1] += a.y; f[2] += a.z; f[3] += a.w;
+      f[4] += b.x; f[5] += b.y; f[6] += b.z; f[7] += b.w;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 8; ++j) sh[ty][tx * 8 + j] = f[j];
+  __syncthreads();
+  {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += sh[k][threadIdx.x];
+    if (cb + static_cast<int>(threadIdx.x) < Hd) dbias[cb + threadIdx.x] += t;
+  }
+  if (threadIdx.x == 0) counters[blockIdx.x] = 0u;
+}
+
+// dbias[c] += sum over partial rows of kv_part[row][c] (fixed order): 32
+// columns x 32 row-lanes per block, 8 independent loads per thread.
+__global__ void __launch_bounds__(1024) kv_bias_reduce(const float* __restrict__ kv_part,
+                                                       float* __restrict__ dbias, int prow, int n) {
+  __shared__ float sh[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + tx;
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (c < n) {
+    int r = ty;
+    for (; r + 7 * 32 < prow; r += 8 * 32) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[u] += kv_part[static_cast<int64_t>(r + u * 32) * n + c];
+    }
+    for (; r < prow; r += 32) acc[0] += kv_part[static_cast<int64_t>(r) * n + c];
+  }
+  sh[ty][tx] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+  __syncthreads();
+  if (ty == 0 && c < n) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) t += sh[i][tx];
+    dbias[c] += t;
+  }
+}
+
 template <bool CAUSAL>
 int fused_t(const void* qkv, const void* o, const void* dout, const float* lse, float* delta,
-            float* dq_acc, void* dqkv, int64_t B, int64_t S, int64_t H, cudaStream_t st) {
+            float* dq_acc, void* dqkv, int64_t B, int64_t S, int64_t H, float* dbias,
+            float* part_ws, unsigned* counters, float* kv_part, cudaStream_t st) {
   using L = FbSmem;
   constexpr int D = FB_D;
   const int64_t tokens = B * S;
@@ -508,37 +633,58 @@ int fused_t(const void* qkv, const void* o, const void* dout, const float* lse, 
   const int64_t rows = tokens * H;
   attn_delta_zero_kernel<<<static_cast<unsigned>((rows * (D / 8) + 255) / 256), 256, 0, st>>>(
       reinterpret_cast<const __nv_bfloat16*>(o), reinterpret_cast<const __nv_bfloat16*>(dout),
-      delta, dq_acc, tokens, static_cast<int>(S), static_cast<int>(H));
+      delta, dq_acc, tokens, static_cast<int>(S), static_cast<int>(H), counters);
   const float scale = 1.f / sqrtf(static_cast<float>(D));
   const float scale_log2 = 1.4426950408889634f * scale;
   const int n_kb = static_cast<int>((S + FB_M - 1) / FB_M);
   const int BH = static_cast<int>(B * H);
   k<<<static_cast<unsigned>(n_kb * BH), FB_THREADS, L::TOTAL, st>>>(
       tq, tdo, tdq, lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), static_cast<int>(S),
-      static_cast<int>(H), BH, scale_log2, scale, dq_acc);
-  dq_convert_kernel<<<static_cast<unsigned>((tokens * Hd / 8 + 255) / 256), 256, 0, st>>>(
-      dq_acc, reinterpret_cast<__nv_bfloat16*>(dqkv), tokens, Hd, scale);
+      static_cast<int>(H), BH, scale_log2, scale, dq_acc, dbias ? kv_part : nullptr);
+  if (!dbias) {
+    dq_convert_kernel<<<static_cast<unsigned>((tokens * Hd / 8 + 255) / 256), 256, 0, st>>>(
+        dq_acc, reinterpret_cast<__nv_bfloat16*>(dqkv), tokens, Hd, scale);
+  } else {
+    const int col_blocks = (Hd + 255) / 256;
+    int parts = static_cast<int>(std::min<int64_t>(kConvParts, std::max<int64_t>(
+        1, (8 * static_cast<int64_t>(device_sms()) + col_blocks - 1) / col_blocks)));
+    const int64_t rpp = (tokens + parts - 1) / parts;
+    parts = static_cast<int>((tokens + rpp - 1) / rpp);
+    dq_convert_bias_kernel<<<dim3(col_blocks, parts), 256, 0, st>>>(
+        dq_acc, reinterpret_cast<__nv_bfloat16*>(dqkv), tokens, Hd, scale, rpp, parts, part_ws,
+        counters, dbias);
+    const int prow = static_cast<int>(B * n_kb * 4);
+    kv_bias_reduce<<<(2 * Hd + 31) / 32, 1024, 0, st>>>(kv_part, dbias + Hd, prow, 2 * Hd);
+  }
   return launch_status();
 }
 
 }  // namespace
 
-// Workspace of the fused backward: delta [B*H*S] then dQacc [B*S*H*D] (fp32),
-// dQacc 16-byte aligned.
+// Workspace of the fused backward (fp32 elements, 16-byte aligned pieces):
+// delta [B*H*S] | dQacc [B*S*H*D] | Q-bias partials [kConvParts][H*D] |
+// arrival counters [64] | K/V-bias partials [B*n_kb*4][2*H*D]
+static int64_t al4(int64_t n) { return (n + 3) / 4 * 4; }
 int64_t attention_bwd_fused_ws(int64_t B, int64_t S, int64_t H, int64_t D) {
-  const int64_t d = (B * H * S + 3) / 4 * 4;
-  return d + B * S * H * D;
+  const int64_t n_kb = (S + FB_M - 1) / FB_M;
+  return al4(B * H * S) + al4(B * S * H * D) + al4(kConvParts * H * D) + 64 +
+         B * n_kb * 4 * 2 * H * D;
 }
 
 bool attention_bwd_fused_ok(int64_t D) { return D == FB_D; }
 
 int attention_bwd_fused(const void* qkv, const void* o, const void* dout, const float* lse,
                         void* dqkv, float* ws, int64_t B, int64_t S, int64_t H, int causal,
-                        cudaStream_t st) {
+                        float* dbias, cudaStream_t st) {
   float* delta = ws;
-  float* dq_acc = ws + (B * H * S + 3) / 4 * 4;
-  return causal ? fused_t<true>(qkv, o, dout, lse, delta, dq_acc, dqkv, B, S, H, st)
-                : fused_t<false>(qkv, o, dout, lse, delta, dq_acc, dqkv, B, S, H, st);
+  float* dq_acc = delta + al4(B * H * S);
+  float* part_ws = dq_acc + al4(B * S * H * FB_D);
+  unsigned* counters = reinterpret_cast<unsigned*>(part_ws + al4(kConvParts * H * FB_D));
+  float* kv_part = reinterpret_cast<float*>(counters) + 64;
+  return causal ? fused_t<true>(qkv, o, dout, lse, delta, dq_acc, dqkv, B, S, H, dbias, part_ws,
+                                counters, kv_part, st)
+                : fused_t<false>(qkv, o, dout, lse, delta, dq_acc, dqkv, B, S, H, dbias, part_ws,
+                                 counters, kv_part, st);
 }
 
 }  // namespace vp

@@ -31,7 +31,8 @@ _SIGS = {
     "vp_layernorm_bwd": [vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, c_int, vp, vp],
     "vp_attention_fwd": [vp, vp, vp, i64, i64, i64, i64, c_int, vp],
     "vp_attention_bwd": [vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, c_int, vp],
-    "vp_attention_bwd_ex": [vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, i64, c_int, c_int, vp],
+    "vp_attention_bwd_ex": [vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, i64, c_int, c_int, vp,
+                            vp],
     "vp_attention_bwd_ws_elems": [i64, i64, i64, i64],
     "vp_layernorm_ws_elems": [i64],
     "vp_gemm_dbias_ws_elems": [i64, i64],
@@ -198,20 +199,23 @@ def attention_bwd_ws_elems(batch, seq, heads, head_dim) -> int:
 
 
 def attention_bwd(qkv, out, dout, lse, dqkv, ws, batch, seq, heads, head_dim, causal=True,
-                  stream=None, deterministic=False):
+                  stream=None, deterministic=False, dbias=None):
     """dqkv = d(qkv). ``ws``: fp32 workspace of attention_bwd_ws_elems()
     elements. head_dim 64 runs the fused one-pass kernel (dQ accumulated by
     TMA reduce-add); ``deterministic`` (or other head dims) the two-kernel
-    path."""
+    path. ``dbias`` (fp32 [3*heads*head_dim]) += column sums of dqkv, fused
+    on the one-pass path; returns False when the caller must sum itself."""
     need = attention_bwd_ws_elems(batch, seq, heads, head_dim)
     if ws.numel() < need or ws.dtype != torch.float32:
         raise ValueError(f"attention_bwd: workspace needs {need} fp32 elements")
-    _count(3)
+    fused_bias = dbias is not None and head_dim == 64 and not deterministic
+    _count(3 + (1 if fused_bias else 0))
     check(L.vp_attention_bwd_ex(qkv.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(),
                                 dqkv.data_ptr(), ws.data_ptr(), ws.numel(), batch, seq, heads,
                                 head_dim, int(causal), 1 if deterministic else 0,
-                                _stream(stream)), "vp_attention_bwd")
-    return dqkv
+                                dbias.data_ptr() if fused_bias else None, _stream(stream)),
+          "vp_attention_bwd")
+    return fused_bias
 
 
 def embed_fwd(ids, wte, wpe, x, batch, seq, stream=None):

@@ -379,11 +379,13 @@ class GPT2Stage:
         K.gemm(g, w.o, P.g(p + "w_o"), a_kmajor=False, b_kmajor=False,
                epilogue=K.EPI_ACC_F32, stream=stream)
         K.bias_grad(g, P.g(p + "b_o"), self.bias_ws, stream)
-        K.attention_bwd(w.qkv, w.o, self.do, w.lse, self.dqkv, self.delta, self.mb,
-                        cfg.seq_len, cfg.heads, cfg.head_dim, cfg.causal, stream)
+        fused_bq = K.attention_bwd(w.qkv, w.o, self.do, w.lse, self.dqkv, self.delta, self.mb,
+                                   cfg.seq_len, cfg.heads, cfg.head_dim, cfg.causal, stream,
+                                   dbias=P.g(p + "b_qkv"))
         K.gemm(self.dqkv, x, P.g(p + "w_qkv"), a_kmajor=False, b_kmajor=False,
                epilogue=K.EPI_ACC_F32, stream=stream)
-        K.bias_grad(self.dqkv, P.g(p + "b_qkv"), self.bias_ws, stream)
+        if not fused_bq:
+            K.bias_grad(self.dqkv, P.g(p + "b_qkv"), self.bias_ws, stream)
         # dx = dy1 + dqkv @ Wqkv (in place on g)
         K.gemm(self.dqkv, P.w(p + "w_qkv"), g, b_kmajor=False, epilogue=K.EPI_RESID, aux=g,
                stream=stream)
@@ -538,12 +540,15 @@ class GPT2Stage:
                epilogue=K.EPI_ACC_F32, stream=stream)
         if not fused:
             K.bias_grad(gy, P.g(p + "b_o"), self.bias_ws, stream)
-        K.attention_bwd(w.qkv, w.o, self.do, w.lse, self.dqkv, self.delta, self.mb,
-                        cfg.seq_len, cfg.heads, cfg.head_dim, cfg.causal, stream)
+        # dqkv, and the QKV bias gradient (its column sums) in the same passes
+        fused_bq = K.attention_bwd(w.qkv, w.o, self.do, w.lse, self.dqkv, self.delta, self.mb,
+                                   cfg.seq_len, cfg.heads, cfg.head_dim, cfg.causal, stream,
+                                   dbias=P.g(p + "b_qkv"))
         K.gemm(self.dqkv, P.w(p + "w_qkv"), self.dc, b_kmajor=False, stream=stream)
         K.gemm(self.dqkv, w.a, P.g(p + "w_qkv"), a_kmajor=False, b_kmajor=False,
                epilogue=K.EPI_ACC_F32, stream=stream)
-        K.bias_grad(self.dqkv, P.g(p + "b_qkv"), self.bias_ws, stream)
+        if not fused_bq:
+            K.bias_grad(self.dqkv, P.g(p + "b_qkv"), self.bias_ws, stream)
         # g = d(layer input) = d(output of the layer below)
         lower_fc2 = P.g(f"l{lower}.b_fc2") if (fused and lower is not None) else None
         K.layernorm_bwd(self.dc, x, P.w(p + "ln1_g"), w.mean1, w.rstd1, g,

@@ -111,6 +111,14 @@ def test_attention_bwd_fused_matches_deterministic():
     assert rel(a, b.float()) < 5e-3
     # dK, dV come from one CTA each: identical up to the P/dS rounding order
     assert rel(a[:, H * D:], b[:, H * D:].float()) < 5e-3
+    # QKV bias gradient fused into the passes = column sums of dqkv
+    db = torch.ones(3 * H * D, device="cuda")
+    c = torch.empty_like(qkv)
+    assert K.attention_bwd(qkv, o, do, lse, c, ws, B, S, H, D, True, dbias=db)
+    assert rel(db, 1 + c.float().sum(0)) < 2e-3
+    db2 = torch.ones(3 * H * D, device="cuda")
+    assert K.attention_bwd(qkv, o, do, lse, c, ws, B, S, H, D, True, dbias=db2)
+    assert rel(db2, db) < 1e-4
 
 
 def test_attention_forward_deterministic():
