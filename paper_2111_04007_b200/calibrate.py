@@ -40,14 +40,23 @@ AR_BW = 725e9
 
 
 def _time(fn, iters=5):
-    for _ in range(2):
-        fn()
+    """GPU time of ``fn`` (µs): captured once into a CUDA graph and replayed,
+    as the executor runs it, so host launch cost does not inflate it."""
+    fn()
     torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(iters):
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
         fn()
-    b.record()
+    with torch.cuda.stream(s):
+        for _ in range(2):
+            g.replay()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        for _ in range(iters):
+            g.replay()
+        b.record(s)
     torch.cuda.synchronize()
     return a.elapsed_time(b) / iters * 1e3  # µs
 
