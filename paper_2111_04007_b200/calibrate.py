@@ -68,7 +68,9 @@ def measure(cfg_name: str, m: int):
     mid = GPT2Stage(cfg, StageSpec(1, 3, (1,)), m, dev, seed=0, init_device="cuda")
     x = torch.randn(mid.T, cfg.hidden, device=dev).bfloat16()
     g = torch.randn_like(x) * 1e-3
-    layer_f = _time(lambda: mid.forward(x, None, save=False))
+    # the simulator prices F and R alike (recompute_scale 1): use the saving
+    # forward, which is what R (and a last stage's F) executes
+    layer_f = _time(lambda: mid.forward(x, None, save=True))
     mid.forward(x, None, save=True)
     layer_b = _time(lambda: mid.backward(g, None))
     del mid
@@ -82,7 +84,7 @@ def measure(cfg_name: str, m: int):
     ids = b["input_ids"].to(dev).view(-1)
     types = b.get("token_type_ids")
     types = types.to(dev).view(-1) if types is not None else None
-    full_f = _time(lambda: first.forward(None, ids, save=False, types=types))
+    full_f = _time(lambda: first.forward(None, ids, save=True, types=types))
     embed_f = max(full_f - layer_f, 0.0)
     del first
     torch.cuda.empty_cache()

@@ -339,6 +339,42 @@ class Varuna:
         order = execution_order(self.schedule, pc, profile, model, opportunistic=True)
         return order[self.stage_id]
 
+    def retune_dispatch(self, timeline: dict) -> None:
+        """Re-derive the opportunistic dispatch order from MEASURED task
+        times: every rank contributes its stage's mean F/R/B of a traced step
+        (``step(trace=True)`` timeline), and the replica kernel re-runs the
+        schedule over one cut-point per stage with those times. Collective
+        over the pipeline ranks; all ranks compute the same orders."""
+        from .calibration import CalibrationProfile, CutpointTimes
+        from .core import make_block_model
+        from .simulator import execution_order
+        P = self.P
+        sums = torch.zeros(self.world, 3, dtype=torch.float64, device=self.device)
+        by = {F: [], B: [], R: []}
+        for kind, _, a, b in timeline["tasks"]:
+            by[kind].append(b - a)
+        for kind, col in ((F, 0), (B, 1), (R, 2)):
+            if by[kind]:
+                sums[self.rank, col] = sum(by[kind]) / len(by[kind])
+        if self.world > 1:
+            dist.all_reduce(sums)
+        f = [max(1.0, float(sums[s, 0])) for s in range(P)]     # replica 0: ranks 0..P-1
+        bw = [max(1.0, float(sums[s, 1])) for s in range(P)]
+        rr = [float(sums[s, 2]) / f[s] for s in range(P) if sums[s, 2] > 0]
+        rscale = sum(rr) / len(rr) if rr else 1.0
+        m = self.m
+        z = {m: 0}
+        cps = tuple(CutpointTimes({m: round(f[s])}, {m: round(bw[s])}, z, z, z, z, z, z,
+                                  {d: 0 for d in sorted({1, self.D})}) for s in range(P))
+        prof = CalibrationProfile((m,), tuple(sorted({1, self.D})), cps)
+        pc = ParallelConfig(P, self.D, m, self.N, tuple(range(P)))
+        model = make_block_model("stages", P, self.cfg.hidden, self.cfg.seq_len)
+        order = execution_order(self.schedule, pc, prof, model, opportunistic=True,
+                                recompute_scale=rscale)
+        self.tasks = order[self.stage_id]
+        self.dispatch = "opportunistic"
+        self._check_plan()
+
     def _check_plan(self):
         """The executor relies on rule 2 (R(j) directly before B(j)) and on the
         last stage's F(j)/B(j) alternation (sp/scheduler.py:228-241)."""
