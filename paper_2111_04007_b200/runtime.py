@@ -369,9 +369,38 @@ class Varuna:
         prof = CalibrationProfile((m,), tuple(sorted({1, self.D})), cps)
         pc = ParallelConfig(P, self.D, m, self.N, tuple(range(P)))
         model = make_block_model("stages", P, self.cfg.hidden, self.cfg.seq_len)
-        order = execution_order(self.schedule, pc, prof, model, opportunistic=True,
-                                recompute_scale=rscale)
-        self.tasks = order[self.stage_id]
+        # candidates: the opportunistic order under the measured times, the
+        # static Varuna order and the order in use; each is replayed
+        # statically by the simulator with the measured times and the
+        # shortest predicted mini-batch wins (all ranks agree: same inputs)
+        import numpy as np
+        from .simulator import build_placement, simulate_minibatch
+        from .core import uniform_cluster
+        current = [None] * self.world
+        if self.world > 1:
+            dist.all_gather_object(current, self.tasks)
+        else:
+            current = [self.tasks]
+        cands = [execution_order(self.schedule, pc, prof, model, opportunistic=True,
+                                 recompute_scale=rscale),
+                 [list(zip(*[a.tolist() for a in self.schedule.stage_slice(k)]))
+                  for k in range(P)],
+                 current[:P]]
+        place = build_placement(uniform_cluster(P * self.D, max(P * self.D, 1)), P, self.D)
+        best, best_t = None, None
+        for order in cands:
+            kinds, mbs, offs = [], [], [0]
+            for k in range(P):
+                kinds += [a for a, _ in order[k]]
+                mbs += [j for _, j in order[k]]
+                offs.append(len(kinds))
+            sch = Schedule("candidate", P, self.N, np.array(kinds, np.int64),
+                           np.array(mbs, np.int64), np.array(offs, np.int64), 1, 2, 1)
+            t = simulate_minibatch(sch, pc, prof, place, model, opportunistic=False,
+                                   recompute_scale=rscale).minibatch_us
+            if best_t is None or t < best_t:
+                best, best_t = order, t
+        self.tasks = best[self.stage_id]
         self.dispatch = "opportunistic"
         self._check_plan()
 
