@@ -27,7 +27,7 @@ def timed(fn, n_sets, iters=20):
 def main():
     rows = 8192
     out = {}
-    for cols in (1024, 3072):
+    for cols in (1024, 1920, 3072):
         n = 4
         xs = [torch.randn(rows, cols, device="cuda").bfloat16() for _ in range(n)]
         dys = [torch.randn(rows, cols, device="cuda").bfloat16() for _ in range(n)]

@@ -219,28 +219,29 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   }
 }
 
-// ------------------------------------------- fused backward, warp pairs
-// A row is split between the two warps of a pair (half the 16-byte vectors
-// each): x and dy are unpacked once into fp32 registers, gamma stays in
-// registers for the whole kernel, and the two row sums (dy*g, dy*g*xhat) are
-// exchanged through shared memory with a 64-thread named barrier. Half the
-// columns per thread halves the register-resident partials (dgamma, dbeta,
-// dsum), so 12 warps fit per SM; ~40 % fewer instructions per element than
-// the one-warp-per-row kernel above.
+// ------------------------------------- fused backward, warp groups per row
+// A row is split between the W warps of a group (1/W of the 16-byte vectors
+// each; G groups per CTA): x and dy are unpacked once into fp32 registers,
+// gamma stays in registers for the whole kernel, and the two row sums
+// (dy*g, dy*g*xhat) are exchanged through shared memory with a named
+// barrier over the group's W*32 threads. 1/W of the columns per thread keeps
+// the register-resident partials (dgamma, dbeta, dsum) small: W=2 for
+// h <= 1024 (12 warps per SM), W=4/8 for the 1920/3072/4096-wide rows of the
+// larger models (8 warps per SM).
 constexpr int kPairs = 6;
-template <int NV, bool SUM>
-__global__ void __launch_bounds__(kPairs * 64, 1)
-    ln_bwd_pair_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+template <int W, int G, int NV, bool SUM>
+__global__ void __launch_bounds__(W * G * 32, 1)
+    ln_bwd_group_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
                        const __nv_bfloat16* __restrict__ g, const float* __restrict__ mean,
                        const float* __restrict__ rstd, __nv_bfloat16* __restrict__ dx,
                        float* __restrict__ ws, int64_t rows, int cols, int accumulate) {
-  extern __shared__ float red[];  // [kPairs][cols] reduction buffer
-  __shared__ float xch[kPairs][2][2][2];  // [pair][row parity][half][s1, s2]
+  extern __shared__ float red[];  // [G][cols] reduction buffer
+  __shared__ float xch[G][2][W][2];  // [group][row parity][member][s1, s2]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int pair = warp >> 1, half = warp & 1;
-  const int nvec = cols >> 3, hvec = nvec >> 1;  // vectors per half row
+  const int pair = warp / W, half = warp % W;  // group, member
+  const int nvec = cols >> 3, hvec = nvec / W;   // vectors per member
   const int v0 = half * hvec;
-  const int64_t npairs = static_cast<int64_t>(gridDim.x) * kPairs;
+  const int64_t npairs = static_cast<int64_t>(gridDim.x) * G;
   float gam[NV][8];
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
@@ -267,7 +268,7 @@ __global__ void __launch_bounds__(kPairs * 64, 1)
       v[i] = c < hvec ? r[c] : make_uint4(0u, 0u, 0u, 0u);
     }
   };
-  int64_t row = static_cast<int64_t>(blockIdx.x) * kPairs + pair;
+  int64_t row = static_cast<int64_t>(blockIdx.x) * G + pair;
   uint4 xc[NV], dc[NV];
   if (row < rows) {
     load_half(x, row, xc);
@@ -306,9 +307,14 @@ __global__ void __launch_bounds__(kPairs * 64, 1)
       xch[pair][parity][half][0] = s1;
       xch[pair][parity][half][1] = s2;
     }
-    asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
-    const float m1 = (s1 + xch[pair][parity][half ^ 1][0]) / cols;
-    const float m2 = (s2 + xch[pair][parity][half ^ 1][1]) / cols;
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + pair), "r"(W * 32) : "memory");
+    float t1 = 0.f, t2 = 0.f;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {  // fixed order: every member gets the same sums
+      t1 += xch[pair][parity][w][0];
+      t2 += xch[pair][parity][w][1];
+    }
+    const float m1 = t1 / cols, m2 = t2 / cols;
     uint4* dxr = reinterpret_cast<uint4*>(dx + row * cols) + v0;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
@@ -358,7 +364,7 @@ __global__ void __launch_bounds__(kPairs * 64, 1)
     for (int c = threadIdx.x; c < cols; c += blockDim.x) {
       float t = 0.f;
 #pragma unroll
-      for (int w = 0; w < kPairs; ++w) t += red[w * cols + c];
+      for (int w = 0; w < G; ++w) t += red[w * cols + c];
       ws[(static_cast<int64_t>(blockIdx.x) * 3 + q) * cols + c] = t;
     }
     __syncthreads();
@@ -581,25 +587,51 @@ extern "C" int vp_layernorm_bwd_ex(const void* dy, const void* x, const void* ga
   const int c3 = static_cast<int>(nq * cols);
   int parts;
   const int64_t nvec = cols / 8;
-  const int64_t hneed = (nvec / 2 + 31) / 32;  // vectors per lane of a half row
-  if ((nvec % 2) == 0 && hneed <= 2 && !getenv("VP_LN_WARP_ROW")) {
-    // warp pairs, one CTA (12 warps) per SM, partials in registers
-    parts = static_cast<int>(std::min<int64_t>(device_sms(), (rows + kPairs - 1) / kPairs));
-    const size_t smem = static_cast<size_t>(kPairs) * cols * sizeof(float);
-    auto launch = [&](auto kern) {
+  // warps per row W: 2 up to h=1024, else the smallest W in {4, 8} giving
+  // <= 3 vectors per lane (W must divide the row's vectors)
+  int W = 0, need = 0;
+  if (nvec % 2 == 0 && (nvec / 2 + 31) / 32 <= 2) {
+    W = 2;
+    need = static_cast<int>((nvec / 2 + 31) / 32);
+  } else if (nvec % 4 == 0 && (nvec / 4 + 31) / 32 <= 3) {
+    W = 4;
+    need = static_cast<int>((nvec / 4 + 31) / 32);
+  } else if (nvec % 8 == 0 && (nvec / 8 + 31) / 32 <= 3) {
+    W = 8;
+    need = static_cast<int>((nvec / 8 + 31) / 32);
+  }
+  if (getenv("VP_LN_WARP_ROW")) W = 0;
+  if (W) {
+    auto launch = [&](auto kern, int G) {
+      parts = static_cast<int>(std::min<int64_t>(device_sms(), (rows + G - 1) / G));
+      const size_t smem = static_cast<size_t>(G) * cols * sizeof(float);
       static bool set = false;
       if (!set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
         set = true;
       }
-      kern<<<parts, kPairs * 64, smem, st>>>(
+      kern<<<parts, W * G * 32, smem, st>>>(
           reinterpret_cast<const __nv_bfloat16*>(dy), reinterpret_cast<const __nv_bfloat16*>(x),
           reinterpret_cast<const __nv_bfloat16*>(gamma), mean, rstd,
           reinterpret_cast<__nv_bfloat16*>(dx), workspace, rows, static_cast<int>(cols),
           accumulate);
     };
-    if (hneed == 1) dsum ? launch(ln_bwd_pair_kernel<1, true>) : launch(ln_bwd_pair_kernel<1, false>);
-    else dsum ? launch(ln_bwd_pair_kernel<2, true>) : launch(ln_bwd_pair_kernel<2, false>);
+#define LN_G(WW, GG, NN)                                                              \
+  (dsum ? launch(ln_bwd_group_kernel<WW, GG, NN, true>, GG)                            \
+        : launch(ln_bwd_group_kernel<WW, GG, NN, false>, GG))
+    if (W == 2) {
+      if (need == 1) LN_G(2, kPairs, 1);
+      else LN_G(2, kPairs, 2);
+    } else if (W == 4) {
+      if (need == 1) LN_G(4, 2, 1);
+      else if (need == 2) LN_G(4, 2, 2);
+      else LN_G(4, 2, 3);
+    } else {
+      if (need == 1) LN_G(8, 1, 1);
+      else if (need == 2) LN_G(8, 1, 2);
+      else LN_G(8, 1, 3);
+    }
+#undef LN_G
   } else if (nv <= 4) {
     // one CTA per SM (register-resident partials); 8 rows per warp pass
     parts = row_ctas(rows, 1);
