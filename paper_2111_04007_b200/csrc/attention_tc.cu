@@ -240,23 +240,29 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_empty[j & 1]);
+      // masked scores -> -inf: exp2 gives exactly 0, no select per element
       if (need_mask) {
 #pragma unroll
         for (int i = 0; i < TA_BN; ++i)
-          if (k0 + i >= lim) sc[i] = __float_as_uint(-FLT_MAX);
+          if (k0 + i >= lim) sc[i] = __float_as_uint(-INFINITY);
       }
+      // row max: 3-input FMNMX3, 8 independent chains
       float pm[8];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) pm[t] = -FLT_MAX;
+      for (int t = 0; t < 8; ++t) pm[t] = __uint_as_float(sc[t]);
 #pragma unroll
-      for (int i = 0; i < TA_BN; ++i) pm[i & 7] = fmaxf(pm[i & 7], __uint_as_float(sc[i]));
-      const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
-                             fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
+      for (int i = 8; i < TA_BN; i += 16) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          pm[t] = fmax3(pm[t], __uint_as_float(sc[i + t]), __uint_as_float(sc[i + 8 + t]));
+      }
+      const float mx = fmax3(fmax3(pm[0], pm[1], pm[2]), fmax3(pm[3], pm[4], pm[5]),
+                             fmaxf(pm[6], pm[7]));
       const float m_cand = fmaxf(m, mx * scale_log2);
       const bool grow = m_cand > m + 8.f;   // lazy: keep a stale max unless it grew > 2^8
       const float m_new = grow ? m_cand : m;
       const float corr = fast_exp2(m - m_new);  // 1 when !grow; 0 for the first block
-      // P = exp2(s*scale - m) (masked -> 0), row sum
+      // P = exp2(s*scale - m), row sum
       float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       uint4 pk[TA_BN / 8];
 #pragma unroll
@@ -264,9 +270,7 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
         float f[8];
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
-          const float xs = __uint_as_float(sc[g * 8 + t]);
-          const float e = fast_exp2(fmaf(xs, scale_log2, -m_new));
-          f[t] = (!need_mask || xs != -FLT_MAX) ? e : 0.f;
+          f[t] = fast_exp2(fmaf(__uint_as_float(sc[g * 8 + t]), scale_log2, -m_new));
           ps[t] += f[t];
         }
         pk[g] = pack8(f);
