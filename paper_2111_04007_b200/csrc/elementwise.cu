@@ -245,12 +245,29 @@ __global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __rest
   // fixed-order sum of the parts: thread (tx, ty) takes parts ty, ty+8, ...
   float f[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (c0 < cols) {
-    for (int p = ty; p < parts; p += 8) {
-      const float4* src = reinterpret_cast<const float4*>(ws + static_cast<int64_t>(p) * cols + c0);
-      const float4 a = __ldcg(src), b = __ldcg(src + 1);
-      f[0] += a.x; f[1] += a.y; f[2] += a.z; f[3] += a.w;
-      f[4] += b.x; f[5] += b.y; f[6] += b.z; f[7] += b.w;
+    // 4 parts in flight per step (the tail of the last CTA is latency-bound);
+    // the grouping is fixed, so the sum order does not depend on timing
+    float g4[4][8] = {};
+    int p = ty;
+    for (; p + 24 < parts; p += 32) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int pp = p + 8 * u;
+        const float4* src = reinterpret_cast<const float4*>(ws + static_cast<int64_t>(pp) * cols + c0);
+        const float4 a = __ldcg(src), b = __ldcg(src + 1);
+        g4[u][0] += a.x; g4[u][1] += a.y; g4[u][2] += a.z; g4[u][3] += a.w;
+        g4[u][4] += b.x; g4[u][5] += b.y; g4[u][6] += b.z; g4[u][7] += b.w;
+      }
     }
+    for (; p < parts; p += 8) {
+      const int pp = p;
+      const float4* src = reinterpret_cast<const float4*>(ws + static_cast<int64_t>(pp) * cols + c0);
+      const float4 a = __ldcg(src), b = __ldcg(src + 1);
+      g4[0][0] += a.x; g4[0][1] += a.y; g4[0][2] += a.z; g4[0][3] += a.w;
+      g4[0][4] += b.x; g4[0][5] += b.y; g4[0][6] += b.z; g4[0][7] += b.w;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[j] = (g4[0][j] + g4[1][j]) + (g4[2][j] + g4[3][j]);
   }
   __syncthreads();
 #pragma unroll
