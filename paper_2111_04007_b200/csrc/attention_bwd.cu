@@ -48,9 +48,6 @@ constexpr int FB_CW = 8;   // softmax-gradient warps (4..11)
 constexpr int FB_DW = 4;   // dQ drain warps (12..15), one per TMEM lane quadrant
 constexpr int FB_THREADS = 128 + 32 * (FB_CW + FB_DW);
 constexpr int64_t kConvParts = 64;  // row parts of the dQ convert / Q-bias column sums
-#ifndef FB_SPLIT_S
-#define FB_SPLIT_S 0
-#endif
 
 struct FbSmem {
   static constexpr int TILE = 128 * 128;                     // 128 rows x 64 bf16 (SW128)
@@ -85,15 +82,6 @@ __device__ __forceinline__ float warp_colsum32(const float (&v)[32], uint32_t la
   return t[0];
 }
 
-__device__ __forceinline__ void red_add_v4(float* p, uint32_t a, uint32_t b, uint32_t c,
-                                           uint32_t d) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(__uint_as_float(a)),
-               "f"(__uint_as_float(b)), "f"(__uint_as_float(c)), "f"(__uint_as_float(d))
-               : "memory");
-}
-#ifndef FB_DQ_RED
-#define FB_DQ_RED 0
-#endif
 
 // TMEM columns (512, one CTA per SM):
 //   [0,128) S^T   [128,256) dP^T   [256,320) dV   [320,384) dK   [384,448) dQ
@@ -208,7 +196,7 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       // ===== MMA issuer =====
-      constexpr uint32_t idST = idesc_bf16(128, FB_SPLIT_S ? FB_N / 2 : FB_N, false, false);
+      constexpr uint32_t idST = idesc_bf16(128, FB_N, false, false);
       constexpr uint32_t idG = idesc_bf16(128, D, false, true);
       constexpr uint32_t idQ = idesc_bf16(128, D, true, true);
       const uint32_t sK = smem_u32(smem + L::K_OFF), sV = smem_u32(smem + L::V_OFF);
@@ -252,22 +240,6 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
         TR(8);
         // two 64-query halves: half 0 may overwrite TMEM as soon as every
         // warp has loaded its half-0 columns of the previous block
-#if FB_SPLIT_S
-#pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
-          mbar_wait(&st_empty[hf], (it & 1) ^ 1);
-          if (hf == 0) TR(9); else TR(10);
-          tc_fence_after();
-#pragma unroll
-          for (int k = 0; k < D / 16; ++k) {
-            umma_f16(tS + hf * 64, sdesc_sw128(sK + k * 32, 16, 1024),
-                     sdesc_sw128(sQ + hf * 8192 + k * 32, 16, 1024), idST, k > 0);
-            umma_f16(tdP + hf * 64, sdesc_sw128(sV + k * 32, 16, 1024),
-                     sdesc_sw128(sdO + hf * 8192 + k * 32, 16, 1024), idST, k > 0);
-          }
-          umma_commit(&st_full[hf]);
-        }
-#else
         mbar_wait(&st_empty[0], (it & 1) ^ 1);
         mbar_wait(&st_empty[1], (it & 1) ^ 1);
         TR(9);
@@ -281,7 +253,6 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
         }
         umma_commit(&st_full[0]);
         umma_commit(&st_full[1]);
-#endif
         if (it >= 1) issue_grad(it - 1);
       }
       issue_grad(n_it - 1);
@@ -424,19 +395,6 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(dq_empty);
       const int q = (i0 + j) * FB_N + qd * 32;
-#if FB_DQ_RED
-      // vector reductions straight from registers into the fp32 accumulator
-      if (q + static_cast<int>(lane) < S) {
-        float* dst = dq_acc + (static_cast<int64_t>(b) * S + q + lane) * Hd + h * D;
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          red_add_v4(dst + 4 * k, v0[4 * k], v0[4 * k + 1], v0[4 * k + 2], v0[4 * k + 3]);
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          red_add_v4(dst + 32 + 4 * k, v1[4 * k], v1[4 * k + 1], v1[4 * k + 2], v1[4 * k + 3]);
-      }
-      continue;
-#endif
       const uint32_t s0 = smem_u32(stg + lane * 128);
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
@@ -451,9 +409,7 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
         fence_async_smem();
         __syncwarp();
         if (lane == 0) {
-#ifndef VP_NO_DQ_REDUCE
           tma_reduce_add_3d(&tmDQ, stg, h * D + half * 32, q, b);
-#endif
           bulk_commit();
         }
       }
