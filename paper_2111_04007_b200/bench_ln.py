@@ -60,6 +60,11 @@ def main():
     bws = torch.zeros(K.bias_grad_ws_elems(4096), device="cuda")
     t = timed(lambda i: K.bias_grad(big, db4, bws), 1)
     out["colsum_4096_warm_us"] = round(t, 2)
+    lg = torch.randn(8192, 51200, device="cuda").bfloat16()
+    lab = torch.randint(0, 51200, (8192,), device="cuda")
+    lr = torch.empty(8192, device="cuda")
+    t = timed(lambda i: K.xent_fwd_bwd(lg, lab, lr, 1e-6), 1, iters=5)
+    out["xent_8192x51200_us"] = round(t, 1)
     print(json.dumps(out))
 
 

@@ -125,7 +125,27 @@ __global__ void __launch_bounds__(THREADS)
   float m = -FLT_MAX, s = 0.f;
   const int64_t nvec = vocab >> 3;
   const uint4* lv = reinterpret_cast<const uint4*>(lr);
-  for (int64_t c = threadIdx.x; c < nvec; c += THREADS) {
+  // 4 independent 16-byte loads in flight per thread, then the online
+  // (max, sum-exp) update over the 32 values
+  int64_t c = threadIdx.x;
+  for (; c + 3 * THREADS < nvec; c += 4 * THREADS) {
+    uint4 u[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) u[k] = lv[c + k * THREADS];
+    float f[32];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) unpack8(u[k], *reinterpret_cast<float(*)[8]>(f + 8 * k));
+    float mm = f[0];
+#pragma unroll
+    for (int j = 1; j < 32; ++j) mm = fmaxf(mm, f[j]);
+    if (mm > m) {
+      s *= __expf(m - mm);
+      m = mm;
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) s += __expf(f[j] - m);
+  }
+  for (; c < nvec; c += THREADS) {
     float f[8];
     unpack8(lv[c], f);
     float mm = f[0];
@@ -170,17 +190,26 @@ __global__ void __launch_bounds__(THREADS)
   const float lse = s_lse;
   const bool valid = label >= 0 && label < vocab;
   uint4* ov = reinterpret_cast<uint4*>(lr);
-  for (int64_t c = threadIdx.x; c < nvec; c += THREADS) {
+  auto grad8 = [&](int64_t cc, uint4 v) {
     float f[8];
-    unpack8(ov[c], f);
+    unpack8(v, f);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       float p = valid ? __expf(f[j] - lse) : 0.f;
-      if (c * 8 + j == label) p -= 1.f;
+      if (cc * 8 + j == label) p -= 1.f;
       f[j] = p * scale;
     }
-    ov[c] = pack8(f);
+    ov[cc] = pack8(f);
+  };
+  int64_t c2 = threadIdx.x;
+  for (; c2 + 3 * THREADS < nvec; c2 += 4 * THREADS) {
+    uint4 u[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) u[k] = ov[c2 + k * THREADS];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) grad8(c2 + k * THREADS, u[k]);
   }
+  for (; c2 < nvec; c2 += THREADS) grad8(c2, ov[c2]);
 }
 
 // ---------------------------------------------------------------- bias grad
