@@ -3,8 +3,10 @@
 // residual add, grad-norm/overflow reduction (K11), fused AdamW (K10), casts.
 #include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 
 #include "common.cuh"
+#include "sm100.cuh"
 
 namespace vp {
 namespace {
@@ -210,6 +212,93 @@ __global__ void __launch_bounds__(THREADS)
     for (int k = 0; k < 4; ++k) grad8(c2 + k * THREADS, u[k]);
   }
   for (; c2 < nvec; c2 += THREADS) grad8(c2, ov[c2]);
+}
+
+// One HBM read per logit: the row (vocab*2 bytes <= 110 KB) is pulled into
+// shared memory by bulk async copies, the (max, sum-exp) reduction and the
+// gradient pass both read it from there; two rows (CTAs) per SM in flight.
+__global__ void __launch_bounds__(512)
+    xent_smem_kernel(__nv_bfloat16* __restrict__ logits, const int64_t* __restrict__ labels,
+                     float* __restrict__ loss_rows, float* __restrict__ loss_sum, int64_t vocab,
+                     float scale) {
+  constexpr int T = 512;
+  extern __shared__ __align__(128) uint8_t xs_raw[];
+  __shared__ uint64_t bar;
+  __shared__ float s_m[T / 32], s_s[T / 32];
+  __shared__ float s_lse;
+  const int64_t row = blockIdx.x;
+  __nv_bfloat16* lr = logits + row * vocab;
+  const uint32_t bytes = static_cast<uint32_t>(vocab * 2);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    mbar_expect_tx(&bar, bytes);
+    constexpr uint32_t CHUNK = 32768;
+    for (uint32_t off = 0; off < bytes; off += CHUNK)
+      bulk_g2s(xs_raw + off, reinterpret_cast<const uint8_t*>(lr) + off,
+               bytes - off < CHUNK ? bytes - off : CHUNK, &bar);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  uint4* sv = reinterpret_cast<uint4*>(xs_raw);
+  const int nvec = static_cast<int>(vocab >> 3);
+  const int64_t label = labels[row];
+  const int w = threadIdx.x >> 5;
+  // pass 1: row max
+  float m = -FLT_MAX;
+  for (int c = threadIdx.x; c < nvec; c += T) {
+    float f[8];
+    unpack8(sv[c], f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) m = fmaxf(m, f[j]);
+  }
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) s_m[w] = m;
+  __syncthreads();
+  float mx = s_m[0];
+#pragma unroll
+  for (int i = 1; i < T / 32; ++i) mx = fmaxf(mx, s_m[i]);
+  const bool valid = label >= 0 && label < vocab;
+  const float lab = valid ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(xs_raw)[label]) : 0.f;
+  __syncthreads();  // the label logit is read before pass 2 overwrites the row
+  // pass 2: e = exp(x - max) once per logit, summed in fp32 and kept (bf16)
+  // in place for the gradient pass
+  float sum = 0.f;
+  for (int c = threadIdx.x; c < nvec; c += T) {
+    float f[8];
+    unpack8(sv[c], f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      f[j] = __expf(f[j] - mx);
+      sum += f[j];
+    }
+    sv[c] = pack8(f);
+  }
+  sum = warp_sum(sum);
+  if ((threadIdx.x & 31) == 0) s_s[w] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float Sx = 0.f;
+    for (int i = 0; i < T / 32; ++i) Sx += s_s[i];
+    s_lse = Sx;
+    const float l = valid ? mx + __logf(Sx) - lab : 0.f;
+    loss_rows[row] = l;
+    if (loss_sum && l != 0.f) atomicAdd(loss_sum, l * scale);
+  }
+  __syncthreads();
+  // pass 3: d logits = (e / sum - onehot) * scale
+  const float inv = valid ? scale / s_lse : 0.f;
+  uint4* ov = reinterpret_cast<uint4*>(lr);
+  for (int c = threadIdx.x; c < nvec; c += T) {
+    float f[8];
+    unpack8(sv[c], f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      f[j] *= inv;
+      if (static_cast<int64_t>(c) * 8 + j == label) f[j] -= scale;
+    }
+    ov[c] = pack8(f);
+  }
 }
 
 // ---------------------------------------------------------------- bias grad
@@ -522,8 +611,21 @@ extern "C" int vp_xent_fwd_bwd(void* logits, const int64_t* labels, float* loss_
                                float* loss_sum, int64_t rows, int64_t vocab, float scale,
                                void* stream) {
   if (rows <= 0 || vocab <= 0 || (vocab % 8)) return VP_ERR_ARGS;
-  xent_kernel<512><<<static_cast<unsigned>(rows), 512, 0, ST>>>(BF(logits), labels, loss_rows,
-                                                                loss_sum, vocab, scale);
+  const size_t smem = static_cast<size_t>(vocab) * 2;
+  if (smem <= 110 * 1024 && (reinterpret_cast<uintptr_t>(logits) & 15) == 0 && !getenv("VP_XENT_2PASS")) {
+    static bool set = false;
+    if (!set) {
+      cudaFuncSetAttribute(xent_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           110 * 1024);
+      set = true;
+    }
+    xent_smem_kernel<<<static_cast<unsigned>(rows), 512, smem, ST>>>(BF(logits), labels,
+                                                                    loss_rows, loss_sum, vocab,
+                                                                    scale);
+  } else {
+    xent_kernel<512><<<static_cast<unsigned>(rows), 512, 0, ST>>>(BF(logits), labels, loss_rows,
+                                                                  loss_sum, vocab, scale);
+  }
   return launch_status();
 }
 
