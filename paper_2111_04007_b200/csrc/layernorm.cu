@@ -98,6 +98,92 @@ __global__ void __launch_bounds__(kWarps * 32)
   }
 }
 
+// Forward for wide rows: a group of W warps per row (1/W of the vectors
+// each), row sums exchanged through shared memory with a named barrier per
+// group; the next row's slice is loaded before the current one is reduced.
+template <int W, int G, int NV>
+__global__ void __launch_bounds__(W * G * 32)
+    ln_fwd_group_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g,
+                        const __nv_bfloat16* __restrict__ b, __nv_bfloat16* __restrict__ y,
+                        float* __restrict__ mean_out, float* __restrict__ rstd_out, int64_t rows,
+                        int cols, float eps) {
+  __shared__ float xch[G][2][2][W];  // [group][row parity][sum | sumsq-dev][member]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = warp / W, mem = warp % W;
+  const int nvec = cols >> 3, hvec = nvec / W, v0 = mem * hvec;
+  const int64_t ngroups = static_cast<int64_t>(gridDim.x) * G;
+  const uint4* gv = reinterpret_cast<const uint4*>(g) + v0;
+  const uint4* bv = reinterpret_cast<const uint4*>(b) + v0;
+  auto load = [&](int64_t row, uint4 (&v)[NV]) {
+    const uint4* r = reinterpret_cast<const uint4*>(x + row * cols) + v0;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = lane + i * 32;
+      v[i] = c < hvec ? r[c] : make_uint4(0u, 0u, 0u, 0u);
+    }
+  };
+  int64_t row = static_cast<int64_t>(blockIdx.x) * G + grp;
+  uint4 cur[NV];
+  if (row < rows) load(row, cur);
+  int parity = 0;
+  for (; row < rows; row += ngroups, parity ^= 1) {
+    uint4 nxt[NV];
+    if (row + ngroups < rows) load(row + ngroups, nxt);
+    float v[NV][8];
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      unpack8(cur[i], v[i]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s += v[i][j];
+    }
+    s = warp_sum(s);
+    if (lane == 0) xch[grp][parity][0][mem] = s;
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(W * 32) : "memory");
+    float tot = 0.f;
+#pragma unroll
+    for (int w = 0; w < W; ++w) tot += xch[grp][parity][0][w];
+    const float mu = tot / cols;
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      if (lane + i * 32 < hvec) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float d = v[i][j] - mu;
+          ss += d * d;
+        }
+      }
+    }
+    ss = warp_sum(ss);
+    if (lane == 0) xch[grp][parity][1][mem] = ss;
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(W * 32) : "memory");
+    float tss = 0.f;
+#pragma unroll
+    for (int w = 0; w < W; ++w) tss += xch[grp][parity][1][w];
+    const float rs = rsqrtf(tss / cols + eps);
+    if (mem == 0 && lane == 0) {
+      mean_out[row] = mu;
+      rstd_out[row] = rs;
+    }
+    uint4* yr = reinterpret_cast<uint4*>(y + row * cols) + v0;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = lane + i * 32;
+      if (c < hvec) {
+        float gg[8], bb[8], o[8];
+        unpack8(gv[c], gg);
+        unpack8(bv[c], bb);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = (v[i][j] - mu) * rs * gg[j] + bb[j];
+        yr[c] = pack8(o);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NV; ++i) cur[i] = nxt[i];
+  }
+}
+
 // ------------------------------------------------------- fused backward
 // ws[cta][3][cols]: dgamma, dbeta, dsum partials of this CTA's rows.
 template <int NV, bool SUM>
@@ -557,6 +643,24 @@ extern "C" int vp_layernorm_fwd(const void* x, const void* gamma, const void* be
   if (rows <= 0 || cols <= 0 || (cols % 8)) return VP_ERR_ARGS;
   const int nv = pick_nv(cols);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t nvec = cols / 8;
+  if (nv > 4 && nvec % 4 == 0 && (nvec / 4 + 31) / 32 <= 4 && !getenv("VP_LN_WARP_ROW")) {
+    // wide rows: 4 warps per row, 2 rows per CTA, 4 CTAs per SM
+    const int need = static_cast<int>((nvec / 4 + 31) / 32);
+    const unsigned grid = static_cast<unsigned>(
+        std::min<int64_t>(4 * static_cast<int64_t>(device_sms()), (rows + 1) / 2));
+#define LNF(NN)                                                                              \
+  ln_fwd_group_kernel<4, 2, NN><<<grid, 256, 0, st>>>(                                       \
+      reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<const __nv_bfloat16*>(gamma), \
+      reinterpret_cast<const __nv_bfloat16*>(beta), reinterpret_cast<__nv_bfloat16*>(y), mean, \
+      rstd, rows, static_cast<int>(cols), eps)
+    if (need == 1) LNF(1);
+    else if (need == 2) LNF(2);
+    else if (need == 3) LNF(3);
+    else LNF(4);
+#undef LNF
+    return launch_status();
+  }
   const int grid = row_ctas(rows, 4);
   LN_DISPATCH(nv, ln_fwd_kernel<NV><<<grid, kWarps * 32, 0, st>>>(
                       reinterpret_cast<const __nv_bfloat16*>(x),
