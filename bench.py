@@ -358,14 +358,19 @@ def main():
         e2e = {"value": round(M / (ms_e2e / 1e3), 3), "unit": "samples/s",
                "h2d_bytes_per_step": int(tot[0].item()), "d2h_bytes_per_step": int(tot[1].item())}
 
-    # ---- instrumented step (not timed): GEMM launch durations + task timeline
-    K.GEMM_TIMING["on"] = True
-    K.GEMM_TIMING["records"].clear()
+    # ---- instrumented steps (not timed): the task timeline of a normal
+    # (graph-replayed) step, then GEMM launch durations of an eager step
+    barrier()
     v.trace = True
     res = v.step(dbatch)
     torch.cuda.synchronize()
-    K.GEMM_TIMING["on"] = False
     v.trace = False
+    barrier()
+    K.GEMM_TIMING["on"] = True
+    K.GEMM_TIMING["records"].clear()
+    v.step(dbatch)
+    torch.cuda.synchronize()
+    K.GEMM_TIMING["on"] = False
     recs = K.GEMM_TIMING["records"]
     g_flops = sum(r[0] for r in recs)
     g_ms = sum(r[1].elapsed_time(r[2]) for r in recs)

@@ -381,11 +381,21 @@ class Varuna:
             dist.all_gather_object(current, self.tasks)
         else:
             current = [self.tasks]
-        cands = [execution_order(self.schedule, pc, prof, model, opportunistic=True,
-                                 recompute_scale=rscale),
-                 [list(zip(*[a.tolist() for a in self.schedule.stage_slice(k)]))
-                  for k in range(P)],
-                 current[:P]]
+        # the opportunistic kernel is a heuristic: also run it on perturbed
+        # copies of the measured times (backward and recompute x0.85..1.15)
+        # and keep every distinct order as a candidate
+        def scaled(fb):
+            c2 = tuple(CutpointTimes({m: round(f[s])}, {m: max(1, round(bw[s] * fb))}, z, z, z, z,
+                                     z, z, {d: 0 for d in sorted({1, self.D})}) for s in range(P))
+            return CalibrationProfile((m,), tuple(sorted({1, self.D})), c2)
+        cands = [[list(zip(*[a.tolist() for a in self.schedule.stage_slice(k)]))
+                  for k in range(P)], current[:P]]
+        for fb in (1.0, 0.85, 1.15):
+            for rs in (1.0, 0.85, 1.15):
+                o = execution_order(self.schedule, pc, scaled(fb), model, opportunistic=True,
+                                    recompute_scale=rscale * rs)
+                if o not in cands:
+                    cands.append(o)
         place = build_placement(uniform_cluster(P * self.D, max(P * self.D, 1)), P, self.D)
         best, best_t = None, None
         for order in cands:
