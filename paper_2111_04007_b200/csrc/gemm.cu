@@ -844,7 +844,10 @@ int launch2_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& t
     attr_set = true;
   }
   const int64_t units = ((M + 255) / 256) * ((N + 255) / 256) * split_k;
-  const int64_t clusters = std::min<int64_t>(units, sm_count() / 2);
+  int64_t clusters = std::min<int64_t>(units, sm_count() / 2);
+#ifdef VP_GEMM_TRACE
+  if (const char* c = getenv("VP_GEMM_MAXCL")) clusters = std::min<int64_t>(clusters, atoi(c));
+#endif
   kern<<<static_cast<unsigned>(2 * clusters), kThreads2, G2Cfg<EPI>::kSmem, st>>>(ta, tb, td, tx, M, N, K,
                                                                         split_k, e);
   return cudaGetLastError();
