@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--config", default="gpt2_355m", choices=sorted(MODEL_CONFIGS))
     ap.add_argument("--pd", default=None, help="override P x D, e.g. 4x2")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--m", default="auto",
+                    help="micro-batch size: 'auto' (the planner's choice over the calibration "
+                         "profile's m grid) or an integer")
     ap.add_argument("--dispatch", default="opportunistic", choices=["opportunistic", "static"],
                     help="P>1 task order: the reference's opportunistic policy over the "
                          "calibration profile (default) or the static Varuna schedule")
@@ -102,6 +105,37 @@ def stage_map_for(cfg, P, m, config_name=None):
     prof = CalibrationProfile((m,), (1,), cps)
     model = make_block_model(cfg_name(cfg), cfg.n_layer, cfg.hidden, cfg.seq_len)
     return assign_stages(model, P, m, prof, last_stage_weight=0.75 if P > 1 else 1.0).stage_map
+
+
+def choose_micro_batch(cfg, P, D, M, config_name):
+    """Micro-batch size as the reference planner chooses it (sp/planner.py:
+    106-145): simulate the mini-batch for every m of the B200 calibration
+    profile's grid (Varuna schedule, opportunistic dispatch, the stage map
+    assign_stages picks at that m) and keep the fastest. None without a
+    multi-m profile."""
+    from paper_2111_04007_b200 import (ParallelConfig, build_placement, generate_varuna_schedule,
+                                       load_profile, make_block_model, simulate_minibatch,
+                                       uniform_cluster, JobSpec, micro_batches_for)
+    path = os.path.join(ROOT, "profiles", f"b200_{config_name}.yaml")
+    if not os.path.exists(path):
+        return None
+    prof = load_profile(path)
+    if len(prof.m_grid) < 2 or prof.num_cutpoints != cfg.n_layer:
+        return None
+    model = make_block_model(cfg_name(cfg), cfg.n_layer, cfg.hidden, cfg.seq_len)
+    place = build_placement(uniform_cluster(P * D, 8), P, D)
+    best, best_t = None, None
+    for m in prof.m_grid:
+        N = micro_batches_for(JobSpec(M), m, D)
+        if N < P:  # fewer micro-batches than stages: the pipeline cannot fill
+            continue
+        sm = stage_map_for(cfg, P, m, config_name)
+        pc = ParallelConfig(P, D, m, N, tuple(sm))
+        t = simulate_minibatch(generate_varuna_schedule(P, N, 1.0, 2.0, 1.0), pc, prof, place,
+                               model, opportunistic=P > 1).minibatch_us
+        if best_t is None or t < best_t:
+            best, best_t = m, t
+    return best
 
 
 def gemm_traffic():
@@ -270,6 +304,13 @@ def main():
         P, D = map(int, args.pd.lower().split("x"))
     else:
         P, D = LADDER.get(world, (world, 1))
+    m_how = "config default"
+    if args.m == "auto":
+        m_sel = choose_micro_batch(cfg, P, D, M, args.config)
+        if m_sel is not None:
+            m, m_how = m_sel, "planner: fastest simulated mini-batch over the calibration m grid"
+    elif args.m:
+        m, m_how = int(args.m), "command line"
     N = micro_batches_for(JobSpec(M), m, D)
     stage_map = stage_map_for(cfg, P, m, args.config)
     pc = ParallelConfig(P, D, m, N, stage_map)
@@ -427,7 +468,7 @@ def main():
                        "parallelism": f"pp{P}xdp{D}", "stage_map_sizes":
                            [sum(1 for x in stage_map if x == s) for s in range(P)],
                        "l2": "working set >> 126 MB L2 (no flush needed)", "dropout": cfg.dropout,
-                       "dispatch": dispatch},
+                       "dispatch": dispatch, "micro_batch": m, "micro_batch_choice": m_how},
             "clocks": clk,
             "e2e": e2e,
             "gpu_launches": launches,
