@@ -574,6 +574,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     const uint32_t half = (warp - 4) >> 2;
     uint8_t* wbuf = staging + (warp - 4) * C::kStaging;
     uint32_t local = 0, nbuf = 0;
+    uint32_t aux_phase = 0;  // parity of the two aux-prefetch barriers of this warp
     const uint32_t lane = lane_id();
     for (int64_t u = cid; u < n_units; u += n_clusters, ++local) {
       int64_t mb, nb, kb0, kb1;
@@ -648,7 +649,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             for (int i = 0; i < 32; ++i) v[32 + i] = __uint_as_float(raw[i]);
           }
           if constexpr (kAuxIn) {
-            mbar_wait(&abar[ci], local & 1);
+            // per-chunk phase: a ragged last N tile skips chunks (and their
+            // prefetch), so the barrier phase is not the tile count
+            mbar_wait(&abar[ci], (aux_phase >> ci) & 1u);
+            aux_phase ^= 1u << ci;
             load_row_swizzled(wbuf + ci * 4096, lane, xin);
             __syncwarp();  // every lane has read its aux row before outputs overwrite it
           }

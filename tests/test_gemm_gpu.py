@@ -150,3 +150,23 @@ def test_gemm_fused_bias_grad(M, N):
     out2 = torch.empty_like(out)
     K.gemm(A, B, out2, b_kmajor=False, epilogue=K.EPI_DGELU, aux=x, dbias=db2, dbias_ws=ws)
     assert torch.equal(db, db2) and torch.equal(out, out2)
+
+
+def test_gemm_aux_epilogue_ragged_n_many_tiles():
+    """BIAS_RESID / DGELU / RESID with a ragged last N tile over many
+    persistent tiles per cluster (aux-prefetch barrier phases must follow the
+    chunks actually prefetched; 2.5B shapes: N = 1920, 5760)."""
+    torch.manual_seed(5)
+    for M, N, Kd in ((8192, 1920, 256), (8192, 5760, 128), (4096, 1920, 1920)):
+        A = torch.randn(M, Kd, device="cuda").bfloat16()
+        B = (torch.randn(N, Kd, device="cuda") * 0.05).bfloat16()
+        bias = torch.randn(N, device="cuda").bfloat16()
+        res = torch.randn(M, N, device="cuda").bfloat16()
+        out = res.clone()
+        K.gemm(A, B, out, epilogue=K.EPI_BIAS_RESID, bias=bias, aux=out)
+        ref = res.float() + A.float() @ B.float().t() + bias.float()
+        assert rel(out, ref) < 5e-3
+        x = torch.randn(M, N, device="cuda").bfloat16()
+        out2 = torch.empty_like(x)
+        K.gemm(A, B, out2, epilogue=K.EPI_DGELU, aux=x)
+        assert rel(out2, (A.float() @ B.float().t()) * dgelu(x.float())) < 1e-2
