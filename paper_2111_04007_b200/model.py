@@ -68,6 +68,9 @@ class GPT2Config:
 # BASELINE.json configs.
 CONFIGS = {
     "tiny": GPT2Config(vocab_size=50304, n_layer=4, hidden=256, heads=4, seq_len=128),
+    # parity-only: every GEMM N (576/192/768/2008) and LN width is ragged
+    # against the 128/256-wide tiles, so the partial-tile paths run in-model.
+    "tiny_ragged": GPT2Config(vocab_size=2008, n_layer=4, hidden=192, heads=3, seq_len=128),
     "gpt2_355m": GPT2Config(vocab_size=51200, n_layer=24, hidden=1024, heads=16, seq_len=1024),
     "gpt2_2_5b": GPT2Config(vocab_size=51200, n_layer=54, hidden=1920, heads=20, seq_len=1024),
     "gpt2_8_3b": GPT2Config(vocab_size=51200, n_layer=72, hidden=3072, heads=32, seq_len=1024),

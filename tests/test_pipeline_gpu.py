@@ -18,11 +18,11 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def tiny_setup(P=1, D=1, N=4, m=4):
+def tiny_setup(P=1, D=1, N=4, m=4, name="tiny"):
     from paper_2111_04007_b200 import ParallelConfig, assign_stages, make_block_model, uniform_profile
     from paper_2111_04007_b200.model import CONFIGS
-    cfg = CONFIGS["tiny"]
-    model = make_block_model("tiny", cfg.n_layer, cfg.hidden, cfg.seq_len)
+    cfg = CONFIGS[name]
+    model = make_block_model(name, cfg.n_layer, cfg.hidden, cfg.seq_len)
     a = assign_stages(model, P, m, uniform_profile(cfg.n_layer, 1.0, 2.0, m_grid=(m,)))
     pc = ParallelConfig(P, D, m, N, a.stage_map)
     return cfg, pc
@@ -42,9 +42,10 @@ def oracle_run(cfg, pc, batch, steps=0):
     return o, loss
 
 
-def test_single_gpu_loss_grads_and_update():
+@pytest.mark.parametrize("name", ["tiny", "tiny_ragged"])
+def test_single_gpu_loss_grads_and_update(name):
     from paper_2111_04007_b200.runtime import Varuna, synthetic_batch
-    cfg, pc = tiny_setup()
+    cfg, pc = tiny_setup(name=name)
     batch = synthetic_batch(cfg, pc.micro_batch_size * pc.num_micro_batches, 0)
     v = Varuna(cfg, pc, seed=0)
     res = v.step(batch, apply=False)
