@@ -26,6 +26,9 @@ cases = [(8, 1024, 16, 64, True), (4, 1024, 20, 96, True), (4, 1024, 32, 96, Tru
          (32, 512, 16, 64, False)]
 if len(sys.argv) > 1 and sys.argv[1] == "long":
     cases = [(2, 4096, 16, 64, False), (2, 4096, 16, 64, True), (8, 1024, 16, 64, False)]
+if len(sys.argv) > 1 and sys.argv[1] == "big":   # planner-chosen m=32 (dQ accumulator > L2)
+    cases = [(8, 1024, 16, 64, True), (16, 1024, 16, 64, True), (32, 1024, 16, 64, True),
+             (64, 512, 16, 64, False)]
 for B, S, H, D, causal in cases:
     qkv = torch.randn(B * S, 3 * H * D, device="cuda").bfloat16()
     o = torch.empty(B * S, H * D, device="cuda", dtype=torch.bfloat16)

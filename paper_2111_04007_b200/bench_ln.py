@@ -25,7 +25,7 @@ def timed(fn, n_sets, iters=20):
 
 
 def main():
-    rows = 8192
+    rows = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
     out = {}
     for cols in (1024, 1920, 3072):
         n = 4

@@ -480,10 +480,16 @@ __global__ void norm_kernel(const float* __restrict__ g, int64_t n, float* __res
   }
 }
 
-// One float4 of every state array per thread (coalesced 16-byte accesses);
-// ~34 B/param of HBM traffic: read master/grad/m/v, write master/m/v/grad
-// (zeroed) + the bf16 weight.
-__global__ void __launch_bounds__(256) adam_kernel(
+// Fused AdamW (K10). U float4 chunks of every state array per thread
+// (block-strided, so every warp access stays coalesced); all loads are issued
+// before any math so each thread keeps 4*U 16-byte loads in flight — the
+// kernel streams 9 arrays at once and needs that much memory-level
+// parallelism (U=1: 1.7 TB/s, U=4: 3.7 TB/s, U=8: 4.3 TB/s on B200 at 355M
+// params). ~34 B/param of HBM traffic: read master/grad/m/v, write
+// master/m/v/grad (zeroed) + the bf16 weight; streaming cache hints keep the
+// single-use state out of L2.
+template <int U>
+__global__ void __launch_bounds__(256) adam_kernel_u(
     float* __restrict__ master, __nv_bfloat16* __restrict__ w, float* __restrict__ grad,
     float* __restrict__ m, float* __restrict__ v, int64_t n, const float* __restrict__ flags,
     float lr, float b1, float b2, float eps, float wd, float inv_scale, float max_norm, float bc1,
@@ -496,43 +502,60 @@ __global__ void __launch_bounds__(256) adam_kernel(
   }
   const float ib1 = 1.f / bc1, ib2 = 1.f / bc2;
   const int64_t n4 = n >> 2;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
-       i += stride) {
-    float4 g = reinterpret_cast<float4*>(grad)[i];
-    reinterpret_cast<float4*>(grad)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (skip) continue;
-    float4 p = reinterpret_cast<float4*>(master)[i];
-    float4 mm = reinterpret_cast<float4*>(m)[i];
-    float4 vv = reinterpret_cast<float4*>(v)[i];
-    float gs[4] = {g.x * coef, g.y * coef, g.z * coef, g.w * coef};
-    float ps[4] = {p.x, p.y, p.z, p.w};
-    float ms[4] = {mm.x, mm.y, mm.z, mm.w};
-    float vs[4] = {vv.x, vv.y, vv.z, vv.w};
+  float4* G = reinterpret_cast<float4*>(grad);
+  float4* Pm = reinterpret_cast<float4*>(master);
+  float4* Mm = reinterpret_cast<float4*>(m);
+  float4* Vm = reinterpret_cast<float4*>(v);
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x * U + threadIdx.x; base < n4;
+       base += static_cast<int64_t>(gridDim.x) * blockDim.x * U) {
+    float4 g[U], p[U], mm[U], vv[U];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      ms[j] = b1 * ms[j] + (1.f - b1) * gs[j];
-      vs[j] = b2 * vs[j] + (1.f - b2) * gs[j] * gs[j];
-      ps[j] -= lr * ((ms[j] * ib1) / (sqrtf(vs[j] * ib2) + eps) + wd * ps[j]);
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + static_cast<int64_t>(u) * blockDim.x;
+      if (i < n4) {
+        g[u] = __ldcs(G + i);
+        if (!skip) {
+          p[u] = __ldcs(Pm + i);
+          mm[u] = __ldcs(Mm + i);
+          vv[u] = __ldcs(Vm + i);
+        }
+      }
     }
-    reinterpret_cast<float4*>(master)[i] = make_float4(ps[0], ps[1], ps[2], ps[3]);
-    reinterpret_cast<float4*>(m)[i] = make_float4(ms[0], ms[1], ms[2], ms[3]);
-    reinterpret_cast<float4*>(v)[i] = make_float4(vs[0], vs[1], vs[2], vs[3]);
-    __nv_bfloat162 lo = __floats2bfloat162_rn(ps[0], ps[1]);
-    __nv_bfloat162 hi = __floats2bfloat162_rn(ps[2], ps[3]);
-    uint2 pk;
-    pk.x = *reinterpret_cast<uint32_t*>(&lo);
-    pk.y = *reinterpret_cast<uint32_t*>(&hi);
-    reinterpret_cast<uint2*>(w)[i] = pk;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + static_cast<int64_t>(u) * blockDim.x;
+      if (i >= n4) continue;
+      __stcs(G + i, z);
+      if (skip) continue;
+      float gs[4] = {g[u].x * coef, g[u].y * coef, g[u].z * coef, g[u].w * coef};
+      float ps[4] = {p[u].x, p[u].y, p[u].z, p[u].w};
+      float ms[4] = {mm[u].x, mm[u].y, mm[u].z, mm[u].w};
+      float vs[4] = {vv[u].x, vv[u].y, vv[u].z, vv[u].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        ms[j] = b1 * ms[j] + (1.f - b1) * gs[j];
+        vs[j] = b2 * vs[j] + (1.f - b2) * gs[j] * gs[j];
+        ps[j] -= lr * ((ms[j] * ib1) / (sqrtf(vs[j] * ib2) + eps) + wd * ps[j]);
+      }
+      __stcs(Pm + i, make_float4(ps[0], ps[1], ps[2], ps[3]));
+      __stcs(Mm + i, make_float4(ms[0], ms[1], ms[2], ms[3]));
+      __stcs(Vm + i, make_float4(vs[0], vs[1], vs[2], vs[3]));
+      __nv_bfloat162 lo = __floats2bfloat162_rn(ps[0], ps[1]);
+      __nv_bfloat162 hi = __floats2bfloat162_rn(ps[2], ps[3]);
+      uint2 pk;
+      pk.x = *reinterpret_cast<uint32_t*>(&lo);
+      pk.y = *reinterpret_cast<uint32_t*>(&hi);
+      __stcs(reinterpret_cast<uint2*>(w) + i, pk);
+    }
   }
-  // scalar tail (n % 4)
   if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
     const int64_t k = n4 * 4 + threadIdx.x;
-    const float g = grad[k] * coef;
+    const float gk = grad[k] * coef;
     grad[k] = 0.f;
     if (!skip) {
-      const float mk = b1 * m[k] + (1.f - b1) * g;
-      const float vk = b2 * v[k] + (1.f - b2) * g * g;
+      const float mk = b1 * m[k] + (1.f - b1) * gk;
+      const float vk = b2 * v[k] + (1.f - b2) * gk * gk;
       m[k] = mk;
       v[k] = vk;
       const float nw = master[k] - lr * ((mk * ib1) / (sqrtf(vk * ib2) + eps) + wd * master[k]);
@@ -686,10 +709,13 @@ extern "C" int vp_adam_step(float* master, void* weight_bf16, float* grad, float
        reinterpret_cast<uintptr_t>(exp_avg) | reinterpret_cast<uintptr_t>(exp_avg_sq)) & 15 ||
       reinterpret_cast<uintptr_t>(weight_bf16) & 7)
     return VP_ERR_UNSUPPORTED;
-  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(148 * 16, (n / 4 + 255) / 256 + 1));
-  adam_kernel<<<grid, 256, 0, ST>>>(
-      master, BF(weight_bf16), grad, exp_avg, exp_avg_sq, n, flags, lr, beta1, beta2, eps,
-      weight_decay, inv_loss_scale, max_grad_norm, bias_c1, bias_c2);
+  constexpr int U = 8;
+  const int64_t want = (n / 4 + 256 * U - 1) / (256 * U);
+  const unsigned grid = static_cast<unsigned>(
+      std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(device_sms()) * 8, want)));
+  adam_kernel_u<U><<<grid, 256, 0, ST>>>(master, BF(weight_bf16), grad, exp_avg, exp_avg_sq, n,
+                                         flags, lr, beta1, beta2, eps, weight_decay,
+                                         inv_loss_scale, max_grad_norm, bias_c1, bias_c2);
   return launch_status();
 }
 
