@@ -3,9 +3,26 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+
 #include "vpipe.h"
 
 namespace vp {
+
+// Opt kernel `fn` into `bytes` of dynamic shared memory, once per process
+// per kernel (keyed by the function pointer: a `static bool` inside a generic
+// launch lambda would be shared by every kernel of the same signature).
+inline cudaError_t smem_optin(const void* fn, int bytes) {
+  static std::mutex mu;
+  static const void* done[256];
+  static int nd = 0;
+  std::lock_guard<std::mutex> lock(mu);
+  for (int i = 0; i < nd; ++i)
+    if (done[i] == fn) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess && nd < 256) done[nd++] = fn;
+  return e;
+}
 
 // SM count of the current device (cached per process; B200: 148).
 inline int device_sms() {

@@ -14,6 +14,7 @@
 // across the CTA in shared memory and across CTAs by a fixed-order kernel
 // (deterministic). Wider rows use dx + column-partial kernels.
 #include "common.cuh"
+#include "sm100.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -97,6 +98,9 @@ __global__ void __launch_bounds__(kWarps * 32)
     for (int i = 0; i < NV; ++i) cur[i] = nxt[i];
   }
 }
+
+// Shared-memory row slot of the TMA-staged backward ring (128 B aligned).
+__host__ __device__ constexpr int ring_row_bytes(int cols) { return ((cols * 2 + 127) / 128) * 128; }
 
 // Forward for wide rows: a group of W warps per row (1/W of the vectors
 // each), row sums exchanged through shared memory with a named barrier per
@@ -457,6 +461,185 @@ __global__ void __launch_bounds__(W * G * 32, 1)
   }
 }
 
+// Fused backward, TMA-staged (rows <= 1024 wide): the group kernel's math
+// with every group's x / dy / residual-gradient rows streamed through a ring
+// of R slots in shared memory by 1-D bulk copies issued by the group's first
+// lane, mean/rstd of the next row loaded one row ahead. The register version
+// holds ~1 row per group in flight at 1 CTA/SM (its partials pin ~165
+// registers) and reaches 3.75 TB/s; the ring keeps R rows per group in
+// flight without registers. A slot is refilled right after the group's
+// named barrier, by which point every member has its slice in registers.
+template <int W, int G, int NV, bool SUM, int R>
+__global__ void __launch_bounds__(W * G * 32)
+    ln_bwd_ring_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+                       const __nv_bfloat16* __restrict__ g, const float* __restrict__ mean,
+                       const float* __restrict__ rstd, __nv_bfloat16* __restrict__ dx,
+                       float* __restrict__ ws, int64_t rows, int cols, int accumulate) {
+  extern __shared__ __align__(128) uint8_t ring_smem[];
+  __shared__ float xch[G][2][W][2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pair = warp / W, half = warp % W;
+  const int nvec = cols >> 3, hvec = nvec / W;
+  const int v0 = half * hvec;
+  const int rb = ring_row_bytes(cols);
+  const int nt = accumulate ? 3 : 2;  // x, dy (, dx) per slot
+  const uint32_t bytes = static_cast<uint32_t>(cols) * 2u;
+  float* red = reinterpret_cast<float*>(ring_smem);  // [G][cols], after the loop only
+  uint8_t* ring = ring_smem + static_cast<size_t>(G) * cols * sizeof(float) +
+                  static_cast<size_t>(pair) * R * 3 * rb;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring_smem + static_cast<size_t>(G) * cols * 4 +
+                                               static_cast<size_t>(G) * R * 3 * rb) +
+                   pair * R;
+  const int64_t npairs = static_cast<int64_t>(gridDim.x) * G;
+  const int64_t row0 = static_cast<int64_t>(blockIdx.x) * G + pair;
+  const bool issuer = half == 0 && lane == 0;
+  auto issue = [&](int slot, int64_t row) {
+    uint8_t* d = ring + slot * 3 * rb;
+    mbar_expect_tx(&bars[slot], bytes * nt);
+    bulk_g2s(d, x + row * cols, bytes, &bars[slot]);
+    bulk_g2s(d + rb, dy + row * cols, bytes, &bars[slot]);
+    if (accumulate) bulk_g2s(d + 2 * rb, dx + row * cols, bytes, &bars[slot]);
+  };
+  if (issuer) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) mbar_init(&bars[r], 1);
+    fence_mbar_init();
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (row0 + r * npairs < rows) issue(r, row0 + r * npairs);
+  }
+  // members wait on barriers the issuer initialised
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + pair), "r"(W * 32) : "memory");
+  float gam[NV][8];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = lane + i * 32;
+    if (c < hvec) unpack8(reinterpret_cast<const uint4*>(g)[v0 + c], gam[i]);
+    else
+#pragma unroll
+      for (int j = 0; j < 8; ++j) gam[i][j] = 0.f;
+  }
+  float ag[NV][8], ab[NV][8], as[SUM ? NV : 1][8];
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      ag[i][j] = 0.f;
+      ab[i][j] = 0.f;
+      if constexpr (SUM) as[i][j] = 0.f;
+    }
+  float mu = 0.f, rs = 0.f;
+  if (row0 < rows) {
+    mu = mean[row0];
+    rs = rstd[row0];
+  }
+  int it = 0, parity = 0;
+  for (int64_t row = row0; row < rows; row += npairs, ++it, parity ^= 1) {
+    const int slot = it % R;
+    const int64_t nrow = row + npairs;
+    float mu_n = 0.f, rs_n = 0.f;
+    if (nrow < rows) {
+      mu_n = mean[nrow];
+      rs_n = rstd[nrow];
+    }
+    mbar_wait(&bars[slot], (it / R) & 1);
+    const uint4* sx = reinterpret_cast<const uint4*>(ring + slot * 3 * rb) + v0;
+    const uint4* sd = reinterpret_cast<const uint4*>(ring + slot * 3 * rb + rb) + v0;
+    const uint4* sp = reinterpret_cast<const uint4*>(ring + slot * 3 * rb + 2 * rb) + v0;
+    uint4 pu[NV];
+    float xf[NV][8], df[NV][8];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = lane + i * 32;
+      const bool ok = c < hvec;
+      unpack8(ok ? sx[c] : make_uint4(0u, 0u, 0u, 0u), xf[i]);
+      unpack8(ok ? sd[c] : make_uint4(0u, 0u, 0u, 0u), df[i]);
+      pu[i] = (ok && accumulate) ? sp[c] : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float xh = (xf[i][j] - mu) * rs;
+        const float gy = df[i][j] * gam[i][j];
+        s1 += gy;
+        s2 = fmaf(gy, xh, s2);
+        ag[i][j] = fmaf(df[i][j], xh, ag[i][j]);
+        ab[i][j] += df[i][j];
+      }
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if (lane == 0) {
+      xch[pair][parity][half][0] = s1;
+      xch[pair][parity][half][1] = s2;
+    }
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + pair), "r"(W * 32) : "memory");
+    if (issuer) {
+      const int64_t rrow = row + R * npairs;
+      if (rrow < rows) {
+        fence_async_smem();  // members' generic reads of the slot precede the refill
+        issue(slot, rrow);
+      }
+    }
+    float t1 = 0.f, t2 = 0.f;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      t1 += xch[pair][parity][w][0];
+      t2 += xch[pair][parity][w][1];
+    }
+    const float m1 = t1 / cols, m2 = t2 / cols;
+    uint4* dxr = reinterpret_cast<uint4*>(dx + row * cols) + v0;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = lane + i * 32;
+      if (c < hvec) {
+        float o[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float xh = (xf[i][j] - mu) * rs;
+          o[j] = rs * fmaf(-xh, m2, fmaf(df[i][j], gam[i][j], -m1));
+        }
+        if (accumulate) {
+          float pv[8];
+          unpack8(pu[i], pv);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) o[j] += pv[j];
+        }
+        if constexpr (SUM) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) as[i][j] += o[j];
+        }
+        dxr[c] = pack8(o);
+      }
+    }
+    mu = mu_n;
+    rs = rs_n;
+  }
+  __syncthreads();  // CTA reduction of the partials (red[] sits in front of the ring)
+  constexpr int NQ = SUM ? 3 : 2;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    float* mine = red + pair * cols + v0 * 8;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = lane + i * 32;
+      if (c < hvec) {
+        const float* src = q == 0 ? ag[i] : (q == 1 ? ab[i] : as[SUM ? i : 0]);
+        float4* dst = reinterpret_cast<float4*>(mine + c * 8);
+        dst[0] = make_float4(src[0], src[1], src[2], src[3]);
+        dst[1] = make_float4(src[4], src[5], src[6], src[7]);
+      }
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+      float t = 0.f;
+#pragma unroll
+      for (int w = 0; w < G; ++w) t += red[w * cols + c];
+      ws[(static_cast<int64_t>(blockIdx.x) * 3 + q) * cols + c] = t;
+    }
+    __syncthreads();
+  }
+}
+
 // -------------------------------------------------- split backward (wide)
 // dx only: one warp per row (rows >> SMs here), row in registers.
 template <int NV>
@@ -709,11 +892,7 @@ extern "C" int vp_layernorm_bwd_ex(const void* dy, const void* x, const void* ga
     auto launch = [&](auto kern, int G) {
       parts = static_cast<int>(std::min<int64_t>(device_sms(), (rows + G - 1) / G));
       const size_t smem = static_cast<size_t>(G) * cols * sizeof(float);
-      static bool set = false;
-      if (!set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-        set = true;
-      }
+      smem_optin(reinterpret_cast<const void*>(kern), 96 * 1024);
       kern<<<parts, W * G * 32, smem, st>>>(
           reinterpret_cast<const __nv_bfloat16*>(dy), reinterpret_cast<const __nv_bfloat16*>(x),
           reinterpret_cast<const __nv_bfloat16*>(gamma), mean, rstd,
@@ -723,7 +902,40 @@ extern "C" int vp_layernorm_bwd_ex(const void* dy, const void* x, const void* ga
 #define LN_G(WW, GG, NN)                                                              \
   (dsum ? launch(ln_bwd_group_kernel<WW, GG, NN, true>, GG)                            \
         : launch(ln_bwd_group_kernel<WW, GG, NN, false>, GG))
-    if (W == 2) {
+    static const bool no_ring = getenv("VP_LN_NO_RING") != nullptr;
+    int attr_err = 0;
+    auto launch_ring = [&](auto kern, int WW, int GG, int R) {
+      parts = static_cast<int>(std::min<int64_t>(device_sms(), (rows + GG - 1) / GG));
+      const size_t smem = static_cast<size_t>(GG) * cols * sizeof(float) +
+                          static_cast<size_t>(GG) * R * 3 * ring_row_bytes(cols) +
+                          GG * R * sizeof(uint64_t);
+      attr_err = smem_optin(reinterpret_cast<const void*>(kern), 200 * 1024);
+      if (attr_err) return;
+      kern<<<parts, WW * GG * 32, smem, st>>>(
+          reinterpret_cast<const __nv_bfloat16*>(dy), reinterpret_cast<const __nv_bfloat16*>(x),
+          reinterpret_cast<const __nv_bfloat16*>(gamma), mean, rstd,
+          reinterpret_cast<__nv_bfloat16*>(dx), workspace, rows, static_cast<int>(cols),
+          accumulate);
+    };
+    // TMA-staged ring (R rows per group in flight); smem = G*cols*4 + G*R*3*row bytes
+#define LN_R(WW, GG, NN, RR)                                                               \
+  (dsum ? launch_ring(ln_bwd_ring_kernel<WW, GG, NN, true, RR>, WW, GG, RR)                \
+        : launch_ring(ln_bwd_ring_kernel<WW, GG, NN, false, RR>, WW, GG, RR))
+    if (!no_ring && W == 2) {
+      if (need == 1) LN_R(2, kPairs, 1, 3);
+      else LN_R(2, kPairs, 2, 3);
+      if (attr_err) return attr_err;
+    } else if (!no_ring && W == 4) {
+      if (need == 1) LN_R(4, 3, 1, 3);
+      else if (need == 2) LN_R(4, 3, 2, 3);
+      else LN_R(4, 2, 3, 3);
+      if (attr_err) return attr_err;
+    } else if (!no_ring && W == 8) {
+      if (need == 1) LN_R(8, 1, 1, 4);
+      else if (need == 2) LN_R(8, 1, 2, 4);
+      else LN_R(8, 1, 3, 4);
+      if (attr_err) return attr_err;
+    } else if (W == 2) {
       if (need == 1) LN_G(2, kPairs, 1);
       else LN_G(2, kPairs, 2);
     } else if (W == 4) {
@@ -736,6 +948,7 @@ extern "C" int vp_layernorm_bwd_ex(const void* dy, const void* x, const void* ga
       else LN_G(8, 1, 3);
     }
 #undef LN_G
+#undef LN_R
   } else if (nv <= 4) {
     // one CTA per SM (register-resident partials); 8 rows per warp pass
     parts = row_ctas(rows, 1);

@@ -17,7 +17,7 @@ def rel(a, b):
 
 
 @pytest.mark.parametrize("rows,cols", [(8192, 1024), (4096, 1920), (4096, 3072), (512, 256),
-                                       (33, 64)])
+                                       (33, 64), (1000, 768), (777, 192), (3, 1024), (300, 4096)])
 def test_layernorm(rows, cols):
     torch.manual_seed(0)
     x = (torch.randn(rows, cols, device="cuda") * 2 + 0.5).bfloat16()
