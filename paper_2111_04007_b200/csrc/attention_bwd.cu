@@ -28,6 +28,8 @@
 #include "sm100.cuh"
 #include "tmap.cuh"
 
+#include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 namespace vp {
@@ -91,8 +93,8 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
     attn_bwd_fused(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
                    const __grid_constant__ CUtensorMap tmDQ, const float* __restrict__ lse,
                    const float* __restrict__ delta, __nv_bfloat16* __restrict__ dqkv, int S, int H,
-                   int BH, float scale_log2, float scale, float* __restrict__ dq_acc,
-                   float* __restrict__ kv_part) {
+                   int BH, int bh_chunk, float scale_log2, float scale,
+                   float* __restrict__ dq_acc, float* __restrict__ kv_part) {
   using L = FbSmem;
   constexpr int D = FB_D;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -112,9 +114,19 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
   uint64_t* acc_full = bars + 17;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
 
-  // longest-first order: all CTAs of key block 0 (most query blocks) first
-  const int kb = static_cast<int>(blockIdx.x) / BH;
-  const int bh = static_cast<int>(blockIdx.x) % BH;
+  // CTA order: (batch, head) pairs in chunks of bh_chunk; inside a chunk
+  // longest-first (all key blocks 0 — most query blocks — then 1, ...). The
+  // chunk bounds the set of (b, h) whose Q / dO / dQ-accumulator are live at
+  // once so their re-reads (one per key block) hit L2: with one global
+  // longest-first order every (b, h) is revisited a full wave later and at
+  // B*H = 512 the kernel read 3.8x its algorithmic bytes from DRAM (chunks
+  // of 128: -5% time at B*H = 512, unchanged at 128).
+  const int n_kbt = (S + FB_M - 1) / FB_M;
+  const int chunk = static_cast<int>(blockIdx.x) / (bh_chunk * n_kbt);
+  const int within = static_cast<int>(blockIdx.x) % (bh_chunk * n_kbt);
+  const int csz = min(bh_chunk, BH - chunk * bh_chunk);
+  const int kb = within / csz;
+  const int bh = chunk * bh_chunk + within % csz;
   const int b = bh / H, h = bh % H;
   const int k0 = kb * FB_M;
   const int n_qb = (S + FB_N - 1) / FB_N;
@@ -611,9 +623,11 @@ int fused_t(const void* qkv, const void* o, const void* dout, const float* lse, 
   const float scale_log2 = 1.4426950408889634f * scale;
   const int n_kb = static_cast<int>((S + FB_M - 1) / FB_M);
   const int BH = static_cast<int>(B * H);
+  static const int env_chunk = getenv("VP_ATTN_BH_CHUNK") ? atoi(getenv("VP_ATTN_BH_CHUNK")) : 0;
+  const int bh_chunk = std::max(1, std::min(BH, env_chunk > 0 ? env_chunk : 128));
   k<<<static_cast<unsigned>(n_kb * BH), FB_THREADS, L::TOTAL, st>>>(
       tq, tdo, tdq, lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), static_cast<int>(S),
-      static_cast<int>(H), BH, scale_log2, scale, dq_acc, dbias ? kv_part : nullptr);
+      static_cast<int>(H), BH, bh_chunk, scale_log2, scale, dq_acc, dbias ? kv_part : nullptr);
   if (!dbias) {
     dq_convert_kernel<<<static_cast<unsigned>((tokens * Hd / 8 + 255) / 256), 256, 0, st>>>(
         dq_acc, reinterpret_cast<__nv_bfloat16*>(dqkv), tokens, Hd, scale);
