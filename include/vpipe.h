@@ -100,9 +100,11 @@ int vp_device_sm_count(int* out);
  * Epilogues (VP_EPI_*), `bias` [N] bf16, `aux` [M,N] bf16 (ldaux):
  *   STORE       D = acc                              (bf16)
  *   BIAS        D = acc + bias                       (bf16)
- *   BIAS_GELU   D = gelu(acc + bias), aux <- acc+bias (pre-activation, bf16)
+ *   BIAS_GELU   D = gelu(x), x = bf16(acc + bias); aux (optional) <- gelu'(x)
+ *               (bf16: the saving forward keeps the derivative so the backward
+ *               DGELU epilogue is a single multiply)
  *   BIAS_RESID  D = aux + acc + bias  (residual add; D may alias aux)
- *   DGELU       D = acc * gelu'(aux)                 (bf16)
+ *   DGELU       D = acc * aux, aux = gelu'(x) from BIAS_GELU (bf16)
  *   ACC_F32     Df32 += acc  (fp32 D, ldd in elements; weight-grad accumulate)
  *   STORE_F32   Df32 = acc   (fp32 D)
  * Replaces the F_i/B_i cost terms of sp/calibration.py:219-221. */
@@ -214,6 +216,10 @@ int vp_dropout(void* x, int64_t n, float p, uint64_t seed, uint64_t offset, void
 
 /* Residual add: y = a + b (bf16), n elements. */
 int vp_add(const void* a, const void* b, void* y, int64_t n, void* stream);
+
+/* Elementwise product y = a * b (bf16), n elements: the backward of a GELU
+ * whose saving forward stored gelu'(pre) (VP_EPI_BIAS_GELU with aux). */
+int vp_mul(const void* a, const void* b, void* y, int64_t n, void* stream);
 
 /* Squared-L2 norm and non-finite flag of an fp32 buffer, accumulated into
  * out[0] (sum of squares, fp32) and out[1] (count of non-finite values).

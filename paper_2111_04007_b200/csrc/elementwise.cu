@@ -439,6 +439,22 @@ __global__ void add_kernel(const __nv_bfloat16* __restrict__ a, const __nv_bfloa
   }
 }
 
+__global__ void mul_kernel(const __nv_bfloat16* __restrict__ a, const __nv_bfloat16* __restrict__ b,
+                           __nv_bfloat16* __restrict__ y, int64_t n) {
+  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 8;
+  if (i + 8 <= n) {
+    float fa[8], fb[8];
+    unpack8(*reinterpret_cast<const uint4*>(a + i), fa);
+    unpack8(*reinterpret_cast<const uint4*>(b + i), fb);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) fa[j] *= fb[j];
+    *reinterpret_cast<uint4*>(y + i) = pack8(fa);
+  } else {
+    for (int64_t k = i; k < n; ++k)
+      y[k] = __float2bfloat16(__bfloat162float(a[k]) * __bfloat162float(b[k]));
+  }
+}
+
 // ---------------------------------------------------------- grad norm / Adam
 __global__ void norm_kernel(const float* __restrict__ g, int64_t n, float* __restrict__ out) {
   float ss = 0.f, bad = 0.f;
@@ -688,6 +704,12 @@ extern "C" int vp_dropout(void* x, int64_t n, float p, uint64_t seed, uint64_t o
 extern "C" int vp_add(const void* a, const void* b, void* y, int64_t n, void* stream) {
   if (n <= 0) return VP_ERR_ARGS;
   add_kernel<<<blocks_for(n, 256 * 8), 256, 0, ST>>>(CBF(a), CBF(b), BF(y), n);
+  return launch_status();
+}
+
+extern "C" int vp_mul(const void* a, const void* b, void* y, int64_t n, void* stream) {
+  if (n <= 0) return VP_ERR_ARGS;
+  mul_kernel<<<blocks_for(n, 256 * 8), 256, 0, ST>>>(CBF(a), CBF(b), BF(y), n);
   return launch_status();
 }
 

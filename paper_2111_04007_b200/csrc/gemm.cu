@@ -91,26 +91,28 @@ __device__ __forceinline__ void epilogue_chunk(const EpiArgs& e, int64_t row, in
       }
     }
     if constexpr (EPI == VP_EPI_BIAS_GELU) {
+      // GELU of the bf16-rounded pre-activation; a saving forward stores
+      // gelu'(pre) in aux for the backward's DGELU multiply
+      float dg[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        v[i] = gelu_tanh_and_grad(__bfloat162float(__float2bfloat16(v[i])), dg[i]);
       if (e.aux) {
         __nv_bfloat16* a = e.aux + row * e.ldaux + col0;
         if (full) {
 #pragma unroll
           for (int i = 0; i < 32; i += 8) {
             uint4 o;
-            o.x = pack_bf16(v[i], v[i + 1]);
-            o.y = pack_bf16(v[i + 2], v[i + 3]);
-            o.z = pack_bf16(v[i + 4], v[i + 5]);
-            o.w = pack_bf16(v[i + 6], v[i + 7]);
+            o.x = pack_bf16(dg[i], dg[i + 1]);
+            o.y = pack_bf16(dg[i + 2], dg[i + 3]);
+            o.z = pack_bf16(dg[i + 4], dg[i + 5]);
+            o.w = pack_bf16(dg[i + 6], dg[i + 7]);
             *reinterpret_cast<uint4*>(a + i) = o;
           }
         } else {
-          for (int i = 0; i < 32 && col0 + i < N; ++i) a[i] = __float2bfloat16(v[i]);
+          for (int i = 0; i < 32 && col0 + i < N; ++i) a[i] = __float2bfloat16(dg[i]);
         }
       }
-      // The stored pre-activation is bf16; apply GELU to the rounded value so
-      // the backward (which only sees the bf16 pre-activation) is consistent.
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(__bfloat162float(__float2bfloat16(v[i])));
     }
     if constexpr (EPI == VP_EPI_BIAS_RESID || EPI == VP_EPI_DGELU || EPI == VP_EPI_RESID) {
       const __nv_bfloat16* a = e.aux + row * e.ldaux + col0;
@@ -123,14 +125,14 @@ __device__ __forceinline__ void epilogue_chunk(const EpiArgs& e, int64_t row, in
           for (int j = 0; j < 8; ++j) {
             float x = __bfloat162float(ah[j]);
             if constexpr (EPI == VP_EPI_BIAS_RESID || EPI == VP_EPI_RESID) v[i + j] += x;
-            else v[i + j] *= gelu_tanh_grad(x);
+            else v[i + j] *= x;  // aux = gelu'(pre), stored by the forward
           }
         }
       } else {
         for (int i = 0; i < 32 && col0 + i < N; ++i) {
           float x = __bfloat162float(a[i]);
           if constexpr (EPI == VP_EPI_BIAS_RESID || EPI == VP_EPI_RESID) v[i] += x;
-          else v[i] *= gelu_tanh_grad(x);
+          else v[i] *= x;
         }
       }
     }
@@ -396,17 +398,22 @@ __device__ __forceinline__ void epi2_apply(const Epi2& e, int64_t row, int64_t c
     }
   }
   if constexpr (EPI == VP_EPI_BIAS_GELU) {
+    // GELU of the bf16-rounded pre-activation; the saving forward also keeps
+    // gelu'(pre) (-> aux) so the backward's DGELU epilogue is one multiply
+    if (e.aux_in != nullptr) {
 #pragma unroll
-    for (int i = 0; i < 64; ++i) {
-      pre[i] = __bfloat162float(__float2bfloat16(v[i]));
-      v[i] = gelu_tanh(pre[i]);
+      for (int i = 0; i < 64; ++i)
+        v[i] = gelu_tanh_and_grad(__bfloat162float(__float2bfloat16(v[i])), pre[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 64; ++i) v[i] = gelu_tanh(__bfloat162float(__float2bfloat16(v[i])));
     }
   }
   if constexpr (EPI == VP_EPI_BIAS_RESID || EPI == VP_EPI_DGELU || EPI == VP_EPI_RESID) {
     // aux row values were staged in smem by TMA (see gemm2_kernel)
 #pragma unroll
     for (int i = 0; i < 64; ++i) {
-      if constexpr (EPI == VP_EPI_DGELU) v[i] *= gelu_tanh_grad(xin[i]);
+      if constexpr (EPI == VP_EPI_DGELU) v[i] *= xin[i];  // aux = gelu'(pre)
       else v[i] += xin[i];
     }
   }

@@ -237,6 +237,17 @@ __device__ __forceinline__ float gelu_tanh(float x) {
   const float u = k0 * fmaf(k1 * x, x * x, x);
   return 0.5f * x * (1.f + tanh_fast(u));
 }
+// GELU and its derivative from one tanh (the saving forward stores gelu'(x)
+// for the backward, so the DGELU epilogue is a plain multiply).
+__device__ __forceinline__ float gelu_tanh_and_grad(float x, float& dg) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  const float x2 = x * x;
+  const float u = k0 * x * fmaf(k1, x2, 1.f);
+  const float t = tanh_fast(u);
+  const float hx = 0.5f * x;
+  dg = fmaf(0.5f, t, 0.5f) + hx * fmaf(-t, t, 1.f) * k0 * fmaf(3.f * k1, x2, 1.f);
+  return fmaf(hx, t, hx);
+}
 __device__ __forceinline__ float gelu_tanh_grad(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
   const float u = k0 * fmaf(k1 * x, x * x, x);

@@ -51,6 +51,7 @@ _SIGS = {
     "vp_gelu_bwd": [vp, vp, vp, i64, vp],
     "vp_dropout": [vp, i64, f32, u64, u64, vp],
     "vp_add": [vp, vp, vp, i64, vp],
+    "vp_mul": [vp, vp, vp, i64, vp],
     "vp_grad_norm_sq": [vp, i64, vp, vp],
     "vp_adam_step": [vp, vp, vp, vp, vp, i64, vp, f32, f32, f32, f32, f32, f32, f32, f32, f32, vp],
     "vp_cast_f32_bf16": [vp, vp, i64, vp],
@@ -283,6 +284,12 @@ def dropout_(x, p, seed, offset, stream=None):
 def add(a, b, y, stream=None):
     _count(1)
     check(L.vp_add(a.data_ptr(), b.data_ptr(), y.data_ptr(), a.numel(), _stream(stream)), "vp_add")
+    return y
+
+
+def mul(a, b, y, stream=None):
+    _count(1)
+    check(L.vp_mul(a.data_ptr(), b.data_ptr(), y.data_ptr(), a.numel(), _stream(stream)), "vp_mul")
     return y
 
 

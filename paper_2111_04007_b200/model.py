@@ -325,8 +325,9 @@ class GPT2Stage:
         self._proj_resid(w.o, P.w(p + "w_o"), P.w(p + "b_o"), x, w.x1, dseed, 0, stream)
         K.layernorm_fwd(w.x1, P.w(p + "ln2_g"), P.w(p + "ln2_b"), w.c, w.mean2, w.rstd2,
                         cfg.ln_eps, stream)
-        # the pre-activation is only needed by the backward: a non-saving
-        # forward (F on a recomputing stage) writes the GELU output alone
+        # gelu'(pre-activation) is only needed by the backward (its DGELU
+        # epilogue multiplies by it): a non-saving forward (F on a
+        # recomputing stage) writes the GELU output alone
         K.gemm(w.c, P.w(p + "w_fc1"), w.f, epilogue=K.EPI_BIAS_GELU, bias=P.w(p + "b_fc1"),
                aux=w.pre if w is not self.scratch else None, stream=stream)
         self._proj_resid(w.f, P.w(p + "w_fc2"), P.w(p + "b_fc2"), w.x1, out, dseed, 1, stream)
@@ -493,7 +494,7 @@ class GPT2Stage:
         K.layernorm_bwd(self.dc, self.mlm_act, P.w("lnm_g"), self.lnf_mean, self.lnf_rstd,
                         self.do, P.g("lnm_g"), P.g("lnm_b"), self.ln_ws, accumulate=False,
                         stream=stream)
-        K.gelu_bwd(self.do, self.mlm_pre, self.dc, stream)
+        K.mul(self.do, self.mlm_pre, self.dc, stream)  # mlm_pre holds gelu'(pre)
         K.gemm(self.dc, P.w("w_mlm"), self.g, b_kmajor=False, stream=stream)
         K.gemm(self.dc, x, P.g("w_mlm"), a_kmajor=False, b_kmajor=False,
                epilogue=K.EPI_ACC_F32, stream=stream)

@@ -57,7 +57,9 @@ def test_gemm_epilogues():
     assert rel(out, base + bias.float()) < 5e-3
     pre = torch.empty_like(out)
     K.gemm(A, B, out, epilogue=K.EPI_BIAS_GELU, bias=bias, aux=pre)
-    assert rel(pre, base + bias.float()) < 5e-3
+    # the saving forward stores gelu'(pre-activation) for the DGELU multiply
+    xpre = (base + bias.float()).bfloat16().float()
+    assert rel(pre, dgelu(xpre)) < 1e-2
     assert rel(out, gelu(base + bias.float())) < 1e-2
     out_only = torch.empty_like(out)  # no pre-activation output (non-saving forward)
     K.gemm(A, B, out_only, epilogue=K.EPI_BIAS_GELU, bias=bias)
@@ -67,8 +69,12 @@ def test_gemm_epilogues():
     K.gemm(A, B, out2, epilogue=K.EPI_BIAS_RESID, bias=bias, aux=out2)
     assert rel(out2, res.float() + base + bias.float()) < 5e-3
     x = torch.randn(M, N, device="cuda").bfloat16()
-    K.gemm(A, B, out, epilogue=K.EPI_DGELU, aux=x)
-    assert rel(out, base * dgelu(x.float())) < 1e-2
+    K.gemm(A, B, out, epilogue=K.EPI_DGELU, aux=x)   # aux = gelu'(pre) from the forward
+    assert rel(out, base * x.float()) < 5e-3
+    # end to end: forward-saved derivative -> DGELU == acc * gelu'(pre)
+    K.gemm(A, B, out, epilogue=K.EPI_BIAS_GELU, bias=bias, aux=pre)
+    K.gemm(A, B, out_only, epilogue=K.EPI_DGELU, aux=pre)
+    assert rel(out_only, base * dgelu(xpre)) < 1e-2
     acc = torch.randn(M, N, device="cuda")
     acc0 = acc.clone()
     K.gemm(A, B, acc, epilogue=K.EPI_ACC_F32)
@@ -103,6 +109,15 @@ def test_gemm_paths_agree(direct):
     out = res.clone()
     K.gemm(A, B, out, epilogue=K.EPI_BIAS_RESID, bias=bias, aux=out, direct=direct)
     assert rel(out, res.float() + base + bias.float()) < 5e-3
+    act = torch.empty_like(res)
+    der = torch.empty_like(res)
+    K.gemm(A, B, act, epilogue=K.EPI_BIAS_GELU, bias=bias, aux=der, direct=direct)
+    xpre = (base + bias.float()).bfloat16().float()
+    assert rel(act, gelu(xpre)) < 1e-2
+    assert rel(der, dgelu(xpre)) < 1e-2
+    dg = torch.empty_like(res)
+    K.gemm(A, B, dg, epilogue=K.EPI_DGELU, aux=der, direct=direct)
+    assert rel(dg, base * dgelu(xpre)) < 1e-2
 
 
 @pytest.mark.parametrize("T,N,Kd", [(8192, 1024, 1024), (8192, 3072, 1024), (4096, 1920, 7680),
@@ -143,7 +158,7 @@ def test_gemm_fused_bias_grad(M, N):
     ws = torch.empty(K.gemm_dbias_ws_elems(M, N), device="cuda")
     db = torch.ones(N, device="cuda")
     K.gemm(A, B, out, b_kmajor=False, epilogue=K.EPI_DGELU, aux=x, dbias=db, dbias_ws=ws)
-    ref = (A.float() @ B.float()) * dgelu(x.float())
+    ref = (A.float() @ B.float()) * x.float()   # aux = gelu'(pre)
     assert rel(out, ref) < 1e-2
     assert rel(db, 1 + ref.sum(0)) < 1e-3
     db2 = torch.ones(N, device="cuda")
@@ -169,4 +184,4 @@ def test_gemm_aux_epilogue_ragged_n_many_tiles():
         x = torch.randn(M, N, device="cuda").bfloat16()
         out2 = torch.empty_like(x)
         K.gemm(A, B, out2, epilogue=K.EPI_DGELU, aux=x)
-        assert rel(out2, (A.float() @ B.float().t()) * dgelu(x.float())) < 1e-2
+        assert rel(out2, (A.float() @ B.float().t()) * x.float()) < 1e-2
