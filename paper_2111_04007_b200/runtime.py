@@ -256,6 +256,85 @@ class _Links:
               "vp_stream_wait_event")
 
 
+def group_ranks(P: int, D: int) -> Dict[str, List[List[int]]]:
+    """Process groups of a P x D job under the reference placement
+    rank = r*P + s (sp/simulator.py:71-76): ``dp[s]`` the D replicas of stage
+    s (C1), ``pipe[r]`` the P stages of replica r (C2), ``tie[r]`` the first
+    and last stage of replica r (C3, tied embedding; P > 1 only)."""
+    return {"dp": [[r * P + s for r in range(D)] for s in range(P)],
+            "pipe": [[r * P + s for s in range(P)] for r in range(D)],
+            "tie": [[r * P, r * P + P - 1] for r in range(D)] if P > 1 else []}
+
+
+def stage_means(timeline: dict):
+    """Mean F, B, R duration (us) of one stage's traced step (0 if absent)."""
+    by = {KIND_FORWARD: [], KIND_BACKWARD: [], KIND_RECOMPUTE: []}
+    for kind, _, a, b in timeline["tasks"]:
+        by[kind].append(b - a)
+    return tuple(sum(v) / len(v) if v else 0.0
+                 for v in (by[KIND_FORWARD], by[KIND_BACKWARD], by[KIND_RECOMPUTE]))
+
+
+def exchange_stage_means(means, rank: int, world: int, device="cpu", group=None) -> torch.Tensor:
+    """[world, 3] table of every rank's (F, B, R) means (one all-reduce)."""
+    sums = torch.zeros(world, 3, dtype=torch.float64, device=device)
+    sums[rank] = torch.tensor(means, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(sums, group=group)
+    return sums
+
+
+def retune_order(schedule: Schedule, P: int, D: int, m: int, N: int, hidden: int, seq_len: int,
+                 table: torch.Tensor, current) -> list:
+    """Pick the per-stage dispatch order with the shortest simulated
+    mini-batch under the measured stage times (replica 0's rows of
+    ``table``): candidates are the static Varuna order, the order in use
+    (``current``, one task list per stage) and the opportunistic replica
+    kernel's orders under the measured times with backward and recompute
+    scaled x0.85..1.15 (the kernel is a heuristic). Deterministic: every
+    rank given the same table and current orders returns the same order."""
+    from .calibration import CalibrationProfile, CutpointTimes
+    from .core import make_block_model, uniform_cluster
+    from .simulator import build_placement, execution_order, simulate_minibatch
+    f = [max(1.0, float(table[s, 0])) for s in range(P)]     # replica 0: ranks 0..P-1
+    bw = [max(1.0, float(table[s, 1])) for s in range(P)]
+    rr = [float(table[s, 2]) / f[s] for s in range(P) if table[s, 2] > 0]
+    rscale = sum(rr) / len(rr) if rr else 1.0
+    z = {m: 0}
+    d_grid = tuple(sorted({1, D}))
+
+    def profile(fb):
+        c = tuple(CutpointTimes({m: round(f[s])}, {m: max(1, round(bw[s] * fb))}, z, z, z, z, z,
+                                z, {d: 0 for d in d_grid}) for s in range(P))
+        return CalibrationProfile((m,), d_grid, c)
+    prof = profile(1.0)
+    pc = ParallelConfig(P, D, m, N, tuple(range(P)))
+    model = make_block_model("stages", P, hidden, seq_len)
+    cands = [[list(zip(*[a.tolist() for a in schedule.stage_slice(k)])) for k in range(P)],
+             [list(t) for t in current]]
+    for fb in (1.0, 0.85, 1.15):
+        for rs in (1.0, 0.85, 1.15):
+            o = execution_order(schedule, pc, profile(fb), model, opportunistic=True,
+                                recompute_scale=rscale * rs)
+            if o not in cands:
+                cands.append(o)
+    place = build_placement(uniform_cluster(P * D, max(P * D, 1)), P, D)
+    best, best_t = None, None
+    for order in cands:
+        kinds, mbs, offs = [], [], [0]
+        for k in range(P):
+            kinds += [a for a, _ in order[k]]
+            mbs += [j for _, j in order[k]]
+            offs.append(len(kinds))
+        sch = Schedule("candidate", P, N, np.array(kinds, np.int64), np.array(mbs, np.int64),
+                       np.array(offs, np.int64), 1, 2, 1)
+        t = simulate_minibatch(sch, pc, prof, place, model, opportunistic=False,
+                               recompute_scale=rscale).minibatch_us
+        if best_t is None or t < best_t:
+            best, best_t = order, t
+    return best
+
+
 class Varuna:
     """Pipeline-parallel training of a GPT-2 described by ``model`` under the
     ``config`` (P, D, m, N_m, stage_map) chosen by the reference planner."""
@@ -345,71 +424,14 @@ class Varuna:
         (``step(trace=True)`` timeline), and the replica kernel re-runs the
         schedule over one cut-point per stage with those times. Collective
         over the pipeline ranks; all ranks compute the same orders."""
-        from .calibration import CalibrationProfile, CutpointTimes
-        from .core import make_block_model
-        from .simulator import execution_order
-        P = self.P
-        sums = torch.zeros(self.world, 3, dtype=torch.float64, device=self.device)
-        by = {F: [], B: [], R: []}
-        for kind, _, a, b in timeline["tasks"]:
-            by[kind].append(b - a)
-        for kind, col in ((F, 0), (B, 1), (R, 2)):
-            if by[kind]:
-                sums[self.rank, col] = sum(by[kind]) / len(by[kind])
-        if self.world > 1:
-            dist.all_reduce(sums)
-        f = [max(1.0, float(sums[s, 0])) for s in range(P)]     # replica 0: ranks 0..P-1
-        bw = [max(1.0, float(sums[s, 1])) for s in range(P)]
-        rr = [float(sums[s, 2]) / f[s] for s in range(P) if sums[s, 2] > 0]
-        rscale = sum(rr) / len(rr) if rr else 1.0
-        m = self.m
-        z = {m: 0}
-        cps = tuple(CutpointTimes({m: round(f[s])}, {m: round(bw[s])}, z, z, z, z, z, z,
-                                  {d: 0 for d in sorted({1, self.D})}) for s in range(P))
-        prof = CalibrationProfile((m,), tuple(sorted({1, self.D})), cps)
-        pc = ParallelConfig(P, self.D, m, self.N, tuple(range(P)))
-        model = make_block_model("stages", P, self.cfg.hidden, self.cfg.seq_len)
-        # candidates: the opportunistic order under the measured times, the
-        # static Varuna order and the order in use; each is replayed
-        # statically by the simulator with the measured times and the
-        # shortest predicted mini-batch wins (all ranks agree: same inputs)
-        import numpy as np
-        from .simulator import build_placement, simulate_minibatch
-        from .core import uniform_cluster
+        table = exchange_stage_means(stage_means(timeline), self.rank, self.world, self.device)
         current = [None] * self.world
         if self.world > 1:
             dist.all_gather_object(current, self.tasks)
         else:
             current = [self.tasks]
-        # the opportunistic kernel is a heuristic: also run it on perturbed
-        # copies of the measured times (backward and recompute x0.85..1.15)
-        # and keep every distinct order as a candidate
-        def scaled(fb):
-            c2 = tuple(CutpointTimes({m: round(f[s])}, {m: max(1, round(bw[s] * fb))}, z, z, z, z,
-                                     z, z, {d: 0 for d in sorted({1, self.D})}) for s in range(P))
-            return CalibrationProfile((m,), tuple(sorted({1, self.D})), c2)
-        cands = [[list(zip(*[a.tolist() for a in self.schedule.stage_slice(k)]))
-                  for k in range(P)], current[:P]]
-        for fb in (1.0, 0.85, 1.15):
-            for rs in (1.0, 0.85, 1.15):
-                o = execution_order(self.schedule, pc, scaled(fb), model, opportunistic=True,
-                                    recompute_scale=rscale * rs)
-                if o not in cands:
-                    cands.append(o)
-        place = build_placement(uniform_cluster(P * self.D, max(P * self.D, 1)), P, self.D)
-        best, best_t = None, None
-        for order in cands:
-            kinds, mbs, offs = [], [], [0]
-            for k in range(P):
-                kinds += [a for a, _ in order[k]]
-                mbs += [j for _, j in order[k]]
-                offs.append(len(kinds))
-            sch = Schedule("candidate", P, self.N, np.array(kinds, np.int64),
-                           np.array(mbs, np.int64), np.array(offs, np.int64), 1, 2, 1)
-            t = simulate_minibatch(sch, pc, prof, place, model, opportunistic=False,
-                                   recompute_scale=rscale).minibatch_us
-            if best_t is None or t < best_t:
-                best, best_t = order, t
+        best = retune_order(self.schedule, self.P, self.D, self.m, self.N, self.cfg.hidden,
+                            self.cfg.seq_len, table, current[:self.P])
         self.tasks = best[self.stage_id]
         self.dispatch = "opportunistic"
         self._check_plan()
@@ -433,19 +455,19 @@ class Varuna:
         self.shm = None
         if self.world == 1:
             return
-        for s in range(P):
-            g = dist.new_group([r * P + s for r in range(D)])
+        gr = group_ranks(P, D)
+        for s, ranks in enumerate(gr["dp"]):
+            g = dist.new_group(ranks)
             if s == self.stage_id:
                 self.dp_group = g
-        for r in range(D):
-            g = dist.new_group([r * P + s for s in range(P)])
+        for r, ranks in enumerate(gr["pipe"]):
+            g = dist.new_group(ranks)
             if r == self.replica:
                 self.pipe_group = g
-        if P > 1:
-            for r in range(D):
-                g = dist.new_group([r * P, r * P + P - 1])
-                if r == self.replica and (self.spec.first or self.spec.last):
-                    self.tie_group = g
+        for r, ranks in enumerate(gr["tie"]):
+            g = dist.new_group(ranks)
+            if r == self.replica and (self.spec.first or self.spec.last):
+                self.tie_group = g
         self.gloo = dist.new_group(list(range(self.world)), backend="gloo")
         tag = os.environ.get("MASTER_PORT", "0")
         name = f"vpipe_{tag}_{os.getuid()}"
