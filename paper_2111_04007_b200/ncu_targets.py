@@ -2,7 +2,7 @@
 cudaProfilerStart/Stop for
 
     ncu --profile-from-start off --set full --clock-control none --import-source on \\
-        -o profiles/r01d_kernels_355m_m32 python paper_2111_04007_b200/ncu_targets.py
+        -o profiles/r01e_kernels_355m_m32 python paper_2111_04007_b200/ncu_targets.py
 """
 import os
 import sys
