@@ -26,7 +26,7 @@ VP_ERR_NOTIMPL = -7
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
-            f"libvpipe.so not built at {LIB_PATH}; run `python -m paper_2111_04007_b200.build` "
+            f"libvpipe.so not built at {LIB_PATH}; run `python __graft_entry__.py` (or `python paper_2111_04007_b200/build.py`) "
             "(there is no fallback implementation)")
     return ctypes.CDLL(LIB_PATH)
 

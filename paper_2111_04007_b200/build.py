@@ -1,6 +1,7 @@
 """Build libvpipe.so in-tree: every CUDA source for sm_100a + the C++ control
-plane. Invoked by ``__graft_entry__.build()`` and by ``python -m
-paper_2111_04007_b200.build``. Incremental by mtime (objects under
+plane. Invoked by ``__graft_entry__.build()`` and by ``python
+paper_2111_04007_b200/build.py`` (loaded by path: the package itself needs the
+built library to import). Incremental by mtime (objects under
 ``paper_2111_04007_b200/_build/``)."""
 
 from __future__ import annotations
