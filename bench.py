@@ -242,6 +242,24 @@ def cpu_layer_sample(cfg, m, budget_s, recompute=False):
     return mm / per_mb, threads, sample, time.perf_counter() - t0
 
 
+def workload_shape(args, cfg, world):
+    """(M_total, P, D, m, how m was chosen) — shared by both arms so the
+    reference arm times the same workload as the vpipe arm."""
+    M, m = MODEL_CONFIGS[args.config]
+    if args.pd:
+        P, D = map(int, args.pd.lower().split("x"))
+    else:
+        P, D = LADDER.get(world, (world, 1))
+    m_how = "config default"
+    if args.m == "auto":
+        m_sel = choose_micro_batch(cfg, P, D, M, args.config)
+        if m_sel is not None:
+            m, m_how = m_sel, "planner: fastest simulated mini-batch over the calibration m grid"
+    elif args.m:
+        m, m_how = int(args.m), "command line"
+    return M, P, D, m, m_how
+
+
 def run_reference(args):
     """--impl reference: the reference CPU path of this hot path (the fp32
     oracle port — the reference itself has no tensor math) on the host cores."""
@@ -250,8 +268,7 @@ def run_reference(args):
     if rank != 0:
         return 0
     cfg = CONFIGS[args.config]
-    M, m = MODEL_CONFIGS[args.config]
-    P, D = LADDER.get(args.gpus, (args.gpus, 1))
+    M, P, D, m, _ = workload_shape(args, cfg, args.gpus)
     vals = []
     for i in range(args.warmup + args.steps):
         v, threads, sample, _ = cpu_layer_sample(cfg, m, budget_s=min(args.cpu_sample_s, 8.0),
@@ -299,18 +316,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     cfg = CONFIGS[args.config]
-    M, m = MODEL_CONFIGS[args.config]
-    if args.pd:
-        P, D = map(int, args.pd.lower().split("x"))
-    else:
-        P, D = LADDER.get(world, (world, 1))
-    m_how = "config default"
-    if args.m == "auto":
-        m_sel = choose_micro_batch(cfg, P, D, M, args.config)
-        if m_sel is not None:
-            m, m_how = m_sel, "planner: fastest simulated mini-batch over the calibration m grid"
-    elif args.m:
-        m, m_how = int(args.m), "command line"
+    M, P, D, m, m_how = workload_shape(args, cfg, world)
     N = micro_batches_for(JobSpec(M), m, D)
     stage_map = stage_map_for(cfg, P, m, args.config)
     pc = ParallelConfig(P, D, m, N, stage_map)
