@@ -206,7 +206,8 @@ int vp_xent_fwd_bwd(void* logits, const int64_t* labels, float* loss_rows, float
 
 /* Column sum of dy[rows, cols] (bf16) accumulated into dbias (fp32), one
  * launch, deterministic. workspace: vp_bias_grad_ws_elems(cols) floats,
- * zero-filled before its first use (arrival counters; left at zero). */
+ * zero-filled before its first use (arrival counters; left at zero). A
+ * workspace sized for C columns may be reused by calls with any cols <= C. */
 int64_t vp_bias_grad_ws_elems(int64_t cols);
 int vp_bias_grad(const void* dy, float* dbias, int64_t rows, int64_t cols, float* workspace,
                  void* stream);

@@ -669,10 +669,15 @@ extern "C" int vp_xent_fwd_bwd(void* logits, const int64_t* labels, float* loss_
 }
 
 // workspace: vp_bias_grad_ws_elems(cols) floats, zero-filled before first use
-// (the arrival counters live at its end and are left at zero).
+// (the arrival counters are left at zero by each call).
+// Layout: arrival counters first at a FIXED offset (one per 256-column block,
+// up to kColsumCounters), partials after them. A workspace sized for C columns
+// is then reusable for any cols <= C: a narrower call's partials never land on
+// a wider call's counters (with counters after the partials they did).
 static constexpr int64_t kColsumMaxParts = 128;
+static constexpr int64_t kColsumCounters = 4096;
 extern "C" int64_t vp_bias_grad_ws_elems(int64_t cols) {
-  return kColsumMaxParts * cols + (cols + 255) / 256 + 64;
+  return kColsumCounters + kColsumMaxParts * cols;
 }
 
 extern "C" int vp_bias_grad(const void* dy, float* dbias, int64_t rows, int64_t cols,
@@ -680,16 +685,17 @@ extern "C" int vp_bias_grad(const void* dy, float* dbias, int64_t rows, int64_t 
   if (rows <= 0 || cols <= 0 || !workspace) return VP_ERR_ARGS;
   if (cols % 8) return VP_ERR_UNSUPPORTED;
   const int64_t col_blocks = (cols + 255) / 256;
+  if (col_blocks > kColsumCounters) return VP_ERR_UNSUPPORTED;
   // ~4 CTAs per SM, >= 32 rows per part, <= kColsumMaxParts parts
   int64_t parts = (4 * static_cast<int64_t>(device_sms()) + col_blocks - 1) / col_blocks;
   parts = std::min<int64_t>(parts, std::max<int64_t>(1, rows / 32));
   parts = std::max<int64_t>(1, std::min<int64_t>(parts, kColsumMaxParts));
   const int64_t rpp = (rows + parts - 1) / parts;
   parts = (rows + rpp - 1) / rpp;
-  unsigned* counters = reinterpret_cast<unsigned*>(workspace + kColsumMaxParts * cols);
+  unsigned* counters = reinterpret_cast<unsigned*>(workspace);
   dim3 grid(static_cast<unsigned>(col_blocks), static_cast<unsigned>(parts));
-  colsum_kernel<<<grid, 256, 0, ST>>>(CBF(dy), workspace, counters, dbias, rows, cols, rpp,
-                                      static_cast<int>(parts));
+  colsum_kernel<<<grid, 256, 0, ST>>>(CBF(dy), workspace + kColsumCounters, counters, dbias,
+                                      rows, cols, rpp, static_cast<int>(parts));
   return launch_status();
 }
 

@@ -187,6 +187,15 @@ def test_bias_grad_and_misc():
         K.bias_grad(x, o2, w)
         assert torch.equal(o1, o2)
         assert rel(o1, x.float().sum(0)) < 1e-5
+    # one workspace shared by calls of different widths (the BERT last stage:
+    # MLM-head vocab, 4h and h columns from the same buffer)
+    w = torch.zeros(K.bias_grad_ws_elems(30528), device="cuda")
+    for rows, cols in ((1024, 30528), (1024, 1024), (1024, 4096), (1024, 1024), (300, 30528),
+                       (2048, 1024)):
+        x = torch.randn(rows, cols, device="cuda").bfloat16()
+        o = torch.zeros(cols, device="cuda")
+        K.bias_grad(x, o, w)
+        assert rel(o, x.float().sum(0)) < 1e-5, (rows, cols)
     a = torch.randn(1000, 24, device="cuda").bfloat16()
     b = torch.randn(1000, 24, device="cuda").bfloat16()
     y = torch.empty_like(a)

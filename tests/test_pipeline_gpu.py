@@ -230,10 +230,11 @@ def test_graph_replay_matches_eager():
         assert abs(a - b) <= 1e-4 * abs(a)
 
 
-@pytest.mark.parametrize("name,n_layer,m,N", [("gpt2_355m", 2, 1, 2), ("gpt2_8_3b", 1, 1, 1)])
+@pytest.mark.parametrize("name,n_layer,m,N", [("gpt2_355m", 2, 1, 2), ("gpt2_2_5b", 1, 1, 1),
+                                                 ("gpt2_8_3b", 1, 1, 1)])
 def test_full_width_layers_match_oracle(name, n_layer, m, N):
-    """The BASELINE model widths (355M: h=1024, 16 heads; 8.3B: h=3072, 32
-    heads; s=1024, V=51200) with the layer count cut to what the fp32 CPU
+    """The BASELINE model widths (355M: h=1024, 16 heads; 2.5B: h=1920, 20
+    heads of 96; 8.3B: h=3072, 32 heads; s=1024, V=51200) with the layer count cut to what the fp32 CPU
     oracle runs in ~10 s: loss and every gradient under the tolerances of
     the module docstring, so the full-size GEMM/attention/LN tilings run
     in-model, not just the tiny ones."""
@@ -248,6 +249,31 @@ def test_full_width_layers_match_oracle(name, n_layer, m, N):
     res = v.step(batch, apply=False)
     torch.cuda.synchronize()
     o, loss = oracle_run(cfg, pc, batch)
+    assert abs(res.loss - loss) / abs(loss) < 5e-3, (res.loss, loss)
+    og = o.grads()
+    for pname, g in v.param_tensors("grad").items():
+        assert rel(g, og[pname]) < 3e-2, (pname, rel(g, og[pname]))
+
+
+def test_bert_large_width_layer_matches_oracle():
+    """BERT-large width (h=1024, 16 heads, s=512, V=30528, post-LN, MLM head)
+    with one layer, two micro-batches of 2, against the fp32 oracle."""
+    import dataclasses
+    from paper_2111_04007_b200 import ParallelConfig
+    from paper_2111_04007_b200.model import CONFIGS
+    from paper_2111_04007_b200.runtime import Varuna, synthetic_batch
+    from oracle.gpt2_fp32 import PipelineOracle
+    cfg = dataclasses.replace(CONFIGS["bert_large"], n_layer=1)
+    m, N = 2, 2
+    pc = ParallelConfig(1, 1, m, N, (0,))
+    batch = synthetic_batch(cfg, m * N, 0)
+    v = Varuna(cfg, pc, seed=0)
+    res = v.step(batch, apply=False)
+    torch.cuda.synchronize()
+    o = PipelineOracle(cfg.n_layer, cfg.hidden, cfg.heads, cfg.vocab_size, cfg.seq_len,
+                       pc.stage_map, m, N, seed=0, arch="bert")
+    loss = o.run_minibatch(batch["input_ids"], batch["labels"], m * N * cfg.mlm_per_seq,
+                           types=batch["token_type_ids"])
     assert abs(res.loss - loss) / abs(loss) < 5e-3, (res.loss, loss)
     og = o.grads()
     for pname, g in v.param_tensors("grad").items():
