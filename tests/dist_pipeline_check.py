@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--N", type=int, default=4)
     ap.add_argument("--config", default="tiny")
     ap.add_argument("--dispatch", default="static")
+    ap.add_argument("--layers", type=int, default=0, help="cut the config to this many layers")
+    ap.add_argument("--m", type=int, default=4)
     args = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
@@ -38,7 +40,10 @@ def main():
     from paper_2111_04007_b200.runtime import Varuna, synthetic_batch
     from oracle.gpt2_fp32 import PipelineOracle
     cfg = CONFIGS[args.config]
-    P, D, N, m = args.P, args.D, args.N, 4
+    if args.layers:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, n_layer=args.layers)
+    P, D, N, m = args.P, args.D, args.N, args.m
     model = make_block_model("tiny", cfg.n_layer, cfg.hidden, cfg.seq_len)
     a = assign_stages(model, P, m, uniform_profile(cfg.n_layer, 1.0, 2.0, m_grid=(m,)))
     pc = ParallelConfig(P, D, m, N, a.stage_map)

@@ -278,3 +278,22 @@ def test_bert_large_width_layer_matches_oracle():
     og = o.grads()
     for pname, g in v.param_tensors("grad").items():
         assert rel(g, og[pname]) < 3e-2, (pname, rel(g, og[pname]))
+
+
+@pytest.mark.multigpu
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 4,
+                    reason="needs 4 GPUs")
+@pytest.mark.parametrize("P,D,config,nproc", [(2, 1, "gpt2_355m", 2), (2, 2, "bert_large", 4)])
+def test_full_width_pipeline_matches_oracle(P, D, config, nproc):
+    """Two-layer cuts of the BASELINE widths through the real pipeline: the
+    boundary activations/gradients (m*s*h*2 bytes) cross GPUs over the P2P
+    path and replicas all-reduce, against the fp32 oracle."""
+    env = dict(os.environ, PYTHONPATH=ROOT)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1",
+           f"--master-port={29561 + nproc}",
+           os.path.join(ROOT, "tests", "dist_pipeline_check.py"), "--P", str(P), "--D", str(D),
+           "--config", config, "--layers", "2", "--m", "1", "--N", "2"]
+    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-4000:]
+    assert "PARITY OK" in p.stdout
