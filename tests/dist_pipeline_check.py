@@ -30,7 +30,7 @@ def main():
     ap.add_argument("--config", default="tiny")
     ap.add_argument("--dispatch", default="static")
     ap.add_argument("--layers", type=int, default=0, help="cut the config to this many layers")
-    ap.add_argument("--m", type=int, default=4)
+    ap.add_argument("--micro-batch", type=int, default=4)
     args = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
@@ -43,7 +43,7 @@ def main():
     if args.layers:
         import dataclasses
         cfg = dataclasses.replace(cfg, n_layer=args.layers)
-    P, D, N, m = args.P, args.D, args.N, args.m
+    P, D, N, m = args.P, args.D, args.N, args.micro_batch
     model = make_block_model("tiny", cfg.n_layer, cfg.hidden, cfg.seq_len)
     a = assign_stages(model, P, m, uniform_profile(cfg.n_layer, 1.0, 2.0, m_grid=(m,)))
     pc = ParallelConfig(P, D, m, N, a.stage_map)

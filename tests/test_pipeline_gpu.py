@@ -293,7 +293,7 @@ def test_full_width_pipeline_matches_oracle(P, D, config, nproc):
            f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1",
            f"--master-port={29561 + nproc}",
            os.path.join(ROOT, "tests", "dist_pipeline_check.py"), "--P", str(P), "--D", str(D),
-           "--config", config, "--layers", "2", "--m", "1", "--N", "2"]
+           "--config", config, "--layers", "2", "--micro-batch", "1", "--N", "2"]
     p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
     assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-4000:]
     assert "PARITY OK" in p.stdout
