@@ -1,5 +1,6 @@
 """End-to-end parity of the Varuna executor (GPU, bf16 kernels) against the
-fp32 CPU oracle (oracle/gpt2_fp32.py) on the tiny GPT-2 config.
+fp32 CPU oracle (oracle/gpt2_fp32.py) on the tiny GPT-2/BERT configs and on
+layer-count cuts of the BASELINE widths (355M, 2.5B, 8.3B, BERT-large).
 
 Tolerances (stated here): loss |Δ|/|loss| <= 5e-3;
 per-tensor gradient relative L2 <= 3e-2; weights after one AdamW step
