@@ -197,102 +197,239 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- CPU arm
+# Everything in this section runs WITHOUT importing the product package
+# (paper_2111_04007_b200 / libvpipe.so): the reference arm times the
+# reference's own control plane (spotpipe from baseline/_ref) and the fp32
+# CPU port of the executor's tensor path (oracle/gpt2_fp32.py — the reference
+# has no tensor math), on a plan read from the committed
+# profiles/plans.json.
 
-def cpu_layer_sample(cfg, m, budget_s, recompute=False):
-    """The fp32 CPU oracle (oracle/gpt2_fp32.py) timed on this host: one
-    transformer layer's F + R + B at the config's (m, s, h), plus the LM head
-    F + B, extrapolated by layer count and schedule to samples/s."""
-    import torch
-    from oracle import gpt2_fp32 as og
-    threads = os.cpu_count() or 1
-    torch.set_num_threads(threads)
-    h, S, H, V = cfg.hidden, cfg.seq_len, cfg.heads, cfg.vocab_size
-    p = og.init_params(1, h, 8, S)   # layer 0 weights (tiny vocab; head timed separately)
-    for k in p:
-        p[k].requires_grad_(True)
-    mm = m
-    x = torch.randn(mm * S, h, requires_grad=True)
-    t0 = time.perf_counter()
-    y = og.layer_forward(p, 0, x, mm, S, H)
-    y.backward(torch.ones_like(y))
-    t_layer_fb = time.perf_counter() - t0
-    reps = 1
-    while time.perf_counter() - t0 < budget_s * 0.6 and reps < 3:
-        t1 = time.perf_counter()
-        if recompute:
-            with torch.no_grad():
-                og.layer_forward(p, 0, x, mm, S, H)
-        y = og.layer_forward(p, 0, x, mm, S, H)
-        y.backward(torch.ones_like(y))
-        t_layer_fb = time.perf_counter() - t1  # [F(no-save) +] F/R + B, steady state
-        reps += 1
-    # LM head on a slice of rows (bounded), scaled to m*S rows
-    rows = min(mm * S, 1024)
-    w = torch.randn(V, h) * 0.02
-    w.requires_grad_(True)
-    yy = torch.randn(rows, h, requires_grad=True)
-    lab = torch.randint(0, V, (rows,))
-    t2 = time.perf_counter()
-    l = torch.nn.functional.cross_entropy(yy @ w.t(), lab)
-    l.backward()
-    t_head = (time.perf_counter() - t2) * (mm * S / rows)
-    per_mb = cfg.n_layer * t_layer_fb + t_head
-    sample = (f"1 layer F{'+R' if recompute else ''}+B at m={mm}, s={S}, h={h} and LM head F+B on {rows} rows "
-              f"(fp32 torch-CPU oracle), extrapolated x{cfg.n_layer} layers")
-    return mm / per_mb, threads, sample, time.perf_counter() - t0
+# (n_layer, hidden, heads, vocab, seq, arch, mlm_per_seq) — the BASELINE
+# model shapes, restated here so the CPU arm does not import the product
+MODEL_DIMS = {
+    "tiny": (4, 256, 4, 50304, 128, "gpt2", 0),
+    "gpt2_355m": (24, 1024, 16, 51200, 1024, "gpt2", 0),
+    "gpt2_2_5b": (54, 1920, 20, 51200, 1024, "gpt2", 0),
+    "gpt2_8_3b": (72, 3072, 32, 51200, 1024, "gpt2", 0),
+    "bert_large": (24, 1024, 16, 30528, 512, "bert", 77),
+}
+# north-star P x D of each BASELINE config (BASELINE.json "configs")
+NORTH_STAR_PD = {"tiny": (2, 1), "gpt2_355m": (4, 2), "bert_large": (2, 4),
+                 "gpt2_2_5b": (8, 1), "gpt2_8_3b": (4, 2)}
+# the fp32 CPU port keeps params + grads + Adam state on the host: models
+# above this many layers x hidden^2 run a layer cut, extrapolated
+CPU_FULL_MODEL_MAX = 24 * 1024 ** 2
 
 
-def workload_shape(args, cfg, world):
-    """(M_total, P, D, m, how m was chosen) — shared by both arms so the
-    reference arm times the same workload as the vpipe arm."""
-    M, m = MODEL_CONFIGS[args.config]
+def load_plan(config, P, D):
+    """The committed plan (tools/write_plans.py) for this config at P x D."""
+    with open(os.path.join(ROOT, "profiles", "plans.json")) as f:
+        plans = json.load(f)
+    ent = plans.get(config, {}).get(f"{P}x{D}")
+    if ent is None:
+        raise SystemExit(f"no committed plan for {config} {P}x{D} in profiles/plans.json "
+                         "(run tools/write_plans.py)")
+    return ent
+
+
+def _ladder_pd(args, world):
     if args.pd:
-        P, D = map(int, args.pd.lower().split("x"))
-    else:
-        P, D = LADDER.get(world, (world, 1))
-    m_how = "config default"
-    if args.m == "auto":
-        m_sel = choose_micro_batch(cfg, P, D, M, args.config)
-        if m_sel is not None:
-            m, m_how = m_sel, "planner: fastest simulated mini-batch over the calibration m grid"
-    elif args.m:
-        m, m_how = int(args.m), "command line"
-    return M, P, D, m, m_how
+        return tuple(map(int, args.pd.lower().split("x")))
+    return LADDER.get(world, (world, 1))
+
+
+def _timeit(fn, min_s=0.2, max_reps=2000):
+    """Median wall time (s) of fn() over repetitions filling ~min_s."""
+    ts = []
+    t_end = time.perf_counter() + min_s
+    while len(ts) < 3 or (time.perf_counter() < t_end and len(ts) < max_reps):
+        t0 = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t0)
+    return statistics.median(ts)
+
+
+def control_plane_times(api, plans, configs=None):
+    """Single-threaded wall time (us) of the control-plane entry points the
+    executor depends on: the Varuna plan (uncached),
+    assign_stages over the B200 calibration profile, and simulate_minibatch
+    (opportunistic), at each BASELINE config's north-star P x D. ``api`` is
+    the reference's spotpipe module or the product package (C++ twins)."""
+    out = {}
+    for name in configs or NORTH_STAR_PD:
+        P, D = NORTH_STAR_PD[name]
+        ent = plans.get(name, {}).get(f"{P}x{D}")
+        prof_path = os.path.join(ROOT, "profiles", f"b200_{name}.yaml")
+        if ent is None or not os.path.exists(prof_path):
+            continue
+        L, h, _, _, S, _, _ = MODEL_DIMS[name]
+        m, N = ent["m"], ent["N"]
+        prof = api.load_profile(prof_path)
+        if m not in prof.m_grid:
+            continue
+        model = api.make_block_model(name, L, h, S)
+        gen = getattr(api.generate_varuna_schedule, "__wrapped__", api.generate_varuna_schedule)
+        sched = gen(P, N, 1.0, 2.0, 1.0)
+        pc = api.ParallelConfig(P, D, m, N, tuple(ent["stage_map"]))
+        place = api.build_placement(api.uniform_cluster(P * D, 8), P, D)
+        out[f"{name} {P}x{D} N_m={N}"] = {
+            "generate_varuna_schedule_us": round(1e6 * _timeit(
+                lambda: gen(P, N, 1.0, 2.0, 1.0)), 1),
+            "assign_stages_us": round(1e6 * _timeit(
+                lambda: api.assign_stages(model, P, m, prof)), 1),
+            "simulate_minibatch_us": round(1e6 * _timeit(
+                lambda: api.simulate_minibatch(sched, pc, prof, place, model,
+                                               opportunistic=True)), 1),
+        }
+    return out
+
+
+def reference_control_plane(plans):
+    """The reference's own CPU control plane (spotpipe 0.1.0 installed
+    unmodified into baseline/_ref; its compiled Cython replica kernel when
+    it built), or a one-line reason it is unavailable."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "spotpipe")):
+        return {"unavailable": "baseline/_ref/spotpipe not installed"}
+    sys.path.insert(0, ref)
+    try:
+        import spotpipe
+        import spotpipe.engine as eng
+        res = control_plane_times(spotpipe, plans)
+        res["engine"] = eng.ENGINE_NAME
+        return res
+    except Exception as ex:  # noqa: BLE001
+        return {"unavailable": f"spotpipe import/run failed: {ex}"}
+    finally:
+        sys.path.remove(ref)
+
+
+class CpuPipelineSample:
+    """The executor's tensor path on the host cores: the fp32 torch-CPU port
+    (oracle/gpt2_fp32.py) walking the Varuna plan of this config's stage map
+    for ONE sample per step (m = 1, one micro-batch: F, R on every
+    recomputing stage, B), plus 1/M_total of one AdamW update over all
+    parameters (timed once). Models too large to hold fp32 params + grads +
+    Adam state on the host run a cut of the layers and the time is scaled by
+    the layer count (said in ``sample``)."""
+
+    def __init__(self, config, stage_map):
+        import torch
+        from oracle.gpt2_fp32 import PipelineOracle
+        self.threads = os.cpu_count() or 1
+        torch.set_num_threads(self.threads)
+        L, h, H, V, S, arch, mlm = MODEL_DIMS[config]
+        self.config, self.S, self.V, self.arch, self.mlm = config, S, V, arch, mlm
+        self.L = L
+        P = max(stage_map) + 1
+        cut = L
+        if L * h * h > CPU_FULL_MODEL_MAX:
+            cut = max(P, (CPU_FULL_MODEL_MAX // (h * h)) // P * P)
+        # the same P-stage structure on the cut: layers spread evenly
+        smap = [min(P - 1, i * P // cut) for i in range(cut)] if cut != L else list(stage_map)
+        self.cut = cut
+        self.o = PipelineOracle(cut, h, H, V, S, smap, 1, 1, seed=0, arch=arch)
+        self.P = P
+        g = torch.Generator()
+        g.manual_seed(1234)
+        toks = torch.randint(0, V, (1, S + 1), generator=g)
+        if arch == "bert":
+            self.ids = toks[:, :S].contiguous()
+            self.types = torch.zeros(1, S, dtype=torch.int64)
+            self.types[:, S // 2:] = 1
+            self.labels = torch.full((1, S), -100, dtype=torch.int64)
+            self.labels[0, :mlm] = toks[0, 1:mlm + 1]
+        else:
+            self.ids, self.labels, self.types = toks[:, :-1].contiguous(), toks[:, 1:].contiguous(), None
+        self.adam_s = None
+
+    def step(self, M_total):
+        """Seconds for one sample's F(+R)+B (+ its AdamW share)."""
+        t0 = time.perf_counter()
+        self.o.run_minibatch(self.ids, self.labels, self.S if self.arch != "bert" else self.mlm,
+                             types=self.types)
+        t = time.perf_counter() - t0
+        if self.adam_s is None:
+            t1 = time.perf_counter()
+            self.o.adamw_step(1)
+            self.adam_s = time.perf_counter() - t1
+        for p in self.o.params.values():
+            p.grad = None
+        return (t + self.adam_s / M_total) * (self.L / self.cut)
+
+    def describe(self):
+        L, h = self.L, MODEL_DIMS[self.config][1]
+        cut = "" if self.cut == L else (f"; {self.cut} of {L} layers run, time scaled x{L / self.cut:.2f} "
+                                         "(extrapolated)")
+        return (f"1 sample per step: fp32 torch-CPU port of the executor (oracle/gpt2_fp32.py) walking "
+                f"the Varuna plan over {self.P} stage(s) — F, R on recomputing stages, B — at s={self.S}, "
+                f"h={h}, plus 1/M_total of one AdamW update{cut}")
 
 
 def run_reference(args):
-    """--impl reference: the reference CPU path of this hot path (the fp32
-    oracle port — the reference itself has no tensor math) on the host cores."""
-    from paper_2111_04007_b200.model import CONFIGS
+    """--impl reference: the reference-side CPU arm. Rank 0 alone runs (other
+    ranks exit at once). No product import: the plan comes from the committed
+    profiles/plans.json, the control plane is spotpipe's own, the tensor path
+    the fp32 CPU port."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    cfg = CONFIGS[args.config]
-    M, P, D, m, _ = workload_shape(args, cfg, args.gpus)
-    vals = []
+    with open(os.path.join(ROOT, "profiles", "plans.json")) as f:
+        plans = json.load(f)
+    P, D = _ladder_pd(args, args.gpus)
+    ent = load_plan(args.config, P, D)
+    M, m, N = ent["M_total"], ent["m"], ent["N"]
+    L, h, H, V, S, arch, _ = MODEL_DIMS[args.config]
+    cp = reference_control_plane(plans)
+    sample = CpuPipelineSample(args.config, ent["stage_map"])
+    times = []
     for i in range(args.warmup + args.steps):
-        v, threads, sample, _ = cpu_layer_sample(cfg, m, budget_s=min(args.cpu_sample_s, 8.0),
-                                                 recompute=P > 1)
+        t = sample.step(M)
         if i >= args.warmup:
-            vals.append(v)
-    value = statistics.median(vals)
+            times.append(t)
+    total = sum(times)
+    value = len(times) / total
     line = {"metric": f"samples/sec ({METRIC_NAMES[args.config]} Varuna pipeline step)",
-            "value": round(value, 4),
-            "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(M / value * 1e3, 1), "higher_is_better": True,
+            "value": round(value, 5), "unit": "samples/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * total / len(times), 1), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": f"{args.config} {P}x{D} m={m} M_total={M} (CPU oracle)",
-                       "global_batch": M, "seq_len": cfg.seq_len, "parallelism": f"pp{P}xdp{D}"},
-            "cpu_baseline": {"value": round(value, 4), "unit": "samples/s", "cores": threads,
-                             "kind": "port", "sample": sample},
-            "e2e": {"value": round(value, 4), "unit": "samples/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+            "config": {"workload": f"{args.config} P{P}xD{D} m={m} N_m={N} M_total={M}",
+                       "global_batch": M, "seq_len": S, "parallelism": f"pp{P}xdp{D}",
+                       "plan": "profiles/plans.json (committed)"},
+            "cpu_baseline": {"value": round(value, 5), "unit": "samples/s",
+                             "cores": sample.threads, "kind": "port",
+                             "sample": sample.describe()},
+            "e2e": {"value": round(value, 5), "unit": "samples/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "control_plane_reference_cpu_us": cp}
     print(json.dumps(line), flush=True)
     return 0
 
 
 # ---------------------------------------------------------------- GPU arm
+
+def workload_shape(args, cfg, world):
+    """(M_total, P, D, m, how m was chosen, stage_map) — from the committed
+    plan (profiles/plans.json) so both arms time the same workload; an
+    explicit --m recomputes N_m and the stage map."""
+    M, m = MODEL_CONFIGS[args.config]
+    P, D = _ladder_pd(args, world)
+    if args.m == "auto":
+        try:
+            ent = load_plan(args.config, P, D)
+            return ent["M_total"], P, D, ent["m"], ent["m_choice"] + " (profiles/plans.json)", \
+                tuple(ent["stage_map"])
+        except (SystemExit, OSError):
+            m_sel = choose_micro_batch(cfg, P, D, M, args.config)
+            if m_sel is not None:
+                m = m_sel
+            how = "planner (computed: no committed plan)"
+    else:
+        m, how = int(args.m), "command line"
+    return M, P, D, m, how, tuple(stage_map_for(cfg, P, m, args.config))
+
 
 def main():
     args = parse()
@@ -316,9 +453,8 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     cfg = CONFIGS[args.config]
-    M, P, D, m, m_how = workload_shape(args, cfg, world)
+    M, P, D, m, m_how, stage_map = workload_shape(args, cfg, world)
     N = micro_batches_for(JobSpec(M), m, D)
-    stage_map = stage_map_for(cfg, P, m, args.config)
     pc = ParallelConfig(P, D, m, N, stage_map)
     init_dev = "cuda"
     # P > 1: the reference's opportunistic policy (sp/engine decide) run over
@@ -454,14 +590,24 @@ def main():
                                  opportunistic=dispatch == "opportunistic")
 
     cpu = None
+    control_plane = None
     if rank == 0:
-        try:
-            cv, threads, sample, _ = cpu_layer_sample(cfg, m, args.cpu_sample_s, recompute=P > 1)
-            cpu = {"value": round(cv, 5), "unit": "samples/s", "cores": threads, "kind": "port",
-                   "sample": sample}
+        try:   # bounded: ~cpu_sample_s of host work after one warm-up sample
+            cs = CpuPipelineSample(args.config, stage_map)
+            cs.step(M)
+            ts = []
+            while sum(ts) < args.cpu_sample_s and len(ts) < 50:
+                ts.append(cs.step(M))
+            cpu = {"value": round(len(ts) / sum(ts), 5), "unit": "samples/s",
+                   "cores": cs.threads, "kind": "port",
+                   "sample": cs.describe() + f"; {len(ts)} samples timed"}
+            del cs
         except Exception as ex:  # noqa: BLE001
             cpu = {"value": None, "unit": "samples/s", "cores": os.cpu_count(), "kind": "port",
                    "sample": f"failed: {ex}"}
+        import paper_2111_04007_b200 as vpapi
+        with open(os.path.join(ROOT, "profiles", "plans.json")) as f:
+            control_plane = control_plane_times(vpapi, json.load(f))
     if rank == 0:
         line = {
             "metric": f"samples/sec ({METRIC_NAMES[args.config]} Varuna pipeline step)",
@@ -488,6 +634,7 @@ def main():
                                "frac": round(value / roof_samples, 4)},
             "bubble": {"measured": round(bubble, 4), "predicted": predicted},
             "cpu_baseline": cpu,
+            "control_plane_cpp_us": control_plane,
         }
         print(json.dumps(line), flush=True)
     v.close()

@@ -179,6 +179,10 @@ int vp_attention_bwd_ex(const void* qkv, const void* o, const void* dout, const 
 /* dbias (optional, fused path only, else VP_ERR_UNSUPPORTED): dbias[3*H*D]
  * += column sums of dqkv — the QKV bias gradient — from the dQ post-pass
  * and the dK/dV epilogue partials (fixed-order reductions). */
+/* 1 when vp_attention_bwd_ex with these flags (and the VP_ATTN_DETERMINISTIC
+ * environment override) takes the fused path, i.e. accepts dbias; callers
+ * that get 0 sum the QKV bias gradient themselves. */
+int vp_attention_bwd_fuses_bias(int64_t head_dim, int flags);
 
 /* Token + position embedding gather: x[T,h] = wte[ids] + wpe[pos]. */
 int vp_embed_fwd(const int64_t* ids, const void* wte, const void* wpe, void* x, int64_t batch,

@@ -168,6 +168,16 @@ class PipelineOracle:
         P, N = self.P, self.N
         plan = osch.varuna_plan(P, N, 1_000_000, 2_000_000, 1_000_000)
         order = _global_order(plan, P)
+        rows = N * self.m
+        if ids.shape[0] < rows:
+            # M_total semantics (sp/planner.py:99-103): N_m = ceil(M/(m*D)),
+            # the last micro-batch partially filled; padded rows carry no label
+            pad = rows - ids.shape[0]
+            ids = torch.cat([ids, torch.zeros(pad, ids.shape[1], dtype=ids.dtype)], 0)
+            labels = torch.cat([labels, torch.full((pad, labels.shape[1]), -100,
+                                                   dtype=labels.dtype)], 0)
+            if types is not None:
+                types = torch.cat([types, torch.zeros(pad, types.shape[1], dtype=types.dtype)], 0)
         ids = ids.view(N, self.m * self.S)
         labels = labels.view(N, self.m * self.S)
         if types is not None:

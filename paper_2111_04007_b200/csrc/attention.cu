@@ -109,6 +109,11 @@ extern "C" int64_t vp_attention_bwd_ws_elems(int64_t batch, int64_t seq, int64_t
   return attention_bwd_fused_ws(batch, seq, heads, head_dim);
 }
 
+extern "C" int vp_attention_bwd_fuses_bias(int64_t head_dim, int flags) {
+  const bool det = (flags & VP_ATTN_DETERMINISTIC) || getenv("VP_ATTN_DETERMINISTIC");
+  return (!det && attention_bwd_fused_ok(head_dim)) ? 1 : 0;
+}
+
 extern "C" int vp_attention_bwd_ex(const void* qkv, const void* o, const void* dout,
                                    const float* lse, void* dqkv, float* workspace,
                                    int64_t ws_elems, int64_t batch, int64_t seq, int64_t heads,

@@ -609,12 +609,7 @@ int fused_t(const void* qkv, const void* o, const void* dout, const float* lse, 
       !make_tmap_bsc_f32(&tdq, dq_acc, H * D, S, B, 32))
     return VP_ERR_UNSUPPORTED;
   auto k = attn_bwd_fused<CAUSAL>;
-  static bool set = false;
-  if (!set) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
-    if (e != cudaSuccess) return e;
-    set = true;
-  }
+  if (cudaError_t e = smem_optin(k, L::TOTAL); e != cudaSuccess) return e;
   const int64_t rows = tokens * H;
   attn_delta_zero_kernel<<<static_cast<unsigned>((rows * (D / 8) + 255) / 256), 256, 0, st>>>(
       reinterpret_cast<const __nv_bfloat16*>(o), reinterpret_cast<const __nv_bfloat16*>(dout),

@@ -855,14 +855,8 @@ int bwd_tc_t(const void* qkv, const void* dout, const float* lse, const float* d
     return VP_ERR_UNSUPPORTED;
   auto k1 = attn_bwd_dkdv_tc<D, CAUSAL>;
   auto k2 = attn_bwd_dq_tc<D, CAUSAL>;
-  static bool set = false;
-  if (!set) {
-    cudaError_t e = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
-    if (e != cudaSuccess) return e;
-    set = true;
-  }
+  if (cudaError_t e = smem_optin(k1, L::TOTAL); e != cudaSuccess) return e;
+  if (cudaError_t e = smem_optin(k2, L::TOTAL); e != cudaSuccess) return e;
   const float scale = 1.f / sqrtf(static_cast<float>(D));
   const float scale_log2 = 1.4426950408889634f * scale;
   const int n_kb = static_cast<int>((S + TB_M - 1) / TB_M);
@@ -902,12 +896,7 @@ int fwd_tc_t(const void* qkv, void* o, float* lse, int64_t B, int64_t S, int64_t
   if (!make_tmap_bsc(&tm, qkv, 3 * H * D, S, B, 128)) return VP_ERR_UNSUPPORTED;
   if (!make_tmap_bsc(&tkv, qkv, 3 * H * D, S, B, TA_BN)) return VP_ERR_UNSUPPORTED;
   auto k = attn_fwd_tc<D, CAUSAL>;
-  static bool set = false;
-  if (!set) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
-    if (e != cudaSuccess) return e;
-    set = true;
-  }
+  if (cudaError_t e = smem_optin(k, L::TOTAL); e != cudaSuccess) return e;
   const int n_qb = static_cast<int>((S + TA_BM - 1) / TA_BM);
   dim3 grid(n_qb, static_cast<unsigned>(B * H));
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(D));

@@ -9,31 +9,41 @@
 
 namespace vp {
 
-// Opt kernel `fn` into `bytes` of dynamic shared memory, once per process
-// per kernel (keyed by the function pointer: a `static bool` inside a generic
-// launch lambda would be shared by every kernel of the same signature).
+// Opt kernel `fn` into `bytes` of dynamic shared memory, once per (kernel,
+// device, size) — keyed by the function pointer (a `static bool` inside a
+// generic launch lambda would be shared by every kernel of the same
+// signature) and by the current device (the attribute is per-device state).
 inline cudaError_t smem_optin(const void* fn, int bytes) {
+  struct Key { const void* fn; int dev; int bytes; };
   static std::mutex mu;
-  static const void* done[256];
+  static Key done[1024];
   static int nd = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lock(mu);
   for (int i = 0; i < nd; ++i)
-    if (done[i] == fn) return cudaSuccess;
+    if (done[i].fn == fn && done[i].dev == dev && done[i].bytes >= bytes) return cudaSuccess;
   const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e == cudaSuccess && nd < 256) done[nd++] = fn;
+  if (e == cudaSuccess && nd < 1024) done[nd++] = Key{fn, dev, bytes};
   return e;
 }
+template <typename F>
+inline cudaError_t smem_optin(F* fn, int bytes) {
+  return smem_optin(reinterpret_cast<const void*>(fn), bytes);
+}
 
-// SM count of the current device (cached per process; B200: 148).
+// SM count of the current device (cached per device; B200: 148).
 inline int device_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cache[dev]) {
+    int n = 0;
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+    cache[dev] = n > 0 ? n : 148;
   }
-  return n;
+  return cache[dev];
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

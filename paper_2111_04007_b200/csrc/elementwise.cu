@@ -652,12 +652,7 @@ extern "C" int vp_xent_fwd_bwd(void* logits, const int64_t* labels, float* loss_
   if (rows <= 0 || vocab <= 0 || (vocab % 8)) return VP_ERR_ARGS;
   const size_t smem = static_cast<size_t>(vocab) * 2;
   if (smem <= 110 * 1024 && (reinterpret_cast<uintptr_t>(logits) & 15) == 0 && !getenv("VP_XENT_2PASS")) {
-    static bool set = false;
-    if (!set) {
-      cudaFuncSetAttribute(xent_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           110 * 1024);
-      set = true;
-    }
+    if (cudaError_t e = vp::smem_optin(xent_smem_kernel, 110 * 1024); e != cudaSuccess) return e;
     xent_smem_kernel<<<static_cast<unsigned>(rows), 512, smem, ST>>>(BF(logits), labels,
                                                                     loss_rows, loss_sum, vocab,
                                                                     scale);

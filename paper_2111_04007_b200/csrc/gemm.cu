@@ -782,29 +782,14 @@ bool make_tmap(CUtensorMap* map, const void* base, uint64_t inner, uint64_t oute
   return r == CUDA_SUCCESS;
 }
 
-int g_sm_count = 0;
-int sm_count() {
-  if (!g_sm_count) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
-    if (g_sm_count <= 0) g_sm_count = 148;
-  }
-  return g_sm_count;
-}
+int sm_count() { return device_sms(); }
 
 template <int BN, int STAGES, int EPI, bool A_MN, bool B_MN>
 int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, int64_t M, int64_t N, int64_t K,
              const EpiArgs& e, cudaStream_t st) {
   using S = Smem<BN, STAGES>;
   auto kern = gemm_kernel<BN, STAGES, EPI, A_MN, B_MN>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t err =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL);
-    if (err != cudaSuccess) return err;
-    attr_set = true;
-  }
+  if (cudaError_t err = vp::smem_optin(kern, S::TOTAL); err != cudaSuccess) return err;
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = static_cast<int>(std::min<int64_t>(tiles, sm_count()));
   kern<<<grid, kThreads, S::TOTAL, st>>>(ta, tb, M, N, K, e);
@@ -847,13 +832,7 @@ int launch2_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& t
               const CUtensorMap& tx, int64_t M, int64_t N, int64_t K, int split_k,
               const Epi2& e, cudaStream_t st) {
   auto kern = gemm2_kernel<EPI, A_MN, B_MN>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t err =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G2Cfg<EPI>::kSmem);
-    if (err != cudaSuccess) return err;
-    attr_set = true;
-  }
+  if (cudaError_t err = vp::smem_optin(kern, G2Cfg<EPI>::kSmem); err != cudaSuccess) return err;
   const int64_t units = ((M + 255) / 256) * ((N + 255) / 256) * split_k;
   int64_t clusters = std::min<int64_t>(units, sm_count() / 2);
 #ifdef VP_GEMM_TRACE

@@ -34,6 +34,7 @@ _SIGS = {
     "vp_attention_bwd_ex": [vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, i64, c_int, c_int, vp,
                             vp],
     "vp_attention_bwd_ws_elems": [i64, i64, i64, i64],
+    "vp_attention_bwd_fuses_bias": [i64, c_int],
     "vp_layernorm_ws_elems": [i64],
     "vp_gemm_dbias_ws_elems": [i64, i64],
     "vp_gemm_bf16_dbias": [c_int, c_int, c_int, vp, i64, vp, i64, vp, i64, vp, vp, i64, i64, i64,
@@ -209,7 +210,8 @@ def attention_bwd(qkv, out, dout, lse, dqkv, ws, batch, seq, heads, head_dim, ca
     need = attention_bwd_ws_elems(batch, seq, heads, head_dim)
     if ws.numel() < need or ws.dtype != torch.float32:
         raise ValueError(f"attention_bwd: workspace needs {need} fp32 elements")
-    fused_bias = dbias is not None and head_dim == 64 and not deterministic
+    fused_bias = dbias is not None and bool(
+        L.vp_attention_bwd_fuses_bias(head_dim, 1 if deterministic else 0))
     _count(3 + (1 if fused_bias else 0))
     check(L.vp_attention_bwd_ex(qkv.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(),
                                 dqkv.data_ptr(), ws.data_ptr(), ws.numel(), batch, seq, heads,

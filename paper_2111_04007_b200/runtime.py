@@ -87,7 +87,9 @@ class StepResult:
 
     @property
     def loss(self) -> Optional[float]:
-        return None if self._loss is None else float(self._loss.item())
+        """Mean loss over the mini-batch's M_total samples (the device sum
+        carries the loss scale; it is removed here)."""
+        return None if self._loss is None else float(self._loss.item()) * self.inv_scale
 
     @property
     def overflow(self) -> bool:
@@ -236,6 +238,22 @@ class _Links:
         check(K.L.vp_ipc_event_open(handle, ctypes.byref(e)), "vp_ipc_event_open")
         return e.value
 
+    def close(self):
+        """Unmap the peer rings and destroy the IPC events (every rank of the
+        job calls this before any rank frees its rings, Varuna.close)."""
+        for ptr in self.peer_ring.values():
+            check(K.L.vp_ipc_close_mem_handle(ptr), "vp_ipc_close_mem_handle")
+        self.peer_ring = {}
+        for evs in list(self.rx_events.values()) + list(self.tx_events.values()):
+            for e in evs:
+                check(K.L.vp_event_destroy(e), "vp_event_destroy")
+        self.rx_events, self.tx_events = {}, {}
+
+    def free_local(self):
+        for buf in self.rx.values():
+            buf.free()
+        self.rx = {}
+
     def rx_slot(self, direction, j, shape):
         return self.rx[direction].tensor(shape, torch.bfloat16, j * self.slot_bytes)
 
@@ -342,7 +360,8 @@ class Varuna:
     def __init__(self, model: GPT2Config, config: ParallelConfig, *,
                  optimizer: AdamWConfig = AdamWConfig(), seed: int = 0, loss_scale: float = 1.0,
                  device=None, init_device: str = "cpu", trace: bool = False,
-                 dispatch: str = "static", profile=None, graphs: Optional[bool] = None):
+                 dispatch: str = "static", profile=None, graphs: Optional[bool] = None,
+                 backend: Optional[str] = None, global_batch: Optional[int] = None):
         if len(config.stage_map) != model.n_layer:
             raise ConfigError(f"stage_map covers {len(config.stage_map)} cut-points, model has "
                               f"{model.n_layer} (one CutPoint per transformer layer)")
@@ -354,15 +373,43 @@ class Varuna:
             self.rank, self.world = dist.get_rank(), dist.get_world_size()
         else:
             self.rank, self.world = 0, 1
-        if self.world != P * D:
-            raise ConfigError(f"world size {self.world} != P*D = {P * D}")
-        self.stage_id, self.replica = self.rank % P, self.rank // P
-        layers = tuple(i for i, s in enumerate(config.stage_map) if s == self.stage_id)
-        if not layers:
-            raise ConfigError(f"stage {self.stage_id} owns no cut-points")
+        if self.world < P * D:
+            raise ConfigError(f"world size {self.world} < P*D = {P * D}")
+        # ranks >= P*D are spares (the planner may leave GPUs unused,
+        # PlanResult.unused_gpus, sp/planner.py): they join the collective
+        # setup and teardown but own no stage and run no tasks
+        self.active = self.rank < P * D
+        self.stage_id, self.replica = (self.rank % P, self.rank // P) if self.active else (-1, -1)
+        # M_total (sp/planner.py:99-103): N_m = ceil(M/(m*D)); the last
+        # micro-batches may be partial (padded rows carry ignored labels) and
+        # the loss is the mean over M_total samples, not over the padded count
+        cap = self.m * self.N * D
+        self.global_batch = cap if global_batch is None else int(global_batch)
+        if not (cap - self.m * D < self.global_batch <= cap):
+            raise ConfigError(f"global_batch {self.global_batch} does not need N_m = {self.N} "
+                              f"micro-batches of {self.m} on {D} replicas "
+                              f"(ceil(M/(m*D)) = {-(-self.global_batch // (self.m * D))})")
+        # collective backend of the DP / pipeline / tie groups: NCCL when each
+        # rank has its own GPU (the product); gloo when several ranks share
+        # one device (NCCL refuses duplicate GPUs). The data plane is the same.
+        self.backend = backend
+        self.loss_scale = loss_scale
+        self.links = None
+        self.shm = None
+        self._graphs = {}
+        self.step_count = 0
         if device is None:
             device = torch.device("cuda", torch.cuda.current_device())
         self.device = torch.device(device)
+        if not self.active:
+            self.spec = self.stage = None
+            self._setup_groups()
+            if P > 1:   # the peer-handle exchange of _Links is collective
+                dist.all_gather_object([None] * self.world, {"rank": self.rank}, group=self.gloo)
+            return
+        layers = tuple(i for i, s in enumerate(config.stage_map) if s == self.stage_id)
+        if not layers:
+            raise ConfigError(f"stage {self.stage_id} owns no cut-points")
         torch.cuda.set_device(self.device)
         self.stream = torch.cuda.Stream(self.device)
         self.spec = StageSpec(self.stage_id, P, layers)
@@ -377,13 +424,10 @@ class Varuna:
             raise ConfigError(f"dispatch must be 'static' or 'opportunistic', not {dispatch!r}")
         self.dispatch = dispatch
         self._check_plan()
-        self.loss_scale = loss_scale
-        self.step_count = 0
         self.trace = trace
         self.loss_sum = torch.zeros(1, device=self.device)
         self.flags = torch.zeros(2, device=self.device)
         self._setup_groups()
-        self.links = None
         if P > 1:
             slot_elems = self.m * model.seq_len * model.hidden
             self.links = _Links(self.rank, self.stage_id, P, self.N, slot_elems,
@@ -396,7 +440,6 @@ class Varuna:
         # Disabled with dropout (per-step seeds) and while kernel timing hooks
         # are active.
         self.use_graphs = (model.dropout <= 0) if graphs is None else bool(graphs)
-        self._graphs = {}
         T = self.m * model.seq_len
         self._in_ids = torch.zeros(T, dtype=torch.int64, device=self.device)
         self._in_types = torch.zeros(T, dtype=torch.int64, device=self.device)
@@ -456,19 +499,26 @@ class Varuna:
         if self.world == 1:
             return
         gr = group_ranks(P, D)
+        self._groups = []
+
+        def new(ranks):   # collective over the whole world, members or not
+            g = dist.new_group(ranks, backend=self.backend)
+            self._groups.append(g)
+            return g
         for s, ranks in enumerate(gr["dp"]):
-            g = dist.new_group(ranks)
+            g = new(ranks)
             if s == self.stage_id:
                 self.dp_group = g
         for r, ranks in enumerate(gr["pipe"]):
-            g = dist.new_group(ranks)
+            g = new(ranks)
             if r == self.replica:
                 self.pipe_group = g
         for r, ranks in enumerate(gr["tie"]):
-            g = dist.new_group(ranks)
-            if r == self.replica and (self.spec.first or self.spec.last):
+            g = new(ranks)
+            if r == self.replica and self.active and (self.spec.first or self.spec.last):
                 self.tie_group = g
         self.gloo = dist.new_group(list(range(self.world)), backend="gloo")
+        self._groups.append(self.gloo)
         tag = os.environ.get("MASTER_PORT", "0")
         name = f"vpipe_{tag}_{os.getuid()}"
         if self.rank == 0:
@@ -491,10 +541,14 @@ class Varuna:
             if types is None:
                 types = torch.zeros_like(ids)
         rows = self.N * self.m
+        share = min(max(self.global_batch - self.replica * rows, 0), rows)
         out = {}
         for key, t, fill in (("ids", ids, 0), ("labels", labels, -100), ("types", types, 0)):
             if t is None:
                 continue
+            if t.shape[0] not in (share, rows):
+                raise ConfigError(f"replica {self.replica} got {t.shape[0]} rows; its share of "
+                                  f"M_total = {self.global_batch} is {share}")
             if t.shape[0] < rows:
                 pad = torch.full((rows - t.shape[0], t.shape[1]), fill, dtype=torch.int64,
                                  device=t.device)
@@ -509,13 +563,14 @@ class Varuna:
         """One mini-batch: N_m micro-batches through this stage's task list,
         then gradient synchronisation and the optimizer update."""
         self.step_count += 1
+        if not self.active:
+            return StepResult(None, torch.zeros(2), 1.0 / self.loss_scale)
         seq_no = self.step_count
         st = self.stream
         cfg, stage = self.cfg, self.stage
-        rows_total = self.pc.micro_batch_size * self.N * self.D
-        # loss = mean over the mini-batch's label tokens (BERT: the generator
-        # fixes mlm_per_seq masked positions per sequence)
-        total_tokens = rows_total * (cfg.mlm_per_seq if cfg.arch == "bert" else cfg.seq_len)
+        # loss = mean over the M_total samples' label tokens (BERT: the
+        # generator fixes mlm_per_seq masked positions per sequence)
+        total_tokens = self.global_batch * (cfg.mlm_per_seq if cfg.arch == "bert" else cfg.seq_len)
         scale = self.loss_scale / total_tokens
         ev = [] if self.trace else None
         st.wait_stream(torch.cuda.current_stream(self.device))
@@ -700,33 +755,67 @@ class Varuna:
     def save_layer_state(self, ckpt_dir: str) -> str:
         """Write this rank's share of the stage's per-layer state (fp32 master,
         Adam moments) keyed by GLOBAL parameter names, so a resume may use a
-        different stage map / P x D. Returns the file written."""
-        os.makedirs(ckpt_dir, exist_ok=True)
-        P = self.stage.params
-        state = {}
-        for name in P.names:
-            if name == "wte_head":      # tied copy: stage 0 owns "wte"
-                continue
-            if self._owner_replica(name) != self.replica:
-                continue
-            state[name] = {k: P.view(getattr(P, buf), name).detach().cpu().clone()
-                           for k, buf in (("master", "master"), ("exp_avg", "exp_avg"),
-                                          ("exp_avg_sq", "exp_avg_sq"))}
-        path = os.path.join(ckpt_dir, f"stage{self.stage_id}_replica{self.replica}.pt")
-        torch.save({"step": self.step_count, "state": state}, path)
+        different stage map / P x D. Each save goes to its own ``step<N>/``
+        subdirectory, and rank 0 writes ``manifest.json`` (step, P, D, shard
+        list), so shards of an earlier save — possibly under another P x D —
+        are never mixed in. Collective: call on every rank. Returns the shard
+        written (None on a spare rank)."""
+        sub = os.path.join(ckpt_dir, f"step{self.step_count:08d}")
+        path = None
+        if self.active:
+            os.makedirs(sub, exist_ok=True)
+            P = self.stage.params
+            state = {}
+            for name in P.names:
+                if name == "wte_head":      # tied copy: stage 0 owns "wte"
+                    continue
+                if self._owner_replica(name) != self.replica:
+                    continue
+                state[name] = {k: P.view(getattr(P, buf), name).detach().cpu().clone()
+                               for k, buf in (("master", "master"), ("exp_avg", "exp_avg"),
+                                              ("exp_avg_sq", "exp_avg_sq"))}
+            path = os.path.join(sub, f"stage{self.stage_id}_replica{self.replica}.pt")
+            torch.save({"step": self.step_count, "P": self.P, "D": self.D, "state": state}, path)
+        if self.world > 1:
+            dist.barrier(group=self.gloo)
+        if self.rank == 0:
+            import json
+            man = {"step": self.step_count, "P": self.P, "D": self.D,
+                   "stage_map": list(self.pc.stage_map), "micro_batch_size": self.m,
+                   "global_batch": self.global_batch,
+                   "shards": [f"stage{s_}_replica{r_}.pt" for r_ in range(self.D)
+                              for s_ in range(self.P)]}
+            tmp = os.path.join(ckpt_dir, "manifest.json.tmp")
+            with open(tmp, "w") as f:
+                json.dump(man, f)
+            os.replace(tmp, os.path.join(ckpt_dir, "manifest.json"))   # the latest save
+        if self.world > 1:
+            dist.barrier(group=self.gloo)
         return path
 
+    @staticmethod
+    def read_manifest(ckpt_dir: str) -> dict:
+        import json
+        with open(os.path.join(ckpt_dir, "manifest.json")) as f:
+            return json.load(f)
+
     def load_layer_state(self, ckpt_dir: str) -> None:
-        """Load every parameter this rank owns from all shard files."""
+        """Load every parameter this rank owns from the shards the manifest
+        lists; every shard must carry the manifest's step and P x D."""
+        man = self.read_manifest(ckpt_dir)
+        self.step_count = int(man["step"])
+        if not self.active:
+            return
+        sub = os.path.join(ckpt_dir, f"step{man['step']:08d}")
         P = self.stage.params
         want = set(P.names)
         found = set()
-        step = None
-        for fn in sorted(os.listdir(ckpt_dir)):
-            if not fn.endswith(".pt"):
-                continue
-            blob = torch.load(os.path.join(ckpt_dir, fn), map_location="cpu")
-            step = blob["step"]
+        for fn in man["shards"]:
+            blob = torch.load(os.path.join(sub, fn), map_location="cpu")
+            if (blob["step"], blob["P"], blob["D"]) != (man["step"], man["P"], man["D"]):
+                raise ConfigError(f"checkpoint shard {fn}: step {blob['step']} at "
+                                  f"{blob['P']}x{blob['D']}, manifest: step {man['step']} at "
+                                  f"{man['P']}x{man['D']}")
             for name, st in blob["state"].items():
                 targets = [name] + (["wte_head"] if name == "wte" else [])
                 for t in targets:
@@ -739,31 +828,81 @@ class Varuna:
         missing = want - found
         if missing:
             raise ConfigError(f"checkpoint {ckpt_dir} lacks {sorted(missing)[:4]}...")
-        self.step_count = int(step or 0)
         torch.cuda.synchronize()
 
     def close(self):
+        """Release what the executor holds: CUDA graphs, peer mappings, IPC
+        events, rings, the stage's parameters / optimizer state / working
+        sets, the shm handshake and the process groups. Collective over the
+        job's ranks (every peer unmaps a ring before its owner frees it)."""
+        if getattr(self, "_closed", False):
+            return
+        self._closed = True
+        if self.active:
+            torch.cuda.synchronize(self.device)
+        self._graphs = {}
+        if self.links is not None:
+            self.links.close()
+        if self.world > 1 and getattr(self, "gloo", None) is not None:
+            dist.barrier(group=self.gloo)
+        if self.links is not None:
+            self.links.free_local()
+            self.links = None
         if self.shm is not None:
             self.shm.close()
             self.shm = None
+        for g in getattr(self, "_groups", []):
+            try:
+                dist.destroy_process_group(g)
+            except Exception:  # noqa: BLE001 - torn down with the world group already
+                pass
+        self._groups = []
+        self.dp_group = self.pipe_group = self.tie_group = self.gloo = None
+        self.stage = None
+        self._in_ids = self._in_types = self._in_labels = None
+        torch.cuda.empty_cache()
 
 
-def morph(v: Varuna, new_config: ParallelConfig, ckpt_dir: str, **kwargs) -> Varuna:
-    """Re-partition a running job onto ``new_config`` (the decision the
-    reference makes with ``plan()`` on a cluster change, sp/morphing.py:
-    383-448): every rank writes its per-layer shard, the old executor is torn
-    down, a new one is built for the new (P, D, stage_map) on the same ranks,
-    and each rank loads exactly the layers its new stage owns. M_total is
-    preserved through N_m = ceil(M/(m*D)) in ``new_config``."""
+def replan(cfg: GPT2Config, gpus: int, profile, global_batch: int, micro_batch_size: int,
+           hw=None, seed: int = 0) -> ParallelConfig:
+    """The morph decision (sp/morphing.py:327-346 → planner.plan,
+    sp/planner.py:106-145): the fastest P x D for ``gpus`` GPUs of one
+    NVSwitch box, keeping the job's cached micro-batch size and M_total
+    (N_m = ceil(M/(m*D)))."""
+    from .core import B200_NVL8, JobSpec, make_block_model, uniform_cluster
+    from .planner import plan
+    model = make_block_model(f"{cfg.arch}-L{cfg.n_layer}-h{cfg.hidden}", cfg.n_layer, cfg.hidden,
+                             cfg.seq_len)
+    res = plan(gpus, model, JobSpec(global_batch), profile, hw or B200_NVL8,
+               uniform_cluster(gpus, 8), seed=seed, micro_batch_size=micro_batch_size)
+    return res.chosen
+
+
+def morph(v: Varuna, ckpt_dir: str, new_config: Optional[ParallelConfig] = None, *,
+          gpus: Optional[int] = None, profile=None, **kwargs) -> Varuna:
+    """Re-partition a running job: every rank writes its
+    per-layer shard, the old executor is torn down and its device memory
+    released (``v`` is closed — callers must rebind to the returned
+    executor), a new executor is built for the new (P, D, stage_map) on the
+    same ranks, and each rank loads exactly the layers its new stage owns.
+
+    Without ``new_config`` the configuration comes from the reference's morph
+    decision, ``replan`` (``plan(gpus, ..., micro_batch_size=cached m)``) over
+    ``profile`` for ``gpus`` available GPUs (default: the world size); ranks
+    beyond the chosen P x D become spares. M_total is preserved."""
+    if new_config is None:
+        if profile is None:
+            raise ConfigError("morph: pass new_config, or a calibration profile to plan with")
+        gpus = v.world if gpus is None else gpus
+        if not 1 <= gpus <= v.world:
+            raise ConfigError(f"morph: {gpus} GPUs available, job has {v.world} ranks")
+        new_config = replan(v.cfg, gpus, profile, v.global_batch, v.m)
     v.save_layer_state(ckpt_dir)
-    if dist.is_initialized():
-        dist.barrier()
-    torch.cuda.synchronize()
-    cfg = v.cfg
-    opt = v.opt
+    cfg, opt = v.cfg, v.opt
+    kwargs.setdefault("global_batch", v.global_batch)
+    kwargs.setdefault("backend", v.backend)
+    kwargs.setdefault("loss_scale", v.loss_scale)
     v.close()
-    del v
-    torch.cuda.empty_cache()
     nv = Varuna(cfg, new_config, optimizer=opt, **kwargs)
     nv.load_layer_state(ckpt_dir)
     if dist.is_initialized():

@@ -31,10 +31,11 @@ def main():
     ap.add_argument("--dispatch", default="static")
     ap.add_argument("--layers", type=int, default=0, help="cut the config to this many layers")
     ap.add_argument("--micro-batch", type=int, default=4)
+    ap.add_argument("--global-batch", type=int, default=0,
+                    help="M_total (default m*N*D); smaller values leave partial micro-batches")
     args = ap.parse_args()
-    local = int(os.environ.get("LOCAL_RANK", 0))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from tests._dist import init
+    dev, _ = init()
     from paper_2111_04007_b200 import ParallelConfig, assign_stages, make_block_model, uniform_profile
     from paper_2111_04007_b200.model import CONFIGS
     from paper_2111_04007_b200.runtime import Varuna, synthetic_batch
@@ -52,18 +53,21 @@ def main():
         # unbalanced per-cut-point times + slow, jittery links: the replica
         # kernel reorders tasks relative to the static schedule
         prof = skewed_profile(m)
-    v = Varuna(cfg, pc, seed=0, dispatch=args.dispatch, profile=prof)
+    M = args.global_batch or m * N * D
+    v = Varuna(cfg, pc, seed=0, dispatch=args.dispatch, profile=prof, global_batch=M)
     if args.dispatch == "opportunistic":
         kinds, mbs = v.schedule.stage_slice(v.stage_id)
         moved = sum(a != b for a, b in zip(zip(kinds.tolist(), mbs.tolist()), v.tasks))
         print(f"rank {v.rank} dispatch order differs from static at {moved} positions", flush=True)
-    batches = [synthetic_batch(cfg, m * N, r) for r in range(D)]
+    shares = [min(max(M - r * m * N, 0), m * N) for r in range(D)]
+    batches = [{k: t[:shares[r]] for k, t in synthetic_batch(cfg, m * N, r).items()}
+               for r in range(D)]
     res = v.step(batches[v.replica], apply=False)
     torch.cuda.synchronize()
     # oracle: D replicas' mini-batches, summed gradients
     o = PipelineOracle(cfg.n_layer, cfg.hidden, cfg.heads, cfg.vocab_size, cfg.seq_len,
                        pc.stage_map, m, N, seed=0, arch=cfg.arch)
-    total = m * N * D * (cfg.mlm_per_seq if cfg.arch == "bert" else cfg.seq_len)
+    total = M * (cfg.mlm_per_seq if cfg.arch == "bert" else cfg.seq_len)
     loss = sum(o.run_minibatch(b["input_ids"], b["labels"], total,
                                types=b.get("token_type_ids")) for b in batches)
     og = o.grads()
@@ -79,7 +83,7 @@ def main():
         lerr = abs(res.loss - loss) / abs(loss)
         print(f"rank {v.rank} loss {res.loss:.6f} oracle {loss:.6f} rel {lerr:.2e}", flush=True)
         ok = ok and lerr < 5e-3
-    flag = torch.tensor([0 if ok else 1], device="cuda")
+    flag = torch.tensor([0 if ok else 1], device=dev)
     dist.all_reduce(flag)
     v.close()
     if dist.get_rank() == 0:

@@ -13,9 +13,8 @@ sys.path.insert(0, ROOT)
 
 
 def main():
-    local = int(os.environ.get("LOCAL_RANK", 0))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from tests._dist import init
+    dev, _ = init()
     from paper_2111_04007_b200 import ParallelConfig
     from paper_2111_04007_b200.model import CONFIGS
     from paper_2111_04007_b200.runtime import AdamWConfig, Varuna, synthetic_batch
@@ -35,7 +34,7 @@ def main():
             else:
                 res = v.step(b)
             out.append(res.loss if res.loss is not None else 0.0)
-        t = torch.tensor(out, device="cuda", dtype=torch.float64)
+        t = torch.tensor(out, device=dev, dtype=torch.float64)
         dist.all_reduce(t)   # the last stage (rank 1) holds the losses
         losses[retune] = t.tolist()
         v.close()

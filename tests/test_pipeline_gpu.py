@@ -7,6 +7,7 @@ per-tensor gradient relative L2 <= 3e-2; weights after one AdamW step
 relative L2 <= 1e-2 (of the update-carrying tensors). Dropout p = 0.
 """
 
+import math
 import os
 import subprocess
 import sys
@@ -106,6 +107,36 @@ def test_bert_single_gpu_loss_and_grads():
         assert rel(g, og[name]) < 3e-2, (name, rel(g, og[name]))
 
 
+def test_partial_minibatch_and_loss_scale():
+    """M_total not divisible by m*D (sp/planner.py:99-103: N_m = ceil(M/(m*D)),
+    the last micro-batch partial): the loss is the mean over M_total samples
+    and the gradients match the oracle's; with a loss scale of 1024 the
+    reported loss is unscaled and the stored gradients carry the scale."""
+    from paper_2111_04007_b200 import ParallelConfig
+    from paper_2111_04007_b200.model import CONFIGS
+    from paper_2111_04007_b200.runtime import Varuna, synthetic_batch
+    from oracle.gpt2_fp32 import PipelineOracle
+    cfg = CONFIGS["tiny"]
+    m, N, M, scale = 4, 4, 14, 1024.0
+    pc = ParallelConfig(1, 1, m, N, (0,) * cfg.n_layer)
+    batch = synthetic_batch(cfg, M, 0)
+    v = Varuna(cfg, pc, seed=0, global_batch=M, loss_scale=scale)
+    res = v.step(batch, apply=False)
+    torch.cuda.synchronize()
+    o = PipelineOracle(cfg.n_layer, cfg.hidden, cfg.heads, cfg.vocab_size, cfg.seq_len,
+                       pc.stage_map, m, N, seed=0)
+    loss = o.run_minibatch(batch["input_ids"], batch["labels"], M * cfg.seq_len)
+    assert abs(res.loss - loss) / abs(loss) < 5e-3, (res.loss, loss)
+    og = o.grads()
+    for name, g in v.param_tensors("grad").items():
+        assert rel(g / scale, og[name]) < 3e-2, (name, rel(g / scale, og[name]))
+    assert abs(res.grad_norm - math.sqrt(sum(float((t * t).sum()) for t in og.values()))) \
+        < 3e-2 * res.grad_norm
+    with pytest.raises(Exception):
+        Varuna(cfg, pc, seed=0, global_batch=12)   # would need only 3 micro-batches
+    v.close()
+
+
 def test_recompute_is_bitwise_forward():
     from paper_2111_04007_b200.model import CONFIGS, GPT2Stage, StageSpec
     cfg = CONFIGS["tiny"]
@@ -123,74 +154,6 @@ def test_loss_decreases_over_steps():
     v = Varuna(cfg, pc, seed=0, optimizer=AdamWConfig(lr=1e-3))
     losses = [v.step(batch).loss for _ in range(8)]
     assert losses[-1] < losses[0] - 0.1, losses
-
-
-@pytest.mark.multigpu
-@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
-                    reason="needs 2 GPUs")
-def test_two_stage_pipeline_matches_oracle():
-    env = dict(os.environ, PYTHONPATH=ROOT)
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr=127.0.0.1", "--master-port=29533",
-           os.path.join(ROOT, "tests", "dist_pipeline_check.py"), "--P", "2", "--D", "1"]
-    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
-    assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-4000:]
-    assert "PARITY OK" in p.stdout
-
-
-@pytest.mark.multigpu
-@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 4,
-                    reason="needs 4 GPUs")
-@pytest.mark.parametrize("P,D,config", [(2, 2, "tiny"), (4, 1, "tiny"), (2, 2, "tiny_bert")])
-def test_four_gpu_pipeline_matches_oracle(P, D, config):
-    env = dict(os.environ, PYTHONPATH=ROOT)
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4",
-           "--master-addr=127.0.0.1", f"--master-port={29541 + P + 7 * (config == 'tiny_bert')}",
-           os.path.join(ROOT, "tests", "dist_pipeline_check.py"), "--P", str(P), "--D", str(D),
-           "--config", config]
-    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
-    assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-4000:]
-    assert "PARITY OK" in p.stdout
-
-
-@pytest.mark.multigpu
-@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
-                    reason="needs 2 GPUs")
-def test_two_stage_opportunistic_dispatch():
-    env = dict(os.environ, PYTHONPATH=ROOT)
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr=127.0.0.1", "--master-port=29573",
-           os.path.join(ROOT, "tests", "dist_pipeline_check.py"), "--P", "2", "--D", "1",
-           "--dispatch", "opportunistic"]
-    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
-    assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-4000:]
-    assert "PARITY OK" in p.stdout
-
-
-@pytest.mark.multigpu
-@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
-                    reason="needs 2 GPUs")
-def test_retuned_dispatch_same_losses():
-    env = dict(os.environ, PYTHONPATH=ROOT)
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr=127.0.0.1", "--master-port=29575",
-           os.path.join(ROOT, "tests", "dist_retune_check.py")]
-    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
-    assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-4000:]
-    assert "RETUNE OK" in p.stdout
-
-
-@pytest.mark.multigpu
-@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
-                    reason="needs 2 GPUs")
-def test_morph_pipeline_to_data_parallel():
-    env = dict(os.environ, PYTHONPATH=ROOT)
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr=127.0.0.1", "--master-port=29571",
-           os.path.join(ROOT, "tests", "dist_morph_check.py")]
-    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
-    assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-4000:]
-    assert "MORPH OK" in p.stdout
 
 
 def test_gantt_export_format():
@@ -279,22 +242,3 @@ def test_bert_large_width_layer_matches_oracle():
     og = o.grads()
     for pname, g in v.param_tensors("grad").items():
         assert rel(g, og[pname]) < 3e-2, (pname, rel(g, og[pname]))
-
-
-@pytest.mark.multigpu
-@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 4,
-                    reason="needs 4 GPUs")
-@pytest.mark.parametrize("P,D,config,nproc", [(2, 1, "gpt2_355m", 2), (2, 2, "bert_large", 4)])
-def test_full_width_pipeline_matches_oracle(P, D, config, nproc):
-    """Two-layer cuts of the BASELINE widths through the real pipeline: the
-    boundary activations/gradients (m*s*h*2 bytes) cross GPUs over the P2P
-    path and replicas all-reduce, against the fp32 oracle."""
-    env = dict(os.environ, PYTHONPATH=ROOT)
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
-           f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1",
-           f"--master-port={29561 + nproc}",
-           os.path.join(ROOT, "tests", "dist_pipeline_check.py"), "--P", str(P), "--D", str(D),
-           "--config", config, "--layers", "2", "--micro-batch", "1", "--N", "2"]
-    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
-    assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-4000:]
-    assert "PARITY OK" in p.stdout
