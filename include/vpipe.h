@@ -163,6 +163,16 @@ int vp_attention_fwd(const void* qkv, void* o, float* lse, int64_t batch, int64_
 int vp_attention_bwd(const void* qkv, const void* o, const void* dout, const float* lse,
                      void* dqkv, float* delta_ws, int64_t batch, int64_t seq, int64_t heads,
                      int64_t head_dim, int causal, void* stream);
+/* As vp_attention_fwd with attention-probability dropout (K7): P[b,h,i,j] is
+ * kept iff the mask of element ((b*heads + h)*seq + i)*seq + j (see
+ * vp_dropout_dev) under the device-resident seed `*seed` and `salt` is set;
+ * the softmax normaliser and lse use the undropped P, kept probabilities are
+ * scaled by 1/(1-p). seq even when p > 0. Dropout is not in the reference
+ * (its compute is priced, sp/calibration.py:219-221); Varuna recomputes it
+ * bit-for-bit in R. */
+int vp_attention_fwd_ex(const void* qkv, void* o, float* lse, int64_t batch, int64_t seq,
+                        int64_t heads, int64_t head_dim, int causal, float p,
+                        const uint64_t* seed, uint32_t salt, void* stream);
 /* Workspace (fp32 elements) of vp_attention_bwd_ex: delta [B*H*S] + the fp32
  * dQ accumulator [B*S*H*D]. */
 int64_t vp_attention_bwd_ws_elems(int64_t batch, int64_t seq, int64_t heads, int64_t head_dim);
@@ -175,7 +185,10 @@ int64_t vp_attention_bwd_ws_elems(int64_t batch, int64_t seq, int64_t heads, int
 int vp_attention_bwd_ex(const void* qkv, const void* o, const void* dout, const float* lse,
                         void* dqkv, float* workspace, int64_t ws_elems, int64_t batch,
                         int64_t seq, int64_t heads, int64_t head_dim, int causal, int flags,
-                        float* dbias, void* stream);
+                        float p, const uint64_t* seed, uint32_t salt, float* dbias,
+                        void* stream);
+/* p > 0: attention-probability dropout of the forward call with the same
+ * (seed, salt) — see vp_attention_fwd_ex — differentiated through. */
 /* dbias (optional, fused path only, else VP_ERR_UNSUPPORTED): dbias[3*H*D]
  * += column sums of dqkv — the QKV bias gradient — from the dQ post-pass
  * and the dK/dV epilogue partials (fixed-order reductions). */
@@ -216,8 +229,37 @@ int64_t vp_bias_grad_ws_elems(int64_t cols);
 int vp_bias_grad(const void* dy, float* dbias, int64_t rows, int64_t cols, float* workspace,
                  void* stream);
 
-/* Philox-keyed dropout applied in place: x *= mask(seed, offset, i)/(1-p). */
+/* Hash-keyed dropout applied in place: x *= mask(seed, offset, i)/(1-p)
+ * (host seed; kept for callers outside the executor). */
 int vp_dropout(void* x, int64_t n, float p, uint64_t seed, uint64_t offset, void* stream);
+
+/* K7 dropout-recompute, graph-capturable. The 64-bit seed of the current
+ * (step, micro-batch) lives in DEVICE memory — written by vp_set_seed (a
+ * one-thread kernel outside any captured graph) before each schedule task —
+ * and every dropout site reads it there, keyed with a static per-site
+ * `salt`. Mask of element e of a site: b = fmix32(key ^ lo32(e/2)*0x9E3779B1
+ * ^ hi32(e/2)*0x85EBCA77), key = fmix32(lo32(seed) ^ fmix32(hi32(seed) ^
+ * fmix32(salt))); u = low 16 bits of b for even e, high for odd e; kept iff
+ * u >= thr = round(p * 65536), kept values scaled by 65536/(65536 - thr).
+ * So R(j) regenerates F(j)'s masks bit for bit (RNG state
+ * restored for recompute). */
+int vp_set_seed(uint64_t* dst, uint64_t value, void* stream);
+/* x[n] (bf16, n even) *= mask(e) in place, e = flat index. */
+int vp_dropout_dev(void* x, int64_t n, float p, const uint64_t* seed, uint32_t salt,
+                   void* stream);
+/* Backward of out = resid + dropout(y) for y[rows, cols]: gy = mask(g) (bf16,
+ * e = row*cols + col) and dbias[cols] += column sums of gy (fp32, fixed
+ * order; workspace as vp_bias_grad's). One pass over g. */
+int vp_dropout_bwd(const void* g, void* gy, int64_t rows, int64_t cols, float p,
+                   const uint64_t* seed, uint32_t salt, float* dbias, float* workspace,
+                   void* stream);
+/* D = resid + dropout(A op B^T + bias): the BIAS_RESID epilogue with the K7
+ * mask (e = row*N + col, N even) applied to the branch before the residual
+ * add; p = 0 is plain BIAS_RESID. flags as vp_gemm_bf16_ex. */
+int vp_gemm_bf16_dropout(int a_kmajor, int b_kmajor, const void* A, int64_t lda, const void* B,
+                         int64_t ldb, void* D, int64_t ldd, const void* bias, const void* resid,
+                         int64_t ldres, int64_t M, int64_t N, int64_t K, float p,
+                         const uint64_t* seed, uint32_t salt, int flags, void* stream);
 
 /* Residual add: y = a + b (bf16), n elements. */
 int vp_add(const void* a, const void* b, void* y, int64_t n, void* stream);

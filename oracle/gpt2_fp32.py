@@ -26,6 +26,7 @@ from __future__ import annotations
 import math
 from typing import Dict, List
 
+import numpy as np
 import torch
 
 from . import schedule as osch
@@ -78,27 +79,88 @@ def init_params(n_layer, hidden, vocab, seq, seed=0, init_std=0.02, arch="gpt2",
     return out
 
 
+# ------------------------------------------------------------------ dropout
+# Restatement of the K7 mask (include/vpipe.h vp_set_seed / vp_dropout_dev,
+# csrc/common.cuh drop_key / drop_bits) and of the executor's per-(step,
+# micro-batch) seed (paper_2111_04007_b200/runtime.py task_seed), so the
+# oracle draws exactly the GPU's masks. Dropout is not in the reference
+# (SPEC.md:18); its recompute-correctness requirement is PAPER.md:577.
+_M32 = np.uint64(0xFFFFFFFF)
+_M64 = (1 << 64) - 1
+
+
+def task_seed(seed: int, step: int, mb: int) -> int:
+    x = (seed * 0x9E3779B97F4A7C15 + step * 0xD1B54A32D192ED03 + mb * 0xBF58476D1CE4E5B9 + 1) & _M64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & _M64
+    return x ^ (x >> 31)
+
+
+def _fmix32(h):
+    """murmur3 finalizer on uint64 arrays holding 32-bit values."""
+    h = h ^ (h >> np.uint64(16))
+    h = (h * np.uint64(0x85EBCA6B)) & _M32
+    h = h ^ (h >> np.uint64(13))
+    h = (h * np.uint64(0xC2B2AE35)) & _M32
+    return h ^ (h >> np.uint64(16))
+
+
+def drop_threshold(p: float) -> int:
+    return min(65535, int(p * 65536.0 + 0.5))
+
+
+def drop_keep(seed64: int, salt: int, e: np.ndarray, p: float) -> np.ndarray:
+    """Keep flags of flat element indices ``e`` (uint64) at one call site."""
+    lo = np.uint64(seed64 & 0xFFFFFFFF)
+    hi = np.uint64(seed64 >> 32)
+    key = _fmix32(lo ^ _fmix32(hi ^ _fmix32(np.uint64(salt & 0xFFFFFFFF))))
+    pair = e >> np.uint64(1)
+    b = _fmix32(key ^ (((pair & _M32) * np.uint64(0x9E3779B1)) & _M32)
+                ^ (((pair >> np.uint64(32)) * np.uint64(0x85EBCA77)) & _M32))
+    u = np.where((e & np.uint64(1)) == 1, b >> np.uint64(16), b & np.uint64(0xFFFF))
+    return u >= np.uint64(drop_threshold(p))
+
+
+def dropout(x: torch.Tensor, p: float, seed64, salt: int) -> torch.Tensor:
+    """x * mask / (1 - p) over the flat (row-major) element index."""
+    if p <= 0 or seed64 is None:
+        return x
+    thr = drop_threshold(p)
+    e = np.arange(x.numel(), dtype=np.uint64)
+    keep = torch.from_numpy(drop_keep(seed64, salt, e, p)).view(x.shape)
+    return x * keep.to(x.dtype) * (65536.0 / (65536 - thr))
+
+
 def gelu(x):
     return 0.5 * x * (1.0 + torch.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3)))
 
 
-def layer_forward_post(p, li, x, B, S, H, eps=1e-12):
-    """BERT post-LN layer (bidirectional attention)."""
+# dropout call-site salts (paper_2111_04007_b200/model.py drop_salt)
+def _salt(li, site):
+    return li * 4 + site
+
+
+SALT_EMBED = 0x7FFFFFF0
+
+
+def layer_forward_post(p, li, x, B, S, H, eps=1e-12, drop=0.0, seed64=None):
+    """BERT post-LN layer (bidirectional attention); hidden dropout on the
+    proj / FC2 branches, attention-probability dropout."""
     h = x.shape[-1]
     D = h // H
     pre = f"l{li}."
     qkv = x @ p[pre + "w_qkv"].t() + p[pre + "b_qkv"]
     q, k, v = qkv.view(B, S, 3, H, D).permute(2, 0, 3, 1, 4)
     s = q @ k.transpose(-1, -2) / math.sqrt(D)
-    o = (s.softmax(-1) @ v).permute(0, 2, 1, 3).reshape(B * S, h)
-    y1 = x + o @ p[pre + "w_o"].t() + p[pre + "b_o"]
+    o = (dropout(s.softmax(-1), drop, seed64, _salt(li, 0)) @ v).permute(0, 2, 1, 3).reshape(B * S, h)
+    y1 = x + dropout(o @ p[pre + "w_o"].t() + p[pre + "b_o"], drop, seed64, _salt(li, 1))
     x1 = torch.nn.functional.layer_norm(y1, (h,), p[pre + "ln1_g"], p[pre + "ln1_b"], eps)
     f = gelu(x1 @ p[pre + "w_fc1"].t() + p[pre + "b_fc1"])
-    y2 = x1 + f @ p[pre + "w_fc2"].t() + p[pre + "b_fc2"]
+    y2 = x1 + dropout(f @ p[pre + "w_fc2"].t() + p[pre + "b_fc2"], drop, seed64, _salt(li, 2))
     return torch.nn.functional.layer_norm(y2, (h,), p[pre + "ln2_g"], p[pre + "ln2_b"], eps)
 
 
-def layer_forward(p, li, x, B, S, H, eps=1e-5):
+def layer_forward(p, li, x, B, S, H, eps=1e-5, drop=0.0, seed64=None):
     h = x.shape[-1]
     D = h // H
     pre = f"l{li}."
@@ -108,18 +170,18 @@ def layer_forward(p, li, x, B, S, H, eps=1e-5):
     s = q @ k.transpose(-1, -2) / math.sqrt(D)
     mask = torch.ones(S, S, dtype=torch.bool).triu(1)
     s = s.masked_fill(mask, float("-inf"))
-    o = (s.softmax(-1) @ v).permute(0, 2, 1, 3).reshape(B * S, h)
-    x1 = x + o @ p[pre + "w_o"].t() + p[pre + "b_o"]
+    o = (dropout(s.softmax(-1), drop, seed64, _salt(li, 0)) @ v).permute(0, 2, 1, 3).reshape(B * S, h)
+    x1 = x + dropout(o @ p[pre + "w_o"].t() + p[pre + "b_o"], drop, seed64, _salt(li, 1))
     c = torch.nn.functional.layer_norm(x1, (h,), p[pre + "ln2_g"], p[pre + "ln2_b"], eps)
     f = gelu(c @ p[pre + "w_fc1"].t() + p[pre + "b_fc1"])
-    return x1 + f @ p[pre + "w_fc2"].t() + p[pre + "b_fc2"]
+    return x1 + dropout(f @ p[pre + "w_fc2"].t() + p[pre + "b_fc2"], drop, seed64, _salt(li, 2))
 
 
 class PipelineOracle:
     """Sequential execution of a P-stage Varuna pipeline on CPU fp32."""
 
     def __init__(self, n_layer, hidden, heads, vocab, seq, stage_map, micro_batch, n_micro,
-                 seed=0, arch="gpt2"):
+                 seed=0, arch="gpt2", dropout=0.0):
         self.L, self.h, self.H, self.V, self.S = n_layer, hidden, heads, vocab, seq
         self.arch = arch
         self.eps = 1e-12 if arch == "bert" else 1e-5
@@ -130,6 +192,8 @@ class PipelineOracle:
                        for k, v in init_params(n_layer, hidden, vocab, seq, seed,
                                                arch=arch).items()}
         self.layers = [[i for i, s in enumerate(stage_map) if s == k] for k in range(self.P)]
+        self.seed, self.drop = seed, dropout
+        self._seed64 = None   # of the micro-batch being run
 
     def _stage_forward(self, k, x_or_ids, types=None):
         p = self.params
@@ -139,13 +203,16 @@ class PipelineOracle:
             if self.arch == "bert":
                 x = x + p["tte"][types]
                 x = torch.nn.functional.layer_norm(x, (self.h,), p["lne_g"], p["lne_b"], self.eps)
+            x = dropout(x, self.drop, self._seed64, SALT_EMBED)
         else:
             x = x_or_ids
         for li in self.layers[k]:
             if self.arch == "bert":
-                x = layer_forward_post(p, li, x, self.m, self.S, self.H, self.eps)
+                x = layer_forward_post(p, li, x, self.m, self.S, self.H, self.eps, self.drop,
+                                       self._seed64)
             else:
-                x = layer_forward(p, li, x, self.m, self.S, self.H)
+                x = layer_forward(p, li, x, self.m, self.S, self.H, drop=self.drop,
+                                  seed64=self._seed64)
         return x
 
     def _head_loss(self, x, labels, scale):
@@ -162,9 +229,11 @@ class PipelineOracle:
         l = torch.nn.functional.cross_entropy(logits, labels, ignore_index=-100, reduction="sum")
         return l * scale
 
-    def run_minibatch(self, ids, labels, total_tokens, types=None):
+    def run_minibatch(self, ids, labels, total_tokens, types=None, step=1, replica=0):
         """ids/labels: [N*m, S] int64. Returns the (scaled) loss; grads are
-        accumulated in ``self.params[*].grad`` in schedule order."""
+        accumulated in ``self.params[*].grad`` in schedule order. With
+        dropout, micro-batch j of ``replica`` in training step ``step`` draws
+        the executor's masks (seed task_seed(seed, step, replica*N + j))."""
         P, N = self.P, self.N
         plan = osch.varuna_plan(P, N, 1_000_000, 2_000_000, 1_000_000)
         order = _global_order(plan, P)
@@ -189,6 +258,7 @@ class PipelineOracle:
         loss = 0.0
         for k, kind, j in order:
             last = k == P - 1
+            self._seed64 = task_seed(self.seed, step, replica * N + j) if self.drop > 0 else None
             inp = ids[j] if k == 0 else act[(k, j)]
             tj = types[j] if (types is not None and k == 0) else None
             if kind == osch.F and not last:

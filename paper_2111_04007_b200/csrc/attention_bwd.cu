@@ -88,13 +88,16 @@ __device__ __forceinline__ float warp_colsum32(const float (&v)[32], uint32_t la
 // TMEM columns (512, one CTA per SM):
 //   [0,128) S^T   [128,256) dP^T   [256,320) dV   [320,384) dK   [384,448) dQ
 //   [448,512) P^T as packed bf16x2 (A operand of the dV MMA)
-template <bool CAUSAL>
+// DROP (K7 attention dropout, mask as the forward's): the dV MMA consumes the
+// dropped P^T (the 1/(1-p) scale applied to dV at the end), dS^T = P^T *
+// (mask * dP^T / (1-p) - delta).
+template <bool CAUSAL, bool DROP>
 __global__ void __launch_bounds__(FB_THREADS, 1)
     attn_bwd_fused(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
                    const __grid_constant__ CUtensorMap tmDQ, const float* __restrict__ lse,
                    const float* __restrict__ delta, __nv_bfloat16* __restrict__ dqkv, int S, int H,
                    int BH, int bh_chunk, float scale_log2, float scale,
-                   float* __restrict__ dq_acc, float* __restrict__ kv_part) {
+                   float* __restrict__ dq_acc, float* __restrict__ kv_part, AttnDrop drop) {
   using L = FbSmem;
   constexpr int D = FB_D;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -279,6 +282,8 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
     const uint32_t trow = (qd * 32) << 16;
     const uint32_t rowG = smem_u32(smem + L::DST_OFF + r * 128);
     const uint32_t lv_base = smem_u32(sv);
+    uint32_t dkey = 0;
+    if constexpr (DROP) dkey = drop_key(drop.seed, drop.salt);
 
     // P^T, dS^T for 32 query columns starting at q0c into packed bf16x2 words
     auto softmax_grad = [&](auto masked, const uint32_t (&rs)[32], const uint32_t (&rd)[32],
@@ -299,8 +304,17 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
             const int q = q0c + i;
             pv = (q >= qlo && q < S) ? pv : 0.f;
           }
-          p[t] = pv;
-          gr[t] = pv * (__uint_as_float(rd[i]) - dq[t]);
+          if constexpr (DROP) {
+            // element (query q0c+i, this key); thread = key: one hash each
+            const uint64_t e = (static_cast<uint64_t>(bh) * S + (q0c + i)) * S + key;
+            const uint32_t bits = drop_bits(dkey, e >> 1);
+            const bool keep = ((key & 1) ? (bits >> 16) : (bits & 0xFFFFu)) >= drop.thr;
+            p[t] = keep ? pv : 0.f;
+            gr[t] = pv * ((keep ? __uint_as_float(rd[i]) * drop.scale : 0.f) - dq[t]);
+          } else {
+            p[t] = pv;
+            gr[t] = pv * (__uint_as_float(rd[i]) - dq[t]);
+          }
         }
         const __nv_bfloat162 p01 = __floats2bfloat162_rn(p[0], p[1]);
         const __nv_bfloat162 p23 = __floats2bfloat162_rn(p[2], p[3]);
@@ -372,7 +386,7 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         fk[i] = key < S ? __uint_as_float(rk[i]) * scale : 0.f;
-        fv[i] = key < S ? __uint_as_float(rv[i]) : 0.f;
+        fv[i] = key < S ? __uint_as_float(rv[i]) * (DROP ? drop.scale : 1.f) : 0.f;
       }
       if (key < S) {
         __nv_bfloat16* row = dqkv + (static_cast<int64_t>(b) * S + key) * (3 * Hd) + h * D + c;
@@ -595,10 +609,11 @@ __global__ void __launch_bounds__(1024) kv_bias_reduce(const float* __restrict__
   }
 }
 
-template <bool CAUSAL>
+template <bool CAUSAL, bool DROP>
 int fused_t(const void* qkv, const void* o, const void* dout, const float* lse, float* delta,
             float* dq_acc, void* dqkv, int64_t B, int64_t S, int64_t H, float* dbias,
-            float* part_ws, unsigned* counters, float* kv_part, cudaStream_t st) {
+            float* part_ws, unsigned* counters, float* kv_part, const AttnDrop& drop,
+            cudaStream_t st) {
   using L = FbSmem;
   constexpr int D = FB_D;
   const int64_t tokens = B * S;
@@ -608,7 +623,7 @@ int fused_t(const void* qkv, const void* o, const void* dout, const float* lse, 
       !make_tmap_bsc(&tdo, dout, H * D, S, B, 128) ||
       !make_tmap_bsc_f32(&tdq, dq_acc, H * D, S, B, 32))
     return VP_ERR_UNSUPPORTED;
-  auto k = attn_bwd_fused<CAUSAL>;
+  auto k = attn_bwd_fused<CAUSAL, DROP>;
   if (cudaError_t e = smem_optin(k, L::TOTAL); e != cudaSuccess) return e;
   const int64_t rows = tokens * H;
   attn_delta_zero_kernel<<<static_cast<unsigned>((rows * (D / 8) + 255) / 256), 256, 0, st>>>(
@@ -622,7 +637,8 @@ int fused_t(const void* qkv, const void* o, const void* dout, const float* lse, 
   const int bh_chunk = std::max(1, std::min(BH, env_chunk > 0 ? env_chunk : 128));
   k<<<static_cast<unsigned>(n_kb * BH), FB_THREADS, L::TOTAL, st>>>(
       tq, tdo, tdq, lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), static_cast<int>(S),
-      static_cast<int>(H), BH, bh_chunk, scale_log2, scale, dq_acc, dbias ? kv_part : nullptr);
+      static_cast<int>(H), BH, bh_chunk, scale_log2, scale, dq_acc, dbias ? kv_part : nullptr,
+      drop);
   if (!dbias) {
     dq_convert_kernel<<<static_cast<unsigned>((tokens * Hd / 8 + 255) / 256), 256, 0, st>>>(
         dq_acc, reinterpret_cast<__nv_bfloat16*>(dqkv), tokens, Hd, scale);
@@ -657,16 +673,17 @@ bool attention_bwd_fused_ok(int64_t D) { return D == FB_D; }
 
 int attention_bwd_fused(const void* qkv, const void* o, const void* dout, const float* lse,
                         void* dqkv, float* ws, int64_t B, int64_t S, int64_t H, int causal,
-                        float* dbias, cudaStream_t st) {
+                        float* dbias, const AttnDrop& drop, cudaStream_t st) {
   float* delta = ws;
   float* dq_acc = delta + al4(B * H * S);
   float* part_ws = dq_acc + al4(B * S * H * FB_D);
   unsigned* counters = reinterpret_cast<unsigned*>(part_ws + al4(kConvParts * H * FB_D));
   float* kv_part = reinterpret_cast<float*>(counters) + 64;
-  return causal ? fused_t<true>(qkv, o, dout, lse, delta, dq_acc, dqkv, B, S, H, dbias, part_ws,
-                                counters, kv_part, st)
-                : fused_t<false>(qkv, o, dout, lse, delta, dq_acc, dqkv, B, S, H, dbias, part_ws,
-                                 counters, kv_part, st);
+#define FT(C, DR) fused_t<C, DR>(qkv, o, dout, lse, delta, dq_acc, dqkv, B, S, H, dbias, part_ws, \
+                                 counters, kv_part, drop, st)
+  if (drop.seed) return causal ? FT(true, true) : FT(false, true);
+  return causal ? FT(true, false) : FT(false, false);
+#undef FT
 }
 
 }  // namespace vp

@@ -63,11 +63,15 @@ __device__ unsigned long long g_vp_ftrace[4][32][8];
 #else
 #define TRF(j, slot) do {} while (0)
 #endif
-template <int D, bool CAUSAL>
+// Attention-probability dropout (K7, DROP; AttnDrop in common.cuh): P_ij is
+// kept iff the mask bit of element ((b*H + h)*S + i)*S + j is set; the row
+// sum l (and the LSE) use the undropped P, the 1/(1-p) scale is folded into
+// the final O = acc * scale / l.
+template <int D, bool CAUSAL, bool DROP>
 __global__ void __launch_bounds__(TA_THREADS, 2)
     attn_fwd_tc(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmKV,
                 __nv_bfloat16* __restrict__ out,
-                float* __restrict__ lse, int S, int H, int n_qb, float scale_log2) {
+                float* __restrict__ lse, int S, int H, int n_qb, float scale_log2, AttnDrop drop) {
   using L = TaSmem<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -199,6 +203,8 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
     const uint32_t tO = tmem + trow + 128;
     uint8_t* sP = smem + L::P_OFF;
     float m = -FLT_MAX, l = 0.f;
+    uint32_t dkey = 0;
+    if constexpr (DROP) dkey = drop_key(drop.seed, drop.salt);
     if constexpr (L::QT) {
       // Q row r (128 B, swizzled in smem) -> TMEM as the A operand of S = Q K^T
       mbar_wait(q_full, 0);
@@ -265,6 +271,7 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
       // P = exp2(s*scale - m), row sum
       float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       uint4 pk[TA_BN / 8];
+      const uint64_t dpair = (((static_cast<uint64_t>(bh) * S + q) * S) + k0) >> 1;
 #pragma unroll
       for (int g = 0; g < TA_BN / 8; ++g) {
         float f[8];
@@ -272,6 +279,14 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
         for (int t = 0; t < 8; ++t) {
           f[t] = fast_exp2(fmaf(__uint_as_float(sc[g * 8 + t]), scale_log2, -m_new));
           ps[t] += f[t];
+        }
+        if constexpr (DROP) {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const uint32_t kk = drop_keep2(dkey, dpair + g * 4 + t, drop.thr);
+            f[2 * t] = (kk & 1u) ? f[2 * t] : 0.f;
+            f[2 * t + 1] = (kk & 2u) ? f[2 * t + 1] : 0.f;
+          }
         }
         pk[g] = pack8(f);
       }
@@ -319,7 +334,7 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
     }
     mbar_wait(&o_full[(n_kb - 1) & 1], ((n_kb - 1) >> 1) & 1);
     tc_fence_after();
-    const float inv = 1.f / l;
+    const float inv = (DROP ? drop.scale : 1.f) / l;
     __nv_bfloat16* orow = out + (static_cast<int64_t>(b) * S + q) * Hd + h * D;
 #pragma unroll 1
     for (int c = 0; c < D; c += 32) {
@@ -391,13 +406,13 @@ struct TbSmem {
   static constexpr int TMEM_Q = NB * 128 + D <= 256 ? 256 : 512;       // dq allocation
 };
 
-template <int D, bool CAUSAL>
+template <int D, bool CAUSAL, bool DROP>
 __global__ void __launch_bounds__(TB_THREADS, TbSmem<D>::MINB)
     attn_bwd_dkdv_tc(const __grid_constant__ CUtensorMap tmQKV128,
                      const __grid_constant__ CUtensorMap tmQKV64,
                      const __grid_constant__ CUtensorMap tmDO64, const float* __restrict__ lse,
                      const float* __restrict__ delta, __nv_bfloat16* __restrict__ dqkv, int S,
-                     int H, float scale_log2, float scale) {
+                     int H, float scale_log2, float scale, AttnDrop drop) {
   using L = TbSmem<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -558,6 +573,8 @@ __global__ void __launch_bounds__(TB_THREADS, TbSmem<D>::MINB)
     const int key = k0 + r;
     const int qlo = CAUSAL ? key : 0;
     const uint32_t trow = (qd * 32) << 16;
+    uint32_t dkey = 0;
+    if constexpr (DROP) dkey = drop_key(drop.seed, drop.salt);
     for (int it = 0; it < n_it; ++it) {
       const int st = it % NB;
       const int qi = (i0 + it) * TB_N;
@@ -598,8 +615,18 @@ __global__ void __launch_bounds__(TB_THREADS, TbSmem<D>::MINB)
               const int qq = qi + c + i;
               pv = (qq >= qlo && qq < S) ? pv : 0.f;
             }
-            fp[t] = pv;
-            fg[t] = pv * (__uint_as_float(rd[i]) - dq[t]);
+            if constexpr (DROP) {
+              // element (query qi+c+i, this key): thread = key, so one hash
+              // per element (the mask pairs adjacent keys)
+              const uint64_t e = (static_cast<uint64_t>(bh) * S + (qi + c + i)) * S + key;
+              const uint32_t bits = drop_bits(dkey, e >> 1);
+              const bool keep = ((key & 1) ? (bits >> 16) : (bits & 0xFFFFu)) >= drop.thr;
+              fp[t] = keep ? pv : 0.f;
+              fg[t] = pv * ((keep ? __uint_as_float(rd[i]) * drop.scale : 0.f) - dq[t]);
+            } else {
+              fp[t] = pv;
+              fg[t] = pv * (__uint_as_float(rd[i]) - dq[t]);
+            }
           }
           const int chunk = (c >> 3) + g;
           const int sw = (chunk ^ (r & 7)) << 4;
@@ -630,7 +657,7 @@ __global__ void __launch_bounds__(TB_THREADS, TbSmem<D>::MINB)
 #pragma unroll
           for (int t = 0; t < 8; ++t) {
             fk[t] = n_it > 0 ? __uint_as_float(rk[i + t]) * scale : 0.f;
-            fv[t] = n_it > 0 ? __uint_as_float(rv[i + t]) : 0.f;
+            fv[t] = n_it > 0 ? __uint_as_float(rv[i + t]) * (DROP ? drop.scale : 1.f) : 0.f;
           }
           *reinterpret_cast<uint4*>(row + Hd + h * D + c + i) = pack8(fk);
           *reinterpret_cast<uint4*>(row + 2 * Hd + h * D + c + i) = pack8(fv);
@@ -646,13 +673,13 @@ __global__ void __launch_bounds__(TB_THREADS, TbSmem<D>::MINB)
   }
 }
 
-template <int D, bool CAUSAL>
+template <int D, bool CAUSAL, bool DROP>
 __global__ void __launch_bounds__(TB_THREADS, TbSmem<D>::MINB)
     attn_bwd_dq_tc(const __grid_constant__ CUtensorMap tmQKV128,
                    const __grid_constant__ CUtensorMap tmQKV64,
                    const __grid_constant__ CUtensorMap tmDO128, const float* __restrict__ lse,
                    const float* __restrict__ delta, __nv_bfloat16* __restrict__ dqkv, int S, int H,
-                   int n_qb, float scale_log2, float scale) {
+                   int n_qb, float scale_log2, float scale, AttnDrop drop) {
   using L = TbSmem<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -776,6 +803,8 @@ __global__ void __launch_bounds__(TB_THREADS, TbSmem<D>::MINB)
     const int lim = CAUSAL ? min(S, q + 1) : S;
     const float lrow = q < S ? lse[static_cast<int64_t>(bh) * S + q] : 0.f;
     const float drow = q < S ? delta[static_cast<int64_t>(bh) * S + q] : 0.f;
+    uint32_t dkey = 0;
+    if constexpr (DROP) dkey = drop_key(drop.seed, drop.salt);
     for (int j = 0; j < n_kb; ++j) {
       const int st = j % NB;
       const int kj = j * TB_N;
@@ -797,6 +826,17 @@ __global__ void __launch_bounds__(TB_THREADS, TbSmem<D>::MINB)
         if (need_mask) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) pv[i] = (kj + c + i < lim) ? pv[i] : 0.f;
+        }
+        if constexpr (DROP) {
+          // dP = mask * dP_dropped / (1 - p); thread = query: pairs of keys
+          const uint64_t p0 = ((static_cast<uint64_t>(bh) * S + q) * S + kj + c) >> 1;
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            const uint32_t kk = drop_keep2(dkey, p0 + t, drop.thr);
+            rd[2 * t] = __float_as_uint((kk & 1u) ? __uint_as_float(rd[2 * t]) * drop.scale : 0.f);
+            rd[2 * t + 1] =
+                __float_as_uint((kk & 2u) ? __uint_as_float(rd[2 * t + 1]) * drop.scale : 0.f);
+          }
         }
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
@@ -844,17 +884,17 @@ __global__ void __launch_bounds__(TB_THREADS, TbSmem<D>::MINB)
   }
 }
 
-template <int D, bool CAUSAL>
+template <int D, bool CAUSAL, bool DROP>
 int bwd_tc_t(const void* qkv, const void* dout, const float* lse, const float* delta, void* dqkv,
-             int64_t B, int64_t S, int64_t H, cudaStream_t st) {
+             int64_t B, int64_t S, int64_t H, const AttnDrop& drop, cudaStream_t st) {
   using L = TbSmem<D>;
   CUtensorMap q128, q64, do64, do128;
   const uint64_t cols = 3 * H * D;
   if (!make_tmap_bsc(&q128, qkv, cols, S, B, 128) || !make_tmap_bsc(&q64, qkv, cols, S, B, 64) ||
       !make_tmap_bsc(&do64, dout, H * D, S, B, 64) || !make_tmap_bsc(&do128, dout, H * D, S, B, 128))
     return VP_ERR_UNSUPPORTED;
-  auto k1 = attn_bwd_dkdv_tc<D, CAUSAL>;
-  auto k2 = attn_bwd_dq_tc<D, CAUSAL>;
+  auto k1 = attn_bwd_dkdv_tc<D, CAUSAL, DROP>;
+  auto k2 = attn_bwd_dq_tc<D, CAUSAL, DROP>;
   if (cudaError_t e = smem_optin(k1, L::TOTAL); e != cudaSuccess) return e;
   if (cudaError_t e = smem_optin(k2, L::TOTAL); e != cudaSuccess) return e;
   const float scale = 1.f / sqrtf(static_cast<float>(D));
@@ -862,47 +902,55 @@ int bwd_tc_t(const void* qkv, const void* dout, const float* lse, const float* d
   const int n_kb = static_cast<int>((S + TB_M - 1) / TB_M);
   k1<<<dim3(n_kb, static_cast<unsigned>(B * H)), TB_THREADS, L::TOTAL, st>>>(
       q128, q64, do64, lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), static_cast<int>(S),
-      static_cast<int>(H), scale_log2, scale);
+      static_cast<int>(H), scale_log2, scale, drop);
   const int n_qb = static_cast<int>((S + TB_M - 1) / TB_M);
   k2<<<dim3(n_qb, static_cast<unsigned>(B * H)), TB_THREADS, L::TOTAL, st>>>(
       q128, q64, do128, lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), static_cast<int>(S),
-      static_cast<int>(H), n_qb, scale_log2, scale);
+      static_cast<int>(H), n_qb, scale_log2, scale, drop);
   return launch_status();
 }
 
+template <int D>
+int bwd_tc_d(const void* qkv, const void* dout, const float* lse, const float* delta, void* dqkv,
+             int64_t B, int64_t S, int64_t H, int causal, const AttnDrop& dr, cudaStream_t st) {
+  if (dr.seed)
+    return causal ? bwd_tc_t<D, true, true>(qkv, dout, lse, delta, dqkv, B, S, H, dr, st)
+                  : bwd_tc_t<D, false, true>(qkv, dout, lse, delta, dqkv, B, S, H, dr, st);
+  return causal ? bwd_tc_t<D, true, false>(qkv, dout, lse, delta, dqkv, B, S, H, dr, st)
+                : bwd_tc_t<D, false, false>(qkv, dout, lse, delta, dqkv, B, S, H, dr, st);
+}
 }  // namespace
 
 int attention_bwd_tc(const void* qkv, const void* dout, const float* lse, const float* delta,
                      void* dqkv, int64_t B, int64_t S, int64_t H, int64_t D, int causal,
-                     cudaStream_t st) {
+                     float p, const uint64_t* seed, uint32_t salt, cudaStream_t st) {
   if ((3 * H * D) % 8) return VP_ERR_UNSUPPORTED;
+  const AttnDrop dr = make_attn_drop(p, seed, salt);
+  if (dr.seed && (S & 1)) return VP_ERR_UNSUPPORTED;
   switch (D) {
-    case 64: return causal ? bwd_tc_t<64, true>(qkv, dout, lse, delta, dqkv, B, S, H, st)
-                           : bwd_tc_t<64, false>(qkv, dout, lse, delta, dqkv, B, S, H, st);
-    case 96: return causal ? bwd_tc_t<96, true>(qkv, dout, lse, delta, dqkv, B, S, H, st)
-                           : bwd_tc_t<96, false>(qkv, dout, lse, delta, dqkv, B, S, H, st);
-    case 128: return causal ? bwd_tc_t<128, true>(qkv, dout, lse, delta, dqkv, B, S, H, st)
-                            : bwd_tc_t<128, false>(qkv, dout, lse, delta, dqkv, B, S, H, st);
+    case 64: return bwd_tc_d<64>(qkv, dout, lse, delta, dqkv, B, S, H, causal, dr, st);
+    case 96: return bwd_tc_d<96>(qkv, dout, lse, delta, dqkv, B, S, H, causal, dr, st);
+    case 128: return bwd_tc_d<128>(qkv, dout, lse, delta, dqkv, B, S, H, causal, dr, st);
     default: return VP_ERR_UNSUPPORTED;
   }
 }
 
 namespace {
-template <int D, bool CAUSAL>
+template <int D, bool CAUSAL, bool DROP>
 int fwd_tc_t(const void* qkv, void* o, float* lse, int64_t B, int64_t S, int64_t H,
-             cudaStream_t st) {
+             const AttnDrop& drop, cudaStream_t st) {
   using L = TaSmem<D>;
   CUtensorMap tm, tkv;
   if (!make_tmap_bsc(&tm, qkv, 3 * H * D, S, B, 128)) return VP_ERR_UNSUPPORTED;
   if (!make_tmap_bsc(&tkv, qkv, 3 * H * D, S, B, TA_BN)) return VP_ERR_UNSUPPORTED;
-  auto k = attn_fwd_tc<D, CAUSAL>;
+  auto k = attn_fwd_tc<D, CAUSAL, DROP>;
   if (cudaError_t e = smem_optin(k, L::TOTAL); e != cudaSuccess) return e;
   const int n_qb = static_cast<int>((S + TA_BM - 1) / TA_BM);
   dim3 grid(n_qb, static_cast<unsigned>(B * H));
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(D));
   k<<<grid, TA_THREADS, L::TOTAL, st>>>(tm, tkv, reinterpret_cast<__nv_bfloat16*>(o), lse,
                                         static_cast<int>(S), static_cast<int>(H), n_qb,
-                                        scale_log2);
+                                        scale_log2, drop);
   return launch_status();
 }
 
@@ -913,16 +961,28 @@ extern "C" int vp_debug_fwd_trace(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, g_vp_ftrace, sizeof(g_vp_ftrace));
 }
 #endif
+namespace {
+template <int D>
+int fwd_tc_d(const void* qkv, void* o, float* lse, int64_t B, int64_t S, int64_t H, int causal,
+             const AttnDrop& dr, cudaStream_t st) {
+  if (dr.seed)
+    return causal ? fwd_tc_t<D, true, true>(qkv, o, lse, B, S, H, dr, st)
+                  : fwd_tc_t<D, false, true>(qkv, o, lse, B, S, H, dr, st);
+  return causal ? fwd_tc_t<D, true, false>(qkv, o, lse, B, S, H, dr, st)
+                : fwd_tc_t<D, false, false>(qkv, o, lse, B, S, H, dr, st);
+}
+}  // namespace
+
 int attention_fwd_tc(const void* qkv, void* o, float* lse, int64_t B, int64_t S, int64_t H,
-                     int64_t D, int causal, cudaStream_t st) {
+                     int64_t D, int causal, float p, const uint64_t* seed, uint32_t salt,
+                     cudaStream_t st) {
   if ((3 * H * D) % 8) return VP_ERR_UNSUPPORTED;
+  const AttnDrop dr = make_attn_drop(p, seed, salt);
+  if (dr.seed && (S & 1)) return VP_ERR_UNSUPPORTED;
   switch (D) {
-    case 64: return causal ? fwd_tc_t<64, true>(qkv, o, lse, B, S, H, st)
-                           : fwd_tc_t<64, false>(qkv, o, lse, B, S, H, st);
-    case 96: return causal ? fwd_tc_t<96, true>(qkv, o, lse, B, S, H, st)
-                           : fwd_tc_t<96, false>(qkv, o, lse, B, S, H, st);
-    case 128: return causal ? fwd_tc_t<128, true>(qkv, o, lse, B, S, H, st)
-                            : fwd_tc_t<128, false>(qkv, o, lse, B, S, H, st);
+    case 64: return fwd_tc_d<64>(qkv, o, lse, B, S, H, causal, dr, st);
+    case 96: return fwd_tc_d<96>(qkv, o, lse, B, S, H, causal, dr, st);
+    case 128: return fwd_tc_d<128>(qkv, o, lse, B, S, H, causal, dr, st);
     default: return VP_ERR_UNSUPPORTED;
   }
 }

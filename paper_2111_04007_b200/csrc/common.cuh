@@ -92,6 +92,55 @@ __device__ __forceinline__ uint32_t hash_u32(uint64_t seed, uint64_t idx) {
   return static_cast<uint32_t>(x);
 }
 
+// ---------------------------------------------------------------- dropout
+// K7 dropout mask, regenerated bit-for-bit by recompute and by the backward.
+// The 64-bit seed of the current (step, micro-batch) is READ FROM DEVICE
+// MEMORY (written by vp_set_seed before each task), so captured CUDA graphs
+// replay with fresh masks; the per-call-site salt (layer, site) is static.
+// Element e of a call site's tensor: bits = fmix32(key ^ lo(e/2)*A ^ hi(e/2)*B),
+// its 16-bit half (low for even e, high for odd e) u; kept iff u >= thr,
+// thr = round(p * 65536); kept values are scaled by 65536 / (65536 - thr).
+// oracle/gpt2_fp32.py restates this function for the parity tests.
+__host__ __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
+  h ^= h >> 16;
+  h *= 0x85EBCA6Bu;
+  h ^= h >> 13;
+  h *= 0xC2B2AE35u;
+  h ^= h >> 16;
+  return h;
+}
+__device__ __forceinline__ uint32_t drop_key(const uint64_t* seed, uint32_t salt) {
+  const uint64_t s = *seed;
+  return fmix32(static_cast<uint32_t>(s) ^ fmix32(static_cast<uint32_t>(s >> 32) ^ fmix32(salt)));
+}
+__device__ __forceinline__ uint32_t drop_bits(uint32_t key, uint64_t pair) {
+  return fmix32(key ^ (static_cast<uint32_t>(pair) * 0x9E3779B1u) ^
+                (static_cast<uint32_t>(pair >> 32) * 0x85EBCA77u));
+}
+// keep flags of elements 2*pair (bit 0) and 2*pair + 1 (bit 1)
+__device__ __forceinline__ uint32_t drop_keep2(uint32_t key, uint64_t pair, uint32_t thr) {
+  const uint32_t b = drop_bits(key, pair);
+  return ((b & 0xFFFFu) >= thr ? 1u : 0u) | ((b >> 16) >= thr ? 2u : 0u);
+}
+inline uint32_t drop_threshold(float p) {
+  const double t = static_cast<double>(p) * 65536.0 + 0.5;
+  return t >= 65535.0 ? 65535u : static_cast<uint32_t>(t);
+}
+inline float drop_scale(uint32_t thr) { return 65536.f / static_cast<float>(65536u - thr); }
+
+// Attention-probability dropout of one call site (seed == nullptr: none).
+struct AttnDrop {
+  const uint64_t* seed;
+  uint32_t salt;
+  uint32_t thr;
+  float scale;
+};
+inline AttnDrop make_attn_drop(float p, const uint64_t* seed, uint32_t salt) {
+  if (p <= 0.f || !seed) return AttnDrop{nullptr, 0, 0, 1.f};
+  const uint32_t thr = drop_threshold(p);
+  return AttnDrop{seed, salt, thr, drop_scale(thr)};
+}
+
 inline int launch_status() {
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? VP_OK : static_cast<int>(e);

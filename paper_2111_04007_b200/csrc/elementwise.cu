@@ -310,11 +310,30 @@ __global__ void __launch_bounds__(512)
 // CTA of a column block to finish (arrival counter) adds the parts in a fixed
 // order, so the result does not depend on CTA timing. The counter is reset
 // by that CTA, so the workspace stays reusable (zero-filled once).
+// Dropout mask of 8 consecutive elements starting at flat index e0 (even),
+// applied in place to f (the backward of out = x + dropout(y): dy = mask(g)).
+__device__ __forceinline__ void drop8(float (&f)[8], uint32_t key, int64_t e0, uint32_t thr,
+                                      float scale) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t k = drop_keep2(key, static_cast<uint64_t>(e0 >> 1) + q, thr);
+    f[2 * q] = (k & 1u) ? f[2 * q] * scale : 0.f;
+    f[2 * q + 1] = (k & 2u) ? f[2 * q + 1] * scale : 0.f;
+  }
+}
+
+// DROP: the input is first passed through the dropout mask of call site
+// (seed, salt) and written to gy; the column sums are those of gy (the bias
+// gradient of a dropped-out branch). Otherwise gy is unused.
+template <bool DROP>
 __global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __restrict__ dy,
                                                      float* __restrict__ ws,
                                                      unsigned* __restrict__ counters,
                                                      float* __restrict__ out, int64_t rows,
-                                                     int64_t cols, int64_t rpp, int parts) {
+                                                     int64_t cols, int64_t rpp, int parts,
+                                                     __nv_bfloat16* __restrict__ gy,
+                                                     const uint64_t* __restrict__ seed,
+                                                     uint32_t salt, uint32_t thr, float scale) {
   __shared__ float sh[8][256 + 4];
   __shared__ bool is_last;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -323,6 +342,8 @@ __global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __rest
   const int64_t r0 = blockIdx.y * rpp;
   const int64_t r1 = min(rows, r0 + rpp);
   float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  uint32_t key = 0;
+  if constexpr (DROP) key = drop_key(seed, salt);
   if (c0 < cols) {
     int64_t r = r0 + ty;
     for (; r + 24 < r1; r += 32) {
@@ -333,6 +354,12 @@ __global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __rest
       for (int k = 0; k < 4; ++k) {
         float f[8];
         unpack8(u[k], f);
+        if constexpr (DROP) {
+          drop8(f, key, (r + 8 * k) * cols + c0, thr, scale);
+          const uint4 o = pack8(f);
+          *reinterpret_cast<uint4*>(gy + (r + 8 * k) * cols + c0) = o;
+          unpack8(o, f);   // sum what the GEMMs consume (bf16)
+        }
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[j] += f[j];
       }
@@ -340,6 +367,12 @@ __global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __rest
     for (; r < r1; r += 8) {
       float f[8];
       unpack8(*reinterpret_cast<const uint4*>(dy + r * cols + c0), f);
+      if constexpr (DROP) {
+        drop8(f, key, r * cols + c0, thr, scale);
+        const uint4 o = pack8(f);
+        *reinterpret_cast<uint4*>(gy + r * cols + c0) = o;
+        unpack8(o, f);
+      }
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[j] += f[j];
     }
@@ -402,6 +435,29 @@ __global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __rest
 }
 
 // ------------------------------------------------------------ dropout / add
+__global__ void set_seed_kernel(uint64_t* dst, uint64_t v) { *dst = v; }
+
+// in place, flat element index e (n even; 8 per thread)
+__global__ void dropout_dev_kernel(__nv_bfloat16* __restrict__ x, int64_t n,
+                                   const uint64_t* __restrict__ seed, uint32_t salt, uint32_t thr,
+                                   float scale) {
+  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 8;
+  if (i >= n) return;
+  const uint32_t key = drop_key(seed, salt);
+  if (i + 8 <= n) {
+    uint4* v = reinterpret_cast<uint4*>(x + i);
+    float f[8];
+    unpack8(*v, f);
+    drop8(f, key, i, thr, scale);
+    *v = pack8(f);
+  } else {
+    for (int64_t k = i; k < n; ++k) {
+      const uint32_t kk = drop_keep2(key, static_cast<uint64_t>(k >> 1), thr);
+      const float f = __bfloat162float(x[k]);
+      x[k] = __float2bfloat16((kk >> (k & 1)) & 1u ? f * scale : 0.f);
+    }
+  }
+}
 __global__ void dropout_kernel(__nv_bfloat16* __restrict__ x, int64_t n, float p, uint64_t seed,
                                uint64_t offset) {
   const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 8;
@@ -689,8 +745,49 @@ extern "C" int vp_bias_grad(const void* dy, float* dbias, int64_t rows, int64_t 
   parts = (rows + rpp - 1) / rpp;
   unsigned* counters = reinterpret_cast<unsigned*>(workspace);
   dim3 grid(static_cast<unsigned>(col_blocks), static_cast<unsigned>(parts));
-  colsum_kernel<<<grid, 256, 0, ST>>>(CBF(dy), workspace + kColsumCounters, counters, dbias,
-                                      rows, cols, rpp, static_cast<int>(parts));
+  colsum_kernel<false><<<grid, 256, 0, ST>>>(CBF(dy), workspace + kColsumCounters, counters,
+                                             dbias, rows, cols, rpp, static_cast<int>(parts),
+                                             nullptr, nullptr, 0, 0, 0.f);
+  return launch_status();
+}
+
+extern "C" int vp_set_seed(uint64_t* dst, uint64_t value, void* stream) {
+  if (!dst) return VP_ERR_ARGS;
+  set_seed_kernel<<<1, 1, 0, ST>>>(dst, value);
+  return launch_status();
+}
+
+extern "C" int vp_dropout_dev(void* x, int64_t n, float p, const uint64_t* seed, uint32_t salt,
+                              void* stream) {
+  if (n <= 0 || p < 0.f || p >= 1.f || !seed || (n & 1)) return VP_ERR_ARGS;
+  if (p == 0.f) return VP_OK;
+  const uint32_t thr = drop_threshold(p);
+  dropout_dev_kernel<<<blocks_for(n, 256 * 8), 256, 0, ST>>>(BF(x), n, seed, salt, thr,
+                                                             drop_scale(thr));
+  return launch_status();
+}
+
+extern "C" int vp_dropout_bwd(const void* g, void* gy, int64_t rows, int64_t cols, float p,
+                              const uint64_t* seed, uint32_t salt, float* dbias, float* workspace,
+                              void* stream) {
+  if (rows <= 0 || cols <= 0 || !seed || !workspace || p <= 0.f || p >= 1.f) return VP_ERR_ARGS;
+  if (cols % 8) return VP_ERR_UNSUPPORTED;
+  const int64_t col_blocks = (cols + 255) / 256;
+  if (col_blocks > kColsumCounters) return VP_ERR_UNSUPPORTED;
+  int64_t parts = (4 * static_cast<int64_t>(device_sms()) + col_blocks - 1) / col_blocks;
+  parts = std::min<int64_t>(parts, std::max<int64_t>(1, rows / 32));
+  parts = std::max<int64_t>(1, std::min<int64_t>(parts, kColsumMaxParts));
+  const int64_t rpp = (rows + parts - 1) / parts;
+  parts = (rows + rpp - 1) / rpp;
+  unsigned* counters = reinterpret_cast<unsigned*>(workspace);
+  const uint32_t thr = drop_threshold(p);
+  dim3 grid(static_cast<unsigned>(col_blocks), static_cast<unsigned>(parts));
+  // without dbias the column sums land in a workspace scratch row (unused)
+  float* out = dbias;
+  if (!out) return VP_ERR_ARGS;
+  colsum_kernel<true><<<grid, 256, 0, ST>>>(CBF(g), workspace + kColsumCounters, counters, out,
+                                            rows, cols, rpp, static_cast<int>(parts), BF(gy),
+                                            seed, salt, thr, drop_scale(thr));
   return launch_status();
 }
 

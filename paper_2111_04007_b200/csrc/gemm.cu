@@ -26,12 +26,36 @@ constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int kThreads = 256;
 
+// Dropout of the branch output before the residual add (BIAS_RESID only):
+// out = resid + dropout(acc + bias), mask of element (row, col) keyed by the
+// device-resident seed and the call site's salt (common.cuh, K7).
+struct EpiDrop {
+  const uint64_t* seed;   // nullptr: no dropout
+  uint32_t salt;
+  uint32_t thr;
+  float scale;
+};
+
+template <int NV>
+__device__ __forceinline__ void apply_drop(const EpiDrop& d, int64_t row, int64_t col0, int64_t N,
+                                           float (&v)[NV]) {
+  const uint32_t key = drop_key(d.seed, d.salt);
+  const uint64_t p0 = static_cast<uint64_t>(row * N + col0) >> 1;   // N, col0 even
+#pragma unroll
+  for (int q = 0; q < NV / 2; ++q) {
+    const uint32_t k = drop_keep2(key, p0 + q, d.thr);
+    v[2 * q] = (k & 1u) ? v[2 * q] * d.scale : 0.f;
+    v[2 * q + 1] = (k & 2u) ? v[2 * q + 1] * d.scale : 0.f;
+  }
+}
+
 struct EpiArgs {
   void* D;
   int64_t ldd;
   const __nv_bfloat16* bias;
   __nv_bfloat16* aux;
   int64_t ldaux;
+  EpiDrop drop;
 };
 
 template <int BN, int STAGES>
@@ -113,6 +137,9 @@ __device__ __forceinline__ void epilogue_chunk(const EpiArgs& e, int64_t row, in
           for (int i = 0; i < 32 && col0 + i < N; ++i) a[i] = __float2bfloat16(dg[i]);
         }
       }
+    }
+    if constexpr (EPI == VP_EPI_BIAS_RESID) {
+      if (e.drop.seed != nullptr) apply_drop(e.drop, row, col0, N, v);
     }
     if constexpr (EPI == VP_EPI_BIAS_RESID || EPI == VP_EPI_DGELU || EPI == VP_EPI_RESID) {
       const __nv_bfloat16* a = e.aux + row * e.ldaux + col0;
@@ -343,6 +370,7 @@ struct Epi2 {
   int64_t ldaux;
   int64_t group;                // rasterisation group (M tiles per N sweep)
   float* colsum_ws;             // optional: per-32-row partial column sums of D (fp32)
+  EpiDrop drop;                 // BIAS_RESID: dropout of the branch before the residual add
 };
 
 // Sum of v[0..63] over the 32 lanes (rows) of a warp, scattered so that lane
@@ -408,6 +436,9 @@ __device__ __forceinline__ void epi2_apply(const Epi2& e, int64_t row, int64_t c
 #pragma unroll
       for (int i = 0; i < 64; ++i) v[i] = gelu_tanh(__bfloat162float(__float2bfloat16(v[i])));
     }
+  }
+  if constexpr (EPI == VP_EPI_BIAS_RESID) {
+    if (e.drop.seed != nullptr) apply_drop(e.drop, row, col0, N, v);
   }
   if constexpr (EPI == VP_EPI_BIAS_RESID || EPI == VP_EPI_DGELU || EPI == VP_EPI_RESID) {
     // aux row values were staged in smem by TMA (see gemm2_kernel)
@@ -883,7 +914,8 @@ extern "C" int vp_device_sm_count(int* out) {
 static int gemm_entry(int a_kmajor, int b_kmajor, int epilogue, const void* A, int64_t lda,
                       const void* B, int64_t ldb, void* D, int64_t ldd, const void* bias,
                       void* aux, int64_t ldaux, int64_t M, int64_t N, int64_t K, int flags,
-                      void* stream, float* colsum_ws = nullptr) {
+                      void* stream, float* colsum_ws = nullptr,
+                      vp::EpiDrop drop = vp::EpiDrop{nullptr, 0, 0, 1.f}) {
   using namespace vp;
   if (M <= 0 || N <= 0 || K <= 0 || !A || !B || !D) return VP_ERR_ARGS;
   if ((lda % 8) || (ldb % 8) || (ldd % 8)) return VP_ERR_UNSUPPORTED;
@@ -903,6 +935,7 @@ static int gemm_entry(int a_kmajor, int b_kmajor, int epilogue, const void* A, i
   const bool use2 = !(flags & VP_GEMM_DIRECT_STORE) && !getenv("VP_GEMM_1SM") &&
                     (ldd % (f32_out ? 4 : 8)) == 0;
   if (colsum_ws && (!use2 || f32_out || (N % 2))) return VP_ERR_UNSUPPORTED;
+  if (drop.seed && (epilogue != VP_EPI_BIAS_RESID || (N % 2))) return VP_ERR_UNSUPPORTED;
   if (use2) {
     CUtensorMap ta, tb, td, tx;
     bool ok = a_mn ? make_tmap(&ta, A, M, K, lda, 64, BK) : make_tmap(&ta, A, K, M, lda, BK, 128);
@@ -941,7 +974,7 @@ static int gemm_entry(int a_kmajor, int b_kmajor, int epilogue, const void* A, i
     int64_t group = 8;
     if (const char* g = getenv("VP_GEMM_GROUP")) group = std::max(1, atoi(g));
     Epi2 e{reinterpret_cast<const __nv_bfloat16*>(bias), reinterpret_cast<const __nv_bfloat16*>(aux),
-           ldaux, group, colsum_ws};
+           ldaux, group, colsum_ws, drop};
     return gemm2_dispatch(epilogue, a_mn, b_mn, ta, tb, td, tx, M, N, K, split, e, st);
   }
   const int BNsel = N <= 128 ? 128 : 256;
@@ -951,7 +984,7 @@ static int gemm_entry(int a_kmajor, int b_kmajor, int epilogue, const void* A, i
                    : make_tmap(&tb, B, K, N, ldb, BK, BNsel));
   if (!ok) return VP_ERR_UNSUPPORTED;
   EpiArgs e{D, ldd, reinterpret_cast<const __nv_bfloat16*>(bias),
-            reinterpret_cast<__nv_bfloat16*>(aux), ldaux};
+            reinterpret_cast<__nv_bfloat16*>(aux), ldaux, drop};
   if (BNsel == 256) return dispatch_epi<256>(epilogue, a_mn, b_mn, ta, tb, M, N, K, e, st);
   return dispatch_epi<128>(epilogue, a_mn, b_mn, ta, tb, M, N, K, e, st);
 }
@@ -970,6 +1003,22 @@ extern "C" int vp_gemm_bf16_ex(int a_kmajor, int b_kmajor, int epilogue, const v
                                int64_t K, int flags, void* stream) {
   return gemm_entry(a_kmajor, b_kmajor, epilogue, A, lda, B, ldb, D, ldd, bias, aux, ldaux, M, N,
                     K, flags, stream);
+}
+
+extern "C" int vp_gemm_bf16_dropout(int a_kmajor, int b_kmajor, const void* A, int64_t lda,
+                                    const void* B, int64_t ldb, void* D, int64_t ldd,
+                                    const void* bias, const void* resid, int64_t ldres, int64_t M,
+                                    int64_t N, int64_t K, float p, const uint64_t* seed,
+                                    uint32_t salt, int flags, void* stream) {
+  if (p < 0.f || p >= 1.f) return VP_ERR_ARGS;
+  if (p > 0.f && !seed) return VP_ERR_ARGS;
+  vp::EpiDrop drop{nullptr, 0, 0, 1.f};
+  if (p > 0.f) {
+    const uint32_t thr = vp::drop_threshold(p);
+    drop = vp::EpiDrop{seed, salt, thr, vp::drop_scale(thr)};
+  }
+  return gemm_entry(a_kmajor, b_kmajor, VP_EPI_BIAS_RESID, A, lda, B, ldb, D, ldd, bias,
+                    const_cast<void*>(resid), ldres, M, N, K, flags, stream, nullptr, drop);
 }
 
 #ifdef VP_GEMM_TRACE

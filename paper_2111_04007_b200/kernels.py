@@ -18,6 +18,7 @@ from ._lib import check, f32, i64, vp
 L = _lib.lib
 c_int = ctypes.c_int
 u64 = ctypes.c_uint64
+u32 = ctypes.c_uint32
 
 (EPI_STORE, EPI_BIAS, EPI_BIAS_GELU, EPI_BIAS_RESID, EPI_DGELU, EPI_ACC_F32, EPI_STORE_F32,
  EPI_RESID) = range(8)
@@ -31,8 +32,14 @@ _SIGS = {
     "vp_layernorm_bwd": [vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, c_int, vp, vp],
     "vp_attention_fwd": [vp, vp, vp, i64, i64, i64, i64, c_int, vp],
     "vp_attention_bwd": [vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, c_int, vp],
-    "vp_attention_bwd_ex": [vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, i64, c_int, c_int, vp,
-                            vp],
+    "vp_attention_bwd_ex": [vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, i64, c_int, c_int, f32,
+                            vp, u32, vp, vp],
+    "vp_attention_fwd_ex": [vp, vp, vp, i64, i64, i64, i64, c_int, f32, vp, u32, vp],
+    "vp_set_seed": [vp, u64, vp],
+    "vp_dropout_dev": [vp, i64, f32, vp, u32, vp],
+    "vp_dropout_bwd": [vp, vp, i64, i64, f32, vp, u32, vp, vp, vp],
+    "vp_gemm_bf16_dropout": [c_int, c_int, vp, i64, vp, i64, vp, i64, vp, vp, i64, i64, i64, i64,
+                             f32, vp, u32, c_int, vp],
     "vp_attention_bwd_ws_elems": [i64, i64, i64, i64],
     "vp_attention_bwd_fuses_bias": [i64, c_int],
     "vp_layernorm_ws_elems": [i64],
@@ -189,10 +196,14 @@ def layernorm_bwd(dy, x, gamma, mean, rstd, dx, dgamma, dbeta, workspace, accumu
     return dx
 
 
-def attention_fwd(qkv, out, lse, batch, seq, heads, head_dim, causal=True, stream=None):
+def attention_fwd(qkv, out, lse, batch, seq, heads, head_dim, causal=True, stream=None,
+                  p=0.0, seed=None, salt=0):
+    """``p`` > 0: attention-probability dropout keyed by the device seed
+    tensor ``seed`` (int64 [1]) and the call site's ``salt``."""
     _count(1)
-    check(L.vp_attention_fwd(qkv.data_ptr(), out.data_ptr(), lse.data_ptr(), batch, seq, heads,
-                             head_dim, int(causal), _stream(stream)), "vp_attention_fwd")
+    check(L.vp_attention_fwd_ex(qkv.data_ptr(), out.data_ptr(), lse.data_ptr(), batch, seq, heads,
+                                head_dim, int(causal), p, _p(seed) if p > 0 else None,
+                                salt & 0xFFFFFFFF, _stream(stream)), "vp_attention_fwd_ex")
     return out
 
 
@@ -201,7 +212,7 @@ def attention_bwd_ws_elems(batch, seq, heads, head_dim) -> int:
 
 
 def attention_bwd(qkv, out, dout, lse, dqkv, ws, batch, seq, heads, head_dim, causal=True,
-                  stream=None, deterministic=False, dbias=None):
+                  stream=None, deterministic=False, dbias=None, p=0.0, seed=None, salt=0):
     """dqkv = d(qkv). ``ws``: fp32 workspace of attention_bwd_ws_elems()
     elements. head_dim 64 runs the fused one-pass kernel (dQ accumulated by
     TMA reduce-add); ``deterministic`` (or other head dims) the two-kernel
@@ -215,7 +226,8 @@ def attention_bwd(qkv, out, dout, lse, dqkv, ws, batch, seq, heads, head_dim, ca
     _count(3 + (1 if fused_bias else 0))
     check(L.vp_attention_bwd_ex(qkv.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(),
                                 dqkv.data_ptr(), ws.data_ptr(), ws.numel(), batch, seq, heads,
-                                head_dim, int(causal), 1 if deterministic else 0,
+                                head_dim, int(causal), 1 if deterministic else 0, p,
+                                _p(seed) if p > 0 else None, salt & 0xFFFFFFFF,
                                 dbias.data_ptr() if fused_bias else None, _stream(stream)),
           "vp_attention_bwd")
     return fused_bias
@@ -281,6 +293,61 @@ def dropout_(x, p, seed, offset, stream=None):
         _count()
     check(L.vp_dropout(x.data_ptr(), x.numel(), p, seed, offset, _stream(stream)), "vp_dropout")
     return x
+
+
+def set_seed(buf, value: int, stream=None):
+    """Write the current (step, micro-batch) dropout seed into the device
+    buffer every dropout site reads (outside captured graphs)."""
+    _count(1)
+    check(L.vp_set_seed(buf.data_ptr(), value & 0xFFFFFFFFFFFFFFFF, _stream(stream)), "vp_set_seed")
+
+
+def dropout_dev_(x, p, seed, salt, stream=None):
+    """x *= K7 mask (device seed, static salt), in place."""
+    if p <= 0:
+        return x
+    _count(1)
+    check(L.vp_dropout_dev(x.data_ptr(), x.numel(), p, seed.data_ptr(), salt & 0xFFFFFFFF,
+                           _stream(stream)), "vp_dropout_dev")
+    return x
+
+
+def dropout_bwd(g, gy, p, seed, salt, dbias, workspace, stream=None):
+    """gy = mask(g) (the gradient of a dropped-out branch) and dbias += its
+    column sums, one pass."""
+    rows, cols = g.shape
+    _count(1)
+    check(L.vp_dropout_bwd(g.data_ptr(), gy.data_ptr(), rows, cols, p, seed.data_ptr(),
+                           salt & 0xFFFFFFFF, dbias.data_ptr(), workspace.data_ptr(),
+                           _stream(stream)), "vp_dropout_bwd")
+    return gy
+
+
+def gemm_dropout(a, b, out, bias, resid, p, seed, salt, *, stream=None, out_ptr=None, ldd=None,
+                 direct=False):
+    """out[M,N] = resid + dropout(a @ b^T + bias) (a [M,K], b [N,K]); the K7
+    mask applied in the GEMM epilogue."""
+    _need(a, torch.bfloat16, "gemm.a")
+    _need(b, torch.bfloat16, "gemm.b")
+    M, K = a.shape
+    N = b.shape[0]
+    if out is not None:
+        out_ptr, ldd = out.data_ptr(), out.stride(0)
+    timing = GEMM_TIMING["on"]
+    if timing:
+        st = stream or torch.cuda.current_stream()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+    _count()
+    check(L.vp_gemm_bf16_dropout(1, 1, a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0),
+                                 out_ptr, ldd, bias.data_ptr(), resid.data_ptr(), resid.stride(0),
+                                 M, N, K, p, _p(seed) if p > 0 else None, salt & 0xFFFFFFFF,
+                                 1 if direct else 0, _stream(stream)), "vp_gemm_bf16_dropout")
+    if timing:
+        e1.record(st)
+        GEMM_TIMING["records"].append((2 * M * N * K, e0, e1, (M, N, K, True, True)))
+    return out
 
 
 def add(a, b, y, stream=None):

@@ -128,6 +128,16 @@ def init_mlm_head(cfg: GPT2Config, seed: int, device="cpu") -> Dict[str, torch.T
             * cfg.init_std}
 
 
+# K7 dropout call sites: a static salt per (layer, site), keyed with the
+# per-(step, micro-batch) seed in device memory (vp_set_seed / vp_dropout_dev)
+SITE_ATTN, SITE_PROJ, SITE_FC2 = 0, 1, 2
+SALT_EMBED = 0x7FFFFFF0
+
+
+def drop_salt(layer: int, site: int) -> int:
+    return layer * 4 + site
+
+
 def round_bf16(t: torch.Tensor) -> torch.Tensor:
     return t.to(torch.bfloat16).to(torch.float32)
 
@@ -311,18 +321,26 @@ class GPT2Stage:
             self.emb_mean = torch.empty(T, **f32)
             self.emb_rstd = torch.empty(T, **f32)
         self.drop_tmp = torch.empty(T, h, **bf) if cfg.dropout > 0 else None
+        # the current (step, micro-batch) dropout seed: every dropout site
+        # reads it from here, so captured graphs replay with fresh masks
+        self.seed_buf = torch.zeros(1, dtype=torch.int64, device=dev)
 
     # --------------------------------------------------------------- forward
-    def _layer_fwd(self, li: int, x: torch.Tensor, out, w: _LayerWS, dseed: int, stream=None):
+    def _attn_fwd(self, li, w, stream):
+        cfg = self.cfg
+        K.attention_fwd(w.qkv, w.o, w.lse, self.mb, cfg.seq_len, cfg.heads, cfg.head_dim,
+                        cfg.causal, stream, p=cfg.dropout, seed=self.seed_buf,
+                        salt=drop_salt(li, SITE_ATTN))
+
+    def _layer_fwd(self, li: int, x: torch.Tensor, out, w: _LayerWS, stream=None):
         cfg, P = self.cfg, self.params
         p = f"l{li}."
         K.layernorm_fwd(x, P.w(p + "ln1_g"), P.w(p + "ln1_b"), w.a, w.mean1, w.rstd1,
                         cfg.ln_eps, stream)
         K.gemm(w.a, P.w(p + "w_qkv"), w.qkv, epilogue=K.EPI_BIAS, bias=P.w(p + "b_qkv"),
                stream=stream)
-        K.attention_fwd(w.qkv, w.o, w.lse, self.mb, cfg.seq_len, cfg.heads, cfg.head_dim,
-                        cfg.causal, stream)
-        self._proj_resid(w.o, P.w(p + "w_o"), P.w(p + "b_o"), x, w.x1, dseed, 0, stream)
+        self._attn_fwd(li, w, stream)
+        self._proj_resid(w.o, P.w(p + "w_o"), P.w(p + "b_o"), x, w.x1, li, SITE_PROJ, stream)
         K.layernorm_fwd(w.x1, P.w(p + "ln2_g"), P.w(p + "ln2_b"), w.c, w.mean2, w.rstd2,
                         cfg.ln_eps, stream)
         # gelu'(pre-activation) is only needed by the backward (its DGELU
@@ -330,7 +348,7 @@ class GPT2Stage:
         # recomputing stage) writes the GELU output alone
         K.gemm(w.c, P.w(p + "w_fc1"), w.f, epilogue=K.EPI_BIAS_GELU, bias=P.w(p + "b_fc1"),
                aux=w.pre if w is not self.scratch else None, stream=stream)
-        self._proj_resid(w.f, P.w(p + "w_fc2"), P.w(p + "b_fc2"), w.x1, out, dseed, 1, stream)
+        self._proj_resid(w.f, P.w(p + "w_fc2"), P.w(p + "b_fc2"), w.x1, out, li, SITE_FC2, stream)
 
     def _layer_fwd_post(self, li: int, x: torch.Tensor, out, w: _LayerWS, stream=None):
         """BERT (post-LN) layer: y1 = x + proj(attn(qkv(x))); x1 = LN1(y1);
@@ -340,16 +358,13 @@ class GPT2Stage:
         p = f"l{li}."
         K.gemm(x, P.w(p + "w_qkv"), w.qkv, epilogue=K.EPI_BIAS, bias=P.w(p + "b_qkv"),
                stream=stream)
-        K.attention_fwd(w.qkv, w.o, w.lse, self.mb, cfg.seq_len, cfg.heads, cfg.head_dim,
-                        cfg.causal, stream)
-        K.gemm(w.o, P.w(p + "w_o"), w.x1, epilogue=K.EPI_BIAS_RESID, bias=P.w(p + "b_o"), aux=x,
-               stream=stream)
+        self._attn_fwd(li, w, stream)
+        self._proj_resid(w.o, P.w(p + "w_o"), P.w(p + "b_o"), x, w.x1, li, SITE_PROJ, stream)
         K.layernorm_fwd(w.x1, P.w(p + "ln1_g"), P.w(p + "ln1_b"), w.c, w.mean1, w.rstd1,
                         cfg.ln_eps, stream)
         K.gemm(w.c, P.w(p + "w_fc1"), w.f, epilogue=K.EPI_BIAS_GELU, bias=P.w(p + "b_fc1"),
                aux=w.pre, stream=stream)
-        K.gemm(w.f, P.w(p + "w_fc2"), w.a, epilogue=K.EPI_BIAS_RESID, bias=P.w(p + "b_fc2"),
-               aux=w.c, stream=stream)
+        self._proj_resid(w.f, P.w(p + "w_fc2"), P.w(p + "b_fc2"), w.c, w.a, li, SITE_FC2, stream)
         if isinstance(out, int):  # next stage's ring slot: normalise locally, then ship
             K.layernorm_fwd(w.a, P.w(p + "ln2_g"), P.w(p + "ln2_b"), self.dc, w.mean2, w.rstd2,
                             cfg.ln_eps, stream)
@@ -366,11 +381,11 @@ class GPT2Stage:
         dy2 = self.do
         K.layernorm_bwd(g, w.a, P.w(p + "ln2_g"), w.mean2, w.rstd2, dy2, P.g(p + "ln2_g"),
                         P.g(p + "ln2_b"), self.ln_ws, accumulate=False, stream=stream)
-        K.gemm(dy2, P.w(p + "w_fc2"), self.dpre, b_kmajor=False, epilogue=K.EPI_DGELU,
+        gy2 = self._branch_grad(dy2, P.g(p + "b_fc2"), li, SITE_FC2, stream)
+        K.gemm(gy2, P.w(p + "w_fc2"), self.dpre, b_kmajor=False, epilogue=K.EPI_DGELU,
                aux=w.pre, stream=stream, dbias=P.g(p + "b_fc1"), dbias_ws=self.dbias_ws)
-        K.gemm(dy2, w.f, P.g(p + "w_fc2"), a_kmajor=False, b_kmajor=False,
+        K.gemm(gy2, w.f, P.g(p + "w_fc2"), a_kmajor=False, b_kmajor=False,
                epilogue=K.EPI_ACC_F32, stream=stream)
-        K.bias_grad(dy2, P.g(p + "b_fc2"), self.bias_ws, stream)
         # dx1 = dy2 + dpre @ W1 (residual folded into the dgrad epilogue)
         K.gemm(self.dpre, P.w(p + "w_fc1"), self.dc, b_kmajor=False, epilogue=K.EPI_RESID,
                aux=dy2, stream=stream)
@@ -379,13 +394,11 @@ class GPT2Stage:
         K.layernorm_bwd(self.dc, w.x1, P.w(p + "ln1_g"), w.mean1, w.rstd1, g, P.g(p + "ln1_g"),
                         P.g(p + "ln1_b"), self.ln_ws, accumulate=False, stream=stream)
         # g = dy1: attention branch
-        K.gemm(g, P.w(p + "w_o"), self.do, b_kmajor=False, stream=stream)
-        K.gemm(g, w.o, P.g(p + "w_o"), a_kmajor=False, b_kmajor=False,
+        gy1 = self._branch_grad(g, P.g(p + "b_o"), li, SITE_PROJ, stream)
+        K.gemm(gy1, P.w(p + "w_o"), self.do, b_kmajor=False, stream=stream)
+        K.gemm(gy1, w.o, P.g(p + "w_o"), a_kmajor=False, b_kmajor=False,
                epilogue=K.EPI_ACC_F32, stream=stream)
-        K.bias_grad(g, P.g(p + "b_o"), self.bias_ws, stream)
-        fused_bq = K.attention_bwd(w.qkv, w.o, self.do, w.lse, self.dqkv, self.delta, self.mb,
-                                   cfg.seq_len, cfg.heads, cfg.head_dim, cfg.causal, stream,
-                                   dbias=P.g(p + "b_qkv"))
+        fused_bq = self._attn_bwd(li, w, p, stream)
         K.gemm(self.dqkv, x, P.g(p + "w_qkv"), a_kmajor=False, b_kmajor=False,
                epilogue=K.EPI_ACC_F32, stream=stream)
         if not fused_bq:
@@ -394,34 +407,52 @@ class GPT2Stage:
         K.gemm(self.dqkv, P.w(p + "w_qkv"), g, b_kmajor=False, epilogue=K.EPI_RESID, aux=g,
                stream=stream)
 
-    def _proj_resid(self, a, wt, b, resid, out, dseed, which, stream):
-        """out = resid + dropout(a @ wt^T + b) (fused epilogue when p = 0)."""
+    def _proj_resid(self, a, wt, b, resid, out, li, site, stream):
+        """out = resid + dropout(a @ wt^T + b): one GEMM, the bias, the K7
+        dropout mask and the residual add in its epilogue (``out`` an int:
+        an NVLink peer address the epilogue stores into directly)."""
         out_t, out_ptr = (None, out) if isinstance(out, int) else (out, None)
         ld = self.cfg.hidden
         if self.cfg.dropout <= 0:
             K.gemm(a, wt, out_t, epilogue=K.EPI_BIAS_RESID, bias=b, aux=resid, stream=stream,
                    out_ptr=out_ptr, ldd=ld, direct=out_ptr is not None)
             return
-        tmp = self.drop_tmp
-        K.gemm(a, wt, tmp, epilogue=K.EPI_BIAS, bias=b, stream=stream)
-        K.dropout_(tmp, self.cfg.dropout, dseed, which * tmp.numel(), stream)
-        if out_t is None:
-            out_t = tmp  # dropout + peer write: add locally, then ship
-            K.add(tmp, resid, tmp, stream)
-            K.p2p_put(out_ptr, tmp, stream=stream)
-        else:
-            K.add(tmp, resid, out_t, stream)
+        K.gemm_dropout(a, wt, out_t, b, resid, self.cfg.dropout, self.seed_buf,
+                       drop_salt(li, site), stream=stream, out_ptr=out_ptr, ldd=ld,
+                       direct=out_ptr is not None)
+
+    def _branch_grad(self, g, dbias, li, site, stream):
+        """Gradient entering a dropped-out branch (out = resid + dropout(y)):
+        mask(g) and the branch bias gradient (its column sums), one pass.
+        Without dropout the branch sees g itself and the bias gradient is a
+        plain column sum."""
+        if self.cfg.dropout <= 0:
+            K.bias_grad(g, dbias, self.bias_ws, stream)
+            return g
+        return K.dropout_bwd(g, self.drop_tmp, self.cfg.dropout, self.seed_buf,
+                             drop_salt(li, site), dbias, self.bias_ws, stream)
+
+    def _attn_bwd(self, li, w, p, stream):
+        cfg, P = self.cfg, self.params
+        return K.attention_bwd(w.qkv, w.o, self.do, w.lse, self.dqkv, self.delta, self.mb,
+                               cfg.seq_len, cfg.heads, cfg.head_dim, cfg.causal, stream,
+                               dbias=P.g(p + "b_qkv"), p=cfg.dropout, seed=self.seed_buf,
+                               salt=drop_salt(li, SITE_ATTN))
 
     def forward(self, x_in: Optional[torch.Tensor], ids: Optional[torch.Tensor], save: bool,
-                dseed: int = 0, stream=None, out_ptr: Optional[int] = None,
+                dseed: Optional[int] = None, stream=None, out_ptr: Optional[int] = None,
                 types: Optional[torch.Tensor] = None) -> torch.Tensor:
         """Run the stage on one micro-batch. Stage 0 takes token ``ids``
         [T] (int64); others take the received activation ``x_in`` [T, h].
         Returns the stage output (residual stream after the last layer).
         ``out_ptr``: write the final layer's output straight into this
         (NVLink peer-mapped) address from the FC2 GEMM epilogue — the fused
-        compute + P2P send of a checkpointed forward (K9 fused into K1)."""
+        compute + P2P send of a checkpointed forward (K9 fused into K1).
+        ``dseed``: write this dropout seed to the device seed buffer first
+        (the executor sets it itself, outside its captured graphs)."""
         cfg, P = self.cfg, self.params
+        if dseed is not None:
+            K.set_seed(self.seed_buf, dseed, stream)
         if self.spec.first:
             if self.bert:
                 K.embed_typed_fwd(ids, types, P.w("wte"), P.w("wpe"), P.w("tte"), self.emb_pre,
@@ -432,8 +463,7 @@ class GPT2Stage:
                 K.embed_fwd(ids, P.w("wte"), P.w("wpe"), self.emb_out, self.mb, cfg.seq_len,
                             stream)
             x = self.emb_out
-            if cfg.dropout > 0:
-                K.dropout_(x, cfg.dropout, dseed ^ 0x5EED, 7 * x.numel(), stream)
+            K.dropout_dev_(x, cfg.dropout, self.seed_buf, SALT_EMBED, stream)
         else:
             x = x_in
         self.xs[0] = x
@@ -444,7 +474,7 @@ class GPT2Stage:
             if self.bert:
                 self._layer_fwd_post(li, x, dst, w, stream)
             else:
-                self._layer_fwd(li, x, dst, w, dseed * 1315423911 + li, stream)
+                self._layer_fwd(li, x, dst, w, stream)
             x = self.xs[i + 1]
         return x
 
@@ -502,15 +532,7 @@ class GPT2Stage:
         return self.loss_rows
 
     # -------------------------------------------------------------- backward
-    def _drop_grad(self, g, dseed, which, stream):
-        """Gradient through out = resid + dropout(y): dy = dropout_mask(g)."""
-        if self.cfg.dropout <= 0:
-            return g
-        self.drop_tmp.copy_(g)
-        K.dropout_(self.drop_tmp, self.cfg.dropout, dseed, which * g.numel(), stream)
-        return self.drop_tmp
-
-    def _layer_bwd(self, li: int, w: _LayerWS, x: torch.Tensor, dseed: int, stream=None,
+    def _layer_bwd(self, li: int, w: _LayerWS, x: torch.Tensor, stream=None,
                    fc2_done: bool = False, lower: Optional[int] = None) -> bool:
         """self.g holds d(layer output); on return it holds d(layer input).
         ``fc2_done``: this layer's FC2 bias gradient (= column sum of g) was
@@ -521,15 +543,16 @@ class GPT2Stage:
         p = f"l{li}."
         g = self.g
         fused = cfg.dropout <= 0  # dropout masks the branch gradients
-        # --- MLP: out = x1 + fc2(gelu(fc1(ln2(x1))))
-        gy = self._drop_grad(g, dseed, 1, stream)
+        # --- MLP: out = x1 + dropout(fc2(gelu(fc1(ln2(x1)))))
+        if fused and fc2_done:
+            gy = g   # FC2 bias gradient already summed by the LN backward that made g
+        else:
+            gy = self._branch_grad(g, P.g(p + "b_fc2"), li, SITE_FC2, stream)
         # dpre = (gy W2) * gelu'(pre); its column sum (FC1 bias grad) in the epilogue
         K.gemm(gy, P.w(p + "w_fc2"), self.dpre, b_kmajor=False, epilogue=K.EPI_DGELU,
                aux=w.pre, stream=stream, dbias=P.g(p + "b_fc1"), dbias_ws=self.dbias_ws)
         K.gemm(gy, w.f, P.g(p + "w_fc2"), a_kmajor=False, b_kmajor=False,
                epilogue=K.EPI_ACC_F32, stream=stream)
-        if not (fc2_done and fused):
-            K.bias_grad(gy, P.g(p + "b_fc2"), self.bias_ws, stream)
         K.gemm(self.dpre, P.w(p + "w_fc1"), self.dc, b_kmajor=False, stream=stream)
         K.gemm(self.dpre, w.c, P.g(p + "w_fc1"), a_kmajor=False, b_kmajor=False,
                epilogue=K.EPI_ACC_F32, stream=stream)
@@ -537,17 +560,13 @@ class GPT2Stage:
         K.layernorm_bwd(self.dc, w.x1, P.w(p + "ln2_g"), w.mean2, w.rstd2, g,
                         P.g(p + "ln2_g"), P.g(p + "ln2_b"), self.ln_ws, accumulate=True,
                         stream=stream, dsum=P.g(p + "b_o") if fused else None)
-        # --- attention: x1 = x + proj(attn(qkv(ln1(x))))
-        gy = self._drop_grad(g, dseed, 0, stream)
+        # --- attention: x1 = x + dropout(proj(attn(qkv(ln1(x)))))
+        gy = g if fused else self._branch_grad(g, P.g(p + "b_o"), li, SITE_PROJ, stream)
         K.gemm(gy, P.w(p + "w_o"), self.do, b_kmajor=False, stream=stream)
         K.gemm(gy, w.o, P.g(p + "w_o"), a_kmajor=False, b_kmajor=False,
                epilogue=K.EPI_ACC_F32, stream=stream)
-        if not fused:
-            K.bias_grad(gy, P.g(p + "b_o"), self.bias_ws, stream)
         # dqkv, and the QKV bias gradient (its column sums) in the same passes
-        fused_bq = K.attention_bwd(w.qkv, w.o, self.do, w.lse, self.dqkv, self.delta, self.mb,
-                                   cfg.seq_len, cfg.heads, cfg.head_dim, cfg.causal, stream,
-                                   dbias=P.g(p + "b_qkv"))
+        fused_bq = self._attn_bwd(li, w, p, stream)
         K.gemm(self.dqkv, P.w(p + "w_qkv"), self.dc, b_kmajor=False, stream=stream)
         K.gemm(self.dqkv, w.a, P.g(p + "w_qkv"), a_kmajor=False, b_kmajor=False,
                epilogue=K.EPI_ACC_F32, stream=stream)
@@ -561,16 +580,23 @@ class GPT2Stage:
         return lower_fc2 is not None
 
     def backward(self, grad_out: Optional[torch.Tensor], ids: Optional[torch.Tensor],
-                 dseed: int = 0, stream=None, types: Optional[torch.Tensor] = None) -> torch.Tensor:
+                 dseed: Optional[int] = None, stream=None,
+                 types: Optional[torch.Tensor] = None) -> torch.Tensor:
         """Backward through the stage's layers using the saved working set.
         ``grad_out`` = d(stage output) from the next stage (None on the last
         stage, where loss_and_head_backward already filled ``self.g``).
         Returns d(stage input) (in ``self.g``); on stage 0 it is consumed by
         the embedding backward instead."""
         cfg, P = self.cfg, self.params
+        if dseed is not None:
+            K.set_seed(self.seed_buf, dseed, stream)
         fc2_done = False
+        g_own = self.g
         if grad_out is not None:
-            self.g.copy_(grad_out)
+            # the received gradient (ring slot) is the working buffer itself:
+            # consumed in place, no copy (the slot is rewritten only in the
+            # next mini-batch)
+            self.g = grad_out
         elif self.spec.last:
             fc2_done = getattr(self, "_fc2_done", False)
             self._fc2_done = False
@@ -580,11 +606,10 @@ class GPT2Stage:
                 self._layer_bwd_post(li, self.ws[i], self.xs[i], stream)
             else:
                 lower = self.spec.layers[i - 1] if i > 0 else None
-                fc2_done = self._layer_bwd(li, self.ws[i], self.xs[i], dseed * 1315423911 + li,
-                                           stream, fc2_done=fc2_done, lower=lower)
+                fc2_done = self._layer_bwd(li, self.ws[i], self.xs[i], stream,
+                                           fc2_done=fc2_done, lower=lower)
         if self.spec.first:
-            if cfg.dropout > 0:
-                K.dropout_(self.g, cfg.dropout, dseed ^ 0x5EED, 7 * self.g.numel(), stream)
+            K.dropout_dev_(self.g, cfg.dropout, self.seed_buf, SALT_EMBED, stream)
             if self.bert:
                 K.layernorm_bwd(self.g, self.emb_pre, P.w("lne_g"), self.emb_mean, self.emb_rstd,
                                 self.dc, P.g("lne_g"), P.g("lne_b"), self.ln_ws,
@@ -593,9 +618,59 @@ class GPT2Stage:
                                   self.mb, cfg.seq_len, stream)
             else:
                 K.embed_bwd(ids, self.g, P.g("wte"), P.g("wpe"), self.mb, cfg.seq_len, stream)
-        return self.g
+        out, self.g = self.g, g_own
+        return out
 
     # ------------------------------------------------------------- utilities
+    @staticmethod
+    def memory_plan(cfg: GPT2Config, spec: StageSpec, micro_batch: int) -> Dict[str, int]:
+        """HBM bytes this stage allocates (mirrors ``__init__``/``_alloc``):
+        parameters at 18 B/param (bf16 weight, fp32 master, grad, Adam m, v;
+        the reference prices 16, sp/core.py:17-18 — the extra 2 B is the fp32
+        gradient accumulator), the per-layer working sets of one micro-batch
+        (Varuna rule 2: R(j) is directly followed by B(j), so one is live),
+        the no-save forward scratch, backward scratch and workspaces, and the
+        head's logits. Rings are sized by the executor (``ring_bytes``)."""
+        h, V, S = cfg.hidden, cfg.vocab_size, cfg.seq_len
+        T = micro_batch * S
+        bert = cfg.arch == "bert"
+
+        def al(n):
+            return (n + 127) // 128 * 128
+        n = 0
+        if spec.first:
+            n += al(V * h) + al(S * h)
+            if bert:
+                n += al(cfg.type_vocab * h) + 2 * al(h)
+        per_layer = sum(al(math.prod(shape)) for _, shape in layer_param_shapes(cfg))
+        n += per_layer * len(spec.layers)
+        if spec.last:
+            n += (al(h * h) + 3 * al(h) + al(V)) if bert else 2 * al(h)
+            if not spec.first:
+                n += al(V * h)
+        params = 18 * n
+        ws_one = (2 * T * h * (1 + 3 + 1 + 1 + 1 + 4 + 4)
+                  + 4 * micro_batch * cfg.heads * S + 4 * 4 * T)
+        nl = len(spec.layers)
+        working = nl * ws_one + nl * 2 * T * h                # ws + residual stream xs
+        scratch = ws_one + (2 * T * h if spec.first else 0)   # no-save temporaries, emb_out
+        scratch += 2 * T * h * (1 + 4 + 1 + 1 + 3)            # g, dpre, dc, do, dqkv
+        scratch += 4 * K.attention_bwd_ws_elems(micro_batch, S, cfg.heads, cfg.head_dim)
+        scratch += 4 * K.layernorm_ws_elems(h)
+        bias_cols = max(4 * h, V) if (bert and spec.last) else 4 * h
+        scratch += 4 * K.bias_grad_ws_elems(bias_cols) + 4 * K.gemm_dbias_ws_elems(T, 4 * h)
+        head = 0
+        if spec.last:
+            head = 2 * T * h + 2 * 4 * T + 2 * T * V + 4 * T
+            if bert:
+                head += 2 * 2 * T * h
+        if bert and spec.first:
+            scratch += 2 * T * h + 2 * 4 * T
+        if cfg.dropout > 0:
+            scratch += 2 * T * h
+        return {"params": params, "working_sets": working, "scratch": scratch, "head": head,
+                "total": params + working + scratch + head, "param_count": n}
+
     def flops_per_microbatch(self) -> int:
         """Algorithmic forward FLOPs of this stage for one micro-batch (GPT-2
         convention; the BERT MLM dense adds 2h^2 per token)."""

@@ -100,6 +100,21 @@ class StepResult:
         return math.sqrt(max(float(self._flags[0].item()), 0.0)) * self.inv_scale
 
 
+_M64 = (1 << 64) - 1
+
+
+def task_seed(seed: int, step: int, mb: int) -> int:
+    """64-bit dropout seed of micro-batch ``mb`` (global index r*N_m + j, so
+    DP replicas draw different masks) in training step ``step``: F(j), R(j)
+    and B(j) of one step share it, so recompute regenerates the forward's
+    masks. splitmix64 of a linear combination; restated in
+    oracle/gpt2_fp32.py."""
+    x = (seed * 0x9E3779B97F4A7C15 + step * 0xD1B54A32D192ED03 + mb * 0xBF58476D1CE4E5B9 + 1) & _M64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & _M64
+    return x ^ (x >> 31)
+
+
 def synthetic_batch(cfg: GPT2Config, rows: int, replica: int, step: int = 0, seed: int = 1234):
     """Deterministic token rows for one replica: global row g = replica·rows + i
     (DP replicas partition M_total). GPT-2: labels are inputs shifted by one.
@@ -437,9 +452,12 @@ class Varuna:
         # once into a CUDA graph and replayed: the per-launch host cost would
         # otherwise approach the GPU time of the short kernels. Inputs reach
         # the graph through fixed buffers; IPC waits / signals stay outside.
-        # Disabled with dropout (per-step seeds) and while kernel timing hooks
-        # are active.
-        self.use_graphs = (model.dropout <= 0) if graphs is None else bool(graphs)
+        # Dropout masks stay fresh under replay: every site reads the
+        # (step, micro-batch) seed from a device buffer written by a kernel
+        # launched before each task, outside the graph. Disabled while kernel
+        # timing hooks are active.
+        self.use_graphs = True if graphs is None else bool(graphs)
+        self.seed = seed
         T = self.m * model.seq_len
         self._in_ids = torch.zeros(T, dtype=torch.int64, device=self.device)
         self._in_types = torch.zeros(T, dtype=torch.int64, device=self.device)
@@ -582,7 +600,6 @@ class Varuna:
             x_in = {}
             graphs = self.use_graphs and not K.GEMM_TIMING["on"] and self.step_count > 1
             for kind, j in self.tasks:
-                dseed = (self.step_count * 1000003 + j) & 0x7FFFFFFF
                 # inputs first (stream waits on the peer's IPC event), so the
                 # task's timing events bracket compute only
                 if kind != B and not self.spec.first and j not in x_in:
@@ -598,10 +615,12 @@ class Varuna:
                         self._in_types.copy_(data["types"][j], non_blocking=True)
                 if self.spec.last and kind == B:
                     self._in_labels.copy_(data["labels"][j], non_blocking=True)
+                if cfg.dropout > 0:
+                    K.set_seed(stage.seed_buf, task_seed(self.seed, self.step_count,
+                                                         self.replica * self.N + j), st)
                 e0 = self._mark(ev)
-                body = (lambda kind=kind, j=j, dseed=dseed, g_in=g_in:
-                        self._task(kind, j, dseed, x_in.get(j), g_in, scale, st,
-                                   "types" in data))
+                body = (lambda kind=kind, j=j, g_in=g_in:
+                        self._task(kind, j, x_in.get(j), g_in, scale, st, "types" in data))
                 if graphs:
                     self._replay(kind, j, body, st)
                 else:
@@ -630,7 +649,7 @@ class Varuna:
         loss = self.loss_sum if self.spec.last else None
         return StepResult(loss, self.flags, 1.0 / self.loss_scale, timeline)
 
-    def _task(self, kind, j, dseed, x, g_in, scale, st, typed):
+    def _task(self, kind, j, x, g_in, scale, st, typed):
         """The launches of one schedule task on this stage (graph-capturable:
         every pointer is fixed for a given (kind, micro-batch))."""
         stage = self.stage
@@ -641,12 +660,11 @@ class Varuna:
             out_ptr = None
             if kind == F and not self.spec.last:
                 out_ptr = self.links.peer_slot_ptr(_Links.ACT, j)
-            stage.forward(x, ids, save=save, dseed=dseed, stream=st, out_ptr=out_ptr,
-                          types=types)
+            stage.forward(x, ids, save=save, stream=st, out_ptr=out_ptr, types=types)
         else:
             if self.spec.last:
                 stage.loss_and_head_backward(self._in_labels, scale, self.loss_sum, stream=st)
-            g = stage.backward(g_in, ids, dseed=dseed, stream=st, types=types)
+            g = stage.backward(g_in, ids, stream=st, types=types)
             if not self.spec.first:
                 K.p2p_put(self.links.peer_slot_ptr(_Links.GRAD, j), g, stream=st)
 
@@ -861,6 +879,25 @@ class Varuna:
         self.stage = None
         self._in_ids = self._in_types = self._in_labels = None
         torch.cuda.empty_cache()
+
+
+def memory_plan(cfg: GPT2Config, config: ParallelConfig) -> List[Dict[str, int]]:
+    """Per-stage HBM plan of a P x D job (bytes per rank): the stage's own
+    allocation (``GPT2Stage.memory_plan``) plus the receiver-owned
+    activation / gradient rings (one m*s*h*2-byte slot per micro-batch per
+    direction). Compare the reference's feasibility model, ``memory_check``
+    (16 B/param + stash + one working set, sp/partitioner.py:404-436)."""
+    P = config.pipeline_depth
+    out = []
+    slot = config.micro_batch_size * cfg.seq_len * cfg.hidden * 2
+    for s in range(P):
+        layers = tuple(i for i, x in enumerate(config.stage_map) if x == s)
+        plan = GPT2Stage.memory_plan(cfg, StageSpec(s, P, layers), config.micro_batch_size)
+        rings = (int(s > 0) + int(s < P - 1)) * config.num_micro_batches * slot
+        plan["rings"] = rings
+        plan["total"] += rings
+        out.append(plan)
+    return out
 
 
 def replan(cfg: GPT2Config, gpus: int, profile, global_batch: int, micro_batch_size: int,

@@ -83,16 +83,24 @@ def main():
         print("configs", configs, flush=True)
         print("morph losses", got, "reference", ref_losses, flush=True)
         ok = configs == [(2, 1), (2, 1), (1, 2), (1, 2), (1, 1)]
-        ok = ok and all(abs(a - b) / abs(b) < 2e-2 for a, b in zip(got, ref_losses))
+        ok = ok and all(abs(a - b) / abs(b) < 1e-4 for a, b in zip(got, ref_losses))
         assert step_count == ref["step_count"] == STEPS, (step_count, ref["step_count"])
-        worst = {}
+        # global relative L2 over all tensors (per-tensor errors of the
+        # near-zero-gradient entries, e.g. the key bias, are Adam sign noise)
+        worst, glob = {}, {}
         for key in ("master", "exp_avg", "exp_avg_sq"):
+            num = den = 0.0
             for n, t in state[key].items():
                 r = ref[key][n]
-                e = ((t.float().cpu() - r).norm() / r.norm().clamp_min(1e-20)).item()
-                worst[key] = max(worst.get(key, 0.0), e)
-        print("state rel err", worst, flush=True)
-        ok = ok and worst["master"] < 1e-2 and worst["exp_avg"] < 5e-2 and worst["exp_avg_sq"] < 5e-2
+                d = (t.float().cpu() - r).norm().item()
+                num += d * d
+                den += r.norm().item() ** 2
+                e = d / max(r.norm().item(), 1e-20)
+                if e > worst.get(key, ("", 0.0))[1]:
+                    worst[key] = (n, e)
+            glob[key] = (num / max(den, 1e-30)) ** 0.5
+        print("state rel err (global)", glob, "worst tensor", worst, flush=True)
+        ok = ok and glob["master"] < 1e-3 and glob["exp_avg"] < 5e-2 and glob["exp_avg_sq"] < 5e-2
         print("MORPH OK" if ok else "MORPH FAIL", flush=True)
     flag = torch.tensor([0 if ok else 1], device=dev)
     dist.all_reduce(flag)

@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--dispatch", default="static")
     ap.add_argument("--layers", type=int, default=0, help="cut the config to this many layers")
     ap.add_argument("--micro-batch", type=int, default=4)
+    ap.add_argument("--dropout", type=float, default=0.0)
     ap.add_argument("--global-batch", type=int, default=0,
                     help="M_total (default m*N*D); smaller values leave partial micro-batches")
     args = ap.parse_args()
@@ -41,9 +42,11 @@ def main():
     from paper_2111_04007_b200.runtime import Varuna, synthetic_batch
     from oracle.gpt2_fp32 import PipelineOracle
     cfg = CONFIGS[args.config]
+    import dataclasses
     if args.layers:
-        import dataclasses
         cfg = dataclasses.replace(cfg, n_layer=args.layers)
+    if args.dropout:
+        cfg = dataclasses.replace(cfg, dropout=args.dropout)
     P, D, N, m = args.P, args.D, args.N, args.micro_batch
     model = make_block_model("tiny", cfg.n_layer, cfg.hidden, cfg.seq_len)
     a = assign_stages(model, P, m, uniform_profile(cfg.n_layer, 1.0, 2.0, m_grid=(m,)))
@@ -66,10 +69,11 @@ def main():
     torch.cuda.synchronize()
     # oracle: D replicas' mini-batches, summed gradients
     o = PipelineOracle(cfg.n_layer, cfg.hidden, cfg.heads, cfg.vocab_size, cfg.seq_len,
-                       pc.stage_map, m, N, seed=0, arch=cfg.arch)
+                       pc.stage_map, m, N, seed=0, arch=cfg.arch, dropout=cfg.dropout)
     total = M * (cfg.mlm_per_seq if cfg.arch == "bert" else cfg.seq_len)
     loss = sum(o.run_minibatch(b["input_ids"], b["labels"], total,
-                               types=b.get("token_type_ids")) for b in batches)
+                               types=b.get("token_type_ids"), step=1, replica=r)
+               for r, b in enumerate(batches))
     og = o.grads()
     ok = True
     for name, g in v.param_tensors("grad").items():

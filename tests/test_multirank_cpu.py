@@ -101,7 +101,7 @@ def _worker(rank, world, port, P, D, errq):
         raise
 
 
-@pytest.mark.parametrize("P,D", [(2, 1), (1, 2), (2, 2), (4, 1)])
+@pytest.mark.parametrize("P,D", [(2, 1), (1, 2), (2, 2), (4, 1), (4, 2), (2, 4), (8, 1)])
 def test_multirank_host_logic(P, D):
     world = P * D
     ctx = mp.get_context("spawn")

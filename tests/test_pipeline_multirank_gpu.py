@@ -31,6 +31,10 @@ PIPE_CASES = [
     # M_total = 27 at m=4, N=4, D=2: replica 1 gets 11 rows — one partial and
     # one empty micro-batch; the loss is the mean over 27 samples
     (4, 2, 2, "tiny", ["--global-batch", "27"]),
+    # K7 dropout-recompute across stages and replicas: F on stage 0 and R
+    # before B regenerate the same masks; replicas draw different ones
+    (4, 2, 2, "tiny", ["--dropout", "0.1"]),
+    (2, 2, 1, "tiny_bert", ["--dropout", "0.1"]),
     # BASELINE widths, two-layer cuts: 16 MiB (355M, m=1) and 1 MiB-per-row
     # (BERT-large) boundary messages through the rings
     (2, 2, 1, "gpt2_355m", ["--layers", "2", "--micro-batch", "1", "--N", "2"]),
@@ -39,7 +43,8 @@ PIPE_CASES = [
 
 
 def _ids(c):
-    return f"{c[3]}-{c[1]}x{c[2]}" + ("-M27" if "--global-batch" in c[4] else "")
+    return (f"{c[3]}-{c[1]}x{c[2]}" + ("-M27" if "--global-batch" in c[4] else "")
+            + ("-p0.1" if "--dropout" in c[4] else ""))
 
 
 def _check(p, token):
