@@ -59,9 +59,15 @@ def parse():
     ap.add_argument("--m", default="auto",
                     help="micro-batch size: 'auto' (the planner's choice over the calibration "
                          "profile's m grid) or an integer")
-    ap.add_argument("--dispatch", default="opportunistic", choices=["opportunistic", "static"],
-                    help="P>1 task order: the reference's opportunistic policy over the "
-                         "calibration profile (default) or the static Varuna schedule")
+    ap.add_argument("--dispatch", default="opportunistic",
+                    choices=["opportunistic", "live", "static"],
+                    help="P>1 task order: the reference's opportunistic policy replayed over "
+                         "the calibration profile (default), run live on real arrivals, or the "
+                         "static Varuna schedule")
+    ap.add_argument("--retune", action="store_true",
+                    help="opportunistic replay: re-derive the order from one traced step's "
+                         "measured stage times, keeping the fastest of a few perturbed "
+                         "candidates (off by default)")
     ap.add_argument("--cpu-sample-s", type=float, default=20.0)
     return ap.parse_args()
 
@@ -463,7 +469,9 @@ def main():
     # uniform stage times).
     prof_path = os.path.join(ROOT, "profiles", f"b200_{args.config}.yaml")
     dispatch, prof = "static", None
-    if P > 1 and os.path.exists(prof_path) and args.dispatch == "opportunistic":
+    if P > 1 and args.dispatch == "live":
+        dispatch = "live"
+    elif P > 1 and os.path.exists(prof_path) and args.dispatch == "opportunistic":
         from paper_2111_04007_b200 import load_profile
         prof = load_profile(prof_path)
         if m in prof.m_grid and prof.num_cutpoints == cfg.n_layer:
@@ -493,7 +501,7 @@ def main():
     for _ in range(args.warmup):
         v.step(dbatch)
     barrier()
-    if P > 1 and dispatch == "opportunistic":
+    if P > 1 and dispatch == "opportunistic" and args.retune:
         # one traced step: the dispatch order is re-derived by the reference's
         # opportunistic replica kernel from the MEASURED per-stage task times
         v.trace = True
@@ -559,15 +567,19 @@ def main():
     g_ms = sum(r[1].elapsed_time(r[2]) for r in recs)
     tl = res.timeline
     step_us = tl["step_us"]
-    ar_us = tl["allreduce_us"][1] - tl["allreduce_us"][0]
-    local_busy = tl["busy_us"]
-    # measured bubble by the reference definition (sp/simulator.py:107-114),
-    # taken over the pipeline part (task busy + AR) of the slowest stage's clock
-    busy_all = torch.tensor([local_busy, ar_us, step_us], device=dev, dtype=torch.float64)
+    # measured bubble by the reference definition (sp/simulator.py:107-114):
+    # 1 - (sum of task busy + sum of AR WORK) / (P*D*T_mb). AR work is the
+    # C1 bucket spans on the comm stream (not the sync bracket, which also
+    # holds C2/C3 waits on other stages); T_mb the latest task / AR end.
+    # Every rank's clock starts at its step's first event, right after a
+    # barrier with idle streams (one common origin to ~0.1 ms).
+    ends = [b for _, _, _, b in tl["tasks"]] + [b for _, b in tl["ar_spans"]]
+    busy_all = torch.tensor([tl["busy_us"], tl["ar_work_us"]], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(busy_all)
-    mb_us = max_over_ranks(tl["allreduce_us"][1])
+    mb_us = max_over_ranks(max(ends) if ends else 0.0)
     bubble = 1.0 - (busy_all[0].item() + busy_all[1].item()) / (world * mb_us) if mb_us else 0.0
+    k9_us = measure_k9(v, P, dev)
     gemm_tf = g_flops / (g_ms / 1e3) / 1e12 if g_ms else 0.0
     gemm_share = g_ms / (step_us / 1e3) if step_us else 0.0
     burst, sustained, hbm, src = peaks()
@@ -586,8 +598,8 @@ def main():
     roof_samples = D * m / worst
 
     # measured stage profile -> reference bubble predictor (simulate_minibatch)
-    predicted = predicted_bubble(v, tl, P, D, N, m, stage_map, world, dev, dist,
-                                 opportunistic=dispatch == "opportunistic")
+    predicted = predicted_bubble(v, tl, P, D, N, m, world, dev, dist,
+                                 opportunistic=dispatch != "static", k9_us=k9_us)
 
     cpu = None
     control_plane = None
@@ -632,7 +644,16 @@ def main():
                          "peak_kind": f"{src} bf16 sustained", "share_of_step": round(gemm_share, 3)},
             "stage_roofline": {"roofline_samples_per_s": round(roof_samples, 1),
                                "frac": round(value / roof_samples, 4)},
-            "bubble": {"measured": round(bubble, 4), "predicted": predicted},
+            "bubble": {"measured": round(bubble, 4), "predicted": predicted["bubble"],
+                       "rel_err": (round(abs(bubble - predicted["bubble"]) / predicted["bubble"], 4)
+                                   if predicted["bubble"] else None),
+                       "measured_minibatch_us": round(mb_us, 1),
+                       "predicted_minibatch_us": predicted["minibatch_us"],
+                       "basis": "reference formula (sp/simulator.py:107-114); predicted = "
+                                "simulate_minibatch twin on the Varuna schedule with the "
+                                f"dispatch used ({dispatch}), over an in-step profile: measured "
+                                "per-stage F/B/R, K9 put time, C1 bucket work",
+                       "k9_put_us": k9_us},
             "cpu_baseline": cpu,
             "control_plane_cpp_us": control_plane,
         }
@@ -643,53 +664,79 @@ def main():
     return 0
 
 
-def predicted_bubble(v, tl, P, D, N, m, stage_map, world, dev, dist, opportunistic=False):
-    """The reference bubble predictor (simulate_minibatch, sp/simulator.py:
-    259-389) applied to the task order this run EXECUTED (every stage's
-    dispatch list, replayed statically) with the MEASURED per-stage mean
-    F/B times and R/F ratio, zero transfer cost; returns its bubble fraction."""
-    import numpy as np
+def measure_k9(v, P, dev):
+    """K9 transfer time: the gradient put of one m*s*h*2-byte slot into the
+    upstream stage's ring (median of 5 after one warm-up, CUDA events on
+    the executor stream; all stages idle). Max over ranks; 0 at P = 1."""
+    import torch
+    import torch.distributed as dist
+    from paper_2111_04007_b200 import kernels as K
+    t = 0.0
+    if P > 1 and v.active and not v.spec.first:
+        src = v.stage.g
+        dst = v.links.peer_slot_ptr(1, 1)
+        st = v.stream
+        times = []
+        for i in range(6):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            K.p2p_put(dst, src, stream=st)
+            b.record(st)
+            b.synchronize()
+            if i:
+                times.append(a.elapsed_time(b) * 1e3)
+        t = statistics.median(times)
+    if dist.is_initialized() and dist.get_world_size() > 1:
+        x = torch.tensor([t], device=dev, dtype=torch.float64)
+        dist.all_reduce(x, op=dist.ReduceOp.MAX)
+        t = float(x.item())
+    return round(t, 2)
+
+
+def predicted_bubble(v, tl, P, D, N, m, world, dev, dist, opportunistic=False, k9_us=0.0):
+    """The reference's prediction for this run (simulate_minibatch,
+    sp/simulator.py:259-389, on the C++ replica kernel): the Varuna schedule
+    generate_varuna_schedule(P, N, 1, 2, 1) under the dispatch policy used
+    (opportunistic for the replayed and the live dispatch), over an IN-STEP
+    calibration profile — one cut-point per stage carrying that stage's
+    measured mean F and B (replica 0), R as a measured R/F ratio, the
+    measured K9 put time as the intra-node act/grad transfer, and the stage's
+    measured C1 bucket work as its AR time."""
     import torch
     from paper_2111_04007_b200 import (ModelSpec, ParallelConfig, build_placement,
-                                       simulate_minibatch, uniform_cluster)
+                                       generate_varuna_schedule, simulate_minibatch,
+                                       uniform_cluster)
     from paper_2111_04007_b200.calibration import CalibrationProfile, CutpointTimes
     from paper_2111_04007_b200.core import KIND_BACKWARD, KIND_FORWARD, KIND_RECOMPUTE
-    from paper_2111_04007_b200.scheduler import Schedule
-    sums = torch.zeros(world, 3, device=dev, dtype=torch.float64)
+    sums = torch.zeros(world, 4, device=dev, dtype=torch.float64)
     cnt = {0: [], 1: [], 2: []}
     for kind, j, a, b in tl["tasks"]:
         cnt[kind].append(b - a)
     for kind, col in ((KIND_FORWARD, 0), (KIND_BACKWARD, 1), (KIND_RECOMPUTE, 2)):
         if cnt[kind]:
             sums[v.rank, col] = statistics.mean(cnt[kind])
+    sums[v.rank, 3] = tl["ar_work_us"]
     if world > 1:
         dist.all_reduce(sums)
     stage_f = [float(sums[s, 0].item()) for s in range(P)]
     stage_b = [float(sums[s, 1].item()) for s in range(P)]
+    stage_ar = [float(sums[[r * P + s for r in range(D)], 3].mean().item()) for s in range(P)]
     rec = [float(sums[s, 2].item()) / stage_f[s] for s in range(P) if sums[s, 2] > 0 and stage_f[s]]
     rscale = statistics.mean(rec) if rec else 1.0
-    tasks = [None] * world
-    if world > 1:
-        dist.all_gather_object(tasks, v.tasks)
-    else:
-        tasks = [v.tasks]
-    kinds, mbs, offs = [], [], [0]
-    for s in range(P):          # replica 0's ranks are 0..P-1
-        kinds += [k for k, _ in tasks[s]]
-        mbs += [j for _, j in tasks[s]]
-        offs.append(len(kinds))
-    sched = Schedule("executed", P, N, np.array(kinds, np.int64), np.array(mbs, np.int64),
-                     np.array(offs, np.int64), 1, 2, 1)
-    # one cut-point per stage carrying the whole stage's time
-    z = {m: 0}
+    tx = {m: int(round(k9_us))}
+    d_grid = tuple(sorted({1, D}))
     cps = tuple(CutpointTimes({m: max(1, round(stage_f[s]))}, {m: max(1, round(stage_b[s]))},
-                              z, z, z, z, z, z, {d: 0 for d in sorted({1, D})}) for s in range(P))
-    prof = CalibrationProfile((m,), tuple(sorted({1, D})), cps)
+                              tx, tx, tx, {m: 0}, tx, {m: 0},
+                              {d: (int(round(stage_ar[s])) if d == D and D > 1 else 0)
+                               for d in d_grid}) for s in range(P))
+    prof = CalibrationProfile((m,), d_grid, cps)
     model = ModelSpec("stages", (1,) * P, (1,) * P)
     pc = ParallelConfig(P, D, m, N, tuple(range(P)))
-    r = simulate_minibatch(sched, pc, prof, build_placement(uniform_cluster(P * D, 8), P, D),
-                           model, opportunistic=False, recompute_scale=rscale)
-    return round(r.bubble_fraction, 4)
+    r = simulate_minibatch(generate_varuna_schedule(P, N, 1.0, 2.0, 1.0), pc, prof,
+                           build_placement(uniform_cluster(P * D, 8), P, D), model,
+                           opportunistic=opportunistic, recompute_scale=rscale)
+    return {"bubble": round(r.bubble_fraction, 4), "minibatch_us": int(r.minibatch_us)}
 
 
 if __name__ == "__main__":

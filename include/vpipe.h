@@ -284,6 +284,12 @@ int vp_adam_step(float* master, void* weight_bf16, float* grad, float* exp_avg, 
 
 /* Cast fp32 -> bf16 (n elements). */
 int vp_cast_f32_bf16(const float* x, void* y, int64_t n, void* stream);
+/* DP gradient exchange in bf16 (C1): pack a bucket of the fp32 gradient
+ * accumulator to bf16 before the allreduce, unpack the reduced sum back
+ * (16-byte aligned buffers). Halves the payload of sp/calibration.py:162-176
+ * (2 bytes per parameter, sp/core.py:17-18). */
+int vp_grad_pack_bf16(const float* x, void* y, int64_t n, void* stream);
+int vp_grad_unpack_bf16(const void* x, float* y, int64_t n, void* stream);
 
 /* ======================================================================
  * Inter-stage P2P over NVLink (device-initiated copies into registered

@@ -642,6 +642,33 @@ __global__ void cast_kernel(const float* __restrict__ x, __nv_bfloat16* __restri
   if (i < n) y[i] = __float2bfloat16(x[i]);
 }
 
+// fp32 <-> bf16 gradient buckets of the DP exchange, 8 elements per thread
+// (16-byte bf16 vectors, two float4) with a scalar tail.
+__global__ void pack_bf16_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ y,
+                                 int64_t n) {
+  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 8;
+  if (i + 8 <= n) {
+    const float4 a = reinterpret_cast<const float4*>(x + i)[0];
+    const float4 b = reinterpret_cast<const float4*>(x + i)[1];
+    const float f[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    *reinterpret_cast<uint4*>(y + i) = pack8(f);
+  } else {
+    for (int64_t k = i; k < n; ++k) y[k] = __float2bfloat16(x[k]);
+  }
+}
+__global__ void unpack_bf16_kernel(const __nv_bfloat16* __restrict__ x, float* __restrict__ y,
+                                   int64_t n) {
+  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 8;
+  if (i + 8 <= n) {
+    float f[8];
+    unpack8(*reinterpret_cast<const uint4*>(x + i), f);
+    reinterpret_cast<float4*>(y + i)[0] = make_float4(f[0], f[1], f[2], f[3]);
+    reinterpret_cast<float4*>(y + i)[1] = make_float4(f[4], f[5], f[6], f[7]);
+  } else {
+    for (int64_t k = i; k < n; ++k) y[k] = __bfloat162float(x[k]);
+  }
+}
+
 inline unsigned blocks_for(int64_t n, int per_block) {
   return static_cast<unsigned>((n + per_block - 1) / per_block);
 }
@@ -842,5 +869,21 @@ extern "C" int vp_adam_step(float* master, void* weight_bf16, float* grad, float
 extern "C" int vp_cast_f32_bf16(const float* x, void* y, int64_t n, void* stream) {
   if (n <= 0) return VP_OK;
   cast_kernel<<<blocks_for(n, 256), 256, 0, ST>>>(x, BF(y), n);
+  return launch_status();
+}
+
+extern "C" int vp_grad_pack_bf16(const float* x, void* y, int64_t n, void* stream) {
+  if (n <= 0) return VP_OK;
+  if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(y) & 15))
+    return VP_ERR_UNSUPPORTED;
+  pack_bf16_kernel<<<blocks_for(n, 256 * 8), 256, 0, ST>>>(x, BF(y), n);
+  return launch_status();
+}
+
+extern "C" int vp_grad_unpack_bf16(const void* x, float* y, int64_t n, void* stream) {
+  if (n <= 0) return VP_OK;
+  if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(y) & 15))
+    return VP_ERR_UNSUPPORTED;
+  unpack_bf16_kernel<<<blocks_for(n, 256 * 8), 256, 0, ST>>>(CBF(x), y, n);
   return launch_status();
 }

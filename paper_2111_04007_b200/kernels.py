@@ -36,6 +36,8 @@ _SIGS = {
                             vp, u32, vp, vp],
     "vp_attention_fwd_ex": [vp, vp, vp, i64, i64, i64, i64, c_int, f32, vp, u32, vp],
     "vp_set_seed": [vp, u64, vp],
+    "vp_grad_pack_bf16": [vp, vp, i64, vp],
+    "vp_grad_unpack_bf16": [vp, vp, i64, vp],
     "vp_dropout_dev": [vp, i64, f32, vp, u32, vp],
     "vp_dropout_bwd": [vp, vp, i64, i64, f32, vp, u32, vp, vp, vp],
     "vp_gemm_bf16_dropout": [c_int, c_int, vp, i64, vp, i64, vp, i64, vp, vp, i64, i64, i64, i64,
@@ -377,6 +379,18 @@ def adam_step(master, weight, grad, m, v, flags, lr, beta1, beta2, eps, weight_d
                          v.data_ptr(), master.numel(), flags.data_ptr(), lr, beta1, beta2, eps,
                          weight_decay, inv_loss_scale, max_grad_norm, bc1, bc2, _stream(stream)),
           "vp_adam_step")
+
+
+def grad_pack_bf16(x, y, stream=None):
+    _count(1)
+    check(L.vp_grad_pack_bf16(x.data_ptr(), y.data_ptr(), x.numel(), _stream(stream)),
+          "vp_grad_pack_bf16")
+
+
+def grad_unpack_bf16(x, y, stream=None):
+    _count(1)
+    check(L.vp_grad_unpack_bf16(x.data_ptr(), y.data_ptr(), x.numel(), _stream(stream)),
+          "vp_grad_unpack_bf16")
 
 
 def cast_f32_bf16(x, y, stream=None):

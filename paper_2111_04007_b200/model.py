@@ -581,12 +581,14 @@ class GPT2Stage:
 
     def backward(self, grad_out: Optional[torch.Tensor], ids: Optional[torch.Tensor],
                  dseed: Optional[int] = None, stream=None,
-                 types: Optional[torch.Tensor] = None) -> torch.Tensor:
+                 types: Optional[torch.Tensor] = None, layer_done=None) -> torch.Tensor:
         """Backward through the stage's layers using the saved working set.
         ``grad_out`` = d(stage output) from the next stage (None on the last
         stage, where loss_and_head_backward already filled ``self.g``).
         Returns d(stage input) (in ``self.g``); on stage 0 it is consumed by
-        the embedding backward instead."""
+        the embedding backward instead. ``layer_done(li)`` is called (host
+        side, in stream order) once layer li's parameter gradients are
+        final — the executor hangs its per-layer DP buckets on it."""
         cfg, P = self.cfg, self.params
         if dseed is not None:
             K.set_seed(self.seed_buf, dseed, stream)
@@ -608,6 +610,8 @@ class GPT2Stage:
                 lower = self.spec.layers[i - 1] if i > 0 else None
                 fc2_done = self._layer_bwd(li, self.ws[i], self.xs[i], stream,
                                            fc2_done=fc2_done, lower=lower)
+            if layer_done is not None:
+                layer_done(li)
         if self.spec.first:
             K.dropout_dev_(self.g, cfg.dropout, self.seed_buf, SALT_EMBED, stream)
             if self.bert:

@@ -137,12 +137,16 @@ def synthetic_batch(cfg: GPT2Config, rows: int, replica: int, step: int = 0, see
 
 
 class _Shm:
-    """Per-(sender rank, direction, slot) int64 sequence counters shared by
-    the processes of one box."""
+    """Per-(rank, channel, slot) int64 sequence counters in POSIX shared
+    memory, shared by the processes of one box. Channels: data posted by a
+    ring's producer (ACT, GRAD) and credits posted by its consumer
+    (FREE_ACT, FREE_GRAD)."""
+
+    CHANNELS = 6   # ACT, GRAD data; FREE_ACT, FREE_GRAD credits; DL_SEQ, DL_TIME (live dispatch)
 
     def __init__(self, name: str, world: int, slots: int, create: bool):
-        self.shape = (world, 2, slots)
-        nbytes = 8 * world * 2 * slots
+        self.shape = (world, self.CHANNELS, slots)
+        nbytes = 8 * world * self.CHANNELS * slots
         if create:
             try:
                 old = shared_memory.SharedMemory(name=name)
@@ -162,17 +166,20 @@ class _Shm:
         self.arr = np.ndarray(self.shape, dtype=np.int64, buffer=self.shm.buf)
         self.owner = create
 
-    def post(self, rank, direction, slot, seq):
-        self.arr[rank, direction, slot] = seq
+    def post(self, rank, channel, slot, seq):
+        self.arr[rank, channel, slot] = seq
 
-    def wait(self, rank, direction, slot, seq, timeout=600.0):
+    def ready(self, rank, channel, slot, seq) -> bool:
+        return self.arr[rank, channel, slot] >= seq
+
+    def wait(self, rank, channel, slot, seq, timeout=600.0):
         a = self.arr
-        if a[rank, direction, slot] >= seq:
+        if a[rank, channel, slot] >= seq:
             return
         t0 = time.monotonic()
-        while a[rank, direction, slot] < seq:
+        while a[rank, channel, slot] < seq:
             if time.monotonic() - t0 > timeout:
-                raise TimeoutError(f"p2p handshake timed out (peer {rank}, dir {direction}, "
+                raise TimeoutError(f"p2p handshake timed out (peer {rank}, channel {channel}, "
                                    f"slot {slot}, seq {seq})")
             time.sleep(20e-6)
 
@@ -185,44 +192,101 @@ class _Shm:
                 pass
 
 
+def in_flight(order) -> int:
+    """Largest number of forwards a stage has issued whose backward it has
+    not yet started, over its task order (max prefix #F - #B; the
+    reference's Schedule.in_flight_bound, sp/scheduler.py:88-97, taken on
+    the order actually dispatched)."""
+    cur = best = 0
+    for kind, _ in order:
+        if kind == F:
+            cur += 1
+            best = max(best, cur)
+        elif kind == B:
+            cur -= 1
+    return best
+
+
+# Ring slots beyond the producer's in-flight bound (the reference pads the
+# opportunistic stash the same way, DEFAULT_STASH_PAD, sp/simulator.py:
+# 256, 309-312), and gradient-ring credits: a stage consumes gradients in
+# ascending micro-batch order right after they land (rule 1 JIT recompute).
+RING_PAD = 2
+GRAD_SLOTS = 4
+
+
+def ring_slots(orders, P: int, N: int):
+    """(activation slots, gradient slots) of every stage's receive rings.
+    Stage k >= 1 receives activations F(j) of stage k-1 and holds slot j
+    until its own B(j); k-1 starts B(j) only after k's B(j) (the gradient
+    dependency), so at most in_flight(order[k-1]) slots are live."""
+    act = [0] + [min(N, in_flight(orders[k - 1]) + RING_PAD) for k in range(1, P)]
+    grad = [min(N, GRAD_SLOTS) for _ in range(P - 1)] + [0]
+    return act, grad
+
+
 class _Links:
     """IPC-registered activation / gradient rings between adjacent stages of
-    one replica. Ring slot j holds micro-batch j of the current mini-batch;
-    a slot is rewritten only in the next mini-batch, after its consumer B(j)
-    has completed (guaranteed by the schedule's dependency chain)."""
+    one replica, BOUNDED: the receiver's activation ring has in_flight(
+    upstream order) + RING_PAD slots, its gradient ring GRAD_SLOTS, not one
+    per micro-batch (8.3B at N_m = 1024 would need 24 GiB per ring).
+
+    Micro-batch g (a global counter, (step-1)*N + j + 1) uses slot g mod n.
+    Data: the producer writes the slot on its stream, records the slot's
+    data event (IPC) and posts g (shm); the consumer waits for g on the host,
+    then makes its stream wait on the event. Credits: when the consumer's
+    last reader of the slot (B(j)) is enqueued it records the slot's free
+    event and posts g; before writing g the producer waits for credit
+    g - n on the host and on the device. No host synchronisation with the
+    GPU on the data path."""
 
     ACT, GRAD = 0, 1
+    FREE = 2   # channel offset of the credits
 
-    def __init__(self, rank, stage, P, n_micro, slot_elems, gloo_group, shm):
-        self.rank, self.stage, self.P, self.N = rank, stage, P, n_micro
+    def __init__(self, rank, stage, P, slots_act, slots_grad, slot_elems, gloo_group, shm):
+        self.rank, self.stage, self.P = rank, stage, P
         self.slot_bytes = slot_elems * 2
         self.shm = shm
-        self.rx = {}       # direction -> DeviceBuffer (local ring I receive into)
-        self.tx_events = {}  # direction -> [event handles I record]
+        up, down = rank - 1, rank + 1
+        # direction -> (local ring, slots) I receive into
+        self.rx, self.rx_n = {}, {}
+        self.data_tx, self.free_tx = {}, {}   # events I record: data (I produce), free (I consume)
         mine = {"rank": rank}
-        if stage > 0:      # receive activations, send gradients upstream
-            buf = K.DeviceBuffer(n_micro * self.slot_bytes)
-            self.rx[self.ACT] = buf
-            mine["act_ring"] = self._mem_handle(buf.ptr)
-            self.tx_events[self.GRAD], mine["grad_events"] = self._events(n_micro)
-        if stage < P - 1:  # receive gradients, send activations downstream
-            buf = K.DeviceBuffer(n_micro * self.slot_bytes)
-            self.rx[self.GRAD] = buf
-            mine["grad_ring"] = self._mem_handle(buf.ptr)
-            self.tx_events[self.ACT], mine["act_events"] = self._events(n_micro)
+        if stage > 0:        # receive activations from up, send gradients to up
+            self.rx_n[self.ACT] = slots_act[stage]
+            self.rx[self.ACT] = K.DeviceBuffer(slots_act[stage] * self.slot_bytes)
+            mine["act_ring"] = self._mem_handle(self.rx[self.ACT].ptr)
+            self.free_tx[self.ACT], mine["act_free"] = self._events(slots_act[stage])
+            self.data_tx[self.GRAD], mine["grad_data"] = self._events(slots_grad[stage - 1])
+        if stage < P - 1:    # receive gradients from down, send activations to down
+            self.rx_n[self.GRAD] = slots_grad[stage]
+            self.rx[self.GRAD] = K.DeviceBuffer(slots_grad[stage] * self.slot_bytes)
+            mine["grad_ring"] = self._mem_handle(self.rx[self.GRAD].ptr)
+            self.free_tx[self.GRAD], mine["grad_free"] = self._events(slots_grad[stage])
+            self.data_tx[self.ACT], mine["act_data"] = self._events(slots_act[stage + 1])
         world = dist.get_world_size()
         allinfo = [None] * world
         dist.all_gather_object(allinfo, mine, group=gloo_group)
-        self.peer_ring = {}    # direction -> mapped peer base pointer I write into
-        self.rx_events = {}    # direction -> [opened peer events I wait on]
+        self.peer_ring, self.tx_n = {}, {}   # direction -> mapped peer ring I write, its slots
+        self.data_rx, self.free_rx = {}, {}  # opened peer events I wait on
         if stage > 0:
-            up = allinfo[rank - 1]
-            self.peer_ring[self.GRAD] = self._open_mem(up["grad_ring"])
-            self.rx_events[self.ACT] = [self._open_event(h) for h in up["act_events"]]
+            info = allinfo[up]
+            self.peer_ring[self.GRAD] = self._open_mem(info["grad_ring"])
+            self.tx_n[self.GRAD] = slots_grad[stage - 1]
+            self.data_rx[self.ACT] = [self._open_event(h) for h in info["act_data"]]
+            self.free_rx[self.GRAD] = [self._open_event(h) for h in info["grad_free"]]
         if stage < P - 1:
-            down = allinfo[rank + 1]
-            self.peer_ring[self.ACT] = self._open_mem(down["act_ring"])
-            self.rx_events[self.GRAD] = [self._open_event(h) for h in down["grad_events"]]
+            info = allinfo[down]
+            self.peer_ring[self.ACT] = self._open_mem(info["act_ring"])
+            self.tx_n[self.ACT] = slots_act[stage + 1]
+            self.data_rx[self.GRAD] = [self._open_event(h) for h in info["grad_data"]]
+            self.free_rx[self.ACT] = [self._open_event(h) for h in info["act_free"]]
+        self.peer = {self.ACT: up, self.GRAD: down}   # producer of what I receive
+        self.consumer = {self.ACT: down, self.GRAD: up}
+
+    @property
+    def ring_bytes(self) -> int:
+        return sum(n * self.slot_bytes for n in self.rx_n.values())
 
     @staticmethod
     def _mem_handle(ptr):
@@ -259,34 +323,68 @@ class _Links:
         for ptr in self.peer_ring.values():
             check(K.L.vp_ipc_close_mem_handle(ptr), "vp_ipc_close_mem_handle")
         self.peer_ring = {}
-        for evs in list(self.rx_events.values()) + list(self.tx_events.values()):
-            for e in evs:
-                check(K.L.vp_event_destroy(e), "vp_event_destroy")
-        self.rx_events, self.tx_events = {}, {}
+        for d in (self.data_rx, self.free_rx, self.data_tx, self.free_tx):
+            for evs in d.values():
+                for e in evs:
+                    check(K.L.vp_event_destroy(e), "vp_event_destroy")
+            d.clear()
 
     def free_local(self):
         for buf in self.rx.values():
             buf.free()
         self.rx = {}
 
-    def rx_slot(self, direction, j, shape):
-        return self.rx[direction].tensor(shape, torch.bfloat16, j * self.slot_bytes)
+    # ---- receiver side
+    def rx_slot(self, direction, g, shape):
+        s = g % self.rx_n[direction]
+        return self.rx[direction].tensor(shape, torch.bfloat16, s * self.slot_bytes)
 
-    def peer_slot_ptr(self, direction, j):
-        return self.peer_ring[direction] + j * self.slot_bytes
+    def arrived(self, direction, g) -> bool:
+        """Host view: the producer has enqueued micro-batch g's write."""
+        return self.shm.ready(self.peer[direction], direction, g % self.rx_n[direction], g)
 
-    def signal(self, direction, j, seq, stream):
-        """After the producing work on ``stream``: record the slot's IPC event,
-        then publish the sequence number to the receiver's host."""
-        check(K.L.vp_event_record(self.tx_events[direction][j], stream.cuda_stream),
-              "vp_event_record")
-        self.shm.post(self.rank, direction, j, seq)
+    def landed(self, direction, g) -> bool:
+        """Device view (after ``arrived``): the write has completed."""
+        s = g % self.rx_n[direction]
+        return K.L.vp_event_query(self.data_rx[direction][s]) == 0
 
-    def wait(self, direction, j, seq, stream):
-        peer = self.rank - 1 if direction == self.ACT else self.rank + 1
-        self.shm.wait(peer, direction, j, seq)
-        check(K.L.vp_stream_wait_event(stream.cuda_stream, self.rx_events[direction][j]),
+    def wait(self, direction, g, stream):
+        """Order ``stream`` after the producer's write of micro-batch g."""
+        s = g % self.rx_n[direction]
+        self.shm.wait(self.peer[direction], direction, s, g)
+        check(K.L.vp_stream_wait_event(stream.cuda_stream, self.data_rx[direction][s]),
               "vp_stream_wait_event")
+
+    def release(self, direction, g, stream):
+        """After the last reader of micro-batch g's slot is enqueued on
+        ``stream``: record the slot's free event and post the credit."""
+        s = g % self.rx_n[direction]
+        check(K.L.vp_event_record(self.free_tx[direction][s], stream.cuda_stream),
+              "vp_event_record")
+        self.shm.post(self.rank, self.FREE + direction, s, g)
+
+    # ---- producer side
+    def peer_slot_ptr(self, direction, g):
+        return self.peer_ring[direction] + (g % self.tx_n[direction]) * self.slot_bytes
+
+    def acquire(self, direction, g, stream):
+        """Before writing micro-batch g into the peer ring: wait (host, then
+        device) until the slot's previous occupant g - n was released."""
+        n = self.tx_n[direction]
+        if g - n < 1:
+            return
+        s = g % n
+        self.shm.wait(self.consumer[direction], self.FREE + direction, s, g - n)
+        check(K.L.vp_stream_wait_event(stream.cuda_stream, self.free_rx[direction][s]),
+              "vp_stream_wait_event")
+
+    def signal(self, direction, g, stream):
+        """After the producing work on ``stream``: record the slot's data
+        event, then publish g to the receiver's host."""
+        s = g % self.tx_n[direction]
+        check(K.L.vp_event_record(self.data_tx[direction][s], stream.cuda_stream),
+              "vp_event_record")
+        self.shm.post(self.rank, direction, s, g)
 
 
 def group_ranks(P: int, D: int) -> Dict[str, List[List[int]]]:
@@ -318,7 +416,7 @@ def exchange_stage_means(means, rank: int, world: int, device="cpu", group=None)
 
 
 def retune_order(schedule: Schedule, P: int, D: int, m: int, N: int, hidden: int, seq_len: int,
-                 table: torch.Tensor, current) -> list:
+                 table: torch.Tensor, current, max_in_flight: Optional[int] = None) -> list:
     """Pick the per-stage dispatch order with the shortest simulated
     mini-batch under the measured stage times (replica 0's rows of
     ``table``): candidates are the static Varuna order, the order in use
@@ -354,6 +452,8 @@ def retune_order(schedule: Schedule, P: int, D: int, m: int, N: int, hidden: int
     place = build_placement(uniform_cluster(P * D, max(P * D, 1)), P, D)
     best, best_t = None, None
     for order in cands:
+        if max_in_flight is not None and any(in_flight(o) > max_in_flight for o in order):
+            continue   # would overrun the bounded activation rings
         kinds, mbs, offs = [], [], [0]
         for k in range(P):
             kinds += [a for a, _ in order[k]]
@@ -366,6 +466,17 @@ def retune_order(schedule: Schedule, P: int, D: int, m: int, N: int, hidden: int
         if best_t is None or t < best_t:
             best, best_t = order, t
     return best
+
+
+@dataclass
+class _StepCtx:
+    g0: int                 # global micro-batch number of this step's j = 0
+    data: dict
+    scale: float
+    ev: Optional[list]
+    graphs: bool
+    x_in: dict = field(default_factory=dict)
+    executed: list = field(default_factory=list)
 
 
 class Varuna:
@@ -430,24 +541,38 @@ class Varuna:
         self.spec = StageSpec(self.stage_id, P, layers)
         self.stage = GPT2Stage(model, self.spec, self.m, self.device, seed, init_device)
         self.schedule: Schedule = generate_varuna_schedule(P, self.N, 1.0, 2.0, 1.0)
-        kinds, mbs = self.schedule.stage_slice(self.stage_id)
-        if dispatch == "static":
-            self.tasks = list(zip(kinds.tolist(), mbs.tolist()))
+        plan = [list(zip(*[a.tolist() for a in self.schedule.stage_slice(k)])) for k in range(P)]
+        if dispatch in ("static", "live"):
+            orders = plan
         elif dispatch == "opportunistic":
-            self.tasks = self._opportunistic_order(profile)
+            orders = self._opportunistic_orders(profile)
         else:
-            raise ConfigError(f"dispatch must be 'static' or 'opportunistic', not {dispatch!r}")
+            raise ConfigError(f"dispatch must be 'static', 'opportunistic' or 'live', "
+                              f"not {dispatch!r}")
+        self.tasks = list(orders[self.stage_id])
         self.dispatch = dispatch
         self._check_plan()
+        if dispatch == "static":
+            assert self.tasks == plan[self.stage_id]   # executed order == the plan arrays
+        # bounded rings: one slot count for every activation ring (so a
+        # task's slot pointers repeat every n_ring micro-batches and its
+        # captured graph can be reused), a multiple of the gradient ring's
+        self.n_grad = min(self.N, GRAD_SLOTS)
+        need = max(in_flight(o) for o in orders) + RING_PAD
+        self.n_ring = min(self.N, -(-need // self.n_grad) * self.n_grad)
+        # live dispatch: per-stage policy state + measured task durations
+        self._profile = profile
+        self._est = {F: 0.0, R: 0.0, B: 0.0}
         self.trace = trace
         self.loss_sum = torch.zeros(1, device=self.device)
         self.flags = torch.zeros(2, device=self.device)
         self._setup_groups()
         if P > 1:
             slot_elems = self.m * model.seq_len * model.hidden
-            self.links = _Links(self.rank, self.stage_id, P, self.N, slot_elems,
-                                self.gloo, self.shm)
+            self.links = _Links(self.rank, self.stage_id, P, [0] + [self.n_ring] * (P - 1),
+                                [self.n_grad] * (P - 1) + [0], slot_elems, self.gloo, self.shm)
         self.gpu_launches_per_step = None
+        self._setup_dp()
         # Each task's launch sequence (tens to hundreds of kernels) is captured
         # once into a CUDA graph and replayed: the per-launch host cost would
         # otherwise approach the GPU time of the short kernels. Inputs reach
@@ -464,10 +589,10 @@ class Varuna:
         self._in_labels = torch.zeros(T, dtype=torch.int64, device=self.device)
 
     # ---------------------------------------------------------------- setup
-    def _opportunistic_order(self, profile):
-        """This stage's dispatch order as the reference's opportunistic replica
-        kernel runs the schedule under ``profile`` (default: the generator's
-        own 1:2:1 F:B:R times per cut-point, no transfer cost)."""
+    def _opportunistic_orders(self, profile):
+        """Every stage's dispatch order as the reference's opportunistic
+        replica kernel runs the schedule under ``profile`` (default: the
+        generator's own 1:2:1 F:B:R times per cut-point, no transfer cost)."""
         from .calibration import uniform_profile
         from .core import make_block_model
         from .simulator import execution_order
@@ -476,8 +601,7 @@ class Varuna:
             profile = uniform_profile(cfg.n_layer, 1.0, 2.0, m_grid=(self.m,),
                                       d_grid=tuple(sorted({1, self.D})))
         model = make_block_model("stages", cfg.n_layer, cfg.hidden, cfg.seq_len)
-        order = execution_order(self.schedule, pc, profile, model, opportunistic=True)
-        return order[self.stage_id]
+        return execution_order(self.schedule, pc, profile, model, opportunistic=True)
 
     def retune_dispatch(self, timeline: dict) -> None:
         """Re-derive the opportunistic dispatch order from MEASURED task
@@ -492,15 +616,21 @@ class Varuna:
         else:
             current = [self.tasks]
         best = retune_order(self.schedule, self.P, self.D, self.m, self.N, self.cfg.hidden,
-                            self.cfg.seq_len, table, current[:self.P])
+                            self.cfg.seq_len, table, current[:self.P],
+                            max_in_flight=self.n_ring - RING_PAD if self.P > 1 else None)
         self.tasks = best[self.stage_id]
         self.dispatch = "opportunistic"
         self._check_plan()
 
     def _check_plan(self):
-        """The executor relies on rule 2 (R(j) directly before B(j)) and on the
-        last stage's F(j)/B(j) alternation (sp/scheduler.py:228-241)."""
+        """The executor relies on rule 2 (R(j) directly before B(j)), on the
+        last stage's F(j)/B(j) alternation (sp/scheduler.py:228-241) and on
+        backwards in ascending micro-batch order (the gradient rings are
+        consumed in order)."""
         last = self.spec.last
+        bs = [j for kind, j in self.tasks if kind == B]
+        if bs != sorted(bs):
+            raise ConfigError(f"stage {self.stage_id}: backwards out of micro-batch order")
         for i, (kind, j) in enumerate(self.tasks):
             if kind == B:
                 prev = self.tasks[i - 1] if i else None
@@ -508,6 +638,64 @@ class Varuna:
                 if prev != (want, j):
                     raise ConfigError(f"stage {self.stage_id}: B{j + 1} not preceded by "
                                       f"{'F' if last else 'R'}{j + 1}")
+
+    def _setup_dp(self):
+        """C1 buckets: one per transformer layer of the stage (its gradients
+        are final once the LAST backward of the step has passed it — they are
+        exchanged on a side stream while that backward continues down the
+        stage) plus the embedding / head remainder after it. The payload is
+        bf16 (2 B/param, the reference's pricing, sp/calibration.py:162-176)
+        packed from the fp32 accumulators and unpacked after the sum."""
+        self._comm = None
+        self._ar_spans = []
+        if self.D == 1:
+            return
+        from .model import layer_param_shapes
+        P = self.stage.params
+        self._comm = torch.cuda.Stream(self.device)
+        self._gbf = torch.empty(P.numel, dtype=torch.bfloat16, device=self.device)
+        names = [n for n, _ in layer_param_shapes(self.cfg)]
+        self._layer_seg = {li: P.segment([f"l{li}.{n}" for n in names])
+                           for li in self.spec.layers}
+        cuts = sorted(self._layer_seg.values())
+        rest, pos = [], 0
+        for lo, hi in cuts:
+            if lo > pos:
+                rest.append((pos, lo))
+            pos = max(pos, hi)
+        if pos < P.numel:
+            rest.append((pos, P.numel))
+        self._rest_seg = rest
+        self._layer_ev = {li: torch.cuda.Event(external=True) for li in self.spec.layers}
+        self._last_b = max(j for kind, j in self.tasks if kind == B)
+
+    def _dp_bucket(self, lo, hi):
+        """Pack, allreduce (bf16) and unpack gradient[lo:hi] on the comm
+        stream; the span is timed (the measured AR work of the bubble)."""
+        P, comm = self.stage.params, self._comm
+        with torch.cuda.stream(comm):
+            e0 = torch.cuda.Event(enable_timing=True) if self.trace else None
+            if e0 is not None:
+                e0.record(comm)
+            K.grad_pack_bf16(P.grad[lo:hi], self._gbf[lo:hi], stream=comm)
+            w = dist.all_reduce(self._gbf[lo:hi], group=self.dp_group, async_op=True)
+            w.wait()
+            K.grad_unpack_bf16(self._gbf[lo:hi], P.grad[lo:hi], stream=comm)
+            if e0 is not None:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record(comm)
+                self._ar_spans.append((e0, e1))
+
+    def _layer_mark(self, li):
+        self._layer_ev[li].record(self.stream)
+
+    def _start_dp_layers(self):
+        """After the last backward is enqueued: one bucket per layer, each
+        behind the event its layer's backward recorded (top layer first)."""
+        for li in reversed(self.spec.layers):
+            self._comm.wait_event(self._layer_ev[li])
+            lo, hi = self._layer_seg[li]
+            self._dp_bucket(lo, hi)
 
     def _setup_groups(self):
         P, D = self.P, self.D
@@ -583,7 +771,6 @@ class Varuna:
         self.step_count += 1
         if not self.active:
             return StepResult(None, torch.zeros(2), 1.0 / self.loss_scale)
-        seq_no = self.step_count
         st = self.stream
         cfg, stage = self.cfg, self.stage
         # loss = mean over the M_total samples' label tokens (BERT: the
@@ -591,48 +778,22 @@ class Varuna:
         total_tokens = self.global_batch * (cfg.mlm_per_seq if cfg.arch == "bert" else cfg.seq_len)
         scale = self.loss_scale / total_tokens
         ev = [] if self.trace else None
+        self._ar_spans = []
         st.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(st):
             data = self._device_batch(batch)
             if self.spec.last:
                 self.loss_sum.zero_()
             t_start = self._mark(ev)
-            x_in = {}
-            graphs = self.use_graphs and not K.GEMM_TIMING["on"] and self.step_count > 1
-            for kind, j in self.tasks:
-                # inputs first (stream waits on the peer's IPC event), so the
-                # task's timing events bracket compute only
-                if kind != B and not self.spec.first and j not in x_in:
-                    self.links.wait(_Links.ACT, j, seq_no, st)
-                    x_in[j] = self.links.rx_slot(_Links.ACT, j, (stage.T, cfg.hidden))
-                g_in = None
-                if kind == B and not self.spec.last:
-                    self.links.wait(_Links.GRAD, j, seq_no, st)
-                    g_in = self.links.rx_slot(_Links.GRAD, j, (stage.T, cfg.hidden))
-                if self.spec.first:
-                    self._in_ids.copy_(data["ids"][j], non_blocking=True)
-                    if "types" in data:
-                        self._in_types.copy_(data["types"][j], non_blocking=True)
-                if self.spec.last and kind == B:
-                    self._in_labels.copy_(data["labels"][j], non_blocking=True)
-                if cfg.dropout > 0:
-                    K.set_seed(stage.seed_buf, task_seed(self.seed, self.step_count,
-                                                         self.replica * self.N + j), st)
-                e0 = self._mark(ev)
-                body = (lambda kind=kind, j=j, g_in=g_in:
-                        self._task(kind, j, x_in.get(j), g_in, scale, st, "types" in data))
-                if graphs:
-                    self._replay(kind, j, body, st)
-                else:
-                    body()
-                if kind == F and not self.spec.last:
-                    self.links.signal(_Links.ACT, j, seq_no, st)
-                if kind == B:
-                    if not self.spec.first:
-                        self.links.signal(_Links.GRAD, j, seq_no, st)
-                    x_in.pop(j, None)
-                if ev is not None:
-                    ev.append((kind, j, e0, self._mark(ev)))
+            ctx = _StepCtx(g0=(self.step_count - 1) * self.N + 1, data=data, scale=scale, ev=ev,
+                           graphs=self.use_graphs and not K.GEMM_TIMING["on"]
+                           and self.step_count > 1)
+            if self.dispatch == "live":
+                self._run_live(ctx)
+            else:
+                for kind, j in self.tasks:
+                    self._launch(kind, j, ctx)
+            self.executed = ctx.executed
             t_ar0 = self._mark(ev)
             self._sync_grads()
             t_ar1 = self._mark(ev)
@@ -649,9 +810,140 @@ class Varuna:
         loss = self.loss_sum if self.spec.last else None
         return StepResult(loss, self.flags, 1.0 / self.loss_scale, timeline)
 
-    def _task(self, kind, j, x, g_in, scale, st, typed):
+    def _launch(self, kind, j, ctx):
+        """Enqueue task (kind, j) on the compute stream: ring waits / credits,
+        the task's launches (graph replay), then the data signals and slot
+        releases. Micro-batch j of this step is global micro-batch g."""
+        st, stage, cfg, links = self.stream, self.stage, self.cfg, self.links
+        g = ctx.g0 + j
+        data = ctx.data
+        # inputs first (the stream waits on the peer's IPC event), so the
+        # task's timing events bracket compute only
+        if kind != B and not self.spec.first and j not in ctx.x_in:
+            links.wait(_Links.ACT, g, st)
+            ctx.x_in[j] = links.rx_slot(_Links.ACT, g, (stage.T, cfg.hidden))
+        g_in = None
+        if kind == B and not self.spec.last:
+            links.wait(_Links.GRAD, g, st)
+            g_in = links.rx_slot(_Links.GRAD, g, (stage.T, cfg.hidden))
+        # credits: the peer slot this task writes must have been released
+        if kind == F and not self.spec.last:
+            links.acquire(_Links.ACT, g, st)
+        if kind == B and not self.spec.first:
+            links.acquire(_Links.GRAD, g, st)
+        if self.spec.first:
+            self._in_ids.copy_(data["ids"][j], non_blocking=True)
+            if "types" in data:
+                self._in_types.copy_(data["types"][j], non_blocking=True)
+        if self.spec.last and kind == B:
+            self._in_labels.copy_(data["labels"][j], non_blocking=True)
+        if cfg.dropout > 0:
+            K.set_seed(stage.seed_buf, task_seed(self.seed, self.step_count,
+                                                 self.replica * self.N + j), st)
+        e0 = self._mark(ctx.ev)
+        x = ctx.x_in.get(j)
+
+        dp_hook = kind == B and self.D > 1 and j == self._last_b
+
+        def body():
+            self._task(kind, g, x, g_in, ctx.scale, st, "types" in data,
+                       layer_done=self._layer_mark if dp_hook else None)
+        if ctx.graphs:
+            key = (kind, g % self.n_ring) if links is not None else (kind, 0)
+            self._replay(key + (dp_hook,), body, st)
+        else:
+            body()
+        if dp_hook:
+            self._start_dp_layers()
+        if kind == F and not self.spec.last:
+            links.signal(_Links.ACT, g, st)
+        if kind == B:
+            if not self.spec.first:
+                links.signal(_Links.GRAD, g, st)
+                links.release(_Links.ACT, g, st)    # B(j) was the stash slot's last reader
+            if not self.spec.last:
+                links.release(_Links.GRAD, g, st)
+            ctx.x_in.pop(j, None)
+        if ctx.ev is not None:
+            ctx.ev.append((kind, j, e0, self._mark(ctx.ev)))
+        ctx.executed.append((kind, j))
+
+    # ------------------------------------------------------- live dispatch
+    def _run_live(self, ctx):
+        """Run this stage's tasks as the reference's opportunistic policy
+        decides them ON LINE (dispatch.StagePolicy = decide(),
+        sp/engine/py_kernel.py:250-322) from real arrivals: an activation has
+        arrived when the producer posted it and its IPC event completed; a
+        gradient is known once posted (arriving) and arrived on completion;
+        the rule-1 deadline of R(j) is announced by the downstream stage when
+        it starts B(j) (its start + measured T_b, minus our T_r). The stage
+        decides only when idle (its previous task complete), as the
+        reference does, so the host stays at most one task ahead."""
+        from .dispatch import StagePolicy
+        links = self.links
+        last, first = self.spec.last, self.spec.first
+        pol = StagePolicy(self.tasks, self.N, last, self.n_ring if not last else self.N,
+                          opportunistic=True)
+        down = self.rank + 1
+
+        def now_us():
+            return time.monotonic_ns() / 1000.0
+
+        def act_arr(mb):
+            if first:
+                return 0
+            g = ctx.g0 + mb
+            if links.arrived(_Links.ACT, g) and links.landed(_Links.ACT, g):
+                return 0
+            return -1
+
+        def grad_arr(mb):
+            g = ctx.g0 + mb
+            if not links.arrived(_Links.GRAD, g):
+                return -1
+            return 0 if links.landed(_Links.GRAD, g) else now_us() + 1.0
+
+        def deadline(mb):
+            a = self.shm.arr
+            if a[down, 4, mb] != ctx.g0 + mb:
+                return -1
+            return a[down, 5, mb] / 1000.0 - self._est[R]
+
+        pending = None   # (pos, kind, done event, start event)
+        while not pol.done:
+            if pending is not None:
+                pos, kind, done, t0 = pending
+                if not done.query():
+                    time.sleep(10e-6)
+                    continue
+                pol.complete(pos)
+                dur = t0.elapsed_time(done) * 1e3
+                self._est[kind] = dur if self._est[kind] == 0 else 0.7 * self._est[kind] + 0.3 * dur
+                pending = None
+            now = now_us()
+            pos = pol.decide(now, act_arr, grad_arr, deadline, self._est[F], self._est[R])
+            if pos is None:
+                time.sleep(10e-6)
+                continue
+            kind, j = pol.kinds[pos], pol.mbs[pos]
+            pol.start(pos)
+            if kind == B and not first:
+                # rule-1 announcement to the stage below: our B(j) ends at
+                # now + T_b; its R(j) should then be done
+                self.shm.arr[self.rank, 5, j] = int((now + self._est[B]) * 1000.0)
+                self.shm.arr[self.rank, 4, j] = ctx.g0 + j
+            t0 = torch.cuda.Event(enable_timing=True)
+            t0.record(self.stream)
+            self._launch(kind, j, ctx)
+            done = torch.cuda.Event(enable_timing=True)
+            done.record(self.stream)
+            pending = (pos, kind, done, t0)
+        if pending is not None:
+            pass   # the last task is left running; the step's tail orders after it
+
+    def _task(self, kind, g, x, g_in, scale, st, typed, layer_done=None):
         """The launches of one schedule task on this stage (graph-capturable:
-        every pointer is fixed for a given (kind, micro-batch))."""
+        every pointer is fixed for a given (kind, ring slot))."""
         stage = self.stage
         ids = self._in_ids if self.spec.first else None
         types = self._in_types if (self.spec.first and typed) else None
@@ -659,20 +951,19 @@ class Varuna:
             save = kind == R or self.spec.last
             out_ptr = None
             if kind == F and not self.spec.last:
-                out_ptr = self.links.peer_slot_ptr(_Links.ACT, j)
+                out_ptr = self.links.peer_slot_ptr(_Links.ACT, g)
             stage.forward(x, ids, save=save, stream=st, out_ptr=out_ptr, types=types)
         else:
             if self.spec.last:
                 stage.loss_and_head_backward(self._in_labels, scale, self.loss_sum, stream=st)
-            g = stage.backward(g_in, ids, stream=st, types=types)
+            out = stage.backward(g_in, ids, stream=st, types=types, layer_done=layer_done)
             if not self.spec.first:
-                K.p2p_put(self.links.peer_slot_ptr(_Links.GRAD, j), g, stream=st)
+                K.p2p_put(self.links.peer_slot_ptr(_Links.GRAD, g), out, stream=st)
 
-    def _replay(self, kind, j, body, st):
-        """Run ``body`` through a CUDA graph captured on first use. Stages
-        without rings have the same pointers for every micro-batch, so one
-        graph per task kind serves them all."""
-        key = (kind, j) if self.links is not None else (kind, 0)
+    def _replay(self, key, body, st):
+        """Run ``body`` through a CUDA graph captured on first use, keyed by
+        (task kind, ring slot): the slot pointers repeat every n_ring
+        micro-batches. Stages without rings use one graph per task kind."""
         g = self._graphs.get(key)
         if g is None:
             n0 = K.LAUNCHES[0]
@@ -694,10 +985,17 @@ class Varuna:
         return e
 
     def _timeline(self, t0, ev, ar0, ar1, t_end):
+        """Per-task (kind, mb, start, end) in us from the step start on the
+        compute stream; ``allreduce_us`` the sync bracket (C1 tail, C3, C2 —
+        including waits on other stages), ``ar_work_us`` the C1 bucket work
+        itself (pack + NCCL + unpack spans on the comm stream, overlapping
+        the last backward) — the AR busy time of the bubble formula."""
         tasks = [(k, j, t0.elapsed_time(a) * 1e3, t0.elapsed_time(b) * 1e3) for k, j, a, b in ev]
         busy = sum(b - a for _, _, a, b in tasks)
+        spans = [(t0.elapsed_time(a) * 1e3, t0.elapsed_time(b) * 1e3) for a, b in self._ar_spans]
         return {"tasks": tasks, "allreduce_us": (t0.elapsed_time(ar0) * 1e3,
                                                  t0.elapsed_time(ar1) * 1e3),
+                "ar_spans": spans, "ar_work_us": sum(b - a for a, b in spans),
                 "step_us": t0.elapsed_time(t_end) * 1e3, "busy_us": busy}
 
     # --------------------------------------------------- gradients + update
@@ -713,7 +1011,13 @@ class Varuna:
     def _sync_grads(self):
         P = self.stage.params
         if self.D > 1:
-            dist.all_reduce(P.grad, group=self.dp_group)                       # C1
+            # C1: the per-layer buckets are in flight since the last backward;
+            # the embedding / head remainder follows, then the compute stream
+            # joins the comm stream
+            self._comm.wait_stream(self.stream)
+            for lo, hi in self._rest_seg:
+                self._dp_bucket(lo, hi)
+            self.stream.wait_stream(self._comm)
             if self.spec.last:
                 dist.all_reduce(self.loss_sum, group=self.dp_group)
         seg = self._tied_segment()

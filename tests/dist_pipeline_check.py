@@ -32,6 +32,8 @@ def main():
     ap.add_argument("--layers", type=int, default=0, help="cut the config to this many layers")
     ap.add_argument("--micro-batch", type=int, default=4)
     ap.add_argument("--dropout", type=float, default=0.0)
+    ap.add_argument("--steps", type=int, default=1,
+                    help="train steps-1 steps (AdamW on both sides), check the last")
     ap.add_argument("--global-batch", type=int, default=0,
                     help="M_total (default m*N*D); smaller values leave partial micro-batches")
     args = ap.parse_args()
@@ -62,18 +64,32 @@ def main():
         kinds, mbs = v.schedule.stage_slice(v.stage_id)
         moved = sum(a != b for a, b in zip(zip(kinds.tolist(), mbs.tolist()), v.tasks))
         print(f"rank {v.rank} dispatch order differs from static at {moved} positions", flush=True)
+    print(f"rank {v.rank} ring slots {v.n_ring} (act) {v.n_grad} (grad) for N_m = {N}", flush=True)
     shares = [min(max(M - r * m * N, 0), m * N) for r in range(D)]
-    batches = [{k: t[:shares[r]] for k, t in synthetic_batch(cfg, m * N, r).items()}
-               for r in range(D)]
-    res = v.step(batches[v.replica], apply=False)
-    torch.cuda.synchronize()
-    # oracle: D replicas' mini-batches, summed gradients
     o = PipelineOracle(cfg.n_layer, cfg.hidden, cfg.heads, cfg.vocab_size, cfg.seq_len,
                        pc.stage_map, m, N, seed=0, arch=cfg.arch, dropout=cfg.dropout)
     total = M * (cfg.mlm_per_seq if cfg.arch == "bert" else cfg.seq_len)
-    loss = sum(o.run_minibatch(b["input_ids"], b["labels"], total,
-                               types=b.get("token_type_ids"), step=1, replica=r)
-               for r, b in enumerate(batches))
+    for step in range(1, args.steps + 1):
+        batches = [{k: t[:shares[r]] for k, t in synthetic_batch(cfg, m * N, r,
+                                                                   step=step - 1).items()}
+                   for r in range(D)]
+        final = step == args.steps
+        res = v.step(batches[v.replica], apply=not final)
+        torch.cuda.synchronize()
+        if v.dispatch == "live":
+            # the executed order is a valid Varuna execution: rule 2 and the
+            # last stage's F/B alternation (checked against the policy's own
+            # bookkeeping: every task exactly once)
+            assert sorted(v.executed) == sorted(v.tasks), v.executed
+            for i, (kind, j) in enumerate(v.executed):
+                if kind == 0:
+                    assert v.executed[i - 1] == ((2 if v.spec.last else 1), j), v.executed
+        # oracle: D replicas' mini-batches, summed gradients
+        loss = sum(o.run_minibatch(b["input_ids"], b["labels"], total,
+                                   types=b.get("token_type_ids"), step=step, replica=r)
+                   for r, b in enumerate(batches))
+        if not final:
+            o.adamw_step(step)
     og = o.grads()
     ok = True
     for name, g in v.param_tensors("grad").items():

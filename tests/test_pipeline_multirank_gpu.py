@@ -34,6 +34,14 @@ PIPE_CASES = [
     # K7 dropout-recompute across stages and replicas: F on stage 0 and R
     # before B regenerate the same masks; replicas draw different ones
     (4, 2, 2, "tiny", ["--dropout", "0.1"]),
+    # bounded rings: N_m = 12 micro-batches through 8-slot rings, three
+    # steps (slots reused within and across steps; AdamW applied between)
+    (2, 2, 1, "tiny", ["--N", "12", "--micro-batch", "2", "--steps", "3"]),
+    (4, 4, 1, "tiny", ["--N", "10", "--micro-batch", "2", "--steps", "2"]),
+    # live opportunistic dispatch (StagePolicy on real arrivals)
+    (2, 2, 1, "tiny", ["--dispatch", "live", "--steps", "2"]),
+    (4, 2, 2, "tiny", ["--dispatch", "live", "--dropout", "0.1"]),
+    (4, 4, 1, "tiny", ["--dispatch", "live", "--N", "8", "--micro-batch", "2", "--steps", "2"]),
     (2, 2, 1, "tiny_bert", ["--dropout", "0.1"]),
     # BASELINE widths, two-layer cuts: 16 MiB (355M, m=1) and 1 MiB-per-row
     # (BERT-large) boundary messages through the rings
@@ -43,8 +51,7 @@ PIPE_CASES = [
 
 
 def _ids(c):
-    return (f"{c[3]}-{c[1]}x{c[2]}" + ("-M27" if "--global-batch" in c[4] else "")
-            + ("-p0.1" if "--dropout" in c[4] else ""))
+    return f"{c[3]}-{c[1]}x{c[2]}-" + "".join(a.strip("-")[:4] for a in c[4])
 
 
 def _check(p, token):
