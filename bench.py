@@ -69,6 +69,8 @@ def parse():
                          "measured stage times, keeping the fastest of a few perturbed "
                          "candidates (off by default)")
     ap.add_argument("--cpu-sample-s", type=float, default=20.0)
+    ap.add_argument("--trace-dir", default=None,
+                    help="write every rank's measured Gantt CSV of the traced step here")
     return ap.parse_args()
 
 
@@ -580,6 +582,11 @@ def main():
     mb_us = max_over_ranks(max(ends) if ends else 0.0)
     bubble = 1.0 - (busy_all[0].item() + busy_all[1].item()) / (world * mb_us) if mb_us else 0.0
     k9_us = measure_k9(v, P, dev)
+    if args.trace_dir:
+        os.makedirs(args.trace_dir, exist_ok=True)
+        with open(os.path.join(args.trace_dir, f"gantt_{P}x{D}_{dispatch}_rank{rank}.csv"),
+                  "w") as f:
+            f.write(v.gantt_csv(v.gantt_rows(tl)))
     gemm_tf = g_flops / (g_ms / 1e3) / 1e12 if g_ms else 0.0
     gemm_share = g_ms / (step_us / 1e3) if step_us else 0.0
     burst, sustained, hbm, src = peaks()
@@ -598,8 +605,13 @@ def main():
     roof_samples = D * m / worst
 
     # measured stage profile -> reference bubble predictor (simulate_minibatch)
+    # the dispatch used: the replayed opportunistic order is a FIXED order
+    # (computed by the replica kernel from the calibration profile), so it is
+    # predicted as that order run statically; live and static dispatch are
+    # the reference policy itself on the Varuna schedule
     predicted = predicted_bubble(v, tl, P, D, N, m, world, dev, dist,
-                                 opportunistic=dispatch != "static", k9_us=k9_us)
+                                 opportunistic=dispatch == "live", k9_us=k9_us,
+                                 replay=dispatch == "opportunistic")
 
     cpu = None
     control_plane = None
@@ -694,7 +706,8 @@ def measure_k9(v, P, dev):
     return round(t, 2)
 
 
-def predicted_bubble(v, tl, P, D, N, m, world, dev, dist, opportunistic=False, k9_us=0.0):
+def predicted_bubble(v, tl, P, D, N, m, world, dev, dist, opportunistic=False, k9_us=0.0,
+                     replay=False):
     """The reference's prediction for this run (simulate_minibatch,
     sp/simulator.py:259-389, on the C++ replica kernel): the Varuna schedule
     generate_varuna_schedule(P, N, 1, 2, 1) under the dispatch policy used
@@ -702,7 +715,8 @@ def predicted_bubble(v, tl, P, D, N, m, world, dev, dist, opportunistic=False, k
     calibration profile — one cut-point per stage carrying that stage's
     measured mean F and B (replica 0), R as a measured R/F ratio, the
     measured K9 put time as the intra-node act/grad transfer, and the stage's
-    measured C1 bucket work as its AR time."""
+    measured C1 bucket work as its AR time. ``replay``: the schedule is the
+    per-stage order actually executed (replica 0), simulated statically."""
     import torch
     from paper_2111_04007_b200 import (ModelSpec, ParallelConfig, build_placement,
                                        generate_varuna_schedule, simulate_minibatch,
@@ -733,7 +747,23 @@ def predicted_bubble(v, tl, P, D, N, m, world, dev, dist, opportunistic=False, k
     prof = CalibrationProfile((m,), d_grid, cps)
     model = ModelSpec("stages", (1,) * P, (1,) * P)
     pc = ParallelConfig(P, D, m, N, tuple(range(P)))
-    r = simulate_minibatch(generate_varuna_schedule(P, N, 1.0, 2.0, 1.0), pc, prof,
+    sched = generate_varuna_schedule(P, N, 1.0, 2.0, 1.0)
+    if replay:
+        import numpy as np
+        from paper_2111_04007_b200.scheduler import Schedule
+        orders = [None] * world
+        if world > 1:
+            dist.all_gather_object(orders, v.executed)
+        else:
+            orders = [v.executed]
+        kinds, mbs, offs = [], [], [0]
+        for s in range(P):          # replica 0's ranks are 0..P-1
+            kinds += [k for k, _ in orders[s]]
+            mbs += [j for _, j in orders[s]]
+            offs.append(len(kinds))
+        sched = Schedule("executed", P, N, np.array(kinds, np.int64), np.array(mbs, np.int64),
+                         np.array(offs, np.int64), 1, 2, 1)
+    r = simulate_minibatch(sched, pc, prof,
                            build_placement(uniform_cluster(P * D, 8), P, D), model,
                            opportunistic=opportunistic, recompute_scale=rscale)
     return {"bubble": round(r.bubble_fraction, 4), "minibatch_us": int(r.minibatch_us)}

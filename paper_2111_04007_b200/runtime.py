@@ -1046,8 +1046,9 @@ class Varuna:
         from .core import KIND_NAMES
         rows = [(self.stage_id + 1, KIND_NAMES[k], j + 1, int(round(a)), int(round(b)))
                 for k, j, a, b in timeline["tasks"]]
-        a0, a1 = timeline["allreduce_us"]
-        rows.append((self.stage_id + 1, "A", 0, int(round(a0)), int(round(a1))))
+        spans = timeline.get("ar_spans") or [timeline["allreduce_us"]]
+        for a0, a1 in spans:   # the C1 bucket work (or the sync bracket at D = 1)
+            rows.append((self.stage_id + 1, "A", 0, int(round(a0)), int(round(a1))))
         return sorted(rows, key=lambda r: (r[0], r[3], r[1]))
 
     @staticmethod
