@@ -69,6 +69,8 @@ def parse():
                          "measured stage times, keeping the fastest of a few perturbed "
                          "candidates (off by default)")
     ap.add_argument("--cpu-sample-s", type=float, default=20.0)
+    ap.add_argument("--dropout", type=float, default=None,
+                    help="hidden + attention dropout of the run (default: the config's)")
     ap.add_argument("--trace-dir", default=None,
                     help="write every rank's measured Gantt CSV of the traced step here")
     return ap.parse_args()
@@ -461,6 +463,9 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     cfg = CONFIGS[args.config]
+    if args.dropout is not None:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, dropout=args.dropout)
     M, P, D, m, m_how, stage_map = workload_shape(args, cfg, world)
     N = micro_batches_for(JobSpec(M), m, D)
     pc = ParallelConfig(P, D, m, N, stage_map)

@@ -220,6 +220,12 @@ int vp_gelu_bwd(const void* dy, const void* pre, void* dx, int64_t n, void* stre
  * with dlogits = (softmax - onehot) * scale. labels < 0 are ignored. */
 int vp_xent_fwd_bwd(void* logits, const int64_t* labels, float* loss_rows, float* loss_sum,
                     int64_t rows, int64_t vocab, float scale, void* stream);
+/* As vp_xent_fwd_bwd with the loss scale read from device memory:
+ * scale_eff = scale * scale_dev[0] (the dynamic loss scaler's current scale,
+ * so captured graphs follow it). */
+int vp_xent_fwd_bwd_dev(void* logits, const int64_t* labels, float* loss_rows, float* loss_sum,
+                        int64_t rows, int64_t vocab, float scale, const float* scale_dev,
+                        void* stream);
 
 /* Column sum of dy[rows, cols] (bf16) accumulated into dbias (fp32), one
  * launch, deterministic. workspace: vp_bias_grad_ws_elems(cols) floats,
@@ -281,6 +287,21 @@ int vp_adam_step(float* master, void* weight_bf16, float* grad, float* exp_avg, 
                  int64_t n, const float* flags, float lr, float beta1, float beta2, float eps,
                  float weight_decay, float inv_loss_scale, float max_grad_norm,
                  float bias_c1, float bias_c2, void* stream);
+/* Loss scaling without host round trips (fp16 mixed precision as apex /
+ * Megatron run it; the overflow decision is global): the
+ * scaler state lives in device memory, float[4] = {loss scale, applied Adam
+ * steps, good steps since the last change, scale used by the last step}.
+ * vp_adam_step_dev unscales by 1/scaler[0] and takes its bias corrections
+ * from step scaler[1]+1 (skipping on overflow as vp_adam_step does);
+ * vp_loss_scaler_update then backs the scale off on overflow or grows it
+ * after `window` clean steps, and advances the applied-step count only on a
+ * clean step. A static scale is growth = backoff = 1. */
+int vp_adam_step_dev(float* master, void* weight_bf16, float* grad, float* exp_avg,
+                     float* exp_avg_sq, int64_t n, const float* flags, float lr, float beta1,
+                     float beta2, float eps, float weight_decay, float max_grad_norm,
+                     const float* scaler, void* stream);
+int vp_loss_scaler_update(float* scaler, const float* flags, float growth, float backoff,
+                          int64_t window, float min_scale, float max_scale, void* stream);
 
 /* Cast fp32 -> bf16 (n elements). */
 int vp_cast_f32_bf16(const float* x, void* y, int64_t n, void* stream);

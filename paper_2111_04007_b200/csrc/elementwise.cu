@@ -118,7 +118,8 @@ template <int THREADS>
 __global__ void __launch_bounds__(THREADS)
     xent_kernel(__nv_bfloat16* __restrict__ logits, const int64_t* __restrict__ labels,
                 float* __restrict__ loss_rows, float* __restrict__ loss_sum, int64_t vocab,
-                float scale) {
+                float scale, const float* __restrict__ scale_dev) {
+  if (scale_dev != nullptr) scale *= scale_dev[0];   // dynamic loss scale (device)
   const int64_t row = blockIdx.x;
   __nv_bfloat16* lr = logits + row * vocab;
   const int64_t label = labels[row];
@@ -220,7 +221,8 @@ __global__ void __launch_bounds__(THREADS)
 __global__ void __launch_bounds__(512)
     xent_smem_kernel(__nv_bfloat16* __restrict__ logits, const int64_t* __restrict__ labels,
                      float* __restrict__ loss_rows, float* __restrict__ loss_sum, int64_t vocab,
-                     float scale) {
+                     float scale, const float* __restrict__ scale_dev) {
+  if (scale_dev != nullptr) scale *= scale_dev[0];   // dynamic loss scale (device)
   constexpr int T = 512;
   extern __shared__ __align__(128) uint8_t xs_raw[];
   __shared__ uint64_t bar;
@@ -565,8 +567,17 @@ __global__ void __launch_bounds__(256) adam_kernel_u(
     float* __restrict__ master, __nv_bfloat16* __restrict__ w, float* __restrict__ grad,
     float* __restrict__ m, float* __restrict__ v, int64_t n, const float* __restrict__ flags,
     float lr, float b1, float b2, float eps, float wd, float inv_scale, float max_norm, float bc1,
-    float bc2) {
+    float bc2, const float* __restrict__ ss) {
   const bool skip = flags[1] != 0.f;
+  if (ss != nullptr) {
+    // device scaler state [loss scale, applied steps, good steps, scale used]:
+    // the unscale factor and the bias corrections of the (steps+1)-th
+    // APPLIED step (a skipped step does not advance Adam's clock)
+    inv_scale = 1.f / ss[0];
+    const float t = ss[1] + 1.f;
+    bc1 = 1.f - powf(b1, t);
+    bc2 = 1.f - powf(b2, t);
+  }
   float coef = inv_scale;
   if (max_norm > 0.f) {
     const float norm = sqrtf(flags[0]) * inv_scale;
@@ -729,21 +740,33 @@ extern "C" int vp_gelu_bwd(const void* dy, const void* pre, void* dx, int64_t n,
   return launch_status();
 }
 
-extern "C" int vp_xent_fwd_bwd(void* logits, const int64_t* labels, float* loss_rows,
-                               float* loss_sum, int64_t rows, int64_t vocab, float scale,
-                               void* stream) {
+static int xent_entry(void* logits, const int64_t* labels, float* loss_rows, float* loss_sum,
+                      int64_t rows, int64_t vocab, float scale, const float* scale_dev,
+                      void* stream) {
   if (rows <= 0 || vocab <= 0 || (vocab % 8)) return VP_ERR_ARGS;
   const size_t smem = static_cast<size_t>(vocab) * 2;
   if (smem <= 110 * 1024 && (reinterpret_cast<uintptr_t>(logits) & 15) == 0 && !getenv("VP_XENT_2PASS")) {
     if (cudaError_t e = vp::smem_optin(xent_smem_kernel, 110 * 1024); e != cudaSuccess) return e;
     xent_smem_kernel<<<static_cast<unsigned>(rows), 512, smem, ST>>>(BF(logits), labels,
                                                                     loss_rows, loss_sum, vocab,
-                                                                    scale);
+                                                                    scale, scale_dev);
   } else {
     xent_kernel<512><<<static_cast<unsigned>(rows), 512, 0, ST>>>(BF(logits), labels, loss_rows,
-                                                                  loss_sum, vocab, scale);
+                                                                  loss_sum, vocab, scale, scale_dev);
   }
   return launch_status();
+}
+
+extern "C" int vp_xent_fwd_bwd(void* logits, const int64_t* labels, float* loss_rows,
+                               float* loss_sum, int64_t rows, int64_t vocab, float scale,
+                               void* stream) {
+  return xent_entry(logits, labels, loss_rows, loss_sum, rows, vocab, scale, nullptr, stream);
+}
+
+extern "C" int vp_xent_fwd_bwd_dev(void* logits, const int64_t* labels, float* loss_rows,
+                                   float* loss_sum, int64_t rows, int64_t vocab, float scale,
+                                   const float* scale_dev, void* stream) {
+  return xent_entry(logits, labels, loss_rows, loss_sum, rows, vocab, scale, scale_dev, stream);
 }
 
 // workspace: vp_bias_grad_ws_elems(cols) floats, zero-filled before first use
@@ -862,7 +885,63 @@ extern "C" int vp_adam_step(float* master, void* weight_bf16, float* grad, float
       std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(device_sms()) * 8, want)));
   adam_kernel_u<U><<<grid, 256, 0, ST>>>(master, BF(weight_bf16), grad, exp_avg, exp_avg_sq, n,
                                          flags, lr, beta1, beta2, eps, weight_decay,
-                                         inv_loss_scale, max_grad_norm, bias_c1, bias_c2);
+                                         inv_loss_scale, max_grad_norm, bias_c1, bias_c2,
+                                         nullptr);
+  return launch_status();
+}
+
+extern "C" int vp_adam_step_dev(float* master, void* weight_bf16, float* grad, float* exp_avg,
+                                float* exp_avg_sq, int64_t n, const float* flags, float lr,
+                                float beta1, float beta2, float eps, float weight_decay,
+                                float max_grad_norm, const float* scaler, void* stream) {
+  if (n <= 0) return VP_OK;
+  if (!scaler || !flags) return VP_ERR_ARGS;
+  if ((reinterpret_cast<uintptr_t>(master) | reinterpret_cast<uintptr_t>(grad) |
+       reinterpret_cast<uintptr_t>(exp_avg) | reinterpret_cast<uintptr_t>(exp_avg_sq)) & 15 ||
+      reinterpret_cast<uintptr_t>(weight_bf16) & 7)
+    return VP_ERR_UNSUPPORTED;
+  constexpr int U = 8;
+  const int64_t want = (n / 4 + 256 * U - 1) / (256 * U);
+  const unsigned grid = static_cast<unsigned>(
+      std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(device_sms()) * 8, want)));
+  adam_kernel_u<U><<<grid, 256, 0, ST>>>(master, BF(weight_bf16), grad, exp_avg, exp_avg_sq, n,
+                                         flags, lr, beta1, beta2, eps, weight_decay, 1.f,
+                                         max_grad_norm, 1.f, 1.f, scaler);
+  return launch_status();
+}
+
+namespace vp {
+namespace {
+// One thread: the dynamic loss scaler after the step (apex/Megatron
+// schedule): overflow (flags[1] != 0) -> scale *= backoff (>= min_scale),
+// good = 0, Adam's applied-step count unchanged (the update was skipped);
+// otherwise steps += 1, good += 1 and after `window` good steps scale *=
+// growth. ss[3] keeps the scale this step used (for unscaling its loss).
+__global__ void loss_scaler_kernel(float* ss, const float* flags, float growth, float backoff,
+                                   float window, float min_scale, float max_scale) {
+  ss[3] = ss[0];
+  if (flags[1] != 0.f) {
+    ss[0] = fmaxf(ss[0] * backoff, min_scale);
+    ss[2] = 0.f;
+  } else {
+    ss[1] += 1.f;
+    ss[2] += 1.f;
+    if (ss[2] >= window) {
+      ss[0] = fminf(ss[0] * growth, max_scale);
+      ss[2] = 0.f;
+    }
+  }
+}
+}  // namespace
+}  // namespace vp
+
+extern "C" int vp_loss_scaler_update(float* scaler, const float* flags, float growth,
+                                     float backoff, int64_t window, float min_scale,
+                                     float max_scale, void* stream) {
+  if (!scaler || !flags || window <= 0 || growth < 1.f || backoff <= 0.f || backoff > 1.f)
+    return VP_ERR_ARGS;
+  loss_scaler_kernel<<<1, 1, 0, ST>>>(scaler, flags, growth, backoff, static_cast<float>(window),
+                                      min_scale, max_scale);
   return launch_status();
 }
 

@@ -36,6 +36,9 @@ _SIGS = {
                             vp, u32, vp, vp],
     "vp_attention_fwd_ex": [vp, vp, vp, i64, i64, i64, i64, c_int, f32, vp, u32, vp],
     "vp_set_seed": [vp, u64, vp],
+    "vp_xent_fwd_bwd_dev": [vp, vp, vp, vp, i64, i64, f32, vp, vp],
+    "vp_adam_step_dev": [vp, vp, vp, vp, vp, i64, vp, f32, f32, f32, f32, f32, f32, vp, vp],
+    "vp_loss_scaler_update": [vp, vp, f32, f32, i64, f32, f32, vp],
     "vp_grad_pack_bf16": [vp, vp, i64, vp],
     "vp_grad_unpack_bf16": [vp, vp, i64, vp],
     "vp_dropout_dev": [vp, i64, f32, vp, u32, vp],
@@ -270,9 +273,16 @@ def gelu_bwd(dy, pre, dx, stream=None):
     return dx
 
 
-def xent_fwd_bwd(logits, labels, loss_rows, scale, loss_sum=None, stream=None):
+def xent_fwd_bwd(logits, labels, loss_rows, scale, loss_sum=None, stream=None, scale_dev=None):
+    """``scale_dev`` (device fp32, optional): multiply ``scale`` by
+    scale_dev[0] in-kernel — the dynamic loss scale."""
     rows, vocab = logits.shape
     _count(1)
+    if scale_dev is not None:
+        check(L.vp_xent_fwd_bwd_dev(logits.data_ptr(), labels.data_ptr(), loss_rows.data_ptr(),
+                                    _p(loss_sum), rows, vocab, scale, scale_dev.data_ptr(),
+                                    _stream(stream)), "vp_xent_fwd_bwd_dev")
+        return loss_rows
     check(L.vp_xent_fwd_bwd(logits.data_ptr(), labels.data_ptr(), loss_rows.data_ptr(),
                             _p(loss_sum), rows, vocab, scale, _stream(stream)), "vp_xent_fwd_bwd")
     return loss_rows
@@ -391,6 +401,24 @@ def grad_unpack_bf16(x, y, stream=None):
     _count(1)
     check(L.vp_grad_unpack_bf16(x.data_ptr(), y.data_ptr(), x.numel(), _stream(stream)),
           "vp_grad_unpack_bf16")
+
+
+def adam_step_dev(master, weight, grad, m, v, flags, lr, beta1, beta2, eps, weight_decay,
+                  max_grad_norm, scaler, stream=None):
+    """Fused unscale / skip / clip / AdamW with the unscale factor and the
+    bias-correction step read from the device scaler state."""
+    _count(1)
+    check(L.vp_adam_step_dev(master.data_ptr(), weight.data_ptr(), grad.data_ptr(), m.data_ptr(),
+                             v.data_ptr(), master.numel(), flags.data_ptr(), lr, beta1, beta2, eps,
+                             weight_decay, max_grad_norm, scaler.data_ptr(), _stream(stream)),
+          "vp_adam_step_dev")
+
+
+def loss_scaler_update(scaler, flags, growth, backoff, window, min_scale=1.0,
+                       max_scale=2.0 ** 64, stream=None):
+    _count(1)
+    check(L.vp_loss_scaler_update(scaler.data_ptr(), flags.data_ptr(), growth, backoff, window,
+                                  min_scale, max_scale, _stream(stream)), "vp_loss_scaler_update")
 
 
 def cast_f32_bf16(x, y, stream=None):

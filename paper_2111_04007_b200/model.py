@@ -479,18 +479,19 @@ class GPT2Stage:
         return x
 
     def loss_and_head_backward(self, labels: torch.Tensor, loss_scale: float, loss_sum=None,
-                               stream=None):
+                               stream=None, scale_dev=None):
         """Last stage: final LN + tied head + softmax cross-entropy fwd/bwd.
         Leaves d(stage output) in ``self.g``; returns the per-row losses."""
         cfg, P = self.cfg, self.params
         x = self.xs[-1]
         if self.bert:
-            return self._mlm_head(labels, loss_scale, loss_sum, stream)
+            return self._mlm_head(labels, loss_scale, loss_sum, stream, scale_dev)
         K.layernorm_fwd(x, P.w("lnf_g"), P.w("lnf_b"), self.lnf_out, self.lnf_mean,
                         self.lnf_rstd, cfg.ln_eps, stream)
         wte = P.w(self.head_weight_name)
         K.gemm(self.lnf_out, wte, self.logits, stream=stream)
-        K.xent_fwd_bwd(self.logits, labels, self.loss_rows, loss_scale, loss_sum, stream)
+        K.xent_fwd_bwd(self.logits, labels, self.loss_rows, loss_scale, loss_sum, stream,
+                       scale_dev=scale_dev)
         # dlnf_out = dlogits @ wte ; dwte += dlogits^T @ lnf_out
         K.gemm(self.logits, wte, self.dc, b_kmajor=False, stream=stream)
         K.gemm(self.logits, self.lnf_out, P.g(self.head_weight_name), a_kmajor=False,
@@ -504,7 +505,7 @@ class GPT2Stage:
                         dsum=P.g(f"l{self.spec.layers[-1]}.b_fc2") if fused else None)
         return self.loss_rows
 
-    def _mlm_head(self, labels, loss_scale, loss_sum, stream):
+    def _mlm_head(self, labels, loss_scale, loss_sum, stream, scale_dev=None):
         """BERT MLM head: z = LN(gelu(x W^T + b)); logits = z wte^T + b_dec;
         cross-entropy on masked positions (labels >= 0). Leaves d(x) in g."""
         cfg, P = self.cfg, self.params
@@ -516,7 +517,8 @@ class GPT2Stage:
         wte = P.w(self.head_weight_name)
         K.gemm(self.lnf_out, wte, self.logits, epilogue=K.EPI_BIAS, bias=P.w("b_dec"),
                stream=stream)
-        K.xent_fwd_bwd(self.logits, labels, self.loss_rows, loss_scale, loss_sum, stream)
+        K.xent_fwd_bwd(self.logits, labels, self.loss_rows, loss_scale, loss_sum, stream,
+                       scale_dev=scale_dev)
         K.bias_grad(self.logits, P.g("b_dec"), self.bias_ws, stream)
         K.gemm(self.logits, wte, self.dc, b_kmajor=False, stream=stream)
         K.gemm(self.logits, self.lnf_out, P.g(self.head_weight_name), a_kmajor=False,

@@ -77,19 +77,49 @@ class AdamWConfig:
 
 
 @dataclass
+class LossScaler:
+    """Loss scaling for mixed precision. ``dynamic``: the apex / Megatron
+    schedule (start at ``init``, x``backoff`` on overflow — the step is
+    skipped on every rank, the overflow decision being global, PAPER.md:547 —
+    x``growth`` after ``window`` clean steps); otherwise a static ``init``.
+    The state lives on the device (vp_loss_scaler_update), so no step ever
+    waits on the host for it."""
+
+    init: float = 1.0
+    dynamic: bool = False
+    growth: float = 2.0
+    backoff: float = 0.5
+    window: int = 2000
+    min_scale: float = 1.0
+
+    @classmethod
+    def of(cls, x) -> "LossScaler":
+        if isinstance(x, LossScaler):
+            return x
+        if x == "dynamic":
+            return cls(init=2.0 ** 16, dynamic=True)
+        return cls(init=float(x))
+
+
+@dataclass
 class StepResult:
-    """Loss is only known on last-stage ranks (None elsewhere)."""
+    """Loss is only known on last-stage ranks (None elsewhere). ``_scale``:
+    device copy of the loss scale this step ran with."""
 
     _loss: Optional[torch.Tensor]
     _flags: torch.Tensor
-    inv_scale: float
+    _scale: Optional[torch.Tensor]
     timeline: Optional[dict] = None
+
+    @property
+    def loss_scale(self) -> float:
+        return 1.0 if self._scale is None else float(self._scale.item())
 
     @property
     def loss(self) -> Optional[float]:
         """Mean loss over the mini-batch's M_total samples (the device sum
         carries the loss scale; it is removed here)."""
-        return None if self._loss is None else float(self._loss.item()) * self.inv_scale
+        return None if self._loss is None else float(self._loss.item()) / self.loss_scale
 
     @property
     def overflow(self) -> bool:
@@ -97,7 +127,7 @@ class StepResult:
 
     @property
     def grad_norm(self) -> float:
-        return math.sqrt(max(float(self._flags[0].item()), 0.0)) * self.inv_scale
+        return math.sqrt(max(float(self._flags[0].item()), 0.0)) / self.loss_scale
 
 
 _M64 = (1 << 64) - 1
@@ -519,6 +549,7 @@ class Varuna:
         # rank has its own GPU (the product); gloo when several ranks share
         # one device (NCCL refuses duplicate GPUs). The data plane is the same.
         self.backend = backend
+        self.scaler = LossScaler.of(loss_scale)
         self.loss_scale = loss_scale
         self.links = None
         self.shm = None
@@ -566,6 +597,10 @@ class Varuna:
         self.trace = trace
         self.loss_sum = torch.zeros(1, device=self.device)
         self.flags = torch.zeros(2, device=self.device)
+        # device loss-scaler state {scale, applied Adam steps, good steps, scale used}
+        s0 = self.scaler.init
+        self._ss = torch.tensor([s0, 0.0, 0.0, s0], dtype=torch.float32, device=self.device)
+        self._scale_used = None
         self._setup_groups()
         if P > 1:
             slot_elems = self.m * model.seq_len * model.hidden
@@ -770,13 +805,13 @@ class Varuna:
         then gradient synchronisation and the optimizer update."""
         self.step_count += 1
         if not self.active:
-            return StepResult(None, torch.zeros(2), 1.0 / self.loss_scale)
+            return StepResult(None, torch.zeros(2), None)
         st = self.stream
         cfg, stage = self.cfg, self.stage
         # loss = mean over the M_total samples' label tokens (BERT: the
         # generator fixes mlm_per_seq masked positions per sequence)
         total_tokens = self.global_batch * (cfg.mlm_per_seq if cfg.arch == "bert" else cfg.seq_len)
-        scale = self.loss_scale / total_tokens
+        scale = 1.0 / total_tokens      # x the device loss scale, in the xent kernel
         ev = [] if self.trace else None
         self._ar_spans = []
         st.wait_stream(torch.cuda.current_stream(self.device))
@@ -797,6 +832,7 @@ class Varuna:
             t_ar0 = self._mark(ev)
             self._sync_grads()
             t_ar1 = self._mark(ev)
+            self._scale_used = self._ss[0:1].clone()   # before the scaler moves it
             if apply:
                 self._optimizer_step()
             t_end = self._mark(ev)
@@ -808,7 +844,7 @@ class Varuna:
             st.synchronize()
             timeline = self._timeline(t_start, ev, t_ar0, t_ar1, t_end)
         loss = self.loss_sum if self.spec.last else None
-        return StepResult(loss, self.flags, 1.0 / self.loss_scale, timeline)
+        return StepResult(loss, self.flags, self._scale_used, timeline)
 
     def _launch(self, kind, j, ctx):
         """Enqueue task (kind, j) on the compute stream: ring waits / credits,
@@ -955,7 +991,8 @@ class Varuna:
             stage.forward(x, ids, save=save, stream=st, out_ptr=out_ptr, types=types)
         else:
             if self.spec.last:
-                stage.loss_and_head_backward(self._in_labels, scale, self.loss_sum, stream=st)
+                stage.loss_and_head_backward(self._in_labels, scale, self.loss_sum, stream=st,
+                                             scale_dev=self._ss)
             out = stage.backward(g_in, ids, stream=st, types=types, layer_done=layer_done)
             if not self.spec.first:
                 K.p2p_put(self.links.peer_slot_ptr(_Links.GRAD, g), out, stream=st)
@@ -1032,10 +1069,17 @@ class Varuna:
             dist.all_reduce(self.flags, group=self.pipe_group)                 # C2
 
     def _optimizer_step(self):
-        P, o = self.stage.params, self.opt
-        K.adam_step(P.master, P.weight, P.grad, P.exp_avg, P.exp_avg_sq, self.flags, o.lr,
-                    o.betas[0], o.betas[1], o.eps, o.weight_decay, 1.0 / self.loss_scale,
-                    o.max_grad_norm, self.step_count, stream=self.stream)
+        """Unscale + skip-on-overflow + clip + AdamW (bias corrections of the
+        applied-step count on the device), then the loss-scaler update."""
+        P, o, ls = self.stage.params, self.opt, self.scaler
+        K.adam_step_dev(P.master, P.weight, P.grad, P.exp_avg, P.exp_avg_sq, self.flags, o.lr,
+                        o.betas[0], o.betas[1], o.eps, o.weight_decay, o.max_grad_norm,
+                        self._ss, stream=self.stream)
+        if ls.dynamic:
+            K.loss_scaler_update(self._ss, self.flags, ls.growth, ls.backoff, ls.window,
+                                 ls.min_scale, stream=self.stream)
+        else:
+            K.loss_scaler_update(self._ss, self.flags, 1.0, 1.0, 1 << 40, stream=self.stream)
 
     # ---------------------------------------------------------------- traces
     def gantt_rows(self, timeline: dict):
@@ -1104,6 +1148,7 @@ class Varuna:
         if self.rank == 0:
             import json
             man = {"step": self.step_count, "P": self.P, "D": self.D,
+                   "scaler": self._ss.tolist() if self.active else None,
                    "stage_map": list(self.pc.stage_map), "micro_batch_size": self.m,
                    "global_batch": self.global_batch,
                    "shards": [f"stage{s_}_replica{r_}.pt" for r_ in range(self.D)
@@ -1129,6 +1174,8 @@ class Varuna:
         self.step_count = int(man["step"])
         if not self.active:
             return
+        if man.get("scaler") is not None:   # loss scale + Adam's applied-step count
+            self._ss.copy_(torch.tensor(man["scaler"], dtype=torch.float32))
         sub = os.path.join(ckpt_dir, f"step{man['step']:08d}")
         P = self.stage.params
         want = set(P.names)

@@ -242,3 +242,47 @@ def test_bert_large_width_layer_matches_oracle():
     og = o.grads()
     for pname, g in v.param_tensors("grad").items():
         assert rel(g, og[pname]) < 3e-2, (pname, rel(g, og[pname]))
+
+
+def test_dynamic_loss_scaler_skip_and_recover():
+    """Dynamic loss scaling (LossScaler, device-resident state): a step whose
+    gradients hold a non-finite value is skipped on the device (master and
+    Adam moments untouched, Adam's applied-step count unchanged, gradients
+    zeroed) and the scale backs off; the next clean step is applied as Adam
+    step 1 and equals a fresh run's first step at that scale; after
+    ``window`` clean steps the scale grows."""
+    from paper_2111_04007_b200 import ParallelConfig
+    from paper_2111_04007_b200.model import CONFIGS
+    from paper_2111_04007_b200.runtime import AdamWConfig, LossScaler, Varuna, synthetic_batch
+    cfg = CONFIGS["tiny"]
+    pc = ParallelConfig(1, 1, 4, 2, (0,) * cfg.n_layer)
+    opt = AdamWConfig(lr=1e-3)
+    b = [synthetic_batch(cfg, 8, 0, step=s) for s in range(4)]
+    v = Varuna(cfg, pc, seed=0, optimizer=opt,
+               loss_scale=LossScaler(init=2.0 ** 16, dynamic=True, window=2))
+    P = v.stage.params
+    w0 = P.master.clone()
+    m0 = P.exp_avg.clone()
+    v.step(b[0], apply=False)
+    P.grad[123] = float("inf")            # an overflowed gradient
+    with torch.cuda.stream(v.stream):
+        v._sync_grads()
+        v._optimizer_step()
+    torch.cuda.synchronize()
+    assert v.flags[1].item() > 0
+    assert torch.equal(P.master, w0) and torch.equal(P.exp_avg, m0)
+    assert P.grad.abs().max().item() == 0.0
+    assert v._ss.tolist()[:3] == [2.0 ** 15, 0.0, 0.0]
+    r = v.step(b[1])
+    assert not r.overflow and r.loss_scale == 2.0 ** 15
+    ref = Varuna(cfg, pc, seed=0, optimizer=opt, loss_scale=2.0 ** 15)
+    rr = ref.step(b[1])
+    torch.cuda.synchronize()
+    assert abs(r.loss - rr.loss) <= 1e-6 * abs(rr.loss)
+    assert (P.master - ref.stage.params.master).abs().max().item() <= 1e-6
+    assert v._ss.tolist()[:3] == [2.0 ** 15, 1.0, 1.0]
+    r = v.step(b[2])                       # second clean step: window reached
+    torch.cuda.synchronize()
+    assert v._ss.tolist()[:3] == [2.0 ** 16, 2.0, 0.0]
+    v.close()
+    ref.close()
