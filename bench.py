@@ -71,6 +71,9 @@ def parse():
     ap.add_argument("--cpu-sample-s", type=float, default=20.0)
     ap.add_argument("--dropout", type=float, default=None,
                     help="hidden + attention dropout of the run (default: the config's)")
+    ap.add_argument("--side-dropout", type=float, default=0.1,
+                    help="also time the same workload at this dropout (SURVEY §8(d): 0.1 for "
+                         "perf runs) and report it beside the headline; 0 disables")
     ap.add_argument("--trace-dir", default=None,
                     help="write every rank's measured Gantt CSV of the traced step here")
     return ap.parse_args()
@@ -637,6 +640,31 @@ def main():
         import paper_2111_04007_b200 as vpapi
         with open(os.path.join(ROOT, "profiles", "plans.json")) as f:
             control_plane = control_plane_times(vpapi, json.load(f))
+    # ---- the same workload at the perf-run dropout (fused K7: masks in the
+    # GEMM epilogues and attention, recompute-exact), device-resident inputs
+    side = None
+    if args.side_dropout and args.side_dropout != cfg.dropout:
+        import dataclasses
+        v.close()
+        torch.cuda.empty_cache()
+        cfg_d = dataclasses.replace(cfg, dropout=args.side_dropout)
+        vd = Varuna(cfg_d, pc, seed=0, init_device=init_dev, dispatch=dispatch, profile=prof)
+        for _ in range(args.warmup):
+            vd.step(dbatch)
+        barrier()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(vd.stream)
+        for _ in range(args.steps):
+            vd.step(dbatch)
+        a1.record(vd.stream)
+        barrier()
+        ms_d = max_over_ranks(a0.elapsed_time(a1)) / args.steps
+        side = {"dropout": args.side_dropout, "value": round(M / (ms_d / 1e3), 3),
+                "unit": "samples/s", "ms_per_step": round(ms_d, 2),
+                "note": "hidden (GEMM-epilogue) + attention-probability + embedding dropout, "
+                        "masks regenerated bit-exactly by recompute; CUDA graphs on"}
+        v = vd
     if rank == 0:
         line = {
             "metric": f"samples/sec ({METRIC_NAMES[args.config]} Varuna pipeline step)",
@@ -673,6 +701,7 @@ def main():
                        "k9_put_us": k9_us},
             "cpu_baseline": cpu,
             "control_plane_cpp_us": control_plane,
+            "with_dropout": side,
         }
         print(json.dumps(line), flush=True)
     v.close()
