@@ -172,7 +172,12 @@ int vp_attention_bwd(const void* qkv, const void* o, const void* dout, const flo
  * bit-for-bit in R. */
 int vp_attention_fwd_ex(const void* qkv, void* o, float* lse, int64_t batch, int64_t seq,
                         int64_t heads, int64_t head_dim, int causal, float p,
-                        const uint64_t* seed, uint32_t salt, void* stream);
+                        const uint64_t* seed, uint32_t salt, uint32_t* mask_out, void* stream);
+/* mask_out (optional, seq % 32 == 0): vp_attention_mask_words(batch, seq,
+ * heads) uint32 words receiving the keep bits KEY-major — word
+ * [(b*heads + h)*seq + key][q / 32], bit q % 32 — for the backward
+ * (a saving forward: Varuna's R, or F on the last stage). */
+int64_t vp_attention_mask_words(int64_t batch, int64_t seq, int64_t heads);
 /* Workspace (fp32 elements) of vp_attention_bwd_ex: delta [B*H*S] + the fp32
  * dQ accumulator [B*S*H*D]. */
 int64_t vp_attention_bwd_ws_elems(int64_t batch, int64_t seq, int64_t heads, int64_t head_dim);
@@ -185,10 +190,12 @@ int64_t vp_attention_bwd_ws_elems(int64_t batch, int64_t seq, int64_t heads, int
 int vp_attention_bwd_ex(const void* qkv, const void* o, const void* dout, const float* lse,
                         void* dqkv, float* workspace, int64_t ws_elems, int64_t batch,
                         int64_t seq, int64_t heads, int64_t head_dim, int causal, int flags,
-                        float p, const uint64_t* seed, uint32_t salt, float* dbias,
-                        void* stream);
+                        float p, const uint64_t* seed, uint32_t salt, const uint32_t* mask_in,
+                        float* dbias, void* stream);
 /* p > 0: attention-probability dropout of the forward call with the same
- * (seed, salt) — see vp_attention_fwd_ex — differentiated through. */
+ * (seed, salt) — see vp_attention_fwd_ex — differentiated through; mask_in
+ * (optional) the bit mask that forward wrote: the backward reads the keep
+ * bits instead of re-hashing every element. */
 /* dbias (optional, fused path only, else VP_ERR_UNSUPPORTED): dbias[3*H*D]
  * += column sums of dqkv — the QKV bias gradient — from the dQ post-pass
  * and the dK/dV epilogue partials (fixed-order reductions). */

@@ -11,10 +11,11 @@ namespace vp {
 
 int attention_fwd_tc(const void* qkv, void* o, float* lse, int64_t B, int64_t S, int64_t H,
                      int64_t D, int causal, float p, const uint64_t* seed, uint32_t salt,
-                     cudaStream_t st);
+                     uint32_t* mask, cudaStream_t st);
 int attention_bwd_tc(const void* qkv, const void* dout, const float* lse, const float* delta,
                      void* dqkv, int64_t B, int64_t S, int64_t H, int64_t D, int causal,
-                     float p, const uint64_t* seed, uint32_t salt, cudaStream_t st);
+                     float p, const uint64_t* seed, uint32_t salt, const uint32_t* mask,
+                     cudaStream_t st);
 int64_t attention_bwd_fused_ws(int64_t B, int64_t S, int64_t H, int64_t D);
 bool attention_bwd_fused_ok(int64_t D);
 int attention_bwd_fused(const void* qkv, const void* o, const void* dout, const float* lse,
@@ -64,14 +65,15 @@ __global__ void __launch_bounds__(256) attn_delta_kernel(const __nv_bfloat16* __
 template <int D, bool CAUSAL>
 int bwd_t(const void* qkv, const void* o, const void* dout, const float* lse, void* dqkv,
           float* delta, int64_t B, int64_t S, int64_t H, float p, const uint64_t* seed,
-          uint32_t salt, cudaStream_t st) {
+          uint32_t salt, const uint32_t* mask, cudaStream_t st) {
   const int64_t tokens = B * S;
   constexpr int RPW = 32 / (D / 8);
   const int64_t warps = (tokens * H + RPW - 1) / RPW;
   attn_delta_kernel<D><<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, st>>>(
       reinterpret_cast<const __nv_bfloat16*>(o), reinterpret_cast<const __nv_bfloat16*>(dout),
       delta, tokens, static_cast<int>(S), static_cast<int>(H));
-  return attention_bwd_tc(qkv, dout, lse, delta, dqkv, B, S, H, D, CAUSAL, p, seed, salt, st);
+  return attention_bwd_tc(qkv, dout, lse, delta, dqkv, B, S, H, D, CAUSAL, p, seed, salt, mask,
+                          st);
 }
 
 }  // namespace
@@ -84,27 +86,34 @@ extern "C" int vp_attention_fwd(const void* qkv, void* o, float* lse, int64_t ba
                                 int64_t heads, int64_t head_dim, int causal, void* stream) {
   if (batch <= 0 || seq <= 0 || heads <= 0) return VP_ERR_ARGS;
   return attention_fwd_tc(qkv, o, lse, batch, seq, heads, head_dim, causal, 0.f, nullptr, 0,
-                          reinterpret_cast<cudaStream_t>(stream));
+                          nullptr, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" int vp_attention_fwd_ex(const void* qkv, void* o, float* lse, int64_t batch,
                                    int64_t seq, int64_t heads, int64_t head_dim, int causal,
-                                   float p, const uint64_t* seed, uint32_t salt, void* stream) {
+                                   float p, const uint64_t* seed, uint32_t salt,
+                                   uint32_t* mask_out, void* stream) {
   if (batch <= 0 || seq <= 0 || heads <= 0 || p < 0.f || p >= 1.f) return VP_ERR_ARGS;
   if (p > 0.f && !seed) return VP_ERR_ARGS;
   return attention_fwd_tc(qkv, o, lse, batch, seq, heads, head_dim, causal, p, seed, salt,
-                          reinterpret_cast<cudaStream_t>(stream));
+                          mask_out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int64_t vp_attention_mask_words(int64_t batch, int64_t seq, int64_t heads) {
+  if (batch <= 0 || seq <= 0 || heads <= 0 || (seq % 32)) return 0;
+  return batch * heads * seq * (seq / 32);
 }
 
 namespace {
 int attn_bwd_det(const void* qkv, const void* o, const void* dout, const float* lse, void* dqkv,
                  float* delta_ws, int64_t batch, int64_t seq, int64_t heads, int64_t head_dim,
-                 int causal, float p, const uint64_t* seed, uint32_t salt, cudaStream_t st) {
+                 int causal, float p, const uint64_t* seed, uint32_t salt, const uint32_t* mask,
+                 cudaStream_t st) {
 #define BWD(DD)                                                                              \
   return causal ? bwd_t<DD, true>(qkv, o, dout, lse, dqkv, delta_ws, batch, seq, heads, p, seed, \
-                                  salt, st)                                                   \
+                                  salt, mask, st)                                             \
                 : bwd_t<DD, false>(qkv, o, dout, lse, dqkv, delta_ws, batch, seq, heads, p,     \
-                                   seed, salt, st)
+                                   seed, salt, mask, st)
   switch (head_dim) {
     case 64: BWD(64);
     case 96: BWD(96);
@@ -121,7 +130,7 @@ extern "C" int vp_attention_bwd(const void* qkv, const void* o, const void* dout
                                 int64_t heads, int64_t head_dim, int causal, void* stream) {
   if (batch <= 0 || seq <= 0 || heads <= 0 || !delta_ws) return VP_ERR_ARGS;
   return attn_bwd_det(qkv, o, dout, lse, dqkv, delta_ws, batch, seq, heads, head_dim, causal, 0.f,
-                      nullptr, 0, reinterpret_cast<cudaStream_t>(stream));
+                      nullptr, 0, nullptr, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" int64_t vp_attention_bwd_ws_elems(int64_t batch, int64_t seq, int64_t heads,
@@ -139,20 +148,21 @@ extern "C" int vp_attention_bwd_ex(const void* qkv, const void* o, const void* d
                                    const float* lse, void* dqkv, float* workspace,
                                    int64_t ws_elems, int64_t batch, int64_t seq, int64_t heads,
                                    int64_t head_dim, int causal, int flags, float p,
-                                   const uint64_t* seed, uint32_t salt, float* dbias,
-                                   void* stream) {
+                                   const uint64_t* seed, uint32_t salt, const uint32_t* mask_in,
+                                   float* dbias, void* stream) {
   if (batch <= 0 || seq <= 0 || heads <= 0 || !workspace) return VP_ERR_ARGS;
   if (p < 0.f || p >= 1.f || (p > 0.f && !seed)) return VP_ERR_ARGS;
   if (ws_elems < attention_bwd_fused_ws(batch, seq, heads, head_dim)) return VP_ERR_ARGS;
   if ((reinterpret_cast<uintptr_t>(workspace) & 15) != 0) return VP_ERR_ARGS;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (vp_attention_bwd_fuses_bias(head_dim, flags)) {
-    const AttnDrop dr = make_attn_drop(p, seed, salt);
+    const AttnDrop dr = make_attn_drop(p, seed, salt,
+                                       (seq % 32) ? nullptr : const_cast<uint32_t*>(mask_in));
     if (dr.seed && (seq & 1)) return VP_ERR_UNSUPPORTED;
     return attention_bwd_fused(qkv, o, dout, lse, dqkv, workspace, batch, seq, heads, causal,
                                dbias, dr, st);
   }
   if (dbias) return VP_ERR_UNSUPPORTED;  // bias sums are fused only into the one-pass kernel
   return attn_bwd_det(qkv, o, dout, lse, dqkv, workspace, batch, seq, heads, head_dim, causal, p,
-                      seed, salt, st);
+                      seed, salt, mask_in, st);
 }

@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
     // P^T, dS^T for 32 query columns starting at q0c into packed bf16x2 words
     auto softmax_grad = [&](auto masked, const uint32_t (&rs)[32], const uint32_t (&rd)[32],
                             uint32_t lv, int q0c, int qlo, uint32_t (&pp)[16],
-                            uint32_t (&pg)[16]) {
+                            uint32_t (&pg)[16], uint32_t mword) {
 #pragma unroll
       for (int g = 0; g < 8; ++g) {
         const float4 l4 = lds128f(lv + 16 * g);
@@ -305,10 +305,16 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
             pv = (q >= qlo && q < S) ? pv : 0.f;
           }
           if constexpr (DROP) {
-            // element (query q0c+i, this key); thread = key: one hash each
-            const uint64_t e = (static_cast<uint64_t>(bh) * S + (q0c + i)) * S + key;
-            const uint32_t bits = drop_bits(dkey, e >> 1);
-            const bool keep = ((key & 1) ? (bits >> 16) : (bits & 0xFFFFu)) >= drop.thr;
+            // element (query q0c+i, this key): bit i of the forward's mask
+            // word for these 32 queries, else one hash per element
+            bool keep;
+            if (drop.mask != nullptr) {
+              keep = (mword >> i) & 1u;
+            } else {
+              const uint64_t e = (static_cast<uint64_t>(bh) * S + (q0c + i)) * S + key;
+              const uint32_t bits = drop_bits(dkey, e >> 1);
+              keep = ((key & 1) ? (bits >> 16) : (bits & 0xFFFFu)) >= drop.thr;
+            }
             p[t] = keep ? pv : 0.f;
             gr[t] = pv * ((keep ? __uint_as_float(rd[i]) * drop.scale : 0.f) - dq[t]);
           } else {
@@ -350,10 +356,16 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&st_empty[cc]);
         const uint32_t lv = lv_base + (qs * 2 * FB_N + c) * 4;
+        uint32_t mword = 0;
+        if constexpr (DROP) {
+          if (drop.mask != nullptr)   // keep bits of queries qi+c .. +31 for this key
+            mword = drop.mask[(static_cast<uint64_t>(bh) * S + min(key, S - 1)) * (S >> 5) +
+                              ((qi + c) >> 5)];
+        }
         if (need_mask)
-          softmax_grad(std::true_type{}, rs, rd, lv, qi + c, qlo, pp, pg);
+          softmax_grad(std::true_type{}, rs, rd, lv, qi + c, qlo, pp, pg, mword);
         else
-          softmax_grad(std::false_type{}, rs, rd, lv, qi + c, qlo, pp, pg);
+          softmax_grad(std::false_type{}, rs, rd, lv, qi + c, qlo, pp, pg, mword);
         if (warp == 4 && lane == 0) { if (cc == 0) TR(2); else TR(4); }
         if (cc == 0) {
           mbar_wait(pt_empty, (it & 1) ^ 1);                  // dV of the previous block done

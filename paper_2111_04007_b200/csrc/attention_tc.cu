@@ -272,6 +272,11 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
       float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       uint4 pk[TA_BN / 8];
       const uint64_t dpair = (((static_cast<uint64_t>(bh) * S + q) * S) + k0) >> 1;
+      // key-major mask words of this warp's 32 rows: lane l collects the
+      // words of keys k0+l (w_lo) and k0+32+l (w_hi), by one warp ballot
+      // per key as the keep bits are drawn
+      uint32_t w_lo = 0, w_hi = 0;
+      const bool want_mask = DROP && drop.mask != nullptr;
 #pragma unroll
       for (int g = 0; g < TA_BN / 8; ++g) {
         float f[8];
@@ -286,9 +291,30 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
             const uint32_t kk = drop_keep2(dkey, dpair + g * 4 + t, drop.thr);
             f[2 * t] = (kk & 1u) ? f[2 * t] : 0.f;
             f[2 * t + 1] = (kk & 2u) ? f[2 * t + 1] : 0.f;
+            if (want_mask) {
+              const uint32_t a = __ballot_sync(0xffffffffu, kk & 1u);
+              const uint32_t b2 = __ballot_sync(0xffffffffu, kk & 2u);
+              const uint32_t c0 = (g * 8 + 2 * t) & 31;
+              if (g < 4) {
+                w_lo = lane == c0 ? a : w_lo;
+                w_lo = lane == c0 + 1 ? b2 : w_lo;
+              } else {
+                w_hi = lane == c0 ? a : w_hi;
+                w_hi = lane == c0 + 1 ? b2 : w_hi;
+              }
+            }
           }
         }
         pk[g] = pack8(f);
+      }
+      if constexpr (DROP) {
+        if (want_mask) {
+          const int words = S >> 5;
+          const int qw = (q0 >> 5) + static_cast<int>(qd);
+          uint32_t* mrow = drop.mask + (static_cast<uint64_t>(bh) * S + k0 + lane) * words + qw;
+          if (k0 + static_cast<int>(lane) < S) mrow[0] = w_lo;
+          if (k0 + 32 + static_cast<int>(lane) < S) mrow[static_cast<uint64_t>(32) * words] = w_hi;
+        }
       }
       if (warp == 4 && lane == 0) TRF(j, 2);
       // P buffer: TMEM (single, last read by PV_{j-1}) or smem (j & 1, by PV_{j-2})
@@ -616,11 +642,19 @@ __global__ void __launch_bounds__(TB_THREADS, TbSmem<D>::MINB)
               pv = (qq >= qlo && qq < S) ? pv : 0.f;
             }
             if constexpr (DROP) {
-              // element (query qi+c+i, this key): thread = key, so one hash
-              // per element (the mask pairs adjacent keys)
-              const uint64_t e = (static_cast<uint64_t>(bh) * S + (qi + c + i)) * S + key;
-              const uint32_t bits = drop_bits(dkey, e >> 1);
-              const bool keep = ((key & 1) ? (bits >> 16) : (bits & 0xFFFFu)) >= drop.thr;
+              // element (query qi+c+i, this key): the forward's key-major bit
+              // mask when it wrote one, else one hash per element
+              bool keep;
+              if (drop.mask != nullptr) {
+                const int qq = qi + c + i;
+                const uint32_t w = drop.mask[(static_cast<uint64_t>(bh) * S + min(key, S - 1)) *
+                                                 (S >> 5) + (qq >> 5)];
+                keep = (w >> (qq & 31)) & 1u;
+              } else {
+                const uint64_t e = (static_cast<uint64_t>(bh) * S + (qi + c + i)) * S + key;
+                const uint32_t bits = drop_bits(dkey, e >> 1);
+                keep = ((key & 1) ? (bits >> 16) : (bits & 0xFFFFu)) >= drop.thr;
+              }
               fp[t] = keep ? pv : 0.f;
               fg[t] = pv * ((keep ? __uint_as_float(rd[i]) * drop.scale : 0.f) - dq[t]);
             } else {
@@ -923,9 +957,11 @@ int bwd_tc_d(const void* qkv, const void* dout, const float* lse, const float* d
 
 int attention_bwd_tc(const void* qkv, const void* dout, const float* lse, const float* delta,
                      void* dqkv, int64_t B, int64_t S, int64_t H, int64_t D, int causal,
-                     float p, const uint64_t* seed, uint32_t salt, cudaStream_t st) {
+                     float p, const uint64_t* seed, uint32_t salt, const uint32_t* mask,
+                     cudaStream_t st) {
   if ((3 * H * D) % 8) return VP_ERR_UNSUPPORTED;
-  const AttnDrop dr = make_attn_drop(p, seed, salt);
+  const AttnDrop dr = make_attn_drop(p, seed, salt,
+                                     (S % 32) ? nullptr : const_cast<uint32_t*>(mask));
   if (dr.seed && (S & 1)) return VP_ERR_UNSUPPORTED;
   switch (D) {
     case 64: return bwd_tc_d<64>(qkv, dout, lse, delta, dqkv, B, S, H, causal, dr, st);
@@ -975,9 +1011,9 @@ int fwd_tc_d(const void* qkv, void* o, float* lse, int64_t B, int64_t S, int64_t
 
 int attention_fwd_tc(const void* qkv, void* o, float* lse, int64_t B, int64_t S, int64_t H,
                      int64_t D, int causal, float p, const uint64_t* seed, uint32_t salt,
-                     cudaStream_t st) {
+                     uint32_t* mask, cudaStream_t st) {
   if ((3 * H * D) % 8) return VP_ERR_UNSUPPORTED;
-  const AttnDrop dr = make_attn_drop(p, seed, salt);
+  const AttnDrop dr = make_attn_drop(p, seed, salt, (S % 32) ? nullptr : mask);
   if (dr.seed && (S & 1)) return VP_ERR_UNSUPPORTED;
   switch (D) {
     case 64: return fwd_tc_d<64>(qkv, o, lse, B, S, H, causal, dr, st);

@@ -129,16 +129,23 @@ inline uint32_t drop_threshold(float p) {
 inline float drop_scale(uint32_t thr) { return 65536.f / static_cast<float>(65536u - thr); }
 
 // Attention-probability dropout of one call site (seed == nullptr: none).
+// mask (optional): the keep bits packed KEY-major, word
+// mask[(b*H + h)*S + key][q / 32] bit (q % 32) = keep(q, key) (S % 32 == 0):
+// a saving forward writes it (32x32 bit transposes by warp ballots), the
+// backward — whose threads own key rows — reads one 16-byte vector per
+// (key, 128 queries) instead of re-hashing every element.
 struct AttnDrop {
   const uint64_t* seed;
   uint32_t salt;
   uint32_t thr;
   float scale;
+  uint32_t* mask;
 };
-inline AttnDrop make_attn_drop(float p, const uint64_t* seed, uint32_t salt) {
-  if (p <= 0.f || !seed) return AttnDrop{nullptr, 0, 0, 1.f};
+inline AttnDrop make_attn_drop(float p, const uint64_t* seed, uint32_t salt,
+                               uint32_t* mask = nullptr) {
+  if (p <= 0.f || !seed) return AttnDrop{nullptr, 0, 0, 1.f, nullptr};
   const uint32_t thr = drop_threshold(p);
-  return AttnDrop{seed, salt, thr, drop_scale(thr)};
+  return AttnDrop{seed, salt, thr, drop_scale(thr), mask};
 }
 
 inline int launch_status() {

@@ -33,8 +33,9 @@ _SIGS = {
     "vp_attention_fwd": [vp, vp, vp, i64, i64, i64, i64, c_int, vp],
     "vp_attention_bwd": [vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, c_int, vp],
     "vp_attention_bwd_ex": [vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, i64, c_int, c_int, f32,
-                            vp, u32, vp, vp],
-    "vp_attention_fwd_ex": [vp, vp, vp, i64, i64, i64, i64, c_int, f32, vp, u32, vp],
+                            vp, u32, vp, vp, vp],
+    "vp_attention_fwd_ex": [vp, vp, vp, i64, i64, i64, i64, c_int, f32, vp, u32, vp, vp],
+    "vp_attention_mask_words": [i64, i64, i64],
     "vp_set_seed": [vp, u64, vp],
     "vp_xent_fwd_bwd_dev": [vp, vp, vp, vp, i64, i64, f32, vp, vp],
     "vp_adam_step_dev": [vp, vp, vp, vp, vp, i64, vp, f32, f32, f32, f32, f32, f32, vp, vp],
@@ -85,6 +86,7 @@ for _name, _args in _SIGS.items():
         _fn.argtypes = _args
         _fn.restype = c_int
 L.vp_attention_bwd_ws_elems.restype = ctypes.c_int64
+L.vp_attention_mask_words.restype = ctypes.c_int64
 L.vp_layernorm_ws_elems.restype = ctypes.c_int64
 L.vp_gemm_dbias_ws_elems.restype = ctypes.c_int64
 L.vp_bias_grad_ws_elems.restype = ctypes.c_int64
@@ -201,14 +203,20 @@ def layernorm_bwd(dy, x, gamma, mean, rstd, dx, dgamma, dbeta, workspace, accumu
     return dx
 
 
+def attention_mask_words(batch, seq, heads) -> int:
+    return int(L.vp_attention_mask_words(batch, seq, heads))
+
+
 def attention_fwd(qkv, out, lse, batch, seq, heads, head_dim, causal=True, stream=None,
-                  p=0.0, seed=None, salt=0):
+                  p=0.0, seed=None, salt=0, mask=None):
     """``p`` > 0: attention-probability dropout keyed by the device seed
-    tensor ``seed`` (int64 [1]) and the call site's ``salt``."""
+    tensor ``seed`` (int64 [1]) and the call site's ``salt``; ``mask``
+    (int32 [attention_mask_words]) receives the keep bits for the backward."""
     _count(1)
     check(L.vp_attention_fwd_ex(qkv.data_ptr(), out.data_ptr(), lse.data_ptr(), batch, seq, heads,
                                 head_dim, int(causal), p, _p(seed) if p > 0 else None,
-                                salt & 0xFFFFFFFF, _stream(stream)), "vp_attention_fwd_ex")
+                                salt & 0xFFFFFFFF, _p(mask) if p > 0 else None, _stream(stream)),
+          "vp_attention_fwd_ex")
     return out
 
 
@@ -217,7 +225,8 @@ def attention_bwd_ws_elems(batch, seq, heads, head_dim) -> int:
 
 
 def attention_bwd(qkv, out, dout, lse, dqkv, ws, batch, seq, heads, head_dim, causal=True,
-                  stream=None, deterministic=False, dbias=None, p=0.0, seed=None, salt=0):
+                  stream=None, deterministic=False, dbias=None, p=0.0, seed=None, salt=0,
+                  mask=None):
     """dqkv = d(qkv). ``ws``: fp32 workspace of attention_bwd_ws_elems()
     elements. head_dim 64 runs the fused one-pass kernel (dQ accumulated by
     TMA reduce-add); ``deterministic`` (or other head dims) the two-kernel
@@ -233,6 +242,7 @@ def attention_bwd(qkv, out, dout, lse, dqkv, ws, batch, seq, heads, head_dim, ca
                                 dqkv.data_ptr(), ws.data_ptr(), ws.numel(), batch, seq, heads,
                                 head_dim, int(causal), 1 if deterministic else 0, p,
                                 _p(seed) if p > 0 else None, salt & 0xFFFFFFFF,
+                                _p(mask) if p > 0 else None,
                                 dbias.data_ptr() if fused_bias else None, _stream(stream)),
           "vp_attention_bwd")
     return fused_bias
