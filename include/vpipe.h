@@ -172,12 +172,20 @@ int vp_attention_bwd(const void* qkv, const void* o, const void* dout, const flo
  * bit-for-bit in R. */
 int vp_attention_fwd_ex(const void* qkv, void* o, float* lse, int64_t batch, int64_t seq,
                         int64_t heads, int64_t head_dim, int causal, float p,
-                        const uint64_t* seed, uint32_t salt, uint32_t* mask_out, void* stream);
-/* mask_out (optional, seq % 32 == 0): vp_attention_mask_words(batch, seq,
- * heads) uint32 words receiving the keep bits KEY-major — word
- * [(b*heads + h)*seq + key][q / 32], bit q % 32 — for the backward
- * (a saving forward: Varuna's R, or F on the last stage). */
+                        const uint64_t* seed, uint32_t salt, const uint32_t* mask_q, void* stream);
+/* The keep bits of one attention dropout site, drawn once per (layer,
+ * micro-batch) — before the forward, off its softmax critical path — in
+ * two layouts of vp_attention_mask_words(batch, seq, heads) uint32 words
+ * each (seq % 32 == 0): mask_q word [((b*heads+h)*(seq/32) + key/32)*seq + q]
+ * bit key%32 (read by the forward, whose threads own query rows) and mask_k
+ * word [((b*heads+h)*(seq/32) + q/32)*seq + key] bit q%32 (read by the
+ * backward, whose threads own key rows). Bits = the K7 mask function of
+ * (*seed, salt, element ((b*heads+h)*seq + q)*seq + key). Causal: words
+ * entirely above the diagonal are not written. */
 int64_t vp_attention_mask_words(int64_t batch, int64_t seq, int64_t heads);
+int vp_attention_dropout_mask(int64_t batch, int64_t seq, int64_t heads, int causal, float p,
+                              const uint64_t* seed, uint32_t salt, uint32_t* mask_q,
+                              uint32_t* mask_k, void* stream);
 /* Workspace (fp32 elements) of vp_attention_bwd_ex: delta [B*H*S] + the fp32
  * dQ accumulator [B*S*H*D]. */
 int64_t vp_attention_bwd_ws_elems(int64_t batch, int64_t seq, int64_t heads, int64_t head_dim);
@@ -190,12 +198,12 @@ int64_t vp_attention_bwd_ws_elems(int64_t batch, int64_t seq, int64_t heads, int
 int vp_attention_bwd_ex(const void* qkv, const void* o, const void* dout, const float* lse,
                         void* dqkv, float* workspace, int64_t ws_elems, int64_t batch,
                         int64_t seq, int64_t heads, int64_t head_dim, int causal, int flags,
-                        float p, const uint64_t* seed, uint32_t salt, const uint32_t* mask_in,
-                        float* dbias, void* stream);
+                        float p, const uint64_t* seed, uint32_t salt, const uint32_t* mask_q,
+                        const uint32_t* mask_k, float* dbias, void* stream);
 /* p > 0: attention-probability dropout of the forward call with the same
- * (seed, salt) — see vp_attention_fwd_ex — differentiated through; mask_in
- * (optional) the bit mask that forward wrote: the backward reads the keep
- * bits instead of re-hashing every element. */
+ * (seed, salt) — see vp_attention_fwd_ex — differentiated through; mask_q /
+ * mask_k (optional): the keep bits vp_attention_dropout_mask drew for that
+ * call, read instead of re-hashing every element. */
 /* dbias (optional, fused path only, else VP_ERR_UNSUPPORTED): dbias[3*H*D]
  * += column sums of dqkv — the QKV bias gradient — from the dQ post-pass
  * and the dK/dV epilogue partials (fixed-order reductions). */

@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
             // element (query q0c+i, this key): bit i of the forward's mask
             // word for these 32 queries, else one hash per element
             bool keep;
-            if (drop.mask != nullptr) {
+            if (drop.mask_k != nullptr) {
               keep = (mword >> i) & 1u;
             } else {
               const uint64_t e = (static_cast<uint64_t>(bh) * S + (q0c + i)) * S + key;
@@ -358,9 +358,9 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
         const uint32_t lv = lv_base + (qs * 2 * FB_N + c) * 4;
         uint32_t mword = 0;
         if constexpr (DROP) {
-          if (drop.mask != nullptr)   // keep bits of queries qi+c .. +31 for this key
-            mword = drop.mask[(static_cast<uint64_t>(bh) * S + min(key, S - 1)) * (S >> 5) +
-                              ((qi + c) >> 5)];
+          const int qw = (qi + c) >> 5;   // keep bits of queries qi+c .. +31, this key
+          if (drop.mask_k != nullptr && key < S && qw * 32 < S)
+            mword = drop.mask_k[(static_cast<uint64_t>(bh) * (S >> 5) + qw) * S + key];
         }
         if (need_mask)
           softmax_grad(std::true_type{}, rs, rd, lv, qi + c, qlo, pp, pg, mword);

@@ -272,11 +272,16 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
       float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       uint4 pk[TA_BN / 8];
       const uint64_t dpair = (((static_cast<uint64_t>(bh) * S + q) * S) + k0) >> 1;
-      // key-major mask words of this warp's 32 rows: lane l collects the
-      // words of keys k0+l (w_lo) and k0+32+l (w_hi), by one warp ballot
-      // per key as the keep bits are drawn
-      uint32_t w_lo = 0, w_hi = 0;
-      const bool want_mask = DROP && drop.mask != nullptr;
+      // keep bits of keys k0..k0+63 for this row: from the pre-drawn mask
+      // (two coalesced words) or hashed here
+      uint32_t mk0 = 0, mk1 = 0;
+      if constexpr (DROP) {
+        if (drop.mask_q != nullptr && q < S) {
+          const uint32_t* mq = drop.mask_q + (static_cast<uint64_t>(bh) * (S >> 5) + (k0 >> 5)) * S + q;
+          mk0 = mq[0];
+          if (k0 + 32 < S) mk1 = mq[S];
+        }
+      }
 #pragma unroll
       for (int g = 0; g < TA_BN / 8; ++g) {
         float f[8];
@@ -286,35 +291,20 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
           ps[t] += f[t];
         }
         if constexpr (DROP) {
+          if (drop.mask_q != nullptr) {
+            const uint32_t mw = (g < 4 ? mk0 : mk1) >> ((g & 3) * 8);
 #pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const uint32_t kk = drop_keep2(dkey, dpair + g * 4 + t, drop.thr);
-            f[2 * t] = (kk & 1u) ? f[2 * t] : 0.f;
-            f[2 * t + 1] = (kk & 2u) ? f[2 * t + 1] : 0.f;
-            if (want_mask) {
-              const uint32_t a = __ballot_sync(0xffffffffu, kk & 1u);
-              const uint32_t b2 = __ballot_sync(0xffffffffu, kk & 2u);
-              const uint32_t c0 = (g * 8 + 2 * t) & 31;
-              if (g < 4) {
-                w_lo = lane == c0 ? a : w_lo;
-                w_lo = lane == c0 + 1 ? b2 : w_lo;
-              } else {
-                w_hi = lane == c0 ? a : w_hi;
-                w_hi = lane == c0 + 1 ? b2 : w_hi;
-              }
+            for (int t = 0; t < 8; ++t) f[t] = ((mw >> t) & 1u) ? f[t] : 0.f;
+          } else {
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const uint32_t kk = drop_keep2(dkey, dpair + g * 4 + t, drop.thr);
+              f[2 * t] = (kk & 1u) ? f[2 * t] : 0.f;
+              f[2 * t + 1] = (kk & 2u) ? f[2 * t + 1] : 0.f;
             }
           }
         }
         pk[g] = pack8(f);
-      }
-      if constexpr (DROP) {
-        if (want_mask) {
-          const int words = S >> 5;
-          const int qw = (q0 >> 5) + static_cast<int>(qd);
-          uint32_t* mrow = drop.mask + (static_cast<uint64_t>(bh) * S + k0 + lane) * words + qw;
-          if (k0 + static_cast<int>(lane) < S) mrow[0] = w_lo;
-          if (k0 + 32 + static_cast<int>(lane) < S) mrow[static_cast<uint64_t>(32) * words] = w_hi;
-        }
       }
       if (warp == 4 && lane == 0) TRF(j, 2);
       // P buffer: TMEM (single, last read by PV_{j-1}) or smem (j & 1, by PV_{j-2})
@@ -613,6 +603,12 @@ __global__ void __launch_bounds__(TB_THREADS, TbSmem<D>::MINB)
       const bool need_mask = (qi + TB_N > S) || (CAUSAL && qi < k0 + TB_M - 1);
       const uint32_t rowP = smem_u32(smem + L::P_OFF + st * 128 * TB_N * 2 + r * 128);
       const uint32_t rowG = smem_u32(smem + L::G_OFF + st * 128 * TB_N * 2 + r * 128);
+      uint32_t mword = 0;   // keep bits of queries qi+chalf*32 .. +31 for this key
+      if constexpr (DROP) {
+        const int qw = (qi >> 5) + chalf;
+        if (drop.mask_k != nullptr && key < S && qw * 32 < S)
+          mword = drop.mask_k[(static_cast<uint64_t>(bh) * (S >> 5) + qw) * S + key];
+      }
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         // 16 queries at a time (keeps the register footprint small enough
@@ -645,11 +641,8 @@ __global__ void __launch_bounds__(TB_THREADS, TbSmem<D>::MINB)
               // element (query qi+c+i, this key): the forward's key-major bit
               // mask when it wrote one, else one hash per element
               bool keep;
-              if (drop.mask != nullptr) {
-                const int qq = qi + c + i;
-                const uint32_t w = drop.mask[(static_cast<uint64_t>(bh) * S + min(key, S - 1)) *
-                                                 (S >> 5) + (qq >> 5)];
-                keep = (w >> (qq & 31)) & 1u;
+              if (drop.mask_k != nullptr) {
+                keep = (mword >> (hh * 16 + i)) & 1u;
               } else {
                 const uint64_t e = (static_cast<uint64_t>(bh) * S + (qi + c + i)) * S + key;
                 const uint32_t bits = drop_bits(dkey, e >> 1);
@@ -862,14 +855,24 @@ __global__ void __launch_bounds__(TB_THREADS, TbSmem<D>::MINB)
           for (int i = 0; i < 32; ++i) pv[i] = (kj + c + i < lim) ? pv[i] : 0.f;
         }
         if constexpr (DROP) {
-          // dP = mask * dP_dropped / (1 - p); thread = query: pairs of keys
-          const uint64_t p0 = ((static_cast<uint64_t>(bh) * S + q) * S + kj + c) >> 1;
+          // dP = mask * dP_dropped / (1 - p); thread = query: the pre-drawn
+          // word of keys kj+c .. +31, or pairs of keys hashed
+          if (drop.mask_q != nullptr) {
+            const int kw = (kj + c) >> 5;
+            const uint32_t mw = (q < S && kw * 32 < S)
+                ? drop.mask_q[(static_cast<uint64_t>(bh) * (S >> 5) + kw) * S + q] : 0u;
 #pragma unroll
-          for (int t = 0; t < 16; ++t) {
-            const uint32_t kk = drop_keep2(dkey, p0 + t, drop.thr);
-            rd[2 * t] = __float_as_uint((kk & 1u) ? __uint_as_float(rd[2 * t]) * drop.scale : 0.f);
-            rd[2 * t + 1] =
-                __float_as_uint((kk & 2u) ? __uint_as_float(rd[2 * t + 1]) * drop.scale : 0.f);
+            for (int t = 0; t < 32; ++t)
+              rd[t] = __float_as_uint(((mw >> t) & 1u) ? __uint_as_float(rd[t]) * drop.scale : 0.f);
+          } else {
+            const uint64_t p0 = ((static_cast<uint64_t>(bh) * S + q) * S + kj + c) >> 1;
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+              const uint32_t kk = drop_keep2(dkey, p0 + t, drop.thr);
+              rd[2 * t] = __float_as_uint((kk & 1u) ? __uint_as_float(rd[2 * t]) * drop.scale : 0.f);
+              rd[2 * t + 1] =
+                  __float_as_uint((kk & 2u) ? __uint_as_float(rd[2 * t + 1]) * drop.scale : 0.f);
+            }
           }
         }
 #pragma unroll
@@ -957,11 +960,11 @@ int bwd_tc_d(const void* qkv, const void* dout, const float* lse, const float* d
 
 int attention_bwd_tc(const void* qkv, const void* dout, const float* lse, const float* delta,
                      void* dqkv, int64_t B, int64_t S, int64_t H, int64_t D, int causal,
-                     float p, const uint64_t* seed, uint32_t salt, const uint32_t* mask,
-                     cudaStream_t st) {
+                     float p, const uint64_t* seed, uint32_t salt, const uint32_t* mask_q,
+                     const uint32_t* mask_k, cudaStream_t st) {
   if ((3 * H * D) % 8) return VP_ERR_UNSUPPORTED;
-  const AttnDrop dr = make_attn_drop(p, seed, salt,
-                                     (S % 32) ? nullptr : const_cast<uint32_t*>(mask));
+  const AttnDrop dr = (S % 32) ? make_attn_drop(p, seed, salt)
+                               : make_attn_drop(p, seed, salt, mask_q, mask_k);
   if (dr.seed && (S & 1)) return VP_ERR_UNSUPPORTED;
   switch (D) {
     case 64: return bwd_tc_d<64>(qkv, dout, lse, delta, dqkv, B, S, H, causal, dr, st);
@@ -1011,9 +1014,9 @@ int fwd_tc_d(const void* qkv, void* o, float* lse, int64_t B, int64_t S, int64_t
 
 int attention_fwd_tc(const void* qkv, void* o, float* lse, int64_t B, int64_t S, int64_t H,
                      int64_t D, int causal, float p, const uint64_t* seed, uint32_t salt,
-                     uint32_t* mask, cudaStream_t st) {
+                     const uint32_t* mask_q, cudaStream_t st) {
   if ((3 * H * D) % 8) return VP_ERR_UNSUPPORTED;
-  const AttnDrop dr = make_attn_drop(p, seed, salt, (S % 32) ? nullptr : mask);
+  const AttnDrop dr = make_attn_drop(p, seed, salt, (S % 32) ? nullptr : mask_q);
   if (dr.seed && (S & 1)) return VP_ERR_UNSUPPORTED;
   switch (D) {
     case 64: return fwd_tc_d<64>(qkv, o, lse, B, S, H, causal, dr, st);

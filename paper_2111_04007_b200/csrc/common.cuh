@@ -128,24 +128,44 @@ inline uint32_t drop_threshold(float p) {
 }
 inline float drop_scale(uint32_t thr) { return 65536.f / static_cast<float>(65536u - thr); }
 
+// Transpose of the 32x32 bit matrix whose row r is lane r's word: on
+// return lane c holds column c (bit r = row r's bit c). Butterfly: at
+// distance j lanes l, l^j swap the off-diagonal j x j bit blocks.
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, uint32_t lane) {
+  const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int s = 0; s < 5; ++s) {
+    const int j = 16 >> s;
+    const uint32_t m = masks[s];
+    const uint32_t o = __shfl_xor_sync(0xffffffffu, x, j);
+    x = (lane & j) ? (((o >> j) & m) | (x & ~m)) : ((x & m) | ((o & m) << j));
+  }
+  return x;
+}
+
 // Attention-probability dropout of one call site (seed == nullptr: none).
-// mask (optional): the keep bits packed KEY-major, word
-// mask[(b*H + h)*S + key][q / 32] bit (q % 32) = keep(q, key) (S % 32 == 0):
-// a saving forward writes it (32x32 bit transposes by warp ballots), the
-// backward — whose threads own key rows — reads one 16-byte vector per
-// (key, 128 queries) instead of re-hashing every element.
+// Keep-bit masks (optional, S % 32 == 0), drawn ONCE per (layer, micro-
+// batch) by vp_attention_dropout_mask — off the softmax critical path — in
+// the two layouts the kernels' thread mappings read coalesced:
+//   mask_q: word [((b*H + h)*(S/32) + key/32)*S + q], bit key % 32
+//           (threads own query rows: forward, dQ kernel);
+//   mask_k: word [((b*H + h)*(S/32) + q/32)*S + key], bit q % 32
+//           (threads own key rows: the fused backward, the dK/dV kernel).
+// Without them the kernels hash every element (common.cuh drop_bits).
 struct AttnDrop {
   const uint64_t* seed;
   uint32_t salt;
   uint32_t thr;
   float scale;
-  uint32_t* mask;
+  const uint32_t* mask_q;
+  const uint32_t* mask_k;
 };
 inline AttnDrop make_attn_drop(float p, const uint64_t* seed, uint32_t salt,
-                               uint32_t* mask = nullptr) {
-  if (p <= 0.f || !seed) return AttnDrop{nullptr, 0, 0, 1.f, nullptr};
+                               const uint32_t* mask_q = nullptr,
+                               const uint32_t* mask_k = nullptr) {
+  if (p <= 0.f || !seed) return AttnDrop{nullptr, 0, 0, 1.f, nullptr, nullptr};
   const uint32_t thr = drop_threshold(p);
-  return AttnDrop{seed, salt, thr, drop_scale(thr), mask};
+  return AttnDrop{seed, salt, thr, drop_scale(thr), mask_q, mask_k};
 }
 
 inline int launch_status() {

@@ -33,7 +33,8 @@ _SIGS = {
     "vp_attention_fwd": [vp, vp, vp, i64, i64, i64, i64, c_int, vp],
     "vp_attention_bwd": [vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, c_int, vp],
     "vp_attention_bwd_ex": [vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, i64, c_int, c_int, f32,
-                            vp, u32, vp, vp, vp],
+                            vp, u32, vp, vp, vp, vp],
+    "vp_attention_dropout_mask": [i64, i64, i64, c_int, f32, vp, u32, vp, vp, vp],
     "vp_attention_fwd_ex": [vp, vp, vp, i64, i64, i64, i64, c_int, f32, vp, u32, vp, vp],
     "vp_attention_mask_words": [i64, i64, i64],
     "vp_set_seed": [vp, u64, vp],
@@ -207,11 +208,21 @@ def attention_mask_words(batch, seq, heads) -> int:
     return int(L.vp_attention_mask_words(batch, seq, heads))
 
 
+def attention_dropout_mask(batch, seq, heads, causal, p, seed, salt, mask_q, mask_k,
+                           stream=None):
+    """Draw the keep bits of one attention dropout site once, in the forward
+    (``mask_q``) and backward (``mask_k``) layouts."""
+    _count(1)
+    check(L.vp_attention_dropout_mask(batch, seq, heads, int(causal), p, seed.data_ptr(),
+                                      salt & 0xFFFFFFFF, mask_q.data_ptr(), mask_k.data_ptr(),
+                                      _stream(stream)), "vp_attention_dropout_mask")
+
+
 def attention_fwd(qkv, out, lse, batch, seq, heads, head_dim, causal=True, stream=None,
                   p=0.0, seed=None, salt=0, mask=None):
     """``p`` > 0: attention-probability dropout keyed by the device seed
-    tensor ``seed`` (int64 [1]) and the call site's ``salt``; ``mask``
-    (int32 [attention_mask_words]) receives the keep bits for the backward."""
+    tensor ``seed`` (int64 [1]) and the call site's ``salt``; ``mask``: the
+    site's pre-drawn keep bits (``mask_q`` of attention_dropout_mask)."""
     _count(1)
     check(L.vp_attention_fwd_ex(qkv.data_ptr(), out.data_ptr(), lse.data_ptr(), batch, seq, heads,
                                 head_dim, int(causal), p, _p(seed) if p > 0 else None,
@@ -226,7 +237,7 @@ def attention_bwd_ws_elems(batch, seq, heads, head_dim) -> int:
 
 def attention_bwd(qkv, out, dout, lse, dqkv, ws, batch, seq, heads, head_dim, causal=True,
                   stream=None, deterministic=False, dbias=None, p=0.0, seed=None, salt=0,
-                  mask=None):
+                  mask_q=None, mask_k=None):
     """dqkv = d(qkv). ``ws``: fp32 workspace of attention_bwd_ws_elems()
     elements. head_dim 64 runs the fused one-pass kernel (dQ accumulated by
     TMA reduce-add); ``deterministic`` (or other head dims) the two-kernel
@@ -242,7 +253,7 @@ def attention_bwd(qkv, out, dout, lse, dqkv, ws, batch, seq, heads, head_dim, ca
                                 dqkv.data_ptr(), ws.data_ptr(), ws.numel(), batch, seq, heads,
                                 head_dim, int(causal), 1 if deterministic else 0, p,
                                 _p(seed) if p > 0 else None, salt & 0xFFFFFFFF,
-                                _p(mask) if p > 0 else None,
+                                _p(mask_q) if p > 0 else None, _p(mask_k) if p > 0 else None,
                                 dbias.data_ptr() if fused_bias else None, _stream(stream)),
           "vp_attention_bwd")
     return fused_bias

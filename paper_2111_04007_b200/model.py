@@ -204,10 +204,11 @@ class _LayerWS:
         self.rstd1 = torch.empty(T, **f32)
         self.mean2 = torch.empty(T, **f32)
         self.rstd2 = torch.empty(T, **f32)
-        # attention dropout keep bits (1 bit per probability, key-major),
-        # written by the saving forward and read by the backward
+        # attention dropout keep bits (1 bit per probability) in the forward
+        # and backward layouts, drawn once per (layer, micro-batch)
         nw = K.attention_mask_words(B, cfg.seq_len, cfg.heads) if cfg.dropout > 0 else 0
-        self.dmask = torch.empty(nw, dtype=torch.int32, device=dev) if nw else None
+        self.dmask_q = torch.empty(nw, dtype=torch.int32, device=dev) if nw else None
+        self.dmask_k = torch.empty(nw, dtype=torch.int32, device=dev) if nw else None
 
 
 @dataclass
@@ -332,10 +333,13 @@ class GPT2Stage:
     # --------------------------------------------------------------- forward
     def _attn_fwd(self, li, w, stream):
         cfg = self.cfg
+        salt = drop_salt(li, SITE_ATTN)
+        if w.dmask_q is not None:
+            K.attention_dropout_mask(self.mb, cfg.seq_len, cfg.heads, cfg.causal, cfg.dropout,
+                                     self.seed_buf, salt, w.dmask_q, w.dmask_k, stream)
         K.attention_fwd(w.qkv, w.o, w.lse, self.mb, cfg.seq_len, cfg.heads, cfg.head_dim,
-                        cfg.causal, stream, p=cfg.dropout, seed=self.seed_buf,
-                        salt=drop_salt(li, SITE_ATTN),
-                        mask=w.dmask if w is not self.scratch else None)
+                        cfg.causal, stream, p=cfg.dropout, seed=self.seed_buf, salt=salt,
+                        mask=w.dmask_q)
 
     def _layer_fwd(self, li: int, x: torch.Tensor, out, w: _LayerWS, stream=None):
         cfg, P = self.cfg, self.params
@@ -442,7 +446,8 @@ class GPT2Stage:
         return K.attention_bwd(w.qkv, w.o, self.do, w.lse, self.dqkv, self.delta, self.mb,
                                cfg.seq_len, cfg.heads, cfg.head_dim, cfg.causal, stream,
                                dbias=P.g(p + "b_qkv"), p=cfg.dropout, seed=self.seed_buf,
-                               salt=drop_salt(li, SITE_ATTN), mask=w.dmask)
+                               salt=drop_salt(li, SITE_ATTN), mask_q=w.dmask_q,
+                               mask_k=w.dmask_k)
 
     def forward(self, x_in: Optional[torch.Tensor], ids: Optional[torch.Tensor], save: bool,
                 dseed: Optional[int] = None, stream=None, out_ptr: Optional[int] = None,
@@ -662,8 +667,8 @@ class GPT2Stage:
         params = 18 * n
         ws_one = (2 * T * h * (1 + 3 + 1 + 1 + 1 + 4 + 4)
                   + 4 * micro_batch * cfg.heads * S + 4 * 4 * T)
-        if cfg.dropout > 0:   # attention dropout keep bits
-            ws_one += 4 * K.attention_mask_words(micro_batch, S, cfg.heads)
+        if cfg.dropout > 0:   # attention dropout keep bits, two layouts
+            ws_one += 2 * 4 * K.attention_mask_words(micro_batch, S, cfg.heads)
         nl = len(spec.layers)
         working = nl * ws_one + nl * 2 * T * h                # ws + residual stream xs
         scratch = ws_one + (2 * T * h if spec.first else 0)   # no-save temporaries, emb_out

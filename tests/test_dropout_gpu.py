@@ -120,21 +120,24 @@ def test_attention_dropout_fwd_bwd(B, S, H, D, causal):
     ref.backward(do.float())
     g = q.grad.view(B * S, 3, H * D)
     ws = torch.empty(K.attention_bwd_ws_elems(B, S, H, D), device="cuda")
-    # the forward's key-major keep-bit mask: the backward reading it instead
-    # of re-hashing draws identical bits (dK / dV bitwise, one CTA each)
-    mask = torch.zeros(K.attention_mask_words(B, S, H), dtype=torch.int32, device="cuda")
+    # the pre-drawn keep bits (both layouts): forward and backward reading
+    # them draw exactly the hashed masks (dK / dV bitwise: one CTA each)
+    nw = K.attention_mask_words(B, S, H)
+    mq = torch.zeros(nw, dtype=torch.int32, device="cuda")
+    mk = torch.zeros(nw, dtype=torch.int32, device="cuda")
+    K.attention_dropout_mask(B, S, H, causal, P, sb, 3, mq, mk)
     o2 = torch.empty_like(o)
-    K.attention_fwd(qkv, o2, lse, B, S, H, D, causal, p=P, seed=sb, salt=3, mask=mask)
+    K.attention_fwd(qkv, o2, lse, B, S, H, D, causal, p=P, seed=sb, salt=3, mask=mq)
     assert torch.equal(o, o2)
     for det in (False, True):
         outs = []
-        for m in (None, mask):
+        for m in ((None, None), (mq, mk)):
             dqkv = torch.full_like(qkv, float("nan"))
             K.attention_bwd(qkv, o, do, lse, dqkv, ws, B, S, H, D, causal, deterministic=det,
-                            p=P, seed=sb, salt=3, mask=m)
+                            p=P, seed=sb, salt=3, mask_q=m[0], mask_k=m[1])
             d = dqkv.view(B * S, 3, H * D)
             for i, name in enumerate("qkv"):
-                assert rel(d[:, i], g[:, i]) < 2e-2, (name, det, m is None)
+                assert rel(d[:, i], g[:, i]) < 2e-2, (name, det, m[0] is None)
             outs.append(d)
         assert torch.equal(outs[0][:, 1:], outs[1][:, 1:]), det
 

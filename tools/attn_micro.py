@@ -36,18 +36,26 @@ def run(B, S, H, D, causal):
     dqkv = torch.empty_like(qkv)
     ws = torch.empty(K.attention_bwd_ws_elems(B, S, H, D), device="cuda")
     seed = torch.full((1,), 12345, dtype=torch.int64, device="cuda")
+    nw = max(1, K.attention_mask_words(B, S, H))
+    mq = torch.zeros(nw, dtype=torch.int32, device="cuda")
+    mk = torch.zeros(nw, dtype=torch.int32, device="cuda")
     f = 4 * B * S * S * H * D * (0.5 if causal else 1.0)
     out = {"B": B, "S": S, "H": H, "D": D, "causal": causal}
     for p in (0.0, 0.1):
-        ms_f = t(lambda: K.attention_fwd(qkv, o, lse, B, S, H, D, causal, p=p, seed=seed))
+        ms_m = t(lambda: K.attention_dropout_mask(B, S, H, causal, 0.1, seed, 3, mq, mk)) \
+            if p > 0 else 0.0
+        ms_f = t(lambda: K.attention_fwd(qkv, o, lse, B, S, H, D, causal, p=p, seed=seed,
+                                         mask=mq))
         db = torch.zeros(3 * H * D, device="cuda")
         ms_b = t(lambda: K.attention_bwd(qkv, o, do, lse, dqkv, ws, B, S, H, D, causal, dbias=db,
-                                         p=p, seed=seed))
+                                         p=p, seed=seed, mask_q=mq, mask_k=mk))
         tag = "" if p == 0 else "_p0.1"
         out.update({f"fwd_us{tag}": round(ms_f * 1e3, 1),
                     f"fwd_tflops{tag}": round(f / ms_f / 1e9, 1),
                     f"bwd_us{tag}": round(ms_b * 1e3, 1),
                     f"bwd_tflops{tag}": round(2.5 * f / ms_b / 1e9, 1)})
+        if p > 0:
+            out["mask_us_p0.1"] = round(ms_m * 1e3, 1)
     if "sdpa" in sys.argv:
         import torch.nn.functional as F
         from torch.nn.attention import SDPBackend, sdpa_kernel
