@@ -329,14 +329,27 @@ class GPT2Stage:
         # the current (step, micro-batch) dropout seed: every dropout site
         # reads it from here, so captured graphs replay with fresh masks
         self.seed_buf = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.side = torch.cuda.Stream(dev) if cfg.dropout > 0 else None
 
     # --------------------------------------------------------------- forward
+    def _draw_attn_mask(self, li, w, stream):
+        """Fork: draw layer li's attention keep bits on the side stream, so
+        the (ALU-only) mask kernel runs beside the LN / QKV GEMM that precede
+        the attention (tensor-bound, ALU idle); joined in _attn_fwd."""
+        if w.dmask_q is None:
+            return
+        cfg = self.cfg
+        cur = stream or torch.cuda.current_stream()
+        self.side.wait_stream(cur)
+        K.attention_dropout_mask(self.mb, cfg.seq_len, cfg.heads, cfg.causal, cfg.dropout,
+                                 self.seed_buf, drop_salt(li, SITE_ATTN), w.dmask_q, w.dmask_k,
+                                 self.side)
+
     def _attn_fwd(self, li, w, stream):
         cfg = self.cfg
         salt = drop_salt(li, SITE_ATTN)
         if w.dmask_q is not None:
-            K.attention_dropout_mask(self.mb, cfg.seq_len, cfg.heads, cfg.causal, cfg.dropout,
-                                     self.seed_buf, salt, w.dmask_q, w.dmask_k, stream)
+            (stream or torch.cuda.current_stream()).wait_stream(self.side)   # join
         K.attention_fwd(w.qkv, w.o, w.lse, self.mb, cfg.seq_len, cfg.heads, cfg.head_dim,
                         cfg.causal, stream, p=cfg.dropout, seed=self.seed_buf, salt=salt,
                         mask=w.dmask_q)
@@ -344,6 +357,7 @@ class GPT2Stage:
     def _layer_fwd(self, li: int, x: torch.Tensor, out, w: _LayerWS, stream=None):
         cfg, P = self.cfg, self.params
         p = f"l{li}."
+        self._draw_attn_mask(li, w, stream)
         K.layernorm_fwd(x, P.w(p + "ln1_g"), P.w(p + "ln1_b"), w.a, w.mean1, w.rstd1,
                         cfg.ln_eps, stream)
         K.gemm(w.a, P.w(p + "w_qkv"), w.qkv, epilogue=K.EPI_BIAS, bias=P.w(p + "b_qkv"),
@@ -365,6 +379,7 @@ class GPT2Stage:
         y1 (w.x1), x1 (w.c), pre, f, y2 (w.a) and both LN statistics."""
         cfg, P = self.cfg, self.params
         p = f"l{li}."
+        self._draw_attn_mask(li, w, stream)
         K.gemm(x, P.w(p + "w_qkv"), w.qkv, epilogue=K.EPI_BIAS, bias=P.w(p + "b_qkv"),
                stream=stream)
         self._attn_fwd(li, w, stream)
