@@ -286,16 +286,45 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
     if constexpr (DROP) dkey = drop_key(drop.seed, drop.salt);
 
     // P^T, dS^T for 32 query columns starting at q0c into packed bf16x2 words
+    // (lse, delta of the first 4 queries are loaded by the caller, l0/d0,
+    // before it waits for the TMEM loads; each group prefetches the next
+    // group's pair so the shared-memory latency overlaps the math)
     auto softmax_grad = [&](auto masked, const uint32_t (&rs)[32], const uint32_t (&rd)[32],
                             uint32_t lv, int q0c, int qlo, uint32_t (&pp)[16],
-                            uint32_t (&pg)[16], uint32_t mword) {
+                            uint32_t (&pg)[16], uint32_t mword, float4 l4, float4 d4) {
 #pragma unroll
       for (int g = 0; g < 8; ++g) {
-        const float4 l4 = lds128f(lv + 16 * g);
-        const float4 d4 = lds128f(lv + FB_N * 4 + 16 * g);
+        float4 nl4 = l4, nd4 = d4;
+        if (g < 7) {
+          nl4 = lds128f(lv + 16 * (g + 1));
+          nd4 = lds128f(lv + FB_N * 4 + 16 * (g + 1));
+        }
         const float lq[4] = {l4.x, l4.y, l4.z, l4.w};
         const float dq[4] = {d4.x, d4.y, d4.z, d4.w};
         float p[4], gr[4];
+        if constexpr (!DROP) {
+          // two query columns per FFMA2 / FSUB2 / FMUL2
+#pragma unroll
+          for (int t = 0; t < 4; t += 2) {
+            const int i = 4 * g + t;
+            const uint64_t x2 = ffma2(f2pack(__uint_as_float(rs[i]), __uint_as_float(rs[i + 1])),
+                                      f2pack(scale_log2, scale_log2), f2pack(-lq[t], -lq[t + 1]));
+            float a, b;
+            f2unpack(x2, a, b);
+            float pa = fast_exp2(a), pb = fast_exp2(b);
+            if constexpr (decltype(masked)::value) {
+              const int q = q0c + i;
+              pa = (q >= qlo && q < S) ? pa : 0.f;
+              pb = (q + 1 >= qlo && q + 1 < S) ? pb : 0.f;
+            }
+            p[t] = pa;
+            p[t + 1] = pb;
+            const uint64_t g2 = fmul2(f2pack(pa, pb),
+                                      fsub2(f2pack(__uint_as_float(rd[i]), __uint_as_float(rd[i + 1])),
+                                            f2pack(dq[t], dq[t + 1])));
+            f2unpack(g2, gr[t], gr[t + 1]);
+          }
+        } else {
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           const int i = 4 * g + t;
@@ -322,6 +351,7 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
             gr[t] = pv * (__uint_as_float(rd[i]) - dq[t]);
           }
         }
+        }
         const __nv_bfloat162 p01 = __floats2bfloat162_rn(p[0], p[1]);
         const __nv_bfloat162 p23 = __floats2bfloat162_rn(p[2], p[3]);
         const __nv_bfloat162 g01 = __floats2bfloat162_rn(gr[0], gr[1]);
@@ -330,6 +360,8 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
         pp[2 * g + 1] = *reinterpret_cast<const uint32_t*>(&p23);
         pg[2 * g] = *reinterpret_cast<const uint32_t*>(&g01);
         pg[2 * g + 1] = *reinterpret_cast<const uint32_t*>(&g23);
+        l4 = nl4;
+        d4 = nd4;
       }
     };
 
@@ -339,6 +371,19 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
       const bool need_mask = (qi + FB_N > S) || (CAUSAL && qi < k0 + FB_M - 1);
       const int qlo = CAUSAL ? key : 0;
       const uint32_t dsb = rowG + (it & 1) * 2 * L::TILE;
+      // dropout keep bits of this block's two 32-query column groups (one
+      // global word each), requested before any wait so their latency hides
+      uint32_t mwords[2] = {0u, 0u};
+      if constexpr (DROP) {
+        if (drop.mask_k != nullptr && key < S) {
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            const int qw = (qi + cc * 64 + chalf * 32) >> 5;
+            if (qw * 32 < S)
+              mwords[cc] = __ldg(drop.mask_k + (static_cast<uint64_t>(bh) * (S >> 5) + qw) * S + key);
+          }
+        }
+      }
       if (warp == 4 && lane == 0) TR(0);
       mbar_wait(&q_full[qs], (it / FB_NS) & 1);
 #pragma unroll
@@ -350,22 +395,18 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
         tc_fence_after();
         tmem_ld32(tS + trow + c, rs);
         tmem_ld32(tdP + trow + c, rd);
+        const uint32_t lv = lv_base + (qs * 2 * FB_N + c) * 4;
+        const float4 l4 = lds128f(lv), d4 = lds128f(lv + FB_N * 4);
         tmem_ld_wait();
         // this half of S/dP consumed: the next block's half may overwrite it
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&st_empty[cc]);
-        const uint32_t lv = lv_base + (qs * 2 * FB_N + c) * 4;
-        uint32_t mword = 0;
-        if constexpr (DROP) {
-          const int qw = (qi + c) >> 5;   // keep bits of queries qi+c .. +31, this key
-          if (drop.mask_k != nullptr && key < S && qw * 32 < S)
-            mword = drop.mask_k[(static_cast<uint64_t>(bh) * (S >> 5) + qw) * S + key];
-        }
+        const uint32_t mword = mwords[cc];
         if (need_mask)
-          softmax_grad(std::true_type{}, rs, rd, lv, qi + c, qlo, pp, pg, mword);
+          softmax_grad(std::true_type{}, rs, rd, lv, qi + c, qlo, pp, pg, mword, l4, d4);
         else
-          softmax_grad(std::false_type{}, rs, rd, lv, qi + c, qlo, pp, pg, mword);
+          softmax_grad(std::false_type{}, rs, rd, lv, qi + c, qlo, pp, pg, mword, l4, d4);
         if (warp == 4 && lane == 0) { if (cc == 0) TR(2); else TR(4); }
         if (cc == 0) {
           mbar_wait(pt_empty, (it & 1) ^ 1);                  // dV of the previous block done

@@ -226,6 +226,17 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
       if (lane == 0) mbar_arrive(q_tmem);
     }
     for (int j = 0; j < n_kb; ++j) {
+      // keep bits of keys j*64 .. +63 for this row: the pre-drawn mask's two
+      // coalesced words, requested before the wait so the load latency hides
+      uint32_t mk0 = 0, mk1 = 0;
+      if constexpr (DROP) {
+        const int kk0 = j * TA_BN;
+        if (drop.mask_q != nullptr && q < S) {
+          const uint32_t* mq = drop.mask_q + (static_cast<uint64_t>(bh) * (S >> 5) + (kk0 >> 5)) * S + q;
+          mk0 = __ldg(mq);
+          if (kk0 + 32 < S) mk1 = __ldg(mq + S);
+        }
+      }
       if (warp == 4 && lane == 0) TRF(j, 0);
       mbar_wait(&s_full[j & 1], (j >> 1) & 1);
       if (warp == 4 && lane == 0) TRF(j, 1);
@@ -268,27 +279,25 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
       const bool grow = m_cand > m + 8.f;   // lazy: keep a stale max unless it grew > 2^8
       const float m_new = grow ? m_cand : m;
       const float corr = fast_exp2(m - m_new);  // 1 when !grow; 0 for the first block
-      // P = exp2(s*scale - m), row sum
-      float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      // P = exp2(s*scale - m) (scale-and-shift and the row sums two lanes per
+      // FFMA2 / FADD2), row sum
+      const uint64_t sc2 = f2pack(scale_log2, scale_log2), nm2 = f2pack(-m_new, -m_new);
+      uint64_t ps2[4] = {0ull, 0ull, 0ull, 0ull};
       uint4 pk[TA_BN / 8];
       const uint64_t dpair = (((static_cast<uint64_t>(bh) * S + q) * S) + k0) >> 1;
-      // keep bits of keys k0..k0+63 for this row: from the pre-drawn mask
-      // (two coalesced words) or hashed here
-      uint32_t mk0 = 0, mk1 = 0;
-      if constexpr (DROP) {
-        if (drop.mask_q != nullptr && q < S) {
-          const uint32_t* mq = drop.mask_q + (static_cast<uint64_t>(bh) * (S >> 5) + (k0 >> 5)) * S + q;
-          mk0 = mq[0];
-          if (k0 + 32 < S) mk1 = mq[S];
-        }
-      }
+
 #pragma unroll
       for (int g = 0; g < TA_BN / 8; ++g) {
         float f[8];
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          f[t] = fast_exp2(fmaf(__uint_as_float(sc[g * 8 + t]), scale_log2, -m_new));
-          ps[t] += f[t];
+        for (int t = 0; t < 4; ++t) {
+          const uint64_t x2 = ffma2(f2pack(__uint_as_float(sc[g * 8 + 2 * t]),
+                                           __uint_as_float(sc[g * 8 + 2 * t + 1])), sc2, nm2);
+          float a, b;
+          f2unpack(x2, a, b);
+          f[2 * t] = fast_exp2(a);
+          f[2 * t + 1] = fast_exp2(b);
+          ps2[t] = fadd2(ps2[t], f2pack(f[2 * t], f[2 * t + 1]));
         }
         if constexpr (DROP) {
           if (drop.mask_q != nullptr) {
@@ -340,6 +349,9 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
         for (int g = 0; g < TA_BN / 8; ++g) sts128(rowp + ((g ^ (r & 7)) << 4), pk[g]);
       }
       if (warp == 4 && lane == 0) TRF(j, 3);
+      float ps[8];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) f2unpack(ps2[t], ps[2 * t], ps[2 * t + 1]);
       const float sum = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
       tc_fence_before();
       fence_async_smem();
