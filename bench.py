@@ -64,10 +64,13 @@ def parse():
                     help="P>1 task order: the reference's opportunistic policy replayed over "
                          "the calibration profile (default), run live on real arrivals, or the "
                          "static Varuna schedule")
-    ap.add_argument("--retune", action="store_true",
-                    help="opportunistic replay: re-derive the order from one traced step's "
-                         "measured stage times, keeping the fastest of a few perturbed "
-                         "candidates (off by default)")
+    ap.add_argument("--no-retune", action="store_true",
+                    help="opportunistic replay: keep the order derived from the calibration "
+                         "profile instead of re-deriving it (reference policy, replica kernel) "
+                         "from one traced step's MEASURED stage times")
+    ap.add_argument("--retune-perturb", action="store_true",
+                    help="also try the replica kernel's orders under x0.85..1.15-scaled "
+                         "times (off by default)")
     ap.add_argument("--cpu-sample-s", type=float, default=20.0)
     ap.add_argument("--dropout", type=float, default=None,
                     help="hidden + attention dropout of the run (default: the config's)")
@@ -511,13 +514,13 @@ def main():
     for _ in range(args.warmup):
         v.step(dbatch)
     barrier()
-    if P > 1 and dispatch == "opportunistic" and args.retune:
+    if P > 1 and dispatch == "opportunistic" and not args.no_retune:
         # one traced step: the dispatch order is re-derived by the reference's
         # opportunistic replica kernel from the MEASURED per-stage task times
         v.trace = True
         tl0 = v.step(dbatch).timeline
         v.trace = False
-        v.retune_dispatch(tl0)
+        v.retune_dispatch(tl0, perturb=args.retune_perturb)
         v.step(dbatch)
         barrier()
 

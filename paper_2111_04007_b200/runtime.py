@@ -273,8 +273,10 @@ class _Links:
     ACT, GRAD = 0, 1
     FREE = 2   # channel offset of the credits
 
-    def __init__(self, rank, stage, P, slots_act, slots_grad, slot_elems, gloo_group, shm):
+    def __init__(self, rank, stage, P, slots_act, slots_grad, slot_elems, gloo_group, shm,
+                 epoch_g: int = 1):
         self.rank, self.stage, self.P = rank, stage, P
+        self.epoch_g = epoch_g   # first micro-batch written through these rings
         self.slot_bytes = slot_elems * 2
         self.shm = shm
         up, down = rank - 1, rank + 1
@@ -401,7 +403,7 @@ class _Links:
         """Before writing micro-batch g into the peer ring: wait (host, then
         device) until the slot's previous occupant g - n was released."""
         n = self.tx_n[direction]
-        if g - n < 1:
+        if g - n < self.epoch_g:   # the slot has not been used by these rings yet
             return
         s = g % n
         self.shm.wait(self.consumer[direction], self.FREE + direction, s, g - n)
@@ -446,14 +448,17 @@ def exchange_stage_means(means, rank: int, world: int, device="cpu", group=None)
 
 
 def retune_order(schedule: Schedule, P: int, D: int, m: int, N: int, hidden: int, seq_len: int,
-                 table: torch.Tensor, current, max_in_flight: Optional[int] = None) -> list:
+                 table: torch.Tensor, current, max_in_flight: Optional[int] = None,
+                 perturb: bool = False) -> list:
     """Pick the per-stage dispatch order with the shortest simulated
     mini-batch under the measured stage times (replica 0's rows of
     ``table``): candidates are the static Varuna order, the order in use
-    (``current``, one task list per stage) and the opportunistic replica
-    kernel's orders under the measured times with backward and recompute
-    scaled x0.85..1.15 (the kernel is a heuristic). Deterministic: every
-    rank given the same table and current orders returns the same order."""
+    (``current``, one task list per stage) and the reference's opportunistic
+    replica kernel's order under the MEASURED times (the reference policy
+    fed a B200-measured profile); ``perturb`` adds the
+    kernel's orders with backward / recompute scaled x0.85..1.15 (the policy
+    is a heuristic). Deterministic: every rank given the same table and
+    current orders returns the same order."""
     from .calibration import CalibrationProfile, CutpointTimes
     from .core import make_block_model, uniform_cluster
     from .simulator import build_placement, execution_order, simulate_minibatch
@@ -473,8 +478,9 @@ def retune_order(schedule: Schedule, P: int, D: int, m: int, N: int, hidden: int
     model = make_block_model("stages", P, hidden, seq_len)
     cands = [[list(zip(*[a.tolist() for a in schedule.stage_slice(k)])) for k in range(P)],
              [list(t) for t in current]]
-    for fb in (1.0, 0.85, 1.15):
-        for rs in (1.0, 0.85, 1.15):
+    scales = (1.0, 0.85, 1.15) if perturb else (1.0,)
+    for fb in scales:
+        for rs in scales:
             o = execution_order(schedule, pc, profile(fb), model, opportunistic=True,
                                 recompute_scale=rscale * rs)
             if o not in cands:
@@ -638,7 +644,7 @@ class Varuna:
         model = make_block_model("stages", cfg.n_layer, cfg.hidden, cfg.seq_len)
         return execution_order(self.schedule, pc, profile, model, opportunistic=True)
 
-    def retune_dispatch(self, timeline: dict) -> None:
+    def retune_dispatch(self, timeline: dict, perturb: bool = False) -> None:
         """Re-derive the opportunistic dispatch order from MEASURED task
         times: every rank contributes its stage's mean F/R/B of a traced step
         (``step(trace=True)`` timeline), and the replica kernel re-runs the
@@ -651,11 +657,28 @@ class Varuna:
         else:
             current = [self.tasks]
         best = retune_order(self.schedule, self.P, self.D, self.m, self.N, self.cfg.hidden,
-                            self.cfg.seq_len, table, current[:self.P],
-                            max_in_flight=self.n_ring - RING_PAD if self.P > 1 else None)
+                            self.cfg.seq_len, table, current[:self.P], perturb=perturb)
         self.tasks = best[self.stage_id]
         self.dispatch = "opportunistic"
         self._check_plan()
+        need = max(in_flight(o) for o in best) + RING_PAD
+        if self.P > 1 and need > self.n_ring and self.n_ring < self.N:
+            self._resize_rings(min(self.N, -(-need // self.n_grad) * self.n_grad))
+
+    def _resize_rings(self, n_ring: int) -> None:
+        """Rebuild the activation rings with ``n_ring`` slots (every rank of
+        the job, between steps): unmap and free the old rings, exchange new
+        IPC handles, drop the captured graphs (their slot keys changed)."""
+        torch.cuda.synchronize(self.device)
+        self.links.close()
+        dist.barrier(group=self.gloo)
+        self.links.free_local()
+        self.n_ring = n_ring
+        slot_elems = self.m * self.cfg.seq_len * self.cfg.hidden
+        self.links = _Links(self.rank, self.stage_id, self.P, [0] + [n_ring] * (self.P - 1),
+                            [self.n_grad] * (self.P - 1) + [0], slot_elems, self.gloo, self.shm,
+                            epoch_g=self.step_count * self.N + 1)
+        self._graphs = {}
 
     def _check_plan(self):
         """The executor relies on rule 2 (R(j) directly before B(j)), on the

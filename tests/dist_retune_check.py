@@ -19,7 +19,7 @@ def main():
     from paper_2111_04007_b200.model import CONFIGS
     from paper_2111_04007_b200.runtime import AdamWConfig, Varuna, synthetic_batch
     cfg = CONFIGS["tiny"]
-    pc = ParallelConfig(2, 1, 4, 6, (0, 0, 0, 1))   # unbalanced: stage 0 slower
+    pc = ParallelConfig(2, 1, 2, 12, (0, 0, 0, 1))   # unbalanced: stage 0 slower
     losses = {}
     for retune in (False, True):
         v = Varuna(cfg, pc, optimizer=AdamWConfig(lr=1e-3), seed=0)
@@ -31,6 +31,11 @@ def main():
                 res = v.step(b)
                 v.trace = False
                 v.retune_dispatch(res.timeline)
+                # grow the bounded activation rings between steps (what a
+                # retuned order needing more in-flight slots triggers)
+                assert v.n_ring < 12, v.n_ring
+                v._resize_rings(12)
+                assert v.links.rx_n.get(0, 12) == 12 and v.links.tx_n.get(0, 12) == 12
             else:
                 res = v.step(b)
             out.append(res.loss if res.loss is not None else 0.0)
