@@ -16,12 +16,16 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INC = os.path.join(ROOT, "include")
-OBJ = os.path.join(PKG, "_build")
-LIB = os.path.join(PKG, "libvpipe.so")
+# VP_BUILD_TAG builds an alternative library (e.g. with VP_EXTRA_NVCC=-DVP_BWD_TRACE
+# for the clock64 timelines) beside the product one; load it with VP_LIB_PATH
+_TAG = os.environ.get("VP_BUILD_TAG", "")
+OBJ = os.path.join(PKG, "_build" + (f"_{_TAG}" if _TAG else ""))
+LIB = os.path.join(PKG, f"libvpipe{'_' + _TAG if _TAG else ''}.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{INC}", f"-I{CSRC}"]
-CU_FLAGS = ARCH + COMMON + ["-lineinfo", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
+CU_FLAGS = ARCH + COMMON + ["-lineinfo", "--expt-relaxed-constexpr", "-Xptxas", "-v"] + \
+    os.environ.get("VP_EXTRA_NVCC", "").split()
 
 
 def _deps(src):

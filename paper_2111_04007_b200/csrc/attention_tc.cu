@@ -19,6 +19,7 @@
 #include <cudaTypedefs.h>
 
 #include <cfloat>
+#include <cstdlib>
 
 namespace vp {
 namespace {
@@ -53,7 +54,8 @@ struct TaSmem {
   static constexpr int V_OFF = K_OFF + STAGES * KTILE;
   static constexpr int P_OFF = V_OFF + STAGES * KTILE;  // [2][128 x 64] bf16 = 2 x 16 KB
   static constexpr int BAR_OFF = P_OFF + 2 * 128 * TA_BN * 2;
-  static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+  static constexpr int RED_OFF = BAR_OFF + 256;      // [2 bufs][2 halves][128 rows] f32 (SW = 8)
+  static constexpr int TOTAL = RED_OFF + 2 * 2 * 128 * 4 + 1024;
 };
 
 #ifdef VP_BWD_TRACE
@@ -67,11 +69,18 @@ __device__ unsigned long long g_vp_ftrace[4][32][8];
 // kept iff the mask bit of element ((b*H + h)*S + i)*S + j is set; the row
 // sum l (and the LSE) use the undropped P, the 1/(1-p) scale is folded into
 // the final O = acc * scale / l.
-template <int D, bool CAUSAL, bool DROP>
-__global__ void __launch_bounds__(TA_THREADS, 2)
+// SW softmax warps per CTA: 4 (thread = query row, all 64 keys of a block)
+// or 8 (head_dim 64: the two warps of a TMEM lane quadrant split a block's
+// keys 32/32 — half the per-thread work per block and twice the warps to hide
+// the MUFU / TMEM / barrier latencies; the row max is exchanged through shared
+// memory under a 64-thread named barrier, the row sums only at the end).
+template <int D, bool CAUSAL, bool DROP, int SW = 4>
+__global__ void __launch_bounds__(128 + 32 * SW, 2)
     attn_fwd_tc(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmKV,
                 __nv_bfloat16* __restrict__ out,
                 float* __restrict__ lse, int S, int H, int n_qb, float scale_log2, AttnDrop drop) {
+  static_assert(SW == 4 || (SW == 8 && D == 64), "split softmax: head_dim 64 only");
+  constexpr int NK = TA_BN * 4 / SW;      // keys per softmax thread per block
   using L = TaSmem<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -106,13 +115,13 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 4);
+      mbar_init(&s_empty[i], SW);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&o_full[i], 1);
-      mbar_init(&p_full[i], 4);
+      mbar_init(&p_full[i], SW);
     }
-    mbar_init(q_tmem, 4);
+    mbar_init(q_tmem, SW);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 256);
@@ -197,11 +206,14 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
   } else if (warp >= 4) {
     // ===== softmax / correction / epilogue: thread = query row =====
     const uint32_t qd = warp & 3;
+    const int half = static_cast<int>(warp - 4) >> 2;   // 0 when SW == 4
+    const int koff = half * NK;                          // this thread's keys in a block
     const int r = qd * 32 + lane;
     const int q = q0 + r;
     const uint32_t trow = (qd * 32) << 16;
     const uint32_t tO = tmem + trow + 128;
     uint8_t* sP = smem + L::P_OFF;
+    float* red = reinterpret_cast<float*>(smem + L::RED_OFF);
     float m = -FLT_MAX, l = 0.f;
     uint32_t dkey = 0;
     if constexpr (DROP) dkey = drop_key(drop.seed, drop.salt);
@@ -218,8 +230,8 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
                      : "r"(qrow + ((k ^ (r & 7)) << 4)));
         qw[4 * k] = u.x; qw[4 * k + 1] = u.y; qw[4 * k + 2] = u.z; qw[4 * k + 3] = u.w;
       }
-      tmem_st16(tmem + trow + L::TQ, qw);
-      tmem_st16(tmem + trow + L::TQ + 16, qw + 16);
+      if (SW == 4 || half == 0) tmem_st16(tmem + trow + L::TQ, qw);
+      if (SW == 4 || half == 1) tmem_st16(tmem + trow + L::TQ + 16, qw + 16);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
@@ -241,17 +253,17 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
       mbar_wait(&s_full[j & 1], (j >> 1) & 1);
       if (warp == 4 && lane == 0) TRF(j, 1);
       tc_fence_after();
-      const uint32_t ts = tmem + trow + (j & 1) * TA_BN;
-      const int k0 = j * TA_BN;
-      const bool need_mask = (k0 + TA_BN > S) || (CAUSAL && k0 + TA_BN - 1 > q0);
+      const uint32_t ts = tmem + trow + (j & 1) * TA_BN + koff;
+      const int k0 = j * TA_BN + koff;   // this thread's first key
+      const bool need_mask = (k0 + NK > S) || (CAUSAL && k0 + NK - 1 > q0);
       // One TMEM read of the block's scores (64 fp32 per row, in registers);
       // row max with 8 independent partial maxima (short dependency chains).
       // Masking is one compare per element against the row's key limit
       // (keys >= lim are dead: past the sequence or above the diagonal).
       const int lim = CAUSAL ? min(S, q + 1) : S;
-      uint32_t sc[TA_BN];
+      uint32_t sc[NK];
       tmem_ld32(ts, *reinterpret_cast<uint32_t(*)[32]>(sc));
-      tmem_ld32(ts + 32, *reinterpret_cast<uint32_t(*)[32]>(sc + 32));
+      if constexpr (NK == 64) tmem_ld32(ts + 32, *reinterpret_cast<uint32_t(*)[32]>(sc + 32));
       tmem_ld_wait();
       // S_j consumed: the MMA warp may reuse this TMEM buffer
       tc_fence_before();
@@ -260,7 +272,7 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
       // masked scores -> -inf: exp2 gives exactly 0, no select per element
       if (need_mask) {
 #pragma unroll
-        for (int i = 0; i < TA_BN; ++i)
+        for (int i = 0; i < NK; ++i)
           if (k0 + i >= lim) sc[i] = __float_as_uint(-INFINITY);
       }
       // row max: 3-input FMNMX3, 8 independent chains
@@ -268,13 +280,21 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
 #pragma unroll
       for (int t = 0; t < 8; ++t) pm[t] = __uint_as_float(sc[t]);
 #pragma unroll
-      for (int i = 8; i < TA_BN; i += 16) {
+      for (int i = 8; i < NK; i += 16) {
 #pragma unroll
         for (int t = 0; t < 8; ++t)
           pm[t] = fmax3(pm[t], __uint_as_float(sc[i + t]), __uint_as_float(sc[i + 8 + t]));
       }
-      const float mx = fmax3(fmax3(pm[0], pm[1], pm[2]), fmax3(pm[3], pm[4], pm[5]),
-                             fmaxf(pm[6], pm[7]));
+      float mx = fmax3(fmax3(pm[0], pm[1], pm[2]), fmax3(pm[3], pm[4], pm[5]),
+                       fmaxf(pm[6], pm[7]));
+      if constexpr (SW == 8) {
+        // the row's other 32 keys are in the partner warp: exchange maxima
+        // (double-buffered slot, 64-thread named barrier per lane quadrant)
+        float* rb = red + (j & 1) * 256;
+        rb[half * 128 + r] = mx;
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + static_cast<int>(qd)) : "memory");
+        mx = fmaxf(mx, rb[(half ^ 1) * 128 + r]);
+      }
       const float m_cand = fmaxf(m, mx * scale_log2);
       const bool grow = m_cand > m + 8.f;   // lazy: keep a stale max unless it grew > 2^8
       const float m_new = grow ? m_cand : m;
@@ -283,17 +303,19 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
       // FFMA2 / FADD2), row sum
       const uint64_t sc2 = f2pack(scale_log2, scale_log2), nm2 = f2pack(-m_new, -m_new);
       uint64_t ps2[4] = {0ull, 0ull, 0ull, 0ull};
-      uint4 pk[TA_BN / 8];
+      uint4 pk[NK / 8];
       const uint64_t dpair = (((static_cast<uint64_t>(bh) * S + q) * S) + k0) >> 1;
 
 #pragma unroll
-      for (int g = 0; g < TA_BN / 8; ++g) {
+      for (int g = 0; g < NK / 8; ++g) {
         float f[8];
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           const uint64_t x2 = ffma2(f2pack(__uint_as_float(sc[g * 8 + 2 * t]),
                                            __uint_as_float(sc[g * 8 + 2 * t + 1])), sc2, nm2);
           float a, b;
+          // (a degree-3 polynomial exp2 on the FMA pipes for one pair in four
+          // measured slower, 203 vs 164 us at 32x1024x16x64, r02s)
           f2unpack(x2, a, b);
           f[2 * t] = fast_exp2(a);
           f[2 * t + 1] = fast_exp2(b);
@@ -301,7 +323,7 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
         }
         if constexpr (DROP) {
           if (drop.mask_q != nullptr) {
-            const uint32_t mw = (g < 4 ? mk0 : mk1) >> ((g & 3) * 8);
+            const uint32_t mw = ((g + half * 4) < 4 ? mk0 : mk1) >> ((g & 3) * 8);
 #pragma unroll
             for (int t = 0; t < 8; ++t) f[t] = ((mw >> t) & 1u) ? f[t] : 0.f;
           } else {
@@ -328,7 +350,8 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
         tc_fence_after();
         {
 #pragma unroll 1
-          for (int c = 0; c < D; c += 32) {
+          for (int c = (SW == 8 ? half * (D / 2) : 0); c < (SW == 8 ? (half + 1) * (D / 2) : D);
+               c += 32) {
             uint32_t raw[32];
             tmem_ld32(tO + c, raw);
             tmem_ld_wait();
@@ -340,13 +363,15 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
         }
       }
       if constexpr (L::PT) {
-        tmem_st16(tmem + trow + L::TP, reinterpret_cast<const uint32_t*>(pk));
-        tmem_st16(tmem + trow + L::TP + 16, reinterpret_cast<const uint32_t*>(pk + 4));
+        tmem_st16(tmem + trow + L::TP + (koff >> 1), reinterpret_cast<const uint32_t*>(pk));
+        if constexpr (NK == 64)
+          tmem_st16(tmem + trow + L::TP + 16, reinterpret_cast<const uint32_t*>(pk + 4));
         tmem_st_wait();
       } else {
         const uint32_t rowp = smem_u32(sP + (j & 1) * 128 * TA_BN * 2 + r * 128);
 #pragma unroll
-        for (int g = 0; g < TA_BN / 8; ++g) sts128(rowp + ((g ^ (r & 7)) << 4), pk[g]);
+        for (int g = 0; g < NK / 8; ++g)
+          sts128(rowp + (((g + (koff >> 3)) ^ (r & 7)) << 4), pk[g]);
       }
       if (warp == 4 && lane == 0) TRF(j, 3);
       float ps[8];
@@ -360,12 +385,18 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
       l = l * corr + sum;
       m = m_new;
     }
+    if constexpr (SW == 8) {   // the row sum's other half is the partner warp's
+      red[half * 128 + r] = l;
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + static_cast<int>(qd)) : "memory");
+      l += red[(half ^ 1) * 128 + r];
+    }
     mbar_wait(&o_full[(n_kb - 1) & 1], ((n_kb - 1) >> 1) & 1);
     tc_fence_after();
     const float inv = (DROP ? drop.scale : 1.f) / l;
     __nv_bfloat16* orow = out + (static_cast<int64_t>(b) * S + q) * Hd + h * D;
 #pragma unroll 1
-    for (int c = 0; c < D; c += 32) {
+    for (int c = (SW == 8 ? half * (D / 2) : 0); c < (SW == 8 ? (half + 1) * (D / 2) : D);
+         c += 32) {
       uint32_t raw[32];
       tmem_ld32(tO + c, raw);
       tmem_ld_wait();
@@ -379,7 +410,7 @@ __global__ void __launch_bounds__(TA_THREADS, 2)
         }
       }
     }
-    if (q < S) lse[static_cast<int64_t>(bh) * S + q] = m + __log2f(l);
+    if (q < S && half == 0) lse[static_cast<int64_t>(bh) * S + q] = m + __log2f(l);
   }
   tc_fence_before();
   __syncthreads();
@@ -994,11 +1025,26 @@ int fwd_tc_t(const void* qkv, void* o, float* lse, int64_t B, int64_t S, int64_t
   CUtensorMap tm, tkv;
   if (!make_tmap_bsc(&tm, qkv, 3 * H * D, S, B, 128)) return VP_ERR_UNSUPPORTED;
   if (!make_tmap_bsc(&tkv, qkv, 3 * H * D, S, B, TA_BN)) return VP_ERR_UNSUPPORTED;
-  auto k = attn_fwd_tc<D, CAUSAL, DROP>;
-  if (cudaError_t e = smem_optin(k, L::TOTAL); e != cudaSuccess) return e;
   const int n_qb = static_cast<int>((S + TA_BM - 1) / TA_BM);
   dim3 grid(n_qb, static_cast<unsigned>(B * H));
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(D));
+  // 4 softmax warps (a thread owns a whole row); VP_ATTN_FWD_SW=8 selects
+  // the split-row variant for head_dim 64 — measured slower (179 vs 164 us
+  // at 32x1024x16x64 causal, r02q): the extra warps do not hide more than
+  // the max exchange and its named barrier add
+  static const bool sw8 = getenv("VP_ATTN_FWD_SW") && atoi(getenv("VP_ATTN_FWD_SW")) == 8;
+  if constexpr (D == 64) {
+    if (sw8) {
+      auto k = attn_fwd_tc<D, CAUSAL, DROP, 8>;
+      if (cudaError_t e = smem_optin(k, L::TOTAL); e != cudaSuccess) return e;
+      k<<<grid, 128 + 32 * 8, L::TOTAL, st>>>(tm, tkv, reinterpret_cast<__nv_bfloat16*>(o), lse,
+                                              static_cast<int>(S), static_cast<int>(H), n_qb,
+                                              scale_log2, drop);
+      return launch_status();
+    }
+  }
+  auto k = attn_fwd_tc<D, CAUSAL, DROP, 4>;
+  if (cudaError_t e = smem_optin(k, L::TOTAL); e != cudaSuccess) return e;
   k<<<grid, TA_THREADS, L::TOTAL, st>>>(tm, tkv, reinterpret_cast<__nv_bfloat16*>(o), lse,
                                         static_cast<int>(S), static_cast<int>(H), n_qb,
                                         scale_log2, drop);
