@@ -265,6 +265,9 @@ int vp_dropout(void* x, int64_t n, float p, uint64_t seed, uint64_t offset, void
  * So R(j) regenerates F(j)'s masks bit for bit (RNG state
  * restored for recompute). */
 int vp_set_seed(uint64_t* dst, uint64_t value, void* stream);
+/* x[0..n) = value (fp32): the per-step resets of the loss accumulator and
+ * the norm / overflow flags. */
+int vp_fill_f32(float* x, float value, int64_t n, void* stream);
 /* x[n] (bf16, n even) *= mask(e) in place, e = flat index. */
 int vp_dropout_dev(void* x, int64_t n, float p, const uint64_t* seed, uint32_t salt,
                    void* stream);

@@ -439,6 +439,11 @@ __global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __rest
 // ------------------------------------------------------------ dropout / add
 __global__ void set_seed_kernel(uint64_t* dst, uint64_t v) { *dst = v; }
 
+__global__ void fill_f32_kernel(float* __restrict__ x, float v, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = v;
+}
+
 // in place, flat element index e (n even; 8 per thread)
 __global__ void dropout_dev_kernel(__nv_bfloat16* __restrict__ x, int64_t n,
                                    const uint64_t* __restrict__ seed, uint32_t salt, uint32_t thr,
@@ -798,6 +803,13 @@ extern "C" int vp_bias_grad(const void* dy, float* dbias, int64_t rows, int64_t 
   colsum_kernel<false><<<grid, 256, 0, ST>>>(CBF(dy), workspace + kColsumCounters, counters,
                                              dbias, rows, cols, rpp, static_cast<int>(parts),
                                              nullptr, nullptr, 0, 0, 0.f);
+  return launch_status();
+}
+
+extern "C" int vp_fill_f32(float* x, float value, int64_t n, void* stream) {
+  if (!x || n < 0) return VP_ERR_ARGS;
+  if (n == 0) return VP_OK;
+  fill_f32_kernel<<<blocks_for(n, 256), 256, 0, ST>>>(x, value, n);
   return launch_status();
 }
 

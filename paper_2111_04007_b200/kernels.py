@@ -38,6 +38,7 @@ _SIGS = {
     "vp_attention_fwd_ex": [vp, vp, vp, i64, i64, i64, i64, c_int, f32, vp, u32, vp, vp],
     "vp_attention_mask_words": [i64, i64, i64],
     "vp_set_seed": [vp, u64, vp],
+    "vp_fill_f32": [vp, f32, i64, vp],
     "vp_xent_fwd_bwd_dev": [vp, vp, vp, vp, i64, i64, f32, vp, vp],
     "vp_adam_step_dev": [vp, vp, vp, vp, vp, i64, vp, f32, f32, f32, f32, f32, f32, vp, vp],
     "vp_loss_scaler_update": [vp, vp, f32, f32, i64, f32, f32, vp],
@@ -333,6 +334,13 @@ def set_seed(buf, value: int, stream=None):
     buffer every dropout site reads (outside captured graphs)."""
     _count(1)
     check(L.vp_set_seed(buf.data_ptr(), value & 0xFFFFFFFFFFFFFFFF, _stream(stream)), "vp_set_seed")
+
+
+def fill_f32_(x, value=0.0, stream=None):
+    _need(x, torch.float32, "fill_f32_")
+    _count(1)
+    check(L.vp_fill_f32(x.data_ptr(), value, x.numel(), _stream(stream)), "vp_fill_f32")
+    return x
 
 
 def dropout_dev_(x, p, seed, salt, stream=None):

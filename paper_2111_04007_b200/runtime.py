@@ -841,7 +841,7 @@ class Varuna:
         with torch.cuda.stream(st):
             data = self._device_batch(batch)
             if self.spec.last:
-                self.loss_sum.zero_()
+                K.fill_f32_(self.loss_sum, 0.0, st)
             t_start = self._mark(ev)
             ctx = _StepCtx(g0=(self.step_count - 1) * self.N + 1, data=data, scale=scale, ev=ev,
                            graphs=self.use_graphs and not K.GEMM_TIMING["on"]
@@ -1083,7 +1083,7 @@ class Varuna:
         seg = self._tied_segment()
         if seg is not None:
             dist.all_reduce(P.grad[seg[0]:seg[1]], group=self.tie_group)       # C3
-        self.flags.zero_()
+        K.fill_f32_(self.flags, 0.0, self.stream)
         n_unique = P.numel
         if self.spec.last and not self.spec.first:
             n_unique = P.offsets["wte_head"]   # the tied copy is counted on stage 0
