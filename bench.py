@@ -158,7 +158,7 @@ def gemm_traffic():
     """DRAM bytes per launch of the representative GEMM (FC1 shape) from the
     committed ncu --set full capture (profiles/r01e_traffic.json), or None."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01e_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02", "r02t_traffic.json")) as f:
             t = json.load(f)
         return {"bytes_per_launch": t["dram_bytes"], "algorithmic_bytes": t["algorithmic_bytes"],
                 "kernel": t["kernel"], "source": t["source"]}
