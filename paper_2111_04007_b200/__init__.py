@@ -35,7 +35,10 @@ __version__ = "0.1.0"
 
 
 def __getattr__(name):
-    if name in ("Varuna", "CutPoint", "StepResult"):
+    if name in ("Varuna", "CutPoint", "StepResult", "LossScaler", "morph", "replan"):
         from . import runtime
         return getattr(runtime, name)
+    if name in ("GPT2", "TransformerLayer"):
+        from . import modules
+        return getattr(modules, name)
     raise AttributeError(name)

@@ -53,18 +53,8 @@ from .simulator import bubble_fraction
 F, R, B = KIND_FORWARD, KIND_RECOMPUTE, KIND_BACKWARD
 
 
-class CutPoint(torch.nn.Module):
-    """Marks a candidate pipeline boundary. Identity in the
-    forward pass; whether it is an active stage boundary is decided by
-    ``ParallelConfig.stage_map``. The GPT-2 model carries one CutPoint after
-    every transformer layer (K = n_layer)."""
-
-    def __init__(self, index: int = 0):
-        super().__init__()
-        self.index = index
-
-    def forward(self, x):
-        return x
+from .modules import GPT2 as GPT2Module  # noqa: E402  (drop-in model structure)
+from .modules import CutPoint  # noqa: E402,F401
 
 
 @dataclass(frozen=True)
@@ -519,11 +509,21 @@ class Varuna:
     """Pipeline-parallel training of a GPT-2 described by ``model`` under the
     ``config`` (P, D, m, N_m, stage_map) chosen by the reference planner."""
 
-    def __init__(self, model: GPT2Config, config: ParallelConfig, *,
+    def __init__(self, model, config: ParallelConfig, *,
                  optimizer: AdamWConfig = AdamWConfig(), seed: int = 0, loss_scale: float = 1.0,
                  device=None, init_device: str = "cpu", trace: bool = False,
                  dispatch: str = "static", profile=None, graphs: Optional[bool] = None,
                  backend: Optional[str] = None, global_batch: Optional[int] = None):
+        # ``model``: a GPT2Config (one CutPoint after every layer) or a model
+        # structure with user-placed CutPoints (modules.GPT2): the stage map
+        # then covers its CutPoint blocks and is expanded to layers here
+        self.module = None
+        if isinstance(model, GPT2Module):
+            self.module = model
+            config = ParallelConfig(config.pipeline_depth, config.data_parallel,
+                                    config.micro_batch_size, config.num_micro_batches,
+                                    model.layer_stage_map(config.stage_map))
+            model = model.cfg
         if len(config.stage_map) != model.n_layer:
             raise ConfigError(f"stage_map covers {len(config.stage_map)} cut-points, model has "
                               f"{model.n_layer} (one CutPoint per transformer layer)")

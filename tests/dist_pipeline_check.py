@@ -32,6 +32,9 @@ def main():
     ap.add_argument("--layers", type=int, default=0, help="cut the config to this many layers")
     ap.add_argument("--micro-batch", type=int, default=4)
     ap.add_argument("--dropout", type=float, default=0.0)
+    ap.add_argument("--cut-every", type=int, default=0,
+                    help="build the model as modules.GPT2 with a CutPoint every this many "
+                         "layers (stage map over the CutPoint blocks)")
     ap.add_argument("--steps", type=int, default=1,
                     help="train steps-1 steps (AdamW on both sides), check the last")
     ap.add_argument("--global-batch", type=int, default=0,
@@ -50,8 +53,15 @@ def main():
     if args.dropout:
         cfg = dataclasses.replace(cfg, dropout=args.dropout)
     P, D, N, m = args.P, args.D, args.N, args.micro_batch
-    model = make_block_model("tiny", cfg.n_layer, cfg.hidden, cfg.seq_len)
-    a = assign_stages(model, P, m, uniform_profile(cfg.n_layer, 1.0, 2.0, m_grid=(m,)))
+    module = None
+    if args.cut_every:
+        from paper_2111_04007_b200.modules import GPT2
+        module = GPT2(cfg, cut_every=args.cut_every)
+        spec = module.model_spec()
+        a = assign_stages(spec, P, m, uniform_profile(spec.num_cutpoints, 1.0, 2.0, m_grid=(m,)))
+    else:
+        model = make_block_model("tiny", cfg.n_layer, cfg.hidden, cfg.seq_len)
+        a = assign_stages(model, P, m, uniform_profile(cfg.n_layer, 1.0, 2.0, m_grid=(m,)))
     pc = ParallelConfig(P, D, m, N, a.stage_map)
     prof = None
     if args.dispatch == "opportunistic":
@@ -59,7 +69,10 @@ def main():
         # kernel reorders tasks relative to the static schedule
         prof = skewed_profile(m)
     M = args.global_batch or m * N * D
-    v = Varuna(cfg, pc, seed=0, dispatch=args.dispatch, profile=prof, global_batch=M)
+    v = Varuna(module if module is not None else cfg, pc, seed=0, dispatch=args.dispatch,
+               profile=prof, global_batch=M)
+    if module is not None:
+        pc = v.pc        # the per-layer stage map the oracle walks
     if args.dispatch == "opportunistic":
         kinds, mbs = v.schedule.stage_slice(v.stage_id)
         moved = sum(a != b for a, b in zip(zip(kinds.tolist(), mbs.tolist()), v.tasks))

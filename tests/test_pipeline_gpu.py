@@ -286,3 +286,21 @@ def test_dynamic_loss_scaler_skip_and_recover():
     assert v._ss.tolist()[:3] == [2.0 ** 16, 2.0, 0.0]
     v.close()
     ref.close()
+
+
+def test_module_with_cutpoints_equals_config():
+    """Varuna over a model structure with user CutPoints (every 2 layers) runs
+    the same math as over the config (one CutPoint per layer)."""
+    from paper_2111_04007_b200 import ParallelConfig
+    from paper_2111_04007_b200.model import CONFIGS
+    from paper_2111_04007_b200.modules import GPT2
+    from paper_2111_04007_b200.runtime import Varuna, synthetic_batch
+    cfg = CONFIGS["tiny"]
+    batch = synthetic_batch(cfg, 8, 0)
+    a = Varuna(GPT2(cfg, cut_every=2), ParallelConfig(1, 1, 4, 2, (0, 0)), seed=0)
+    b = Varuna(cfg, ParallelConfig(1, 1, 4, 2, (0,) * cfg.n_layer), seed=0)
+    assert a.pc.stage_map == (0,) * cfg.n_layer
+    la, lb = a.step(batch).loss, b.step(batch).loss
+    assert la == lb, (la, lb)
+    a.close()
+    b.close()

@@ -38,6 +38,9 @@ PIPE_CASES = [
     # steps (slots reused within and across steps; AdamW applied between)
     (2, 2, 1, "tiny", ["--N", "12", "--micro-batch", "2", "--steps", "3"]),
     (4, 4, 1, "tiny", ["--N", "10", "--micro-batch", "2", "--steps", "2"]),
+    # a user model structure with a CutPoint every 2 layers (modules.GPT2):
+    # the stage map covers its CutPoint blocks
+    (2, 2, 1, "tiny", ["--cut-every", "2"]),
     # live opportunistic dispatch (StagePolicy on real arrivals)
     (2, 2, 1, "tiny", ["--dispatch", "live", "--steps", "2"]),
     (4, 2, 2, "tiny", ["--dispatch", "live", "--dropout", "0.1"]),
