@@ -301,6 +301,6 @@ def test_module_with_cutpoints_equals_config():
     b = Varuna(cfg, ParallelConfig(1, 1, 4, 2, (0,) * cfg.n_layer), seed=0)
     assert a.pc.stage_map == (0,) * cfg.n_layer
     la, lb = a.step(batch).loss, b.step(batch).loss
-    assert la == lb, (la, lb)
+    assert abs(la - lb) <= 2e-6 * abs(lb), (la, lb)   # fp32 atomic loss sum order
     a.close()
     b.close()
