@@ -28,8 +28,11 @@ constexpr int TA_BM = 128;
 constexpr int TA_BN = 64;   // keys per block: TMEM S0|S1|O = 64+64+<=128 <= 256 cols -> 2 CTAs/SM
 constexpr int TA_THREADS = 256;
 // K/V ring depth: deep enough to cover the L2->SMEM TMA latency of a block
-// while the previous ones are consumed (2 CTAs/SM still fit at D=64).
-__host__ __device__ constexpr int ta_stages(int D) { return 3; }
+// while the previous ones are consumed. With P in TMEM (D <= 96) the smem P
+// buffers are not needed and D = 64 affords 5 stages at 2 CTAs/SM: the MMA
+// warp issues S_{j+2} right after the softmax warps load S_j, so block
+// j+2's K/V must already be resident then.
+__host__ __device__ constexpr int ta_stages(int D) { return D == 64 ? 5 : 3; }
 
 template <int D>
 struct TaSmem {
@@ -52,8 +55,8 @@ struct TaSmem {
   static constexpr int K_OFF = QTILE;                // [stage]
   static constexpr int STAGES = ta_stages(D);
   static constexpr int V_OFF = K_OFF + STAGES * KTILE;
-  static constexpr int P_OFF = V_OFF + STAGES * KTILE;  // [2][128 x 64] bf16 = 2 x 16 KB
-  static constexpr int BAR_OFF = P_OFF + 2 * 128 * TA_BN * 2;
+  static constexpr int P_OFF = V_OFF + STAGES * KTILE;  // [2][128 x 64] bf16 (smem P only)
+  static constexpr int BAR_OFF = P_OFF + (PT ? 0 : 2 * 128 * TA_BN * 2);
   static constexpr int RED_OFF = BAR_OFF + 256;      // [2 bufs][2 halves][128 rows] f32 (SW = 8)
   static constexpr int TOTAL = RED_OFF + 2 * 2 * 128 * 4 + 1024;
 };
@@ -86,15 +89,16 @@ __global__ void __launch_bounds__(128 + 32 * SW, 2)
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  static_assert(L::STAGES <= 8, "attention fwd barrier layout");
   uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;              // [STAGES <= 4]
-  uint64_t* kv_empty = bars + 5;             // [STAGES]
-  uint64_t* s_full = bars + 9;               // [2]
-  uint64_t* s_empty = bars + 11;             // [2]
-  uint64_t* o_full = bars + 13;              // [2]: PV_j commits o_full[j & 1]
-  uint64_t* p_full = bars + 15;              // [2]
-  uint64_t* q_tmem = bars + 17;              // Q copied into TMEM (4 softmax warps)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
+  uint64_t* kv_full = bars + 1;              // [STAGES <= 8]
+  uint64_t* kv_empty = bars + 9;             // [STAGES]
+  uint64_t* s_full = bars + 17;              // [2]
+  uint64_t* s_empty = bars + 19;             // [2]
+  uint64_t* o_full = bars + 21;              // [2]: PV_j commits o_full[j & 1]
+  uint64_t* p_full = bars + 23;              // [2]
+  uint64_t* q_tmem = bars + 25;              // Q copied into TMEM (the softmax warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 26);
 
   const int qb = n_qb - 1 - static_cast<int>(blockIdx.x);  // heavy (late) causal blocks first
   const int bh = blockIdx.y;
@@ -181,7 +185,7 @@ __global__ void __launch_bounds__(128 + 32 * SW, 2)
         umma_commit(&o_full[j & 1]);
         umma_commit(&kv_empty[st]);
       };
-      for (int j = 0; j < n_kb; ++j) {
+      auto issue_s = [&](int j) {
         const int st = j % L::STAGES;
         mbar_wait(&kv_full[st], (j / L::STAGES) & 1);
         mbar_wait(&s_empty[j & 1], ((j >> 1) & 1) ^ 1);
@@ -199,9 +203,18 @@ __global__ void __launch_bounds__(128 + 32 * SW, 2)
           }
         }
         umma_commit(&s_full[j & 1]);
-        if (j >= 1) issue_pv(j - 1);
+      };
+      // S_{j+2} is issued as soon as the softmax warps have LOADED S_j (its
+      // TMEM buffer is free then), ahead of PV_j, which waits for them to
+      // FINISH block j: the next score block is computed while a block's
+      // softmax runs, instead of after it (the MMA issue order used to gate
+      // S_{j+2} on P_j; clock64 timelines, profiles/r02/r02w_*)
+      if (n_kb > 0) issue_s(0);
+      if (n_kb > 1) issue_s(1);
+      for (int j = 0; j < n_kb; ++j) {
+        if (j + 2 < n_kb) issue_s(j + 2);
+        issue_pv(j);
       }
-      issue_pv(n_kb - 1);
     }
   } else if (warp >= 4) {
     // ===== softmax / correction / epilogue: thread = query row =====
@@ -314,9 +327,10 @@ __global__ void __launch_bounds__(128 + 32 * SW, 2)
           const uint64_t x2 = ffma2(f2pack(__uint_as_float(sc[g * 8 + 2 * t]),
                                            __uint_as_float(sc[g * 8 + 2 * t + 1])), sc2, nm2);
           float a, b;
-          // (a degree-3 polynomial exp2 on the FMA pipes for one pair in four
-          // measured slower, 203 vs 164 us at 32x1024x16x64, r02s)
           f2unpack(x2, a, b);
+          // (exp2 moved to the FMA pipes by a polynomial for 1/4 or 1/2 of
+          // the pairs, and the 8-warp split softmax, both measured no faster:
+          // the phase is latency-bound on the MUFU results, r02z)
           f[2 * t] = fast_exp2(a);
           f[2 * t + 1] = fast_exp2(b);
           ps2[t] = fadd2(ps2[t], f2pack(f[2 * t], f[2 * t + 1]));
