@@ -37,8 +37,11 @@ namespace vp {
 __device__ unsigned long long g_vp_trace[4][16][16];
 #define TR(slot) \
   do { if (blockIdx.x < 4 && it < 16) g_vp_trace[blockIdx.x][it][slot] = clock64(); } while (0)
+#define TRJ(jj, slot) \
+  do { if (blockIdx.x < 4 && (jj) < 16) g_vp_trace[blockIdx.x][jj][slot] = clock64(); } while (0)
 #else
 #define TR(slot) do {} while (0)
+#define TRJ(jj, slot) do {} while (0)
 #endif
 namespace {
 
@@ -222,6 +225,7 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
         const uint32_t sdO = sQ + L::TILE;
         const uint32_t sdSt = smem_u32(smem + L::DST_OFF + (j & 1) * 2 * L::TILE);
         mbar_wait(p_full, j & 1);
+        TRJ(j, 10);
         tc_fence_after();
         // dV += P^T dO (A = P^T from TMEM)
 #pragma unroll
@@ -239,6 +243,7 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
         umma_commit(&q_empty[qs]);  // Q_j, dO_j no longer needed
         // dQ_j = dS K once the drain warps emptied dQ_{j-1}
         mbar_wait(dq_empty, (j & 1) ^ 1);
+        TRJ(j, 11);
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < FB_M / 16; ++k)
@@ -246,6 +251,7 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
                    sdesc_sw128(sK + k * 2048, L::TILE, 1024), idQ, k > 0 ? 1u : 0u);
         umma_commit(dq_full);
         umma_commit(&ds_empty[j & 1]);
+        TRJ(j, 12);
       };
       for (int it = 0; it < n_it; ++it) {
         const int qs = it % FB_NS;
@@ -465,6 +471,7 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
     uint8_t* stg = smem + L::STG_OFF + qd * 4096;
     for (int j = 0; j < n_it; ++j) {
       mbar_wait(dq_full, j & 1);
+      if (warp == 4 + FB_CW && lane == 0) TRJ(j, 13);
       tc_fence_after();
       uint32_t v0[32], v1[32];
       tmem_ld32(tDQ + trow, v0);
