@@ -46,6 +46,11 @@ PIPE_CASES = [
     (4, 2, 2, "tiny", ["--dispatch", "live", "--dropout", "0.1"]),
     (4, 4, 1, "tiny", ["--dispatch", "live", "--N", "8", "--micro-batch", "2", "--steps", "2"]),
     (2, 2, 1, "tiny_bert", ["--dropout", "0.1"]),
+    # the 8-GPU north-star shapes as 8 ranks on one GPU: 4x2 (355M / 8.3B),
+    # 2x4 (BERT-large), 8x1 (2.5B; tiny widened to 8 layers)
+    (8, 4, 2, "tiny", []),
+    (8, 2, 4, "tiny", []),
+    (8, 8, 1, "tiny", ["--layers", "8", "--N", "8", "--micro-batch", "2"]),
     # BASELINE widths, two-layer cuts: 16 MiB (355M, m=1) and 1 MiB-per-row
     # (BERT-large) boundary messages through the rings
     (2, 2, 1, "gpt2_355m", ["--layers", "2", "--micro-batch", "1", "--N", "2"]),
