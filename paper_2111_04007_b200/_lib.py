@@ -42,7 +42,8 @@ u8p = ctypes.POINTER(ctypes.c_uint8)
 
 
 class ReplicaOut(ctypes.Structure):
-    _fields_ = [(n, i64p) for n in (
+    # output array addresses as plain integers (filled by the C++ kernel)
+    _fields_ = [(n, ctypes.c_void_p) for n in (
         "task_stage", "task_kind", "task_mb", "task_start", "task_end",
         "msg_send", "msg_grant", "msg_arrive", "msg_boundary", "msg_dir", "msg_mb",
         "last_bwd_end", "peak_stash", "peak_sets", "peak_mem")] + [
@@ -57,12 +58,15 @@ def _sig(name, argtypes, restype=ctypes.c_int):
 
 
 _sig("vp_version", [], ctypes.c_char_p)
-_sig("vp_varuna_schedule", [i64, i64, i64, i64, i64, i64, i64p, i64p, i64p])
-_sig("vp_gpipe_schedule", [i64, i64, i64, i64p, i64p, i64p])
-_sig("vp_run_replica", [i64, i64] + [i64p] * 12 + [ctypes.c_int, ctypes.c_int,
+# array arguments are passed as raw addresses (ptr() below): building a
+# ctypes POINTER object per array cost more than the C++ kernels themselves
+_vp = ctypes.c_void_p
+_sig("vp_varuna_schedule", [i64, i64, i64, i64, i64, i64, _vp, _vp, _vp])
+_sig("vp_gpipe_schedule", [i64, i64, i64, _vp, _vp, _vp])
+_sig("vp_run_replica", [i64, i64] + [_vp] * 12 + [ctypes.c_int, ctypes.c_int,
                                                    ctypes.POINTER(ReplicaOut)])
-_sig("vp_assign_stages", [i64, i64p, i64p, i64, ctypes.c_double, i64p])
-_sig("vp_identify_cutpoints", [i64, i64p, i64p, u8p, i64, ctypes.c_double, i64p])
+_sig("vp_assign_stages", [i64, _vp, _vp, i64, ctypes.c_double, _vp])
+_sig("vp_identify_cutpoints", [i64, _vp, _vp, _vp, i64, ctypes.c_double, _vp])
 
 
 class VpipeError(RuntimeError):
@@ -91,5 +95,6 @@ def check(rc: int, what: str = "vpipe"):
 
 
 def ptr(arr):
-    """int64 numpy array -> int64* (the array must stay alive)."""
-    return arr.ctypes.data_as(i64p)
+    """Address of a C-contiguous numpy array's data (the array must stay
+    alive for the call)."""
+    return arr.__array_interface__["data"][0]
