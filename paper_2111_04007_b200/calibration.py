@@ -11,6 +11,7 @@ from __future__ import annotations
 from dataclasses import dataclass
 from typing import Dict, Sequence, Tuple
 
+import numpy as np
 import yaml
 
 from .core import OPTIMIZER_BYTES_PER_PARAM, ConfigError, HardwareSpec, ModelSpec, us_from_seconds
@@ -84,6 +85,19 @@ class CalibrationProfile:
     @property
     def num_cutpoints(self) -> int:
         return len(self.cutpoints)
+
+    def column(self, name: str, key: int):
+        """int64 vector over cut-points of table ``name`` at grid point ``key``
+        (m, or D for ``allreduce_us``); memoised — the profile is frozen."""
+        cache = self.__dict__.setdefault("_columns", {})
+        col = cache.get((name, key))
+        if col is None:
+            axis = "D" if name == "allreduce_us" else "m"
+            col = np.array([_lookup(getattr(cp, name), key, i, axis)
+                            for i, cp in enumerate(self.cutpoints)], dtype=np.int64)
+            col.setflags(write=False)
+            cache[(name, key)] = col
+        return col
 
     def forward_us(self, i: int, m: int) -> int:
         return _lookup(self.cutpoints[i].forward_us, m, i, "m")

@@ -64,11 +64,26 @@ class Schedule:
     def in_flight_bound(self, stage: int) -> int:
         """Largest prefix (#F − #B) of stage ``stage`` (1-based): the number of
         stashed micro-batches the stage must hold; sizes its receive ring."""
-        kinds, _ = self.stage_slice(stage - 1)
-        if kinds.size == 0:
-            return 0
-        step = (kinds == KIND_FORWARD).astype(np.int64) - (kinds == KIND_BACKWARD).astype(np.int64)
-        return max(int(np.cumsum(step).max()), 0)
+        return self.in_flight_bounds[stage - 1]
+
+    @cached_property
+    def in_flight_bounds(self) -> Tuple[int, ...]:
+        out = []
+        for k in range(self.pipeline_depth):
+            kinds, _ = self.stage_slice(k)
+            if kinds.size == 0:
+                out.append(0)
+                continue
+            step = ((kinds == KIND_FORWARD).astype(np.int64)
+                    - (kinds == KIND_BACKWARD).astype(np.int64))
+            out.append(max(int(np.cumsum(step).max()), 0))
+        return tuple(out)
+
+    @cached_property
+    def recompute_counts(self) -> Tuple[int, ...]:
+        """Number of R tasks per stage (0-based order)."""
+        return tuple(int((self.stage_slice(k)[0] == KIND_RECOMPUTE).sum())
+                     for k in range(self.pipeline_depth))
 
 
 def _make(policy, p, n, kinds, mbs, offsets, tf, tb, tr) -> Schedule:
