@@ -1,6 +1,6 @@
 // Attention entry points (K2/K3 of DESIGN.md). The kernels live in
 // attention_tc.cu (tcgen05 forward, deterministic two-kernel backward) and
-// attention_bwd.cu (fused one-pass backward, head_dim 64); this file holds
+// attention_bwd.cu (fused one-pass backward, head_dim 64 and 96); this file holds
 // the C ABI and the delta pre-pass of the deterministic backward.
 #include <cfloat>
 #include <cstdlib>
@@ -19,8 +19,8 @@ int attention_bwd_tc(const void* qkv, const void* dout, const float* lse, const 
 int64_t attention_bwd_fused_ws(int64_t B, int64_t S, int64_t H, int64_t D);
 bool attention_bwd_fused_ok(int64_t D);
 int attention_bwd_fused(const void* qkv, const void* o, const void* dout, const float* lse,
-                        void* dqkv, float* ws, int64_t B, int64_t S, int64_t H, int causal,
-                        float* dbias, const AttnDrop& drop, cudaStream_t st);
+                        void* dqkv, float* ws, int64_t B, int64_t S, int64_t H, int64_t D,
+                        int causal, float* dbias, const AttnDrop& drop, cudaStream_t st);
 
 namespace {
 
@@ -213,8 +213,8 @@ extern "C" int vp_attention_bwd_ex(const void* qkv, const void* o, const void* d
     const AttnDrop dr = (seq % 32) ? make_attn_drop(p, seed, salt)
                                    : make_attn_drop(p, seed, salt, mask_q, mask_k);
     if (dr.seed && (seq & 1)) return VP_ERR_UNSUPPORTED;
-    return attention_bwd_fused(qkv, o, dout, lse, dqkv, workspace, batch, seq, heads, causal,
-                               dbias, dr, st);
+    return attention_bwd_fused(qkv, o, dout, lse, dqkv, workspace, batch, seq, heads, head_dim,
+                               causal, dbias, dr, st);
   }
   if (dbias) return VP_ERR_UNSUPPORTED;  // bias sums are fused only into the one-pass kernel
   return attn_bwd_det(qkv, o, dout, lse, dqkv, workspace, batch, seq, heads, head_dim, causal, p,

@@ -1,4 +1,4 @@
-// Fused attention backward on tcgen05 (K3 of DESIGN.md), head_dim 64.
+// Fused attention backward on tcgen05 (K3 of DESIGN.md), head_dim 64 and 96.
 //
 // One CTA per (128-key block, batch*head); it loops over the 128-query blocks
 // the keys are visible to (causal: i >= kb) and produces dK, dV for its keys
@@ -25,6 +25,16 @@
 //               then dQ_{i-1}: TMEM -> smem (fp32, SW128) -> TMA reduce-add.
 //               At the end dK (x scale) and dV -> dqkv.
 // dQacc is zeroed by the delta pre-pass and scaled to bf16 by a post-pass.
+//
+// head_dim 96 (GPT-2 2.5B / 8.3B): S^T, dP^T, dV, dK and P^T take
+// 128+128+96+96+64 TMEM columns, so dQ_i has no columns of its own: it is
+// computed into S^T's columns once the softmax warps have loaded the next
+// block's S^T (S^T_{i+1} was issued before dQ_i, so the tensor core never
+// idles for it), and S^T_{i+2} is issued after the drain warps have read
+// dQ_i out — a full softmax block of slack on both sides. Tiles are a
+// 64-wide SWIZZLE_128B chunk plus a 32-wide SWIZZLE_64B chunk (no padding to
+// 128), the Q/dO ring has 2 stages and the dQ staging tiles are 16 rows,
+// which fits the 227 KB of shared memory.
 #include "sm100.cuh"
 #include "tmap.cuh"
 
@@ -47,25 +57,34 @@ namespace {
 
 constexpr int FB_M = 128;  // keys per CTA
 constexpr int FB_N = 128;  // queries per inner block
-constexpr int FB_D = 64;
-constexpr int FB_NS = 3;   // Q/dO ring stages
 constexpr int FB_CW = 8;   // softmax-gradient warps (4..11)
 constexpr int FB_DW = 4;   // dQ drain warps (12..15), one per TMEM lane quadrant
 constexpr int FB_THREADS = 128 + 32 * (FB_CW + FB_DW);
 constexpr int64_t kConvParts = 64;  // row parts of the dQ convert / Q-bias column sums
 
+template <int D>
 struct FbSmem {
-  static constexpr int TILE = 128 * 128;                     // 128 rows x 64 bf16 (SW128)
+  static constexpr bool WIDE = D == 96;
+  static constexpr int NS = WIDE ? 2 : 3;                    // Q/dO ring stages
+  static constexpr int C0 = 128 * 128;                       // 128 rows x 64 bf16 (SW128)
+  static constexpr int C1 = WIDE ? 128 * 64 : 0;             // 128 rows x 32 bf16 (SW64)
+  static constexpr int TILE = C0 + C1;                       // one 128-row operand
   static constexpr int K_OFF = 0;
   static constexpr int V_OFF = K_OFF + TILE;
   static constexpr int Q_OFF = V_OFF + TILE;                 // [NS] {Q, dO}, stride 2*TILE
-  static constexpr int DST_OFF = Q_OFF + FB_NS * 2 * TILE;   // dS^T [2 buffers][2 chunks]
-  static constexpr int STG_OFF = DST_OFF + 2 * 2 * TILE;     // dQ staging: 4 warps x 4 KB
-  static constexpr int LV_OFF = STG_OFF + FB_DW * 4096;      // lse/delta [NS][2][128] f32
-  static constexpr int BAR_OFF = LV_OFF + FB_NS * 2 * FB_N * 4;
+  static constexpr int DST_OFF = Q_OFF + NS * 2 * TILE;      // dS^T [2 buffers][2 chunks C0]
+  static constexpr int STG_ROWS = WIDE ? 16 : 32;            // dQ staging rows per TMA reduce
+  static constexpr int STG = STG_ROWS * 128;                 // per drain warp
+  static constexpr int STG_OFF = DST_OFF + 2 * 2 * C0;
+  static constexpr int LV_OFF = STG_OFF + FB_DW * STG;       // lse/delta [NS][2][128] f32
+  static constexpr int BAR_OFF = LV_OFF + NS * 2 * FB_N * 4;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+  // TMEM: S^T 0, dP^T 128, dV 256, dK 256+D, P^T (bf16x2) 448; dQ at 384
+  // (head_dim 64) or in S^T's columns (96)
+  static constexpr int T_DV = 256, T_DK = 256 + D, T_P = 448, T_DQ = WIDE ? 0 : 384;
+  static_assert(T_DK + D <= T_P, "attention bwd TMEM budget");
 };
-static_assert(FbSmem::TOTAL <= 232448, "attention bwd smem");
+static_assert(FbSmem<64>::TOTAL <= 232448 && FbSmem<96>::TOTAL <= 232448, "attention bwd smem");
 
 // Sum of v[0..31] over the 32 lanes, lane l ending with the total of
 // element l (halving exchanges: 31 shuffles).
@@ -88,21 +107,26 @@ __device__ __forceinline__ float warp_colsum32(const float (&v)[32], uint32_t la
 }
 
 
-// TMEM columns (512, one CTA per SM):
+// TMEM columns (512, one CTA per SM), head_dim 64:
 //   [0,128) S^T   [128,256) dP^T   [256,320) dV   [320,384) dK   [384,448) dQ
 //   [448,512) P^T as packed bf16x2 (A operand of the dV MMA)
+// head_dim 96: dV [256,352), dK [352,448), P^T [448,512), dQ_i in [0,96)
+// between the loads of S^T_{i+1} and the MMA of S^T_{i+2}.
 // DROP (K7 attention dropout, mask as the forward's): the dV MMA consumes the
 // dropped P^T (the 1/(1-p) scale applied to dV at the end), dS^T = P^T *
 // (mask * dP^T / (1-p) - delta).
-template <bool CAUSAL, bool DROP>
+template <int D, bool CAUSAL, bool DROP>
 __global__ void __launch_bounds__(FB_THREADS, 1)
     attn_bwd_fused(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
+                   const __grid_constant__ CUtensorMap tmQKV1,
+                   const __grid_constant__ CUtensorMap tmDO1,
                    const __grid_constant__ CUtensorMap tmDQ, const float* __restrict__ lse,
                    const float* __restrict__ delta, __nv_bfloat16* __restrict__ dqkv, int S, int H,
                    int BH, int bh_chunk, float scale_log2, float scale,
                    float* __restrict__ dq_acc, float* __restrict__ kv_part, AttnDrop drop) {
-  using L = FbSmem;
-  constexpr int D = FB_D;
+  using L = FbSmem<D>;
+  constexpr bool WIDE = L::WIDE;
+  constexpr int FB_NS = L::NS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -128,11 +152,15 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
   // B*H = 512 the kernel read 3.8x its algorithmic bytes from DRAM (chunks
   // of 128: -5% time at B*H = 512, unchanged at 128).
   const int n_kbt = (S + FB_M - 1) / FB_M;
-  const int chunk = static_cast<int>(blockIdx.x) / (bh_chunk * n_kbt);
-  const int within = static_cast<int>(blockIdx.x) % (bh_chunk * n_kbt);
-  const int csz = min(bh_chunk, BH - chunk * bh_chunk);
-  const int kb = within / csz;
-  const int bh = chunk * bh_chunk + within % csz;
+  auto decode = [&](int cta, int& kb_, int& bh_) {
+    const int chunk = cta / (bh_chunk * n_kbt);
+    const int within = cta % (bh_chunk * n_kbt);
+    const int csz = min(bh_chunk, BH - chunk * bh_chunk);
+    kb_ = within / csz;
+    bh_ = chunk * bh_chunk + within % csz;
+  };
+  int kb, bh;
+  decode(static_cast<int>(blockIdx.x), kb, bh);
   const int b = bh / H, h = bh % H;
   const int k0 = kb * FB_M;
   const int n_qb = (S + FB_N - 1) / FB_N;
@@ -147,6 +175,10 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmQKV);
     tma_prefetch(&tmDO);
+    if constexpr (WIDE) {
+      tma_prefetch(&tmQKV1);
+      tma_prefetch(&tmDO1);
+    }
     tma_prefetch(&tmDQ);
     mbar_init(kv_full, 1);
     for (int i = 0; i < FB_NS; ++i) {
@@ -170,15 +202,22 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS = tmem, tdP = tmem + 128, tDV = tmem + 256, tDK = tmem + 320,
-                 tDQ = tmem + 384, tP = tmem + 448;
+  const uint32_t tS = tmem, tdP = tmem + 128, tDV = tmem + L::T_DV, tDK = tmem + L::T_DK,
+                 tDQ = tmem + L::T_DQ, tP = tmem + L::T_P;
+  // one 128-row operand tile: d 0..63 (SW128) and, head_dim 96, d 64..95
+  // (SW64) C0 bytes further
+  auto load_tile = [&](uint8_t* dst, const CUtensorMap* m0, const CUtensorMap* m1,
+                       uint64_t* bar, int col, int row) {
+    tma_load_3d(dst, m0, bar, col, row, b);
+    if constexpr (WIDE) tma_load_3d(dst + L::C0, m1, bar, col + 64, row, b);
+  };
 
   if (warp == 0) {
     // ===== producer =====
     if (lane == 0) {
       mbar_expect_tx(kv_full, 2 * L::TILE);
-      tma_load_3d(smem + L::K_OFF, &tmQKV, kv_full, Hd + h * D, k0, b);
-      tma_load_3d(smem + L::V_OFF, &tmQKV, kv_full, 2 * Hd + h * D, k0, b);
+      load_tile(smem + L::K_OFF, &tmQKV, &tmQKV1, kv_full, Hd + h * D, k0);
+      load_tile(smem + L::V_OFF, &tmQKV, &tmQKV1, kv_full, 2 * Hd + h * D, k0);
     }
     for (int it = 0; it < n_it; ++it) {
       const int st = it % FB_NS;
@@ -191,8 +230,8 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
       if (lane == 0) {
         mbar_wait(&q_empty[st], ph ^ 1);
         mbar_expect_tx(&q_full[st], 2 * L::TILE + (full_blk ? 2 * FB_N * 4 : 0));
-        tma_load_3d(sq, &tmQKV, &q_full[st], h * D, qi, b);
-        tma_load_3d(sq + L::TILE, &tmDO, &q_full[st], h * D, qi, b);
+        load_tile(sq, &tmQKV, &tmQKV1, &q_full[st], h * D, qi);
+        load_tile(sq + L::TILE, &tmDO, &tmDO1, &q_full[st], h * D, qi);
         if (full_blk) {
           bulk_g2s(dst, lse_bh + qi, FB_N * 4, &q_full[st]);
           bulk_g2s(dst + FB_N, del_bh + qi, FB_N * 4, &q_full[st]);
@@ -215,40 +254,70 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
     if (lane == 0) {
       // ===== MMA issuer =====
       constexpr uint32_t idST = idesc_bf16(128, FB_N, false, false);
-      constexpr uint32_t idG = idesc_bf16(128, D, false, true);
-      constexpr uint32_t idQ = idesc_bf16(128, D, true, true);
+      constexpr uint32_t idG = idesc_bf16(128, 64, false, true);
+      constexpr uint32_t idG1 = idesc_bf16(128, 32, false, true);
+      constexpr uint32_t idQ = idesc_bf16(128, 64, true, true);
+      constexpr uint32_t idQ1 = idesc_bf16(128, 32, true, true);
       const uint32_t sK = smem_u32(smem + L::K_OFF), sV = smem_u32(smem + L::V_OFF);
+      // K-major operand (rows = keys or queries, K = d): k-th 16-wide d step
+      auto kdesc = [](uint32_t base, int k) {
+        return k < 4 ? sdesc_sw128(base + k * 32, 16, 1024)
+                     : sdesc_sw64(base + L::C0 + (k - 4) * 32, 16, 512);
+      };
+      // MN-major operand with N = d (Q, dO, K as B of dK, dV, dQ): rows
+      // 16k..16k+15 of the d 0..63 chunk, or of the d 64..95 chunk
+      auto ndesc0 = [](uint32_t base, int k) { return sdesc_sw128(base + k * 2048, L::C0, 1024); };
+      auto ndesc1 = [](uint32_t base, int k) {
+        return sdesc_sw64(base + L::C0 + k * 1024, L::C1, 512);
+      };
       mbar_wait(kv_full, 0);
       auto issue_grad = [&](int j) {
         const int qs = j % FB_NS;
         const uint32_t sQ = smem_u32(smem + L::Q_OFF + qs * 2 * L::TILE);
         const uint32_t sdO = sQ + L::TILE;
-        const uint32_t sdSt = smem_u32(smem + L::DST_OFF + (j & 1) * 2 * L::TILE);
+        const uint32_t sdSt = smem_u32(smem + L::DST_OFF + (j & 1) * 2 * L::C0);
         mbar_wait(p_full, j & 1);
         TRJ(j, 10);
         tc_fence_after();
         // dV += P^T dO (A = P^T from TMEM)
 #pragma unroll
         for (int k = 0; k < FB_N / 16; ++k)
-          umma_f16_ts(tDV, tP + k * 8, sdesc_sw128(sdO + k * 2048, L::TILE, 1024), idG,
-                      (j > 0 || k > 0) ? 1u : 0u);
+          umma_f16_ts(tDV, tP + k * 8, ndesc0(sdO, k), idG, (j > 0 || k > 0) ? 1u : 0u);
+        if constexpr (WIDE) {
+#pragma unroll
+          for (int k = 0; k < FB_N / 16; ++k)
+            umma_f16_ts(tDV + 64, tP + k * 8, ndesc1(sdO, k), idG1, (j > 0 || k > 0) ? 1u : 0u);
+        }
         umma_commit(pt_empty);
         // dK += dS^T Q
 #pragma unroll
         for (int k = 0; k < FB_N / 16; ++k) {
-          const uint32_t koff = (k >> 2) * L::TILE + (k & 3) * 32;
-          umma_f16(tDK, sdesc_sw128(sdSt + koff, 16, 1024), sdesc_sw128(sQ + k * 2048, L::TILE, 1024),
-                   idG, (j > 0 || k > 0) ? 1u : 0u);
+          const uint32_t koff = (k >> 2) * L::C0 + (k & 3) * 32;
+          umma_f16(tDK, sdesc_sw128(sdSt + koff, 16, 1024), ndesc0(sQ, k), idG,
+                   (j > 0 || k > 0) ? 1u : 0u);
+          if constexpr (WIDE)
+            umma_f16(tDK + 64, sdesc_sw128(sdSt + koff, 16, 1024), ndesc1(sQ, k), idG1,
+                     (j > 0 || k > 0) ? 1u : 0u);
         }
         umma_commit(&q_empty[qs]);  // Q_j, dO_j no longer needed
-        // dQ_j = dS K once the drain warps emptied dQ_{j-1}
-        mbar_wait(dq_empty, (j & 1) ^ 1);
+        if constexpr (!WIDE) {
+          // dQ_j = dS K once the drain warps emptied dQ_{j-1}
+          mbar_wait(dq_empty, (j & 1) ^ 1);
+        } else if (j + 1 < n_it) {
+          // dQ_j into S^T's columns once S^T_{j+1} / dP^T_{j+1} are loaded
+          mbar_wait(&st_empty[0], (j + 1) & 1);
+          mbar_wait(&st_empty[1], (j + 1) & 1);
+        }
         TRJ(j, 11);
         tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < FB_M / 16; ++k)
-          umma_f16(tDQ, sdesc_sw128(sdSt + k * 2048, L::TILE, 1024),
-                   sdesc_sw128(sK + k * 2048, L::TILE, 1024), idQ, k > 0 ? 1u : 0u);
+        for (int k = 0; k < FB_M / 16; ++k) {
+          umma_f16(tDQ, sdesc_sw128(sdSt + k * 2048, L::C0, 1024), ndesc0(sK, k), idQ,
+                   k > 0 ? 1u : 0u);
+          if constexpr (WIDE)
+            umma_f16(tDQ + 64, sdesc_sw128(sdSt + k * 2048, L::C0, 1024), ndesc1(sK, k), idQ1,
+                     k > 0 ? 1u : 0u);
+        }
         umma_commit(dq_full);
         umma_commit(&ds_empty[j & 1]);
         TRJ(j, 12);
@@ -263,14 +332,14 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
         // warp has loaded its half-0 columns of the previous block
         mbar_wait(&st_empty[0], (it & 1) ^ 1);
         mbar_wait(&st_empty[1], (it & 1) ^ 1);
+        // head_dim 96: dQ_{it-2} (in S^T's columns) drained
+        if (WIDE && it >= 2) mbar_wait(dq_empty, it & 1);
         TR(9);
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
-          umma_f16(tS, sdesc_sw128(sK + k * 32, 16, 1024), sdesc_sw128(sQ + k * 32, 16, 1024),
-                   idST, k > 0);
-          umma_f16(tdP, sdesc_sw128(sV + k * 32, 16, 1024), sdesc_sw128(sdO + k * 32, 16, 1024),
-                   idST, k > 0);
+          umma_f16(tS, kdesc(sK, k), kdesc(sQ, k), idST, k > 0);
+          umma_f16(tdP, kdesc(sV, k), kdesc(sdO, k), idST, k > 0);
         }
         umma_commit(&st_full[0]);
         umma_commit(&st_full[1]);
@@ -376,7 +445,7 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
       const int qi = (i0 + it) * FB_N;
       const bool need_mask = (qi + FB_N > S) || (CAUSAL && qi < k0 + FB_M - 1);
       const int qlo = CAUSAL ? key : 0;
-      const uint32_t dsb = rowG + (it & 1) * 2 * L::TILE;
+      const uint32_t dsb = rowG + (it & 1) * 2 * L::C0;
       // dropout keep bits of this block's two 32-query column groups (one
       // global word each), requested before any wait so their latency hides
       uint32_t mwords[2] = {0u, 0u};
@@ -423,7 +492,7 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
         tmem_st16(tP + trow + (c >> 1), pp);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          sts128(dsb + cc * L::TILE + (((chalf * 4 + k) ^ (r & 7)) << 4),
+          sts128(dsb + cc * L::C0 + (((chalf * 4 + k) ^ (r & 7)) << 4),
                  make_uint4(pg[4 * k], pg[4 * k + 1], pg[4 * k + 2], pg[4 * k + 3]));
       }
       tmem_st_wait();
@@ -436,21 +505,34 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
     mbar_wait(acc_full, 0);
     tc_fence_after();
     {
-      const int c = chalf * 32;
+      // the two warps of a lane quadrant take D/2 columns each (32 | 48)
+      constexpr int DC = D / 2;
+      const int c = chalf * DC;
       uint32_t rk[32], rv[32];
+      float fk[48], fv[48];
       tmem_ld32(tDK + trow + c, rk);
       tmem_ld32(tDV + trow + c, rv);
       tmem_ld_wait();
-      float fk[32], fv[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         fk[i] = key < S ? __uint_as_float(rk[i]) * scale : 0.f;
         fv[i] = key < S ? __uint_as_float(rv[i]) * (DROP ? drop.scale : 1.f) : 0.f;
       }
+      if constexpr (DC > 32) {
+        uint32_t rk2[16], rv2[16];
+        tmem_ld16(tDK + trow + c + 32, rk2);
+        tmem_ld16(tDV + trow + c + 32, rv2);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          fk[32 + i] = key < S ? __uint_as_float(rk2[i]) * scale : 0.f;
+          fv[32 + i] = key < S ? __uint_as_float(rv2[i]) * (DROP ? drop.scale : 1.f) : 0.f;
+        }
+      }
       if (key < S) {
         __nv_bfloat16* row = dqkv + (static_cast<int64_t>(b) * S + key) * (3 * Hd) + h * D + c;
 #pragma unroll
-        for (int i = 0; i < 32; i += 8) {
+        for (int i = 0; i < DC; i += 8) {
           *reinterpret_cast<uint4*>(row + Hd + i) = pack8(*reinterpret_cast<float(*)[8]>(fk + i));
           *reinterpret_cast<uint4*>(row + 2 * Hd + i) = pack8(*reinterpret_cast<float(*)[8]>(fv + i));
         }
@@ -458,47 +540,71 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
       if (kv_part != nullptr) {
         // K/V bias gradient: this warp's 32 keys summed per column (lane l
         // ends with column c + l) -> kv_part[(b, kb, quadrant)][K | V column]
-        const float sk = warp_colsum32(fk, lane), sv = warp_colsum32(fv, lane);
         float* dst = kv_part + ((static_cast<int64_t>(b) * gridDim.x / BH + kb) * 4 + qd) * (2 * Hd);
+        const float sk = warp_colsum32(*reinterpret_cast<float(*)[32]>(fk), lane);
+        const float sv = warp_colsum32(*reinterpret_cast<float(*)[32]>(fv), lane);
         dst[h * D + c + lane] = sk;
         dst[Hd + h * D + c + lane] = sv;
+        if constexpr (DC > 32) {
+          float tk[32], tv[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            tk[i] = i < 16 ? fk[32 + i] : 0.f;
+            tv[i] = i < 16 ? fv[32 + i] : 0.f;
+          }
+          const float sk2 = warp_colsum32(tk, lane), sv2 = warp_colsum32(tv, lane);
+          if (lane < 16) {
+            dst[h * D + c + 32 + lane] = sk2;
+            dst[Hd + h * D + c + 32 + lane] = sv2;
+          }
+        }
       }
     }
   } else if (warp >= 4 + FB_CW) {
     // ===== dQ drain: TMEM -> smem (fp32, SW128) -> TMA reduce-add =====
     const uint32_t qd = warp & 3;
     const uint32_t trow = (qd * 32) << 16;
-    uint8_t* stg = smem + L::STG_OFF + qd * 4096;
-    for (int j = 0; j < n_it; ++j) {
-      mbar_wait(dq_full, j & 1);
-      if (warp == 4 + FB_CW && lane == 0) TRJ(j, 13);
-      tc_fence_after();
-      uint32_t v0[32], v1[32];
-      tmem_ld32(tDQ + trow, v0);
-      tmem_ld32(tDQ + trow + 32, v1);
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(dq_empty);
-      const int q = (i0 + j) * FB_N + qd * 32;
-      const uint32_t s0 = smem_u32(stg + lane * 128);
+    uint8_t* stg = smem + L::STG_OFF + qd * L::STG;
+    // 32 fp32 columns of this warp's 32 query rows into dQacc (column col),
+    // L::STG_ROWS rows per TMA reduce through the staging tile
+    auto reduce32 = [&](const uint32_t (&v)[32], int col, int q) {
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {
+      for (int part = 0; part < 32 / L::STG_ROWS; ++part) {
         if (lane == 0) bulk_wait_read<0>();  // previous reduce has read the staging tile
         __syncwarp();
+        if (static_cast<int>(lane) / L::STG_ROWS == part) {
+          const int rr = static_cast<int>(lane) % L::STG_ROWS;
+          const uint32_t s0 = smem_u32(stg + rr * 128);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t* v = half ? v1 : v0;
-          sts128(s0 + ((k ^ (lane & 7)) << 4),
-                 make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]));
+          for (int k = 0; k < 8; ++k)
+            sts128(s0 + ((k ^ (rr & 7)) << 4),
+                   make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]));
         }
         fence_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_reduce_add_3d(&tmDQ, stg, h * D + half * 32, q, b);
+          tma_reduce_add_3d(&tmDQ, stg, col, q + part * L::STG_ROWS, b);
           bulk_commit();
         }
       }
+    };
+    for (int j = 0; j < n_it; ++j) {
+      const int q = (i0 + j) * FB_N + qd * 32;
+      uint32_t v0[32], v1[32];
+      mbar_wait(dq_full, j & 1);
+      if (warp == 4 + FB_CW && lane == 0) TRJ(j, 13);
+      tc_fence_after();
+      uint32_t v2[WIDE ? 32 : 1];
+      tmem_ld32(tDQ + trow, v0);
+      tmem_ld32(tDQ + trow + 32, v1);
+      if constexpr (WIDE) tmem_ld32(tDQ + trow + 64, v2);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dq_empty);
+      reduce32(v0, h * D, q);
+      reduce32(v1, h * D + 32, q);
+      if constexpr (WIDE) reduce32(v2, h * D + 64, q);
     }
     if (lane == 0) bulk_wait_all();
     __syncwarp();
@@ -512,12 +618,14 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
 }
 
 // delta[b,h,s] = sum_d O * dO (fp32) and dQacc[t, :] = 0, one (token, head)
-// row per 8-lane group.
+// row per G-lane group (8 lanes x 8 elements at head_dim 64, 4 x 24 at 96).
+template <int D>
 __global__ void __launch_bounds__(256) attn_delta_zero_kernel(
     const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
     float* __restrict__ delta, float* __restrict__ dq_acc, int64_t tokens, int S, int H,
     unsigned* __restrict__ counters) {
-  constexpr int G = FB_D / 8;
+  constexpr int G = D == 96 ? 4 : D / 8;
+  constexpr int E = D / G;
   if (blockIdx.x == 0 && threadIdx.x < 64) counters[threadIdx.x] = 0u;
   const int lane = threadIdx.x & 31;
   const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / G;
@@ -525,15 +633,18 @@ __global__ void __launch_bounds__(256) attn_delta_zero_kernel(
   float acc = 0.f;
   const bool ok = row < tokens * H;
   if (ok) {
-    const int64_t off = row * FB_D + li * 8;
-    float a[8], g[8];
-    unpack8(*reinterpret_cast<const uint4*>(o + off), a);
-    unpack8(*reinterpret_cast<const uint4*>(dout + off), g);
+    const int64_t off = row * D + li * E;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc += a[j] * g[j];
-    float4* z = reinterpret_cast<float4*>(dq_acc + off);
-    z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-    z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int e = 0; e < E; e += 8) {
+      float a[8], g[8];
+      unpack8(*reinterpret_cast<const uint4*>(o + off + e), a);
+      unpack8(*reinterpret_cast<const uint4*>(dout + off + e), g);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc += a[j] * g[j];
+      float4* z = reinterpret_cast<float4*>(dq_acc + off + e);
+      z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+      z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
   }
 #pragma unroll
   for (int m = G / 2; m > 0; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
@@ -669,24 +780,26 @@ __global__ void __launch_bounds__(1024) kv_bias_reduce(const float* __restrict__
   }
 }
 
-template <bool CAUSAL, bool DROP>
+template <int D, bool CAUSAL, bool DROP>
 int fused_t(const void* qkv, const void* o, const void* dout, const float* lse, float* delta,
             float* dq_acc, void* dqkv, int64_t B, int64_t S, int64_t H, float* dbias,
             float* part_ws, unsigned* counters, float* kv_part, const AttnDrop& drop,
             cudaStream_t st) {
-  using L = FbSmem;
-  constexpr int D = FB_D;
+  using L = FbSmem<D>;
   const int64_t tokens = B * S;
   const int Hd = static_cast<int>(H * D);
-  CUtensorMap tq, tdo, tdq;
+  CUtensorMap tq, tdo, tq1, tdo1, tdq;
   if (!make_tmap_bsc(&tq, qkv, 3 * H * D, S, B, 128) ||
       !make_tmap_bsc(&tdo, dout, H * D, S, B, 128) ||
-      !make_tmap_bsc_f32(&tdq, dq_acc, H * D, S, B, 32))
+      !make_tmap_bsc(&tq1, qkv, 3 * H * D, S, B, 128, true) ||
+      !make_tmap_bsc(&tdo1, dout, H * D, S, B, 128, true) ||
+      !make_tmap_bsc_f32(&tdq, dq_acc, H * D, S, B, L::STG_ROWS))
     return VP_ERR_UNSUPPORTED;
-  auto k = attn_bwd_fused<CAUSAL, DROP>;
+  auto k = attn_bwd_fused<D, CAUSAL, DROP>;
   if (cudaError_t e = smem_optin(k, L::TOTAL); e != cudaSuccess) return e;
   const int64_t rows = tokens * H;
-  attn_delta_zero_kernel<<<static_cast<unsigned>((rows * (D / 8) + 255) / 256), 256, 0, st>>>(
+  constexpr int G = D == 96 ? 4 : D / 8;
+  attn_delta_zero_kernel<D><<<static_cast<unsigned>((rows * G + 255) / 256), 256, 0, st>>>(
       reinterpret_cast<const __nv_bfloat16*>(o), reinterpret_cast<const __nv_bfloat16*>(dout),
       delta, dq_acc, tokens, static_cast<int>(S), static_cast<int>(H), counters);
   const float scale = 1.f / sqrtf(static_cast<float>(D));
@@ -696,8 +809,9 @@ int fused_t(const void* qkv, const void* o, const void* dout, const float* lse, 
   static const int env_chunk = getenv("VP_ATTN_BH_CHUNK") ? atoi(getenv("VP_ATTN_BH_CHUNK")) : 0;
   const int bh_chunk = std::max(1, std::min(BH, env_chunk > 0 ? env_chunk : 128));
   k<<<static_cast<unsigned>(n_kb * BH), FB_THREADS, L::TOTAL, st>>>(
-      tq, tdo, tdq, lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), static_cast<int>(S),
-      static_cast<int>(H), BH, bh_chunk, scale_log2, scale, dq_acc, dbias ? kv_part : nullptr,
+      tq, tdo, tq1, tdo1, tdq, lse, delta, reinterpret_cast<__nv_bfloat16*>(dqkv), static_cast<int>(S),
+      static_cast<int>(H), BH, bh_chunk, scale_log2, scale, dq_acc,
+      dbias ? kv_part : nullptr,
       drop);
   if (!dbias) {
     dq_convert_kernel<<<static_cast<unsigned>((tokens * Hd / 8 + 255) / 256), 256, 0, st>>>(
@@ -729,20 +843,25 @@ int64_t attention_bwd_fused_ws(int64_t B, int64_t S, int64_t H, int64_t D) {
          B * n_kb * 4 * 2 * H * D;
 }
 
-bool attention_bwd_fused_ok(int64_t D) { return D == FB_D; }
+bool attention_bwd_fused_ok(int64_t D) { return D == 64 || D == 96; }
 
 int attention_bwd_fused(const void* qkv, const void* o, const void* dout, const float* lse,
-                        void* dqkv, float* ws, int64_t B, int64_t S, int64_t H, int causal,
-                        float* dbias, const AttnDrop& drop, cudaStream_t st) {
+                        void* dqkv, float* ws, int64_t B, int64_t S, int64_t H, int64_t D,
+                        int causal, float* dbias, const AttnDrop& drop, cudaStream_t st) {
   float* delta = ws;
   float* dq_acc = delta + al4(B * H * S);
-  float* part_ws = dq_acc + al4(B * S * H * FB_D);
-  unsigned* counters = reinterpret_cast<unsigned*>(part_ws + al4(kConvParts * H * FB_D));
+  float* part_ws = dq_acc + al4(B * S * H * D);
+  unsigned* counters = reinterpret_cast<unsigned*>(part_ws + al4(kConvParts * H * D));
   float* kv_part = reinterpret_cast<float*>(counters) + 64;
-#define FT(C, DR) fused_t<C, DR>(qkv, o, dout, lse, delta, dq_acc, dqkv, B, S, H, dbias, part_ws, \
-                                 counters, kv_part, drop, st)
-  if (drop.seed) return causal ? FT(true, true) : FT(false, true);
-  return causal ? FT(true, false) : FT(false, false);
+#define FT(DD, C, DR) fused_t<DD, C, DR>(qkv, o, dout, lse, delta, dq_acc, dqkv, B, S, H, dbias, \
+                                         part_ws, counters, kv_part, drop, st)
+  if (D == 96) {
+    if (drop.seed) return causal ? FT(96, true, true) : FT(96, false, true);
+    return causal ? FT(96, true, false) : FT(96, false, false);
+  }
+  if (D != 64) return VP_ERR_UNSUPPORTED;
+  if (drop.seed) return causal ? FT(64, true, true) : FT(64, false, true);
+  return causal ? FT(64, true, false) : FT(64, false, false);
 #undef FT
 }
 

@@ -215,6 +215,13 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo, ui
   return d;
 }
 
+// The same with SWIZZLE_64B (rows of 64 B = 32 bf16; 8-row atoms 512 B
+// apart): the 32-wide tail chunk of a head_dim-96 tile.
+__device__ __forceinline__ uint64_t sdesc_sw64(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (sdesc_sw128(saddr, lbo, sbo) & ~(static_cast<uint64_t>(7) << 61)) |
+         (static_cast<uint64_t>(4) << 61);
+}
+
 // Instruction descriptor, kind::f16: bf16 A/B, fp32 D.
 __host__ __device__ constexpr uint32_t idesc_bf16(uint32_t M, uint32_t N, bool a_mn_major,
                                                   bool b_mn_major) {

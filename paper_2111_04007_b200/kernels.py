@@ -240,9 +240,9 @@ def attention_bwd(qkv, out, dout, lse, dqkv, ws, batch, seq, heads, head_dim, ca
                   stream=None, deterministic=False, dbias=None, p=0.0, seed=None, salt=0,
                   mask_q=None, mask_k=None):
     """dqkv = d(qkv). ``ws``: fp32 workspace of attention_bwd_ws_elems()
-    elements. head_dim 64 runs the fused one-pass kernel (dQ accumulated by
-    TMA reduce-add); ``deterministic`` (or other head dims) the two-kernel
-    path. ``dbias`` (fp32 [3*heads*head_dim]) += column sums of dqkv, fused
+    elements. head_dim 64 and 96 run the fused one-pass kernel (dQ
+    accumulated by TMA reduce-add); ``deterministic`` (or other head dims)
+    the two-kernel path. ``dbias`` (fp32 [3*heads*head_dim]) += column sums of dqkv, fused
     on the one-pass path; returns False when the caller must sum itself."""
     need = attention_bwd_ws_elems(batch, seq, heads, head_dim)
     if ws.numel() < need or ws.dtype != torch.float32:

@@ -12,7 +12,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2111_04007_b200 import kernels as K  # noqa: E402
 
-B, S, H, D = 32, 1024, 16, 64
+B, S, H, D = (int(x) for x in sys.argv[1:5]) if len(sys.argv) >= 5 else (32, 1024, 16, 64)
 qkv = torch.randn(B * S, 3 * H * D, device="cuda").bfloat16()
 o = torch.empty(B * S, H * D, device="cuda", dtype=torch.bfloat16)
 lse = torch.empty(B * H * S, device="cuda")

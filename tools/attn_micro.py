@@ -56,6 +56,11 @@ def run(B, S, H, D, causal):
                     f"bwd_tflops{tag}": round(2.5 * f / ms_b / 1e9, 1)})
         if p > 0:
             out["mask_us_p0.1"] = round(ms_m * 1e3, 1)
+        elif "det" in sys.argv:
+            ms_d = t(lambda: K.attention_bwd(qkv, o, do, lse, dqkv, ws, B, S, H, D, causal,
+                                             deterministic=True))
+            out["bwd_two_kernel_us"] = round(ms_d * 1e3, 1)
+            out["bwd_two_kernel_tflops"] = round(2.5 * f / ms_d / 1e9, 1)
     if "sdpa" in sys.argv:
         import torch.nn.functional as F
         from torch.nn.attention import SDPBackend, sdpa_kernel
@@ -76,8 +81,9 @@ def run(B, S, H, D, causal):
     print(json.dumps(out), flush=True)
 
 
-args = [a for a in sys.argv[1:] if a != "sdpa"]
+args = [a for a in sys.argv[1:] if a not in ("sdpa", "det")]
 cases = [(32, 1024, 16, 64, True), (8, 1024, 16, 64, True), (4, 1024, 20, 96, True),
+         (4, 1024, 32, 96, True), (16, 1024, 20, 96, True),
          (64, 512, 16, 64, False)]
 if len(args) >= 5:
     cases = [tuple(int(x) for x in args[:4]) + (args[4] in ("1", "True", "true"),)]
