@@ -33,6 +33,9 @@ constexpr int TA_THREADS = 256;
 // warp issues S_{j+2} right after the softmax warps load S_j, so block
 // j+2's K/V must already be resident then.
 __host__ __device__ constexpr int ta_stages(int D) { return D == 64 ? 5 : 3; }
+// head_dim 96 tiles are stored compact — a 64-wide SWIZZLE_128B chunk and a
+// 32-wide SWIZZLE_64B chunk — so Q + 3 K/V stages take 99 KB and two CTAs
+// fit on an SM (padded to 128 columns it was one CTA per SM).
 
 template <int D>
 struct TaSmem {
@@ -47,10 +50,11 @@ struct TaSmem {
   static constexpr int TP = 128 + D + (QT ? D / 2 : 0);  // TMEM column of P
   static_assert(TP + (PT ? 32 : 0) <= 256, "attention fwd TMEM budget");
   static constexpr int CH = (D + 63) / 64;           // 64-wide d-chunks (128 B rows)
+  static constexpr bool NARROW = D == 96;            // d 64..95 as a 32-wide SW64 chunk
   static constexpr int QCH = 128 * 128;              // one Q d-chunk: 128 rows x 128 B
   static constexpr int KCH = TA_BN * 128;            // one K/V d-chunk: 64 rows x 128 B
-  static constexpr int QTILE = QCH * CH;
-  static constexpr int KTILE = KCH * CH;
+  static constexpr int QTILE = NARROW ? QCH + 128 * 64 : QCH * CH;
+  static constexpr int KTILE = NARROW ? KCH + TA_BN * 64 : KCH * CH;
   static constexpr int Q_OFF = 0;
   static constexpr int K_OFF = QTILE;                // [stage]
   static constexpr int STAGES = ta_stages(D);
@@ -80,7 +84,8 @@ __device__ unsigned long long g_vp_ftrace[4][32][8];
 template <int D, bool CAUSAL, bool DROP, int SW = 4>
 __global__ void __launch_bounds__(128 + 32 * SW, 2)
     attn_fwd_tc(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmKV,
-                __nv_bfloat16* __restrict__ out,
+                const __grid_constant__ CUtensorMap tmQKV1,
+                const __grid_constant__ CUtensorMap tmKV1, __nv_bfloat16* __restrict__ out,
                 float* __restrict__ lse, int S, int H, int n_qb, float scale_log2, AttnDrop drop) {
   static_assert(SW == 4 || (SW == 8 && D == 64), "split softmax: head_dim 64 only");
   constexpr int NK = TA_BN * 4 / SW;      // keys per softmax thread per block
@@ -112,6 +117,10 @@ __global__ void __launch_bounds__(128 + 32 * SW, 2)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmQKV);
     tma_prefetch(&tmKV);
+    if constexpr (L::NARROW) {
+      tma_prefetch(&tmQKV1);
+      tma_prefetch(&tmKV1);
+    }
     mbar_init(q_full, 1);
     for (int i = 0; i < L::STAGES; ++i) {
       mbar_init(&kv_full[i], 1);
@@ -139,17 +148,22 @@ __global__ void __launch_bounds__(128 + 32 * SW, 2)
       // ===== producer =====
       mbar_expect_tx(q_full, L::QTILE);
 #pragma unroll
-      for (int c = 0; c < L::CH; ++c)
-        tma_load_3d(smem + L::Q_OFF + c * L::QCH, &tmQKV, q_full, h * D + c * 64, q0, b);
+      for (int c = 0; c < L::CH; ++c) {
+        if (L::NARROW && c == 1)
+          tma_load_3d(smem + L::Q_OFF + L::QCH, &tmQKV1, q_full, h * D + 64, q0, b);
+        else
+          tma_load_3d(smem + L::Q_OFF + c * L::QCH, &tmQKV, q_full, h * D + c * 64, q0, b);
+      }
       for (int j = 0; j < n_kb; ++j) {
         const int st = j % L::STAGES;
         mbar_wait(&kv_empty[st], ((j / L::STAGES) & 1) ^ 1);
         mbar_expect_tx(&kv_full[st], 2 * L::KTILE);
 #pragma unroll
         for (int c = 0; c < L::CH; ++c) {
-          tma_load_3d(smem + L::K_OFF + st * L::KTILE + c * L::KCH, &tmKV, &kv_full[st],
+          const CUtensorMap* m = (L::NARROW && c == 1) ? &tmKV1 : &tmKV;
+          tma_load_3d(smem + L::K_OFF + st * L::KTILE + c * L::KCH, m, &kv_full[st],
                       Hd + h * D + c * 64, j * TA_BN, b);
-          tma_load_3d(smem + L::V_OFF + st * L::KTILE + c * L::KCH, &tmKV, &kv_full[st],
+          tma_load_3d(smem + L::V_OFF + st * L::KTILE + c * L::KCH, m, &kv_full[st],
                       2 * Hd + h * D + c * 64, j * TA_BN, b);
         }
       }
@@ -158,7 +172,8 @@ __global__ void __launch_bounds__(128 + 32 * SW, 2)
     if (lane == 0) {
       // ===== MMA issuer =====
       constexpr uint32_t idS = idesc_bf16(128, TA_BN, false, false);
-      constexpr uint32_t idO = idesc_bf16(128, D, false, true);
+      constexpr uint32_t idO = idesc_bf16(128, L::NARROW ? 64 : D, false, true);
+      constexpr uint32_t idO1 = idesc_bf16(128, 32, false, true);
       const uint32_t sQ = smem_u32(smem + L::Q_OFF);
       const uint32_t sP = smem_u32(smem + L::P_OFF);
       mbar_wait(q_full, 0);
@@ -174,7 +189,13 @@ __global__ void __launch_bounds__(128 + 32 * SW, 2)
         for (int k = 0; k < TA_BN / 16; ++k) {
           // B = V [key][d] MN-major: +16 rows * 128 B per 16 keys; d-chunks KCH apart
           const uint64_t bd = sdesc_sw128(sV + k * 2048, L::KCH, 1024);
-          if constexpr (L::PT) {
+          if constexpr (L::NARROW) {
+            // d 0..63 and d 64..95 (SW64 rows of 64 B: +1 KB per 16 keys)
+            umma_f16_ts(tmem + 128, tmem + L::TP + k * 8, bd, idO, (j > 0 || k > 0) ? 1u : 0u);
+            umma_f16_ts(tmem + 192, tmem + L::TP + k * 8,
+                        sdesc_sw64(sV + L::KCH + k * 1024, L::KCH, 512), idO1,
+                        (j > 0 || k > 0) ? 1u : 0u);
+          } else if constexpr (L::PT) {
             umma_f16_ts(tmem + 128, tmem + L::TP + k * 8, bd, idO, (j > 0 || k > 0) ? 1u : 0u);
           } else {
             // A = P [q][key] K-major (one 128 B row chunk): +32 B per 16 keys
@@ -194,6 +215,11 @@ __global__ void __launch_bounds__(128 + 32 * SW, 2)
         const uint32_t sK = smem_u32(smem + L::K_OFF + st * L::KTILE);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
+          if (L::NARROW && k >= 4) {
+            umma_f16(tmem + (j & 1) * TA_BN, sdesc_sw64(sQ + L::QCH + (k - 4) * 32, 16, 512),
+                     sdesc_sw64(sK + L::KCH + (k - 4) * 32, 16, 512), idS, 1u);
+            continue;
+          }
           const uint64_t bd = sdesc_sw128(sK + (k >> 2) * L::KCH + (k & 3) * 32, 16, 1024);
           if constexpr (L::QT) {
             umma_f16_ts(tmem + (j & 1) * TA_BN, tmem + L::TQ + k * 8, bd, idS, k > 0);
@@ -1036,9 +1062,11 @@ template <int D, bool CAUSAL, bool DROP>
 int fwd_tc_t(const void* qkv, void* o, float* lse, int64_t B, int64_t S, int64_t H,
              const AttnDrop& drop, cudaStream_t st) {
   using L = TaSmem<D>;
-  CUtensorMap tm, tkv;
+  CUtensorMap tm, tkv, tm1, tkv1;
   if (!make_tmap_bsc(&tm, qkv, 3 * H * D, S, B, 128)) return VP_ERR_UNSUPPORTED;
   if (!make_tmap_bsc(&tkv, qkv, 3 * H * D, S, B, TA_BN)) return VP_ERR_UNSUPPORTED;
+  if (!make_tmap_bsc(&tm1, qkv, 3 * H * D, S, B, 128, true)) return VP_ERR_UNSUPPORTED;
+  if (!make_tmap_bsc(&tkv1, qkv, 3 * H * D, S, B, TA_BN, true)) return VP_ERR_UNSUPPORTED;
   const int n_qb = static_cast<int>((S + TA_BM - 1) / TA_BM);
   dim3 grid(n_qb, static_cast<unsigned>(B * H));
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(D));
@@ -1051,7 +1079,7 @@ int fwd_tc_t(const void* qkv, void* o, float* lse, int64_t B, int64_t S, int64_t
     if (sw8) {
       auto k = attn_fwd_tc<D, CAUSAL, DROP, 8>;
       if (cudaError_t e = smem_optin(k, L::TOTAL); e != cudaSuccess) return e;
-      k<<<grid, 128 + 32 * 8, L::TOTAL, st>>>(tm, tkv, reinterpret_cast<__nv_bfloat16*>(o), lse,
+      k<<<grid, 128 + 32 * 8, L::TOTAL, st>>>(tm, tkv, tm1, tkv1, reinterpret_cast<__nv_bfloat16*>(o), lse,
                                               static_cast<int>(S), static_cast<int>(H), n_qb,
                                               scale_log2, drop);
       return launch_status();
@@ -1059,7 +1087,7 @@ int fwd_tc_t(const void* qkv, void* o, float* lse, int64_t B, int64_t S, int64_t
   }
   auto k = attn_fwd_tc<D, CAUSAL, DROP, 4>;
   if (cudaError_t e = smem_optin(k, L::TOTAL); e != cudaSuccess) return e;
-  k<<<grid, TA_THREADS, L::TOTAL, st>>>(tm, tkv, reinterpret_cast<__nv_bfloat16*>(o), lse,
+  k<<<grid, TA_THREADS, L::TOTAL, st>>>(tm, tkv, tm1, tkv1, reinterpret_cast<__nv_bfloat16*>(o), lse,
                                         static_cast<int>(S), static_cast<int>(H), n_qb,
                                         scale_log2, drop);
   return launch_status();
