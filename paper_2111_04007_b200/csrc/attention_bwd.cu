@@ -377,8 +377,9 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
         const float lq[4] = {l4.x, l4.y, l4.z, l4.w};
         const float dq[4] = {d4.x, d4.y, d4.z, d4.w};
         float p[4], gr[4];
-        if constexpr (!DROP) {
-          // two query columns per FFMA2 / FSUB2 / FMUL2
+        if (!DROP || drop.mask_k != nullptr) {
+          // two query columns per FFMA2 / FSUB2 / FMUL2; dropout keep bits
+          // as all-ones / zero AND masks on P and on the dP scale
 #pragma unroll
           for (int t = 0; t < 4; t += 2) {
             const int i = 4 * g + t;
@@ -392,40 +393,42 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
               pa = (q >= qlo && q < S) ? pa : 0.f;
               pb = (q + 1 >= qlo && q + 1 < S) ? pb : 0.f;
             }
-            p[t] = pa;
-            p[t + 1] = pb;
-            const uint64_t g2 = fmul2(f2pack(pa, pb),
-                                      fsub2(f2pack(__uint_as_float(rd[i]), __uint_as_float(rd[i + 1])),
-                                            f2pack(dq[t], dq[t + 1])));
+            uint64_t g2;
+            if constexpr (DROP) {
+              const uint32_t ka = 0u - ((mword >> i) & 1u), kb = 0u - ((mword >> (i + 1)) & 1u);
+              p[t] = __uint_as_float(__float_as_uint(pa) & ka);
+              p[t + 1] = __uint_as_float(__float_as_uint(pb) & kb);
+              const uint32_t sb = __float_as_uint(drop.scale);
+              g2 = fmul2(f2pack(pa, pb),
+                         ffma2(f2pack(__uint_as_float(rd[i]), __uint_as_float(rd[i + 1])),
+                               f2pack(__uint_as_float(sb & ka), __uint_as_float(sb & kb)),
+                               f2pack(-dq[t], -dq[t + 1])));
+            } else {
+              p[t] = pa;
+              p[t + 1] = pb;
+              g2 = fmul2(f2pack(pa, pb),
+                         fsub2(f2pack(__uint_as_float(rd[i]), __uint_as_float(rd[i + 1])),
+                               f2pack(dq[t], dq[t + 1])));
+            }
             f2unpack(g2, gr[t], gr[t + 1]);
           }
         } else {
+          // no pre-drawn bits (S % 32 != 0): one hash per element; the same
+          // arithmetic as above, so both forms give identical gradients
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int i = 4 * g + t;
-          float pv = fast_exp2(fmaf(__uint_as_float(rs[i]), scale_log2, -lq[t]));
-          if constexpr (decltype(masked)::value) {
-            const int q = q0c + i;
-            pv = (q >= qlo && q < S) ? pv : 0.f;
-          }
-          if constexpr (DROP) {
-            // element (query q0c+i, this key): bit i of the forward's mask
-            // word for these 32 queries, else one hash per element
-            bool keep;
-            if (drop.mask_k != nullptr) {
-              keep = (mword >> i) & 1u;
-            } else {
-              const uint64_t e = (static_cast<uint64_t>(bh) * S + (q0c + i)) * S + key;
-              const uint32_t bits = drop_bits(dkey, e >> 1);
-              keep = ((key & 1) ? (bits >> 16) : (bits & 0xFFFFu)) >= drop.thr;
+          for (int t = 0; t < 4; ++t) {
+            const int i = 4 * g + t;
+            float pv = fast_exp2(fmaf(__uint_as_float(rs[i]), scale_log2, -lq[t]));
+            if constexpr (decltype(masked)::value) {
+              const int q = q0c + i;
+              pv = (q >= qlo && q < S) ? pv : 0.f;
             }
+            const uint64_t e = (static_cast<uint64_t>(bh) * S + (q0c + i)) * S + key;
+            const uint32_t bits = drop_bits(dkey, e >> 1);
+            const bool keep = ((key & 1) ? (bits >> 16) : (bits & 0xFFFFu)) >= drop.thr;
             p[t] = keep ? pv : 0.f;
-            gr[t] = pv * ((keep ? __uint_as_float(rd[i]) * drop.scale : 0.f) - dq[t]);
-          } else {
-            p[t] = pv;
-            gr[t] = pv * (__uint_as_float(rd[i]) - dq[t]);
+            gr[t] = pv * fmaf(__uint_as_float(rd[i]), keep ? drop.scale : 0.f, -dq[t]);
           }
-        }
         }
         const __nv_bfloat162 p01 = __floats2bfloat162_rn(p[0], p[1]);
         const __nv_bfloat162 p23 = __floats2bfloat162_rn(p[2], p[3]);
