@@ -167,7 +167,7 @@ def gemm_traffic():
 
 
 def cfg_name(cfg):
-    return f"gpt2-L{cfg.n_layer}-h{cfg.hidden}"
+    return f"{getattr(cfg, 'arch', 'gpt2')}-L{cfg.n_layer}-h{cfg.hidden}"
 
 
 class ClockSampler:
