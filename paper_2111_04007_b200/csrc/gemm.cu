@@ -371,6 +371,7 @@ struct Epi2 {
   int64_t group;                // rasterisation group (M tiles per N sweep)
   float* colsum_ws;             // optional: per-32-row partial column sums of D (fp32)
   EpiDrop drop;                 // BIAS_RESID: dropout of the branch before the residual add
+  int dbg;                      // experiment switches (traced builds only)
 };
 
 // Sum of v[0..63] over the 32 lanes (rows) of a warp, scattered so that lane
@@ -417,7 +418,9 @@ __device__ __forceinline__ void epi2_apply(const Epi2& e, int64_t row, int64_t c
         float b[8];
         unpack8(*reinterpret_cast<const uint4*>(e.bias + col0 + i), b);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) v[i + j] += b[j];
+        for (int j = 0; j < 8; j += 2)
+          f2unpack(fadd2(f2pack(v[i + j], v[i + j + 1]), f2pack(b[j], b[j + 1])), v[i + j],
+                   v[i + j + 1]);
       }
     } else {
 #pragma unroll
@@ -428,13 +431,20 @@ __device__ __forceinline__ void epi2_apply(const Epi2& e, int64_t row, int64_t c
   if constexpr (EPI == VP_EPI_BIAS_GELU) {
     // GELU of the bf16-rounded pre-activation; the saving forward also keeps
     // gelu'(pre) (-> aux) so the backward's DGELU epilogue is one multiply
-    if (e.aux_in != nullptr) {
+    // (two columns per FFMA2 / FMUL2; the pre-activation rounded to bf16 by
+    // one cvt per pair)
 #pragma unroll
-      for (int i = 0; i < 64; ++i)
-        v[i] = gelu_tanh_and_grad(__bfloat162float(__float2bfloat16(v[i])), pre[i]);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 64; ++i) v[i] = gelu_tanh(__bfloat162float(__float2bfloat16(v[i])));
+    for (int i = 0; i < 64; i += 2) {
+      const __nv_bfloat162 r = __floats2bfloat162_rn(v[i], v[i + 1]);
+      const uint32_t rb = *reinterpret_cast<const uint32_t*>(&r);
+      const uint64_t x = f2pack(__uint_as_float(rb << 16), __uint_as_float(rb & 0xFFFF0000u));
+      if (e.aux_in != nullptr) {
+        uint64_t dg;
+        f2unpack(gelu_tanh_and_grad2(x, dg), v[i], v[i + 1]);
+        f2unpack(dg, pre[i], pre[i + 1]);
+      } else {
+        f2unpack(gelu_tanh2(x), v[i], v[i + 1]);
+      }
     }
   }
   if constexpr (EPI == VP_EPI_BIAS_RESID) {
@@ -462,6 +472,12 @@ __device__ __forceinline__ void load_row_swizzled(const uint8_t* buf, uint32_t r
 
 #ifdef VP_GEMM_TRACE
 __device__ unsigned long long g_vp_gemm_trace[296][4];
+// epilogue warp 4 of each CTA: [0] tfull wait, [1] TMEM loads, [2] math,
+// [3] staging-buffer waits, [4] smem stores + TMA issue, [5] total
+__device__ unsigned long long g_vp_gemm_etrace[296][6];
+#define ETR(slot, t) do { if (warp == 4 && lane == 0) et[slot] += clock64() - (t); } while (0)
+#else
+#define ETR(slot, t) do {} while (0)
 #endif
 template <int EPI, bool A_MN, bool B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
@@ -614,11 +630,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     uint32_t local = 0, nbuf = 0;
     uint32_t aux_phase = 0;  // parity of the two aux-prefetch barriers of this warp
     const uint32_t lane = lane_id();
+    unsigned long long et[6] = {0, 0, 0, 0, 0, 0};
+    const unsigned long long e_begin = clock64();
+    (void)et; (void)e_begin;
     for (int64_t u = cid; u < n_units; u += n_clusters, ++local) {
       int64_t mb, nb, kb0, kb1;
       unit_coords(u, mb, nb, kb0, kb1);
       const uint32_t acc = local & 1;
+      unsigned long long tq = clock64();
       mbar_wait(&tfull_bar[acc], (local >> 1) & 1);
+      ETR(0, tq);
       tc_fence_after();
       const int32_t row0 = static_cast<int32_t>(mb * 256 + rank * 128 + q * 32);
       const int64_t row = row0 + lane;
@@ -674,6 +695,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
           const int c = half * 128 + ci * 64;
           const int32_t col0 = static_cast<int32_t>(nb * 256 + c);
           if (col0 >= N) break;
+          unsigned long long tq = clock64();
           float v[64], pre[64], xin[64];
           {
             uint32_t raw[32];
@@ -686,6 +708,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[32 + i] = __uint_as_float(raw[i]);
           }
+          ETR(1, tq);
+          tq = clock64();
           if constexpr (kAuxIn) {
             // per-chunk phase: a ragged last N tile skips chunks (and their
             // prefetch), so the barrier phase is not the tile count
@@ -694,7 +718,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             load_row_swizzled(wbuf + ci * 4096, lane, xin);
             __syncwarp();  // every lane has read its aux row before outputs overwrite it
           }
+#ifdef VP_GEMM_TRACE
+          if (epi.dbg & 1) {
+#pragma unroll
+            for (int i = 0; i < 64; ++i) pre[i] = v[i];
+          } else
+#endif
           epi2_apply<EPI>(epi, row, col0, M, N, v, pre, xin);
+#ifdef VP_GEMM_TRACE
+          if (warp == 4) {  // make the math complete before the stamp
+            float z = 0.f;
+#pragma unroll
+            for (int i = 0; i < 64; ++i) z += v[i] + pre[i];
+            if (z == 12345.678f) v[0] = z;
+          }
+#endif
+          ETR(2, tq);
           if (epi.colsum_ws != nullptr) {
             // fused bias gradient: this warp's 32-row partial sums of the
             // 64 output columns -> colsum_ws[row0 / 32][col]
@@ -709,8 +748,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
           }
           if (EPI == VP_EPI_BIAS_GELU && epi.aux_in != nullptr) {
             // pre-activation (aux) then activation (D): both buffers in turn
+            tq = clock64();
             if (lane == 0) bulk_wait_read<0>();
             __syncwarp();
+            ETR(3, tq);
+            tq = clock64();
             uint4 ch[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
@@ -731,12 +773,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             fence_async_smem();
             __syncwarp();
             if (lane == 0) {
+#ifdef VP_GEMM_TRACE
+              if (!(epi.dbg & 2)) {
+#endif
               tma_store_2d(&tmX, wbuf, col0, row0);
               tma_store_2d(&tmD, wbuf + 4096, col0, row0);
+#ifdef VP_GEMM_TRACE
+              }
+#endif
               bulk_commit();
             }
+            ETR(4, tq);
           } else {
             uint8_t* buf = wbuf + (kAuxIn ? ci : (C::kTwoBuf ? (nbuf & 1) : 0)) * 4096;
+            tq = clock64();
             if (!kAuxIn) {
               if (lane == 0) {
                 if constexpr (C::kTwoBuf) bulk_wait_read<1>();
@@ -744,6 +794,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
               }
               __syncwarp();
             }
+            ETR(3, tq);
+            tq = clock64();
             uint4 ch[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
@@ -759,6 +811,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
               tma_store_2d(&tmD, buf, col0, row0);
               bulk_commit();
             }
+            ETR(4, tq);
             ++nbuf;
           }
         }
@@ -770,6 +823,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     }
     if (lane == 0) bulk_wait_all();
     __syncwarp();
+#ifdef VP_GEMM_TRACE
+    if (warp == 4 && lane == 0) {
+      et[5] = clock64() - e_begin;
+      for (int i = 0; i < 6; ++i) g_vp_gemm_etrace[blockIdx.x][i] = et[i];
+    }
+#endif
   }
   tc_fence_before();
   cluster_sync();
@@ -779,6 +838,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
   }
 }
 
+#ifdef VP_GEMM_TRACE
+}  // namespace
+extern "C" int vp_debug_gemm_trace(unsigned long long* mma, unsigned long long* epi) {
+  cudaError_t e = cudaMemcpyFromSymbol(mma, g_vp_gemm_trace, sizeof(g_vp_gemm_trace));
+  if (e == cudaSuccess) e = cudaMemcpyFromSymbol(epi, g_vp_gemm_etrace, sizeof(g_vp_gemm_etrace));
+  return e;
+}
+namespace {
+#endif
 // ---------------------------------------------------------------------------
 // Host side
 // ---------------------------------------------------------------------------
@@ -974,7 +1042,10 @@ static int gemm_entry(int a_kmajor, int b_kmajor, int epilogue, const void* A, i
     int64_t group = 8;
     if (const char* g = getenv("VP_GEMM_GROUP")) group = std::max(1, atoi(g));
     Epi2 e{reinterpret_cast<const __nv_bfloat16*>(bias), reinterpret_cast<const __nv_bfloat16*>(aux),
-           ldaux, group, colsum_ws, drop};
+           ldaux, group, colsum_ws, drop, 0};
+#ifdef VP_GEMM_TRACE
+    if (const char* g = getenv("VP_GEMM_DBG")) e.dbg = atoi(g);
+#endif
     return gemm2_dispatch(epilogue, a_mn, b_mn, ta, tb, td, tx, M, N, K, split, e, st);
   }
   const int BNsel = N <= 128 ? 128 : 256;
@@ -1021,11 +1092,6 @@ extern "C" int vp_gemm_bf16_dropout(int a_kmajor, int b_kmajor, const void* A, i
                     const_cast<void*>(resid), ldres, M, N, K, flags, stream, nullptr, drop);
 }
 
-#ifdef VP_GEMM_TRACE
-extern "C" int vp_debug_gemm_trace(unsigned long long* out) {
-  return cudaMemcpyFromSymbol(out, vp::g_vp_gemm_trace, sizeof(vp::g_vp_gemm_trace));
-}
-#endif
 
 namespace vp {
 namespace {

@@ -347,6 +347,29 @@ __device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
+// Two columns at once on the packed fp32x2 pipes, same operations and
+// rounding as gelu_tanh_and_grad / gelu_tanh lane by lane (bitwise equal).
+__device__ __forceinline__ uint64_t gelu_tanh_and_grad2(uint64_t x, uint64_t& dg) {
+  const float k0 = 0.7978845608028654f, k01 = 0.7978845608028654f * 0.044715f;
+  const uint64_t x3 = fmul2(fmul2(x, x), x);
+  const uint64_t u = ffma2(f2pack(k01, k01), x3, fmul2(f2pack(k0, k0), x));
+  const uint64_t a = ffma2(f2pack(2.f * k01, 2.f * k01), x3, u);
+  float u0, u1;
+  f2unpack(u, u0, u1);
+  const uint64_t t = f2pack(tanh_fast(u0), tanh_fast(u1));
+  const uint64_t h1 = ffma2(f2pack(0.5f, 0.5f), t, f2pack(0.5f, 0.5f));
+  const uint64_t w = ffma2(fmul2(t, f2pack(-1.f, -1.f)), t, f2pack(1.f, 1.f));
+  dg = ffma2(fmul2(f2pack(0.5f, 0.5f), w), a, h1);
+  return fmul2(x, h1);
+}
+__device__ __forceinline__ uint64_t gelu_tanh2(uint64_t x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  const uint64_t u = fmul2(f2pack(k0, k0), ffma2(fmul2(f2pack(k1, k1), x), fmul2(x, x), x));
+  float u0, u1;
+  f2unpack(u, u0, u1);
+  const uint64_t t = f2pack(tanh_fast(u0), tanh_fast(u1));
+  return fmul2(fmul2(f2pack(0.5f, 0.5f), x), fadd2(f2pack(1.f, 1.f), t));
+}
 
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
