@@ -443,6 +443,19 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
       }
     };
 
+    auto load_mwords = [&](int itn, uint32_t (&mw)[2]) {
+      mw[0] = mw[1] = 0u;
+      if (drop.mask_k != nullptr && key < S && itn < n_it) {
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          const int qw = ((i0 + itn) * FB_N + cc * 64 + chalf * 32) >> 5;
+          if (qw * 32 < S)
+            mw[cc] = __ldg(drop.mask_k + (static_cast<uint64_t>(bh) * (S >> 5) + qw) * S + key);
+        }
+      }
+    };
+    uint32_t mnext[2] = {0u, 0u};
+    if constexpr (DROP) load_mwords(0, mnext);
     for (int it = 0; it < n_it; ++it) {
       const int qs = it % FB_NS;
       const int qi = (i0 + it) * FB_N;
@@ -450,18 +463,10 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
       const int qlo = CAUSAL ? key : 0;
       const uint32_t dsb = rowG + (it & 1) * 2 * L::C0;
       // dropout keep bits of this block's two 32-query column groups (one
-      // global word each), requested before any wait so their latency hides
-      uint32_t mwords[2] = {0u, 0u};
-      if constexpr (DROP) {
-        if (drop.mask_k != nullptr && key < S) {
-#pragma unroll
-          for (int cc = 0; cc < 2; ++cc) {
-            const int qw = (qi + cc * 64 + chalf * 32) >> 5;
-            if (qw * 32 < S)
-              mwords[cc] = __ldg(drop.mask_k + (static_cast<uint64_t>(bh) * (S >> 5) + qw) * S + key);
-          }
-        }
-      }
+      // global word each), loaded one block ahead so their latency hides
+      // behind a whole block of work
+      uint32_t mwords[2] = {mnext[0], mnext[1]};
+      if constexpr (DROP) load_mwords(it + 1, mnext);
       if (warp == 4 && lane == 0) TR(0);
       mbar_wait(&q_full[qs], (it / FB_NS) & 1);
 #pragma unroll
