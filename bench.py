@@ -599,6 +599,24 @@ def main():
                   "w") as f:
             f.write(v.gantt_csv(v.gantt_rows(tl)))
     gemm_tf = g_flops / (g_ms / 1e3) / 1e12 if g_ms else 0.0
+    # per GEMM class of the step (per-GEMM TFLOP/s vs burst and
+    # sustained): launches grouped by shape, operand layouts and epilogue
+    epi_names = {K.EPI_STORE: "store", K.EPI_BIAS: "bias", K.EPI_BIAS_GELU: "bias_gelu",
+                 K.EPI_BIAS_RESID: "bias_resid", K.EPI_DGELU: "dgelu",
+                 K.EPI_ACC_F32: "acc_f32", K.EPI_STORE_F32: "store_f32", K.EPI_RESID: "resid"}
+    groups = {}
+    for fl, e0, e1, key in recs:
+        gsum = groups.setdefault(key, [0, 0.0, 0])
+        gsum[0] += fl
+        gsum[1] += e0.elapsed_time(e1)
+        gsum[2] += 1
+    gemm_classes = []
+    for (gm, gn, gk, ak, bk, ep), (fl, ms_, n) in sorted(groups.items(), key=lambda kv: -kv[1][1]):
+        gemm_classes.append({"MxNxK": f"{gm}x{gn}x{gk}", "layout": ("n" if ak else "t") + ("t" if bk else "n"),
+                             "epilogue": epi_names.get(ep, str(ep)), "launches": n,
+                             "us_per_launch": round(1e3 * ms_ / n, 1),
+                             "tflops": round(fl / (ms_ / 1e3) / 1e12, 1),
+                             "share_of_gemm_time": round(ms_ / g_ms, 3) if g_ms else None})
     gemm_share = g_ms / (step_us / 1e3) if step_us else 0.0
     burst, sustained, hbm, src = peaks()
 
@@ -689,7 +707,8 @@ def main():
                          "frac": round(gemm_tf / sustained, 4),
                          "traffic": gemm_traffic(),
                          "kernel": "vp_gemm_bf16 (tcgen05), all GEMM launches of one step",
-                         "peak_kind": f"{src} bf16 sustained", "share_of_step": round(gemm_share, 3)},
+                         "peak_kind": f"{src} bf16 sustained", "share_of_step": round(gemm_share, 3),
+                         "burst_peak": burst, "by_class": gemm_classes[:12]},
             "stage_roofline": {"roofline_samples_per_s": round(roof_samples, 1),
                                "frac": round(value / roof_samples, 4)},
             "bubble": {"measured": round(bubble, 4), "predicted": predicted["bubble"],

@@ -174,7 +174,8 @@ def gemm(a, b, out, *, a_kmajor=True, b_kmajor=True, epilogue=EPI_STORE, bias=No
                                 1 if direct else 0, _stream(stream)), "vp_gemm_bf16")
     if timing:
         e1.record(st)
-        GEMM_TIMING["records"].append((2 * M * N * K, e0, e1, (M, N, K, a_kmajor, b_kmajor)))
+        GEMM_TIMING["records"].append((2 * M * N * K, e0, e1,
+                                       (M, N, K, a_kmajor, b_kmajor, epilogue)))
     return out
 
 
@@ -387,7 +388,8 @@ def gemm_dropout(a, b, out, bias, resid, p, seed, salt, *, stream=None, out_ptr=
                                  1 if direct else 0, _stream(stream)), "vp_gemm_bf16_dropout")
     if timing:
         e1.record(st)
-        GEMM_TIMING["records"].append((2 * M * N * K, e0, e1, (M, N, K, True, True)))
+        GEMM_TIMING["records"].append((2 * M * N * K, e0, e1,
+                                       (M, N, K, True, True, EPI_BIAS_RESID)))
     return out
 
 
