@@ -155,6 +155,18 @@ int vp_layernorm_bwd_ex(const void* dy, const void* x, const void* gamma, const 
                         const float* rstd, void* dx, float* dgamma, float* dbeta, float* dsum,
                         int64_t rows, int64_t cols, int accumulate, float* workspace,
                         void* stream);
+/* The same, also finishing the gradient of the dropped-out residual branch
+ * whose output gradient dx is (K7; the reference only prices recompute,
+ * sp/calibration.py:219-221): gy = mask(dx)/(1-p) with the site's keep bits
+ * (device seed, static salt — the mask its forward GEMM epilogue applied)
+ * and dsum += column sums of gy (the branch bias gradient), in one pass.
+ * VP_ERR_UNSUPPORTED for row widths without the TMA-ring path; the caller
+ * then runs vp_layernorm_bwd_ex + vp_dropout_bwd. */
+int vp_layernorm_bwd_dropout(const void* dy, const void* x, const void* gamma, const float* mean,
+                             const float* rstd, void* dx, float* dgamma, float* dbeta,
+                             float* dsum, void* gy, float p, const uint64_t* seed, uint32_t salt,
+                             int64_t rows, int64_t cols, int accumulate, float* workspace,
+                             void* stream);
 
 /* Causal/bidirectional fused attention over packed qkv[T, 3h] (T = B*S),
  * heads of size head_dim; o[T, h] bf16; lse[B*heads*S] fp32 saved for bwd. */

@@ -122,6 +122,17 @@ __device__ __forceinline__ uint32_t drop_keep2(uint32_t key, uint64_t pair, uint
   const uint32_t b = drop_bits(key, pair);
   return ((b & 0xFFFFu) >= thr ? 1u : 0u) | ((b >> 16) >= thr ? 2u : 0u);
 }
+// Elements e0 .. e0+7 (e0 even) of a call site's tensor through its mask:
+// kept values scaled by 1/(1-p), dropped ones 0.
+__device__ __forceinline__ void drop8(float (&f)[8], uint32_t key, int64_t e0, uint32_t thr,
+                                      float scale) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t k = drop_keep2(key, static_cast<uint64_t>(e0 >> 1) + q, thr);
+    f[2 * q] = (k & 1u) ? f[2 * q] * scale : 0.f;
+    f[2 * q + 1] = (k & 2u) ? f[2 * q + 1] * scale : 0.f;
+  }
+}
 inline uint32_t drop_threshold(float p) {
   const double t = static_cast<double>(p) * 65536.0 + 0.5;
   return t >= 65535.0 ? 65535u : static_cast<uint32_t>(t);

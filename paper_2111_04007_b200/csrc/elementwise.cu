@@ -314,15 +314,6 @@ __global__ void __launch_bounds__(512)
 // by that CTA, so the workspace stays reusable (zero-filled once).
 // Dropout mask of 8 consecutive elements starting at flat index e0 (even),
 // applied in place to f (the backward of out = x + dropout(y): dy = mask(g)).
-__device__ __forceinline__ void drop8(float (&f)[8], uint32_t key, int64_t e0, uint32_t thr,
-                                      float scale) {
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const uint32_t k = drop_keep2(key, static_cast<uint64_t>(e0 >> 1) + q, thr);
-    f[2 * q] = (k & 1u) ? f[2 * q] * scale : 0.f;
-    f[2 * q + 1] = (k & 2u) ? f[2 * q + 1] * scale : 0.f;
-  }
-}
 
 // DROP: the input is first passed through the dropout mask of call site
 // (seed, salt) and written to gy; the column sums are those of gy (the bias

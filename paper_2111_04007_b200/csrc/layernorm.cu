@@ -461,6 +461,16 @@ __global__ void __launch_bounds__(W * G * 32, 1)
   }
 }
 
+// Dropout of the residual branch whose output gradient the LN backward
+// finishes (K7): gy = mask(dx) / (1-p) is written beside dx and the column
+// sums (the branch's bias gradient) are taken over gy as the GEMMs read it.
+struct LnDrop {
+  __nv_bfloat16* gy;
+  const uint64_t* seed;
+  uint32_t salt, thr;
+  float scale;
+};
+
 // Fused backward, TMA-staged (rows <= 1024 wide): the group kernel's math
 // with every group's x / dy / residual-gradient rows streamed through a ring
 // of R slots in shared memory by 1-D bulk copies issued by the group's first
@@ -469,12 +479,14 @@ __global__ void __launch_bounds__(W * G * 32, 1)
 // registers) and reaches 3.75 TB/s; the ring keeps R rows per group in
 // flight without registers. A slot is refilled right after the group's
 // named barrier, by which point every member has its slice in registers.
-template <int W, int G, int NV, bool SUM, int R>
+template <int W, int G, int NV, bool SUM, int R, bool DROP = false>
 __global__ void __launch_bounds__(W * G * 32)
     ln_bwd_ring_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
                        const __nv_bfloat16* __restrict__ g, const float* __restrict__ mean,
                        const float* __restrict__ rstd, __nv_bfloat16* __restrict__ dx,
-                       float* __restrict__ ws, int64_t rows, int cols, int accumulate) {
+                       float* __restrict__ ws, int64_t rows, int cols, int accumulate,
+                       LnDrop drop) {
+  static_assert(!DROP || SUM, "the dropout variant also sums the branch bias gradient");
   extern __shared__ __align__(128) uint8_t ring_smem[];
   __shared__ float xch[G][2][W][2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -533,6 +545,8 @@ __global__ void __launch_bounds__(W * G * 32)
     mu = mean[row0];
     rs = rstd[row0];
   }
+  uint32_t dkey = 0;
+  if constexpr (DROP) dkey = drop_key(drop.seed, drop.salt);
   int it = 0, parity = 0;
   for (int64_t row = row0; row < rows; row += npairs, ++it, parity ^= 1) {
     const int slot = it % R;
@@ -604,11 +618,23 @@ __global__ void __launch_bounds__(W * G * 32)
 #pragma unroll
           for (int j = 0; j < 8; ++j) o[j] += pv[j];
         }
-        if constexpr (SUM) {
+        const uint4 ob = pack8(o);
+        if constexpr (DROP) {
+          // the branch sees mask(dx) of the bf16 dx; its bias gradient is
+          // the column sum of what the GEMMs read (bf16 gy)
+          float f[8];
+          unpack8(ob, f);
+          drop8(f, dkey, row * cols + static_cast<int64_t>(v0 + c) * 8, drop.thr, drop.scale);
+          const uint4 gb = pack8(f);
+          reinterpret_cast<uint4*>(drop.gy + row * cols)[v0 + c] = gb;
+          unpack8(gb, f);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) as[i][j] += f[j];
+        } else if constexpr (SUM) {
 #pragma unroll
           for (int j = 0; j < 8; ++j) as[i][j] += o[j];
         }
-        dxr[c] = pack8(o);
+        dxr[c] = ob;
       }
     }
     mu = mu_n;
@@ -863,11 +889,16 @@ static int split_parts(int64_t rows) {
 
 extern "C" int64_t vp_layernorm_ws_elems(int64_t cols) { return 3 * 296 * cols; }
 
-extern "C" int vp_layernorm_bwd_ex(const void* dy, const void* x, const void* gamma,
-                                   const float* mean, const float* rstd, void* dx, float* dgamma,
-                                   float* dbeta, float* dsum, int64_t rows, int64_t cols,
-                                   int accumulate, float* workspace, void* stream) {
+namespace vp {
+namespace {
+// The LN backward of vp_layernorm_bwd_ex / _dropout (drop.gy != nullptr:
+// the fused dropout variant, ring path only — VP_ERR_UNSUPPORTED otherwise).
+int ln_bwd(const void* dy, const void* x, const void* gamma, const float* mean,
+           const float* rstd, void* dx, float* dgamma, float* dbeta, float* dsum, int64_t rows,
+           int64_t cols, int accumulate, float* workspace, const LnDrop& drop, void* stream) {
   if (rows <= 0 || cols <= 0 || (cols % 8) || !workspace) return VP_ERR_ARGS;
+  const bool dropping = drop.gy != nullptr;
+  if (dropping && !dsum) return VP_ERR_ARGS;
   const int nv = pick_nv(cols);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int nq = dsum ? 3 : 2;
@@ -888,6 +919,7 @@ extern "C" int vp_layernorm_bwd_ex(const void* dy, const void* x, const void* ga
     need = static_cast<int>((nvec / 8 + 31) / 32);
   }
   if (getenv("VP_LN_WARP_ROW")) W = 0;
+  if (dropping && (W == 0 || getenv("VP_LN_NO_RING"))) return VP_ERR_UNSUPPORTED;
   if (W) {
     auto launch = [&](auto kern, int G) {
       parts = static_cast<int>(std::min<int64_t>(device_sms(), (rows + G - 1) / G));
@@ -915,12 +947,13 @@ extern "C" int vp_layernorm_bwd_ex(const void* dy, const void* x, const void* ga
           reinterpret_cast<const __nv_bfloat16*>(dy), reinterpret_cast<const __nv_bfloat16*>(x),
           reinterpret_cast<const __nv_bfloat16*>(gamma), mean, rstd,
           reinterpret_cast<__nv_bfloat16*>(dx), workspace, rows, static_cast<int>(cols),
-          accumulate);
+          accumulate, drop);
     };
     // TMA-staged ring (R rows per group in flight); smem = G*cols*4 + G*R*3*row bytes
-#define LN_R(WW, GG, NN, RR)                                                               \
-  (dsum ? launch_ring(ln_bwd_ring_kernel<WW, GG, NN, true, RR>, WW, GG, RR)                \
-        : launch_ring(ln_bwd_ring_kernel<WW, GG, NN, false, RR>, WW, GG, RR))
+#define LN_R(WW, GG, NN, RR)                                                                 \
+  (dropping ? launch_ring(ln_bwd_ring_kernel<WW, GG, NN, true, RR, true>, WW, GG, RR)        \
+   : dsum   ? launch_ring(ln_bwd_ring_kernel<WW, GG, NN, true, RR>, WW, GG, RR)              \
+            : launch_ring(ln_bwd_ring_kernel<WW, GG, NN, false, RR>, WW, GG, RR))
     if (!no_ring && W == 2) {
       if (need == 1) LN_R(2, kPairs, 1, 3);
       else LN_R(2, kPairs, 2, 3);
@@ -984,6 +1017,30 @@ extern "C" int vp_layernorm_bwd_ex(const void* dy, const void* x, const void* ga
   ln_param_reduce<<<(c3 + 31) / 32, 1024, 0, st>>>(workspace, dgamma, dbeta, dsum, parts,
                                                    static_cast<int>(cols), nq);
   return launch_status();
+}
+}  // namespace
+}  // namespace vp
+
+extern "C" int vp_layernorm_bwd_ex(const void* dy, const void* x, const void* gamma,
+                                   const float* mean, const float* rstd, void* dx, float* dgamma,
+                                   float* dbeta, float* dsum, int64_t rows, int64_t cols,
+                                   int accumulate, float* workspace, void* stream) {
+  return ln_bwd(dy, x, gamma, mean, rstd, dx, dgamma, dbeta, dsum, rows, cols, accumulate,
+                workspace, LnDrop{nullptr, nullptr, 0u, 0u, 1.f}, stream);
+}
+
+extern "C" int vp_layernorm_bwd_dropout(const void* dy, const void* x, const void* gamma,
+                                        const float* mean, const float* rstd, void* dx,
+                                        float* dgamma, float* dbeta, float* dsum, void* gy,
+                                        float p, const uint64_t* seed, uint32_t salt,
+                                        int64_t rows, int64_t cols, int accumulate,
+                                        float* workspace, void* stream) {
+  if (!gy || !seed || !dsum || p <= 0.f || p >= 1.f) return VP_ERR_ARGS;
+  const uint32_t thr = drop_threshold(p);
+  return ln_bwd(dy, x, gamma, mean, rstd, dx, dgamma, dbeta, dsum, rows, cols, accumulate,
+                workspace,
+                LnDrop{reinterpret_cast<__nv_bfloat16*>(gy), seed, salt, thr, drop_scale(thr)},
+                stream);
 }
 
 extern "C" int vp_layernorm_bwd(const void* dy, const void* x, const void* gamma,

@@ -56,6 +56,8 @@ _SIGS = {
                            i64, vp, vp, vp],
     "vp_bias_grad_ws_elems": [i64],
     "vp_layernorm_bwd_ex": [vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, c_int, vp, vp],
+    "vp_layernorm_bwd_dropout": [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, f32, vp, u32, i64, i64,
+                                 c_int, vp, vp],
     "vp_embed_fwd": [vp, vp, vp, vp, i64, i64, i64, vp],
     "vp_embed_bwd": [vp, vp, vp, vp, i64, i64, i64, vp],
     "vp_xent_fwd_bwd": [vp, vp, vp, vp, i64, i64, f32, vp],
@@ -204,6 +206,25 @@ def layernorm_bwd(dy, x, gamma, mean, rstd, dx, dgamma, dbeta, workspace, accumu
                                 dbeta.data_ptr(), _p(dsum), rows, cols, int(accumulate),
                                 workspace.data_ptr(), _stream(stream)), "vp_layernorm_bwd")
     return dx
+
+
+def layernorm_bwd_dropout(dy, x, gamma, mean, rstd, dx, dgamma, dbeta, workspace, dsum, gy, p,
+                          seed, salt, accumulate=False, stream=None) -> bool:
+    """layernorm_bwd plus the dropped-out residual branch's gradient in the
+    same pass: gy = mask(dx) (call site ``salt``, device ``seed``) and dsum
+    += its column sums. Returns False (nothing launched) when this row width
+    has no fused path — the caller then runs layernorm_bwd + dropout_bwd."""
+    rows, cols = x.shape
+    rc = L.vp_layernorm_bwd_dropout(dy.data_ptr(), x.data_ptr(), gamma.data_ptr(),
+                                    mean.data_ptr(), rstd.data_ptr(), dx.data_ptr(),
+                                    dgamma.data_ptr(), dbeta.data_ptr(), dsum.data_ptr(),
+                                    gy.data_ptr(), p, seed.data_ptr(), salt & 0xFFFFFFFF, rows,
+                                    cols, int(accumulate), workspace.data_ptr(), _stream(stream))
+    if rc == _lib.VP_ERR_UNSUPPORTED:
+        return False
+    check(rc, "vp_layernorm_bwd_dropout")
+    _count(2)
+    return True
 
 
 def attention_mask_words(batch, seq, heads) -> int:

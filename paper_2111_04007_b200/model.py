@@ -445,6 +445,21 @@ class GPT2Stage:
                        drop_salt(li, site), stream=stream, out_ptr=out_ptr, ldd=ld,
                        direct=out_ptr is not None)
 
+    def _ln_bwd_branch(self, dy, x, gamma, mean, rstd, g, dgamma, dbeta, dbias, li, site,
+                       accumulate, stream):
+        """LN backward finishing g (the residual-stream gradient) that also
+        produces the gradient of the dropped-out branch whose output feeds
+        that residual (site (li, site)): mask(g) in ``drop_tmp`` and its bias
+        gradient, in the same pass when the row width allows, else by the
+        separate dropout backward. Returns the branch gradient."""
+        if K.layernorm_bwd_dropout(dy, x, gamma, mean, rstd, g, dgamma, dbeta, self.ln_ws,
+                                   dbias, self.drop_tmp, self.cfg.dropout, self.seed_buf,
+                                   drop_salt(li, site), accumulate=accumulate, stream=stream):
+            return self.drop_tmp
+        K.layernorm_bwd(dy, x, gamma, mean, rstd, g, dgamma, dbeta, self.ln_ws,
+                        accumulate=accumulate, stream=stream)
+        return self._branch_grad(g, dbias, li, site, stream)
+
     def _branch_grad(self, g, dbias, li, site, stream):
         """Gradient entering a dropped-out branch (out = resid + dropout(y)):
         mask(g) and the branch bias gradient (its column sums), one pass.
@@ -524,10 +539,17 @@ class GPT2Stage:
         # d(stage output) leaves the final LN; its column sum is the FC2 bias
         # gradient of the top layer (fused into the LN backward when p = 0)
         fused = cfg.dropout <= 0
-        self._fc2_done = fused
-        K.layernorm_bwd(self.dc, x, P.w("lnf_g"), self.lnf_mean, self.lnf_rstd, self.g,
-                        P.g("lnf_g"), P.g("lnf_b"), self.ln_ws, accumulate=False, stream=stream,
-                        dsum=P.g(f"l{self.spec.layers[-1]}.b_fc2") if fused else None)
+        self._fc2_done = True
+        top = self.spec.layers[-1]
+        if fused:
+            K.layernorm_bwd(self.dc, x, P.w("lnf_g"), self.lnf_mean, self.lnf_rstd, self.g,
+                            P.g("lnf_g"), P.g("lnf_b"), self.ln_ws, accumulate=False,
+                            stream=stream, dsum=P.g(f"l{top}.b_fc2"))
+        else:
+            # with dropout the top layer's FC2 branch gradient lands in drop_tmp
+            self._ln_bwd_branch(self.dc, x, P.w("lnf_g"), self.lnf_mean, self.lnf_rstd, self.g,
+                                P.g("lnf_g"), P.g("lnf_b"), P.g(f"l{top}.b_fc2"), top,
+                                SITE_FC2, False, stream)
         return self.loss_rows
 
     def _mlm_head(self, labels, loss_scale, loss_sum, stream, scale_dev=None):
@@ -571,8 +593,10 @@ class GPT2Stage:
         g = self.g
         fused = cfg.dropout <= 0  # dropout masks the branch gradients
         # --- MLP: out = x1 + dropout(fc2(gelu(fc1(ln2(x1)))))
-        if fused and fc2_done:
-            gy = g   # FC2 bias gradient already summed by the LN backward that made g
+        if fc2_done:
+            # the LN backward that made g already summed the FC2 bias gradient
+            # (and, with dropout, left mask(g) in drop_tmp)
+            gy = g if fused else self.drop_tmp
         else:
             gy = self._branch_grad(g, P.g(p + "b_fc2"), li, SITE_FC2, stream)
         # dpre = (gy W2) * gelu'(pre); its column sum (FC1 bias grad) in the epilogue
@@ -583,12 +607,18 @@ class GPT2Stage:
         K.gemm(self.dpre, P.w(p + "w_fc1"), self.dc, b_kmajor=False, stream=stream)
         K.gemm(self.dpre, w.c, P.g(p + "w_fc1"), a_kmajor=False, b_kmajor=False,
                epilogue=K.EPI_ACC_F32, stream=stream)
-        # g += LN2 backward; with p = 0 its column sum is the proj bias gradient
-        K.layernorm_bwd(self.dc, w.x1, P.w(p + "ln2_g"), w.mean2, w.rstd2, g,
-                        P.g(p + "ln2_g"), P.g(p + "ln2_b"), self.ln_ws, accumulate=True,
-                        stream=stream, dsum=P.g(p + "b_o") if fused else None)
+        # g += LN2 backward; its column sum is the proj bias gradient (of
+        # mask(g) with dropout, written to drop_tmp in the same pass)
+        if fused:
+            K.layernorm_bwd(self.dc, w.x1, P.w(p + "ln2_g"), w.mean2, w.rstd2, g,
+                            P.g(p + "ln2_g"), P.g(p + "ln2_b"), self.ln_ws, accumulate=True,
+                            stream=stream, dsum=P.g(p + "b_o"))
+            gy = g
+        else:
+            gy = self._ln_bwd_branch(self.dc, w.x1, P.w(p + "ln2_g"), w.mean2, w.rstd2, g,
+                                     P.g(p + "ln2_g"), P.g(p + "ln2_b"), P.g(p + "b_o"), li,
+                                     SITE_PROJ, True, stream)
         # --- attention: x1 = x + dropout(proj(attn(qkv(ln1(x)))))
-        gy = g if fused else self._branch_grad(g, P.g(p + "b_o"), li, SITE_PROJ, stream)
         K.gemm(gy, P.w(p + "w_o"), self.do, b_kmajor=False, stream=stream)
         K.gemm(gy, w.o, P.g(p + "w_o"), a_kmajor=False, b_kmajor=False,
                epilogue=K.EPI_ACC_F32, stream=stream)
@@ -599,12 +629,22 @@ class GPT2Stage:
                epilogue=K.EPI_ACC_F32, stream=stream)
         if not fused_bq:
             K.bias_grad(self.dqkv, P.g(p + "b_qkv"), self.bias_ws, stream)
-        # g = d(layer input) = d(output of the layer below)
-        lower_fc2 = P.g(f"l{lower}.b_fc2") if (fused and lower is not None) else None
-        K.layernorm_bwd(self.dc, x, P.w(p + "ln1_g"), w.mean1, w.rstd1, g,
-                        P.g(p + "ln1_g"), P.g(p + "ln1_b"), self.ln_ws, accumulate=True,
-                        stream=stream, dsum=lower_fc2)
-        return lower_fc2 is not None
+        # g = d(layer input) = d(output of the layer below); the same pass
+        # finishes the lower layer's FC2 branch gradient
+        if lower is None:
+            K.layernorm_bwd(self.dc, x, P.w(p + "ln1_g"), w.mean1, w.rstd1, g,
+                            P.g(p + "ln1_g"), P.g(p + "ln1_b"), self.ln_ws, accumulate=True,
+                            stream=stream)
+            return False
+        if fused:
+            K.layernorm_bwd(self.dc, x, P.w(p + "ln1_g"), w.mean1, w.rstd1, g,
+                            P.g(p + "ln1_g"), P.g(p + "ln1_b"), self.ln_ws, accumulate=True,
+                            stream=stream, dsum=P.g(f"l{lower}.b_fc2"))
+        else:
+            self._ln_bwd_branch(self.dc, x, P.w(p + "ln1_g"), w.mean1, w.rstd1, g,
+                                P.g(p + "ln1_g"), P.g(p + "ln1_b"), P.g(f"l{lower}.b_fc2"),
+                                lower, SITE_FC2, True, stream)
+        return True
 
     def backward(self, grad_out: Optional[torch.Tensor], ids: Optional[torch.Tensor],
                  dseed: Optional[int] = None, stream=None,
