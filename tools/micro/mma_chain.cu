@@ -7,7 +7,7 @@
 #include "sm100.cuh"
 using namespace vp;
 
-template <int n, int chains, int mn_major_b>
+template <int n, int chains, int mn_major_b, int mn_major_a = 0, int ts = 0>
 __global__ void probe(int reps, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
@@ -24,7 +24,7 @@ __global__ void probe(int reps, unsigned long long* out) {
   const uint32_t tmem = slot;
   if (threadIdx.x == 0) {
     const uint32_t sA = smem_u32(sm), sB = smem_u32(sm + 16384);
-    const uint32_t id = idesc_bf16(128, n, false, mn_major_b != 0);
+    const uint32_t id = idesc_bf16(128, n, mn_major_a != 0, mn_major_b != 0);
     // warm-up
     for (int k = 0; k < 4; ++k)
       umma_f16(tmem, sdesc_sw128(sA + k * 32, 16, 1024), sdesc_sw128(sB + k * 32, 16, 1024), id, k > 0);
@@ -38,7 +38,10 @@ __global__ void probe(int reps, unsigned long long* out) {
         for (int c = 0; c < chains; ++c) {
           const uint64_t bd = mn_major_b ? sdesc_sw128(sB + k * 2048, 16384, 1024)
                                          : sdesc_sw128(sB + k * 32, 16, 1024);
-          umma_f16(tmem + c * n, sdesc_sw128(sA + k * 32, 16, 1024), bd, id, 1u);
+          const uint64_t ad = mn_major_a ? sdesc_sw128(sA + k * 2048, 8192, 1024)
+                                         : sdesc_sw128(sA + k * 32, 16, 1024);
+          if (ts) umma_f16_ts(tmem + c * n, tmem + 448 + k * 8, bd, id, 1u);
+          else umma_f16(tmem + c * n, ad, bd, id, 1u);
         }
     }
     umma_commit(&bar);
@@ -51,17 +54,17 @@ __global__ void probe(int reps, unsigned long long* out) {
   if (threadIdx.x < 32) { tc_fence_after(); tmem_dealloc(tmem, 512); }
 }
 
-template <int n, int chains, int mn>
+template <int n, int chains, int mn, int mna = 0, int ts = 0>
 void run1(unsigned long long* d, int reps) {
   const int smem = 16384 + 32768 + 1024;
-  cudaFuncSetAttribute(probe<n, chains, mn>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  probe<n, chains, mn><<<1, 128, smem>>>(reps, d);
-  probe<n, chains, mn><<<1, 128, smem>>>(reps, d);
+  cudaFuncSetAttribute(probe<n, chains, mn, mna, ts>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  probe<n, chains, mn, mna, ts><<<1, 128, smem>>>(reps, d);
+  probe<n, chains, mn, mna, ts><<<1, 128, smem>>>(reps, d);
   unsigned long long cyc;
   cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
   const double inst = 4.0 * reps * chains;
-  printf("{\"N\": %d, \"chains\": %d, \"b_mn_major\": %d, \"clk_per_mma\": %.1f, \"floor\": %d, "
-         "\"flop_per_clk\": %.0f}\n", n, chains, mn, cyc / inst, n / 2, 2.0 * 128 * n * 16 * inst / cyc);
+  printf("{\"N\": %d, \"chains\": %d, \"b_mn_major\": %d, \"a_mn_major\": %d, \"ts\": %d, \"clk_per_mma\": %.1f, \"floor\": %d, "
+         "\"flop_per_clk\": %.0f}\n", n, chains, mn, mna, ts, cyc / inst, n / 2, 2.0 * 128 * n * 16 * inst / cyc);
 }
 
 int main() {
@@ -74,6 +77,10 @@ int main() {
   run1<256, 1, 0>(d, reps); run1<256, 2, 0>(d, reps);
   run1<32, 1, 1>(d, reps); run1<32, 4, 1>(d, reps);
   run1<64, 1, 1>(d, reps); run1<64, 2, 1>(d, reps); run1<64, 4, 1>(d, reps);
+  // the attention backward's operand forms: dQ (A MN-major, B MN-major),
+  // dV (A from TMEM, B MN-major), dK (A K-major, B MN-major), S/dP (both K-major)
+  run1<64, 1, 1, 1, 0>(d, reps); run1<128, 1, 1, 1, 0>(d, reps);
+  run1<64, 1, 1, 0, 1>(d, reps); run1<128, 1, 0, 0, 1>(d, reps); run1<32, 1, 1, 1, 0>(d, reps);
   printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
 }
