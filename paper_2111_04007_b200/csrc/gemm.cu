@@ -265,8 +265,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane_id() == 0) {
-      // ===== MMA issuer =====
+    {
+      // ===== MMA issuer (whole warp; elect.sync issues) =====
       constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN, B_MN);
       uint32_t stage = 0, phase = 0;
       uint32_t local = 0;
@@ -290,12 +290,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                                      : sdesc_sw128(sa + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? sdesc_sw128(sb + k * 2048, 64 * BK * 2, 1024)
                                      : sdesc_sw128(sb + k * 32, 16, 1024);
-            umma_f16(tmem_d, ad, bd, idesc, (kb | k) != 0);
+            umma_f16_w(tmem_d, ad, bd, idesc, (kb | k) != 0);
           }
-          umma_commit(&empty_bar[stage]);
+          umma_commit_w(&empty_bar[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        umma_commit(&tfull_bar[acc]);
+        umma_commit_w(&tfull_bar[acc]);
       }
     }
   } else if (warp >= 4) {
@@ -570,8 +570,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       }
     }
   } else if (warp == 1) {
-    if (leader && lane_id() == 0) {
-      // ===== MMA issuer (leader CTA only) =====
+    if (leader) {
+      // ===== MMA issuer (leader CTA only; whole warp, elect.sync issues) =====
       constexpr uint32_t idesc = idesc_bf16(256, 256, A_MN, B_MN);
       uint32_t stage = 0, phase = 0, local = 0;
 #ifdef VP_GEMM_TRACE
@@ -607,12 +607,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                                      : sdesc_sw128(sa + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? sdesc_sw128(sb + k * 2048, 64 * BK * 2, 1024)
                                      : sdesc_sw128(sb + k * 32, 16, 1024);
-            umma_f16_2sm(tmem_d, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            umma_f16_2sm_w(tmem_d, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
-          umma_commit_2sm(&empty_bar[stage], 0x3);
+          umma_commit_2sm_w(&empty_bar[stage], 0x3);
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
-        umma_commit_2sm(&tfull_bar[acc], 0x3);
+        umma_commit_2sm_w(&tfull_bar[acc], 0x3);
       }
 #ifdef VP_GEMM_TRACE
       g_vp_gemm_trace[blockIdx.x][0] = w_full;

@@ -210,6 +210,26 @@ __device__ __forceinline__ void umma_commit_w(uint64_t* bar) {
           smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void umma_f16_2sm_w(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                               uint32_t idesc, uint32_t accumulate) {
+  const uint32_t z = 0;
+  asm volatile(
+      "{\n.reg .pred p, e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n}"
+      ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(z)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_2sm_w(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n.reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;\n}" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
 // Arrive on an mbarrier once every previously issued tcgen05.mma completed.
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile(
