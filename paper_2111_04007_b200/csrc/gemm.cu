@@ -539,8 +539,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
   };
 
   if (warp == 0) {
-    if (lane_id() == 0) {
-      // ===== TMA producer (both CTAs) =====
+    {
+      // ===== TMA producer (both CTAs; whole warp, elect.sync issues) =====
       uint32_t stage = 0, phase = 0;
       for (int64_t u = cid; u < n_units; u += n_clusters) {
         int64_t mb, nb, kb0, kb1;
@@ -551,19 +551,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * kStageBytes2;
           uint8_t* sb = sa + 128 * BK * 2;
-          if (leader) mbar_expect_tx(&full_bar[stage], 2 * kStageBytes2);
+          if (leader) mbar_expect_tx_w(&full_bar[stage], 2 * kStageBytes2);
           const int32_t k0 = static_cast<int32_t>(kb * BK);
           if constexpr (!A_MN) {
-            tma_load_2d_2sm(sa, &tmA, &full_bar[stage], k0, m0);
+            tma_load_2d_2sm_w(sa, &tmA, &full_bar[stage], k0, m0);
           } else {
-            tma_load_2d_2sm(sa, &tmA, &full_bar[stage], m0, k0);
-            tma_load_2d_2sm(sa + 64 * BK * 2, &tmA, &full_bar[stage], m0 + 64, k0);
+            tma_load_2d_2sm_w(sa, &tmA, &full_bar[stage], m0, k0);
+            tma_load_2d_2sm_w(sa + 64 * BK * 2, &tmA, &full_bar[stage], m0 + 64, k0);
           }
           if constexpr (!B_MN) {
-            tma_load_2d_2sm(sb, &tmB, &full_bar[stage], k0, n0);
+            tma_load_2d_2sm_w(sb, &tmB, &full_bar[stage], k0, n0);
           } else {
-            tma_load_2d_2sm(sb, &tmB, &full_bar[stage], n0, k0);
-            tma_load_2d_2sm(sb + 64 * BK * 2, &tmB, &full_bar[stage], n0 + 64, k0);
+            tma_load_2d_2sm_w(sb, &tmB, &full_bar[stage], n0, k0);
+            tma_load_2d_2sm_w(sb + 64 * BK * 2, &tmB, &full_bar[stage], n0 + 64, k0);
           }
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
