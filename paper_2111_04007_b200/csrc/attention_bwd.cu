@@ -49,14 +49,7 @@ __device__ unsigned long long g_vp_trace[4][16][16];
   do { if (blockIdx.x < 4 && it < 16) g_vp_trace[blockIdx.x][it][slot] = clock64(); } while (0)
 #define TRJ(jj, slot) \
   do { if (blockIdx.x < 4 && (jj) < 16) g_vp_trace[blockIdx.x][jj][slot] = clock64(); } while (0)
-// diagnostic switches of the traced build (results are garbage when set):
-// 1 = softmax warps skip their TMEM loads of S/dP and the P^T store,
-// 2 = skip the dS^T shared-memory stores, 4 = drain warps skip the dQ
-// TMEM loads and reduce-adds
-__device__ int g_vp_bwd_dbg;
-#define BWD_DBG(bit) (g_vp_bwd_dbg & (bit))
 #else
-#define BWD_DBG(bit) 0
 #define TR(slot) do {} while (0)
 #define TRJ(jj, slot) do {} while (0)
 #endif
@@ -258,8 +251,8 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    {
-      // ===== MMA issuer (whole warp, elect.sync issues) =====
+    if (lane == 0) {
+      // ===== MMA issuer =====
       constexpr uint32_t idST = idesc_bf16(128, FB_N, false, false);
       constexpr uint32_t idG = idesc_bf16(128, 64, false, true);
       constexpr uint32_t idG1 = idesc_bf16(128, 32, false, true);
@@ -289,24 +282,24 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
         // dV += P^T dO (A = P^T from TMEM)
 #pragma unroll
         for (int k = 0; k < FB_N / 16; ++k)
-          umma_f16_ts_w(tDV, tP + k * 8, ndesc0(sdO, k), idG, (j > 0 || k > 0) ? 1u : 0u);
+          umma_f16_ts(tDV, tP + k * 8, ndesc0(sdO, k), idG, (j > 0 || k > 0) ? 1u : 0u);
         if constexpr (WIDE) {
 #pragma unroll
           for (int k = 0; k < FB_N / 16; ++k)
-            umma_f16_ts_w(tDV + 64, tP + k * 8, ndesc1(sdO, k), idG1, (j > 0 || k > 0) ? 1u : 0u);
+            umma_f16_ts(tDV + 64, tP + k * 8, ndesc1(sdO, k), idG1, (j > 0 || k > 0) ? 1u : 0u);
         }
-        umma_commit_w(pt_empty);
+        umma_commit(pt_empty);
         // dK += dS^T Q
 #pragma unroll
         for (int k = 0; k < FB_N / 16; ++k) {
           const uint32_t koff = (k >> 2) * L::C0 + (k & 3) * 32;
-          umma_f16_w(tDK, sdesc_sw128(sdSt + koff, 16, 1024), ndesc0(sQ, k), idG,
+          umma_f16(tDK, sdesc_sw128(sdSt + koff, 16, 1024), ndesc0(sQ, k), idG,
                    (j > 0 || k > 0) ? 1u : 0u);
           if constexpr (WIDE)
-            umma_f16_w(tDK + 64, sdesc_sw128(sdSt + koff, 16, 1024), ndesc1(sQ, k), idG1,
+            umma_f16(tDK + 64, sdesc_sw128(sdSt + koff, 16, 1024), ndesc1(sQ, k), idG1,
                      (j > 0 || k > 0) ? 1u : 0u);
         }
-        umma_commit_w(&q_empty[qs]);  // Q_j, dO_j no longer needed
+        umma_commit(&q_empty[qs]);  // Q_j, dO_j no longer needed
         if constexpr (!WIDE) {
           // dQ_j = dS K once the drain warps emptied dQ_{j-1}
           mbar_wait(dq_empty, (j & 1) ^ 1);
@@ -319,14 +312,14 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < FB_M / 16; ++k) {
-          umma_f16_w(tDQ, sdesc_sw128(sdSt + k * 2048, L::C0, 1024), ndesc0(sK, k), idQ,
+          umma_f16(tDQ, sdesc_sw128(sdSt + k * 2048, L::C0, 1024), ndesc0(sK, k), idQ,
                    k > 0 ? 1u : 0u);
           if constexpr (WIDE)
-            umma_f16_w(tDQ + 64, sdesc_sw128(sdSt + k * 2048, L::C0, 1024), ndesc1(sK, k), idQ1,
+            umma_f16(tDQ + 64, sdesc_sw128(sdSt + k * 2048, L::C0, 1024), ndesc1(sK, k), idQ1,
                      k > 0 ? 1u : 0u);
         }
-        umma_commit_w(dq_full);
-        umma_commit_w(&ds_empty[j & 1]);
+        umma_commit(dq_full);
+        umma_commit(&ds_empty[j & 1]);
         TRJ(j, 12);
       };
       for (int it = 0; it < n_it; ++it) {
@@ -345,15 +338,15 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
-          umma_f16_w(tS, kdesc(sK, k), kdesc(sQ, k), idST, k > 0);
-          umma_f16_w(tdP, kdesc(sV, k), kdesc(sdO, k), idST, k > 0);
+          umma_f16(tS, kdesc(sK, k), kdesc(sQ, k), idST, k > 0);
+          umma_f16(tdP, kdesc(sV, k), kdesc(sdO, k), idST, k > 0);
         }
-        umma_commit_w(&st_full[0]);
-        umma_commit_w(&st_full[1]);
+        umma_commit(&st_full[0]);
+        umma_commit(&st_full[1]);
         if (it >= 1) issue_grad(it - 1);
       }
       issue_grad(n_it - 1);
-      umma_commit_w(acc_full);
+      umma_commit(acc_full);
     }
   } else if (warp >= 4 && warp < 4 + FB_CW) {
     // ===== softmax-gradient warps: thread = key row =====
@@ -483,13 +476,8 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
         mbar_wait(&st_full[cc], it & 1);
         if (warp == 4 && lane == 0) { if (cc == 0) TR(1); else TR(3); }
         tc_fence_after();
-        if (!BWD_DBG(1)) {
-          tmem_ld32(tS + trow + c, rs);
-          tmem_ld32(tdP + trow + c, rd);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) rs[i] = rd[i] = static_cast<uint32_t>(i);
-        }
+        tmem_ld32(tS + trow + c, rs);
+        tmem_ld32(tdP + trow + c, rd);
         const uint32_t lv = lv_base + (qs * 2 * FB_N + c) * 4;
         const float4 l4 = lds128f(lv), d4 = lds128f(lv + FB_N * 4);
         tmem_ld_wait();
@@ -509,15 +497,11 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
           tc_fence_after();
           if (warp == 4 && lane == 0) TR(5);
         }
-        if (!BWD_DBG(1)) tmem_st16(tP + trow + (c >> 1), pp);
-        if (!BWD_DBG(2)) {
+        tmem_st16(tP + trow + (c >> 1), pp);
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            sts128(dsb + cc * L::C0 + (((chalf * 4 + k) ^ (r & 7)) << 4),
-                   make_uint4(pg[4 * k], pg[4 * k + 1], pg[4 * k + 2], pg[4 * k + 3]));
-        } else if (pg[0] == 0x12345u && pp[0] == 0x54321u) {
-          sts128(dsb, make_uint4(pg[1], pg[2], pp[1], pp[2]));  // keep the math live
-        }
+        for (int k = 0; k < 4; ++k)
+          sts128(dsb + cc * L::C0 + (((chalf * 4 + k) ^ (r & 7)) << 4),
+                 make_uint4(pg[4 * k], pg[4 * k + 1], pg[4 * k + 2], pg[4 * k + 3]));
       }
       tmem_st_wait();
       tc_fence_before();
@@ -619,12 +603,6 @@ __global__ void __launch_bounds__(FB_THREADS, 1)
       if (warp == 4 + FB_CW && lane == 0) TRJ(j, 13);
       tc_fence_after();
       uint32_t v2[WIDE ? 32 : 1];
-      if (BWD_DBG(4)) {
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(dq_empty);
-        continue;
-      }
       tmem_ld32(tDQ + trow, v0);
       tmem_ld32(tDQ + trow + 32, v1);
       if constexpr (WIDE) tmem_ld32(tDQ + trow + 64, v2);
@@ -900,8 +878,5 @@ int attention_bwd_fused(const void* qkv, const void* o, const void* dout, const 
 #ifdef VP_BWD_TRACE
 extern "C" int vp_debug_bwd_trace(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, vp::g_vp_trace, sizeof(vp::g_vp_trace));
-}
-extern "C" int vp_debug_bwd_set(int v) {
-  return cudaMemcpyToSymbol(vp::g_vp_bwd_dbg, &v, sizeof(int));
 }
 #endif

@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(128 + 32 * SW, 2)
       }
     }
   } else if (warp == 1) {
-    {  // whole warp; elect.sync issues inside the tcgen05 asm
+    if (lane == 0) {
       // ===== MMA issuer =====
       constexpr uint32_t idS = idesc_bf16(128, TA_BN, false, false);
       constexpr uint32_t idO = idesc_bf16(128, L::NARROW ? 64 : D, false, true);
@@ -191,20 +191,20 @@ __global__ void __launch_bounds__(128 + 32 * SW, 2)
           const uint64_t bd = sdesc_sw128(sV + k * 2048, L::KCH, 1024);
           if constexpr (L::NARROW) {
             // d 0..63 and d 64..95 (SW64 rows of 64 B: +1 KB per 16 keys)
-            umma_f16_ts_w(tmem + 128, tmem + L::TP + k * 8, bd, idO, (j > 0 || k > 0) ? 1u : 0u);
-            umma_f16_ts_w(tmem + 192, tmem + L::TP + k * 8,
+            umma_f16_ts(tmem + 128, tmem + L::TP + k * 8, bd, idO, (j > 0 || k > 0) ? 1u : 0u);
+            umma_f16_ts(tmem + 192, tmem + L::TP + k * 8,
                         sdesc_sw64(sV + L::KCH + k * 1024, L::KCH, 512), idO1,
                         (j > 0 || k > 0) ? 1u : 0u);
           } else if constexpr (L::PT) {
-            umma_f16_ts_w(tmem + 128, tmem + L::TP + k * 8, bd, idO, (j > 0 || k > 0) ? 1u : 0u);
+            umma_f16_ts(tmem + 128, tmem + L::TP + k * 8, bd, idO, (j > 0 || k > 0) ? 1u : 0u);
           } else {
             // A = P [q][key] K-major (one 128 B row chunk): +32 B per 16 keys
             const uint64_t ad = sdesc_sw128(sPj + k * 32, 16, 1024);
-            umma_f16_w(tmem + 128, ad, bd, idO, (j > 0 || k > 0) ? 1u : 0u);
+            umma_f16(tmem + 128, ad, bd, idO, (j > 0 || k > 0) ? 1u : 0u);
           }
         }
-        umma_commit_w(&o_full[j & 1]);
-        umma_commit_w(&kv_empty[st]);
+        umma_commit(&o_full[j & 1]);
+        umma_commit(&kv_empty[st]);
       };
       auto issue_s = [&](int j) {
         const int st = j % L::STAGES;
@@ -216,19 +216,19 @@ __global__ void __launch_bounds__(128 + 32 * SW, 2)
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           if (L::NARROW && k >= 4) {
-            umma_f16_w(tmem + (j & 1) * TA_BN, sdesc_sw64(sQ + L::QCH + (k - 4) * 32, 16, 512),
+            umma_f16(tmem + (j & 1) * TA_BN, sdesc_sw64(sQ + L::QCH + (k - 4) * 32, 16, 512),
                      sdesc_sw64(sK + L::KCH + (k - 4) * 32, 16, 512), idS, 1u);
             continue;
           }
           const uint64_t bd = sdesc_sw128(sK + (k >> 2) * L::KCH + (k & 3) * 32, 16, 1024);
           if constexpr (L::QT) {
-            umma_f16_ts_w(tmem + (j & 1) * TA_BN, tmem + L::TQ + k * 8, bd, idS, k > 0);
+            umma_f16_ts(tmem + (j & 1) * TA_BN, tmem + L::TQ + k * 8, bd, idS, k > 0);
           } else {
-            umma_f16_w(tmem + (j & 1) * TA_BN,
+            umma_f16(tmem + (j & 1) * TA_BN,
                      sdesc_sw128(sQ + (k >> 2) * L::QCH + (k & 3) * 32, 16, 1024), bd, idS, k > 0);
           }
         }
-        umma_commit_w(&s_full[j & 1]);
+        umma_commit(&s_full[j & 1]);
       };
       // S_{j+2} is issued as soon as the softmax warps have LOADED S_j (its
       // TMEM buffer is free then), ahead of PV_j, which waits for them to
@@ -615,7 +615,7 @@ __global__ void __launch_bounds__(TB_THREADS, TbSmem<D>::MINB)
       }
     }
   } else if (warp == 1) {
-    {  // whole warp; elect.sync issues inside the tcgen05 asm
+    if (lane == 0) {
       // ===== MMA issuer =====
       constexpr uint32_t idST = idesc_bf16(128, TB_N, false, false);
       constexpr uint32_t idG = idesc_bf16(128, D, false, true);
@@ -633,13 +633,13 @@ __global__ void __launch_bounds__(TB_THREADS, TbSmem<D>::MINB)
 #pragma unroll
         for (int k = 0; k < TB_N / 16; ++k) {
           const uint32_t acc = (it > 0 || k > 0) ? 1u : 0u;
-          umma_f16_w(tDV, sdesc_sw128(sPt + k * 32, 16, 1024),
+          umma_f16(tDV, sdesc_sw128(sPt + k * 32, 16, 1024),
                    sdesc_sw128(sdO + k * 2048, L::SMALL, 1024), idG, acc);
-          umma_f16_w(tDK, sdesc_sw128(sdSt + k * 32, 16, 1024),
+          umma_f16(tDK, sdesc_sw128(sdSt + k * 32, 16, 1024),
                    sdesc_sw128(sQ + k * 2048, L::SMALL, 1024), idG, acc);
         }
-        umma_commit_w(&p_empty[st]);
-        umma_commit_w(&q_empty[qs]);
+        umma_commit(&p_empty[st]);
+        umma_commit(&q_empty[qs]);
       };
       for (int it = 0; it < n_it; ++it) {
         const int st = it % NB;
@@ -653,16 +653,16 @@ __global__ void __launch_bounds__(TB_THREADS, TbSmem<D>::MINB)
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t ob = (k >> 2) * L::BIG + (k & 3) * 32;
           const uint32_t os = (k >> 2) * L::SMALL + (k & 3) * 32;
-          umma_f16_w(tS + st * TB_N, sdesc_sw128(sK + ob, 16, 1024), sdesc_sw128(sQ + os, 16, 1024),
+          umma_f16(tS + st * TB_N, sdesc_sw128(sK + ob, 16, 1024), sdesc_sw128(sQ + os, 16, 1024),
                    idST, k > 0);
-          umma_f16_w(tP + st * TB_N, sdesc_sw128(sV + ob, 16, 1024),
+          umma_f16(tP + st * TB_N, sdesc_sw128(sV + ob, 16, 1024),
                    sdesc_sw128(sdO + os, 16, 1024), idST, k > 0);
         }
-        umma_commit_w(&st_full[st]);
+        umma_commit(&st_full[st]);
         if (it >= 1) issue_grad(it - 1);
       }
       if (n_it > 0) issue_grad(n_it - 1);
-      umma_commit_w(acc_full);
+      umma_commit(acc_full);
     }
   } else if (warp >= 4) {
     // ===== P^T / dS^T: thread = key row; this warp owns 32 of the 64 columns =====
@@ -862,7 +862,7 @@ __global__ void __launch_bounds__(TB_THREADS, TbSmem<D>::MINB)
       }
     }
   } else if (warp == 1) {
-    {  // whole warp; elect.sync issues inside the tcgen05 asm
+    if (lane == 0) {
       constexpr uint32_t idS = idesc_bf16(128, TB_N, false, false);
       constexpr uint32_t idG = idesc_bf16(128, D, false, true);
       const uint32_t sQ = smem_u32(smem + L::A_OFF), sdO = smem_u32(smem + L::B_OFF);
@@ -876,10 +876,10 @@ __global__ void __launch_bounds__(TB_THREADS, TbSmem<D>::MINB)
         const uint32_t sdS = smem_u32(smem + L::G_OFF + st * 128 * TB_N * 2);
 #pragma unroll
         for (int k = 0; k < TB_N / 16; ++k)
-          umma_f16_w(tDQ, sdesc_sw128(sdS + k * 32, 16, 1024),
+          umma_f16(tDQ, sdesc_sw128(sdS + k * 32, 16, 1024),
                    sdesc_sw128(sK + k * 2048, L::SMALL, 1024), idG, (j > 0 || k > 0) ? 1u : 0u);
-        umma_commit_w(&g_empty[st]);
-        umma_commit_w(&k_empty[ks]);
+        umma_commit(&g_empty[st]);
+        umma_commit(&k_empty[ks]);
       };
       for (int j = 0; j < n_kb; ++j) {
         const int st = j % NB;
@@ -893,16 +893,16 @@ __global__ void __launch_bounds__(TB_THREADS, TbSmem<D>::MINB)
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t ob = (k >> 2) * L::BIG + (k & 3) * 32;
           const uint32_t os = (k >> 2) * L::SMALL + (k & 3) * 32;
-          umma_f16_w(tS + st * TB_N, sdesc_sw128(sQ + ob, 16, 1024), sdesc_sw128(sK + os, 16, 1024),
+          umma_f16(tS + st * TB_N, sdesc_sw128(sQ + ob, 16, 1024), sdesc_sw128(sK + os, 16, 1024),
                    idS, k > 0);
-          umma_f16_w(tP + st * TB_N, sdesc_sw128(sdO + ob, 16, 1024),
+          umma_f16(tP + st * TB_N, sdesc_sw128(sdO + ob, 16, 1024),
                    sdesc_sw128(sV + os, 16, 1024), idS, k > 0);
         }
-        umma_commit_w(&s_full[st]);
+        umma_commit(&s_full[st]);
         if (j >= 1) issue_dq(j - 1);
       }
       issue_dq(n_kb - 1);
-      umma_commit_w(acc_full);
+      umma_commit(acc_full);
     }
   } else if (warp >= 4) {
     const uint32_t qd = warp & 3;
