@@ -92,6 +92,42 @@ def test_dropout_bwd_mask_and_bias():
     assert rel(db.cpu(), 1 + gy.float().cpu().sum(0)) < 1e-4
 
 
+@pytest.mark.parametrize("rows,cols,acc", [(3000, 1024, True), (2048, 1920, False),
+                                           (1000, 3072, True)])
+def test_layernorm_bwd_dropout_fused(rows, cols, acc):
+    """vp_layernorm_bwd_dropout == layernorm_bwd followed by dropout_bwd:
+    dx and gy bitwise, dgamma / dbeta / the branch bias gradient to fp32
+    summation-order noise (widths of GPT-2 355M, 2.5B, 8.3B)."""
+    from paper_2111_04007_b200 import kernels as K
+    torch.manual_seed(5)
+    x = torch.randn(rows, cols, device="cuda").bfloat16()
+    dy = torch.randn(rows, cols, device="cuda").bfloat16()
+    gamma = (1 + 0.1 * torch.randn(cols, device="cuda")).bfloat16()
+    mu = x.float().mean(1)
+    rs = torch.rsqrt(x.float().var(1, unbiased=False) + 1e-5)
+    base = torch.randn(rows, cols, device="cuda").bfloat16()
+    ws = torch.zeros(K.layernorm_ws_elems(cols), device="cuda")
+    bws = torch.zeros(K.bias_grad_ws_elems(cols), device="cuda")
+    sb = _seed_buf()
+    out = {}
+    for fused in (False, True):
+        dx = base.clone()
+        dg, db, ds = (torch.zeros(cols, device="cuda") for _ in range(3))
+        gy = torch.empty_like(dx)
+        if fused:
+            assert K.layernorm_bwd_dropout(dy, x, gamma, mu, rs, dx, dg, db, ws, ds, gy, P, sb, 21,
+                                           accumulate=acc)
+        else:
+            K.layernorm_bwd(dy, x, gamma, mu, rs, dx, dg, db, ws, accumulate=acc)
+            K.dropout_bwd(dx, gy, P, sb, 21, ds, bws)
+        torch.cuda.synchronize()
+        out[fused] = (dx, gy, dg, db, ds)
+    a, b = out[False], out[True]
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+    for u, v in zip(a[2:], b[2:]):
+        assert rel(v, u) < 1e-5
+
+
 def ref_attention_drop(qkv, B, S, H, D, causal, seed, salt):
     from oracle.gpt2_fp32 import dropout
     q, k, v = qkv.float().view(B, S, 3, H, D).permute(2, 0, 3, 1, 4)
