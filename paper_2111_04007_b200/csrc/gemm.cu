@@ -265,8 +265,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane_id() == 0) {
-      // ===== MMA issuer =====
+    {
+      // ===== MMA issuer (whole warp; elect.sync issues) =====
       constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN, B_MN);
       uint32_t stage = 0, phase = 0;
       uint32_t local = 0;
@@ -290,12 +290,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                                      : sdesc_sw128(sa + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? sdesc_sw128(sb + k * 2048, 64 * BK * 2, 1024)
                                      : sdesc_sw128(sb + k * 32, 16, 1024);
-            umma_f16(tmem_d, ad, bd, idesc, (kb | k) != 0);
+            umma_f16_w(tmem_d, ad, bd, idesc, (kb | k) != 0);
           }
-          umma_commit(&empty_bar[stage]);
+          umma_commit_w(&empty_bar[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        umma_commit(&tfull_bar[acc]);
+        umma_commit_w(&tfull_bar[acc]);
       }
     }
   } else if (warp >= 4) {
@@ -539,8 +539,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
   };
 
   if (warp == 0) {
-    if (lane_id() == 0) {
-      // ===== TMA producer (both CTAs) =====
+    {
+      // ===== TMA producer (both CTAs; whole warp, elect.sync issues) =====
       uint32_t stage = 0, phase = 0;
       for (int64_t u = cid; u < n_units; u += n_clusters) {
         int64_t mb, nb, kb0, kb1;
@@ -551,27 +551,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * kStageBytes2;
           uint8_t* sb = sa + 128 * BK * 2;
-          if (leader) mbar_expect_tx(&full_bar[stage], 2 * kStageBytes2);
+          if (leader) mbar_expect_tx_w(&full_bar[stage], 2 * kStageBytes2);
           const int32_t k0 = static_cast<int32_t>(kb * BK);
           if constexpr (!A_MN) {
-            tma_load_2d_2sm(sa, &tmA, &full_bar[stage], k0, m0);
+            tma_load_2d_2sm_w(sa, &tmA, &full_bar[stage], k0, m0);
           } else {
-            tma_load_2d_2sm(sa, &tmA, &full_bar[stage], m0, k0);
-            tma_load_2d_2sm(sa + 64 * BK * 2, &tmA, &full_bar[stage], m0 + 64, k0);
+            tma_load_2d_2sm_w(sa, &tmA, &full_bar[stage], m0, k0);
+            tma_load_2d_2sm_w(sa + 64 * BK * 2, &tmA, &full_bar[stage], m0 + 64, k0);
           }
           if constexpr (!B_MN) {
-            tma_load_2d_2sm(sb, &tmB, &full_bar[stage], k0, n0);
+            tma_load_2d_2sm_w(sb, &tmB, &full_bar[stage], k0, n0);
           } else {
-            tma_load_2d_2sm(sb, &tmB, &full_bar[stage], n0, k0);
-            tma_load_2d_2sm(sb + 64 * BK * 2, &tmB, &full_bar[stage], n0 + 64, k0);
+            tma_load_2d_2sm_w(sb, &tmB, &full_bar[stage], n0, k0);
+            tma_load_2d_2sm_w(sb + 64 * BK * 2, &tmB, &full_bar[stage], n0 + 64, k0);
           }
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (leader && lane_id() == 0) {
-      // ===== MMA issuer (leader CTA only) =====
+    if (leader) {
+      // ===== MMA issuer (leader CTA only; whole warp, elect.sync issues) =====
       constexpr uint32_t idesc = idesc_bf16(256, 256, A_MN, B_MN);
       uint32_t stage = 0, phase = 0, local = 0;
 #ifdef VP_GEMM_TRACE
@@ -607,12 +607,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                                      : sdesc_sw128(sa + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? sdesc_sw128(sb + k * 2048, 64 * BK * 2, 1024)
                                      : sdesc_sw128(sb + k * 32, 16, 1024);
-            umma_f16_2sm(tmem_d, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            umma_f16_2sm_w(tmem_d, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
-          umma_commit_2sm(&empty_bar[stage], 0x3);
+          umma_commit_2sm_w(&empty_bar[stage], 0x3);
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
-        umma_commit_2sm(&tfull_bar[acc], 0x3);
+        umma_commit_2sm_w(&tfull_bar[acc], 0x3);
       }
 #ifdef VP_GEMM_TRACE
       g_vp_gemm_trace[blockIdx.x][0] = w_full;
